@@ -1,0 +1,239 @@
+/* tqp_b200.h — the C-ABI drop-in boundary of the B200 (sm_100a) hot path.
+ *
+ * This library replaces the execution half of the reference (tensql,
+ * /root/reference/proj): the kernel set (include/tensql/kernels.hpp:28-78),
+ * the executor's plumbing ops and dispatch loop (src/executor.cpp:190-429),
+ * the host Tensor/EncodedTable value carriers (include/tensql/tensor.hpp:49-122,
+ * include/tensql/columnar.hpp:33-54) and the thread-pool backend
+ * (include/tensql/backend.hpp:22-70). The reference's frontend, optimizer
+ * and lowering (plan_operators, operator_plan.hpp:96) stay unchanged: a
+ * caller lowers a plan with the reference and hands the resulting
+ * OperatorPlan to tqp_executor_create through the tqp_plan_* builder below
+ * (INTEGRATION.md shows the 60-line adapter a maintainer adds to tensql).
+ *
+ * Conventions
+ *  - Plain C: opaque handles, plain pointers and sizes. No torch types.
+ *  - Every fallible call takes a tqp_status* (may be NULL). On failure it
+ *    returns NULL / nonzero and fills status with a code, the reference's
+ *    message text and the first offending row (FirstBadIndex semantics,
+ *    kernels.cpp:31-45).
+ *  - Tensors are device-resident, immutable, row-major (rows, cols), like
+ *    tensql::Tensor (tensor.hpp:46-48). Utf8 columns are stored on device as
+ *    one byte per UTF-8 byte (TQP_STR8) instead of the reference's Int32 per
+ *    byte; uploads accept either and downloads can widen back to Int32.
+ *  - All work is enqueued on the context's CUDA stream; calls that return a
+ *    data-dependent shape synchronise that stream.
+ */
+#ifndef TQP_B200_H
+#define TQP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TQP_ABI_VERSION 1
+
+/* Physical dtypes: mirrors tensql::DType (tensor.hpp:13) plus STR8. */
+typedef enum {
+  TQP_BOOL = 0, /* uint8 0/1 */
+  TQP_I32 = 1,
+  TQP_I64 = 2,
+  TQP_F64 = 3,
+  TQP_STR8 = 4 /* Utf8 rows, one byte per byte, zero padded (device only) */
+} tqp_dtype;
+
+/* Logical column types: mirrors tensql::LogicalType (columnar.hpp:13). */
+typedef enum {
+  TQP_LT_INT64 = 0,
+  TQP_LT_FLOAT64 = 1,
+  TQP_LT_DATE = 2,
+  TQP_LT_UTF8 = 3,
+  TQP_LT_BOOL = 4
+} tqp_logical_type;
+
+/* Enum values mirror kernels.hpp:11-16 exactly. */
+typedef enum { TQP_EQ = 0, TQP_NE, TQP_LT, TQP_LE, TQP_GT, TQP_GE } tqp_compare_op;
+typedef enum { TQP_ADD = 0, TQP_SUB, TQP_MUL, TQP_DIV } tqp_arith_op;
+typedef enum { TQP_AND = 0, TQP_OR } tqp_logical_op;
+typedef enum { TQP_LEFT = 0, TQP_RIGHT } tqp_search_side;
+typedef enum { TQP_SUM = 0, TQP_COUNT, TQP_MIN, TQP_MAX } tqp_reduce_op;
+typedef enum { TQP_START = 0, TQP_END, TQP_ANY, TQP_EXACT } tqp_match_anchor;
+
+/* Error classes: the reference's exception types. */
+typedef enum {
+  TQP_OK = 0,
+  TQP_ERR_KERNEL = 1,   /* tensql::KernelError   (tensor.hpp:20-23)     */
+  TQP_ERR_EXEC = 2,     /* tensql::ExecError     (interpreter.hpp:11-14) */
+  TQP_ERR_PLAN = 3,     /* tensql::PlanError     (expr.hpp:14-17)       */
+  TQP_ERR_ENCODING = 4, /* tensql::EncodingError (columnar.hpp:23-26)   */
+  TQP_ERR_CUDA = 5,     /* CUDA runtime / device failure               */
+  TQP_ERR_ARG = 6       /* bad argument at the C boundary              */
+} tqp_error_code;
+
+typedef struct tqp_status {
+  int code;        /* tqp_error_code */
+  int64_t bad_row; /* first offending row, or -1 */
+  char msg[1024];  /* reference message text */
+} tqp_status;
+
+typedef struct tqp_ctx tqp_ctx;
+typedef struct tqp_tensor tqp_tensor;
+typedef struct tqp_table tqp_table;
+typedef struct tqp_plan tqp_plan;
+typedef struct tqp_executor tqp_executor;
+typedef struct tqp_result tqp_result;
+
+/* ---- context (replaces KernelBackend/backend_by_name, backend.hpp:22-70) -- */
+int tqp_abi_version(void);
+tqp_ctx* tqp_init(int device, tqp_status* st);
+void tqp_shutdown(tqp_ctx* ctx);
+int tqp_sync(tqp_ctx* ctx, tqp_status* st);
+void* tqp_stream(tqp_ctx* ctx);          /* the cudaStream_t work is enqueued on */
+const char* tqp_backend_name(tqp_ctx* ctx); /* "b200" (KernelBackend::name)  */
+int tqp_device(tqp_ctx* ctx);
+/* Number of this library's kernels launched on ctx since creation. */
+int64_t tqp_launch_count(tqp_ctx* ctx);
+
+/* ---- tensors (tensql::Tensor, tensor.hpp:49-122) ------------------------ */
+size_t tqp_dtype_size(int dtype);
+tqp_tensor* tqp_tensor_from_host(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols,
+                                 const void* host, tqp_status* st);
+/* Utf8 upload: host is (rows, cols) Int32 byte values (the reference layout,
+ * columnar.cpp:161-175); stored as TQP_STR8. */
+tqp_tensor* tqp_tensor_from_host_utf8_i32(tqp_ctx* ctx, int64_t rows, int64_t cols,
+                                          const int32_t* host, tqp_status* st);
+/* Wraps an existing device buffer (copied; the caller keeps ownership). */
+tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols,
+                                   const void* dev, tqp_status* st);
+int tqp_tensor_dtype(const tqp_tensor* t);
+int64_t tqp_tensor_rows(const tqp_tensor* t);
+int64_t tqp_tensor_cols(const tqp_tensor* t);
+const void* tqp_tensor_data(const tqp_tensor* t); /* device pointer */
+/* Copies to a host buffer of rows*cols*dtype_size bytes (STR8 -> bytes). */
+int tqp_tensor_to_host(tqp_ctx* ctx, const tqp_tensor* t, void* host, tqp_status* st);
+/* STR8 -> Int32 per byte (reference layout). */
+int tqp_tensor_to_host_utf8_i32(tqp_ctx* ctx, const tqp_tensor* t, int32_t* host,
+                                tqp_status* st);
+tqp_tensor* tqp_tensor_retain(tqp_tensor* t);
+void tqp_tensor_free(tqp_tensor* t);
+
+/* ---- the kernel set (kernels.hpp:28-78), one entry point per kernel ----- */
+tqp_tensor* tqp_compare(tqp_ctx*, const tqp_tensor* a, const tqp_tensor* b, int op, tqp_status*);   /* kernels.hpp:30 */
+tqp_tensor* tqp_arith(tqp_ctx*, const tqp_tensor* a, const tqp_tensor* b, int op, tqp_status*);     /* kernels.hpp:34 */
+tqp_tensor* tqp_logical(tqp_ctx*, const tqp_tensor* a, const tqp_tensor* b, int op, tqp_status*);   /* kernels.hpp:37 */
+tqp_tensor* tqp_logical_not(tqp_ctx*, const tqp_tensor* v, tqp_status*);                           /* kernels.hpp:38 */
+tqp_tensor* tqp_select_where(tqp_ctx*, const tqp_tensor* cond, const tqp_tensor* a,
+                             const tqp_tensor* b, tqp_status*);                                     /* kernels.hpp:41 */
+tqp_tensor* tqp_prefix_sum_exclusive(tqp_ctx*, const tqp_tensor* x, tqp_status*);                   /* kernels.hpp:44 */
+tqp_tensor* tqp_compact(tqp_ctx*, const tqp_tensor* values, const tqp_tensor* mask, tqp_status*);   /* kernels.hpp:47 */
+tqp_tensor* tqp_argsort_stable(tqp_ctx*, const tqp_tensor* keys, tqp_status*);                      /* kernels.hpp:50 */
+tqp_tensor* tqp_gather(tqp_ctx*, const tqp_tensor* values, const tqp_tensor* idx, tqp_status*);     /* kernels.hpp:53 */
+tqp_tensor* tqp_searchsorted(tqp_ctx*, const tqp_tensor* sorted, const tqp_tensor* probes,
+                             int side, tqp_status*);                                                /* kernels.hpp:57 */
+tqp_tensor* tqp_expand_segments(tqp_ctx*, const tqp_tensor* starts, const tqp_tensor* counts,
+                                tqp_status*);                                                       /* kernels.hpp:61 */
+tqp_tensor* tqp_segment_starts(tqp_ctx*, const tqp_tensor* sorted_keys, tqp_status*);               /* kernels.hpp:64 */
+tqp_tensor* tqp_segmented_reduce(tqp_ctx*, const tqp_tensor* values, const tqp_tensor* ids,
+                                 int64_t num_segments, int op, tqp_status*);                        /* kernels.hpp:69 */
+tqp_tensor* tqp_matmul(tqp_ctx*, const tqp_tensor* a, const tqp_tensor* b, tqp_status*);            /* kernels.hpp:73 */
+tqp_tensor* tqp_substring_match(tqp_ctx*, const tqp_tensor* chars, const char* pattern,
+                                int64_t pattern_len, int anchor, tqp_status*);                      /* kernels.hpp:79 */
+
+/* ---- executor plumbing ops (executor.cpp:190-278) ----------------------- */
+tqp_tensor* tqp_iota(tqp_ctx*, int64_t n, tqp_status*);                                 /* IotaRows/IotaLen :223-236 */
+tqp_tensor* tqp_cast(tqp_ctx*, const tqp_tensor* t, int to_dtype, tqp_status*);         /* Cast :137-146 */
+tqp_tensor* tqp_exp_f64(tqp_ctx*, const tqp_tensor* t, tqp_status*);                    /* ExpF64 :171-178 */
+tqp_tensor* tqp_last_or_zero(tqp_ctx*, const tqp_tensor* t, tqp_status*);               /* LastOrZero :239-242 */
+tqp_tensor* tqp_pack_cols(tqp_ctx*, const tqp_tensor* const* cols, int n, tqp_status*); /* PackCols :243-255 */
+tqp_tensor* tqp_broadcast_rows(tqp_ctx*, const tqp_tensor* value, int64_t n, tqp_status*); /* BroadcastScalar :256-261 */
+tqp_tensor* tqp_pad_width_like(tqp_ctx*, const tqp_tensor* t, const tqp_tensor* like,
+                               tqp_status*);                                            /* PadWidthLike :262-273 */
+tqp_tensor* tqp_sort_perm_rows(tqp_ctx*, const tqp_tensor* key, const tqp_tensor* perm,
+                               int ascending, tqp_status*);                             /* SortPermRows :44-68 */
+tqp_tensor* tqp_string_compare(tqp_ctx*, const tqp_tensor* a, const tqp_tensor* b, int op,
+                               tqp_status*);                                            /* StringCompare :72-108 */
+
+/* ---- tables (EncodedTable, columnar.hpp:41-54) -------------------------- */
+tqp_table* tqp_table_create(tqp_ctx* ctx, tqp_status* st);
+/* Adds a column; takes a reference to t (the caller may free its handle). */
+int tqp_table_add_column(tqp_table* tab, const char* name, int logical_type, tqp_tensor* t,
+                         tqp_status* st);
+int64_t tqp_table_rows(const tqp_table* tab);
+int tqp_table_num_columns(const tqp_table* tab);
+const char* tqp_table_column_name(const tqp_table* tab, int i);
+int tqp_table_column_type(const tqp_table* tab, int i);
+tqp_tensor* tqp_table_column(const tqp_table* tab, int i); /* new handle: tqp_tensor_free */
+void tqp_table_free(tqp_table* tab);
+
+/* Device-side TPC-H generator (include/tqp_gen.h, bit-identical to the host
+ * one): table in {"lineitem","orders","customer","part"}; rows of shard
+ * `shard` of `nshards` (lineitem/orders split on order boundaries). */
+tqp_table* tqp_gen_table(tqp_ctx* ctx, const char* table, double sf, uint64_t seed, int shard,
+                         int nshards, tqp_status* st);
+
+/* ---- OperatorPlan builder (operator_plan.hpp:16-92) ----------------------
+ * op names are the reference's instr_op_name strings (operator_plan.cpp:11-42):
+ * "compare", "arith", ..., "load_column", "const", "iota_rows", ... */
+typedef struct tqp_instr_desc {
+  const char* op;
+  const int* inputs;
+  int num_inputs;
+  int output;
+  int cmp, arith, logic, side, reduce, anchor; /* enum values above */
+  int cast_to;                                 /* tqp_dtype (BOOL..F64) */
+  const char* pattern;                         /* SubstringMatch */
+  int64_t pattern_len;
+  const char* table;                           /* LoadColumn */
+  const char* column;
+  int64_t param;                               /* Instr::param */
+  /* ConstTensor: host data in the reference layout (Int32 for strings) */
+  int const_dtype;
+  int64_t const_rows, const_cols;
+  const void* const_data;
+} tqp_instr_desc;
+
+tqp_plan* tqp_plan_create(int num_slots, tqp_status* st);
+int tqp_plan_begin_step(tqp_plan* p, const char* id, const char* kind, tqp_status* st);
+int tqp_plan_add_instr(tqp_plan* p, const tqp_instr_desc* d, tqp_status* st);
+int tqp_plan_set_step_outputs(tqp_plan* p, const int* slots, int n, tqp_status* st);
+int tqp_plan_add_output(tqp_plan* p, const char* name, int logical_type, int slot,
+                        tqp_status* st);
+int tqp_plan_add_input_column(tqp_plan* p, const char* table, const char* column,
+                              int logical_type, tqp_status* st);
+void tqp_plan_free(tqp_plan* p);
+
+/* ---- executor (tensql::Executor, executor.hpp:43-59) --------------------- */
+#define TQP_EXEC_FUSE 1u      /* pattern-match steps into fused pipelines */
+#define TQP_EXEC_NO_FUSE 0u   /* every instruction on its own device kernel */
+/* Validates SSA form and computes last use (Executor::Executor,
+ * executor.cpp:314-344); PlanError on violation. */
+tqp_executor* tqp_executor_create(tqp_ctx* ctx, const tqp_plan* p, unsigned flags,
+                                  tqp_status* st);
+/* Executor::execute (executor.cpp:346,354-429). tables[i] is bound to names[i]
+ * (case-insensitive). Result stays on device until downloaded. */
+tqp_result* tqp_executor_execute(tqp_executor* ex, const char* const* names,
+                                 tqp_table* const* tables, int ntables, tqp_status* st);
+/* Same run with a ProfileTrace (executor.hpp:12-38) rendered as Chrome
+ * trace-event JSON into a malloc'd string the caller frees with tqp_free_str. */
+tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names,
+                                 tqp_table* const* tables, int ntables, char** trace_json,
+                                 tqp_status* st);
+/* Description of the fused pipelines chosen for this plan (JSON). */
+const char* tqp_executor_explain(tqp_executor* ex);
+void tqp_executor_free(tqp_executor* ex);
+void tqp_free_str(char* s);
+
+int64_t tqp_result_rows(const tqp_result* r);
+int tqp_result_num_columns(const tqp_result* r);
+const char* tqp_result_column_name(const tqp_result* r, int i);
+int tqp_result_column_type(const tqp_result* r, int i);
+tqp_tensor* tqp_result_column(const tqp_result* r, int i); /* borrowed */
+void tqp_result_free(tqp_result* r);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQP_B200_H */

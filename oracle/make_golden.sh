@@ -1,0 +1,22 @@
+#!/usr/bin/env bash
+# Regenerates tests/golden/ from the UNMODIFIED reference (run in the build
+# container, where /root/reference exists). Test infrastructure only.
+set -euo pipefail
+cd "$(dirname "$0")"
+make -j8 >/dev/null
+G=../tests/golden
+./_ref/golden_cases kernels $G/kernels.json
+./_ref/golden_cases plans $G/plans.json _ref/queries
+./_ref/tqp_ref_runner opplan --out ../paper_2209_04579_b200/plans
+SF=0.005
+./_ref/tqp_ref_runner tables --sf $SF --out /tmp/tqp_tables.json
+./_ref/tqp_ref_runner run --sf $SF --repeat 0 --warmup 0 --results /tmp/tqp_results.json >/dev/null
+python3 - "$SF" <<'PY'
+import gzip, json, sys
+sf = float(sys.argv[1])
+t = json.load(open('/tmp/tqp_tables.json')); r = json.load(open('/tmp/tqp_results.json'))
+doc = {"generator": "oracle/make_golden.sh: tqp_ref_runner tables/run (reference executor, par backend)",
+       "sf": sf, "seed": 7, "tables": t, "results": r["results"]}
+with gzip.open('../tests/golden/tpch_sf%s.json.gz' % sys.argv[1], 'wt') as f:
+    json.dump(doc, f)
+PY

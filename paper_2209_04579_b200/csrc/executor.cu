@@ -1,0 +1,322 @@
+// Executor: SSA validation + last-use analysis (executor.cpp:314-344), the
+// instruction dispatch loop (executor.cpp:354-429) and exec_instr
+// (executor.cpp:190-278), over device tensors. Steps covered by a fused
+// pipeline (fused.cu) run as one unit; everything else dispatches one device
+// kernel per instruction. There is no CPU fallback: every InstrOp has a
+// device implementation.
+#include <algorithm>
+#include <cctype>
+#include <cstring>
+#include <limits>
+#include <sstream>
+
+#include "executor.hpp"
+
+namespace tqp {
+
+namespace {
+const char* kOpNames[] = {"compare",       "arith",         "logical",          "not",
+                          "select_where",  "prefix_sum_exclusive", "compact",   "argsort_stable",
+                          "gather",        "searchsorted",  "expand_segments",  "segment_starts",
+                          "segmented_reduce", "matmul",     "substring_match",  "load_column",
+                          "const",         "iota_rows",     "iota_len",         "cast",
+                          "exp",           "last_or_zero",  "pack_cols",        "broadcast_scalar",
+                          "pad_width_like", "sort_perm_rows", "string_compare"};
+constexpr int kNumOps = sizeof(kOpNames) / sizeof(kOpNames[0]);
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+std::string json_escape(const std::string& s) {
+  std::string o;
+  for (char ch : s) {
+    if (ch == '"' || ch == '\\') o += '\\';
+    o += ch;
+  }
+  return o;
+}
+}  // namespace
+
+bool op_from_name(const std::string& name, Op* out) {
+  for (int i = 0; i < kNumOps; ++i) {
+    if (name == kOpNames[i]) {
+      *out = static_cast<Op>(i);
+      return true;
+    }
+  }
+  return false;
+}
+const char* op_name(Op op) { return kOpNames[static_cast<int>(op)]; }
+
+bool iequals(const std::string& a, const std::string& b) {
+  if (a.size() != b.size()) return false;
+  for (size_t i = 0; i < a.size(); ++i) {
+    if (std::tolower(static_cast<unsigned char>(a[i])) != std::tolower(static_cast<unsigned char>(b[i]))) return false;
+  }
+  return true;
+}
+
+const Column* Table::find(const std::string& name) const {
+  for (const auto& c : cols)
+    if (iequals(c.name, name)) return &c;
+  return nullptr;
+}
+
+const Table* bind_table(const TableSet& tables, const std::string& name) {
+  const Table* t = nullptr;
+  for (const auto& [n, tab] : tables)
+    if (iequals(n, name)) t = tab;  // last match wins, as the reference's loop does
+  return t;
+}
+
+std::string ProfileTrace::to_chrome_json() const {
+  std::ostringstream os;
+  os << "[\n";
+  bool first = true;
+  auto sep = [&] {
+    if (!first) os << ",\n";
+    first = false;
+  };
+  for (const auto& op : operators) {
+    sep();
+    os << "  {\"name\": \"" << json_escape(op.id) << "\", \"cat\": \"operator\", \"ph\": \"X\", \"ts\": "
+       << op.start_ns / 1000.0 << ", \"dur\": " << op.wall_ns / 1000.0
+       << ", \"pid\": 0, \"tid\": 0, \"args\": {\"rows\": " << op.rows_out << ", \"bytes\": " << op.bytes
+       << ", \"backend\": \"" << backend << "\"}}";
+  }
+  for (const auto& k : kernels) {
+    sep();
+    os << "  {\"name\": \"" << json_escape(k.kernel) << "\", \"cat\": \"kernel\", \"ph\": \"X\", \"ts\": "
+       << k.start_ns / 1000.0 << ", \"dur\": " << k.wall_ns / 1000.0
+       << ", \"pid\": 0, \"tid\": 1, \"args\": {\"operator\": \"" << json_escape(k.op_id) << "\", \"rows\": " << k.rows
+       << ", \"bytes\": " << k.bytes << "}}";
+  }
+  os << "\n]";
+  return os.str();
+}
+
+Executor::Executor(Ctx& ctx, Plan plan, unsigned flags) : ctx_(ctx), plan_(std::move(plan)), flags_(flags) {
+  // SSA validation and last-use analysis (executor.cpp:314-344)
+  std::vector<bool> written(plan_.num_slots, false);
+  last_use_.assign(plan_.num_slots, -1);
+  int64_t ordinal = 0;
+  for (const auto& step : plan_.steps) {
+    step_first_ordinal_.push_back(ordinal);
+    for (const auto& in : step.instrs) {
+      for (int s : in.inputs) {
+        if (s < 0 || s >= plan_.num_slots || !written[s]) {
+          plan_fail("executor: instruction reads slot " + std::to_string(s) + " before it is written");
+        }
+        last_use_[s] = ordinal;
+      }
+      if (in.output < 0 || in.output >= plan_.num_slots || written[in.output]) {
+        plan_fail("executor: slot " + std::to_string(in.output) + " written twice or out of range");
+      }
+      written[in.output] = true;
+      ++ordinal;
+    }
+  }
+  step_first_ordinal_.push_back(ordinal);
+  for (const auto& o : plan_.outputs) {
+    if (o.slot < 0 || o.slot >= plan_.num_slots || !written[o.slot]) plan_fail("executor: output slot never written");
+    last_use_[o.slot] = std::numeric_limits<int64_t>::max();
+  }
+  // device-resident constants; Int32 constants are Utf8 literals
+  // (lower_literal, operator_plan.cpp:476-490) and live as STR8
+  for (auto& step : plan_.steps) {
+    for (auto& in : step.instrs) {
+      if (in.op != Op::ConstTensor) continue;
+      if (in.const_dtype == TQP_I32) {
+        Tensor wide = upload(ctx_, TQP_I32, in.const_rows, in.const_cols, in.const_host.data());
+        in.constant = k::utf8_i32_to_str8(ctx_, wide);
+      } else {
+        in.constant = upload(ctx_, in.const_dtype, in.const_rows, in.const_cols, in.const_host.data());
+      }
+    }
+  }
+  ctx_.sync();
+  if (flags_ & TQP_EXEC_FUSE) units_ = plan_fusion(ctx_, plan_);
+}
+
+std::string Executor::explain() const {
+  std::ostringstream os;
+  os << "{\"fused\": [";
+  for (size_t i = 0; i < units_.size(); ++i) {
+    const auto& u = units_[i];
+    os << (i ? ", " : "") << "{\"name\": \"" << u.name << "\", \"steps\": [\"" << plan_.steps[u.first_step].id
+       << "\", \"" << plan_.steps[u.last_step].id << "\"], \"detail\": \"" << json_escape(u.explain) << "\"}";
+  }
+  os << "]}";
+  return os.str();
+}
+
+Tensor Executor::exec_instr(const Instr& in, std::vector<std::optional<Tensor>>& slots, const TableSet& tables) {
+  auto arg = [&](size_t i) -> const Tensor& {
+    int s = in.inputs.at(i);
+    if (!slots[s]) exec_fail("internal: slot " + std::to_string(s) + " read after release");
+    return *slots[s];
+  };
+  Ctx& c = ctx_;
+  switch (in.op) {
+    case Op::Compare: return k::compare(c, arg(0), arg(1), in.cmp);
+    case Op::Arith: return k::arith(c, arg(0), arg(1), in.arith);
+    case Op::Logical: return k::logical(c, arg(0), arg(1), in.logic);
+    case Op::Not: return k::logical_not(c, arg(0));
+    case Op::SelectWhere: return k::select_where(c, arg(0), arg(1), arg(2));
+    case Op::PrefixSum: return k::prefix_sum_exclusive(c, arg(0));
+    case Op::Compact: return k::compact(c, arg(0), arg(1));
+    case Op::ArgsortStable: return k::argsort_stable(c, arg(0));
+    case Op::Gather: return k::gather(c, arg(0), arg(1));
+    case Op::SearchSorted: return k::searchsorted(c, arg(0), arg(1), in.side);
+    case Op::ExpandSegments: return k::expand_segments(c, arg(0), arg(1));
+    case Op::SegmentStarts: return k::segment_starts(c, arg(0));
+    case Op::SegmentedReduce: {
+      int64_t num = in.param;
+      if (num < 0) {
+        const Tensor& t = arg(2);
+        if (t.size() != 1) kernel_fail("tensor: item() requires exactly one element");
+        num = std::max<int64_t>(0, read_scalar<int64_t>(c, t));
+      }
+      return k::segmented_reduce(c, arg(0), arg(1), num, in.reduce);
+    }
+    case Op::MatMul: return k::matmul(c, arg(0), arg(1));
+    case Op::SubstringMatch: return k::substring_match(c, arg(0), in.pattern, in.anchor);
+    case Op::LoadColumn: {
+      const Table* t = bind_table(tables, in.table);
+      if (!t) exec_fail("no input table named '" + in.table + "'");
+      const Column* col = t->find(in.column);
+      if (!col) throw Error(TQP_ERR_ENCODING, "table: no column named '" + in.column + "'");
+      return col->t;
+    }
+    case Op::ConstTensor: return in.constant;
+    case Op::IotaRows: {
+      int64_t n = arg(0).rows;
+      if (in.param >= 0) n = std::min(n, in.param);
+      return k::iota(c, n);
+    }
+    case Op::IotaLen: {
+      const Tensor& t = arg(0);
+      if (t.size() != 1) kernel_fail("tensor: item() requires exactly one element");
+      return k::iota(c, read_scalar<int64_t>(c, t));
+    }
+    case Op::Cast: return k::cast(c, arg(0), in.cast_to);
+    case Op::ExpF64: return k::exp_f64(c, arg(0));
+    case Op::LastOrZero: return k::last_or_zero(c, arg(0));
+    case Op::PackCols: {
+      std::vector<Tensor> cols;
+      for (size_t i = 0; i < in.inputs.size(); ++i) cols.push_back(arg(i));
+      return k::pack_cols(c, cols);
+    }
+    case Op::BroadcastScalar: return k::broadcast_rows(c, arg(0), arg(1).rows);
+    case Op::PadWidthLike: return k::pad_width_like(c, arg(0), arg(1));
+    case Op::SortPermRows: return k::sort_perm_rows(c, arg(0), arg(1), in.param == 1);
+    case Op::StringCompare: return k::string_compare(c, arg(0), arg(1), in.cmp);
+  }
+  exec_fail("unknown instruction");
+}
+
+void Executor::run_step(int s, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, ProfileTrace* trace,
+                        int64_t run_start) {
+  const Step& step = plan_.steps[s];
+  int64_t ordinal = step_first_ordinal_[s];
+  int64_t step_start = now_ns(), step_bytes = 0, rows_out = 0;
+  for (const auto& in : step.instrs) {
+    int64_t t0 = now_ns();
+    Tensor r;
+    try {
+      r = exec_instr(in, slots, tables);
+    } catch (const Error& e) {
+      if (e.code == TQP_ERR_KERNEL || e.code == TQP_ERR_ENCODING) {
+        throw Error(TQP_ERR_EXEC, step.id + ": " + e.what(), e.bad_row);
+      }
+      throw;
+    }
+    if (trace) ctx_.sync();
+    int64_t t1 = now_ns();
+    int64_t bytes = static_cast<int64_t>(r.size()) * (r.dtype == TQP_STR8 ? 4 : static_cast<int64_t>(r.elem_size()));
+    rows_out = r.rows;
+    step_bytes += bytes;
+    if (trace) trace->kernels.push_back({step.id, op_name(in.op), t0 - run_start, t1 - t0, r.rows, bytes});
+    slots[in.output] = std::move(r);
+    for (int x : in.inputs)
+      if (last_use_[x] == ordinal) slots[x].reset();
+    ++ordinal;
+  }
+  if (trace) {
+    if (!step.output_slots.empty() && slots[step.output_slots.front()]) rows_out = slots[step.output_slots.front()]->rows;
+    trace->operators.push_back({step.id, step.kind, step_start - run_start, now_ns() - step_start, rows_out, step_bytes});
+  }
+}
+
+void Executor::release_after(int s, std::vector<std::optional<Tensor>>& slots) {
+  int64_t last = step_first_ordinal_[s + 1] - 1;
+  for (int x = 0; x < plan_.num_slots; ++x)
+    if (slots[x] && last_use_[x] <= last) slots[x].reset();
+}
+
+Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
+  // bind and type-check the input tables (executor.cpp:355-371)
+  for (const auto& it : plan_.input_tables) {
+    const Table* t = bind_table(tables, it.name);
+    if (!t) exec_fail("no input table named '" + it.name + "'");
+    for (const auto& [cname, ctype] : it.schema) {
+      const Column* c = t->find(cname);
+      if (!c) exec_fail("input table '" + it.name + "' is missing column '" + cname + "'");
+      if (c->type != ctype) {
+        exec_fail("input table '" + it.name + "': column '" + cname + "' is " + logical_type_name(c->type) +
+                  ", the plan expects " + logical_type_name(ctype));
+      }
+    }
+  }
+  std::vector<std::optional<Tensor>> slots(plan_.num_slots);
+  int64_t run_start = now_ns();
+  size_t u = 0;
+  for (int s = 0; s < static_cast<int>(plan_.steps.size());) {
+    if (u < units_.size() && units_[u].first_step == s) {
+      const FusedUnit& unit = units_[u++];
+      int64_t t0 = now_ns();
+      bool ok = unit.run(ctx_, slots, tables);
+      if (ok) {
+        if (trace) {
+          ctx_.sync();
+          int64_t t1 = now_ns();
+          trace->kernels.push_back({plan_.steps[unit.last_step].id, unit.name, t0 - run_start, t1 - t0, 0, 0});
+          for (int q = unit.first_step; q <= unit.last_step; ++q) {
+            const Step& st = plan_.steps[q];
+            int64_t rows = 0;
+            if (!st.output_slots.empty() && slots[st.output_slots.front()]) rows = slots[st.output_slots.front()]->rows;
+            trace->operators.push_back({st.id, st.kind, t0 - run_start, t1 - t0, rows, 0});
+          }
+        }
+        release_after(unit.last_step, slots);
+        s = unit.last_step + 1;
+        continue;
+      }
+      // preconditions failed on this data: run the covered steps per
+      // instruction (still on device)
+      for (int q = unit.first_step; q <= unit.last_step; ++q) run_step(q, slots, tables, trace, run_start);
+      s = unit.last_step + 1;
+      continue;
+    }
+    run_step(s, slots, tables, trace, run_start);
+    ++s;
+  }
+  Result res;
+  for (const auto& o : plan_.outputs) {
+    if (!slots[o.slot]) exec_fail("internal: slot " + std::to_string(o.slot) + " read after release");
+    res.cols.push_back({o.name, o.type, *slots[o.slot]});
+  }
+  if (!res.cols.empty()) res.rows = res.cols[0].t.rows;
+  for (const auto& c : res.cols) {
+    if (c.t.rows != res.rows) {
+      throw Error(TQP_ERR_ENCODING, "table: column '" + c.name + "' has " + std::to_string(c.t.rows) +
+                                        " rows, expected " + std::to_string(res.rows));
+    }
+  }
+  ctx_.sync();
+  return res;
+}
+
+}  // namespace tqp

@@ -1,0 +1,137 @@
+// B200 executor: device-side counterpart of tensql::Executor
+// (executor.hpp:43-59, executor.cpp:314-429) over the reference's lowered
+// OperatorPlan (operator_plan.hpp:16-92), with pattern-matched fused
+// pipelines (fused.cu) for the relational shapes TPC-H Q1/Q3/Q6/Q14 lower to.
+#pragma once
+
+#include <chrono>
+#include <functional>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "tqp_internal.hpp"
+
+namespace tqp {
+
+enum class Op : uint8_t {
+  Compare, Arith, Logical, Not, SelectWhere, PrefixSum, Compact, ArgsortStable, Gather, SearchSorted,
+  ExpandSegments, SegmentStarts, SegmentedReduce, MatMul, SubstringMatch,
+  LoadColumn, ConstTensor, IotaRows, IotaLen, Cast, ExpF64, LastOrZero, PackCols, BroadcastScalar,
+  PadWidthLike, SortPermRows, StringCompare,
+};
+bool op_from_name(const std::string& name, Op* out);
+const char* op_name(Op op);
+
+struct Instr {
+  Op op{};
+  std::vector<int> inputs;
+  int output = -1;
+  int cmp = 0, arith = 0, logic = 0, side = 0, reduce = 0, anchor = 0, cast_to = 0;
+  std::string pattern, table, column;
+  int64_t param = -1;
+  // ConstTensor: host copy (reference layout) + device copy
+  int const_dtype = TQP_I64;
+  int64_t const_rows = 0, const_cols = 1;
+  std::vector<uint8_t> const_host;
+  Tensor constant;
+};
+
+struct Step {
+  std::string id, kind;
+  std::vector<Instr> instrs;
+  std::vector<int> output_slots;
+};
+
+struct OutputCol {
+  std::string name;
+  int type;
+  int slot;
+};
+
+struct InputTable {
+  std::string name;
+  std::vector<std::pair<std::string, int>> schema;
+};
+
+struct Plan {
+  int num_slots = 0;
+  std::vector<Step> steps;
+  std::vector<OutputCol> outputs;
+  std::vector<InputTable> input_tables;
+};
+
+struct Column {
+  std::string name;
+  int type;  // logical
+  Tensor t;
+};
+
+struct Table {
+  std::vector<Column> cols;
+  int64_t rows = 0;
+  const Column* find(const std::string& name) const;
+};
+
+using TableSet = std::vector<std::pair<std::string, const Table*>>;
+
+struct KernelTrace {
+  std::string op_id, kernel;
+  int64_t start_ns, wall_ns, rows, bytes;
+};
+struct OperatorTrace {
+  std::string id, kind;
+  int64_t start_ns, wall_ns, rows_out, bytes;
+};
+struct ProfileTrace {
+  std::string backend = "b200";
+  std::vector<OperatorTrace> operators;
+  std::vector<KernelTrace> kernels;
+  std::string to_chrome_json() const;
+};
+
+struct Result {
+  std::vector<Column> cols;
+  int64_t rows = 0;
+};
+
+// A fused pipeline replaces a contiguous range of steps [first, last] and
+// writes the slots later instructions (or the plan outputs) read.
+struct FusedUnit {
+  int first_step = 0, last_step = 0;
+  std::string name;  // e.g. "scan_filter_aggregate"
+  std::string explain;
+  // returns false when the data violates the fused path's preconditions
+  // (e.g. a fixed-point overflow or a non-unique build key); the executor
+  // then runs the covered steps through the per-instruction path.
+  std::function<bool(Ctx&, std::vector<std::optional<Tensor>>& slots, const TableSet& tables)> run;
+};
+
+class Executor {
+ public:
+  Executor(Ctx& ctx, Plan plan, unsigned flags);
+  Result execute(const TableSet& tables, ProfileTrace* trace = nullptr);
+  const Plan& plan() const { return plan_; }
+  std::string explain() const;
+
+ private:
+  Tensor exec_instr(const Instr& in, std::vector<std::optional<Tensor>>& slots, const TableSet& tables);
+  void run_step(int s, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, ProfileTrace* trace,
+                int64_t run_start);
+  void release_after(int s, std::vector<std::optional<Tensor>>& slots);
+
+  Ctx& ctx_;
+  Plan plan_;
+  unsigned flags_;
+  std::vector<int64_t> last_use_;          // per slot: global instruction ordinal of last read
+  std::vector<int64_t> step_first_ordinal_;
+  std::vector<FusedUnit> units_;
+};
+
+// fused.cu: recognises fusable step patterns
+std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan);
+
+const Table* bind_table(const TableSet& tables, const std::string& name);
+bool iequals(const std::string& a, const std::string& b);
+
+}  // namespace tqp

@@ -1,0 +1,438 @@
+// segmented_reduce (kernels.cpp:552-672) on device.
+//
+// Segment runs come from binary searches into the validated, non-decreasing
+// ids (segment_runs' contract, kernels.cpp:552-580). Each segment is reduced
+// in index order by contiguous per-lane chunks combined left to right, so:
+//  - SUM over Int64/Int32 carries an exact 128-bit (sum, min prefix, max
+//    prefix) monoid: an overflow is reported exactly when the reference's
+//    sequential accumulation would overflow (kernels.cpp:660-664), for the
+//    first such segment;
+//  - MIN/MAX keep the earliest of equal values (the reference's `v < acc`
+//    keeps the first: visible for -0.0 vs +0.0) and propagate NaN;
+//  - Float64 SUM is a fixed-order tree (run-to-run deterministic; within
+//    1e-9 relative of the reference's sequential / 4096-chunk orders).
+// Segments longer than kLong rows are split over CTAs (64K-row chunks) whose
+// partials are combined in chunk order.
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+
+namespace tqp {
+namespace {
+
+constexpr int kLong = 4096;
+constexpr int64_t kChunk = 65536;
+
+template <typename T>
+struct Part;
+
+// ---- partial monoids ---------------------------------------------------------
+struct SumF {
+  double s = 0.0;
+};
+struct SumI {
+  __int128 s = 0, mn = 0, mx = 0;
+  bool empty = true;
+};
+template <typename T>
+struct MinMax {
+  T v{};
+  int64_t idx = -1;  // -1: empty
+  bool nan = false;
+};
+
+__device__ __forceinline__ SumF combine(SumF a, SumF b) { return {__dadd_rn(a.s, b.s)}; }
+__device__ __forceinline__ SumI combine(const SumI& a, const SumI& b) {
+  if (a.empty) return b;
+  if (b.empty) return a;
+  SumI r;
+  r.empty = false;
+  r.s = a.s + b.s;
+  __int128 bmn = a.s + b.mn, bmx = a.s + b.mx;
+  r.mn = a.mn < bmn ? a.mn : bmn;
+  r.mx = a.mx > bmx ? a.mx : bmx;
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ MinMax<T> combine_mm(const MinMax<T>& a, const MinMax<T>& b, bool is_min) {
+  if (a.idx < 0) return b;
+  if (b.idx < 0) return a;
+  MinMax<T> r;
+  r.nan = a.nan || b.nan;
+  // a precedes b in index order: b wins only if strictly better
+  bool take_b = is_min ? (b.v < a.v) : (b.v > a.v);
+  r.v = take_b ? b.v : a.v;
+  r.idx = take_b ? b.idx : a.idx;
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ SumI sumi_one(T v) {
+  SumI r;
+  r.empty = false;
+  r.s = r.mn = r.mx = static_cast<__int128>(v);
+  return r;
+}
+
+// shuffle helpers for the partial structs
+__device__ __forceinline__ SumF shfl(SumF p, int src) { return {__shfl_sync(0xffffffffu, p.s, src)}; }
+__device__ __forceinline__ __int128 shfl128(__int128 v, int src) {
+  unsigned long long lo = static_cast<unsigned long long>(v), hi = static_cast<unsigned long long>(v >> 64);
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  hi = __shfl_sync(0xffffffffu, hi, src);
+  return (static_cast<__int128>(static_cast<long long>(hi)) << 64) | lo;
+}
+__device__ __forceinline__ SumI shfl(const SumI& p, int src) {
+  SumI r;
+  r.s = shfl128(p.s, src);
+  r.mn = shfl128(p.mn, src);
+  r.mx = shfl128(p.mx, src);
+  r.empty = __shfl_sync(0xffffffffu, static_cast<int>(p.empty), src);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ MinMax<T> shfl(const MinMax<T>& p, int src) {
+  MinMax<T> r;
+  if constexpr (sizeof(T) == 1) {
+    r.v = static_cast<T>(__shfl_sync(0xffffffffu, static_cast<int>(p.v), src));
+  } else {
+    r.v = __shfl_sync(0xffffffffu, p.v, src);
+  }
+  r.idx = __shfl_sync(0xffffffffu, p.idx, src);
+  r.nan = __shfl_sync(0xffffffffu, static_cast<int>(p.nan), src);
+  return r;
+}
+
+// Ordered warp combine: lane l holds the partial of the l-th contiguous chunk;
+// result (in lane 0) = p0 . p1 . ... . p31 in order.
+template <typename P, typename F>
+__device__ __forceinline__ P warp_ordered(P p, F comb) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    P q = shfl(p, (lane + o) & 31);
+    if ((lane & (2 * o - 1)) == 0) p = comb(p, q);
+  }
+  return p;
+}
+
+// ---- per-op accumulation over [lo, hi) by one warp (contiguous lane chunks)
+template <typename T, int OP>
+struct Acc;
+
+template <>
+struct Acc<double, TQP_SUM> {
+  using P = SumF;
+  __device__ static P one(double v, int64_t) { return {v}; }
+  __device__ static P comb(P a, P b) { return combine(a, b); }
+};
+template <typename T>
+struct AccSumI {
+  using P = SumI;
+  __device__ static P one(T v, int64_t) { return sumi_one(v); }
+  __device__ static P comb(const P& a, const P& b) { return combine(a, b); }
+};
+template <>
+struct Acc<int64_t, TQP_SUM> : AccSumI<int64_t> {};
+template <>
+struct Acc<int32_t, TQP_SUM> : AccSumI<int32_t> {};
+template <typename T, bool IS_MIN>
+struct AccMM {
+  using P = MinMax<T>;
+  __device__ static P one(T v, int64_t i) {
+    P r;
+    r.v = v;
+    r.idx = i;
+    if constexpr (std::is_same_v<T, double>) r.nan = isnan(v);
+    return r;
+  }
+  __device__ static P comb(const P& a, const P& b) { return combine_mm(a, b, IS_MIN); }
+};
+template <typename T>
+struct Acc<T, TQP_MIN> : AccMM<T, true> {};
+template <typename T>
+struct Acc<T, TQP_MAX> : AccMM<T, false> {};
+
+template <typename T, int OP>
+__device__ typename Acc<T, OP>::P warp_reduce_range(const T* __restrict__ v, int64_t lo, int64_t hi) {
+  using A = Acc<T, OP>;
+  using P = typename A::P;
+  const int lane = threadIdx.x & 31;
+  int64_t len = hi - lo;
+  int64_t per = (len + 31) / 32;
+  int64_t a = lo + lane * per, b = a + per < hi ? a + per : hi;
+  P p{};
+  for (int64_t i = a; i < b; ++i) p = A::comb(p, A::one(v[i], i));
+  return warp_ordered(p, [](const P& x, const P& y) { return A::comb(x, y); });
+}
+
+template <typename T, int OP>
+__device__ void write_result(T* out, int64_t s, const typename Acc<T, OP>::P& p, long long* err);
+
+template <>
+__device__ void write_result<double, TQP_SUM>(double* out, int64_t s, const SumF& p, long long*) {
+  out[s] = p.s;
+}
+template <typename T>
+__device__ void write_sumi(T* out, int64_t s, const SumI& p, long long* err) {
+  const __int128 lo = static_cast<__int128>(std::numeric_limits<T>::min());
+  const __int128 hi = static_cast<__int128>(std::numeric_limits<T>::max());
+  if (!p.empty && (p.mn < lo || p.mx > hi)) note_bad(err, s);
+  out[s] = static_cast<T>(p.s);
+}
+template <>
+__device__ void write_result<int64_t, TQP_SUM>(int64_t* out, int64_t s, const SumI& p, long long* err) {
+  write_sumi(out, s, p, err);
+}
+template <>
+__device__ void write_result<int32_t, TQP_SUM>(int32_t* out, int64_t s, const SumI& p, long long* err) {
+  write_sumi(out, s, p, err);
+}
+template <typename T>
+__device__ void write_mm(T* out, int64_t s, const MinMax<T>& p) {
+  if constexpr (std::is_same_v<T, double>) {
+    out[s] = p.nan ? __longlong_as_double(0x7ff8000000000000LL) : p.v;
+  } else {
+    out[s] = p.v;
+  }
+}
+
+// ---- kernels -------------------------------------------------------------------
+__global__ void k_check_ids(const int64_t* __restrict__ ids, int64_t n, int64_t num, long long* err) {
+  for (int64_t i = gtid(); i < n; i += gstride()) {
+    int64_t s = ids[i], prev = i ? ids[i - 1] : -1;
+    if (s < prev) note_bad(err, 2 * i);           // decrease (checked first)
+    else if (s < 0 || s >= num) note_bad(err, 2 * i + 1);  // out of range
+  }
+}
+
+__global__ void k_runs(const int64_t* __restrict__ ids, int64_t n, int64_t num, int64_t* __restrict__ lo,
+                       int64_t* __restrict__ hi) {
+  for (int64_t s = gtid(); s < num; s += gstride()) {
+    int64_t a = 0, b = n;
+    while (a < b) {
+      int64_t m = (a + b) >> 1;
+      if (ids[m] < s) a = m + 1;
+      else b = m;
+    }
+    int64_t l = a;
+    b = n;
+    while (a < b) {
+      int64_t m = (a + b) >> 1;
+      if (ids[m] <= s) a = m + 1;
+      else b = m;
+    }
+    lo[s] = l;
+    hi[s] = a;
+  }
+}
+
+__global__ void k_count(const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t num,
+                        int64_t* __restrict__ out) {
+  for (int64_t s = gtid(); s < num; s += gstride()) out[s] = hi[s] - lo[s];
+}
+
+__global__ void k_first_empty(const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t num,
+                              long long* err) {
+  for (int64_t s = gtid(); s < num; s += gstride())
+    if (lo[s] == hi[s]) note_bad(err, s);
+}
+
+template <typename T, int OP>
+__global__ void k_short(const T* __restrict__ v, const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+                        int64_t num, T* __restrict__ out, long long* err, int64_t* long_list,
+                        unsigned long long* long_count) {
+  const int64_t warp = gtid() >> 5, nw = gstride() >> 5;
+  for (int64_t s = warp; s < num; s += nw) {
+    int64_t a = lo[s], b = hi[s];
+    if (b - a > kLong) {
+      if ((threadIdx.x & 31) == 0) long_list[atomicAdd(long_count, 1ULL)] = s;
+      continue;
+    }
+    auto p = warp_reduce_range<T, OP>(v, a, b);
+    if ((threadIdx.x & 31) == 0) {
+      if constexpr (OP == TQP_SUM) {
+        write_result<T, OP>(out, s, p, err);
+      } else {
+        write_mm(out, s, p);
+      }
+    }
+  }
+}
+
+// one CTA per (segment, chunk) work item; partials stored per item
+template <typename T, int OP>
+__global__ void k_long_chunks(const T* __restrict__ v, const int64_t* __restrict__ item_lo,
+                              const int64_t* __restrict__ item_hi, typename Acc<T, OP>::P* __restrict__ parts) {
+  using A = Acc<T, OP>;
+  using P = typename A::P;
+  __shared__ char smem_raw[32 * sizeof(P)];
+  P* sp = reinterpret_cast<P*>(smem_raw);
+  int64_t a = item_lo[blockIdx.x], b = item_hi[blockIdx.x];
+  int nwarps = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  int64_t len = b - a, per = (len + nwarps - 1) / nwarps;
+  int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
+  if (wa > wb) wa = wb;
+  P p = warp_reduce_range<T, OP>(v, wa, wb);
+  if ((threadIdx.x & 31) == 0) sp[warp] = p;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    P acc = sp[0];
+    for (int w = 1; w < nwarps; ++w) acc = A::comb(acc, sp[w]);
+    parts[blockIdx.x] = acc;
+  }
+}
+
+template <typename T, int OP>
+__global__ void k_long_finish(const typename Acc<T, OP>::P* __restrict__ parts, const int64_t* __restrict__ seg,
+                              const int64_t* __restrict__ first_item, const int64_t* __restrict__ nitems, int64_t nlong,
+                              T* __restrict__ out, long long* err) {
+  using A = Acc<T, OP>;
+  for (int64_t q = gtid(); q < nlong; q += gstride()) {
+    auto p = parts[first_item[q]];
+    for (int64_t k = 1; k < nitems[q]; ++k) p = A::comb(p, parts[first_item[q] + k]);
+    if constexpr (OP == TQP_SUM) {
+      write_result<T, OP>(out, seg[q], p, err);
+    } else {
+      write_mm(out, seg[q], p);
+    }
+  }
+}
+
+template <typename T, int OP>
+void run_reduce(Ctx& c, const Tensor& values, const Tensor& lo, const Tensor& hi, int64_t num, Tensor& out) {
+  using P = typename Acc<T, OP>::P;
+  auto long_buf = c.alloc_bytes(sizeof(int64_t) * (num / kLong + 2) + 16);
+  TQP_CUDA(cudaMemsetAsync(long_buf->ptr, 0, 8, c.stream));
+  auto* long_count = static_cast<unsigned long long*>(long_buf->ptr);
+  auto* long_list = reinterpret_cast<int64_t*>(static_cast<char*>(long_buf->ptr) + 16);
+  c.reset_err();
+  k_short<T, OP><<<c.grid_for(num * 32, 256), 256, 0, c.stream>>>(values.ptr<T>(), lo.ptr<int64_t>(),
+                                                                  hi.ptr<int64_t>(), num, out.ptr<T>(), c.d_err,
+                                                                  long_list, long_count);
+  c.count_launch();
+  unsigned long long nlong = 0;
+  TQP_CUDA(cudaMemcpyAsync(&nlong, long_count, 8, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (!nlong) return;
+  std::vector<int64_t> segs(nlong);
+  TQP_CUDA(cudaMemcpyAsync(segs.data(), long_list, 8 * nlong, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  std::sort(segs.begin(), segs.end());
+  std::vector<int64_t> hlo(num ? 0 : 0);
+  // fetch run bounds of the long segments
+  std::vector<int64_t> slo(nlong), shi(nlong);
+  for (size_t q = 0; q < nlong; ++q) {
+    TQP_CUDA(cudaMemcpyAsync(&slo[q], lo.ptr<int64_t>() + segs[q], 8, cudaMemcpyDeviceToHost, c.stream));
+    TQP_CUDA(cudaMemcpyAsync(&shi[q], hi.ptr<int64_t>() + segs[q], 8, cudaMemcpyDeviceToHost, c.stream));
+  }
+  c.sync();
+  std::vector<int64_t> ilo, ihi, first(nlong), cnt(nlong);
+  for (size_t q = 0; q < nlong; ++q) {
+    first[q] = static_cast<int64_t>(ilo.size());
+    for (int64_t a = slo[q]; a < shi[q]; a += kChunk) {
+      ilo.push_back(a);
+      ihi.push_back(std::min(a + kChunk, shi[q]));
+    }
+    cnt[q] = static_cast<int64_t>(ilo.size()) - first[q];
+  }
+  int64_t items = static_cast<int64_t>(ilo.size());
+  Tensor d_ilo = upload(c, TQP_I64, items, 1, ilo.data());
+  Tensor d_ihi = upload(c, TQP_I64, items, 1, ihi.data());
+  Tensor d_seg = upload(c, TQP_I64, nlong, 1, segs.data());
+  Tensor d_first = upload(c, TQP_I64, nlong, 1, first.data());
+  Tensor d_cnt = upload(c, TQP_I64, nlong, 1, cnt.data());
+  auto parts = c.alloc_bytes(sizeof(P) * items);
+  k_long_chunks<T, OP><<<items, 256, 0, c.stream>>>(values.ptr<T>(), d_ilo.ptr<int64_t>(), d_ihi.ptr<int64_t>(),
+                                                    static_cast<P*>(parts->ptr));
+  k_long_finish<T, OP><<<c.grid_for(nlong, 128), 128, 0, c.stream>>>(static_cast<P*>(parts->ptr),
+                                                                     d_seg.ptr<int64_t>(), d_first.ptr<int64_t>(),
+                                                                     d_cnt.ptr<int64_t>(), nlong, out.ptr<T>(), c.d_err);
+  c.count_launch(2);
+  c.sync();  // host vectors above must outlive the async uploads
+}
+
+}  // namespace
+
+namespace k {
+
+Tensor segmented_reduce(Ctx& c, const Tensor& values, const Tensor& ids, int64_t num, int op) {
+  if (!values.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
+  if (ids.dtype != TQP_I64) kernel_fail(std::string("segmented_reduce: expected int64, got ") + dtype_name(ids.dtype));
+  if (!ids.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
+  if (values.rows != ids.rows) kernel_fail("segmented_reduce: values/segment_ids length mismatch");
+  if (num < 0) kernel_fail("segmented_reduce: negative segment count");
+  int64_t n = ids.rows;
+  if (n) {
+    c.reset_err();
+    k_check_ids<<<c.grid_for(n, 256), 256, 0, c.stream>>>(ids.ptr<int64_t>(), n, num, c.d_err);
+    c.count_launch();
+    int64_t bad = c.read_err();
+    if (bad >= 0) {
+      int64_t row = bad / 2;
+      if (bad % 2 == 0) kernel_fail("segmented_reduce: segment_ids decrease at row " + std::to_string(row), row);
+      int64_t s = read_scalar<int64_t>(c, ids, row);
+      kernel_fail("segmented_reduce: segment id " + std::to_string(s) + " out of range [0," + std::to_string(num) +
+                      ") at row " + std::to_string(row),
+                  row);
+    }
+  }
+  Tensor lo = c.alloc(TQP_I64, num, 1), hi = c.alloc(TQP_I64, num, 1);
+  if (num) {
+    k_runs<<<c.grid_for(num, 256), 256, 0, c.stream>>>(ids.ptr<int64_t>(), n, num, lo.ptr<int64_t>(), hi.ptr<int64_t>());
+    c.count_launch();
+  }
+  if (op == TQP_COUNT) {
+    Tensor o = c.alloc(TQP_I64, num, 1);
+    if (num) {
+      k_count<<<c.grid_for(num, 256), 256, 0, c.stream>>>(lo.ptr<int64_t>(), hi.ptr<int64_t>(), num, o.ptr<int64_t>());
+      c.count_launch();
+    }
+    return o;
+  }
+  if (values.dtype == TQP_BOOL || values.dtype == TQP_STR8) kernel_fail("segmented_reduce: bool values not supported");
+  if (op == TQP_MIN || op == TQP_MAX) {
+    if (num) {
+      c.reset_err();
+      k_first_empty<<<c.grid_for(num, 256), 256, 0, c.stream>>>(lo.ptr<int64_t>(), hi.ptr<int64_t>(), num, c.d_err);
+      c.count_launch();
+      int64_t s = c.read_err();
+      if (s >= 0) {
+        kernel_fail("segmented_reduce: empty segment " + std::to_string(s) + " for " + (op == TQP_MIN ? "min" : "max"));
+      }
+    }
+  } else if (op != TQP_SUM) {
+    kernel_fail("segmented_reduce: bad op");
+  }
+  Tensor out = c.alloc(values.dtype, num, 1);
+  if (!num) return out;
+  if (op == TQP_SUM) TQP_CUDA(cudaMemsetAsync(out.data(), 0, out.bytes(), c.stream));
+  switch (values.dtype) {
+    case TQP_F64:
+      if (op == TQP_SUM) run_reduce<double, TQP_SUM>(c, values, lo, hi, num, out);
+      else if (op == TQP_MIN) run_reduce<double, TQP_MIN>(c, values, lo, hi, num, out);
+      else run_reduce<double, TQP_MAX>(c, values, lo, hi, num, out);
+      break;
+    case TQP_I64:
+      if (op == TQP_SUM) run_reduce<int64_t, TQP_SUM>(c, values, lo, hi, num, out);
+      else if (op == TQP_MIN) run_reduce<int64_t, TQP_MIN>(c, values, lo, hi, num, out);
+      else run_reduce<int64_t, TQP_MAX>(c, values, lo, hi, num, out);
+      break;
+    case TQP_I32:
+      if (op == TQP_SUM) run_reduce<int32_t, TQP_SUM>(c, values, lo, hi, num, out);
+      else if (op == TQP_MIN) run_reduce<int32_t, TQP_MIN>(c, values, lo, hi, num, out);
+      else run_reduce<int32_t, TQP_MAX>(c, values, lo, hi, num, out);
+      break;
+    default: kernel_fail("segmented_reduce: unsupported dtype");
+  }
+  if (op == TQP_SUM && values.dtype != TQP_F64) {
+    int64_t s = c.read_err();
+    if (s >= 0) kernel_fail("segmented_reduce: sum overflow in segment " + std::to_string(s));
+  }
+  return out;
+}
+
+}  // namespace k
+}  // namespace tqp

@@ -1,0 +1,153 @@
+// Runtime: context, stream-ordered device memory, tensor upload/download.
+// Replaces the reference's host-only storage (tensor.hpp:105-121) and the
+// thread-pool backend (backend.cpp:27-178) with one CUDA stream per context
+// and a stream-ordered memory pool; slots freed at their last use return
+// memory to the pool without a device synchronisation.
+#include <cstring>
+#include <string>
+
+#include "device.cuh"
+
+namespace tqp {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + " (" + what + ")");
+  }
+}
+
+DevBuf::~DevBuf() {
+  if (ptr && ctx) cudaFreeAsync(ptr, ctx->stream);
+}
+
+size_t dtype_size(int dtype) {
+  switch (dtype) {
+    case TQP_BOOL: return 1;
+    case TQP_I32: return 4;
+    case TQP_I64: return 8;
+    case TQP_F64: return 8;
+    case TQP_STR8: return 1;
+  }
+  return 0;
+}
+
+size_t Tensor::elem_size() const { return dtype_size(dtype); }
+
+const char* dtype_name(int dtype) {
+  switch (dtype) {
+    case TQP_BOOL: return "bool";
+    case TQP_I32: return "int32";
+    case TQP_I64: return "int64";
+    case TQP_F64: return "float64";
+    case TQP_STR8: return "int32";  // strings are Int32 tensors in the reference
+  }
+  return "?";
+}
+
+const char* logical_type_name(int lt) {
+  switch (lt) {
+    case TQP_LT_INT64: return "int64";
+    case TQP_LT_FLOAT64: return "float64";
+    case TQP_LT_DATE: return "date";
+    case TQP_LT_UTF8: return "utf8";
+    case TQP_LT_BOOL: return "bool";
+  }
+  return "?";
+}
+
+int physical_dtype(int lt) {
+  switch (lt) {
+    case TQP_LT_INT64: return TQP_I64;
+    case TQP_LT_FLOAT64: return TQP_F64;
+    case TQP_LT_DATE: return TQP_I64;
+    case TQP_LT_UTF8: return TQP_STR8;
+    case TQP_LT_BOOL: return TQP_BOOL;
+  }
+  return -1;
+}
+
+std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
+  auto b = std::make_shared<DevBuf>();
+  b->ctx = this;
+  b->bytes = bytes;
+  if (bytes) TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream));
+  return b;
+}
+
+Tensor Ctx::alloc(int dtype, int64_t rows, int64_t cols) {
+  Tensor t;
+  t.dtype = dtype;
+  t.rows = rows;
+  t.cols = cols;
+  // pad to 16 B so vectorised kernels may read whole 128-bit words
+  size_t bytes = static_cast<size_t>(rows * cols) * dtype_size(dtype);
+  t.buf = alloc_bytes((bytes + 15) & ~size_t(15));
+  t.buf->bytes = bytes;
+  return t;
+}
+
+void Ctx::sync() { TQP_CUDA(cudaStreamSynchronize(stream)); }
+
+void Ctx::reset_err() {
+  long long init[3] = {kNoBad, 0, 0};
+  TQP_CUDA(cudaMemcpyAsync(d_err, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+}
+
+int64_t Ctx::read_err(long long* aux, long long* kind) {
+  TQP_CUDA(cudaMemcpyAsync(h_err, d_err, 3 * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+  sync();
+  if (aux) *aux = h_err[1];
+  if (kind) *kind = h_err[2];
+  return h_err[0] == kNoBad ? -1 : h_err[0];
+}
+
+int Ctx::grid_for(int64_t n, int block, int per_thread, int waves) const {
+  int64_t need = (n + static_cast<int64_t>(block) * per_thread - 1) / (static_cast<int64_t>(block) * per_thread);
+  int64_t cap = static_cast<int64_t>(num_sms) * waves;
+  if (need < 1) need = 1;
+  return static_cast<int>(need < cap ? need : cap);
+}
+
+Tensor upload(Ctx& c, int dtype, int64_t rows, int64_t cols, const void* host) {
+  if (rows < 0 || cols < 1) kernel_fail("tensor: buffer length does not match shape");
+  Tensor t = c.alloc(dtype, rows, cols);
+  if (t.bytes()) TQP_CUDA(cudaMemcpyAsync(t.data(), host, t.bytes(), cudaMemcpyHostToDevice, c.stream));
+  return t;
+}
+
+void download(Ctx& c, const Tensor& t, void* host) {
+  if (t.bytes()) TQP_CUDA(cudaMemcpyAsync(host, t.data(), t.bytes(), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+}
+
+namespace {
+__global__ void k_i32_to_u8(const int32_t* __restrict__ in, uint8_t* __restrict__ out, int64_t n) {
+  for (int64_t i = gtid(); i < n; i += gstride()) out[i] = static_cast<uint8_t>(in[i]);
+}
+__global__ void k_u8_to_i32(const uint8_t* __restrict__ in, int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = gtid(); i < n; i += gstride()) out[i] = in[i];
+}
+}  // namespace
+
+namespace k {
+Tensor utf8_i32_to_str8(Ctx& c, const Tensor& t) {
+  Tensor o = c.alloc(TQP_STR8, t.rows, t.cols);
+  int64_t n = t.size();
+  if (n) {
+    k_i32_to_u8<<<c.grid_for(n, 256), 256, 0, c.stream>>>(t.ptr<int32_t>(), o.ptr<uint8_t>(), n);
+    c.count_launch();
+  }
+  return o;
+}
+Tensor str8_to_i32(Ctx& c, const Tensor& t) {
+  Tensor o = c.alloc(TQP_I32, t.rows, t.cols);
+  int64_t n = t.size();
+  if (n) {
+    k_u8_to_i32<<<c.grid_for(n, 256), 256, 0, c.stream>>>(t.ptr<uint8_t>(), o.ptr<int32_t>(), n);
+    c.count_launch();
+  }
+  return o;
+}
+}  // namespace k
+
+}  // namespace tqp

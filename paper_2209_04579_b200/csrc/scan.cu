@@ -1,0 +1,286 @@
+// Scan-shaped kernels: prefix_sum_exclusive (kernels.cpp:349-362), compact
+// (kernels.cpp:364-409), expand_segments (kernels.cpp:486-516), searchsorted
+// (kernels.cpp:457-484). The reference runs the scans serially; here they
+// are single-pass decoupled-lookback scans over 2048-element tiles.
+#include <string>
+
+#include "scan.cuh"
+
+namespace tqp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kTile = kThreads * kItems;
+
+struct ScanScratch {
+  std::shared_ptr<DevBuf> buf;
+  longlong2* desc;
+  int* counter;
+};
+
+ScanScratch scan_scratch(Ctx& c, int64_t tiles) {
+  ScanScratch s;
+  size_t bytes = sizeof(longlong2) * (tiles + 1) + 16;
+  s.buf = c.alloc_bytes(bytes);
+  TQP_CUDA(cudaMemsetAsync(s.buf->ptr, 0, bytes, c.stream));
+  s.desc = static_cast<longlong2*>(s.buf->ptr);
+  s.counter = reinterpret_cast<int*>(s.desc + tiles + 1);
+  return s;
+}
+
+// Exclusive int64 scan; reports the first row where the sequential
+// accumulation overflows (the reference's check order, kernels.cpp:356-359).
+__global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restrict__ x, int64_t* __restrict__ out,
+                                                         int64_t n, longlong2* desc, int* counter, long long* err) {
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_warp[33];
+  __shared__ long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  int64_t v[kItems];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    v[j] = base + j < n ? x[base + j] : 0;
+    local += static_cast<unsigned long long>(v[j]);
+  }
+  unsigned long long total;
+  unsigned long long texcl = block_exclusive_scan(local, s_warp, &total);
+  if (threadIdx.x < 32) {
+    long long p = tile_lookback(desc, tile, static_cast<long long>(total));
+    if (threadIdx.x == 0) s_prefix = p;
+  }
+  __syncthreads();
+  unsigned long long acc = static_cast<unsigned long long>(s_prefix) + texcl;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (base + j < n) {
+      out[base + j] = static_cast<int64_t>(acc);
+      int64_t r;
+      if (add_ovf(static_cast<int64_t>(acc), v[j], &r)) note_bad(err, base + j);
+      acc += static_cast<unsigned long long>(v[j]);
+    }
+  }
+}
+
+// Pass 1 of compact: selected-row count per tile.
+__global__ void __launch_bounds__(kThreads) k_mask_count(const uint8_t* __restrict__ mask, int64_t n,
+                                                         int64_t* __restrict__ counts) {
+  __shared__ unsigned long long s_warp[33];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  unsigned long long local = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) local += (base + j < n && mask[base + j]) ? 1 : 0;
+  unsigned long long total;
+  block_exclusive_scan(local, s_warp, &total);
+  if (threadIdx.x == 0) counts[blockIdx.x] = static_cast<int64_t>(total);
+}
+
+// Pass 3 of compact: order-preserving scatter of whole rows.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_compact_scatter(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
+                                                              int64_t n, int64_t m, const int64_t* __restrict__ offs,
+                                                              T* __restrict__ out) {
+  __shared__ unsigned long long s_warp[33];
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  uint8_t sel[kItems];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    sel[j] = (base + j < n && mask[base + j]) ? 1 : 0;
+    local += sel[j];
+  }
+  unsigned long long total;
+  unsigned long long w = block_exclusive_scan(local, s_warp, &total) + static_cast<unsigned long long>(offs[blockIdx.x]);
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (sel[j]) {
+      for (int64_t q = 0; q < m; ++q) out[w * m + q] = vals[(base + j) * m + q];
+      ++w;
+    }
+  }
+}
+
+__global__ void k_check_negative(const int64_t* __restrict__ c, int64_t n, long long* err) {
+  for (int64_t i = gtid(); i < n; i += gstride())
+    if (c[i] < 0) note_bad(err, i);
+}
+
+__global__ void k_expand(const int64_t* __restrict__ starts, const int64_t* __restrict__ offs, int64_t k,
+                         int64_t total, int64_t* __restrict__ out) {
+  for (int64_t j = gtid(); j < total; j += gstride()) {
+    // last segment whose offset <= j (upper_bound - 1)
+    int64_t lo = 0, hi = k;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (offs[mid] <= j) lo = mid + 1;
+      else hi = mid;
+    }
+    int64_t s = lo - 1;
+    out[j] = starts[s] + (j - offs[s]);
+  }
+}
+
+template <typename T>
+__global__ void k_nan_check(const T* __restrict__ v, int64_t n, long long* err) {
+  if constexpr (std::is_same_v<T, double>) {
+    for (int64_t i = gtid(); i < n; i += gstride())
+      if (isnan(v[i])) note_bad(err, i);
+  }
+}
+
+template <typename T>
+__global__ void k_sorted_check(const T* __restrict__ v, int64_t n, long long* err) {
+  for (int64_t i = gtid() + 1; i < n; i += gstride())
+    if (v[i] < v[i - 1]) note_bad(err, i);
+}
+
+template <typename T>
+__global__ void k_searchsorted(const T* __restrict__ s, int64_t n, const T* __restrict__ p, int64_t np, bool left,
+                               int64_t* __restrict__ out) {
+  for (int64_t i = gtid(); i < np; i += gstride()) {
+    T x = p[i];
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      bool go_right = left ? (s[mid] < x) : !(x < s[mid]);
+      if (go_right) lo = mid + 1;
+      else hi = mid;
+    }
+    out[i] = lo;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) kernel_fail(msg);
+}
+
+}  // namespace
+
+namespace k {
+
+// Exclusive scan of an int64 vector; fills `first_overflow` (or -1).
+Tensor prefix_sum_raw(Ctx& c, const Tensor& x, int64_t* first_overflow) {
+  int64_t n = x.rows;
+  Tensor o = c.alloc(TQP_I64, n, 1);
+  *first_overflow = -1;
+  if (!n) return o;
+  int64_t tiles = (n + kTile - 1) / kTile;
+  auto s = scan_scratch(c, tiles);
+  c.reset_err();
+  k_prefix_sum<<<tiles, kThreads, 0, c.stream>>>(x.ptr<int64_t>(), o.ptr<int64_t>(), n, s.desc, s.counter, c.d_err);
+  c.count_launch();
+  *first_overflow = c.read_err();
+  return o;
+}
+
+Tensor prefix_sum_exclusive(Ctx& c, const Tensor& x) {
+  require(x.is_vector(), "prefix_sum_exclusive: expected a vector (m=1)");
+  if (x.dtype != TQP_I64) {
+    kernel_fail(std::string("prefix_sum_exclusive: expected int64, got ") + dtype_name(x.dtype));
+  }
+  int64_t bad;
+  Tensor o = prefix_sum_raw(c, x, &bad);
+  if (bad >= 0) kernel_fail("prefix_sum_exclusive: overflow at row " + std::to_string(bad), bad);
+  return o;
+}
+
+Tensor compact(Ctx& c, const Tensor& values, const Tensor& mask) {
+  if (mask.dtype != TQP_BOOL) kernel_fail(std::string("compact: expected bool, got ") + dtype_name(mask.dtype));
+  require(mask.is_vector(), "compact: expected a vector (m=1)");
+  if (mask.rows != values.rows) {
+    kernel_fail("compact: mask length " + std::to_string(mask.rows) + " does not match rows " +
+                std::to_string(values.rows));
+  }
+  int64_t n = values.rows, m = values.cols;
+  if (n == 0) return c.alloc(values.dtype, 0, m);
+  int64_t tiles = (n + kTile - 1) / kTile;
+  Tensor counts = c.alloc(TQP_I64, tiles, 1);
+  k_mask_count<<<tiles, kThreads, 0, c.stream>>>(mask.ptr<uint8_t>(), n, counts.ptr<int64_t>());
+  c.count_launch();
+  int64_t ovf;
+  Tensor offs = prefix_sum_raw(c, counts, &ovf);
+  int64_t last_off = 0, last_cnt = 0;
+  TQP_CUDA(cudaMemcpyAsync(&last_off, offs.ptr<int64_t>() + tiles - 1, 8, cudaMemcpyDeviceToHost, c.stream));
+  TQP_CUDA(cudaMemcpyAsync(&last_cnt, counts.ptr<int64_t>() + tiles - 1, 8, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  int64_t total = last_off + last_cnt;
+  Tensor o = c.alloc(values.dtype, total, m);
+  if (total) {
+    TQP_DISPATCH(values.dtype, T,
+                 k_compact_scatter<T><<<tiles, kThreads, 0, c.stream>>>(values.ptr<T>(), mask.ptr<uint8_t>(), n, m,
+                                                                        offs.ptr<int64_t>(), o.ptr<T>()));
+    c.count_launch();
+  }
+  return o;
+}
+
+Tensor expand_segments(Ctx& c, const Tensor& starts, const Tensor& counts) {
+  if (starts.dtype != TQP_I64) kernel_fail(std::string("expand_segments: expected int64, got ") + dtype_name(starts.dtype));
+  if (counts.dtype != TQP_I64) kernel_fail(std::string("expand_segments: expected int64, got ") + dtype_name(counts.dtype));
+  require(starts.is_vector(), "expand_segments: expected a vector (m=1)");
+  require(counts.is_vector(), "expand_segments: expected a vector (m=1)");
+  if (starts.rows != counts.rows) kernel_fail("expand_segments: starts/counts length mismatch");
+  int64_t kk = starts.rows;
+  if (kk == 0) return c.alloc(TQP_I64, 0, 1);
+  c.reset_err();
+  k_check_negative<<<c.grid_for(kk, 256), 256, 0, c.stream>>>(counts.ptr<int64_t>(), kk, c.d_err);
+  c.count_launch();
+  int64_t neg = c.read_err();
+  if (neg >= 0) kernel_fail("expand_segments: negative count at row " + std::to_string(neg), neg);
+  int64_t ovf;
+  Tensor offs = prefix_sum_raw(c, counts, &ovf);
+  if (ovf >= 0) kernel_fail("expand_segments: total length overflow");
+  int64_t last_off = read_scalar<int64_t>(c, offs, kk - 1);
+  int64_t last_cnt = read_scalar<int64_t>(c, counts, kk - 1);
+  int64_t total;
+  if (__builtin_add_overflow(last_off, last_cnt, &total)) kernel_fail("expand_segments: total length overflow");
+  Tensor o = c.alloc(TQP_I64, total, 1);
+  if (total) {
+    k_expand<<<c.grid_for(total, 256), 256, 0, c.stream>>>(starts.ptr<int64_t>(), offs.ptr<int64_t>(), kk, total,
+                                                           o.ptr<int64_t>());
+    c.count_launch();
+  }
+  return o;
+}
+
+Tensor searchsorted(Ctx& c, const Tensor& sorted, const Tensor& probes, int side) {
+  {
+    int da = sorted.dtype, db = probes.dtype;
+    if (da != db) {
+      kernel_fail(std::string("searchsorted: dtype mismatch (") + dtype_name(da) + " vs " + dtype_name(db) + ")");
+    }
+  }
+  require(sorted.is_vector(), "searchsorted: expected a vector (m=1)");
+  require(probes.is_vector(), "searchsorted: expected a vector (m=1)");
+  int64_t n = sorted.rows, np = probes.rows;
+  Tensor o = c.alloc(TQP_I64, np, 1);
+  TQP_DISPATCH(sorted.dtype, T, {
+    if (std::is_same_v<T, double>) {
+      c.reset_err();
+      if (n) k_nan_check<T><<<c.grid_for(n, 256), 256, 0, c.stream>>>(sorted.ptr<T>(), n, c.d_err);
+      if (np) k_nan_check<T><<<c.grid_for(np, 256), 256, 0, c.stream>>>(probes.ptr<T>(), np, c.d_err);
+      c.count_launch(2);
+      if (c.read_err() >= 0) kernel_fail("searchsorted: NaN in keys");
+    }
+    if (n > 1) {
+      c.reset_err();
+      k_sorted_check<T><<<c.grid_for(n, 256), 256, 0, c.stream>>>(sorted.ptr<T>(), n, c.d_err);
+      c.count_launch();
+      int64_t bad = c.read_err();
+      if (bad >= 0) kernel_fail("searchsorted: input not non-decreasing at row " + std::to_string(bad), bad);
+    }
+    if (np) {
+      k_searchsorted<T><<<c.grid_for(np, 256), 256, 0, c.stream>>>(sorted.ptr<T>(), n, probes.ptr<T>(), np,
+                                                                   side == TQP_LEFT, o.ptr<int64_t>());
+      c.count_launch();
+    }
+  });
+  return o;
+}
+
+}  // namespace k
+}  // namespace tqp

@@ -1,0 +1,142 @@
+// Internal C++ interfaces of libtqp_b200.so (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tqp_b200.h"
+
+namespace tqp {
+
+// Error carrying the reference's exception class (tqp_error_code) and
+// message; the C boundary converts it into a tqp_status.
+struct Error : std::runtime_error {
+  int code;
+  int64_t bad_row;
+  Error(int c, const std::string& m, int64_t row = -1) : std::runtime_error(m), code(c), bad_row(row) {}
+};
+[[noreturn]] inline void kernel_fail(const std::string& m, int64_t row = -1) { throw Error(TQP_ERR_KERNEL, m, row); }
+[[noreturn]] inline void exec_fail(const std::string& m) { throw Error(TQP_ERR_EXEC, m); }
+[[noreturn]] inline void plan_fail(const std::string& m) { throw Error(TQP_ERR_PLAN, m); }
+
+void cuda_check(cudaError_t e, const char* what);
+#define TQP_CUDA(x) ::tqp::cuda_check((x), #x)
+
+struct Ctx;
+
+// Stream-ordered device allocation (freed on the owning context's stream).
+struct DevBuf {
+  Ctx* ctx = nullptr;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~DevBuf();
+};
+
+// Immutable device tensor: the device analogue of tensql::Tensor
+// (tensor.hpp:49-122), shared by reference.
+struct Tensor {
+  int dtype = TQP_I64;
+  int64_t rows = 0, cols = 1;
+  std::shared_ptr<DevBuf> buf;
+
+  int64_t size() const { return rows * cols; }
+  bool is_vector() const { return cols == 1; }
+  bool is_scalar() const { return rows == 1 && cols == 1; }
+  bool same_shape(const Tensor& o) const { return rows == o.rows && cols == o.cols; }
+  size_t elem_size() const;
+  size_t bytes() const { return static_cast<size_t>(size()) * elem_size(); }
+  template <typename T>
+  T* ptr() const { return buf ? static_cast<T*>(buf->ptr) : nullptr; }
+  void* data() const { return buf ? buf->ptr : nullptr; }
+};
+
+const char* dtype_name(int dtype);  // reference names (tensor.cpp:5-13); STR8 -> "int32"
+size_t dtype_size(int dtype);
+const char* logical_type_name(int lt);
+int physical_dtype(int lt);  // device physical dtype of a logical type
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaMemPool_t pool = nullptr;
+  // device scratch for kernel error reporting: [0] first bad index
+  // (atomicMin, INT64_MAX = none), [1] aux value, [2] error kind
+  long long* d_err = nullptr;
+  long long* h_err = nullptr;  // pinned mirror
+  std::atomic<int64_t> launches{0};
+
+  Tensor alloc(int dtype, int64_t rows, int64_t cols);
+  std::shared_ptr<DevBuf> alloc_bytes(size_t bytes);
+  void sync();
+  void reset_err();
+  // copies d_err to host (syncs); returns first bad index or -1
+  int64_t read_err(long long* aux = nullptr, long long* kind = nullptr);
+  int grid_for(int64_t n, int block, int per_thread = 1, int waves = 8) const;
+  void count_launch(int n = 1) { launches += n; }
+};
+
+Tensor upload(Ctx& c, int dtype, int64_t rows, int64_t cols, const void* host);
+void download(Ctx& c, const Tensor& t, void* host);
+template <typename T>
+T read_scalar(Ctx& c, const Tensor& t, int64_t index = 0) {
+  T v{};
+  TQP_CUDA(cudaMemcpyAsync(&v, t.ptr<T>() + index, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return v;
+}
+
+// ---- kernel set (kernels.cu / scan.cu / sort.cu / reduce.cu) ---------------
+namespace k {
+Tensor compare(Ctx&, const Tensor& a, const Tensor& b, int op);
+Tensor arith(Ctx&, const Tensor& a, const Tensor& b, int op);
+Tensor logical(Ctx&, const Tensor& a, const Tensor& b, int op);
+Tensor logical_not(Ctx&, const Tensor& v);
+Tensor select_where(Ctx&, const Tensor& cond, const Tensor& a, const Tensor& b);
+Tensor prefix_sum_exclusive(Ctx&, const Tensor& x);
+Tensor compact(Ctx&, const Tensor& values, const Tensor& mask);
+Tensor argsort_stable(Ctx&, const Tensor& keys);
+Tensor gather(Ctx&, const Tensor& values, const Tensor& idx);
+Tensor searchsorted(Ctx&, const Tensor& sorted, const Tensor& probes, int side);
+Tensor expand_segments(Ctx&, const Tensor& starts, const Tensor& counts);
+Tensor segment_starts(Ctx&, const Tensor& sorted_keys);
+Tensor segmented_reduce(Ctx&, const Tensor& values, const Tensor& ids, int64_t num_segments, int op);
+Tensor matmul(Ctx&, const Tensor& a, const Tensor& b);
+Tensor substring_match(Ctx&, const Tensor& chars, const std::string& pattern, int anchor);
+// plumbing
+Tensor iota(Ctx&, int64_t n);
+Tensor cast(Ctx&, const Tensor& t, int to);
+Tensor exp_f64(Ctx&, const Tensor& t);
+Tensor last_or_zero(Ctx&, const Tensor& t);
+Tensor pack_cols(Ctx&, const std::vector<Tensor>& cols);
+Tensor broadcast_rows(Ctx&, const Tensor& value, int64_t n);
+Tensor pad_width_like(Ctx&, const Tensor& t, const Tensor& like);
+Tensor sort_perm_rows(Ctx&, const Tensor& key, const Tensor& perm, bool asc);
+Tensor string_compare(Ctx&, const Tensor& a, const Tensor& b, int op);
+// helpers
+Tensor utf8_i32_to_str8(Ctx&, const Tensor& t);
+Tensor str8_to_i32(Ctx&, const Tensor& t);
+// stable radix argsort of `keys` (vector) applied to payload `perm`
+// (perm = nullptr means identity); descending via inverted digits
+Tensor radix_sort_payload(Ctx&, const Tensor& keys, const Tensor* perm, bool descending);
+// exclusive int64 scan; *first_overflow = first overflowing row or -1
+Tensor prefix_sum_raw(Ctx&, const Tensor& x, int64_t* first_overflow);
+}  // namespace k
+
+}  // namespace tqp
+
+// C handles
+struct tqp_tensor {
+  tqp::Tensor t;
+  std::atomic<int> refs{1};
+};
+struct tqp_ctx {
+  tqp::Ctx c;
+};

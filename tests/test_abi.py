@@ -1,0 +1,56 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/*.h declares, and the headers compile as C and C++."""
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from conftest import ROOT
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "tqp_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(tqp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2209_04579_b200 import tqp
+    lib = tqp.lib
+    syms = declared_symbols()
+    assert len(syms) >= 70
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.tqp_abi_version() == 1
+
+
+def test_nm_exports_match_header():
+    lib = ROOT / "paper_2209_04579_b200" / "libtqp_b200.so"
+    out = subprocess.run(["nm", "-D", "--defined-only", str(lib)], capture_output=True, text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.split()[-1].startswith("tqp_")}
+    assert set(declared_symbols()) <= exported
+
+
+@pytest.mark.parametrize("compiler,std", [("gcc", "-std=c99"), ("g++", "-std=c++17")])
+def test_headers_compile(tmp_path, compiler, std):
+    src = tmp_path / ("t.c" if compiler == "gcc" else "t.cpp")
+    src.write_text('#include "tqp_b200.h"\n#include "tqp_gen.h"\nint main(void){return tqp_gen_dummy();}\n'
+                   .replace("tqp_gen_dummy()", "(int)tqp_lineitem_rows(0.001) == 6000 ? 0 : 1"))
+    exe = tmp_path / "t"
+    subprocess.run([compiler, std, "-Wall", "-Werror", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
+
+
+def test_status_struct_layout():
+    import ctypes
+    from paper_2209_04579_b200 import tqp
+    assert ctypes.sizeof(tqp.Status) == 4 + 4 + 8 + 1024  # int, pad, int64, msg
+
+
+def test_plan_builder_without_gpu():
+    """Plans are host objects: building one from a committed lowered plan
+    needs no device."""
+    from paper_2209_04579_b200 import tqp
+    p = tqp.Plan.from_file(ROOT / "paper_2209_04579_b200" / "plans" / "q6.opplan.json")
+    assert p.h

@@ -1,0 +1,124 @@
+"""Pins the numpy oracle (oracle/tqp_oracle.py) to the reference itself:
+every fixture under tests/golden/ was produced by running the unmodified
+reference library (oracle/tools/golden_cases.cpp, oracle/tools/ref_runner.cpp)."""
+import json
+
+import numpy as np
+import pytest
+
+import tqp_oracle as O
+from conftest import GOLDEN, load_tpch_golden
+
+
+def run_kernel(case):
+    a = case["args"]
+    t = [O.tensor_from_json(x) for x in a["tensors"]]
+    k = case["kernel"]
+    if k == "compare":
+        return O.compare(t[0], t[1], O.CMP[a["op"]])
+    if k == "arith":
+        return O.arith(t[0], t[1], O.ARITH[a["op"]])
+    if k == "logical":
+        return O.logical(t[0], t[1], ["and", "or"][a["op"]])
+    if k == "not":
+        return O.logical_not(t[0])
+    if k == "select_where":
+        return O.select_where(*t)
+    if k == "prefix_sum_exclusive":
+        return O.prefix_sum_exclusive(t[0])
+    if k == "compact":
+        return O.compact(t[0], t[1])
+    if k == "argsort_stable":
+        return O.argsort_stable(t[0])
+    if k == "gather":
+        return O.gather(t[0], t[1])
+    if k == "searchsorted":
+        return O.searchsorted(t[0], t[1], ["left", "right"][a["side"]])
+    if k == "expand_segments":
+        return O.expand_segments(t[0], t[1])
+    if k == "segment_starts":
+        return O.segment_starts(t[0])
+    if k == "segmented_reduce":
+        return O.segmented_reduce(t[0], t[1], a["num"], ["sum", "count", "min", "max"][a["op"]])
+    if k == "matmul":
+        return O.matmul(t[0], t[1])
+    if k == "substring_match":
+        return O.substring_match(t[0], a["pattern"], ["start", "end", "any", "exact"][a["anchor"]])
+    raise AssertionError(k)
+
+
+def assert_tensor_equal(got, want, fsum=False, scale=0.0):
+    assert got.shape == want.shape, (got.shape, want.shape)
+    if want.dtype == np.float64 and fsum:
+        for g, w in zip(got.ravel(), want.ravel()):
+            assert O.approx_rel(float(g), float(w), 1e-9, scale), (g, w)
+    elif want.dtype == np.float64:
+        np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+        m = ~np.isnan(want)
+        assert np.array_equal(got[m].view(np.int64), want[m].view(np.int64)) or np.array_equal(got[m], want[m])
+    else:
+        assert got.dtype == want.dtype, (got.dtype, want.dtype)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_oracle_kernels_match_reference(golden_kernels):
+    assert len(golden_kernels) > 150
+    for case in golden_kernels:
+        if "error" in case:
+            with pytest.raises(O.KernelError) as ei:
+                run_kernel(case)
+            assert str(ei.value) == case["error"], case["kernel"]
+            continue
+        got = run_kernel(case)
+        want = O.tensor_from_json(case["out"])
+        fsum = case["kernel"] == "segmented_reduce" and case["args"]["op"] == 0
+        scale = float(np.abs(O.tensor_from_json(case["args"]["tensors"][0])).sum()) if fsum else 0.0
+        assert_tensor_equal(got, want, fsum, scale)
+
+
+def compare_tables(got, want_json, tol=1e-9):
+    """tables_diff_ordered (tests/support/table_compare.hpp:37-64)."""
+    cols = want_json["columns"]
+    assert len(got) == len(cols)
+    for (name, typ, arr), c in zip(got, cols):
+        assert name.lower() == c["name"].lower()
+        assert typ == c["type"]
+        want = O.tensor_from_json(c["tensor"])
+        if typ == "utf8":
+            # decoded strings compare (widths may differ only by padding)
+            assert O_decode(arr) == O_decode(want)
+            continue
+        assert arr.shape == want.shape, (name, arr.shape, want.shape)
+        if want.dtype == np.float64:
+            for g, w in zip(arr.ravel(), want.ravel()):
+                assert (np.isnan(g) and np.isnan(w)) or O.approx_rel(float(g), float(w), tol), (name, g, w)
+        else:
+            np.testing.assert_array_equal(arr, want)
+
+
+def O_decode(a):
+    return [bytes(int(x) for x in r).split(b"\0", 1)[0] for r in a]
+
+
+def test_oracle_plans_match_reference(golden_plans):
+    assert len(golden_plans) > 30
+    for case in golden_plans:
+        tables = O.tables_from_json(case["tables"])
+        if "error" in case:
+            with pytest.raises(O.ExecError) as ei:
+                O.execute(case["opplan"], tables)
+            assert str(ei.value) == case["error"], case["name"]
+            continue
+        got = O.execute(case["opplan"], tables)
+        compare_tables(got, case["result"])
+
+
+def test_tpch_golden_results_match_oracle():
+    """TPC-H Q1/Q3/Q6/Q14 at SF0.005: oracle executor over the committed
+    lowered plans vs the reference executor's results (ref_runner)."""
+    gold = load_tpch_golden()
+    tables = O.tables_from_json(gold["tables"])
+    for q in ("q1", "q3", "q6", "q14"):
+        plan = json.loads((GOLDEN.parent.parent / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
+        got = O.execute(plan, tables)
+        compare_tables(got, gold["results"][q])
