@@ -304,7 +304,9 @@ __global__ void k_long_finish(const typename Acc<T, OP>::P* __restrict__ parts, 
 template <typename T, int OP>
 void run_reduce(Ctx& c, const Tensor& values, const Tensor& lo, const Tensor& hi, int64_t num, Tensor& out) {
   using P = typename Acc<T, OP>::P;
-  auto long_buf = c.alloc_bytes(sizeof(int64_t) * (num / kLong + 2) + 16);
+  // at most min(num, n / kLong) segments can be longer than kLong rows
+  int64_t max_long = std::min<int64_t>(num, values.rows / kLong + 1);
+  auto long_buf = c.alloc_bytes(sizeof(int64_t) * (max_long + 1) + 16);
   TQP_CUDA(cudaMemsetAsync(long_buf->ptr, 0, 8, c.stream));
   auto* long_count = static_cast<unsigned long long*>(long_buf->ptr);
   auto* long_list = reinterpret_cast<int64_t*>(static_cast<char*>(long_buf->ptr) + 16);
@@ -321,7 +323,6 @@ void run_reduce(Ctx& c, const Tensor& values, const Tensor& lo, const Tensor& hi
   TQP_CUDA(cudaMemcpyAsync(segs.data(), long_list, 8 * nlong, cudaMemcpyDeviceToHost, c.stream));
   c.sync();
   std::sort(segs.begin(), segs.end());
-  std::vector<int64_t> hlo(num ? 0 : 0);
   // fetch run bounds of the long segments
   std::vector<int64_t> slo(nlong), shi(nlong);
   for (size_t q = 0; q < nlong; ++q) {

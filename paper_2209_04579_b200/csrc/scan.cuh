@@ -11,7 +11,16 @@ namespace tqp {
 enum : long long { TILE_INVALID = 0, TILE_PARTIAL = 1, TILE_INCLUSIVE = 2 };
 
 __device__ __forceinline__ void tile_publish(longlong2* desc, int tile, long long status, long long value) {
-  __stcg(desc + tile, make_longlong2(status, value));
+  asm volatile("st.relaxed.gpu.global.v2.s64 [%0], {%1, %2};" ::"l"(desc + tile), "l"(status), "l"(value)
+               : "memory");
+}
+
+// Must be a volatile (re-issued) load: a plain __ldcg may be hoisted out of
+// the spin loop below, which would then read unpublished tiles as zero.
+__device__ __forceinline__ longlong2 tile_read(const longlong2* p) {
+  longlong2 d;
+  asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(d.x), "=l"(d.y) : "l"(p) : "memory");
+  return d;
 }
 
 // Called by ALL lanes of one warp; returns the exclusive prefix of `tile`
@@ -31,7 +40,7 @@ __device__ __forceinline__ long long tile_lookback(longlong2* desc, int tile, lo
     longlong2 d = make_longlong2(TILE_INCLUSIVE, 0);
     if (idx >= 0) {
       do {
-        d = __ldcg(desc + idx);
+        d = tile_read(desc + idx);
       } while (d.x == TILE_INVALID);
     }
     unsigned incl = __ballot_sync(0xffffffffu, d.x == TILE_INCLUSIVE);

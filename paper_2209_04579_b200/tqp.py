@@ -291,8 +291,11 @@ def _t(x: Union[Tensor, np.ndarray], ctx=None) -> Tensor:
 
 
 def _call(fn, ctx: Context, *args) -> Tensor:
+    # Tensor arguments stay referenced (alive) for the duration of the call
     st = Status()
-    h = fn(ctx.h, *args, C.byref(st))
+    raw = [a.h if isinstance(a, Tensor) else a for a in args]
+    h = fn(ctx.h, *raw, C.byref(st))
+    del args
     _check(st, bool(h))
     return Tensor(h, ctx)
 
@@ -304,79 +307,79 @@ def _enum(table, v):
 # ---- the kernel set (kernels.hpp:28-78) --------------------------------------
 def compare(lhs, rhs, op, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_compare, ctx, _t(lhs, ctx).h, _t(rhs, ctx).h, _enum(COMPARE, op))
+    return _call(lib.tqp_compare, ctx, _t(lhs, ctx), _t(rhs, ctx), _enum(COMPARE, op))
 
 
 def arith(lhs, rhs, op, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_arith, ctx, _t(lhs, ctx).h, _t(rhs, ctx).h, _enum(ARITH, op))
+    return _call(lib.tqp_arith, ctx, _t(lhs, ctx), _t(rhs, ctx), _enum(ARITH, op))
 
 
 def logical(lhs, rhs, op, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_logical, ctx, _t(lhs, ctx).h, _t(rhs, ctx).h, _enum(LOGICAL, op))
+    return _call(lib.tqp_logical, ctx, _t(lhs, ctx), _t(rhs, ctx), _enum(LOGICAL, op))
 
 
 def logical_not(v, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_logical_not, ctx, _t(v, ctx).h)
+    return _call(lib.tqp_logical_not, ctx, _t(v, ctx))
 
 
 def select_where(cond, a, b, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_select_where, ctx, _t(cond, ctx).h, _t(a, ctx).h, _t(b, ctx).h)
+    return _call(lib.tqp_select_where, ctx, _t(cond, ctx), _t(a, ctx), _t(b, ctx))
 
 
 def prefix_sum_exclusive(x, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_prefix_sum_exclusive, ctx, _t(x, ctx).h)
+    return _call(lib.tqp_prefix_sum_exclusive, ctx, _t(x, ctx))
 
 
 def compact(values, mask, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_compact, ctx, _t(values, ctx).h, _t(mask, ctx).h)
+    return _call(lib.tqp_compact, ctx, _t(values, ctx), _t(mask, ctx))
 
 
 def argsort_stable(keys, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_argsort_stable, ctx, _t(keys, ctx).h)
+    return _call(lib.tqp_argsort_stable, ctx, _t(keys, ctx))
 
 
 def gather(values, idx, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_gather, ctx, _t(values, ctx).h, _t(idx, ctx).h)
+    return _call(lib.tqp_gather, ctx, _t(values, ctx), _t(idx, ctx))
 
 
 def searchsorted(sorted_, probes, side, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_searchsorted, ctx, _t(sorted_, ctx).h, _t(probes, ctx).h, _enum(SIDE, side))
+    return _call(lib.tqp_searchsorted, ctx, _t(sorted_, ctx), _t(probes, ctx), _enum(SIDE, side))
 
 
 def expand_segments(starts, counts, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_expand_segments, ctx, _t(starts, ctx).h, _t(counts, ctx).h)
+    return _call(lib.tqp_expand_segments, ctx, _t(starts, ctx), _t(counts, ctx))
 
 
 def segment_starts(sorted_keys, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_segment_starts, ctx, _t(sorted_keys, ctx).h)
+    return _call(lib.tqp_segment_starts, ctx, _t(sorted_keys, ctx))
 
 
 def segmented_reduce(values, segment_ids, num_segments: int, op, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_segmented_reduce, ctx, _t(values, ctx).h, _t(segment_ids, ctx).h, int(num_segments),
+    return _call(lib.tqp_segmented_reduce, ctx, _t(values, ctx), _t(segment_ids, ctx), int(num_segments),
                  _enum(REDUCE, op))
 
 
 def matmul(a, b, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_matmul, ctx, _t(a, ctx).h, _t(b, ctx).h)
+    return _call(lib.tqp_matmul, ctx, _t(a, ctx), _t(b, ctx))
 
 
 def substring_match(chars, pattern: str, anchor, ctx=None) -> Tensor:
     ctx = ctx or default_context()
     p = pattern.encode("utf-8")
-    return _call(lib.tqp_substring_match, ctx, _t(chars, ctx).h, p, len(p), _enum(ANCHOR, anchor))
+    return _call(lib.tqp_substring_match, ctx, _t(chars, ctx), p, len(p), _enum(ANCHOR, anchor))
 
 
 # ---- plumbing ops (executor.cpp:190-278) -----------------------------------
@@ -387,37 +390,37 @@ def iota(n: int, ctx=None) -> Tensor:
 
 def cast(t, to, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_cast, ctx, _t(t, ctx).h, _enum(DTYPE_NAMES, to))
+    return _call(lib.tqp_cast, ctx, _t(t, ctx), _enum(DTYPE_NAMES, to))
 
 
 def exp_f64(t, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_exp_f64, ctx, _t(t, ctx).h)
+    return _call(lib.tqp_exp_f64, ctx, _t(t, ctx))
 
 
 def last_or_zero(t, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_last_or_zero, ctx, _t(t, ctx).h)
+    return _call(lib.tqp_last_or_zero, ctx, _t(t, ctx))
 
 
 def broadcast_rows(value, n: int, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_broadcast_rows, ctx, _t(value, ctx).h, int(n))
+    return _call(lib.tqp_broadcast_rows, ctx, _t(value, ctx), int(n))
 
 
 def pad_width_like(t, like, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_pad_width_like, ctx, _t(t, ctx).h, _t(like, ctx).h)
+    return _call(lib.tqp_pad_width_like, ctx, _t(t, ctx), _t(like, ctx))
 
 
 def sort_perm_rows(key, perm, ascending: bool, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_sort_perm_rows, ctx, _t(key, ctx).h, _t(perm, ctx).h, 1 if ascending else 0)
+    return _call(lib.tqp_sort_perm_rows, ctx, _t(key, ctx), _t(perm, ctx), 1 if ascending else 0)
 
 
 def string_compare(a, b, op, ctx=None) -> Tensor:
     ctx = ctx or default_context()
-    return _call(lib.tqp_string_compare, ctx, _t(a, ctx).h, _t(b, ctx).h, _enum(COMPARE, op))
+    return _call(lib.tqp_string_compare, ctx, _t(a, ctx), _t(b, ctx), _enum(COMPARE, op))
 
 
 def pack_cols(cols: Sequence, ctx=None) -> Tensor:
