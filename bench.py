@@ -1,0 +1,361 @@
+"""TQP hot-path benchmark on B200: TPC-H Q1/Q6/Q14/Q3 at SF10 through the
+B200 executor (libtqp_b200.so, C ABI), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--sf 10] [--impl b200|reference]
+
+A step runs the four queries once over device-resident tables (synthetic,
+counter-based generator of include/tqp_gen.h, seed 7). value = lineitem rows
+scanned per second over the four queries (4 x rows per step / step time).
+Inputs per query are 1.9-2.5 GB, far larger than the 126 MB L2, so no L2
+flush is needed between steps. `--impl reference` times the reference's own
+CPU executor (oracle/_ref/tqp_ref_runner, built from /root/reference's
+sources, `par` backend on every host core) on a bounded SF1 sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+METRIC = "TPC-H Q1/Q6/Q14/Q3 rows/s & latency, % HBM roofline, SF10/SF100 at 1-8 B200"
+QUERIES = ("q1", "q6", "q14", "q3")
+REF_RUNNER = ROOT / "oracle" / "_ref" / "tqp_ref_runner"
+
+# Compulsory input bytes per query: 8 B per Int64/Float64/
+# Date value, 1 B per UTF-8 byte; intermediates not credited.
+def algorithmic_bytes(q: str, L: int, P: int, O: int, Cn: int) -> int:
+    return {
+        "q6": 32 * L,
+        "q1": 42 * L,
+        "q14": 32 * L + 33 * P,
+        "q3": 32 * L + 32 * O + 18 * Cn,
+    }[q]
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the
+    timed region; falls back to nvidia-smi when NVML is unavailable."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self.max_mhz = None
+
+    def _run(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, rs))
+                self._stop.wait(0.01)
+        except Exception:  # noqa: BLE001
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip().split(",")
+                    self.max_mhz = float(out[1])
+                    self.samples.append((float(out[0]), int(out[2], 16)))
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        time.sleep(0.05)
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({name for _, rs in self.samples for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def run_reference(args, rank: int) -> None:
+    """Reference arm: the reference's CPU executor (par backend, all cores)."""
+    if rank != 0:
+        return
+    sample_sf = args.ref_sf
+    cores = os.cpu_count() or 1
+    if not REF_RUNNER.exists():
+        print(json.dumps({"impl": "reference", "unavailable": f"{REF_RUNNER} not built (make -C oracle)"}))
+        return
+    cmd = [str(REF_RUNNER), "run", "--sf", str(sample_sf), "--queries", ",".join(QUERIES), "--backend", "par",
+           "--threads", str(cores), "--repeat", str(args.steps), "--warmup", str(args.warmup)]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+    lines = [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+    per_q = {d["query"]: d for d in lines}
+    L = lines[0]["lineitem_rows"]
+    step_ms = [sum(per_q[q]["times_ms"][i] for q in QUERIES) for i in range(args.steps)]
+    ms = statistics.median(step_ms)
+    value = len(QUERIES) * L / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
+        "config": {"workload": f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf} (reference timed on an SF{sample_sf} sample)",
+                   "sf": args.sf, "sample_sf": sample_sf, "queries": list(QUERIES), "lineitem_rows": L},
+        "queries": {q: {"latency_ms": per_q[q]["median_ms"], "rows_per_s": L / (per_q[q]["median_ms"] / 1e3)}
+                    for q in QUERIES},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "reference",
+                         "sample": f"tensql Executor(par, {cores} threads) on SF{sample_sf} ({L} lineitem rows), "
+                                   f"median of {args.steps} after {args.warmup} warmups"},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline_sample(sf: float):
+    """Bounded sample of the reference CPU path for the b200 arm's line."""
+    cores = os.cpu_count() or 1
+    if not REF_RUNNER.exists():
+        return None
+    cmd = [str(REF_RUNNER), "run", "--sf", str(sf), "--queries", ",".join(QUERIES), "--backend", "par",
+           "--threads", str(cores), "--repeat", "3", "--warmup", "1"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, check=True, timeout=600).stdout
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "rows/s", "cores": cores, "kind": "reference", "sample": f"failed: {e}"}
+    lines = [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+    L = lines[0]["lineitem_rows"]
+    ms = sum(d["median_ms"] for d in lines)
+    return {"value": len(QUERIES) * L / (ms / 1e3), "unit": "rows/s", "cores": cores, "kind": "reference",
+            "sample": f"tensql Executor(par, {cores} threads), Q1+Q6+Q14+Q3 on SF{sf} ({L} lineitem rows), "
+                      f"median of 3 after 1 warmup",
+            "queries_ms": {d["query"]: d["median_ms"] for d in lines}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sf", type=float, default=10.0)
+    ap.add_argument("--ref-sf", type=float, default=1.0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2209_04579_b200 import tqp
+    ctx = tqp.Context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local_rank))
+    seed = 7
+    tables = {n: tqp.Table.generate(n, args.sf, seed, shard=rank, nshards=world, ctx=ctx)
+              for n in ("lineitem", "orders", "customer", "part")}
+    L, O, P, Cn = (tables[n].rows for n in ("lineitem", "orders", "part", "customer"))
+    execs = {}
+    for q in QUERIES:
+        plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
+        execs[q] = tqp.Executor(plan, fuse=not args.no_fuse, ctx=ctx)
+        execs[q].set_timing(True)
+
+    def step(timing=None):
+        for q in QUERIES:
+            if timing is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            execs[q].execute(tables)
+            if timing is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                timing[q].append((e0, e1))
+
+    for _ in range(args.warmup):
+        step()
+    for ex in execs.values():
+        ex.reset_timings()
+    ctx.sync()
+
+    per_q = {q: [] for q in QUERIES}
+    launches0 = ctx.launches
+    with ClockSampler(local_rank) as clocks:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ctx.sync()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            step(per_q)
+        end.record(stream)
+        end.synchronize()
+        ctx.sync()
+        torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    total_ms = start.elapsed_time(end)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    q_ms = {q: statistics.median([a.elapsed_time(b) for a, b in per_q[q]]) for q in QUERIES}
+
+    # roofline of the dominant unit (largest device time over the timed region)
+    peak_gbs, peak_kind = measured_peaks()
+    units = []
+    for q in QUERIES:
+        for name, t in execs[q].timings().items():
+            units.append((t["total_ms"], q, name, t["calls"]))
+    units.sort(reverse=True)
+    dom_ms, dom_q, dom_name, dom_calls = units[0]
+    dom_avg_ms = dom_ms / max(1, dom_calls)
+    dom_bytes = algorithmic_bytes(dom_q, L, P, O, Cn)
+    achieved = dom_bytes / (dom_avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                "frac": achieved / peak_gbs, "traffic": None, "kernel": f"{dom_q}:{dom_name}",
+                "peak_kind": peak_kind, "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_avg_ms}
+
+    rows_total = len(QUERIES) * L * world
+    value = rows_total / (ms_per_step / 1e3)
+    queries = {}
+    for q in QUERIES:
+        b = algorithmic_bytes(q, L, P, O, Cn)
+        queries[q] = {"latency_ms": q_ms[q], "rows_per_s": L * world / (q_ms[q] / 1e3),
+                      "algorithmic_bytes": b, "hbm_frac": b / (q_ms[q] / 1e3) / 1e9 / peak_gbs,
+                      "units": execs[q].timings(), "explain": execs[q].explain()}
+
+    # e2e: host (pinned) columns -> device -> four queries -> result to host
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, tqp, torch, ctx, stream, tables, execs, L, world, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.ref_sf)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (counter-based TPC-H generator, seed 7)",
+            "config": {"workload": f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf:g} per GPU, device-resident columns",
+                       "sf": args.sf, "queries": list(QUERIES), "lineitem_rows_per_gpu": L,
+                       "fused": not args.no_fuse,
+                       "l2": "inputs larger than L2 (1.9-2.5 GB per query vs 126 MB)",
+                       "parallelism": f"row-sharded lineitem x{world}"},
+            "queries": queries, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, tqp, torch, ctx, stream, tables, execs, L, world, dist):
+    """Same suite through the public C ABI with HOST inputs: every step
+    uploads the columns from pinned host memory, runs the queries and reads
+    the results back; all inside the timed region."""
+    host = {}
+    h2d = 0
+    for name, t in tables.items():
+        cols = []
+        for cname, lt in t.columns():
+            dev = t.column(cname)
+            arr = dev.numpy(widen_strings=False)
+            pin = torch.from_numpy(arr).pin_memory()
+            cols.append((cname, lt, dev.dtype, pin))
+            h2d += pin.numel() * pin.element_size()
+        host[name] = cols
+
+    def upload():
+        out = {}
+        for name, cols in host.items():
+            tab = tqp.Table.create(ctx)
+            for cname, lt, dt, pin in cols:
+                st = tqp.Status()
+                h = tqp.lib.tqp_tensor_from_host(ctx.h, dt, pin.shape[0], pin.shape[1], pin.data_ptr(),
+                                                 tqp.C.byref(st))
+                tqp._check(st, bool(h))
+                tab.add_column(cname, lt, tqp.Tensor(h, ctx))
+            out[name] = tab
+        return out
+
+    def step():
+        d2h = 0
+        tabs = upload()
+        for q in QUERIES:
+            res = execs[q].execute(tabs)
+            for _, _, arr in res.to_numpy():
+                d2h += arr.nbytes
+        return d2h
+
+    for _ in range(2):
+        step()
+    if dist:
+        dist.barrier()
+    ctx.sync()
+    t0 = time.perf_counter()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    steps = max(2, args.steps // 2)
+    d2h = 0
+    for _ in range(steps):
+        d2h = step()
+    end.record(stream)
+    end.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    ms = max(start.elapsed_time(end), wall_ms) / steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": len(QUERIES) * L * world / (ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
+            "path": "pinned host columns -> tqp_tensor_from_host (C ABI) -> tqp_executor_execute x4 -> results to host"}
+
+
+if __name__ == "__main__":
+    main()

@@ -204,6 +204,9 @@ int tqp_plan_add_output(tqp_plan* p, const char* name, int logical_type, int slo
 int tqp_plan_add_input_column(tqp_plan* p, const char* table, const char* column,
                               int logical_type, tqp_status* st);
 void tqp_plan_free(tqp_plan* p);
+/* Fused pipelines the executor would choose for this plan (JSON; needs no
+ * device; the string is owned by the library, valid until the next call). */
+const char* tqp_plan_fusion_explain(const tqp_plan* p);
 
 /* ---- executor (tensql::Executor, executor.hpp:43-59) --------------------- */
 #define TQP_EXEC_FUSE 1u      /* pattern-match steps into fused pipelines */
@@ -221,6 +224,12 @@ tqp_result* tqp_executor_execute(tqp_executor* ex, const char* const* names,
 tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names,
                                  tqp_table* const* tables, int ntables, char** trace_json,
                                  tqp_status* st);
+/* Per-unit device time (CUDA events on the context stream, no host sync
+ * until read): unit = fused pipeline name or "step:<kind>". JSON owned by
+ * the library, valid until the next call on this thread. */
+void tqp_executor_set_timing(tqp_executor* ex, int on);
+const char* tqp_executor_timings(tqp_executor* ex);
+void tqp_executor_reset_timings(tqp_executor* ex);
 /* Description of the fused pipelines chosen for this plan (JSON). */
 const char* tqp_executor_explain(tqp_executor* ex);
 void tqp_executor_free(tqp_executor* ex);

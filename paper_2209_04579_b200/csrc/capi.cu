@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "executor.hpp"
@@ -446,4 +447,43 @@ extern "C" tqp_table* tqp_gen_table(tqp_ctx* ctx, const char* table, double sf, 
     }
     return t;
   });
+}
+
+extern "C" void tqp_executor_set_timing(tqp_executor* ex, int on) {
+  if (ex) ex->ex->set_timing(on != 0);
+}
+
+extern "C" const char* tqp_executor_timings(tqp_executor* ex) {
+  static thread_local std::string s;
+  try {
+    s = ex ? ex->ex->timings_json() : "{}";
+  } catch (const std::exception& e) {
+    s = "{}";
+  }
+  return s.c_str();
+}
+
+extern "C" void tqp_executor_reset_timings(tqp_executor* ex) {
+  if (ex) ex->ex->reset_timings();
+}
+
+// Fusion decisions for a plan without a device (the planner is host code).
+extern "C" const char* tqp_plan_fusion_explain(const tqp_plan* p) {
+  static thread_local std::string s;
+  try {
+    tqp::Ctx dummy;
+    auto units = tqp::plan_fusion(dummy, p->p);
+    std::ostringstream os;
+    os << "{\"fused\": [";
+    for (size_t i = 0; i < units.size(); ++i) {
+      const auto& u = units[i];
+      os << (i ? ", " : "") << "{\"name\": \"" << u.name << "\", \"steps\": [\"" << p->p.steps[u.first_step].id << "\", \""
+         << p->p.steps[u.last_step].id << "\"], \"detail\": \"" << u.explain << "\"}";
+    }
+    os << "]}";
+    s = os.str();
+  } catch (const std::exception& e) {
+    s = std::string("{\"error\": \"") + e.what() + "\"}";
+  }
+  return s.c_str();
 }

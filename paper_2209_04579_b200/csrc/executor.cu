@@ -256,6 +256,55 @@ void Executor::release_after(int s, std::vector<std::optional<Tensor>>& slots) {
     if (slots[x] && last_use_[x] <= last) slots[x].reset();
 }
 
+void Executor::time_begin(cudaEvent_t* ev) {
+  *ev = nullptr;
+  if (!timing_) return;
+  TQP_CUDA(cudaEventCreate(ev));
+  TQP_CUDA(cudaEventRecord(*ev, ctx_.stream));
+}
+
+void Executor::time_end(const std::string& name, cudaEvent_t start) {
+  if (!start) return;
+  cudaEvent_t stop;
+  TQP_CUDA(cudaEventCreate(&stop));
+  TQP_CUDA(cudaEventRecord(stop, ctx_.stream));
+  timings_[name].pending.push_back({start, stop});
+}
+
+void Executor::drain_timings() {
+  for (auto& [name, t] : timings_) {
+    for (auto& [a, b] : t.pending) {
+      TQP_CUDA(cudaEventSynchronize(b));
+      float ms = 0.f;
+      TQP_CUDA(cudaEventElapsedTime(&ms, a, b));
+      t.total_ms += ms;
+      t.calls += 1;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    t.pending.clear();
+  }
+}
+
+std::string Executor::timings_json() {
+  drain_timings();
+  std::ostringstream os;
+  os << "{";
+  bool first = true;
+  for (const auto& [name, t] : timings_) {
+    os << (first ? "" : ", ") << "\"" << json_escape(name) << "\": {\"calls\": " << t.calls
+       << ", \"total_ms\": " << t.total_ms << "}";
+    first = false;
+  }
+  os << "}";
+  return os.str();
+}
+
+void Executor::reset_timings() {
+  drain_timings();
+  timings_.clear();
+}
+
 Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
   // bind and type-check the input tables (executor.cpp:355-371)
   for (const auto& it : plan_.input_tables) {
@@ -277,7 +326,11 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
     if (u < units_.size() && units_[u].first_step == s) {
       const FusedUnit& unit = units_[u++];
       int64_t t0 = now_ns();
+      cudaEvent_t ev;
+      time_begin(&ev);
       bool ok = unit.run(ctx_, slots, tables);
+      if (ok) time_end(unit.name, ev);
+      else if (ev) cudaEventDestroy(ev);
       if (ok) {
         if (trace) {
           ctx_.sync();
@@ -300,7 +353,10 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
       s = unit.last_step + 1;
       continue;
     }
+    cudaEvent_t ev;
+    time_begin(&ev);
     run_step(s, slots, tables, trace, run_start);
+    time_end("step:" + plan_.steps[s].kind, ev);
     ++s;
   }
   Result res;

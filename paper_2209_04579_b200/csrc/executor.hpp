@@ -114,7 +114,24 @@ class Executor {
   const Plan& plan() const { return plan_; }
   std::string explain() const;
 
+  // Device-time accounting per unit (fused pipeline or generic step) with
+  // CUDA events on the context stream; no host synchronisation until read.
+  void set_timing(bool on) { timing_ = on; }
+  std::string timings_json();
+  void reset_timings();
+
  private:
+  struct UnitTiming {
+    int64_t calls = 0;
+    double total_ms = 0.0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  };
+  void time_begin(cudaEvent_t* ev);
+  void time_end(const std::string& name, cudaEvent_t start);
+  void drain_timings();
+  bool timing_ = false;
+  std::map<std::string, UnitTiming> timings_;
+
   Tensor exec_instr(const Instr& in, std::vector<std::optional<Tensor>>& slots, const TableSet& tables);
   void run_step(int s, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, ProfileTrace* trace,
                 int64_t run_start);

@@ -1,6 +1,1653 @@
-// Fused pipelines (filled in below).
+// Fusion planner: recognises the reference's lowering recipes
+// (operator_plan.cpp: lower_filter :227-237, lower_join :249-294,
+// lower_aggregate :309-388, lower_sort :390-404, lower_limit :406-414) in a
+// lowered OperatorPlan, rebuilds the relational pipeline they came from, and
+// replaces [scan -> filter -> join(unique build) -> aggregate -> sort/limit]
+// runs of steps with fused device pipelines (fused_kernels.cuh). Anything
+// outside that contract stays on the per-instruction device path, and a
+// fused unit whose data preconditions fail at run time (duplicate build keys,
+// > 64 groups, fixed-point range, int64 near overflow) hands its steps back
+// to the per-instruction path, which reproduces the reference exactly.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <set>
+#include <sstream>
+
 #include "executor.hpp"
+#include "fused_kernels.cuh"
 
 namespace tqp {
-std::vector<FusedUnit> plan_fusion(Ctx&, const Plan&) { return {}; }
+namespace {
+
+using namespace fz;
+
+// ---- symbolic expressions ----------------------------------------------------
+struct SExpr {
+  enum K { COL, CONST, CMP, ARITH, LOGIC, NOT, LIKE, STRCMP, SELECT, CAST, BAD } k = BAD;
+  int slot = -1;       // COL
+  int op = 0;          // CMP/ARITH/LOGIC op, LIKE anchor, CAST target
+  std::string pattern; // LIKE
+  int a = -1, b = -1, c = -1;
+  const Instr* cinstr = nullptr;  // CONST
+};
+
+struct AggOut {
+  int fn;  // 0 sum 1 count 2 avg 3 min 4 max
+  int expr = -1;
+  int slot = -1;
+};
+
+struct Rel {
+  enum Kind { SCAN, FILTER, JOIN, AGG, PROJECT, SORT, LIMIT, OTHER } kind = OTHER;
+  int step = -1;
+  std::vector<int> cols;
+  int input = -1;  // rel (step index)
+  int left = -1, right = -1, lk = -1, rk = -1;
+  int pred = -1;
+  std::vector<int> keys;  // AGG: input-relation slots
+  std::vector<AggOut> aggs;
+  std::vector<std::pair<int, bool>> sort_keys;  // SORT: input slots, priority order
+  int64_t limit = -1;
+  std::map<int, int> out_of_in;  // FILTER/SORT/LIMIT/JOIN: output slot -> input slot
+};
+
+struct ColSrc {
+  int scan = -1;  // step index of the SCAN
+  std::string table, column;
+};
+
+struct Analysis {
+  const Plan& plan;
+  std::vector<SExpr> ex;
+  std::vector<Rel> rels;
+  std::map<int, int> def_step;          // slot -> producing step
+  std::map<int, const Instr*> def;      // slot -> producing instr
+  std::map<int, int> rel_of;            // relation column slot -> step
+  std::map<int, ColSrc> src;            // relation column slot -> base column
+
+  explicit Analysis(const Plan& p) : plan(p) {}
+
+  int add(SExpr e) {
+    ex.push_back(std::move(e));
+    return static_cast<int>(ex.size()) - 1;
+  }
+
+  // expression for `slot` inside step s; leaves resolve through `leaf`
+  int build(int slot, int s, const std::function<int(int)>& leaf) {
+    auto it = def.find(slot);
+    if (it == def.end() || def_step[slot] != s) return leaf(slot);
+    const Instr& in = *it->second;
+    SExpr e;
+    switch (in.op) {
+      case Op::ConstTensor: e.k = SExpr::CONST; e.cinstr = &in; return add(e);
+      case Op::Compare: e.k = SExpr::CMP; e.op = in.cmp; break;
+      case Op::StringCompare: e.k = SExpr::STRCMP; e.op = in.cmp; break;
+      case Op::Arith: e.k = SExpr::ARITH; e.op = in.arith; break;
+      case Op::Logical: e.k = SExpr::LOGIC; e.op = in.logic; break;
+      case Op::Not: e.k = SExpr::NOT; break;
+      case Op::SubstringMatch: e.k = SExpr::LIKE; e.op = in.anchor; e.pattern = in.pattern; break;
+      case Op::SelectWhere: e.k = SExpr::SELECT; break;
+      case Op::Cast: e.k = SExpr::CAST; e.op = in.cast_to; break;
+      case Op::BroadcastScalar: return build(in.inputs[0], s, leaf);
+      case Op::Gather: return leaf(slot);  // sorted/filtered view of an input column
+      default: return -1;
+    }
+    int kids[3] = {-1, -1, -1};
+    for (size_t i = 0; i < in.inputs.size() && i < 3; ++i) {
+      kids[i] = build(in.inputs[i], s, leaf);
+      if (kids[i] < 0) return -1;
+    }
+    e.a = kids[0];
+    e.b = kids[1];
+    e.c = kids[2];
+    return add(e);
+  }
+
+  int col_leaf(int slot) {
+    SExpr e;
+    e.k = SExpr::COL;
+    e.slot = slot;
+    return add(e);
+  }
+
+  bool analyse() {
+    for (size_t s = 0; s < plan.steps.size(); ++s)
+      for (const auto& in : plan.steps[s].instrs) {
+        def[in.output] = &in;
+        def_step[in.output] = static_cast<int>(s);
+      }
+    rels.resize(plan.steps.size());
+    for (size_t s = 0; s < plan.steps.size(); ++s) {
+      Rel& r = rels[s];
+      r.step = static_cast<int>(s);
+      r.cols = plan.steps[s].output_slots;
+      const std::string& kind = plan.steps[s].kind;
+      bool ok = false;
+      if (kind == "scan") ok = an_scan(r);
+      else if (kind == "filter") ok = an_filter(r);
+      else if (kind == "join") ok = an_join(r);
+      else if (kind == "aggregate") ok = an_agg(r);
+      else if (kind == "project") ok = an_project(r);
+      else if (kind == "sort") ok = an_sort(r);
+      else if (kind == "limit") ok = an_limit(r);
+      if (!ok) {
+        r.kind = Rel::OTHER;
+        if (std::getenv("TQP_FUSION_DEBUG")) std::fprintf(stderr, "[tqp] step %s not recognised\n", plan.steps[s].id.c_str());
+      }
+      for (int c : r.cols) rel_of[c] = static_cast<int>(s);
+    }
+    return true;
+  }
+
+  const std::vector<Instr>& ins(const Rel& r) { return plan.steps[r.step].instrs; }
+
+  bool an_scan(Rel& r) {
+    for (const auto& in : ins(r)) {
+      if (in.op != Op::LoadColumn) return false;
+      src[in.output] = {r.step, in.table, in.column};
+    }
+    r.kind = Rel::SCAN;
+    return true;
+  }
+
+  // input relation that owns every slot in `slots` (same step), or -1
+  int owner(const std::vector<int>& slots) {
+    int o = -1;
+    for (int x : slots) {
+      auto it = rel_of.find(x);
+      if (it == rel_of.end()) return -1;
+      if (o >= 0 && it->second != o) return -1;
+      o = it->second;
+    }
+    return o;
+  }
+
+  bool an_filter(Rel& r) {
+    const auto& v = ins(r);
+    const Instr* compact = nullptr;
+    for (const auto& in : v)
+      if (in.op == Op::Compact) compact = &in;
+    if (!compact) return false;
+    const Instr* io = def.count(compact->inputs[0]) ? def[compact->inputs[0]] : nullptr;
+    if (!io || io->op != Op::IotaRows || io->param >= 0) return false;
+    std::vector<int> in_cols;
+    for (const auto& in : v) {
+      if (in.op == Op::Gather && in.inputs[1] == compact->output) {
+        in_cols.push_back(in.inputs[0]);
+        r.out_of_in[in.output] = in.inputs[0];
+      }
+    }
+    r.input = owner(in_cols);
+    if (r.input < 0 || rels[r.input].cols != in_cols) return false;
+    if (r.cols.size() != in_cols.size()) return false;
+    for (size_t i = 0; i < r.cols.size(); ++i) {
+      if (r.out_of_in[r.cols[i]] != in_cols[i]) return false;
+      if (src.count(in_cols[i])) src[r.cols[i]] = src[in_cols[i]];
+    }
+    r.pred = build(compact->inputs[1], r.step, [&](int x) { return col_leaf(x); });
+    if (r.pred < 0) return false;
+    r.kind = Rel::FILTER;
+    return true;
+  }
+
+  bool an_join(Rel& r) {
+    const auto& v = ins(r);
+    static const Op recipe[] = {Op::ArgsortStable, Op::Gather, Op::SearchSorted, Op::SearchSorted, Op::Arith,
+                                Op::PrefixSum, Op::ConstTensor, Op::Arith, Op::SegmentedReduce, Op::IotaLen,
+                                Op::ConstTensor, Op::SearchSorted, Op::Arith, Op::ExpandSegments, Op::Gather};
+    const size_t nr = sizeof(recipe) / sizeof(recipe[0]);
+    if (v.size() < nr) return false;
+    for (size_t i = 0; i < nr; ++i)
+      if (v[i].op != recipe[i]) return false;
+    r.rk = v[0].inputs[0];
+    r.lk = v[2].inputs[1];
+    int left_ids = v[12].output, right_ids = v[14].output;
+    std::vector<int> lc, rc;
+    for (size_t i = nr; i < v.size(); ++i) {
+      if (v[i].op != Op::Gather) return false;
+      if (v[i].inputs[1] == left_ids) lc.push_back(v[i].inputs[0]);
+      else if (v[i].inputs[1] == right_ids) rc.push_back(v[i].inputs[0]);
+      else return false;
+      r.out_of_in[v[i].output] = v[i].inputs[0];
+      if (src.count(v[i].inputs[0])) src[v[i].output] = src[v[i].inputs[0]];
+    }
+    r.left = owner(lc);
+    r.right = owner(rc);
+    if (r.left < 0 || r.right < 0 || rels[r.left].cols != lc || rels[r.right].cols != rc) return false;
+    if (rel_of[r.lk] != r.left || rel_of[r.rk] != r.right) return false;
+    r.kind = Rel::JOIN;
+    return true;
+  }
+
+  bool an_agg(Rel& r) {
+    const auto& v = ins(r);
+    bool keyed = false;
+    for (const auto& in : v) keyed |= in.op == Op::SortPermRows;
+    std::map<int, int> sorted_to_in;  // keyed: sorted slot -> input slot
+    int perm = -1;
+    if (keyed) {
+      // iota, sort_perm_rows (keys last->first), gathers by perm
+      size_t i = 0;
+      if (v.empty() || v[0].op != Op::IotaRows) return false;
+      ++i;
+      std::vector<int> rev_keys;
+      while (i < v.size() && v[i].op == Op::SortPermRows) {
+        if (v[i].param != 1) return false;
+        rev_keys.push_back(v[i].inputs[0]);
+        perm = v[i].output;
+        ++i;
+      }
+      r.keys.assign(rev_keys.rbegin(), rev_keys.rend());
+      std::vector<int> in_cols;
+      for (; i < v.size() && v[i].op == Op::Gather && v[i].inputs[1] == perm; ++i) {
+        sorted_to_in[v[i].output] = v[i].inputs[0];
+        in_cols.push_back(v[i].inputs[0]);
+      }
+      r.input = owner(in_cols);
+      if (r.input < 0 || rels[r.input].cols != in_cols) return false;
+    } else {
+      if (v.size() < 3 || v[0].op != Op::ConstTensor || v[1].op != Op::IotaRows || v[2].op != Op::Arith) return false;
+      r.input = rel_of.count(v[1].inputs[0]) ? rel_of[v[1].inputs[0]] : -1;
+      if (r.input < 0) return false;
+    }
+    auto leaf = [&](int x) {
+      if (keyed) {
+        auto it = sorted_to_in.find(x);
+        if (it == sorted_to_in.end()) return -1;
+        x = it->second;
+      }
+      if (!rel_of.count(x) || rel_of[x] != r.input) return -1;
+      return col_leaf(x);
+    };
+    const size_t nk = r.keys.size();
+    if (r.cols.size() < nk) return false;
+    for (size_t k = 0; k < nk; ++k) {
+      // key output k = gather(sorted key col, first_idx)
+      const Instr* g = def.count(r.cols[k]) ? def[r.cols[k]] : nullptr;
+      if (!g || g->op != Op::Gather || sorted_to_in[g->inputs[0]] != r.keys[k]) return false;
+    }
+    for (size_t j = nk; j < r.cols.size(); ++j) {
+      int out = r.cols[j];
+      const Instr* d = def.count(out) ? def[out] : nullptr;
+      if (!d) return false;
+      AggOut a;
+      a.slot = out;
+      auto segred_sum_expr = [&](const Instr* sr) -> int {
+        if (!sr || sr->op != Op::SegmentedReduce || sr->reduce != TQP_SUM) return -1;
+        return build(sr->inputs[0], r.step, leaf);
+      };
+      if (d->op == Op::SegmentedReduce) {
+        if (d->reduce == TQP_COUNT) {
+          a.fn = 1;
+        } else {
+          a.fn = d->reduce == TQP_SUM ? 0 : d->reduce == TQP_MIN ? 3 : 4;
+          a.expr = build(d->inputs[0], r.step, leaf);
+          if (a.expr < 0) return false;
+        }
+      } else if (d->op == Op::Arith && d->arith == TQP_DIV) {
+        const Instr* x = def.count(d->inputs[0]) ? def[d->inputs[0]] : nullptr;
+        if (x && x->op == Op::Cast) x = def.count(x->inputs[0]) ? def[x->inputs[0]] : nullptr;
+        a.fn = 2;
+        a.expr = segred_sum_expr(x);
+        if (a.expr < 0) return false;
+      } else {
+        return false;
+      }
+      r.aggs.push_back(a);
+    }
+    r.kind = Rel::AGG;
+    return true;
+  }
+
+  bool an_project(Rel& r) {
+    if (!ins(r).empty()) return false;
+    int o = -1;
+    for (int c : r.cols) {
+      if (!rel_of.count(c)) return false;
+      if (o >= 0 && rel_of[c] != o) return false;
+      o = rel_of[c];
+    }
+    r.input = o;
+    r.kind = Rel::PROJECT;
+    return o >= 0;
+  }
+
+  bool an_sort(Rel& r) {
+    const auto& v = ins(r);
+    if (v.empty() || v[0].op != Op::IotaRows || v[0].param >= 0) return false;
+    size_t i = 1;
+    int perm = v[0].output;
+    std::vector<std::pair<int, bool>> rev;
+    for (; i < v.size() && v[i].op == Op::SortPermRows; ++i) {
+      if (v[i].inputs[1] != perm) return false;
+      rev.push_back({v[i].inputs[0], v[i].param == 1});
+      perm = v[i].output;
+    }
+    r.sort_keys.assign(rev.rbegin(), rev.rend());
+    std::vector<int> in_cols;
+    for (; i < v.size(); ++i) {
+      if (v[i].op != Op::Gather || v[i].inputs[1] != perm) return false;
+      in_cols.push_back(v[i].inputs[0]);
+      r.out_of_in[v[i].output] = v[i].inputs[0];
+    }
+    r.input = step_of_cols(in_cols);
+    if (r.input < 0) return false;
+    r.kind = Rel::SORT;
+    return true;
+  }
+
+  bool an_limit(Rel& r) {
+    const auto& v = ins(r);
+    if (v.empty() || v[0].op != Op::IotaRows) return false;
+    r.limit = v[0].param;
+    std::vector<int> in_cols;
+    for (size_t i = 1; i < v.size(); ++i) {
+      if (v[i].op != Op::Gather || v[i].inputs[1] != v[0].output) return false;
+      in_cols.push_back(v[i].inputs[0]);
+      r.out_of_in[v[i].output] = v[i].inputs[0];
+    }
+    r.input = step_of_cols(in_cols);
+    if (r.input < 0) return false;
+    r.kind = Rel::LIMIT;
+    return true;
+  }
+
+  // relation (step) whose output columns are exactly `cols`
+  int step_of_cols(const std::vector<int>& cols) {
+    for (int s = static_cast<int>(rels.size()) - 1; s >= 0; --s)
+      if (rels[s].cols == cols && rels[s].step >= 0) return s;
+    return -1;
+  }
+};
+
+// ---- pipeline description -----------------------------------------------------
+struct TermDesc {  // conjunct over a base table column
+  std::string column;
+  int kind;        // 0 numeric compare, 1 string compare, 2 like, 3 const true, 4 const false
+  int op = 0;
+  bool f64 = false;
+  long long ik = 0;
+  double fk = 0.0;
+  std::string lit;  // string compare / like pattern
+  int anchor = 0;
+};
+
+struct BuildDesc {
+  int scan = -1;  // root scan step
+  std::string table, key_column;
+  std::vector<TermDesc> terms;
+  struct Child {
+    std::string fact_column;  // column of this root
+    int build = -1;           // index into builds
+  };
+  std::vector<Child> children;
+  std::vector<TermDesc> flags;  // string predicates evaluated per root row
+  bool assign_groups = false;
+};
+
+struct OperandDesc {
+  int probe = -1;  // -1 fact
+  std::string column;
+};
+
+struct FactorDesc {
+  OperandDesc x;
+  int kind = FK_X;
+  double k = 0.0;
+};
+
+struct AccDesc {
+  bool is_int = false;
+  std::vector<FactorDesc> f;
+  int gate_probe = -1, gate_bit = 0;
+  double gate_else = 0.0;
+  std::string sig() const {
+    std::ostringstream os;
+    os << is_int << "|" << gate_probe << "," << gate_bit << "," << gate_else << "|";
+    for (auto& x : f) os << x.x.probe << ":" << x.x.column << ":" << x.kind << ":" << x.k << ";";
+    return os.str();
+  }
+};
+
+struct OutDesc {  // aggregate outputs, in the AGG step's output order
+  int fn;         // 0 sum 1 count 2 avg, 10 + i: group key i
+  int acc = -1;
+  int slot = -1;
+  bool is_int = false;
+};
+
+struct PipeDesc {
+  int first_step = 0, last_step = 0;
+  int fact_scan = -1;
+  std::string fact_table;
+  std::vector<TermDesc> terms;
+  struct ProbeD {
+    std::string fact_column;
+    int build = -1;
+  };
+  std::vector<ProbeD> probes;
+  std::vector<BuildDesc> builds;
+  std::vector<AccDesc> accs;
+  std::vector<OutDesc> outs;  // AGG outputs
+  int mode = MODE_SCALAR;
+  std::vector<std::string> key_columns;     // MODE_SMALL fact key columns
+  std::vector<int> key_width;               // 1-byte strings
+  // MODE_BUILDGRP: keys resolved to root columns of probes[group_probe]
+  int group_probe = -1;
+  std::vector<std::string> group_key_root_columns;
+  // fused sort + limit (MODE_BUILDGRP)
+  bool topk = false;
+  int64_t k = 0;
+  std::vector<std::pair<int, bool>> sort_outs;  // (index into outs, asc)
+  std::vector<int> final_cols;                  // unit output slots -> outs index
+  std::vector<int> final_slots;
+  std::string explain;
+};
+
+// flatten AND conjuncts
+void conjuncts(Analysis& A, int e, std::vector<int>& out) {
+  const SExpr& x = A.ex[e];
+  if (x.k == SExpr::LOGIC && x.op == TQP_AND) {
+    conjuncts(A, x.a, out);
+    conjuncts(A, x.b, out);
+  } else {
+    out.push_back(e);
+  }
+}
+
+const ColSrc* col_src(Analysis& A, int slot) {
+  auto it = A.src.find(slot);
+  return it == A.src.end() ? nullptr : &it->second;
+}
+
+std::string const_string(const Instr* c) {
+  if (!c || c->const_dtype != TQP_I32 || c->const_rows != 1) return {};
+  std::string s;
+  const int32_t* d = reinterpret_cast<const int32_t*>(c->const_host.data());
+  for (int64_t j = 0; j < c->const_cols && d[j] != 0; ++j) s.push_back(static_cast<char>(d[j]));
+  return s;
+}
+
+bool const_scalar(const Instr* c, bool* is_f64, long long* ik, double* fk, bool* is_bool = nullptr) {
+  if (!c || c->const_rows != 1 || c->const_cols != 1) return false;
+  if (is_bool) *is_bool = c->const_dtype == TQP_BOOL;
+  if (c->const_dtype == TQP_F64) {
+    *is_f64 = true;
+    std::memcpy(fk, c->const_host.data(), 8);
+    return true;
+  }
+  if (c->const_dtype == TQP_I64) {
+    *is_f64 = false;
+    std::memcpy(ik, c->const_host.data(), 8);
+    return true;
+  }
+  if (c->const_dtype == TQP_BOOL) {
+    *is_f64 = false;
+    *ik = c->const_host[0];
+    return true;
+  }
+  return false;
+}
+
+int flip(int op) {
+  switch (op) {
+    case TQP_LT: return TQP_GT;
+    case TQP_LE: return TQP_GE;
+    case TQP_GT: return TQP_LT;
+    case TQP_GE: return TQP_LE;
+    default: return op;
+  }
+}
+
+// conjunct over columns of scan `scan` -> TermDesc
+bool term_of(Analysis& A, int e, int scan, const Plan& plan, TermDesc& t) {
+  const SExpr& x = A.ex[e];
+  auto col_of = [&](int ei, std::string& name) {
+    const SExpr& c = A.ex[ei];
+    if (c.k != SExpr::COL) return false;
+    const ColSrc* s = col_src(A, c.slot);
+    if (!s || s->scan != scan) return false;
+    name = s->column;
+    return true;
+  };
+  if (x.k == SExpr::CONST) {
+    bool f, b;
+    long long ik;
+    double fk;
+    if (!const_scalar(x.cinstr, &f, &ik, &fk, &b) || !b) return false;
+    t.kind = ik ? 3 : 4;
+    return true;
+  }
+  if (x.k == SExpr::CMP) {
+    bool f;
+    long long ik = 0;
+    double fk = 0;
+    if (col_of(x.a, t.column) && A.ex[x.b].k == SExpr::CONST && const_scalar(A.ex[x.b].cinstr, &f, &ik, &fk)) {
+      t.op = x.op;
+    } else if (col_of(x.b, t.column) && A.ex[x.a].k == SExpr::CONST && const_scalar(A.ex[x.a].cinstr, &f, &ik, &fk)) {
+      t.op = flip(x.op);
+    } else {
+      return false;
+    }
+    if (A.ex[x.b].k == SExpr::CONST && A.ex[x.b].cinstr->const_dtype == TQP_BOOL) return false;
+    t.kind = 0;
+    t.f64 = f;
+    t.ik = ik;
+    t.fk = fk;
+    return true;
+  }
+  if (x.k == SExpr::STRCMP) {
+    if (!col_of(x.a, t.column) || A.ex[x.b].k != SExpr::CONST) return false;
+    t.lit = const_string(A.ex[x.b].cinstr);
+    if (t.lit.size() > 48) return false;
+    t.kind = 1;
+    t.op = x.op;
+    return true;
+  }
+  if (x.k == SExpr::LIKE) {
+    if (!col_of(x.a, t.column) || x.pattern.size() > 48) return false;
+    t.kind = 2;
+    t.lit = x.pattern;
+    t.anchor = x.op;
+    return true;
+  }
+  (void)plan;
+  return false;
+}
+
+struct Planner {
+  Analysis& A;
+  const Plan& plan;
+  PipeDesc P;
+  std::string why;
+
+  Planner(Analysis& a, const Plan& p) : A(a), plan(p) {}
+
+  bool fail(const std::string& w) {
+    why = w;
+    return false;
+  }
+
+  // root scan of a build subtree; collects filters + nested joins
+  bool parse_build(int rel, int key_slot, int& out_idx) {
+    BuildDesc b;
+    std::vector<int> chain;
+    int r = rel;
+    while (true) {
+      const Rel& R = A.rels[r];
+      if (R.kind == Rel::SCAN) break;
+      if (R.kind == Rel::FILTER) {
+        chain.push_back(r);
+        r = R.input;
+        continue;
+      }
+      if (R.kind == Rel::JOIN) {
+        chain.push_back(r);
+        r = R.left;
+        continue;
+      }
+      return fail("build side is not scan/filter/join");
+    }
+    b.scan = r;
+    b.table = A.plan.steps[r].instrs.empty() ? "" : A.plan.steps[r].instrs[0].table;
+    const ColSrc* ks = col_src(A, key_slot);
+    if (!ks || ks->scan != b.scan) return fail("build key not a root column");
+    b.key_column = ks->column;
+    for (int c : chain) {
+      const Rel& R = A.rels[c];
+      if (R.kind == Rel::FILTER) {
+        std::vector<int> cs;
+        conjuncts(A, R.pred, cs);
+        for (int e : cs) {
+          TermDesc t;
+          if (!term_of(A, e, b.scan, plan, t)) return fail("build filter term unsupported");
+          b.terms.push_back(t);
+        }
+      } else {
+        const ColSrc* ls = col_src(A, R.lk);
+        if (!ls || ls->scan != b.scan) return fail("nested join key not on build root");
+        int child;
+        if (!parse_build(R.right, R.rk, child)) return false;
+        b.children.push_back({ls->column, child});
+      }
+    }
+    P.builds.push_back(b);
+    out_idx = static_cast<int>(P.builds.size()) - 1;
+    return true;
+  }
+
+  // the steps (rels) a build subtree covers
+  void build_steps(int rel, std::set<int>& s) {
+    s.insert(rel);
+    const Rel& R = A.rels[rel];
+    if (R.kind == Rel::FILTER) build_steps(R.input, s);
+    if (R.kind == Rel::JOIN) {
+      build_steps(R.left, s);
+      build_steps(R.right, s);
+    }
+  }
+
+  // operand: column slot of the fact pipeline relation -> fact col or probe root col
+  bool operand(int slot, OperandDesc& o, int* type) {
+    const ColSrc* s = col_src(A, slot);
+    if (!s) return false;
+    int lt = -1;
+    for (const auto& it : plan.input_tables)
+      if (iequals(it.name, s->table))
+        for (const auto& [c, t] : it.schema)
+          if (iequals(c, s->column)) lt = t;
+    if (type) *type = lt;
+    o.column = s->column;
+    if (s->scan == P.fact_scan) {
+      o.probe = -1;
+      return true;
+    }
+    for (size_t p = 0; p < P.probes.size(); ++p) {
+      if (P.builds[P.probes[p].build].scan == s->scan) {
+        o.probe = static_cast<int>(p);
+        return true;
+      }
+    }
+    return false;
+  }
+
+  bool factor_list(int e, std::vector<FactorDesc>& out) {
+    const SExpr& x = A.ex[e];
+    if (x.k == SExpr::ARITH && x.op == TQP_MUL) {
+      // left-deep product: left is a product chain, right is one factor
+      if (!factor_list(x.a, out)) return false;
+      FactorDesc f;
+      if (!one_factor(x.b, f)) return false;
+      out.push_back(f);
+      return true;
+    }
+    FactorDesc f;
+    if (!one_factor(e, f)) return false;
+    out.push_back(f);
+    return true;
+  }
+
+  bool f64_col(int e, OperandDesc& o) {
+    const SExpr& x = A.ex[e];
+    int lt;
+    return x.k == SExpr::COL && operand(x.slot, o, &lt) && lt == TQP_LT_FLOAT64;
+  }
+
+  bool one_factor(int e, FactorDesc& f) {
+    const SExpr& x = A.ex[e];
+    if (f64_col(e, f.x)) {
+      f.kind = FK_X;
+      return true;
+    }
+    if (x.k == SExpr::CONST) {
+      bool isf;
+      long long ik;
+      double fk;
+      if (!const_scalar(x.cinstr, &isf, &ik, &fk) || !isf) return false;
+      f.kind = FK_CONST;
+      f.k = fk;
+      return true;
+    }
+    if (x.k != SExpr::ARITH) return false;
+    bool isf;
+    long long ik;
+    double fk;
+    const SExpr& a = A.ex[x.a];
+    const SExpr& b = A.ex[x.b];
+    if (a.k == SExpr::CONST && f64_col(x.b, f.x) && const_scalar(a.cinstr, &isf, &ik, &fk) && isf) {
+      f.k = fk;
+      switch (x.op) {
+        case TQP_SUB: f.kind = FK_K_MINUS_X; return true;
+        case TQP_ADD: f.kind = FK_K_PLUS_X; return true;
+        case TQP_MUL: f.kind = FK_X_TIMES_K; return true;  // k*x == x*k exactly
+        default: return false;
+      }
+    }
+    if (b.k == SExpr::CONST && f64_col(x.a, f.x) && const_scalar(b.cinstr, &isf, &ik, &fk) && isf) {
+      f.k = fk;
+      switch (x.op) {
+        case TQP_SUB: f.kind = FK_X_MINUS_K; return true;
+        case TQP_ADD: f.kind = FK_X_PLUS_K; return true;
+        case TQP_MUL: f.kind = FK_X_TIMES_K; return true;
+        default: return false;
+      }
+    }
+    return false;
+  }
+
+  // gate: a flag predicate over a probe's root string column
+  bool gate_of(int e, int& probe, int& bit) {
+    const SExpr& x = A.ex[e];
+    if (x.k != SExpr::LIKE && x.k != SExpr::STRCMP) return false;
+    const SExpr& c = A.ex[x.a];
+    if (c.k != SExpr::COL) return false;
+    OperandDesc o;
+    int lt;
+    if (!operand(c.slot, o, &lt) || o.probe < 0 || lt != TQP_LT_UTF8) return false;
+    BuildDesc& b = P.builds[P.probes[o.probe].build];
+    TermDesc t;
+    if (!term_of(A, e, b.scan, plan, t)) return false;
+    if (b.flags.size() >= static_cast<size_t>(kMaxFlags)) return false;
+    probe = o.probe;
+    bit = static_cast<int>(b.flags.size());
+    b.flags.push_back(t);
+    return true;
+  }
+
+  bool acc_of(int e, AccDesc& a) {
+    const SExpr& x = A.ex[e];
+    if (x.k == SExpr::COL) {
+      OperandDesc o;
+      int lt;
+      if (!operand(x.slot, o, &lt)) return false;
+      if (lt == TQP_LT_INT64) {
+        a.is_int = true;
+        a.f.push_back({o, FK_X, 0.0});
+        return true;
+      }
+    }
+    if (x.k == SExpr::SELECT) {
+      const SExpr& el = A.ex[x.c];
+      bool isf;
+      long long ik;
+      double fk;
+      if (el.k != SExpr::CONST || !const_scalar(el.cinstr, &isf, &ik, &fk) || !isf) return false;
+      if (!gate_of(x.a, a.gate_probe, a.gate_bit)) return false;
+      a.gate_else = fk;
+      return factor_list(x.b, a.f) && a.f.size() <= static_cast<size_t>(kMaxFactors);
+    }
+    return factor_list(e, a.f) && a.f.size() <= static_cast<size_t>(kMaxFactors);
+  }
+
+  int acc_index(const AccDesc& a) {
+    for (size_t i = 0; i < P.accs.size(); ++i)
+      if (P.accs[i].sig() == a.sig()) return static_cast<int>(i);
+    P.accs.push_back(a);
+    return static_cast<int>(P.accs.size()) - 1;
+  }
+
+  bool plan_agg(int agg_step) {
+    const Rel& G = A.rels[agg_step];
+    // fact pipeline below the aggregate
+    std::vector<int> chain;
+    int r = G.input;
+    while (true) {
+      const Rel& R = A.rels[r];
+      if (R.kind == Rel::SCAN) break;
+      if (R.kind == Rel::FILTER || R.kind == Rel::JOIN) {
+        chain.push_back(r);
+        r = R.kind == Rel::FILTER ? R.input : R.left;
+        continue;
+      }
+      return fail("aggregate input is not a scan/filter/join pipeline");
+    }
+    P.fact_scan = r;
+    P.fact_table = plan.steps[r].instrs.empty() ? "" : plan.steps[r].instrs[0].table;
+    std::set<int> covered = {r, agg_step};
+    std::reverse(chain.begin(), chain.end());  // bottom-up
+    for (int c : chain) {
+      const Rel& R = A.rels[c];
+      covered.insert(c);
+      if (R.kind == Rel::FILTER) {
+        std::vector<int> cs;
+        conjuncts(A, R.pred, cs);
+        for (int e : cs) {
+          TermDesc t;
+          if (!term_of(A, e, P.fact_scan, plan, t)) return fail("fact filter term unsupported");
+          if (t.kind == 1 || t.kind == 2) return fail("string predicate on fact table");
+          P.terms.push_back(t);
+        }
+      } else {
+        const ColSrc* ls = col_src(A, R.lk);
+        if (!ls || ls->scan != P.fact_scan) return fail("join probe key not on fact table");
+        int b;
+        if (!parse_build(R.right, R.rk, b)) return false;
+        build_steps(R.right, covered);
+        P.probes.push_back({ls->column, b});
+      }
+    }
+    if (static_cast<int>(P.probes.size()) > kMaxProbes || static_cast<int>(P.terms.size()) > kMaxTerms)
+      return fail("too many probes/terms");
+    // group keys
+    if (G.keys.empty()) {
+      P.mode = MODE_SCALAR;
+    } else {
+      bool small = G.keys.size() <= static_cast<size_t>(kMaxKeys);
+      for (int k : G.keys) {
+        OperandDesc o;
+        int lt;
+        if (!operand(k, o, &lt) || o.probe >= 0 || lt != TQP_LT_UTF8) small = false;
+        else P.key_columns.push_back(o.column);
+      }
+      if (small) {
+        P.mode = MODE_SMALL;
+      } else {
+        // group = matched build row of one probe
+        P.key_columns.clear();
+        int gp = -1;
+        for (size_t p = 0; p < P.probes.size() && gp < 0; ++p) {
+          bool ok = true;
+          std::vector<std::string> cols;
+          for (int k : G.keys) {
+            OperandDesc o;
+            int lt;
+            if (!operand(k, o, &lt) || (lt != TQP_LT_INT64 && lt != TQP_LT_DATE)) {
+              ok = false;
+              break;
+            }
+            if (o.probe == static_cast<int>(p)) {
+              cols.push_back(o.column);
+            } else if (o.probe < 0 && iequals(o.column, P.probes[p].fact_column)) {
+              cols.push_back(P.builds[P.probes[p].build].key_column);  // l_orderkey == o_orderkey
+            } else {
+              ok = false;
+              break;
+            }
+          }
+          if (ok) {
+            gp = static_cast<int>(p);
+            P.group_key_root_columns = cols;
+          }
+        }
+        if (gp < 0) return fail("group keys are neither small byte keys nor a build row");
+        P.mode = MODE_BUILDGRP;
+        P.group_probe = gp;
+        P.builds[P.probes[gp].build].assign_groups = true;
+      }
+    }
+    // aggregates
+    for (size_t i = 0; i < G.keys.size(); ++i) P.outs.push_back({10 + static_cast<int>(i), -1, G.cols[i], false});
+    for (const auto& a : G.aggs) {
+      OutDesc o;
+      o.slot = a.slot;
+      if (a.fn == 1) {
+        o.fn = 1;
+        o.is_int = true;
+      } else if (a.fn == 0 || a.fn == 2) {
+        AccDesc ad;
+        if (!acc_of(a.expr, ad)) return fail("aggregate expression outside the fused family");
+        o.fn = a.fn;
+        o.acc = acc_index(ad);
+        o.is_int = a.fn == 0 && ad.is_int;
+      } else {
+        return fail("MIN/MAX aggregate");
+      }
+      P.outs.push_back(o);
+    }
+    if (P.accs.size() > static_cast<size_t>(kMaxAcc)) return fail("too many accumulators");
+    // the unit must cover a contiguous step range
+    P.first_step = *covered.begin();
+    P.last_step = agg_step;
+    for (int s = P.first_step; s <= P.last_step; ++s)
+      if (!covered.count(s)) return fail("pipeline steps are not contiguous");
+    for (int o : G.cols) P.final_slots.push_back(o);
+    for (size_t i = 0; i < P.outs.size(); ++i) P.final_cols.push_back(static_cast<int>(i));
+    // fused sort + limit after the aggregate (through an instruction-free project)
+    int next = agg_step + 1;
+    std::map<int, int> slot_to_out;
+    for (size_t i = 0; i < P.outs.size(); ++i) slot_to_out[P.outs[i].slot] = static_cast<int>(i);
+    if (P.mode == MODE_BUILDGRP && next + 1 < static_cast<int>(A.rels.size())) {
+      int s = next;
+      std::vector<int> proj_cols = G.cols;
+      if (A.rels[s].kind == Rel::PROJECT && A.rels[s].input == agg_step) {
+        proj_cols = A.rels[s].cols;
+        ++s;
+      }
+      if (s + 1 < static_cast<int>(A.rels.size()) && A.rels[s].kind == Rel::SORT && A.rels[s + 1].kind == Rel::LIMIT &&
+          A.rels[s + 1].input == s && A.rels[s + 1].limit >= 0 && A.rels[s + 1].limit <= 64) {
+        const Rel& S = A.rels[s];
+        const Rel& L = A.rels[s + 1];
+        bool ok = S.input >= 0;
+        std::vector<std::pair<int, bool>> keys;
+        for (auto [slot, asc] : S.sort_keys) {
+          if (!slot_to_out.count(slot)) ok = false;
+          else keys.push_back({slot_to_out[slot], asc});
+        }
+        std::vector<int> cols;
+        for (int out : L.cols) {
+          int in_sort = S.out_of_in.count(L.out_of_in.at(out)) ? S.out_of_in.at(L.out_of_in.at(out)) : -1;
+          if (!slot_to_out.count(in_sort)) ok = false;
+          else cols.push_back(slot_to_out[in_sort]);
+        }
+        if (ok && keys.size() <= 4) {
+          P.topk = true;
+          P.k = L.limit;
+          P.sort_outs = keys;
+          P.final_cols = cols;
+          P.final_slots = L.cols;
+          P.last_step = s + 1;
+        }
+      }
+    }
+    return true;
+  }
+};
+
+// ---- finalize kernels ------------------------------------------------------------
+struct OutKind {
+  int fn;  // 0 sum 1 count 2 avg, 10+i key
+  int acc;
+  int is_int;
+};
+
+struct FinalSpec {
+  int nouts = 0;
+  OutKind outs[16];
+  void* out_ptr[16];
+  int nacc = 0;
+  int acc_is_int[kMaxAcc];
+};
+
+__global__ void k_final_scalar(const unsigned long long* __restrict__ part, int nparts, FinalSpec f, long long* err) {
+  __shared__ unsigned long long s_tot[kMaxAcc + 1];
+  int a = threadIdx.x;
+  if (a <= kMaxAcc && (a < f.nacc || a == kMaxAcc)) {
+    bool is_int = a == kMaxAcc || f.acc_is_int[a];
+    unsigned long long t = 0;
+    for (int c = 0; c < nparts; ++c) {
+      unsigned long long v = part[static_cast<long long>(c) * (kMaxAcc + 1) + a];
+      if (is_int) t = static_cast<unsigned long long>(static_cast<long long>(t) + static_cast<long long>(v));
+      else t = static_cast<unsigned long long>(__double_as_longlong(
+          __dadd_rn(__longlong_as_double(static_cast<long long>(t)), __longlong_as_double(static_cast<long long>(v)))));
+    }
+    s_tot[a] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long cnt = static_cast<long long>(s_tot[kMaxAcc]);
+    for (int j = 0; j < f.nouts; ++j) {
+      const OutKind& o = f.outs[j];
+      if (o.fn == 1) {
+        static_cast<long long*>(f.out_ptr[j])[0] = cnt;
+      } else if (o.fn == 0) {
+        static_cast<unsigned long long*>(f.out_ptr[j])[0] = s_tot[o.acc];
+      } else {
+        if (cnt == 0) {
+          err[0] = 1;  // AVG over zero rows: the reference raises division by zero
+          continue;
+        }
+        double sum = f.acc_is_int[o.acc] ? static_cast<double>(static_cast<long long>(s_tot[o.acc]))
+                                         : __longlong_as_double(static_cast<long long>(s_tot[o.acc]));
+        static_cast<double*>(f.out_ptr[j])[0] = __ddiv_rn(sum, static_cast<double>(cnt));
+      }
+    }
+  }
+}
+
+// MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums in CTA order
+constexpr int kMerged = 256;
+__global__ void k_final_small(const SmallPart* __restrict__ parts, int nparts, FinalSpec f, int nkeys,
+                              void* key_ptr0, void* key_ptr1, void* key_ptr2, void* key_ptr3, int* inv /*[nparts][kMerged]*/,
+                              long long* ngroups_out, long long* err) {
+  __shared__ unsigned s_set[kMerged];
+  __shared__ unsigned s_sorted[kMerged];
+  __shared__ int s_n;
+  for (int i = threadIdx.x; i < kMerged; i += blockDim.x) s_set[i] = 0xffffffffu;
+  __syncthreads();
+  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
+    unsigned c = parts[i / kGroups].codes[i % kGroups];
+    if (c == 0xffffffffu || parts[i / kGroups].cnt[i % kGroups] == 0) continue;
+    unsigned h = (c * 2654435761u) >> 24;
+    bool placed = false;
+    for (int p = 0; p < kMerged; ++p) {
+      unsigned cur = s_set[h];
+      if (cur == c) { placed = true; break; }
+      if (cur == 0xffffffffu) {
+        unsigned prev = atomicCAS(&s_set[h], 0xffffffffu, c);
+        if (prev == 0xffffffffu || prev == c) { placed = true; break; }
+      }
+      h = (h + 1) & (kMerged - 1);
+    }
+    if (!placed) err[0] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int i = 0; i < kMerged; ++i)
+      if (s_set[i] != 0xffffffffu) s_sorted[n++] = s_set[i];
+    for (int i = 1; i < n; ++i) {  // insertion sort (n <= 256)
+      unsigned v = s_sorted[i];
+      int j = i - 1;
+      while (j >= 0 && s_sorted[j] > v) {
+        s_sorted[j + 1] = s_sorted[j];
+        --j;
+      }
+      s_sorted[j + 1] = v;
+    }
+    s_n = n;
+    *ngroups_out = n;
+  }
+  __syncthreads();
+  const int n = s_n;
+  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kMerged; i += blockDim.x) inv[i] = -1;
+  __syncthreads();
+  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
+    int c = static_cast<int>(i / kGroups), sl = static_cast<int>(i % kGroups);
+    unsigned code = parts[c].codes[sl];
+    if (code == 0xffffffffu || parts[c].cnt[sl] == 0) continue;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      int m = (lo + hi) / 2;
+      if (s_sorted[m] < code) lo = m + 1;
+      else hi = m;
+    }
+    inv[static_cast<long long>(c) * kMerged + lo] = sl;
+  }
+  __syncthreads();
+  void* kp[4] = {key_ptr0, key_ptr1, key_ptr2, key_ptr3};
+  for (int g = threadIdx.x; g < n; g += blockDim.x) {
+    unsigned code = s_sorted[g];
+    for (int k = 0; k < nkeys; ++k) static_cast<uint8_t*>(kp[k])[g] = (code >> (8 * (nkeys - 1 - k))) & 0xff;
+    unsigned long long tot[kMaxAcc];
+    long long cnt = 0;
+    for (int a = 0; a < f.nacc; ++a) tot[a] = 0;
+    for (int c = 0; c < nparts; ++c) {
+      int sl = inv[static_cast<long long>(c) * kMerged + g];
+      if (sl < 0) continue;
+      cnt += static_cast<long long>(parts[c].cnt[sl]);
+      for (int a = 0; a < f.nacc; ++a) {
+        unsigned long long v = parts[c].acc[sl][a];
+        if (f.acc_is_int[a]) tot[a] = static_cast<unsigned long long>(static_cast<long long>(tot[a]) + static_cast<long long>(v));
+        else tot[a] = static_cast<unsigned long long>(__double_as_longlong(
+            __dadd_rn(__longlong_as_double(static_cast<long long>(tot[a])), __longlong_as_double(static_cast<long long>(v)))));
+      }
+    }
+    for (int j = 0; j < f.nouts; ++j) {
+      const OutKind& o = f.outs[j];
+      if (o.fn >= 10) continue;
+      if (o.fn == 1) static_cast<long long*>(f.out_ptr[j])[g] = cnt;
+      else if (o.fn == 0) static_cast<unsigned long long*>(f.out_ptr[j])[g] = tot[o.acc];
+      else {
+        double sum = f.acc_is_int[o.acc] ? static_cast<double>(static_cast<long long>(tot[o.acc]))
+                                         : __longlong_as_double(static_cast<long long>(tot[o.acc]));
+        static_cast<double*>(f.out_ptr[j])[g] = __ddiv_rn(sum, static_cast<double>(cnt));
+      }
+    }
+  }
+}
+
+// MODE_BUILDGRP outputs
+struct GroupSpec {
+  FinalSpec f;
+  const unsigned long long* gacc;
+  const unsigned long long* gcnt;
+  const int* group_row;
+  int nkeyc;
+  const long long* key_cols[kMaxKeys];  // root columns for the group keys
+  int nsort;
+  int sort_out[4];  // index into f.outs
+  int sort_asc[4];
+};
+
+__device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
+                                                bool& is_f64) {
+  const OutKind& o = s.f.outs[j];
+  const unsigned long long* acc = s.gacc + static_cast<long long>(g) * s.f.nacc * 2;
+  long long cnt = static_cast<long long>(s.gcnt[g]);
+  if (o.fn >= 10) {
+    bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][s.group_row[g]]);
+    is_f64 = false;
+    return true;
+  }
+  if (o.fn == 1) {
+    bits = static_cast<unsigned long long>(cnt);
+    is_f64 = false;
+    return true;
+  }
+  const unsigned long long lo = acc[o.acc * 2], hi = acc[o.acc * 2 + 1];
+  if (s.f.acc_is_int[o.acc]) {
+    long long v = static_cast<long long>(lo);
+    bool fits = static_cast<long long>(hi) == (v >> 63);
+    if (o.fn == 0) {
+      bits = static_cast<unsigned long long>(v);
+      is_f64 = false;
+      return fits;
+    }
+    bits = static_cast<unsigned long long>(__double_as_longlong(__ddiv_rn(static_cast<double>(v), static_cast<double>(cnt))));
+    is_f64 = true;
+    return fits;
+  }
+  double sum = q64_to_f64(lo, hi);
+  is_f64 = true;
+  bits = static_cast<unsigned long long>(__double_as_longlong(o.fn == 0 ? sum : __ddiv_rn(sum, static_cast<double>(cnt))));
+  return true;
+}
+
+// lexicographic candidate key: sort keys (with direction), then group keys asc
+__device__ __forceinline__ int cand_keys(const GroupSpec& s, unsigned g, unsigned long long* k) {
+  int n = 0;
+  for (int i = 0; i < s.nsort; ++i) {
+    unsigned long long bits;
+    bool f;
+    group_out_value(s, s.sort_out[i], g, bits, f);
+    unsigned long long u = f ? radix_key(__longlong_as_double(static_cast<long long>(bits)))
+                             : radix_key(static_cast<int64_t>(bits));
+    k[n++] = s.sort_asc[i] ? u : ~u;
+  }
+  for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(s.key_cols[i][s.group_row[g]]));
+  return n;
+}
+
+__device__ __forceinline__ bool key_less(const unsigned long long* a, const unsigned long long* b, int n) {
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return false;
+}
+
+// k rounds of block-wide "best remaining" over candidates [lo, hi) of `cand`
+// (cand == nullptr: gids lo..hi-1); selected gids appended to out[].
+__device__ void block_select(const GroupSpec& s, const unsigned* cand, long long lo, long long hi, int k, unsigned* out,
+                             int* nout) {
+  __shared__ unsigned long long s_best[kThreads / 32][9];
+  __shared__ unsigned s_bestg[kThreads / 32];
+  __shared__ unsigned s_chosen[64];
+  __shared__ int s_nchosen;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_nchosen = 0;
+  __syncthreads();
+  for (int round = 0; round < k; ++round) {
+    unsigned long long best[9];
+    unsigned bestg = 0xffffffffu;
+    int nk = 0;
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      unsigned g = cand ? cand[i] : static_cast<unsigned>(i);
+      if (g == 0xffffffffu || s.gcnt[g] == 0) continue;
+      bool taken = false;
+      for (int c = 0; c < s_nchosen; ++c) taken |= s_chosen[c] == g;
+      if (taken) continue;
+      unsigned long long key[9];
+      nk = cand_keys(s, g, key);
+      if (bestg == 0xffffffffu || key_less(key, best, nk)) {
+        for (int q = 0; q < nk; ++q) best[q] = key[q];
+        bestg = g;
+      }
+    }
+    nk = s.nsort + s.nkeyc;
+    // warp reduce (candidates compared by key; invalid = 0xffffffff gid)
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned og = __shfl_xor_sync(0xffffffffu, bestg, o);
+      unsigned long long ok[9];
+      for (int q = 0; q < nk; ++q) ok[q] = __shfl_xor_sync(0xffffffffu, best[q], o);
+      bool take = og != 0xffffffffu && (bestg == 0xffffffffu || key_less(ok, best, nk));
+      if (take) {
+        bestg = og;
+        for (int q = 0; q < nk; ++q) best[q] = ok[q];
+      }
+    }
+    if (lane == 0) {
+      s_bestg[warp] = bestg;
+      for (int q = 0; q < nk; ++q) s_best[warp][q] = best[q];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned bg = 0xffffffffu;
+      int bw = -1;
+      for (int w = 0; w < kThreads / 32; ++w) {
+        if (s_bestg[w] == 0xffffffffu) continue;
+        if (bw < 0 || key_less(s_best[w], s_best[bw], nk)) {
+          bw = w;
+          bg = s_bestg[w];
+        }
+      }
+      if (bg != 0xffffffffu) {
+        s_chosen[s_nchosen++] = bg;
+        out[(*nout)++] = bg;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_topk_local(GroupSpec s, long long ngroups, int k, unsigned* cand) {
+  __shared__ int s_n;
+  __shared__ unsigned s_out[64];
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  long long per = (ngroups + gridDim.x - 1) / gridDim.x;
+  long long lo = per * blockIdx.x, hi = lo + per < ngroups ? lo + per : ngroups;
+  block_select(s, nullptr, lo, hi > lo ? hi : lo, k, s_out, &s_n);
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    cand[static_cast<long long>(blockIdx.x) * k + i] = i < s_n ? s_out[i] : 0xffffffffu;
+}
+
+__global__ void __launch_bounds__(kThreads) k_topk_final(GroupSpec s, const unsigned* cand, long long ncand, int k,
+                                                         long long* nout, long long* err) {
+  __shared__ int s_n;
+  __shared__ unsigned s_out[64];
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  block_select(s, cand, 0, ncand, k, s_out, &s_n);
+  __syncthreads();
+  for (int r = threadIdx.x; r < s_n; r += blockDim.x) {
+    unsigned g = s_out[r];
+    for (int j = 0; j < s.f.nouts; ++j) {
+      unsigned long long bits;
+      bool f;
+      if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
+      static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
+    }
+  }
+  if (threadIdx.x == 0) *nout = s_n;
+}
+
+__global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids_sorted, long long n, long long* err) {
+  for (long long r = gtid(); r < n; r += gstride()) {
+    unsigned g = static_cast<unsigned>(gids_sorted[r]);
+    for (int j = 0; j < s.f.nouts; ++j) {
+      unsigned long long bits;
+      bool f;
+      if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
+      static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
+    }
+  }
+}
+
+__global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long n, uint8_t* __restrict__ mask) {
+  for (long long i = gtid(); i < n; i += gstride()) mask[i] = cnt[i] != 0;
+}
+
+__global__ void k_group_keys(const int* __restrict__ group_row, const long long* __restrict__ gids, long long n,
+                             const long long* __restrict__ key_col, long long* __restrict__ out) {
+  for (long long i = gtid(); i < n; i += gstride()) out[i] = key_col[group_row[gids[i]]];
+}
+
+// ---- unit runner ----------------------------------------------------------------
+const Column* find_col(const TableSet& tables, const std::string& t, const std::string& c) {
+  const Table* tab = bind_table(tables, t);
+  return tab ? tab->find(c) : nullptr;
+}
+
+Operand make_operand(const TableSet& tables, const PipeDesc& P, const OperandDesc& o, bool* ok) {
+  Operand r;
+  const std::string& table = o.probe < 0 ? P.fact_table : P.builds[P.probes[o.probe].build].table;
+  const Column* c = find_col(tables, table, o.column);
+  if (!c) {
+    *ok = false;
+    return r;
+  }
+  r.ptr = c->t.data();
+  r.type = c->t.dtype == TQP_F64 ? OT_F64 : (c->t.dtype == TQP_STR8 || c->t.dtype == TQP_BOOL) ? OT_U8 : OT_I64;
+  r.src = o.probe;
+  if (r.type == OT_U8 && c->t.cols != 1) *ok = false;
+  if (reinterpret_cast<uintptr_t>(r.ptr) % 16) *ok = false;
+  return r;
+}
+
+bool make_term(const TableSet& tables, const std::string& table, const TermDesc& t, Term* nt, StrTerm* st, bool* is_str) {
+  *is_str = false;
+  if (t.kind == 3 || t.kind == 4) {
+    nt->kind = t.kind == 3 ? TK_TRUE : TK_FALSE;
+    return true;
+  }
+  const Column* c = find_col(tables, table, t.column);
+  if (!c) return false;
+  if (t.kind == 0) {
+    nt->x.ptr = c->t.data();
+    nt->x.src = -1;
+    if (c->t.dtype == TQP_F64) {
+      if (!t.f64) return false;
+      nt->x.type = OT_F64;
+      nt->kind = TK_F64;
+      nt->fk = t.fk;
+    } else if (c->t.dtype == TQP_I64) {
+      if (t.f64) return false;
+      nt->x.type = OT_I64;
+      nt->kind = TK_INT;
+      nt->ik = t.ik;
+    } else {
+      return false;
+    }
+    nt->op = t.op;
+    return true;
+  }
+  if (c->t.dtype != TQP_STR8) return false;
+  *is_str = true;
+  st->ptr = c->t.ptr<uint8_t>();
+  st->width = static_cast<int>(c->t.cols);
+  st->is_like = t.kind == 2;
+  st->op = t.op;
+  st->anchor = t.anchor;
+  st->litlen = static_cast<int>(t.lit.size());
+  std::memcpy(st->lit, t.lit.data(), t.lit.size());
+  return true;
+}
+
+struct Runner {
+  PipeDesc P;
+
+  bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables) const {
+    // build sides, children first (builds[] is in post-order by construction)
+    auto err_buf = c.alloc_bytes(16);
+    long long* err = static_cast<long long*>(err_buf->ptr);
+    TQP_CUDA(cudaMemsetAsync(err, 0, 16, c.stream));
+    std::vector<Probe> built(P.builds.size());
+    std::vector<std::shared_ptr<DevBuf>> keep;
+    std::vector<long long> build_rows(P.builds.size(), 0);
+    int* group_row = nullptr;
+    unsigned* group_counter = nullptr;
+    for (size_t bi = 0; bi < P.builds.size(); ++bi) {
+      const BuildDesc& B = P.builds[bi];
+      const Table* tab = bind_table(tables, B.table);
+      const Column* key = tab ? tab->find(B.key_column) : nullptr;
+      if (!key || key->t.dtype != TQP_I64) return false;
+      long long n = tab->rows;
+      build_rows[bi] = n;
+      long long mm[2] = {0x7fffffffffffffffLL, static_cast<long long>(0x8000000000000000ULL)};
+      auto mmb = c.alloc_bytes(16);
+      TQP_CUDA(cudaMemcpyAsync(mmb->ptr, mm, 16, cudaMemcpyHostToDevice, c.stream));
+      if (n) {
+        k_minmax<<<c.grid_for(n, 256, 4, 2), 256, 0, c.stream>>>(key->t.ptr<long long>(), n, static_cast<long long*>(mmb->ptr));
+        c.count_launch();
+      }
+      TQP_CUDA(cudaMemcpyAsync(mm, mmb->ptr, 16, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      long long range = n ? mm[1] - mm[0] + 1 : 1;
+      if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
+      BuildSpec bs;
+      bs.n = n;
+      bs.kmin = n ? mm[0] : 0;
+      bs.range = range;
+      auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
+      TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
+      keep.push_back(table);
+      bs.table = static_cast<unsigned long long*>(table->ptr);
+      bs.err = err;
+      bool ok = true;
+      bs.key = {key->t.data(), OT_I64, -1};
+      for (const auto& t : B.terms) {
+        Term nt;
+        StrTerm st;
+        bool is_str;
+        if (!make_term(tables, B.table, t, &nt, &st, &is_str)) return false;
+        if (is_str) {
+          if (bs.nstr >= kMaxStrTerms) return false;
+          bs.str[bs.nstr++] = st;
+        } else {
+          if (bs.nterms >= kMaxTerms) return false;
+          bs.terms[bs.nterms++] = nt;
+        }
+      }
+      for (const auto& t : B.flags) {
+        Term nt;
+        StrTerm st;
+        bool is_str;
+        if (!make_term(tables, B.table, t, &nt, &st, &is_str) || !is_str) return false;
+        bs.flags[bs.nflags++] = st;
+      }
+      for (const auto& ch : B.children) {
+        const Column* kc = tab->find(ch.fact_column);
+        if (!kc || kc->t.dtype != TQP_I64) return false;
+        Probe p = built[ch.build];
+        p.key = {kc->t.data(), OT_I64, -1};
+        bs.probes[bs.nprobes++] = p;
+      }
+      if (B.assign_groups) {
+        auto gr = c.alloc_bytes(sizeof(int) * (n + 1) + 16);
+        keep.push_back(gr);
+        group_row = static_cast<int*>(gr->ptr);
+        group_counter = reinterpret_cast<unsigned*>(group_row + n + 1);
+        TQP_CUDA(cudaMemsetAsync(group_counter, 0, 4, c.stream));
+        bs.assign_groups = 1;
+        bs.group_counter = group_counter;
+        bs.group_row = group_row;
+      }
+      if (!ok) return false;
+      if (n) {
+        k_build<<<c.grid_for(n, kThreads, 1, 4), kThreads, 0, c.stream>>>(bs);
+        c.count_launch();
+      }
+      Probe pr;
+      pr.kmin = bs.kmin;
+      pr.range = range;
+      pr.table = bs.table;
+      built[bi] = pr;
+    }
+    // fact probe
+    const Table* fact = bind_table(tables, P.fact_table);
+    if (!fact) return false;
+    ProbeSpec ps;
+    ps.n = fact->rows;
+    ps.err = err;
+    bool ok = true;
+    for (const auto& t : P.terms) {
+      Term nt;
+      StrTerm st;
+      bool is_str;
+      if (!make_term(tables, P.fact_table, t, &nt, &st, &is_str) || is_str) return false;
+      if (reinterpret_cast<uintptr_t>(nt.x.ptr) % 16) return false;
+      ps.terms[ps.nterms++] = nt;
+    }
+    for (const auto& p : P.probes) {
+      Probe pr = built[p.build];
+      pr.key = make_operand(tables, P, {-1, p.fact_column}, &ok);
+      if (pr.key.type != OT_I64) return false;
+      ps.probes[ps.nprobes++] = pr;
+    }
+    for (const auto& a : P.accs) {
+      Acc& d = ps.acc[ps.nacc++];
+      d.is_int = a.is_int;
+      d.nf = static_cast<int>(a.f.size());
+      for (size_t i = 0; i < a.f.size(); ++i) {
+        if (a.f[i].kind != FK_CONST) d.f[i].x = make_operand(tables, P, a.f[i].x, &ok);
+        d.f[i].kind = a.f[i].kind;
+        d.f[i].k = a.f[i].k;
+      }
+      d.gate_probe = a.gate_probe;
+      d.gate_bit = a.gate_bit;
+      d.gate_else = a.gate_else;
+    }
+    for (const auto& kcol : P.key_columns) ps.keys[ps.nkeys++] = make_operand(tables, P, {-1, kcol}, &ok);
+    if (!ok) return false;
+
+    FinalSpec fs;
+    fs.nacc = ps.nacc;
+    for (int a = 0; a < ps.nacc; ++a) fs.acc_is_int[a] = ps.acc[a].is_int;
+    fs.nouts = static_cast<int>(P.outs.size());
+    if (fs.nouts > 16) return false;
+    for (int j = 0; j < fs.nouts; ++j) fs.outs[j] = {P.outs[j].fn, P.outs[j].acc, P.outs[j].is_int ? 1 : 0};
+
+    const int grid = c.num_sms * 4;
+    auto out_dtype = [&](const OutDesc& o) {
+      if (o.fn >= 10) return P.mode == MODE_SMALL ? TQP_STR8 : TQP_I64;
+      if (o.fn == 1) return TQP_I64;
+      if (o.fn == 2) return TQP_F64;
+      return o.is_int ? TQP_I64 : TQP_F64;
+    };
+    std::vector<Tensor> outs(P.outs.size());
+    long long nrows = 0;
+
+    if (P.mode == MODE_SCALAR) {
+      auto part = c.alloc_bytes(sizeof(unsigned long long) * grid * (kMaxAcc + 1));
+      ps.part = static_cast<unsigned long long*>(part->ptr);
+      k_probe_scalar<<<grid, kThreads, 0, c.stream>>>(ps);
+      for (size_t j = 0; j < outs.size(); ++j) {
+        outs[j] = c.alloc(out_dtype(P.outs[j]), 1, 1);
+        fs.out_ptr[j] = outs[j].data();
+      }
+      k_final_scalar<<<1, 32, 0, c.stream>>>(ps.part, grid, fs, err);
+      c.count_launch(2);
+      nrows = 1;
+    } else if (P.mode == MODE_SMALL) {
+      const int g2 = c.num_sms * 2;
+      auto part = c.alloc_bytes(sizeof(SmallPart) * g2);
+      ps.part = static_cast<unsigned long long*>(part->ptr);
+      k_probe_small<<<g2, kThreads, 0, c.stream>>>(ps);
+      auto inv = c.alloc_bytes(sizeof(int) * g2 * kMerged);
+      auto ng = c.alloc_bytes(8);
+      std::vector<Tensor> tmp(P.outs.size());
+      for (size_t j = 0; j < outs.size(); ++j) {
+        tmp[j] = c.alloc(out_dtype(P.outs[j]), kMerged, 1);
+        fs.out_ptr[j] = tmp[j].data();
+      }
+      void* kp[4] = {nullptr, nullptr, nullptr, nullptr};
+      for (size_t j = 0; j < P.outs.size(); ++j)
+        if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = tmp[j].data();
+      k_final_small<<<1, kThreads, 0, c.stream>>>(reinterpret_cast<SmallPart*>(part->ptr), g2, fs, ps.nkeys, kp[0], kp[1],
+                                                  kp[2], kp[3], static_cast<int*>(inv->ptr),
+                                                  static_cast<long long*>(ng->ptr), err);
+      c.count_launch(2);
+      TQP_CUDA(cudaMemcpyAsync(&nrows, ng->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      for (size_t j = 0; j < outs.size(); ++j) {
+        outs[j] = tmp[j];
+        outs[j].rows = nrows;
+      }
+    } else {
+      // MODE_BUILDGRP
+      long long ngroups = build_rows[P.probes[P.group_probe].build];
+      auto gacc = c.alloc_bytes(sizeof(unsigned long long) * 2 * std::max(1, ps.nacc) * (ngroups + 1));
+      auto gcnt = c.alloc_bytes(sizeof(unsigned long long) * (ngroups + 1));
+      TQP_CUDA(cudaMemsetAsync(gacc->ptr, 0, gacc->bytes, c.stream));
+      TQP_CUDA(cudaMemsetAsync(gcnt->ptr, 0, gcnt->bytes, c.stream));
+      ps.gacc = static_cast<unsigned long long*>(gacc->ptr);
+      ps.gcnt = static_cast<unsigned long long*>(gcnt->ptr);
+      ps.group_probe = P.group_probe;
+      k_probe_buildgrp<<<grid, kThreads, 0, c.stream>>>(ps);
+      c.count_launch();
+      GroupSpec gs;
+      gs.f = fs;
+      gs.gacc = ps.gacc;
+      gs.gcnt = ps.gcnt;
+      gs.group_row = group_row;
+      const BuildDesc& gb = P.builds[P.probes[P.group_probe].build];
+      const Table* groot = bind_table(tables, gb.table);
+      gs.nkeyc = static_cast<int>(P.group_key_root_columns.size());
+      for (int i = 0; i < gs.nkeyc; ++i) {
+        const Column* kc = groot->find(P.group_key_root_columns[i]);
+        if (!kc || kc->t.dtype != TQP_I64) return false;
+        gs.key_cols[i] = kc->t.ptr<long long>();
+      }
+      if (P.topk) {
+        gs.nsort = static_cast<int>(P.sort_outs.size());
+        for (int i = 0; i < gs.nsort; ++i) {
+          gs.sort_out[i] = P.sort_outs[i].first;
+          gs.sort_asc[i] = P.sort_outs[i].second;
+        }
+        // reference sort over NaN keys is an error: leave that to the exact path
+        int k = static_cast<int>(P.k);
+        std::vector<Tensor> tmp(P.outs.size());
+        for (size_t j = 0; j < outs.size(); ++j) {
+          tmp[j] = c.alloc(out_dtype(P.outs[j]), std::max(1, k), 1);
+          gs.f.out_ptr[j] = tmp[j].data();
+        }
+        const int tg = c.num_sms;
+        auto cand = c.alloc_bytes(sizeof(unsigned) * tg * std::max(1, k));
+        auto nout = c.alloc_bytes(8);
+        if (k > 0) {
+          k_topk_local<<<tg, kThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned*>(cand->ptr));
+          k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned*>(cand->ptr), static_cast<long long>(tg) * k, k,
+                                                     static_cast<long long*>(nout->ptr), err);
+          c.count_launch(2);
+          TQP_CUDA(cudaMemcpyAsync(&nrows, nout->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
+        }
+        c.sync();
+        for (size_t j = 0; j < outs.size(); ++j) {
+          outs[j] = tmp[j];
+          outs[j].rows = nrows;
+        }
+      } else {
+        // every group, ascending by the (unique) build key
+        Tensor cnt_view;
+        cnt_view.dtype = TQP_I64;
+        cnt_view.rows = ngroups;
+        cnt_view.buf = gcnt;
+        Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
+        if (ngroups) {
+          k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(ps.gcnt, ngroups, mask.ptr<uint8_t>());
+          c.count_launch();
+        }
+        Tensor gids = k::compact(c, k::iota(c, ngroups), mask);
+        long long n = gids.rows;
+        Tensor keys = c.alloc(TQP_I64, n, 1);
+        const Column* bk = groot->find(gb.key_column);
+        if (n) {
+          k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(group_row, gids.ptr<long long>(), n, bk->t.ptr<long long>(),
+                                                                  keys.ptr<long long>());
+          c.count_launch();
+        }
+        Tensor order = k::radix_sort_payload(c, keys, &gids, false);
+        for (size_t j = 0; j < outs.size(); ++j) {
+          outs[j] = c.alloc(out_dtype(P.outs[j]), n, 1);
+          gs.f.out_ptr[j] = outs[j].data();
+        }
+        if (n) {
+          k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, order.ptr<long long>(), n, err);
+          c.count_launch();
+        }
+        nrows = n;
+      }
+    }
+    long long herr[2] = {0, 0};
+    TQP_CUDA(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (herr[0]) return false;  // preconditions violated: exact per-instruction path
+    (void)nrows;
+    for (size_t i = 0; i < P.final_slots.size(); ++i) slots[P.final_slots[i]] = outs[P.final_cols[i]];
+    return true;
+  }
+};
+
+}  // namespace
+
+std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
+  (void)ctx;
+  std::vector<FusedUnit> units;
+  Analysis A(plan);
+  A.analyse();
+  // live-out check helper: slots produced in [a, b] read after b or output
+  std::map<int, int> last_read_step;
+  for (size_t s = 0; s < plan.steps.size(); ++s)
+    for (const auto& in : plan.steps[s].instrs)
+      for (int x : in.inputs) last_read_step[x] = static_cast<int>(s);
+  std::set<int> plan_outputs;
+  for (const auto& o : plan.outputs) plan_outputs.insert(o.slot);
+  int next_free = 0;
+  for (size_t s = 0; s < plan.steps.size(); ++s) {
+    if (A.rels[s].kind != Rel::AGG || static_cast<int>(s) < next_free) continue;
+    Planner pl(A, plan);
+    if (!pl.plan_agg(static_cast<int>(s))) {
+      if (std::getenv("TQP_FUSION_DEBUG")) std::fprintf(stderr, "[tqp] no fusion at %s: %s\n", plan.steps[s].id.c_str(), pl.why.c_str());
+      continue;
+    }
+    PipeDesc& P = pl.P;
+    if (P.first_step < next_free) continue;
+    // every slot produced inside the unit and needed later must be produced
+    // by the unit
+    std::set<int> provided(P.final_slots.begin(), P.final_slots.end());
+    bool ok = true;
+    for (int q = P.first_step; q <= P.last_step && ok; ++q) {
+      for (const auto& in : plan.steps[q].instrs) {
+        int x = in.output;
+        bool needed = plan_outputs.count(x) || (last_read_step.count(x) && last_read_step[x] > P.last_step);
+        if (needed && !provided.count(x)) ok = false;
+      }
+      // project steps without instructions pass slots through
+      for (int x : plan.steps[q].output_slots) {
+        bool needed = plan_outputs.count(x) || (last_read_step.count(x) && last_read_step[x] > P.last_step);
+        if (needed && !provided.count(x)) ok = false;
+      }
+    }
+    if (!ok) continue;
+    std::ostringstream ex;
+    const char* mode = P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small-group" : "build-group";
+    ex << "fact=" << P.fact_table << " terms=" << P.terms.size() << " probes=" << P.probes.size()
+       << " builds=" << P.builds.size() << " accumulators=" << P.accs.size() << " mode=" << mode
+       << (P.topk ? " topk=" + std::to_string(P.k) : std::string());
+    FusedUnit u;
+    u.first_step = P.first_step;
+    u.last_step = P.last_step;
+    u.name = std::string("fused_") + (P.probes.empty() ? "scan_" : "probe_") + mode + (P.topk ? "_topk" : "");
+    u.explain = ex.str();
+    u.run = Runner{P};
+    units.push_back(std::move(u));
+    next_free = P.last_step + 1;
+  }
+  return units;
+}
+
 }  // namespace tqp

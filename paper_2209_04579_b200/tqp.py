@@ -128,11 +128,13 @@ def _load() -> C.CDLL:
         "tqp_plan_set_step_outputs": (I, [P, C.POINTER(C.c_int), I, S]),
         "tqp_plan_add_output": (I, [P, C.c_char_p, I, I, S]),
         "tqp_plan_add_input_column": (I, [P, C.c_char_p, C.c_char_p, I, S]),
-        "tqp_plan_free": (None, [P]),
+        "tqp_plan_free": (None, [P]), "tqp_plan_fusion_explain": (C.c_char_p, [P]),
         "tqp_executor_create": (P, [P, P, C.c_uint, S]),
         "tqp_executor_execute": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, S]),
         "tqp_executor_profile": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, C.POINTER(C.c_void_p), S]),
         "tqp_executor_explain": (C.c_char_p, [P]), "tqp_executor_free": (None, [P]),
+        "tqp_executor_set_timing": (None, [P, I]), "tqp_executor_timings": (C.c_char_p, [P]),
+        "tqp_executor_reset_timings": (None, [P]),
         "tqp_free_str": (None, [P]),
         "tqp_result_rows": (I64_, [P]), "tqp_result_num_columns": (I, [P]),
         "tqp_result_column_name": (C.c_char_p, [P, I]), "tqp_result_column_type": (I, [P, I]),
@@ -552,6 +554,10 @@ class Plan:
                 _check(st, lib.tqp_plan_add_input_column(self.h, t["name"].encode(), c["name"].encode(),
                                                          LOGICAL_NAMES[c["type"]], C.byref(st)) == 0)
 
+    def fusion(self) -> dict:
+        """Fused pipelines the executor would choose (host-only planning)."""
+        return json.loads(lib.tqp_plan_fusion_explain(self.h).decode())
+
     @staticmethod
     def from_file(path) -> "Plan":
         with open(path) as f:
@@ -612,6 +618,16 @@ class Executor:
         if getattr(self, "h", None):
             lib.tqp_executor_free(self.h)
             self.h = None
+
+    def set_timing(self, on: bool = True):
+        lib.tqp_executor_set_timing(self.h, 1 if on else 0)
+
+    def timings(self) -> dict:
+        """{unit: {"calls", "total_ms"}} measured with CUDA events."""
+        return json.loads(lib.tqp_executor_timings(self.h).decode())
+
+    def reset_timings(self):
+        lib.tqp_executor_reset_timings(self.h)
 
     def explain(self) -> dict:
         return json.loads(lib.tqp_executor_explain(self.h).decode())
