@@ -9,7 +9,9 @@
 // > 64 groups, fixed-point range, int64 near overflow) hands its steps back
 // to the per-instruction path, which reproduces the reference exactly.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -1138,93 +1140,119 @@ __device__ __forceinline__ bool key_less(const unsigned long long* a, const unsi
   return false;
 }
 
-// k rounds of block-wide "best remaining" over candidates [lo, hi) of `cand`
-// (cand == nullptr: gids lo..hi-1); selected gids appended to out[].
-__device__ void block_select(const GroupSpec& s, const unsigned* cand, long long lo, long long hi, int k, unsigned* out,
-                             int* nout) {
-  __shared__ unsigned long long s_best[kThreads / 32][9];
-  __shared__ unsigned s_bestg[kThreads / 32];
-  __shared__ unsigned s_chosen[64];
-  __shared__ int s_nchosen;
+// Top-k with the reference's tie order. Candidates (groups with rows) get
+// their full key tuple computed once; each CTA then runs k rounds of
+// block-wide "best remaining" over its chunk (each thread keeps a taken-mask
+// over the <= 64 candidates it owns), and one CTA merges the per-CTA winners.
+constexpr int kTopkMaxPerThread = 64;
+
+__global__ void k_topk_cands(GroupSpec s, long long ngroups, unsigned* __restrict__ cand_gid,
+                             unsigned long long* __restrict__ cand_key, unsigned* __restrict__ ncand) {
+  const int lane = threadIdx.x & 31;
+  const int nk = s.nsort + s.nkeyc;
+  for (long long base = gtid() & ~31LL; base < ngroups; base += gstride()) {
+    const long long g = base + lane;
+    const bool ok = g < ngroups && s.gcnt[g] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    unsigned first = 0;
+    if (lane == 0 && m) first = atomicAdd(ncand, static_cast<unsigned>(__popc(m)));
+    first = __shfl_sync(0xffffffffu, first, 0);
+    if (!ok) continue;
+    const unsigned pos = first + __popc(m & ((1u << lane) - 1u));
+    cand_gid[pos] = static_cast<unsigned>(g);
+    unsigned long long k[9];
+    cand_keys(s, static_cast<unsigned>(g), k);
+    for (int q = 0; q < nk; ++q) cand_key[static_cast<long long>(pos) * nk + q] = k[q];
+  }
+}
+
+// k rounds over candidates [lo, hi); winners (candidate indices) -> out
+__device__ void block_topk(const unsigned long long* __restrict__ keys, int nk, long long lo, long long hi, int k,
+                           long long* out, int* nout) {
+  __shared__ unsigned long long s_key[kThreads / 32][9];
+  __shared__ long long s_idx[kThreads / 32];
+  __shared__ long long s_win;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_nchosen = 0;
-  __syncthreads();
+  unsigned long long taken = 0;
   for (int round = 0; round < k; ++round) {
+    long long bi = -1;
     unsigned long long best[9];
-    unsigned bestg = 0xffffffffu;
-    int nk = 0;
-    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-      unsigned g = cand ? cand[i] : static_cast<unsigned>(i);
-      if (g == 0xffffffffu || s.gcnt[g] == 0) continue;
-      bool taken = false;
-      for (int c = 0; c < s_nchosen; ++c) taken |= s_chosen[c] == g;
-      if (taken) continue;
-      unsigned long long key[9];
-      nk = cand_keys(s, g, key);
-      if (bestg == 0xffffffffu || key_less(key, best, nk)) {
-        for (int q = 0; q < nk; ++q) best[q] = key[q];
-        bestg = g;
+    for (int j = 0; j < kTopkMaxPerThread; ++j) {
+      long long i = lo + threadIdx.x + static_cast<long long>(j) * blockDim.x;
+      if (i >= hi) break;
+      if ((taken >> j) & 1ULL) continue;
+      const unsigned long long* kk = keys + i * nk;
+      if (bi < 0 || key_less(kk, best, nk)) {
+        for (int q = 0; q < nk; ++q) best[q] = kk[q];
+        bi = i;
       }
     }
-    nk = s.nsort + s.nkeyc;
-    // warp reduce (candidates compared by key; invalid = 0xffffffff gid)
     for (int o = 16; o > 0; o >>= 1) {
-      unsigned og = __shfl_xor_sync(0xffffffffu, bestg, o);
+      long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
       unsigned long long ok[9];
       for (int q = 0; q < nk; ++q) ok[q] = __shfl_xor_sync(0xffffffffu, best[q], o);
-      bool take = og != 0xffffffffu && (bestg == 0xffffffffu || key_less(ok, best, nk));
-      if (take) {
-        bestg = og;
+      if (oi >= 0 && (bi < 0 || key_less(ok, best, nk) || (!key_less(best, ok, nk) && oi < bi))) {
+        bi = oi;
         for (int q = 0; q < nk; ++q) best[q] = ok[q];
       }
     }
     if (lane == 0) {
-      s_bestg[warp] = bestg;
-      for (int q = 0; q < nk; ++q) s_best[warp][q] = best[q];
+      s_idx[warp] = bi;
+      for (int q = 0; q < nk; ++q) s_key[warp][q] = best[q];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      unsigned bg = 0xffffffffu;
       int bw = -1;
       for (int w = 0; w < kThreads / 32; ++w) {
-        if (s_bestg[w] == 0xffffffffu) continue;
-        if (bw < 0 || key_less(s_best[w], s_best[bw], nk)) {
-          bw = w;
-          bg = s_bestg[w];
-        }
+        if (s_idx[w] < 0) continue;
+        if (bw < 0 || key_less(s_key[w], s_key[bw], nk)) bw = w;
       }
-      if (bg != 0xffffffffu) {
-        s_chosen[s_nchosen++] = bg;
-        out[(*nout)++] = bg;
-      }
+      s_win = bw < 0 ? -1 : s_idx[bw];
+      if (s_win >= 0) out[(*nout)++] = s_win;
     }
+    __syncthreads();
+    const long long win = s_win;
+    if (win < 0) break;
+    const long long rel = win - lo - threadIdx.x;
+    if (rel >= 0 && rel % blockDim.x == 0) taken |= 1ULL << (rel / blockDim.x);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_topk_local(GroupSpec s, long long ngroups, int k, unsigned* cand) {
+__global__ void __launch_bounds__(kThreads) k_topk_local(const unsigned long long* __restrict__ keys, int nk,
+                                                         long long ncand, long long chunk, int k,
+                                                         long long* __restrict__ winners) {
+  __shared__ long long s_out[64];
   __shared__ int s_n;
-  __shared__ unsigned s_out[64];
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  long long per = (ngroups + gridDim.x - 1) / gridDim.x;
-  long long lo = per * blockIdx.x, hi = lo + per < ngroups ? lo + per : ngroups;
-  block_select(s, nullptr, lo, hi > lo ? hi : lo, k, s_out, &s_n);
+  const long long lo = chunk * blockIdx.x, hi = lo + chunk < ncand ? lo + chunk : ncand;
+  block_topk(keys, nk, lo, hi > lo ? hi : lo, k, s_out, &s_n);
   __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x)
-    cand[static_cast<long long>(blockIdx.x) * k + i] = i < s_n ? s_out[i] : 0xffffffffu;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) winners[static_cast<long long>(blockIdx.x) * k + i] = i < s_n ? s_out[i] : -1;
 }
 
-__global__ void __launch_bounds__(kThreads) k_topk_final(GroupSpec s, const unsigned* cand, long long ncand, int k,
-                                                         long long* nout, long long* err) {
+__global__ void __launch_bounds__(kThreads) k_topk_final(GroupSpec s, const unsigned long long* __restrict__ keys,
+                                                         const unsigned* __restrict__ cand_gid,
+                                                         const long long* __restrict__ winners, long long nwin, int k,
+                                                         unsigned long long* __restrict__ scratch, long long* nout,
+                                                         long long* err) {
+  __shared__ long long s_out[64];
   __shared__ int s_n;
-  __shared__ unsigned s_out[64];
+  const int nk = s.nsort + s.nkeyc;
+  // gather the winners' keys into a dense scratch (invalid -> max key)
+  for (long long i = threadIdx.x; i < nwin; i += blockDim.x) {
+    long long w = winners[i];
+    for (int q = 0; q < nk; ++q) scratch[i * nk + q] = w >= 0 ? keys[w * nk + q] : ~0ULL;
+  }
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  block_select(s, cand, 0, ncand, k, s_out, &s_n);
+  block_topk(scratch, nk, 0, nwin, k, s_out, &s_n);
   __syncthreads();
   for (int r = threadIdx.x; r < s_n; r += blockDim.x) {
-    unsigned g = s_out[r];
+    long long w = winners[s_out[r]];
+    if (w < 0) continue;
+    const unsigned g = cand_gid[w];
     for (int j = 0; j < s.f.nouts; ++j) {
       unsigned long long bits;
       bool f;
@@ -1232,7 +1260,11 @@ __global__ void __launch_bounds__(kThreads) k_topk_final(GroupSpec s, const unsi
       static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
     }
   }
-  if (threadIdx.x == 0) *nout = s_n;
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int r = 0; r < s_n; ++r) n += winners[s_out[r]] >= 0;
+    *nout = n;
+  }
 }
 
 __global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids_sorted, long long n, long long* err) {
@@ -1317,6 +1349,117 @@ bool make_term(const TableSet& tables, const std::string& table, const TermDesc&
   return true;
 }
 
+// Numeric conjuncts -> one branch-free range per column (RTerm). int64:
+// x < K == x <= K-1 etc.; fp64: x < K == x <= nextafter(K, -inf) for every
+// non-NaN x, and NaN fails lo <= x <= hi exactly as it fails `<`/`>`.
+bool merge_range_terms(const std::vector<Term>& in, ProbeSpec& ps, std::vector<Operand>& cols) {
+  struct R {
+    Operand x;
+    bool f64;
+    long long ilo, ihi;
+    double flo, fhi;
+    bool empty = false;
+  };
+  std::vector<R> ranges;
+  std::vector<std::pair<Operand, Term>> ne;
+  bool any_false = false;
+  for (const Term& t : in) {
+    if (t.kind == TK_TRUE) continue;
+    if (t.kind == TK_FALSE) {
+      any_false = true;
+      continue;
+    }
+    if (t.op == TQP_NE) {
+      ne.push_back({t.x, t});
+      continue;
+    }
+    R r;
+    r.x = t.x;
+    r.f64 = t.kind == TK_F64;
+    r.ilo = std::numeric_limits<long long>::min();
+    r.ihi = std::numeric_limits<long long>::max();
+    r.flo = -std::numeric_limits<double>::infinity();
+    r.fhi = std::numeric_limits<double>::infinity();
+    if (r.f64) {
+      const double k = t.fk;
+      if (std::isnan(k)) {
+        r.empty = true;
+      } else {
+        switch (t.op) {
+          case TQP_EQ: r.flo = r.fhi = k; break;
+          case TQP_LT: r.fhi = std::nextafter(k, -std::numeric_limits<double>::infinity()); break;
+          case TQP_LE: r.fhi = k; break;
+          case TQP_GT: r.flo = std::nextafter(k, std::numeric_limits<double>::infinity()); break;
+          default: r.flo = k; break;
+        }
+        if (t.op == TQP_LT && k == -std::numeric_limits<double>::infinity()) r.empty = true;
+        if (t.op == TQP_GT && k == std::numeric_limits<double>::infinity()) r.empty = true;
+      }
+    } else {
+      const long long k = t.ik;
+      switch (t.op) {
+        case TQP_EQ: r.ilo = r.ihi = k; break;
+        case TQP_LT:
+          if (k == std::numeric_limits<long long>::min()) r.empty = true;
+          else r.ihi = k - 1;
+          break;
+        case TQP_LE: r.ihi = k; break;
+        case TQP_GT:
+          if (k == std::numeric_limits<long long>::max()) r.empty = true;
+          else r.ilo = k + 1;
+          break;
+        default: r.ilo = k; break;
+      }
+    }
+    bool merged = false;
+    for (auto& q : ranges) {
+      if (q.x.ptr == r.x.ptr && q.f64 == r.f64) {
+        q.ilo = std::max(q.ilo, r.ilo);
+        q.ihi = std::min(q.ihi, r.ihi);
+        q.flo = std::max(q.flo, r.flo);
+        q.fhi = std::min(q.fhi, r.fhi);
+        q.empty = q.empty || r.empty;
+        merged = true;
+      }
+    }
+    if (!merged) ranges.push_back(r);
+  }
+  auto push = [&](const RTerm& rt, const Operand& x) {
+    if (ps.nterms >= kMaxTerms) return false;
+    ps.terms[ps.nterms++] = rt;
+    cols.push_back(x);
+    return true;
+  };
+  if (any_false) {
+    RTerm f;
+    f.kind = RK_FALSE;
+    return push(f, Operand{});
+  }
+  for (const auto& r : ranges) {
+    RTerm rt;
+    if (r.empty || (r.f64 ? !(r.flo <= r.fhi) : r.ilo > r.ihi)) {
+      rt.kind = RK_FALSE;
+    } else if (r.f64) {
+      rt.kind = RK_F64;
+      std::memcpy(&rt.lo, &r.flo, 8);
+      std::memcpy(&rt.hi, &r.fhi, 8);
+    } else {
+      rt.kind = RK_INT;
+      rt.lo = static_cast<unsigned long long>(r.ilo);
+      rt.hi = static_cast<unsigned long long>(r.ihi);
+    }
+    if (!push(rt, r.x)) return false;
+  }
+  for (const auto& [x, t] : ne) {
+    RTerm rt;
+    rt.kind = t.kind == TK_F64 ? RK_F64_NE : RK_INT_NE;
+    if (t.kind == TK_F64) std::memcpy(&rt.lo, &t.fk, 8);
+    else rt.lo = static_cast<unsigned long long>(t.ik);
+    if (!push(rt, x)) return false;
+  }
+  return true;
+}
+
 struct Runner {
   PipeDesc P;
 
@@ -1356,6 +1499,11 @@ struct Runner {
       TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
+      const long long bm_words = (range + 31) / 32;
+      auto bitmap = c.alloc_bytes(sizeof(unsigned) * bm_words);
+      TQP_CUDA(cudaMemsetAsync(bitmap->ptr, 0, sizeof(unsigned) * bm_words, c.stream));
+      keep.push_back(bitmap);
+      bs.bitmap = static_cast<unsigned*>(bitmap->ptr);
       bs.err = err;
       bool ok = true;
       bs.key = {key->t.data(), OT_I64, -1};
@@ -1405,6 +1553,7 @@ struct Runner {
       pr.kmin = bs.kmin;
       pr.range = range;
       pr.table = bs.table;
+      pr.bitmap = bs.bitmap;
       built[bi] = pr;
     }
     // fact probe
@@ -1414,14 +1563,18 @@ struct Runner {
     ps.n = fact->rows;
     ps.err = err;
     bool ok = true;
+    // conjuncts on the same column merge into one lo <= x <= hi range
+    std::vector<Term> raw_terms;
     for (const auto& t : P.terms) {
       Term nt;
       StrTerm st;
       bool is_str;
       if (!make_term(tables, P.fact_table, t, &nt, &st, &is_str) || is_str) return false;
-      if (reinterpret_cast<uintptr_t>(nt.x.ptr) % 16) return false;
-      ps.terms[ps.nterms++] = nt;
+      if (nt.kind <= TK_F64 && reinterpret_cast<uintptr_t>(nt.x.ptr) % 16) return false;
+      raw_terms.push_back(nt);
     }
+    std::vector<Operand> term_cols;
+    if (!merge_range_terms(raw_terms, ps, term_cols)) return false;
     for (const auto& p : P.probes) {
       Probe pr = built[p.build];
       pr.key = make_operand(tables, P, {-1, p.fact_column}, &ok);
@@ -1444,6 +1597,73 @@ struct Runner {
     for (const auto& kcol : P.key_columns) ps.keys[ps.nkeys++] = make_operand(tables, P, {-1, kcol}, &ok);
     if (!ok) return false;
 
+    if (P.mode == MODE_SMALL && ps.nacc > kMaxAccSmall) return false;
+    // distinct fact columns staged per tile; operands address them by index
+    TileSpec ts;
+    auto col_index = [&](Operand& o) {
+      if (o.src >= 0 || !o.ptr) return true;
+      const int w = o.type == OT_U8 ? 1 : 8;
+      for (int i = 0; i < ts.ncols; ++i) {
+        if (ts.col_ptr[i] == o.ptr) {
+          o.col = i;
+          return true;
+        }
+      }
+      if (ts.ncols >= kMaxCols) return false;
+      ts.col_ptr[ts.ncols] = static_cast<const unsigned char*>(o.ptr);
+      ts.col_w[ts.ncols] = w;
+      o.col = ts.ncols++;
+      return true;
+    };
+    for (int i = 0; i < ps.nterms; ++i) {
+      if (ps.terms[i].kind >= RK_TRUE) continue;
+      if (!col_index(term_cols[i])) return false;
+      ps.terms[i].col = term_cols[i].col;
+    }
+    for (int i = 0; i < ps.nprobes; ++i)
+      if (!col_index(ps.probes[i].key)) return false;
+    for (int a = 0; a < ps.nacc; ++a)
+      for (int i = 0; i < ps.acc[a].nf; ++i)
+        if (ps.acc[a].f[i].kind != FK_CONST && !col_index(ps.acc[a].f[i].x)) return false;
+    for (int i = 0; i < ps.nkeys; ++i)
+      if (!col_index(ps.keys[i])) return false;
+    for (int i = 0; i < ts.ncols; ++i) {
+      ts.col_off[i] = ts.stage_bytes;
+      ts.stage_bytes += (kTileRows * ts.col_w[i] + 127) & ~127;  // 128 B aligned columns
+    }
+    if (ts.stage_bytes == 0) ts.stage_bytes = 128;
+    // as many stages as fit next to the fixed (static + staging) parts
+    int optin = 0;
+    TQP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    cudaFuncAttributes fa{};
+    size_t fixed = 0;
+    if (P.mode == MODE_SCALAR) {
+      fixed = tile_smem_bytes<MODE_SCALAR>(0, 0);
+      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_SCALAR>));
+    } else if (P.mode == MODE_SMALL) {
+      fixed = tile_smem_bytes<MODE_SMALL>(0, 0);
+      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_SMALL>));
+    } else {
+      fixed = tile_smem_bytes<MODE_BUILDGRP>(0, 0);
+      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_BUILDGRP>));
+    }
+    const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
+    if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
+    ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
+    const size_t smem = fixed + static_cast<size_t>(ts.stages) * ts.stage_bytes;
+    auto launch_tile = [&](auto kernel, int threads, int grid_) {
+      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) {
+        throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + " setting " + std::to_string(smem) +
+                                      " B dynamic smem (static " + std::to_string(fa.sharedSizeBytes) + ", optin " +
+                                      std::to_string(optin) + ", stages " + std::to_string(ts.stages) + ")");
+      }
+      ts.p = ps;
+      kernel<<<grid_, threads, smem, c.stream>>>(ts);
+      TQP_CUDA(cudaGetLastError());
+      c.count_launch();
+    };
+
     FinalSpec fs;
     fs.nacc = ps.nacc;
     for (int a = 0; a < ps.nacc; ++a) fs.acc_is_int[a] = ps.acc[a].is_int;
@@ -1451,7 +1671,7 @@ struct Runner {
     if (fs.nouts > 16) return false;
     for (int j = 0; j < fs.nouts; ++j) fs.outs[j] = {P.outs[j].fn, P.outs[j].acc, P.outs[j].is_int ? 1 : 0};
 
-    const int grid = c.num_sms * 4;
+    const int grid = c.num_sms;  // persistent: one CTA per SM
     auto out_dtype = [&](const OutDesc& o) {
       if (o.fn >= 10) return P.mode == MODE_SMALL ? TQP_STR8 : TQP_I64;
       if (o.fn == 1) return TQP_I64;
@@ -1464,19 +1684,19 @@ struct Runner {
     if (P.mode == MODE_SCALAR) {
       auto part = c.alloc_bytes(sizeof(unsigned long long) * grid * (kMaxAcc + 1));
       ps.part = static_cast<unsigned long long*>(part->ptr);
-      k_probe_scalar<<<grid, kThreads, 0, c.stream>>>(ps);
+      launch_tile(k_tile<MODE_SCALAR>, TileShape<MODE_SCALAR>::THREADS, grid);
       for (size_t j = 0; j < outs.size(); ++j) {
         outs[j] = c.alloc(out_dtype(P.outs[j]), 1, 1);
         fs.out_ptr[j] = outs[j].data();
       }
       k_final_scalar<<<1, 32, 0, c.stream>>>(ps.part, grid, fs, err);
-      c.count_launch(2);
+      c.count_launch();
       nrows = 1;
     } else if (P.mode == MODE_SMALL) {
-      const int g2 = c.num_sms * 2;
+      const int g2 = grid;
       auto part = c.alloc_bytes(sizeof(SmallPart) * g2);
       ps.part = static_cast<unsigned long long*>(part->ptr);
-      k_probe_small<<<g2, kThreads, 0, c.stream>>>(ps);
+      launch_tile(k_tile<MODE_SMALL>, TileShape<MODE_SMALL>::THREADS, g2);
       auto inv = c.alloc_bytes(sizeof(int) * g2 * kMerged);
       auto ng = c.alloc_bytes(8);
       std::vector<Tensor> tmp(P.outs.size());
@@ -1490,7 +1710,7 @@ struct Runner {
       k_final_small<<<1, kThreads, 0, c.stream>>>(reinterpret_cast<SmallPart*>(part->ptr), g2, fs, ps.nkeys, kp[0], kp[1],
                                                   kp[2], kp[3], static_cast<int*>(inv->ptr),
                                                   static_cast<long long*>(ng->ptr), err);
-      c.count_launch(2);
+      c.count_launch();
       TQP_CUDA(cudaMemcpyAsync(&nrows, ng->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
       for (size_t j = 0; j < outs.size(); ++j) {
@@ -1507,8 +1727,7 @@ struct Runner {
       ps.gacc = static_cast<unsigned long long*>(gacc->ptr);
       ps.gcnt = static_cast<unsigned long long*>(gcnt->ptr);
       ps.group_probe = P.group_probe;
-      k_probe_buildgrp<<<grid, kThreads, 0, c.stream>>>(ps);
-      c.count_launch();
+      launch_tile(k_tile<MODE_BUILDGRP>, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
       gs.f = fs;
       gs.gacc = ps.gacc;
@@ -1535,12 +1754,33 @@ struct Runner {
           tmp[j] = c.alloc(out_dtype(P.outs[j]), std::max(1, k), 1);
           gs.f.out_ptr[j] = tmp[j].data();
         }
-        const int tg = c.num_sms;
-        auto cand = c.alloc_bytes(sizeof(unsigned) * tg * std::max(1, k));
+        const int nk = gs.nsort + gs.nkeyc;
+        auto cgid = c.alloc_bytes(sizeof(unsigned) * (ngroups + 1));
+        auto ckey = c.alloc_bytes(sizeof(unsigned long long) * nk * (ngroups + 1));
+        auto ncb = c.alloc_bytes(8);
+        TQP_CUDA(cudaMemsetAsync(ncb->ptr, 0, 8, c.stream));
+        if (ngroups) {
+          k_topk_cands<<<c.grid_for(ngroups, kThreads, 1, 4), kThreads, 0, c.stream>>>(
+              gs, ngroups, static_cast<unsigned*>(cgid->ptr), static_cast<unsigned long long*>(ckey->ptr),
+              static_cast<unsigned*>(ncb->ptr));
+          c.count_launch();
+        }
+        unsigned ncand = 0;
+        TQP_CUDA(cudaMemcpyAsync(&ncand, ncb->ptr, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        const long long chunk = static_cast<long long>(kThreads) * 16;
+        const long long nblk = (static_cast<long long>(ncand) + chunk - 1) / chunk;
+        const long long nwin = nblk * k;
+        if (nwin > static_cast<long long>(kThreads) * kTopkMaxPerThread) return false;
+        auto win = c.alloc_bytes(sizeof(long long) * std::max<long long>(1, nwin));
+        auto scratch = c.alloc_bytes(sizeof(unsigned long long) * nk * std::max<long long>(1, nwin));
         auto nout = c.alloc_bytes(8);
-        if (k > 0) {
-          k_topk_local<<<tg, kThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned*>(cand->ptr));
-          k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned*>(cand->ptr), static_cast<long long>(tg) * k, k,
+        if (k > 0 && ncand > 0) {
+          k_topk_local<<<nblk, kThreads, 0, c.stream>>>(static_cast<unsigned long long*>(ckey->ptr), nk, ncand, chunk, k,
+                                                       static_cast<long long*>(win->ptr));
+          k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned long long*>(ckey->ptr),
+                                                     static_cast<unsigned*>(cgid->ptr), static_cast<long long*>(win->ptr),
+                                                     nwin, k, static_cast<unsigned long long*>(scratch->ptr),
                                                      static_cast<long long*>(nout->ptr), err);
           c.count_launch(2);
           TQP_CUDA(cudaMemcpyAsync(&nrows, nout->ptr, 8, cudaMemcpyDeviceToHost, c.stream));

@@ -31,7 +31,9 @@ constexpr int kMaxFactors = 4;
 constexpr int kMaxKeys = 4;
 constexpr int kMaxStrTerms = 4;
 constexpr int kMaxFlags = 7;
-constexpr int kGroups = 64;  // MODE_SMALL per-CTA slot capacity
+constexpr int kGroups = 8;  // MODE_SMALL per-CTA slot capacity (register accumulators)
+constexpr int kGroupBits = 3;
+constexpr int kMaxAccSmall = 6;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
@@ -46,6 +48,7 @@ struct Operand {
   const void* ptr = nullptr;
   int type = OT_I64;
   int src = -1;
+  int col = -1;  // fact operands: column index in the staged tile
 };
 
 struct Term {
@@ -91,12 +94,39 @@ struct Probe {
   long long kmin = 0;
   long long range = 0;
   const unsigned long long* table = nullptr;
+  const unsigned* bitmap = nullptr;  // presence bits (L2-resident filter)
 };
+
+// Branch-free predicate term for the fact scan: all compares on one column
+// are merged into lo <= x <= hi (int64: one unsigned compare; fp64: two
+// compares, NaN fails both exactly as the reference's `<`/`>` do).
+enum RangeKind : int { RK_INT = 0, RK_F64 = 1, RK_INT_NE = 2, RK_F64_NE = 3, RK_TRUE = 4, RK_FALSE = 5 };
+struct RTerm {
+  int col = -1;
+  int kind = RK_TRUE;
+  unsigned long long lo = 0, hi = 0;  // bit patterns (int64 or fp64)
+};
+
+__device__ __forceinline__ bool eval_rterm(const RTerm& t, unsigned long long x) {
+  switch (t.kind) {
+    case RK_INT: return x - t.lo <= t.hi - t.lo;
+    case RK_F64: {
+      double d = __longlong_as_double(static_cast<long long>(x));
+      return d >= __longlong_as_double(static_cast<long long>(t.lo)) &&
+             d <= __longlong_as_double(static_cast<long long>(t.hi));
+    }
+    case RK_INT_NE: return x != t.lo;
+    case RK_F64_NE:
+      return __longlong_as_double(static_cast<long long>(x)) != __longlong_as_double(static_cast<long long>(t.lo));
+    case RK_TRUE: return true;
+    default: return false;
+  }
+}
 
 struct ProbeSpec {
   long long n = 0;
   int nterms = 0;
-  Term terms[kMaxTerms];
+  RTerm terms[kMaxTerms];
   int nprobes = 0;
   Probe probes[kMaxProbes];
   int nacc = 0;
@@ -125,6 +155,7 @@ struct BuildSpec {
   long long kmin = 0;
   long long range = 0;
   unsigned long long* table = nullptr;
+  unsigned* bitmap = nullptr;
   int assign_groups = 0;
   unsigned int* group_counter = nullptr;
   int* group_row = nullptr;
@@ -233,6 +264,7 @@ __device__ __forceinline__ bool probe_lookup(const Probe& p, long long key, long
                                              unsigned& gid) {
   long long idx = key - p.kmin;
   if (idx < 0 || idx >= p.range) return false;
+  if (p.bitmap && !((__ldg(p.bitmap + (idx >> 5)) >> (idx & 31)) & 1u)) return false;
   unsigned long long e = __ldg(p.table + idx);
   if (!e) return false;
   rid = static_cast<long long>(e & 0xffffffffULL) - 1;
@@ -329,397 +361,472 @@ __global__ void k_minmax(const long long* __restrict__ k, long long n, long long
 }
 
 __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
-  for (long long r = gtid(); r < s.n; r += gstride()) {
-    bool pass = true;
-#pragma unroll
-    for (int t = 0; t < kMaxTerms; ++t)
-      if (t < s.nterms && pass) pass = eval_term(s.terms[t], ld_row(s.terms[t].x, r));
-#pragma unroll
-    for (int t = 0; t < kMaxStrTerms; ++t)
-      if (t < s.nstr && pass) pass = eval_str(s.str[t], r);
-#pragma unroll
-    for (int p = 0; p < kMaxProbes; ++p) {
-      if (p < s.nprobes && pass) {
-        long long rid;
-        unsigned fl, g;
-        pass = probe_lookup(s.probes[p], static_cast<long long>(ld_row(s.probes[p].key, r)), rid, fl, g);
-      }
-    }
-    if (!pass) continue;
-    unsigned flags = 0;
-#pragma unroll
-    for (int f = 0; f < kMaxFlags; ++f)
-      if (f < s.nflags && eval_str(s.flags[f], r)) flags |= 1u << f;
-    long long key = static_cast<long long>(ld_row(s.key, r));
-    long long idx = key - s.kmin;
-    if (idx < 0 || idx >= s.range) {
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-      continue;
+  const int lane = threadIdx.x & 31;
+  for (long long base = gtid() & ~31LL; base < s.n; base += gstride()) {
+    const long long r = base + lane;
+    bool pass = r < s.n;
+    for (int t = 0; t < s.nterms && pass; ++t) pass = eval_term(s.terms[t], ld_row(s.terms[t].x, r));
+    for (int t = 0; t < s.nstr && pass; ++t) pass = eval_str(s.str[t], r);
+    for (int p = 0; p < s.nprobes && pass; ++p) {
+      long long rid;
+      unsigned fl, g;
+      pass = probe_lookup(s.probes[p], static_cast<long long>(ld_row(s.probes[p].key, r)), rid, fl, g);
     }
     unsigned gid = 0;
     if (s.assign_groups) {
-      gid = atomicAdd(s.group_counter, 1u);
-      if (gid >= (1u << 25)) {
-        atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-        continue;
-      }
-      s.group_row[gid] = static_cast<int>(r);
+      // warp-aggregated group-id allocation: one atomic per warp
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      unsigned first = 0;
+      if (lane == 0 && m) first = atomicAdd(s.group_counter, static_cast<unsigned>(__popc(m)));
+      first = __shfl_sync(0xffffffffu, first, 0);
+      gid = first + __popc(m & ((1u << lane) - 1u));
     }
-    unsigned long long e = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(gid) << 32) |
-                           (static_cast<unsigned long long>(flags) << 57);
+    if (!pass) continue;
+    unsigned flags = 0;
+    for (int f = 0; f < s.nflags; ++f)
+      if (eval_str(s.flags[f], r)) flags |= 1u << f;
+    const long long key = static_cast<long long>(ld_row(s.key, r));
+    const long long idx = key - s.kmin;
+    if (idx < 0 || idx >= s.range || gid >= (1u << 25)) {
+      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+      continue;
+    }
+    if (s.assign_groups) s.group_row[gid] = static_cast<int>(r);
+    const unsigned long long e = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(gid) << 32) |
+                                 (static_cast<unsigned long long>(flags) << 57);
     if (atomicCAS(s.table + idx, 0ULL, e) != 0ULL) {
       // duplicate build key: the join is 1:N, outside the fused contract
       atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
     }
+    atomicOr(s.bitmap + (idx >> 5), 1u << (idx & 31));
   }
 }
 
-// ---- probe + aggregate kernel ------------------------------------------------
-// per row: predicate, probes; returns pass and fills rc
-__device__ __forceinline__ void row_filter_probe(const ProbeSpec& s, const unsigned long long (*tv)[2], long long row0,
-                                                 bool pass[2], RowCtx rc[2]) {
-#pragma unroll
-  for (int t = 0; t < kMaxTerms; ++t) {
-    if (t < s.nterms) {
-      pass[0] = pass[0] && eval_term(s.terms[t], tv[t][0]);
-      pass[1] = pass[1] && eval_term(s.terms[t], tv[t][1]);
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < kMaxProbes; ++p) {
-    if (p < s.nprobes && (pass[0] || pass[1])) {
-      unsigned long long k0, k1;
-      ld_pair(s.probes[p].key, row0, k0, k1);
-      if (pass[0]) pass[0] = probe_lookup(s.probes[p], static_cast<long long>(k0), rc[0].rid[p], rc[0].flags[p], rc[0].gid[p]);
-      if (pass[1]) pass[1] = probe_lookup(s.probes[p], static_cast<long long>(k1), rc[1].rid[p], rc[1].flags[p], rc[1].gid[p]);
-    }
+// ---- TMA-staged, warp-specialised tile pipeline for the fact scan -----------
+// A persistent CTA per SM streams tiles of kTileRows rows. Warp 0 is the
+// producer: one lane issues, for every distinct fact column, a 1-D bulk async
+// copy (cp.async.bulk.shared::cluster.global -> SASS UBLKCP) of the tile into
+// a multi-stage shared-memory ring, signalling a `full` mbarrier with the
+// expected transaction bytes. Warps 1..16 consume: wait on `full`, evaluate
+// their rows, arrive on the stage's `empty` mbarrier. There is no CTA-wide
+// barrier per tile, ~100-190 KB per SM stay in flight independent of register
+// use, and operands are addressed by runtime column index in shared memory.
+// Predicates, probes and accumulator expressions run as compact runtime
+// loops whose dispatch is amortised over the rows each thread owns.
+constexpr int kTileRows = 2048;  // 16 KB bulk copies per 8-byte column
+constexpr int kMaxStages = 8;
+constexpr int kMaxCols = 10;
+
+// consumer warps per mode (+1 producer warp): small-group keeps 48 register
+// accumulators per thread, so it runs fewer, wider threads
+template <int MODE>
+struct TileShape {
+  static constexpr int CW = MODE == MODE_SMALL ? 8 : 16;
+  static constexpr int CT = CW * 32;
+  static constexpr int THREADS = CT + 32;
+  static constexpr int R = kTileRows / CT;  // rows per consumer thread
+  static constexpr int SUB = MODE == MODE_SMALL ? 4 : R;  // staged rows per pass
+};
+
+struct TileSpec {
+  ProbeSpec p;
+  int ncols = 0;
+  const unsigned char* col_ptr[kMaxCols];
+  int col_w[kMaxCols];
+  int col_off[kMaxCols];  // byte offset of the column inside a stage
+  int stage_bytes = 0;
+  int stages = 3;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* stage, unsigned long long* bar,
+                                           long long tile) {
+  const long long row0 = tile * kTileRows;
+  long long rows = t.p.n - row0;
+  if (rows > kTileRows) rows = kTileRows;
+  unsigned total = 0;
+  for (int c = 0; c < t.ncols; ++c) total += static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
+  mbar_expect_tx(bar, total);
+  for (int c = 0; c < t.ncols; ++c) {
+    unsigned bytes = static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
+    bulk_g2s(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar);
   }
 }
 
-__device__ __forceinline__ void load_terms(const ProbeSpec& s, long long row0, unsigned long long (*tv)[2]) {
-#pragma unroll
-  for (int t = 0; t < kMaxTerms; ++t)
-    if (t < s.nterms && s.terms[t].kind <= TK_F64) ld_pair(s.terms[t].x, row0, tv[t][0], tv[t][1]);
+__device__ __forceinline__ unsigned long long add_acc(bool is_int, unsigned long long a, unsigned long long b) {
+  if (is_int) return static_cast<unsigned long long>(static_cast<long long>(a) + static_cast<long long>(b));
+  return static_cast<unsigned long long>(__double_as_longlong(
+      __dadd_rn(__longlong_as_double(static_cast<long long>(a)), __longlong_as_double(static_cast<long long>(b)))));
 }
 
-// fact operands of accumulator a for both rows
-__device__ __forceinline__ void load_acc_operands(const Acc& a, long long row0, unsigned long long (*fv)[kMaxFactors]) {
-#pragma unroll
-  for (int i = 0; i < kMaxFactors; ++i) {
-    if (i < (a.is_int ? 1 : a.nf) && a.f[i].x.src < 0 && a.f[i].kind != FK_CONST) {
-      ld_pair(a.f[i].x, row0, fv[0][i], fv[1][i]);
-    } else {
-      fv[0][i] = fv[1][i] = 0;
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ T shfl_xor_u64(T v, int o) {
-  return __shfl_xor_sync(0xffffffffu, v, o);
-}
-
-__global__ void __launch_bounds__(kThreads) k_probe_scalar(const ProbeSpec s) {
-  __shared__ unsigned long long s_part[kWarps][kMaxAcc + 1];
-  unsigned long long acc[kMaxAcc];
-  long long absmax[kMaxAcc];
-#pragma unroll
-  for (int a = 0; a < kMaxAcc; ++a) {
-    acc[a] = 0;  // 0.0 and 0 share the bit pattern
-    absmax[a] = 0;
-  }
-  long long cnt = 0;
-  const long long npairs = (s.n + 1) / 2;
-  for (long long q = gtid(); q < npairs; q += gstride()) {
-    const long long row0 = 2 * q;
-    bool pass[2] = {true, row0 + 1 < s.n};
-    unsigned long long tv[kMaxTerms][2];
-    load_terms(s, row0, tv);
-    RowCtx rc[2];
-    row_filter_probe(s, tv, row0, pass, rc);
-    if (!pass[0] && !pass[1]) continue;
-#pragma unroll
-    for (int a = 0; a < kMaxAcc; ++a) {
-      if (a < s.nacc) {
-        unsigned long long fv[2][kMaxFactors];
-        load_acc_operands(s.acc[a], row0, fv);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          if (!pass[r]) continue;
-          unsigned long long v = eval_acc(s.acc[a], fv[r], rc[r]);
-          if (s.acc[a].is_int) {
-            long long iv = static_cast<long long>(v);
-            acc[a] = static_cast<unsigned long long>(static_cast<long long>(acc[a]) + iv);
-            long long av = iv < 0 ? -iv : iv;
-            absmax[a] = av > absmax[a] ? av : absmax[a];
-          } else {
-            acc[a] = static_cast<unsigned long long>(
-                __double_as_longlong(__dadd_rn(__longlong_as_double(static_cast<long long>(acc[a])),
-                                               __longlong_as_double(static_cast<long long>(v)))));
-          }
-        }
-      }
-    }
-    cnt += (pass[0] ? 1 : 0) + (pass[1] ? 1 : 0);
-  }
-  // fixed-order warp tree, then warps in order
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int a = 0; a < kMaxAcc; ++a) {
-    if (a < s.nacc) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long y = shfl_xor_u64(acc[a], o);
-        long long am = shfl_xor_u64(absmax[a], o);
-        absmax[a] = am > absmax[a] ? am : absmax[a];
-        if (s.acc[a].is_int) {
-          acc[a] = static_cast<unsigned long long>(static_cast<long long>(acc[a]) + static_cast<long long>(y));
-        } else {
-          acc[a] = static_cast<unsigned long long>(__double_as_longlong(
-              __dadd_rn(__longlong_as_double(static_cast<long long>(acc[a])), __longlong_as_double(static_cast<long long>(y)))));
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) {
-#pragma unroll
-    for (int a = 0; a < kMaxAcc; ++a)
-      if (a < s.nacc) s_part[warp][a] = acc[a];
-    s_part[warp][kMaxAcc] = static_cast<unsigned long long>(cnt);
-    // int64 sums may not be exact if |v| * count can reach 2^63 (the
-    // reference errors on the first overflowing prefix): hand over to the
-    // exact per-instruction path
-#pragma unroll
-    for (int a = 0; a < kMaxAcc; ++a) {
-      if (a < s.nacc && s.acc[a].is_int && absmax[a] > 0 && cnt > 0 &&
-          static_cast<double>(absmax[a]) * static_cast<double>(s.n) >= 9.0e18) {
-        atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long* out = s.part + static_cast<long long>(blockIdx.x) * (kMaxAcc + 1);
-    for (int a = 0; a < s.nacc; ++a) {
-      unsigned long long t = s_part[0][a];
-      for (int w = 1; w < kWarps; ++w) {
-        if (s.acc[a].is_int) {
-          t = static_cast<unsigned long long>(static_cast<long long>(t) + static_cast<long long>(s_part[w][a]));
-        } else {
-          t = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(
-              __longlong_as_double(static_cast<long long>(t)), __longlong_as_double(static_cast<long long>(s_part[w][a])))));
-        }
-      }
-      out[a] = t;
-    }
-    unsigned long long c = 0;
-    for (int w = 0; w < kWarps; ++w) c += s_part[w][kMaxAcc];
-    out[kMaxAcc] = c;
-  }
-}
-
-// MODE_SMALL: per-CTA hash of group codes -> slot, per-warp accumulators.
-struct SmallPart {  // per CTA, in global memory
-  unsigned int ncodes;
+struct SmallPart {  // MODE_SMALL per-CTA partial, in global memory
   unsigned int codes[kGroups];
   unsigned long long cnt[kGroups];
   unsigned long long acc[kGroups][kMaxAcc];
 };
 
-__device__ __forceinline__ unsigned hash_code(unsigned c) { return (c * 2654435761u) >> 26; }  // 6 bits
+__device__ __forceinline__ unsigned hash_code(unsigned c) { return (c * 2654435761u) >> (32 - kGroupBits); }
 
-__global__ void __launch_bounds__(kThreads) k_probe_small(const ProbeSpec s) {
-  __shared__ unsigned int s_codes[kGroups];
-  __shared__ unsigned long long s_acc[kWarps][kGroups][kMaxAcc];
-  __shared__ unsigned long long s_cnt[kWarps][kGroups];
-  __shared__ int s_overflow;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kGroups; i += blockDim.x) s_codes[i] = 0xffffffffu;
-  for (int i = threadIdx.x; i < kWarps * kGroups * kMaxAcc; i += blockDim.x) (&s_acc[0][0][0])[i] = 0;
-  for (int i = threadIdx.x; i < kWarps * kGroups; i += blockDim.x) (&s_cnt[0][0])[i] = 0;
-  if (threadIdx.x == 0) s_overflow = 0;
-  __syncthreads();
-  long long absmax[kMaxAcc];
-#pragma unroll
-  for (int a = 0; a < kMaxAcc; ++a) absmax[a] = 0;
+template <int MODE>
+__host__ __device__ constexpr size_t stage_val_bytes() {
+  using S = TileShape<MODE>;
+  return MODE == MODE_SMALL ? sizeof(unsigned long long) * kMaxAccSmall * S::SUB * S::CT
+                            : MODE == MODE_SCALAR ? sizeof(unsigned long long) * kMaxAcc * S::CT : 0;
+}
 
-  const long long npairs = (s.n + 1) / 2;
-  const long long wstride = gstride();
-  // warp-uniform trip count
-  for (long long base = (gtid() & ~31LL); base < npairs; base += wstride) {
-    const long long q = base + lane;
-    const long long row0 = 2 * q;
-    bool pass[2] = {q < npairs, q < npairs && row0 + 1 < s.n};
-    unsigned long long tv[kMaxTerms][2];
-    RowCtx rc[2];
-    if (pass[0]) {
-      load_terms(s, row0, tv);
-      row_filter_probe(s, tv, row0, pass, rc);
+// value of accumulator `ac` for rows k0..k0+N-1 of this thread (row index
+// k * CT + ct inside the tile); operands from the staged tile
+template <int CT, int N>
+__device__ __forceinline__ void acc_rows(const TileSpec& t, const unsigned char* stage, const Acc& ac, const bool* pass,
+                                         const RowCtx* rc, int ct, int k0, unsigned long long* v) {
+  if (ac.is_int) {
+    const Operand& o = ac.f[0].x;
+    const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[o.col < 0 ? 0 : o.col]);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      v[k] = 0;
+      if (pass[k0 + k]) v[k] = o.src < 0 ? col[(k0 + k) * CT + ct] : ld_row(o, rc[k0 + k].rid[o.src]);
     }
-    // group codes (big-endian over the key bytes: numeric order = key order)
-    unsigned code[2] = {0, 0};
+    return;
+  }
+  double d[N];
+  for (int i = 0; i < ac.nf; ++i) {
+    const Factor f = ac.f[i];
+    const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[f.x.col < 0 ? 0 : f.x.col]);
+    double xs[N];
 #pragma unroll
-    for (int k = 0; k < kMaxKeys; ++k) {
-      if (k < s.nkeys && (pass[0] || pass[1])) {
-        unsigned long long b0, b1;
-        ld_pair(s.keys[k], row0, b0, b1);
-        code[0] = (code[0] << 8) | static_cast<unsigned>(b0);
-        code[1] = (code[1] << 8) | static_cast<unsigned>(b1);
-      }
-    }
-    unsigned long long val[2][kMaxAcc];
-#pragma unroll
-    for (int a = 0; a < kMaxAcc; ++a) {
-      if (a < s.nacc) {
-        unsigned long long fv[2][kMaxFactors];
-        if (pass[0] || pass[1]) load_acc_operands(s.acc[a], row0, fv);
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          val[r][a] = pass[r] ? eval_acc(s.acc[a], fv[r], rc[r]) : 0ULL;
-          if (pass[r] && s.acc[a].is_int) {
-            long long iv = static_cast<long long>(val[r][a]);
-            iv = iv < 0 ? -iv : iv;
-            absmax[a] = iv > absmax[a] ? iv : absmax[a];
-          }
-        }
+    for (int k = 0; k < N; ++k) {
+      xs[k] = 0.0;
+      if (f.kind != FK_CONST && pass[k0 + k]) {
+        unsigned long long raw = f.x.src < 0 ? col[(k0 + k) * CT + ct] : ld_row(f.x, rc[k0 + k].rid[f.x.src]);
+        xs[k] = __longlong_as_double(static_cast<long long>(raw));
       }
     }
+    // one uniform dispatch per factor, straight-line over the rows
+    switch (f.kind) {
+      case FK_X:
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      // slot lookup / insert
-      int slot = -1;
-      if (pass[r]) {
-        unsigned h = hash_code(code[r]);
-        for (int probe = 0; probe < kGroups; ++probe) {
-          unsigned cur = s_codes[h];
-          if (cur == code[r]) {
-            slot = static_cast<int>(h);
-            break;
-          }
-          if (cur == 0xffffffffu) {
-            unsigned prev = atomicCAS(&s_codes[h], 0xffffffffu, code[r]);
-            if (prev == 0xffffffffu || prev == code[r]) {
-              slot = static_cast<int>(h);
-              break;
-            }
-          }
-          h = (h + 1) & (kGroups - 1);
-        }
-        if (slot < 0) s_overflow = 1;
-      }
-      // ballot loop over the distinct slots present in this warp batch
-      unsigned todo = __ballot_sync(0xffffffffu, slot >= 0);
-      while (todo) {
-        const int leader = __ffs(todo) - 1;
-        const int sl = __shfl_sync(0xffffffffu, slot, leader);
-        const bool mine = slot == sl;
-        const unsigned members = __ballot_sync(0xffffffffu, mine);
+        for (int k = 0; k < N; ++k) d[k] = i == 0 ? xs[k] : __dmul_rn(d[k], xs[k]);
+        break;
+      case FK_K_MINUS_X:
 #pragma unroll
-        for (int a = 0; a < kMaxAcc; ++a) {
-          if (a < s.nacc) {
-            unsigned long long x = mine ? val[r][a] : 0ULL;  // 0.0 == bits 0
+        for (int k = 0; k < N; ++k) d[k] = i == 0 ? __dsub_rn(f.k, xs[k]) : __dmul_rn(d[k], __dsub_rn(f.k, xs[k]));
+        break;
+      case FK_K_PLUS_X:
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-              if (s.acc[a].is_int) {
-                x = static_cast<unsigned long long>(static_cast<long long>(x) + static_cast<long long>(y));
-              } else {
-                x = static_cast<unsigned long long>(__double_as_longlong(
-                    __dadd_rn(__longlong_as_double(static_cast<long long>(x)), __longlong_as_double(static_cast<long long>(y)))));
-              }
-            }
-            if (lane == 0) {
-              unsigned long long& dst = s_acc[warp][sl][a];
-              if (s.acc[a].is_int) {
-                dst = static_cast<unsigned long long>(static_cast<long long>(dst) + static_cast<long long>(x));
-              } else {
-                dst = static_cast<unsigned long long>(__double_as_longlong(
-                    __dadd_rn(__longlong_as_double(static_cast<long long>(dst)), __longlong_as_double(static_cast<long long>(x)))));
-              }
-            }
-          }
-        }
-        if (lane == 0) s_cnt[warp][sl] += __popc(members);
-        todo &= ~members;
-      }
+        for (int k = 0; k < N; ++k) d[k] = i == 0 ? __dadd_rn(f.k, xs[k]) : __dmul_rn(d[k], __dadd_rn(f.k, xs[k]));
+        break;
+      default:
+#pragma unroll
+        for (int k = 0; k < N; ++k) d[k] = i == 0 ? apply_factor(f, xs[k]) : __dmul_rn(d[k], apply_factor(f, xs[k]));
+        break;
     }
   }
-  // int64 exactness guard (see k_probe_scalar)
 #pragma unroll
-  for (int a = 0; a < kMaxAcc; ++a) {
-    if (a < s.nacc && s.acc[a].is_int && static_cast<double>(absmax[a]) * static_cast<double>(s.n) >= 9.0e18) {
+  for (int k = 0; k < N; ++k) {
+    if (pass[k0 + k] && ac.gate_probe >= 0 && !((rc[k0 + k].flags[ac.gate_probe] >> ac.gate_bit) & 1u))
+      d[k] = ac.gate_else;
+    v[k] = pass[k0 + k] ? static_cast<unsigned long long>(__double_as_longlong(d[k])) : 0ULL;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const TileSpec t) {
+  using S = TileShape<MODE>;
+  constexpr int CW = S::CW, CT = S::CT, R = S::R, SUB = S::SUB;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned long long s_wred[MODE == MODE_SMALL ? kGroups : 1][kMaxAcc + 1][CW];
+  __shared__ unsigned int s_codes[kGroups];
+  __shared__ int s_overflow;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* empty = full + kMaxStages;
+  // per-thread staging (SCALAR: running sums; SMALL: row values), then stages
+  unsigned long long* s_stage_val = reinterpret_cast<unsigned long long*>(smem + 256);
+  unsigned char* stages = smem + 256 + stage_val_bytes<MODE>();
+  const ProbeSpec& s = t.p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long ntiles = (s.n + kTileRows - 1) / kTileRows;
+  const int nst = t.stages;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_overflow = 0;
+  }
+  if (threadIdx.x < kGroups) s_codes[threadIdx.x] = 0xffffffffu;
+  for (int i = threadIdx.x; i < static_cast<int>(stage_val_bytes<MODE>() / 8); i += blockDim.x) s_stage_val[i] = 0;
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- producer: one lane streams tiles into the ring ----
+    if (lane == 0) {
+      long long it = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int st = static_cast<int>(it % nst);
+        if (it >= nst) mbar_wait(&empty[st], static_cast<unsigned>(((it / nst) - 1) & 1));
+        issue_tile(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
+      }
+    }
+  } else {
+    // ---- consumers ----
+    const int ct = threadIdx.x - 32;
+    const int cw = warp - 1;
+    constexpr int NA = MODE == MODE_SMALL ? kMaxAccSmall : kMaxAcc;
+    constexpr int NG = MODE == MODE_SMALL ? kGroups : 1;
+    unsigned long long acc[NG][NA];
+    unsigned int gcnt_local[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      gcnt_local[g] = 0;
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[g][a] = 0;  // 0.0 and 0 share bits
+    }
+    long long absmax = 0;  // int accumulators: exactness guard
+    long long it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int st = static_cast<int>(it % nst);
+      const unsigned char* stage = stages + static_cast<size_t>(st) * t.stage_bytes;
+      mbar_wait(&full[st], static_cast<unsigned>((it / nst) & 1));
+      const long long row0 = tile * kTileRows;
+      bool pass[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) pass[k] = row0 + k * CT + ct < s.n;
+      // predicate: one uniform dispatch per term, straight-line over rows
+      for (int i = 0; i < s.nterms; ++i) {
+        const RTerm tm = s.terms[i];
+        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[tm.col < 0 ? 0 : tm.col]);
+        if (tm.kind == RK_INT) {
+          const unsigned long long span = tm.hi - tm.lo;
+#pragma unroll
+          for (int k = 0; k < R; ++k) pass[k] = pass[k] && (col[k * CT + ct] - tm.lo <= span);
+        } else if (tm.kind == RK_F64) {
+          const double lo = __longlong_as_double(static_cast<long long>(tm.lo));
+          const double hi = __longlong_as_double(static_cast<long long>(tm.hi));
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const double x = __longlong_as_double(static_cast<long long>(col[k * CT + ct]));
+            pass[k] = pass[k] && x >= lo && x <= hi;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            pass[k] = pass[k] && eval_rterm(tm, tm.kind <= RK_F64_NE ? col[k * CT + ct] : 0ULL);
+        }
+      }
+      RowCtx rc[R];
+      for (int p = 0; p < s.nprobes; ++p) {
+        const Probe& pr = s.probes[p];
+        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[pr.key.col]);
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+          if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p]);
+      }
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < R; ++k) any = any || pass[k];
+      if (any) {
+        int slot[R];
+        if constexpr (MODE == MODE_SMALL) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            slot[k] = -1;
+            if (!pass[k]) continue;
+            unsigned code = 0;
+            for (int q = 0; q < s.nkeys; ++q) code = (code << 8) | stage[t.col_off[s.keys[q].col] + k * CT + ct];
+            unsigned h = hash_code(code);
+            for (int probe = 0; probe < kGroups; ++probe) {
+              unsigned cur = s_codes[h];
+              if (cur == code) {
+                slot[k] = static_cast<int>(h);
+                break;
+              }
+              if (cur == 0xffffffffu) {
+                unsigned prev = atomicCAS(&s_codes[h], 0xffffffffu, code);
+                if (prev == 0xffffffffu || prev == code) {
+                  slot[k] = static_cast<int>(h);
+                  break;
+                }
+              }
+              h = (h + 1) & (kGroups - 1);
+            }
+            if (slot[k] < 0) {
+              s_overflow = 1;
+              pass[k] = false;
+            }
+#pragma unroll
+            for (int g = 0; g < NG; ++g) gcnt_local[g] += slot[k] == g ? 1u : 0u;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < R; ++k) gcnt_local[0] += pass[k] ? 1u : 0u;
+        }
+        unsigned g[R];
+        if constexpr (MODE == MODE_BUILDGRP) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            g[k] = pass[k] ? rc[k].gid[s.group_probe] : 0u;
+            if (pass[k]) atomicAdd(s.gcnt + g[k], 1ULL);
+          }
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < R; k0 += SUB) {
+          // values: one runtime loop over the accumulators (code inlined once)
+          for (int a = 0; a < s.nacc; ++a) {
+            const bool is_int = s.acc[a].is_int;
+            unsigned long long v[SUB];
+            acc_rows<CT, SUB>(t, stage, s.acc[a], pass, rc, ct, k0, v);
+            if (is_int) {
+#pragma unroll
+              for (int k = 0; k < SUB; ++k) {
+                long long iv = static_cast<long long>(v[k]);
+                iv = iv < 0 ? -iv : iv;
+                absmax = iv > absmax ? iv : absmax;
+              }
+            }
+            if constexpr (MODE == MODE_SCALAR) {
+              unsigned long long sum = s_stage_val[a * CT + ct];
+#pragma unroll
+              for (int k = 0; k < SUB; ++k)
+                if (pass[k0 + k]) sum = add_acc(is_int, sum, v[k]);
+              s_stage_val[a * CT + ct] = sum;
+            } else if constexpr (MODE == MODE_SMALL) {
+#pragma unroll
+              for (int k = 0; k < SUB; ++k) s_stage_val[(a * SUB + k) * CT + ct] = v[k];
+            } else {
+#pragma unroll
+              for (int k = 0; k < SUB; ++k) {
+                if (!pass[k0 + k]) continue;
+                __int128 qv;
+                if (is_int) {
+                  qv = static_cast<__int128>(static_cast<long long>(v[k]));
+                } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k])), qv)) {
+                  atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+                  qv = 0;
+                }
+                atomic_add_q64(s.gacc + (static_cast<long long>(g[k0 + k]) * s.nacc + a) * 2, qv);
+              }
+            }
+          }
+          if constexpr (MODE == MODE_SMALL) {
+            // register accumulators per (group slot, accumulator): masked
+            // adds in a fixed order (x + 0 == x; sums start at +0.0 like the
+            // reference's); a predicated store would be merged by the
+            // compiler into one dynamically indexed (local-memory) access
+#pragma unroll
+            for (int a = 0; a < NA; ++a) {
+              if (a < s.nacc) {
+                const bool is_int = s.acc[a].is_int;
+#pragma unroll
+                for (int k = 0; k < SUB; ++k) {
+                  const unsigned long long v = s_stage_val[(a * SUB + k) * CT + ct];
+#pragma unroll
+                  for (int gg = 0; gg < NG; ++gg)
+                    acc[gg][a] = add_acc(is_int, acc[gg][a], slot[k0 + k] == gg ? v : 0ULL);
+                }
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    // int64 sums are exact only while |v| * rows < 2^63 (the reference
+    // errors on the first overflowing prefix): otherwise the exact path
+    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
       atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
     }
+    if constexpr (MODE == MODE_SCALAR) {
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+        if (a < s.nacc) acc[0][a] = s_stage_val[a * CT + ct];
+    }
+    if constexpr (MODE != MODE_BUILDGRP) {
+      // fixed-order warp trees, one slot per (group, accumulator, warp)
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) {
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          if (a < s.nacc) {
+            unsigned long long x = acc[gg][a];
+            const bool is_int = s.acc[a].is_int;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x = add_acc(is_int, x, __shfl_xor_sync(0xffffffffu, x, o));
+            if (lane == 0) s_wred[gg][a][cw] = x;
+          }
+        }
+        unsigned long long c = gcnt_local[gg];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) s_wred[gg][kMaxAcc][cw] = c;
+      }
+    }
   }
   __syncthreads();
-  if (s_overflow && threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-  // CTA partial: warps merged in warp order
-  SmallPart* out = reinterpret_cast<SmallPart*>(s.part) + blockIdx.x;
-  for (int sl = threadIdx.x; sl < kGroups; sl += blockDim.x) {
-    out->codes[sl] = s_codes[sl];
-    unsigned long long c = 0;
-    for (int w = 0; w < kWarps; ++w) c += s_cnt[w][sl];
-    out->cnt[sl] = c;
-    for (int a = 0; a < s.nacc; ++a) {
-      unsigned long long t = s_acc[0][sl][a];
-      for (int w = 1; w < kWarps; ++w) {
-        if (s.acc[a].is_int) {
-          t = static_cast<unsigned long long>(static_cast<long long>(t) + static_cast<long long>(s_acc[w][sl][a]));
-        } else {
-          t = static_cast<unsigned long long>(__double_as_longlong(__dadd_rn(
-              __longlong_as_double(static_cast<long long>(t)), __longlong_as_double(static_cast<long long>(s_acc[w][sl][a])))));
-        }
+  if constexpr (MODE == MODE_SCALAR) {
+    if (threadIdx.x == 0) {
+      unsigned long long* out = s.part + static_cast<long long>(blockIdx.x) * (kMaxAcc + 1);
+      for (int a = 0; a < s.nacc; ++a) {
+        unsigned long long tot = s_wred[0][a][0];
+        for (int w = 1; w < CW; ++w) tot = add_acc(s.acc[a].is_int, tot, s_wred[0][a][w]);
+        out[a] = tot;
       }
-      out->acc[sl][a] = t;
+      unsigned long long c = 0;
+      for (int w = 0; w < CW; ++w) c += s_wred[0][kMaxAcc][w];
+      out[kMaxAcc] = c;
+    }
+  } else if constexpr (MODE == MODE_SMALL) {
+    if (s_overflow && threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+    SmallPart* out = reinterpret_cast<SmallPart*>(s.part) + blockIdx.x;
+    for (int sl = threadIdx.x; sl < kGroups; sl += blockDim.x) {
+      out->codes[sl] = s_codes[sl];
+      unsigned long long c = 0;
+      for (int w = 0; w < CW; ++w) c += s_wred[sl][kMaxAcc][w];
+      out->cnt[sl] = c;
+      for (int a = 0; a < s.nacc; ++a) {
+        unsigned long long tot = s_wred[sl][a][0];
+        for (int w = 1; w < CW; ++w) tot = add_acc(s.acc[a].is_int, tot, s_wred[sl][a][w]);
+        out->acc[sl][a] = tot;
+      }
     }
   }
 }
 
-// MODE_BUILDGRP: exact fixed-point atomics per matched build row
-__global__ void __launch_bounds__(kThreads) k_probe_buildgrp(const ProbeSpec s) {
-  const long long npairs = (s.n + 1) / 2;
-  for (long long q = gtid(); q < npairs; q += gstride()) {
-    const long long row0 = 2 * q;
-    bool pass[2] = {true, row0 + 1 < s.n};
-    unsigned long long tv[kMaxTerms][2];
-    load_terms(s, row0, tv);
-    RowCtx rc[2];
-    row_filter_probe(s, tv, row0, pass, rc);
-    if (!pass[0] && !pass[1]) continue;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (!pass[r]) continue;
-      const unsigned g = rc[r].gid[s.group_probe];
-      atomicAdd(s.gcnt + g, 1ULL);
-#pragma unroll
-      for (int a = 0; a < kMaxAcc; ++a) {
-        if (a < s.nacc) {
-          unsigned long long fv[kMaxFactors];
-#pragma unroll
-          for (int i = 0; i < kMaxFactors; ++i) {
-            fv[i] = (i < (s.acc[a].is_int ? 1 : s.acc[a].nf) && s.acc[a].f[i].x.src < 0 && s.acc[a].f[i].kind != FK_CONST)
-                        ? ld_row(s.acc[a].f[i].x, row0 + r)
-                        : 0ULL;
-          }
-          unsigned long long v = eval_acc(s.acc[a], fv, rc[r]);
-          unsigned long long* dst = s.gacc + (static_cast<long long>(g) * s.nacc + a) * 2;
-          if (s.acc[a].is_int) {
-            long long iv = static_cast<long long>(v);
-            atomic_add_q64(dst, static_cast<__int128>(iv));
-          } else {
-            __int128 qv;
-            if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v)), qv)) {
-              atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-              qv = 0;
-            }
-            atomic_add_q64(dst, qv);
-          }
-        }
-      }
-    }
-  }
+template <int MODE>
+inline size_t tile_smem_bytes(int stage_bytes, int stages) {
+  return 256 + stage_val_bytes<MODE>() + static_cast<size_t>(stages) * stage_bytes;
 }
 
 }  // namespace fz
