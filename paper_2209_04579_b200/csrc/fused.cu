@@ -1460,6 +1460,18 @@ bool merge_range_terms(const std::vector<Term>& in, ProbeSpec& ps, std::vector<O
   return true;
 }
 
+// k_tile<MODE, NA> instantiation for an accumulator count (nullptr: none)
+const void* tile_kernel(int mode, int nacc) {
+#define TQP_TK(M, N) \
+  if (mode == M && nacc == N) return reinterpret_cast<const void*>(&k_tile<M, N>);
+  TQP_TK(MODE_SCALAR, 1) TQP_TK(MODE_SCALAR, 2) TQP_TK(MODE_SCALAR, 3) TQP_TK(MODE_SCALAR, 4)
+  TQP_TK(MODE_SMALL, 1) TQP_TK(MODE_SMALL, 2) TQP_TK(MODE_SMALL, 3) TQP_TK(MODE_SMALL, 4) TQP_TK(MODE_SMALL, 5)
+  TQP_TK(MODE_SMALL, 6)
+  TQP_TK(MODE_BUILDGRP, 1) TQP_TK(MODE_BUILDGRP, 2) TQP_TK(MODE_BUILDGRP, 3) TQP_TK(MODE_BUILDGRP, 4)
+#undef TQP_TK
+  return nullptr;
+}
+
 struct Runner {
   PipeDesc P;
 
@@ -1585,10 +1597,25 @@ struct Runner {
       Acc& d = ps.acc[ps.nacc++];
       d.is_int = a.is_int;
       d.nf = static_cast<int>(a.f.size());
+      if (!a.is_int && a.f.size() > static_cast<size_t>(kFixedFactors)) return false;
       for (size_t i = 0; i < a.f.size(); ++i) {
         if (a.f[i].kind != FK_CONST) d.f[i].x = make_operand(tables, P, a.f[i].x, &ok);
         d.f[i].kind = a.f[i].kind;
         d.f[i].k = a.f[i].k;
+        const double k = a.f[i].k;
+        switch (a.f[i].kind) {  // factor = fa + fb * x
+          case FK_X: d.f[i].fa = 0.0; d.f[i].fb = 1.0; break;
+          case FK_K_MINUS_X: d.f[i].fa = k; d.f[i].fb = -1.0; break;
+          case FK_K_PLUS_X: d.f[i].fa = k; d.f[i].fb = 1.0; break;
+          case FK_X_MINUS_K: d.f[i].fa = -k; d.f[i].fb = 1.0; break;
+          case FK_X_PLUS_K: d.f[i].fa = k; d.f[i].fb = 1.0; break;
+          case FK_X_TIMES_K: d.f[i].fa = 0.0; d.f[i].fb = k; break;
+          default: d.f[i].fa = k; d.f[i].fb = 0.0; d.f[i].x = Operand{}; break;  // constant
+        }
+      }
+      for (int i = static_cast<int>(a.f.size()); i < kFixedFactors; ++i) {
+        d.f[i] = Factor{};  // 1 + 0 * 0
+        d.f[i].kind = FK_CONST;
       }
       d.gate_probe = a.gate_probe;
       d.gate_bit = a.gate_bit;
@@ -1596,8 +1623,41 @@ struct Runner {
     }
     for (const auto& kcol : P.key_columns) ps.keys[ps.nkeys++] = make_operand(tables, P, {-1, kcol}, &ok);
     if (!ok) return false;
+    // prefix sharing: an fp64 accumulator whose leading factors equal another
+    // (earlier, ungated) accumulator's whole product starts from that value:
+    // ((p*(1-d))*(1+t)) reuses p*(1-d) with identical rounding
+    for (int a = 0; a < ps.nacc; ++a) {
+      Acc& A = ps.acc[a];
+      A.base = -1;
+      if (A.is_int) continue;
+      for (int b = a - 1; b >= 0 && A.base < 0; --b) {
+        const Acc& B = ps.acc[b];
+        if (B.is_int || B.gate_probe >= 0 || B.base >= 0 || B.nf >= A.nf || B.nf == 0) continue;
+        bool same = true;
+        for (int i = 0; i < B.nf && same; ++i) {
+          const Factor &x = A.f[i], &y = B.f[i];
+          same = x.kind == y.kind && x.k == y.k && x.x.ptr == y.x.ptr && x.x.src == y.x.src;
+        }
+        if (!same) continue;
+        A.base = b;
+        const int rest = A.nf - B.nf;
+        for (int i = 0; i < kFixedFactors; ++i) {
+          if (i < rest) {
+            A.f[i] = A.f[i + B.nf];
+          } else {
+            A.f[i] = Factor{};
+            A.f[i].kind = FK_CONST;
+          }
+        }
+        A.nf = rest;
+      }
+    }
 
-    if (P.mode == MODE_SMALL && ps.nacc > kMaxAccSmall) return false;
+    if (ps.nacc > max_acc_for(P.mode)) return false;
+    // the tile kernels read accumulator operands from the staged fact tile
+    for (int a = 0; a < ps.nacc; ++a)
+      for (int i = 0; i < kFixedFactors; ++i)
+        if (ps.acc[a].f[i].kind != FK_CONST && ps.acc[a].f[i].x.src >= 0) return false;
     // distinct fact columns staged per tile; operands address them by index
     TileSpec ts;
     auto col_index = [&](Operand& o) {
@@ -1627,31 +1687,28 @@ struct Runner {
         if (ps.acc[a].f[i].kind != FK_CONST && !col_index(ps.acc[a].f[i].x)) return false;
     for (int i = 0; i < ps.nkeys; ++i)
       if (!col_index(ps.keys[i])) return false;
+    ts.rows = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::ROWS : kTileRows;
+    ts.aux_bytes = static_cast<int>(P.mode == MODE_SMALL    ? aux_bytes_for<MODE_SMALL>(ps.nacc)
+                                    : P.mode == MODE_SCALAR ? aux_bytes_for<MODE_SCALAR>(ps.nacc)
+                                                            : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
     for (int i = 0; i < ts.ncols; ++i) {
       ts.col_off[i] = ts.stage_bytes;
-      ts.stage_bytes += (kTileRows * ts.col_w[i] + 127) & ~127;  // 128 B aligned columns
+      ts.stage_bytes += (ts.rows * ts.col_w[i] + 127) & ~127;  // 128 B aligned columns
     }
     if (ts.stage_bytes == 0) ts.stage_bytes = 128;
     // as many stages as fit next to the fixed (static + staging) parts
     int optin = 0;
     TQP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
     cudaFuncAttributes fa{};
-    size_t fixed = 0;
-    if (P.mode == MODE_SCALAR) {
-      fixed = tile_smem_bytes<MODE_SCALAR>(0, 0);
-      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_SCALAR>));
-    } else if (P.mode == MODE_SMALL) {
-      fixed = tile_smem_bytes<MODE_SMALL>(0, 0);
-      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_SMALL>));
-    } else {
-      fixed = tile_smem_bytes<MODE_BUILDGRP>(0, 0);
-      TQP_CUDA(cudaFuncGetAttributes(&fa, k_tile<MODE_BUILDGRP>));
-    }
+    const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
+    const void* kfn = tile_kernel(P.mode, ps.nacc);
+    if (!kfn) return false;
+    TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
     if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
     ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
     const size_t smem = fixed + static_cast<size_t>(ts.stages) * ts.stage_bytes;
-    auto launch_tile = [&](auto kernel, int threads, int grid_) {
+    auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) {
         throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + " setting " + std::to_string(smem) +
@@ -1659,7 +1716,8 @@ struct Runner {
                                       std::to_string(optin) + ", stages " + std::to_string(ts.stages) + ")");
       }
       ts.p = ps;
-      kernel<<<grid_, threads, smem, c.stream>>>(ts);
+      void* args[] = {&ts};
+      TQP_CUDA(cudaLaunchKernel(kernel, dim3(grid_), dim3(threads), args, smem, c.stream));
       TQP_CUDA(cudaGetLastError());
       c.count_launch();
     };
@@ -1684,7 +1742,7 @@ struct Runner {
     if (P.mode == MODE_SCALAR) {
       auto part = c.alloc_bytes(sizeof(unsigned long long) * grid * (kMaxAcc + 1));
       ps.part = static_cast<unsigned long long*>(part->ptr);
-      launch_tile(k_tile<MODE_SCALAR>, TileShape<MODE_SCALAR>::THREADS, grid);
+      launch_tile(kfn, TileShape<MODE_SCALAR>::THREADS, grid);
       for (size_t j = 0; j < outs.size(); ++j) {
         outs[j] = c.alloc(out_dtype(P.outs[j]), 1, 1);
         fs.out_ptr[j] = outs[j].data();
@@ -1696,7 +1754,7 @@ struct Runner {
       const int g2 = grid;
       auto part = c.alloc_bytes(sizeof(SmallPart) * g2);
       ps.part = static_cast<unsigned long long*>(part->ptr);
-      launch_tile(k_tile<MODE_SMALL>, TileShape<MODE_SMALL>::THREADS, g2);
+      launch_tile(kfn, TileShape<MODE_SMALL>::THREADS, g2);
       auto inv = c.alloc_bytes(sizeof(int) * g2 * kMerged);
       auto ng = c.alloc_bytes(8);
       std::vector<Tensor> tmp(P.outs.size());
@@ -1727,7 +1785,7 @@ struct Runner {
       ps.gacc = static_cast<unsigned long long*>(gacc->ptr);
       ps.gcnt = static_cast<unsigned long long*>(gcnt->ptr);
       ps.group_probe = P.group_probe;
-      launch_tile(k_tile<MODE_BUILDGRP>, TileShape<MODE_BUILDGRP>::THREADS, grid);
+      launch_tile(kfn, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
       gs.f = fs;
       gs.gacc = ps.gacc;

@@ -72,14 +72,19 @@ struct StrTerm {
   unsigned char lit[48];
 };
 
+// factor = fa + fb * x, evaluated branch-free (fa/fb derived from `kind`):
+// K - x == K + (-1)x and 1 * x == x exactly; padding factors are 1 + 0 * 0
 struct Factor {
   Operand x;
   int kind = FK_X;
   double k = 0.0;
+  double fa = 1.0, fb = 0.0;
 };
+constexpr int kFixedFactors = 3;
 
 struct Acc {
   int is_int = 0;
+  int base = -1;  // earlier accumulator whose factor product is this one's prefix
   int nf = 0;
   Factor f[kMaxFactors];
   int gate_probe = -1;  // value counts only if flag bit of probe is set
@@ -421,11 +426,14 @@ constexpr int kMaxCols = 10;
 // accumulators per thread, so it runs fewer, wider threads
 template <int MODE>
 struct TileShape {
+  // small-group keeps per-thread shared-memory accumulators (groups x
+  // accumulators x threads), so its tiles are half as tall
+  static constexpr int ROWS = MODE == MODE_SMALL ? 1024 : kTileRows;
   static constexpr int CW = MODE == MODE_SMALL ? 8 : 16;
   static constexpr int CT = CW * 32;
   static constexpr int THREADS = CT + 32;
-  static constexpr int R = kTileRows / CT;  // rows per consumer thread
-  static constexpr int SUB = MODE == MODE_SMALL ? 4 : R;  // staged rows per pass
+  static constexpr int R = ROWS / CT;  // rows per consumer thread
+  static constexpr int SUB = R;
 };
 
 struct TileSpec {
@@ -436,6 +444,8 @@ struct TileSpec {
   int col_off[kMaxCols];  // byte offset of the column inside a stage
   int stage_bytes = 0;
   int stages = 3;
+  int rows = kTileRows;   // rows per tile
+  int aux_bytes = 0;      // per-thread accumulator / staging region
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -470,9 +480,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 __device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* stage, unsigned long long* bar,
                                            long long tile) {
-  const long long row0 = tile * kTileRows;
+  const long long row0 = tile * t.rows;
   long long rows = t.p.n - row0;
-  if (rows > kTileRows) rows = kTileRows;
+  if (rows > t.rows) rows = t.rows;
   unsigned total = 0;
   for (int c = 0; c < t.ncols; ++c) total += static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
   mbar_expect_tx(bar, total);
@@ -496,11 +506,12 @@ struct SmallPart {  // MODE_SMALL per-CTA partial, in global memory
 
 __device__ __forceinline__ unsigned hash_code(unsigned c) { return (c * 2654435761u) >> (32 - kGroupBits); }
 
+// per-thread region: SCALAR running sums [acc][thread]; SMALL accumulators
+// [group][acc + count][thread]
 template <int MODE>
-__host__ __device__ constexpr size_t stage_val_bytes() {
+__host__ __device__ constexpr size_t aux_bytes_for(int nacc) {
   using S = TileShape<MODE>;
-  return MODE == MODE_SMALL ? sizeof(unsigned long long) * kMaxAccSmall * S::SUB * S::CT
-                            : MODE == MODE_SCALAR ? sizeof(unsigned long long) * kMaxAcc * S::CT : 0;
+  return MODE == MODE_SMALL ? sizeof(unsigned long long) * kGroups * (nacc + 1) * S::CT : 0;
 }
 
 // value of accumulator `ac` for rows k0..k0+N-1 of this thread (row index
@@ -511,44 +522,39 @@ __device__ __forceinline__ void acc_rows(const TileSpec& t, const unsigned char*
   if (ac.is_int) {
     const Operand& o = ac.f[0].x;
     const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[o.col < 0 ? 0 : o.col]);
+    if (o.src < 0) {
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      v[k] = 0;
-      if (pass[k0 + k]) v[k] = o.src < 0 ? col[(k0 + k) * CT + ct] : ld_row(o, rc[k0 + k].rid[o.src]);
+      for (int k = 0; k < N; ++k) v[k] = pass[k0 + k] ? col[(k0 + k) * CT + ct] : 0ULL;
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) v[k] = pass[k0 + k] ? ld_row(o, rc[k0 + k].rid[o.src]) : 0ULL;
     }
     return;
   }
   double d[N];
-  for (int i = 0; i < ac.nf; ++i) {
-    const Factor f = ac.f[i];
-    const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[f.x.col < 0 ? 0 : f.x.col]);
+#pragma unroll
+  for (int i = 0; i < kFixedFactors; ++i) {
+    const Factor& f = ac.f[i];
     double xs[N];
+    if (f.x.col >= 0 && f.x.src < 0) {
+      // fact operand: every row reads the staged tile (masked rows are
+      // discarded later, so no per-row branch)
+      const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[f.x.col]);
+#pragma unroll
+      for (int k = 0; k < N; ++k) xs[k] = __longlong_as_double(static_cast<long long>(col[(k0 + k) * CT + ct]));
+    } else if (f.x.src >= 0) {
+#pragma unroll
+      for (int k = 0; k < N; ++k)
+        xs[k] = pass[k0 + k] ? __longlong_as_double(static_cast<long long>(ld_row(f.x, rc[k0 + k].rid[f.x.src]))) : 0.0;
+    } else {
+#pragma unroll
+      for (int k = 0; k < N; ++k) xs[k] = 0.0;
+    }
+    const double fa = f.fa, fb = f.fb;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      xs[k] = 0.0;
-      if (f.kind != FK_CONST && pass[k0 + k]) {
-        unsigned long long raw = f.x.src < 0 ? col[(k0 + k) * CT + ct] : ld_row(f.x, rc[k0 + k].rid[f.x.src]);
-        xs[k] = __longlong_as_double(static_cast<long long>(raw));
-      }
-    }
-    // one uniform dispatch per factor, straight-line over the rows
-    switch (f.kind) {
-      case FK_X:
-#pragma unroll
-        for (int k = 0; k < N; ++k) d[k] = i == 0 ? xs[k] : __dmul_rn(d[k], xs[k]);
-        break;
-      case FK_K_MINUS_X:
-#pragma unroll
-        for (int k = 0; k < N; ++k) d[k] = i == 0 ? __dsub_rn(f.k, xs[k]) : __dmul_rn(d[k], __dsub_rn(f.k, xs[k]));
-        break;
-      case FK_K_PLUS_X:
-#pragma unroll
-        for (int k = 0; k < N; ++k) d[k] = i == 0 ? __dadd_rn(f.k, xs[k]) : __dmul_rn(d[k], __dadd_rn(f.k, xs[k]));
-        break;
-      default:
-#pragma unroll
-        for (int k = 0; k < N; ++k) d[k] = i == 0 ? apply_factor(f, xs[k]) : __dmul_rn(d[k], apply_factor(f, xs[k]));
-        break;
+      const double y = __dadd_rn(fa, __dmul_rn(fb, xs[k]));
+      d[k] = i == 0 ? y : __dmul_rn(d[k], y);
     }
   }
 #pragma unroll
@@ -559,7 +565,70 @@ __device__ __forceinline__ void acc_rows(const TileSpec& t, const unsigned char*
   }
 }
 
-template <int MODE>
+// Descriptors pre-resolved once per CTA into shared memory: stage-relative
+// byte offsets and affine factor coefficients, read with static indices by
+// fully unrolled loops (no dynamic param-space indexing in the tile loop).
+constexpr unsigned kNoCol = 0xffffffffu;
+// accumulator slots the tile kernels unroll (register budget per mode)
+__host__ __device__ constexpr int max_acc_for(int mode) { return mode == MODE_SMALL ? kMaxAccSmall : 4; }
+enum FactorMode : int { FM_SKIP = 0, FM_X = 1, FM_A_PLUS_X = 2, FM_A_MINUS_X = 3, FM_AFFINE = 4 };
+struct TileDesc {
+  int nterms, nacc, nkeys, nprobes;
+  int t_kind[kMaxTerms];
+  unsigned t_off[kMaxTerms];
+  unsigned long long t_lo[kMaxTerms], t_hi[kMaxTerms];
+  int a_int[kMaxAcc], a_gate_probe[kMaxAcc], a_gate_bit[kMaxAcc];
+  double a_gate_else[kMaxAcc];
+  unsigned a_off[kMaxAcc][kFixedFactors];
+  int a_src[kMaxAcc][kFixedFactors];
+  int a_mode[kMaxAcc][kFixedFactors];  // FM_* (uniform fast forms)
+  int a_base[kMaxAcc];                 // earlier accumulator whose product is a prefix, or -1
+  double a_fa[kMaxAcc][kFixedFactors], a_fb[kMaxAcc][kFixedFactors];
+  unsigned k_off[kMaxKeys];
+  unsigned p_off[kMaxProbes];
+};
+
+__device__ void load_desc(const TileSpec& t, TileDesc& d) {
+  const ProbeSpec& s = t.p;
+  d.nterms = s.nterms;
+  d.nacc = s.nacc;
+  d.nkeys = s.nkeys;
+  d.nprobes = s.nprobes;
+  for (int i = 0; i < s.nterms; ++i) {
+    d.t_kind[i] = s.terms[i].kind;
+    d.t_off[i] = s.terms[i].col >= 0 ? static_cast<unsigned>(t.col_off[s.terms[i].col]) : 0u;
+    d.t_lo[i] = s.terms[i].lo;
+    d.t_hi[i] = s.terms[i].hi;
+  }
+  for (int a = 0; a < s.nacc; ++a) {
+    const Acc& ac = s.acc[a];
+    d.a_int[a] = ac.is_int;
+    d.a_gate_probe[a] = ac.gate_probe;
+    d.a_gate_bit[a] = ac.gate_bit;
+    d.a_gate_else[a] = ac.gate_else;
+    for (int i = 0; i < kFixedFactors; ++i) {
+      const Factor& f = ac.f[i];
+      d.a_src[a][i] = f.x.src;
+      d.a_off[a][i] = (f.x.src < 0 && f.x.col >= 0) ? static_cast<unsigned>(t.col_off[f.x.col]) : kNoCol;
+      d.a_fa[a][i] = ac.is_int ? 0.0 : f.fa;
+      d.a_fb[a][i] = ac.is_int ? 0.0 : f.fb;
+      // fast forms are exact restatements: 0 + 1*x == x (up to the sign of
+      // a zero, which never survives the +0.0-seeded sums), a + 1*x == a + x,
+      // a + (-1)*x == a - x; padding factors 1 + 0*0 are skipped
+      int m = FM_AFFINE;
+      if (d.a_off[a][i] == kNoCol && f.x.src < 0 && f.fa == 1.0 && f.fb == 0.0) m = FM_SKIP;
+      else if (f.fa == 0.0 && f.fb == 1.0) m = FM_X;
+      else if (f.fb == 1.0) m = FM_A_PLUS_X;
+      else if (f.fb == -1.0) m = FM_A_MINUS_X;
+      d.a_mode[a][i] = m;
+    }
+    d.a_base[a] = ac.base;
+  }
+  for (int q = 0; q < s.nkeys; ++q) d.k_off[q] = static_cast<unsigned>(t.col_off[s.keys[q].col]);
+  for (int p = 0; p < s.nprobes; ++p) d.p_off[p] = static_cast<unsigned>(t.col_off[s.probes[p].key.col]);
+}
+
+template <int MODE, int NA_>
 __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const TileSpec t) {
   using S = TileShape<MODE>;
   constexpr int CW = S::CW, CT = S::CT, R = S::R, SUB = S::SUB;
@@ -567,14 +636,15 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
   __shared__ unsigned long long s_wred[MODE == MODE_SMALL ? kGroups : 1][kMaxAcc + 1][CW];
   __shared__ unsigned int s_codes[kGroups];
   __shared__ int s_overflow;
+  __shared__ TileDesc d;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem);
   unsigned long long* empty = full + kMaxStages;
   // per-thread staging (SCALAR: running sums; SMALL: row values), then stages
   unsigned long long* s_stage_val = reinterpret_cast<unsigned long long*>(smem + 256);
-  unsigned char* stages = smem + 256 + stage_val_bytes<MODE>();
+  unsigned char* stages = smem + 256 + t.aux_bytes;
   const ProbeSpec& s = t.p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long ntiles = (s.n + kTileRows - 1) / kTileRows;
+  const long long ntiles = (s.n + S::ROWS - 1) / S::ROWS;
   const int nst = t.stages;
 
   if (threadIdx.x == 0) {
@@ -584,9 +654,10 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_overflow = 0;
+    load_desc(t, d);
   }
   if (threadIdx.x < kGroups) s_codes[threadIdx.x] = 0xffffffffu;
-  for (int i = threadIdx.x; i < static_cast<int>(stage_val_bytes<MODE>() / 8); i += blockDim.x) s_stage_val[i] = 0;
+  for (int i = threadIdx.x; i < t.aux_bytes / 8; i += blockDim.x) s_stage_val[i] = 0;
   __syncthreads();
 
   if (warp == 0) {
@@ -603,8 +674,9 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     // ---- consumers ----
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
-    constexpr int NA = MODE == MODE_SMALL ? kMaxAccSmall : kMaxAcc;
-    constexpr int NG = MODE == MODE_SMALL ? kGroups : 1;
+    constexpr int NA = kMaxAcc;
+    constexpr int NAX = NA_;  // accumulators: exact count, fully unrolled
+    constexpr int NG = 1;
     unsigned long long acc[NG][NA];
     unsigned int gcnt_local[NG];
 #pragma unroll
@@ -619,75 +691,93 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       const int st = static_cast<int>(it % nst);
       const unsigned char* stage = stages + static_cast<size_t>(st) * t.stage_bytes;
       mbar_wait(&full[st], static_cast<unsigned>((it / nst) & 1));
-      const long long row0 = tile * kTileRows;
+      const long long row0 = tile * S::ROWS;
       bool pass[R];
 #pragma unroll
       for (int k = 0; k < R; ++k) pass[k] = row0 + k * CT + ct < s.n;
-      // predicate: one uniform dispatch per term, straight-line over rows
-      for (int i = 0; i < s.nterms; ++i) {
-        const RTerm tm = s.terms[i];
-        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[tm.col < 0 ? 0 : tm.col]);
-        if (tm.kind == RK_INT) {
-          const unsigned long long span = tm.hi - tm.lo;
+      // predicate: unrolled over the term slots, uniform dispatch per term,
+      // straight-line over this thread's rows
 #pragma unroll
-          for (int k = 0; k < R; ++k) pass[k] = pass[k] && (col[k * CT + ct] - tm.lo <= span);
-        } else if (tm.kind == RK_F64) {
-          const double lo = __longlong_as_double(static_cast<long long>(tm.lo));
-          const double hi = __longlong_as_double(static_cast<long long>(tm.hi));
+      for (int i = 0; i < kMaxTerms; ++i) {
+        if (i < d.nterms) {
+          const int kind = d.t_kind[i];
+          const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.t_off[i]);
+          const unsigned long long lo = d.t_lo[i], hi = d.t_hi[i];
+          if (kind == RK_INT) {
+            const unsigned long long span = hi - lo;
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            const double x = __longlong_as_double(static_cast<long long>(col[k * CT + ct]));
-            pass[k] = pass[k] && x >= lo && x <= hi;
+            for (int k = 0; k < R; ++k) pass[k] = pass[k] && (col[k * CT + ct] - lo <= span);
+          } else if (kind == RK_F64) {
+            const double flo = __longlong_as_double(static_cast<long long>(lo));
+            const double fhi = __longlong_as_double(static_cast<long long>(hi));
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              const double x = __longlong_as_double(static_cast<long long>(col[k * CT + ct]));
+              pass[k] = pass[k] && x >= flo && x <= fhi;
+            }
+          } else {
+            RTerm tm;
+            tm.kind = kind;
+            tm.lo = lo;
+            tm.hi = hi;
+#pragma unroll
+            for (int k = 0; k < R; ++k) pass[k] = pass[k] && eval_rterm(tm, kind <= RK_F64_NE ? col[k * CT + ct] : 0ULL);
           }
-        } else {
-#pragma unroll
-          for (int k = 0; k < R; ++k)
-            pass[k] = pass[k] && eval_rterm(tm, tm.kind <= RK_F64_NE ? col[k * CT + ct] : 0ULL);
         }
       }
       RowCtx rc[R];
       for (int p = 0; p < s.nprobes; ++p) {
         const Probe& pr = s.probes[p];
-        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + t.col_off[pr.key.col]);
+        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.p_off[p]);
 #pragma unroll
         for (int k = 0; k < R; ++k)
           if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p]);
       }
-      bool any = false;
+      bool any = MODE == MODE_SMALL;  // small-group runs warp-collective slot claims: no per-thread skip
 #pragma unroll
       for (int k = 0; k < R; ++k) any = any || pass[k];
       if (any) {
         int slot[R];
         if constexpr (MODE == MODE_SMALL) {
+          // the CTA's <= kGroups codes in registers: branch-free match
+          unsigned cr[kGroups];
+#pragma unroll
+          for (int j = 0; j < kGroups; ++j) cr[j] = s_codes[j];
+          unsigned code[R];
+          bool miss = false;
 #pragma unroll
           for (int k = 0; k < R; ++k) {
+            code[k] = 0;
+#pragma unroll
+            for (int q = 0; q < kMaxKeys; ++q)
+              if (q < d.nkeys) code[k] = (code[k] << 8) | stage[d.k_off[q] + k * CT + ct];
             slot[k] = -1;
-            if (!pass[k]) continue;
-            unsigned code = 0;
-            for (int q = 0; q < s.nkeys; ++q) code = (code << 8) | stage[t.col_off[s.keys[q].col] + k * CT + ct];
-            unsigned h = hash_code(code);
-            for (int probe = 0; probe < kGroups; ++probe) {
-              unsigned cur = s_codes[h];
-              if (cur == code) {
-                slot[k] = static_cast<int>(h);
-                break;
-              }
-              if (cur == 0xffffffffu) {
-                unsigned prev = atomicCAS(&s_codes[h], 0xffffffffu, code);
-                if (prev == 0xffffffffu || prev == code) {
-                  slot[k] = static_cast<int>(h);
+#pragma unroll
+            for (int j = 0; j < kGroups; ++j) slot[k] = cr[j] == code[k] ? j : slot[k];
+            if (!pass[k]) slot[k] = -1;
+            miss = miss || (pass[k] && slot[k] < 0);
+          }
+          if (__any_sync(0xffffffffu, miss)) {
+            // first sighting of a code in this CTA: claim a free slot (rare)
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              if (!pass[k] || slot[k] >= 0) continue;
+              for (int j = 0; j < kGroups; ++j) {
+                const unsigned prev = atomicCAS(&s_codes[j], 0xffffffffu, code[k]);
+                if (prev == 0xffffffffu || prev == code[k]) {
+                  slot[k] = j;
                   break;
                 }
               }
-              h = (h + 1) & (kGroups - 1);
+              if (slot[k] < 0) {
+                s_overflow = 1;
+                pass[k] = false;
+              }
             }
-            if (slot[k] < 0) {
-              s_overflow = 1;
-              pass[k] = false;
-            }
-#pragma unroll
-            for (int g = 0; g < NG; ++g) gcnt_local[g] += slot[k] == g ? 1u : 0u;
           }
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (pass[k]) s_stage_val[(slot[k] * (NA_ + 1) + NA_) * CT + ct] += 1;
         } else {
 #pragma unroll
           for (int k = 0; k < R; ++k) gcnt_local[0] += pass[k] ? 1u : 0u;
@@ -700,62 +790,84 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             if (pass[k]) atomicAdd(s.gcnt + g[k], 1ULL);
           }
         }
+        // values, fully unrolled (NA is a template parameter) and branch-free:
+        // product = start * (fa0 + fb0 x0) * (fa1 + fb1 x1) * (fa2 + fb2 x2),
+        // start = 1.0 (1 * f0 == f0 exactly) or an earlier accumulator's
+        // product (prefix sharing); a missing operand reads as 0 and a
+        // padding factor is 1 + 0 * 0, so every slot runs the same code
+        double dvals[NAX][R];
 #pragma unroll
-        for (int k0 = 0; k0 < R; k0 += SUB) {
-          // values: one runtime loop over the accumulators (code inlined once)
-          for (int a = 0; a < s.nacc; ++a) {
-            const bool is_int = s.acc[a].is_int;
-            unsigned long long v[SUB];
-            acc_rows<CT, SUB>(t, stage, s.acc[a], pass, rc, ct, k0, v);
-            if (is_int) {
+        for (int a = 0; a < NAX; ++a) {
+          const bool is_int = d.a_int[a];
+          unsigned long long v[R];
+          if (is_int) {
+            const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.a_off[a][0]);
 #pragma unroll
-              for (int k = 0; k < SUB; ++k) {
-                long long iv = static_cast<long long>(v[k]);
-                iv = iv < 0 ? -iv : iv;
-                absmax = iv > absmax ? iv : absmax;
+            for (int k = 0; k < R; ++k) {
+              v[k] = pass[k] ? col[k * CT + ct] : 0ULL;
+              long long iv = static_cast<long long>(v[k]);
+              iv = iv < 0 ? -iv : iv;
+              absmax = iv > absmax ? iv : absmax;
+              dvals[a][k] = 1.0;
+            }
+          } else {
+            const int base = d.a_base[a];
+            double dv[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              dv[k] = 1.0;
+#pragma unroll
+              for (int b = 0; b < a; ++b) dv[k] = base == b ? dvals[b][k] : dv[k];
+            }
+#pragma unroll
+            for (int i = 0; i < kFixedFactors; ++i) {
+              const unsigned off = d.a_off[a][i];
+              const bool has = off != kNoCol;
+              const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + (has ? off : 0u));
+              const double fa = d.a_fa[a][i], fb = d.a_fb[a][i];
+#pragma unroll
+              for (int k = 0; k < R; ++k) {
+                const double x = has ? __longlong_as_double(static_cast<long long>(col[k * CT + ct])) : 0.0;
+                dv[k] = __dmul_rn(dv[k], __dadd_rn(fa, __dmul_rn(fb, x)));
               }
             }
-            if constexpr (MODE == MODE_SCALAR) {
-              unsigned long long sum = s_stage_val[a * CT + ct];
 #pragma unroll
-              for (int k = 0; k < SUB; ++k)
-                if (pass[k0 + k]) sum = add_acc(is_int, sum, v[k]);
-              s_stage_val[a * CT + ct] = sum;
-            } else if constexpr (MODE == MODE_SMALL) {
+            for (int k = 0; k < R; ++k) dvals[a][k] = dv[k];
+            const int gp = d.a_gate_probe[a];
+            if (gp >= 0) {
+              const int gb = d.a_gate_bit[a];
+              const double ge = d.a_gate_else[a];
 #pragma unroll
-              for (int k = 0; k < SUB; ++k) s_stage_val[(a * SUB + k) * CT + ct] = v[k];
-            } else {
-#pragma unroll
-              for (int k = 0; k < SUB; ++k) {
-                if (!pass[k0 + k]) continue;
-                __int128 qv;
-                if (is_int) {
-                  qv = static_cast<__int128>(static_cast<long long>(v[k]));
-                } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k])), qv)) {
-                  atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-                  qv = 0;
-                }
-                atomic_add_q64(s.gacc + (static_cast<long long>(g[k0 + k]) * s.nacc + a) * 2, qv);
-              }
+              for (int k = 0; k < R; ++k)
+                if (pass[k] && !((rc[k].flags[gp] >> gb) & 1u)) dv[k] = ge;
             }
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = pass[k] ? static_cast<unsigned long long>(__double_as_longlong(dv[k])) : 0ULL;
           }
-          if constexpr (MODE == MODE_SMALL) {
-            // register accumulators per (group slot, accumulator): masked
-            // adds in a fixed order (x + 0 == x; sums start at +0.0 like the
-            // reference's); a predicated store would be merged by the
-            // compiler into one dynamically indexed (local-memory) access
+          if constexpr (MODE == MODE_SCALAR) {
 #pragma unroll
-            for (int a = 0; a < NA; ++a) {
-              if (a < s.nacc) {
-                const bool is_int = s.acc[a].is_int;
+            for (int k = 0; k < R; ++k) acc[0][a] = add_acc(is_int, acc[0][a], v[k]);  // masked rows add 0
+          } else if constexpr (MODE == MODE_SMALL) {
+            // per-thread accumulator slot [group][a][thread]; masked rows add
+            // 0 to slot 0 (x + 0 == x), so no per-row branch
 #pragma unroll
-                for (int k = 0; k < SUB; ++k) {
-                  const unsigned long long v = s_stage_val[(a * SUB + k) * CT + ct];
+            for (int k = 0; k < R; ++k) {
+              const int sl = slot[k] < 0 ? 0 : slot[k];
+              unsigned long long* cell = s_stage_val + (sl * (NAX + 1) + a) * CT + ct;
+              *cell = add_acc(is_int, *cell, v[k]);
+            }
+          } else {
 #pragma unroll
-                  for (int gg = 0; gg < NG; ++gg)
-                    acc[gg][a] = add_acc(is_int, acc[gg][a], slot[k0 + k] == gg ? v : 0ULL);
-                }
+            for (int k = 0; k < R; ++k) {
+              if (!pass[k]) continue;
+              __int128 qv;
+              if (is_int) {
+                qv = static_cast<__int128>(static_cast<long long>(v[k]));
+              } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k])), qv)) {
+                atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+                qv = 0;
               }
+              atomic_add_q64(s.gacc + (static_cast<long long>(g[k]) * NAX + a) * 2, qv);
             }
           }
         }
@@ -768,13 +880,19 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
       atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
     }
-    if constexpr (MODE == MODE_SCALAR) {
+    if constexpr (MODE == MODE_SMALL) {
+      for (int gg = 0; gg < kGroups; ++gg) {
+        for (int a = 0; a <= s.nacc; ++a) {
+          unsigned long long x = s_stage_val[(gg * (NA_ + 1) + a) * CT + ct];
+          const bool is_int = a == s.nacc || s.acc[a].is_int;
 #pragma unroll
-      for (int a = 0; a < NA; ++a)
-        if (a < s.nacc) acc[0][a] = s_stage_val[a * CT + ct];
+          for (int o = 16; o > 0; o >>= 1) x = add_acc(is_int, x, __shfl_xor_sync(0xffffffffu, x, o));
+          if (lane == 0) s_wred[gg][a == s.nacc ? kMaxAcc : a][cw] = x;
+        }
+      }
     }
-    if constexpr (MODE != MODE_BUILDGRP) {
-      // fixed-order warp trees, one slot per (group, accumulator, warp)
+    if constexpr (MODE == MODE_SCALAR) {
+      // fixed-order warp trees, one slot per (accumulator, warp)
 #pragma unroll
       for (int gg = 0; gg < NG; ++gg) {
 #pragma unroll
@@ -822,11 +940,6 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       }
     }
   }
-}
-
-template <int MODE>
-inline size_t tile_smem_bytes(int stage_bytes, int stages) {
-  return 256 + stage_val_bytes<MODE>() + static_cast<size_t>(stages) * stage_bytes;
 }
 
 }  // namespace fz
