@@ -21,6 +21,7 @@
 
 #include "executor.hpp"
 #include "fused_kernels.cuh"
+#include "scan.cuh"
 
 namespace tqp {
 namespace {
@@ -1146,23 +1147,36 @@ __device__ __forceinline__ bool key_less(const unsigned long long* a, const unsi
 // over the <= 64 candidates it owns), and one CTA merges the per-CTA winners.
 constexpr int kTopkMaxPerThread = 64;
 
-__global__ void k_topk_cands(GroupSpec s, long long ngroups, unsigned* __restrict__ cand_gid,
-                             unsigned long long* __restrict__ cand_key, unsigned* __restrict__ ncand) {
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(kThreads) k_topk_cands(GroupSpec s, long long ngroups, unsigned* __restrict__ cand_gid,
+                                                         unsigned long long* __restrict__ cand_key,
+                                                         unsigned* __restrict__ ncand) {
+  // block-aggregated append: one global atomic per 2048 groups
+  __shared__ unsigned long long s_w[33];
+  __shared__ unsigned s_base;
+  constexpr int kPer = 8;
   const int nk = s.nsort + s.nkeyc;
-  for (long long base = gtid() & ~31LL; base < ngroups; base += gstride()) {
-    const long long g = base + lane;
-    const bool ok = g < ngroups && s.gcnt[g] != 0;
-    const unsigned m = __ballot_sync(0xffffffffu, ok);
-    unsigned first = 0;
-    if (lane == 0 && m) first = atomicAdd(ncand, static_cast<unsigned>(__popc(m)));
-    first = __shfl_sync(0xffffffffu, first, 0);
-    if (!ok) continue;
-    const unsigned pos = first + __popc(m & ((1u << lane) - 1u));
-    cand_gid[pos] = static_cast<unsigned>(g);
+  const long long base = static_cast<long long>(blockIdx.x) * kThreads * kPer + threadIdx.x * kPer;
+  bool ok[kPer];
+  unsigned mine = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    ok[j] = base + j < ngroups && s.gcnt[base + j] != 0;
+    mine += ok[j];
+  }
+  unsigned long long total;
+  unsigned long long excl = block_exclusive_scan(mine, s_w, &total);
+  if (threadIdx.x == 0) s_base = total ? atomicAdd(ncand, static_cast<unsigned>(total)) : 0u;
+  __syncthreads();
+  unsigned pos = s_base + static_cast<unsigned>(excl);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    if (!ok[j]) continue;
+    const unsigned g = static_cast<unsigned>(base + j);
+    cand_gid[pos] = g;
     unsigned long long k[9];
-    cand_keys(s, static_cast<unsigned>(g), k);
+    cand_keys(s, g, k);
     for (int q = 0; q < nk; ++q) cand_key[static_cast<long long>(pos) * nk + q] = k[q];
+    ++pos;
   }
 }
 
@@ -1496,7 +1510,7 @@ struct Runner {
       auto mmb = c.alloc_bytes(16);
       TQP_CUDA(cudaMemcpyAsync(mmb->ptr, mm, 16, cudaMemcpyHostToDevice, c.stream));
       if (n) {
-        k_minmax<<<c.grid_for(n, 256, 4, 2), 256, 0, c.stream>>>(key->t.ptr<long long>(), n, static_cast<long long*>(mmb->ptr));
+        k_minmax<<<c.grid_for(n, 256, 8, 16), 256, 0, c.stream>>>(key->t.ptr<long long>(), n, static_cast<long long*>(mmb->ptr));
         c.count_launch();
       }
       TQP_CUDA(cudaMemcpyAsync(mm, mmb->ptr, 16, cudaMemcpyDeviceToHost, c.stream));
@@ -1558,7 +1572,9 @@ struct Runner {
       }
       if (!ok) return false;
       if (n) {
-        k_build<<<c.grid_for(n, kThreads, 1, 4), kThreads, 0, c.stream>>>(bs);
+        // one row per thread: the per-row dependent loads (term, probe,
+        // insert) need many warps in flight
+        k_build<<<c.grid_for(n, kThreads, kBuildRows, 1 << 20), kThreads, 0, c.stream>>>(bs);
         c.count_launch();
       }
       Probe pr;
@@ -1818,7 +1834,7 @@ struct Runner {
         auto ncb = c.alloc_bytes(8);
         TQP_CUDA(cudaMemsetAsync(ncb->ptr, 0, 8, c.stream));
         if (ngroups) {
-          k_topk_cands<<<c.grid_for(ngroups, kThreads, 1, 4), kThreads, 0, c.stream>>>(
+          k_topk_cands<<<(ngroups + kThreads * 8 - 1) / (kThreads * 8), kThreads, 0, c.stream>>>(
               gs, ngroups, static_cast<unsigned*>(cgid->ptr), static_cast<unsigned long long*>(ckey->ptr),
               static_cast<unsigned*>(ncb->ptr));
           c.count_launch();
@@ -1826,7 +1842,7 @@ struct Runner {
         unsigned ncand = 0;
         TQP_CUDA(cudaMemcpyAsync(&ncand, ncb->ptr, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
-        const long long chunk = static_cast<long long>(kThreads) * 16;
+        const long long chunk = static_cast<long long>(kThreads) * 4;
         const long long nblk = (static_cast<long long>(ncand) + chunk - 1) / chunk;
         const long long nwin = nblk * k;
         if (nwin > static_cast<long long>(kThreads) * kTopkMaxPerThread) return false;

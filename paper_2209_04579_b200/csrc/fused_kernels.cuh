@@ -20,6 +20,7 @@
 #pragma once
 
 #include "device.cuh"
+#include "scan.cuh"
 
 namespace tqp {
 namespace fz {
@@ -365,45 +366,100 @@ __global__ void k_minmax(const long long* __restrict__ k, long long n, long long
   }
 }
 
+constexpr int kBuildRows = 4;
 __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
   const int lane = threadIdx.x & 31;
-  for (long long base = gtid() & ~31LL; base < s.n; base += gstride()) {
-    const long long r = base + lane;
-    bool pass = r < s.n;
-    for (int t = 0; t < s.nterms && pass; ++t) pass = eval_term(s.terms[t], ld_row(s.terms[t].x, r));
-    for (int t = 0; t < s.nstr && pass; ++t) pass = eval_str(s.str[t], r);
-    for (int p = 0; p < s.nprobes && pass; ++p) {
-      long long rid;
-      unsigned fl, g;
-      pass = probe_lookup(s.probes[p], static_cast<long long>(ld_row(s.probes[p].key, r)), rid, fl, g);
+  // kBuildRows rows per thread (stride blockDim) with every independent column
+  // load issued before any dependent work: the per-row chain (filter ->
+  // child probe -> insert) is latency-bound otherwise
+  const long long span = static_cast<long long>(blockDim.x) * kBuildRows;
+  for (long long base0 = static_cast<long long>(blockIdx.x) * span; base0 < s.n; base0 += static_cast<long long>(gridDim.x) * span) {
+    bool pass[kBuildRows];
+    long long key[kBuildRows], pk[kBuildRows][kMaxProbes];
+#pragma unroll
+    for (int j = 0; j < kBuildRows; ++j) {
+      const long long r = base0 + j * blockDim.x + threadIdx.x;
+      pass[j] = r < s.n;
+      key[j] = pass[j] ? static_cast<long long>(ld_row(s.key, r)) : 0;
+#pragma unroll
+      for (int p = 0; p < kMaxProbes; ++p)
+        pk[j][p] = (p < s.nprobes && pass[j]) ? static_cast<long long>(ld_row(s.probes[p].key, r)) : 0;
     }
-    unsigned gid = 0;
+#pragma unroll
+    for (int t = 0; t < kMaxTerms; ++t) {
+      if (t < s.nterms) {
+        unsigned long long v[kBuildRows];
+#pragma unroll
+        for (int j = 0; j < kBuildRows; ++j) {
+          const long long r = base0 + j * blockDim.x + threadIdx.x;
+          v[j] = pass[j] ? ld_row(s.terms[t].x, r) : 0ULL;
+        }
+#pragma unroll
+        for (int j = 0; j < kBuildRows; ++j) pass[j] = pass[j] && eval_term(s.terms[t], v[j]);
+      }
+    }
+    for (int t = 0; t < s.nstr; ++t)
+#pragma unroll
+      for (int j = 0; j < kBuildRows; ++j)
+        if (pass[j]) pass[j] = eval_str(s.str[t], base0 + j * blockDim.x + threadIdx.x);
+#pragma unroll
+    for (int p = 0; p < kMaxProbes; ++p) {
+      if (p < s.nprobes) {
+#pragma unroll
+        for (int j = 0; j < kBuildRows; ++j) {
+          long long rid;
+          unsigned fl, g;
+          if (pass[j]) pass[j] = probe_lookup(s.probes[p], pk[j][p], rid, fl, g);
+        }
+      }
+    }
+    // group ids: one global atomic per block (block scan of per-thread
+    // counts); a per-warp atomic on a single counter serialises at L2
+    unsigned gid_next = 0;
     if (s.assign_groups) {
-      // warp-aggregated group-id allocation: one atomic per warp
-      const unsigned m = __ballot_sync(0xffffffffu, pass);
-      unsigned first = 0;
-      if (lane == 0 && m) first = atomicAdd(s.group_counter, static_cast<unsigned>(__popc(m)));
-      first = __shfl_sync(0xffffffffu, first, 0);
-      gid = first + __popc(m & ((1u << lane) - 1u));
+      __shared__ unsigned long long s_w[33];
+      __shared__ unsigned s_gbase;
+      unsigned mine = 0;
+#pragma unroll
+      for (int j = 0; j < kBuildRows; ++j) mine += pass[j] ? 1u : 0u;
+      unsigned long long total;
+      const unsigned long long excl = block_exclusive_scan(mine, s_w, &total);
+      if (threadIdx.x == 0) s_gbase = total ? atomicAdd(s.group_counter, static_cast<unsigned>(total)) : 0u;
+      __syncthreads();
+      gid_next = s_gbase + static_cast<unsigned>(excl);
+      __syncthreads();
     }
-    if (!pass) continue;
-    unsigned flags = 0;
-    for (int f = 0; f < s.nflags; ++f)
-      if (eval_str(s.flags[f], r)) flags |= 1u << f;
-    const long long key = static_cast<long long>(ld_row(s.key, r));
-    const long long idx = key - s.kmin;
-    if (idx < 0 || idx >= s.range || gid >= (1u << 25)) {
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-      continue;
+#pragma unroll
+    for (int j = 0; j < kBuildRows; ++j) {
+      const long long r = base0 + j * blockDim.x + threadIdx.x;
+      unsigned gid = 0;
+      if (s.assign_groups && pass[j]) gid = gid_next++;
+      long long idx = -1;
+      if (pass[j]) {
+        unsigned flags = 0;
+        for (int f = 0; f < s.nflags; ++f)
+          if (eval_str(s.flags[f], r)) flags |= 1u << f;
+        idx = key[j] - s.kmin;
+        if (idx < 0 || idx >= s.range || gid >= (1u << 25)) {
+          atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+          idx = -1;
+        } else {
+          if (s.assign_groups) s.group_row[gid] = static_cast<int>(r);
+          const unsigned long long e = static_cast<unsigned long long>(r + 1) |
+                                       (static_cast<unsigned long long>(gid) << 32) |
+                                       (static_cast<unsigned long long>(flags) << 57);
+          if (atomicCAS(s.table + idx, 0ULL, e) != 0ULL) {
+            // duplicate build key: the join is 1:N, outside the fused contract
+            atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+          }
+        }
+      }
+      // presence bits: lanes sharing a bitmap word OR-reduce, one atomic per word
+      const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, word);
+      const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
+      if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(s.bitmap + word, bits);
     }
-    if (s.assign_groups) s.group_row[gid] = static_cast<int>(r);
-    const unsigned long long e = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(gid) << 32) |
-                                 (static_cast<unsigned long long>(flags) << 57);
-    if (atomicCAS(s.table + idx, 0ULL, e) != 0ULL) {
-      // duplicate build key: the join is 1:N, outside the fused contract
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-    }
-    atomicOr(s.bitmap + (idx >> 5), 1u << (idx & 31));
   }
 }
 
@@ -726,12 +782,15 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
         }
       }
       RowCtx rc[R];
-      for (int p = 0; p < s.nprobes; ++p) {
-        const Probe& pr = s.probes[p];
-        const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.p_off[p]);
 #pragma unroll
-        for (int k = 0; k < R; ++k)
-          if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p]);
+      for (int p = 0; p < kMaxProbes; ++p) {
+        if (p < d.nprobes) {
+          const Probe& pr = s.probes[p];
+          const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.p_off[p]);
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p]);
+        }
       }
       bool any = MODE == MODE_SMALL;  // small-group runs warp-collective slot claims: no per-thread skip
 #pragma unroll
@@ -786,7 +845,10 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
         if constexpr (MODE == MODE_BUILDGRP) {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
-            g[k] = pass[k] ? rc[k].gid[s.group_probe] : 0u;
+            unsigned gg = rc[k].gid[0];
+#pragma unroll
+            for (int p = 1; p < kMaxProbes; ++p) gg = s.group_probe == p ? rc[k].gid[p] : gg;
+            g[k] = pass[k] ? gg : 0u;
             if (pass[k]) atomicAdd(s.gcnt + g[k], 1ULL);
           }
         }
@@ -838,8 +900,12 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
               const int gb = d.a_gate_bit[a];
               const double ge = d.a_gate_else[a];
 #pragma unroll
-              for (int k = 0; k < R; ++k)
-                if (pass[k] && !((rc[k].flags[gp] >> gb) & 1u)) dv[k] = ge;
+              for (int k = 0; k < R; ++k) {
+                unsigned fl = rc[k].flags[0];  // static select keeps rc in registers
+#pragma unroll
+                for (int p = 1; p < kMaxProbes; ++p) fl = gp == p ? rc[k].flags[p] : fl;
+                if (pass[k] && !((fl >> gb) & 1u)) dv[k] = ge;
+              }
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) v[k] = pass[k] ? static_cast<unsigned long long>(__double_as_longlong(dv[k])) : 0ULL;
