@@ -271,7 +271,14 @@ void Executor::time_end(const std::string& name, cudaEvent_t start) {
   timings_[name].pending.push_back({start, stop});
 }
 
+void Executor::collect_kernel_events() {
+  // kernel events recorded on the shared context during this executor's run
+  for (auto& [name, ev] : ctx_.kernel_events) timings_["kernel:" + name].pending.push_back(ev);
+  ctx_.kernel_events.clear();
+}
+
 void Executor::drain_timings() {
+  collect_kernel_events();
   for (auto& [name, t] : timings_) {
     for (auto& [a, b] : t.pending) {
       TQP_CUDA(cudaEventSynchronize(b));
@@ -372,6 +379,7 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
     }
   }
   ctx_.sync();
+  if (timing_) collect_kernel_events();
   return res;
 }
 

@@ -116,7 +116,10 @@ class Executor {
 
   // Device-time accounting per unit (fused pipeline or generic step) with
   // CUDA events on the context stream; no host synchronisation until read.
-  void set_timing(bool on) { timing_ = on; }
+  void set_timing(bool on) {
+    timing_ = on;
+    ctx_.time_kernels = on;
+  }
   std::string timings_json();
   void reset_timings();
 
@@ -129,6 +132,7 @@ class Executor {
   void time_begin(cudaEvent_t* ev);
   void time_end(const std::string& name, cudaEvent_t start);
   void drain_timings();
+  void collect_kernel_events();
   bool timing_ = false;
   std::map<std::string, UnitTiming> timings_;
 

@@ -1724,6 +1724,9 @@ struct Runner {
     if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
     ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
     const size_t smem = fixed + static_cast<size_t>(ts.stages) * ts.stage_bytes;
+    const std::string tile_name = std::string("k_tile<") +
+                                  (P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small" : "buildgrp") + "," +
+                                  std::to_string(ps.nacc) + ">";
     auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {
       cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       if (e != cudaSuccess) {
@@ -1733,7 +1736,9 @@ struct Runner {
       }
       ts.p = ps;
       void* args[] = {&ts};
+      cudaEvent_t ev = c.kernel_begin();
       TQP_CUDA(cudaLaunchKernel(kernel, dim3(grid_), dim3(threads), args, smem, c.stream));
+      c.kernel_end(tile_name, ev);
       TQP_CUDA(cudaGetLastError());
       c.count_launch();
     };

@@ -81,6 +81,25 @@ struct Ctx {
   int64_t read_err(long long* aux = nullptr, long long* kind = nullptr);
   int grid_for(int64_t n, int block, int per_thread = 1, int waves = 8) const;
   void count_launch(int n = 1) { launches += n; }
+
+  // optional per-kernel device timing (CUDA events on `stream`), drained by
+  // the executor's timings
+  bool time_kernels = false;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> kernel_events;
+  cudaEvent_t kernel_begin() {
+    if (!time_kernels) return nullptr;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    return e;
+  }
+  void kernel_end(const std::string& name, cudaEvent_t start) {
+    if (!start) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    kernel_events.push_back({name, {start, e}});
+  }
 };
 
 Tensor upload(Ctx& c, int dtype, int64_t rows, int64_t cols, const void* host);
