@@ -230,6 +230,23 @@ tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names,
 void tqp_executor_set_timing(tqp_executor* ex, int on);
 const char* tqp_executor_timings(tqp_executor* ex);
 void tqp_executor_reset_timings(tqp_executor* ex);
+/* ---- sharded execution (the reference runs one process,
+ * so there is no reference entry point: executor.cpp:346 is the unsharded
+ * equivalent). Each shard runs phase 1 over its rows of the fact table
+ * (lineitem cut on order boundaries, dimension tables whole or co-partitioned)
+ * and gets an opaque partial: a device I64 tensor of `rows` words, moved
+ * between GPUs as rows*8 bytes (NCCL all-gather). Phase 2 merges the partials
+ * of all shards, in shard order, on any one GPU and runs the remaining steps;
+ * the result equals the unsharded run (bit-exact for integers and
+ * build-grouped sums, fp64 scan sums within 1e-9 relative). */
+/* 1 if the plan can run sharded; else 0 and *why (thread-local string). */
+int tqp_executor_shardable(tqp_executor* ex, const char** why);
+tqp_tensor* tqp_executor_execute_partial(tqp_executor* ex, const char* const* names,
+                                         tqp_table* const* tables, int ntables, tqp_status* st);
+/* parts[i]: device pointer to partial i's words, words[i] its word count. */
+tqp_result* tqp_executor_finish(tqp_executor* ex, const void* const* parts, const int64_t* words,
+                                int nparts, tqp_status* st);
+
 /* Description of the fused pipelines chosen for this plan (JSON). */
 const char* tqp_executor_explain(tqp_executor* ex);
 void tqp_executor_free(tqp_executor* ex);

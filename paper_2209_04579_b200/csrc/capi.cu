@@ -413,6 +413,50 @@ tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names, tqp
   });
 }
 
+tqp_tensor* tqp_executor_execute_partial(tqp_executor* ex, const char* const* names, tqp_table* const* tables, int n,
+                                         tqp_status* st) {
+  return guard(st, [&] {
+    if (!ex) throw Error(TQP_ERR_ARG, "null executor");
+    TableSet ts;
+    for (int i = 0; i < n; ++i) ts.push_back({names[i], &tables[i]->t});
+    Partial p = ex->ex->execute_partial(ts);
+    Tensor t;
+    t.dtype = TQP_I64;
+    t.rows = p.words;
+    t.cols = 1;
+    t.buf = p.buf;
+    return wrap(std::move(t));
+  });
+}
+
+tqp_result* tqp_executor_finish(tqp_executor* ex, const void* const* parts, const int64_t* words, int nparts,
+                                tqp_status* st) {
+  return guard(st, [&] {
+    if (!ex) throw Error(TQP_ERR_ARG, "null executor");
+    if (nparts < 1 || !parts || !words) throw Error(TQP_ERR_ARG, "finish needs at least one partial");
+    std::vector<PartRef> refs;
+    for (int i = 0; i < nparts; ++i) refs.push_back({parts[i], words[i]});
+    auto* r = new tqp_result;
+    try {
+      r->r = ex->ex->finish(refs);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    for (auto& c : r->r.cols) r->handles.push_back(wrap(c.t));
+    return r;
+  });
+}
+
+int tqp_executor_shardable(tqp_executor* ex, const char** why) {
+  static thread_local std::string msg;
+  msg.clear();
+  const bool ok = ex && ex->ex->shardable(&msg);
+  if (!ex) msg = "null executor";
+  if (why) *why = msg.c_str();
+  return ok ? 1 : 0;
+}
+
 const char* tqp_executor_explain(tqp_executor* ex) { return ex ? ex->explain.c_str() : ""; }
 void tqp_executor_free(tqp_executor* ex) { delete ex; }
 void tqp_free_str(char* s) { std::free(s); }

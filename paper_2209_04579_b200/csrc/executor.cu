@@ -8,6 +8,7 @@
 #include <cctype>
 #include <cstring>
 #include <limits>
+#include <set>
 #include <sstream>
 
 #include "executor.hpp"
@@ -312,7 +313,7 @@ void Executor::reset_timings() {
   timings_.clear();
 }
 
-Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
+void Executor::check_inputs(const TableSet& tables) const {
   // bind and type-check the input tables (executor.cpp:355-371)
   for (const auto& it : plan_.input_tables) {
     const Table* t = bind_table(tables, it.name);
@@ -326,6 +327,10 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
       }
     }
   }
+}
+
+Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
+  check_inputs(tables);
   std::vector<std::optional<Tensor>> slots(plan_.num_slots);
   int64_t run_start = now_ns();
   size_t u = 0;
@@ -366,6 +371,10 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
     time_end("step:" + plan_.steps[s].kind, ev);
     ++s;
   }
+  return collect_outputs(slots);
+}
+
+Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots) {
   Result res;
   for (const auto& o : plan_.outputs) {
     if (!slots[o.slot]) exec_fail("internal: slot " + std::to_string(o.slot) + " read after release");
@@ -381,6 +390,74 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
   ctx_.sync();
   if (timing_) collect_kernel_events();
   return res;
+}
+
+// ---- sharded execution -------------------------------------------------------
+bool Executor::shardable(std::string* why) const {
+  auto no = [&](const std::string& m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (units_.empty() || !units_[0].partial) return no("the plan has no fused scan unit (run unsharded, or with fusion on)");
+  const FusedUnit& u = units_[0];
+  // steps before the unit only load columns or constants (their slots feed
+  // the unit alone); steps after it read the unit's outputs, never a table
+  std::set<int> before;
+  for (int s = 0; s < u.first_step; ++s) {
+    for (const auto& in : plan_.steps[s].instrs) {
+      if (in.op != Op::LoadColumn && in.op != Op::ConstTensor) return no("step " + plan_.steps[s].id + " runs before the fused unit");
+      before.insert(in.output);
+    }
+  }
+  for (size_t s = u.last_step + 1; s < plan_.steps.size(); ++s) {
+    for (const auto& in : plan_.steps[s].instrs) {
+      if (in.op == Op::LoadColumn) return no("step " + plan_.steps[s].id + " reads a table after the fused unit");
+      for (int x : in.inputs)
+        if (before.count(x)) return no("step " + plan_.steps[s].id + " reads a slot loaded before the fused unit");
+    }
+  }
+  for (const auto& o : plan_.outputs)
+    if (before.count(o.slot)) return no("a plan output is loaded before the fused unit");
+  return true;
+}
+
+Partial Executor::execute_partial(const TableSet& tables) {
+  std::string why;
+  if (!shardable(&why)) exec_fail("plan is not shardable: " + why);
+  check_inputs(tables);
+  const FusedUnit& u = units_[0];
+  cudaEvent_t ev;
+  time_begin(&ev);
+  Partial p;
+  if (!u.partial(ctx_, tables, &p)) {
+    if (ev) cudaEventDestroy(ev);
+    exec_fail(plan_.steps[u.last_step].id + ": this shard violates the fused path's preconditions "
+              "(non-unique or sparse build keys, an int64 overflow, or more than 8 groups per block); "
+              "run it unsharded");
+  }
+  time_end(u.name + ":partial", ev);
+  ctx_.sync();
+  if (timing_) collect_kernel_events();
+  return p;
+}
+
+Result Executor::finish(const std::vector<PartRef>& parts) {
+  std::string why;
+  if (!shardable(&why)) exec_fail("plan is not shardable: " + why);
+  const FusedUnit& u = units_[0];
+  std::vector<std::optional<Tensor>> slots(plan_.num_slots);
+  cudaEvent_t ev;
+  time_begin(&ev);
+  u.finish(ctx_, slots, parts);
+  time_end(u.name + ":merge", ev);
+  int64_t run_start = now_ns();
+  for (int s = u.last_step + 1; s < static_cast<int>(plan_.steps.size()); ++s) {
+    cudaEvent_t e2;
+    time_begin(&e2);
+    run_step(s, slots, TableSet{}, nullptr, run_start);
+    time_end("step:" + plan_.steps[s].kind, e2);
+  }
+  return collect_outputs(slots);
 }
 
 }  // namespace tqp

@@ -95,6 +95,17 @@ struct Result {
   int64_t rows = 0;
 };
 
+// Phase-1 state of a sharded run (fused.cu describes the word layout).
+struct Partial {
+  std::shared_ptr<DevBuf> buf;
+  int64_t words = 0;
+};
+// a partial as handed back for the merge (device pointer, any owner)
+struct PartRef {
+  const void* ptr = nullptr;
+  int64_t words = 0;
+};
+
 // A fused pipeline replaces a contiguous range of steps [first, last] and
 // writes the slots later instructions (or the plan outputs) read.
 struct FusedUnit {
@@ -105,12 +116,25 @@ struct FusedUnit {
   // (e.g. a fixed-point overflow or a non-unique build key); the executor
   // then runs the covered steps through the per-instruction path.
   std::function<bool(Ctx&, std::vector<std::optional<Tensor>>& slots, const TableSet& tables)> run;
+  // sharded runs: phase 1 writes this shard's partial state (false: the data
+  // violates the preconditions); phase 2 merges the parts of every shard
+  std::function<bool(Ctx&, const TableSet& tables, Partial* out)> partial;
+  std::function<void(Ctx&, std::vector<std::optional<Tensor>>& slots, const std::vector<PartRef>& parts)> finish;
 };
 
 class Executor {
  public:
   Executor(Ctx& ctx, Plan plan, unsigned flags);
   Result execute(const TableSet& tables, ProfileTrace* trace = nullptr);
+
+  // Sharded execution: every shard runs phase 1 over its
+  // rows of the fact table; the concatenated partials of all shards (rank
+  // order) go through finish() on any one of them. Requires the plan to be a
+  // single fused unit over the fact table plus steps that only read its
+  // outputs; shardable() says why not otherwise.
+  Partial execute_partial(const TableSet& tables);
+  Result finish(const std::vector<PartRef>& parts);
+  bool shardable(std::string* why = nullptr) const;
   const Plan& plan() const { return plan_; }
   std::string explain() const;
 
@@ -140,6 +164,8 @@ class Executor {
   void run_step(int s, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, ProfileTrace* trace,
                 int64_t run_start);
   void release_after(int s, std::vector<std::optional<Tensor>>& slots);
+  void check_inputs(const TableSet& tables) const;
+  Result collect_outputs(std::vector<std::optional<Tensor>>& slots);
 
   Ctx& ctx_;
   Plan plan_;

@@ -1078,7 +1078,7 @@ struct GroupSpec {
   FinalSpec f;
   const unsigned long long* gacc;
   const unsigned long long* gcnt;
-  const int* group_row;
+  const int* group_row;  // group -> build row; nullptr: merged groups (identity)
   int nkeyc;
   const long long* key_cols[kMaxKeys];  // root columns for the group keys
   int nsort;
@@ -1086,13 +1086,17 @@ struct GroupSpec {
   int sort_asc[4];
 };
 
+__device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g) {
+  return s.group_row ? s.group_row[g] : static_cast<long long>(g);
+}
+
 __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
                                                 bool& is_f64) {
   const OutKind& o = s.f.outs[j];
   const unsigned long long* acc = s.gacc + static_cast<long long>(g) * s.f.nacc * 2;
   long long cnt = static_cast<long long>(s.gcnt[g]);
   if (o.fn >= 10) {
-    bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][s.group_row[g]]);
+    bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][group_src_row(s, g)]);
     is_f64 = false;
     return true;
   }
@@ -1131,7 +1135,7 @@ __device__ __forceinline__ int cand_keys(const GroupSpec& s, unsigned g, unsigne
                              : radix_key(static_cast<int64_t>(bits));
     k[n++] = s.sort_asc[i] ? u : ~u;
   }
-  for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(s.key_cols[i][s.group_row[g]]));
+  for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(s.key_cols[i][group_src_row(s, g)]));
   return n;
 }
 
@@ -1299,7 +1303,68 @@ __global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, lon
 
 __global__ void k_group_keys(const int* __restrict__ group_row, const long long* __restrict__ gids, long long n,
                              const long long* __restrict__ key_col, long long* __restrict__ out) {
-  for (long long i = gtid(); i < n; i += gstride()) out[i] = key_col[group_row[gids[i]]];
+  for (long long i = gtid(); i < n; i += gstride()) out[i] = key_col[group_row ? group_row[gids[i]] : gids[i]];
+}
+
+// ---- sharded-run partials ------------------------------------------------------
+// A partial is a device buffer of u64 words: an 8-word header
+//   [magic, mode, nrec, words per record, nacc, nouts, nkeys, 0]
+// followed by nrec records: MODE_SCALAR per-CTA sums [kMaxAcc + 1];
+// MODE_SMALL per-CTA SmallPart; MODE_BUILDGRP one record per touched group
+//   [build key, group key columns..., count, (lo, hi) per accumulator].
+constexpr unsigned long long kPartMagic = 0x3154524150505154ULL;  // "TQPPART1"
+constexpr int kHdrWords = 8;
+constexpr int kSmallPartWords = static_cast<int>(sizeof(SmallPart) / sizeof(unsigned long long));
+static_assert(sizeof(SmallPart) % sizeof(unsigned long long) == 0, "SmallPart must be word-sized");
+constexpr int record_words(int nkeyc, int nacc) { return 2 + nkeyc + 2 * nacc; }
+
+__global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, long long n,
+                               const long long* __restrict__ bkey, int words, unsigned long long* __restrict__ out) {
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const unsigned g = static_cast<unsigned>(gids[i]);
+    const long long row = group_src_row(s, g);
+    unsigned long long* w = out + i * words;
+    w[0] = static_cast<unsigned long long>(bkey[row]);
+    for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(s.key_cols[k][row]);
+    w[1 + s.nkeyc] = s.gcnt[g];
+    const unsigned long long* acc = s.gacc + static_cast<long long>(g) * s.f.nacc * 2;
+    for (int a = 0; a < 2 * s.f.nacc; ++a) w[2 + s.nkeyc + a] = acc[a];
+  }
+}
+
+// records -> open-addressing table keyed by the build key (tag = key ^ 2^63,
+// 0 = empty); counts and Q64.64 sums add exactly, so the merge is
+// order-independent and equals the unsharded run bit for bit
+__global__ void k_merge_records(const unsigned long long* __restrict__ rec, long long n, int words, int nkeyc, int nacc,
+                                long long mask, unsigned long long* __restrict__ tag, long long* __restrict__ hbk,
+                                long long* __restrict__ hkeys, unsigned long long* __restrict__ hcnt,
+                                unsigned long long* __restrict__ hacc, long long* err) {
+  const long long cap = mask + 1;
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const unsigned long long* r = rec + i * words;
+    const unsigned long long t = r[0] ^ 0x8000000000000000ULL;
+    if (t == 0) {
+      err[0] = 1;
+      continue;
+    }
+    long long h = static_cast<long long>((r[0] * 0x9E3779B97F4A7C15ULL) >> 20) & mask;
+    unsigned long long prev;
+    for (;;) {
+      prev = atomicCAS(&tag[h], 0ULL, t);
+      if (prev == 0ULL || prev == t) break;
+      h = (h + 1) & mask;
+    }
+    if (prev == 0ULL) {
+      hbk[h] = static_cast<long long>(r[0]);
+      for (int k = 0; k < nkeyc; ++k) hkeys[k * cap + h] = static_cast<long long>(r[1 + k]);
+    }
+    atomicAdd(&hcnt[h], r[1 + nkeyc]);
+    for (int a = 0; a < nacc; ++a) {
+      const unsigned long long lo = r[2 + nkeyc + 2 * a], hi = r[3 + nkeyc + 2 * a];
+      const __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
+      atomic_add_q64(&hacc[(h * nacc + a) * 2], v);
+    }
+  }
 }
 
 // ---- unit runner ----------------------------------------------------------------
@@ -1490,6 +1555,11 @@ struct Runner {
   PipeDesc P;
 
   bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables) const {
+    return run(c, &slots, tables, nullptr);
+  }
+
+  // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
+  bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po) const {
     // build sides, children first (builds[] is in post-order by construction)
     auto err_buf = c.alloc_bytes(16);
     long long* err = static_cast<long long*>(err_buf->ptr);
@@ -1744,58 +1814,39 @@ struct Runner {
     };
 
     FinalSpec fs;
-    fs.nacc = ps.nacc;
-    for (int a = 0; a < ps.nacc; ++a) fs.acc_is_int[a] = ps.acc[a].is_int;
-    fs.nouts = static_cast<int>(P.outs.size());
-    if (fs.nouts > 16) return false;
-    for (int j = 0; j < fs.nouts; ++j) fs.outs[j] = {P.outs[j].fn, P.outs[j].acc, P.outs[j].is_int ? 1 : 0};
-
+    if (!final_spec(P, fs)) return false;
     const int grid = c.num_sms;  // persistent: one CTA per SM
-    auto out_dtype = [&](const OutDesc& o) {
-      if (o.fn >= 10) return P.mode == MODE_SMALL ? TQP_STR8 : TQP_I64;
-      if (o.fn == 1) return TQP_I64;
-      if (o.fn == 2) return TQP_F64;
-      return o.is_int ? TQP_I64 : TQP_F64;
-    };
     std::vector<Tensor> outs(P.outs.size());
     long long nrows = 0;
+    // phase 1 of a sharded run writes its partial state straight after the
+    // header; the local run merges it with the same phase-2 kernels (one part)
+    auto part_buf = [&](long long nrec, int words) {
+      auto buf = c.alloc_bytes(sizeof(unsigned long long) * (kHdrWords + nrec * words));
+      if (po) {
+        unsigned long long h[kHdrWords] = {kPartMagic,
+                                           static_cast<unsigned long long>(P.mode),
+                                           static_cast<unsigned long long>(nrec),
+                                           static_cast<unsigned long long>(words),
+                                           static_cast<unsigned long long>(fs.nacc),
+                                           static_cast<unsigned long long>(fs.nouts),
+                                           static_cast<unsigned long long>(P.key_columns.size()),
+                                           0};
+        TQP_CUDA(cudaMemcpyAsync(buf->ptr, h, sizeof(h), cudaMemcpyHostToDevice, c.stream));
+        po->buf = buf;
+        po->words = kHdrWords + nrec * words;
+      }
+      return static_cast<unsigned long long*>(buf->ptr) + kHdrWords;
+    };
 
     if (P.mode == MODE_SCALAR) {
-      auto part = c.alloc_bytes(sizeof(unsigned long long) * grid * (kMaxAcc + 1));
-      ps.part = static_cast<unsigned long long*>(part->ptr);
+      ps.part = part_buf(grid, kMaxAcc + 1);
       launch_tile(kfn, TileShape<MODE_SCALAR>::THREADS, grid);
-      for (size_t j = 0; j < outs.size(); ++j) {
-        outs[j] = c.alloc(out_dtype(P.outs[j]), 1, 1);
-        fs.out_ptr[j] = outs[j].data();
-      }
-      k_final_scalar<<<1, 32, 0, c.stream>>>(ps.part, grid, fs, err);
-      c.count_launch();
+      if (!po) final_scalar(c, ps.part, grid, fs, err, outs);
       nrows = 1;
     } else if (P.mode == MODE_SMALL) {
-      const int g2 = grid;
-      auto part = c.alloc_bytes(sizeof(SmallPart) * g2);
-      ps.part = static_cast<unsigned long long*>(part->ptr);
-      launch_tile(kfn, TileShape<MODE_SMALL>::THREADS, g2);
-      auto inv = c.alloc_bytes(sizeof(int) * g2 * kMerged);
-      auto ng = c.alloc_bytes(8);
-      std::vector<Tensor> tmp(P.outs.size());
-      for (size_t j = 0; j < outs.size(); ++j) {
-        tmp[j] = c.alloc(out_dtype(P.outs[j]), kMerged, 1);
-        fs.out_ptr[j] = tmp[j].data();
-      }
-      void* kp[4] = {nullptr, nullptr, nullptr, nullptr};
-      for (size_t j = 0; j < P.outs.size(); ++j)
-        if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = tmp[j].data();
-      k_final_small<<<1, kThreads, 0, c.stream>>>(reinterpret_cast<SmallPart*>(part->ptr), g2, fs, ps.nkeys, kp[0], kp[1],
-                                                  kp[2], kp[3], static_cast<int*>(inv->ptr),
-                                                  static_cast<long long*>(ng->ptr), err);
-      c.count_launch();
-      TQP_CUDA(cudaMemcpyAsync(&nrows, ng->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      for (size_t j = 0; j < outs.size(); ++j) {
-        outs[j] = tmp[j];
-        outs[j].rows = nrows;
-      }
+      ps.part = part_buf(grid, kSmallPartWords);
+      launch_tile(kfn, TileShape<MODE_SMALL>::THREADS, grid);
+      if (!po) nrows = final_small(c, reinterpret_cast<const SmallPart*>(ps.part), grid, fs, err, outs);
     } else {
       // MODE_BUILDGRP
       long long ngroups = build_rows[P.probes[P.group_probe].build];
@@ -1820,94 +1871,254 @@ struct Runner {
         if (!kc || kc->t.dtype != TQP_I64) return false;
         gs.key_cols[i] = kc->t.ptr<long long>();
       }
-      if (P.topk) {
-        gs.nsort = static_cast<int>(P.sort_outs.size());
-        for (int i = 0; i < gs.nsort; ++i) {
-          gs.sort_out[i] = P.sort_outs[i].first;
-          gs.sort_asc[i] = P.sort_outs[i].second;
-        }
-        // reference sort over NaN keys is an error: leave that to the exact path
-        int k = static_cast<int>(P.k);
-        std::vector<Tensor> tmp(P.outs.size());
-        for (size_t j = 0; j < outs.size(); ++j) {
-          tmp[j] = c.alloc(out_dtype(P.outs[j]), std::max(1, k), 1);
-          gs.f.out_ptr[j] = tmp[j].data();
-        }
-        const int nk = gs.nsort + gs.nkeyc;
-        auto cgid = c.alloc_bytes(sizeof(unsigned) * (ngroups + 1));
-        auto ckey = c.alloc_bytes(sizeof(unsigned long long) * nk * (ngroups + 1));
-        auto ncb = c.alloc_bytes(8);
-        TQP_CUDA(cudaMemsetAsync(ncb->ptr, 0, 8, c.stream));
-        if (ngroups) {
-          k_topk_cands<<<(ngroups + kThreads * 8 - 1) / (kThreads * 8), kThreads, 0, c.stream>>>(
-              gs, ngroups, static_cast<unsigned*>(cgid->ptr), static_cast<unsigned long long*>(ckey->ptr),
-              static_cast<unsigned*>(ncb->ptr));
-          c.count_launch();
-        }
-        unsigned ncand = 0;
-        TQP_CUDA(cudaMemcpyAsync(&ncand, ncb->ptr, 4, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        const long long chunk = static_cast<long long>(kThreads) * 4;
-        const long long nblk = (static_cast<long long>(ncand) + chunk - 1) / chunk;
-        const long long nwin = nblk * k;
-        if (nwin > static_cast<long long>(kThreads) * kTopkMaxPerThread) return false;
-        auto win = c.alloc_bytes(sizeof(long long) * std::max<long long>(1, nwin));
-        auto scratch = c.alloc_bytes(sizeof(unsigned long long) * nk * std::max<long long>(1, nwin));
-        auto nout = c.alloc_bytes(8);
-        if (k > 0 && ncand > 0) {
-          k_topk_local<<<nblk, kThreads, 0, c.stream>>>(static_cast<unsigned long long*>(ckey->ptr), nk, ncand, chunk, k,
-                                                       static_cast<long long*>(win->ptr));
-          k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned long long*>(ckey->ptr),
-                                                     static_cast<unsigned*>(cgid->ptr), static_cast<long long*>(win->ptr),
-                                                     nwin, k, static_cast<unsigned long long*>(scratch->ptr),
-                                                     static_cast<long long*>(nout->ptr), err);
-          c.count_launch(2);
-          TQP_CUDA(cudaMemcpyAsync(&nrows, nout->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
-        }
-        c.sync();
-        for (size_t j = 0; j < outs.size(); ++j) {
-          outs[j] = tmp[j];
-          outs[j].rows = nrows;
-        }
-      } else {
-        // every group, ascending by the (unique) build key
-        Tensor cnt_view;
-        cnt_view.dtype = TQP_I64;
-        cnt_view.rows = ngroups;
-        cnt_view.buf = gcnt;
-        Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
-        if (ngroups) {
-          k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(ps.gcnt, ngroups, mask.ptr<uint8_t>());
-          c.count_launch();
-        }
-        Tensor gids = k::compact(c, k::iota(c, ngroups), mask);
-        long long n = gids.rows;
-        Tensor keys = c.alloc(TQP_I64, n, 1);
-        const Column* bk = groot->find(gb.key_column);
+      const Column* bk = groot->find(gb.key_column);
+      if (po) {
+        // the touched groups as self-describing records, keyed by the unique
+        // build key: shards may split a group (the merge adds exactly)
+        Tensor gids = touched_groups(c, ps.gcnt, ngroups);
+        const long long n = gids.rows;
+        const int words = record_words(gs.nkeyc, fs.nacc);
+        unsigned long long* rec = part_buf(n, words);
         if (n) {
-          k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(group_row, gids.ptr<long long>(), n, bk->t.ptr<long long>(),
-                                                                  keys.ptr<long long>());
+          k_fill_records<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(), n, bk->t.ptr<long long>(),
+                                                                  words, rec);
           c.count_launch();
         }
-        Tensor order = k::radix_sort_payload(c, keys, &gids, false);
-        for (size_t j = 0; j < outs.size(); ++j) {
-          outs[j] = c.alloc(out_dtype(P.outs[j]), n, 1);
-          gs.f.out_ptr[j] = outs[j].data();
-        }
-        if (n) {
-          k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, order.ptr<long long>(), n, err);
-          c.count_launch();
-        }
-        nrows = n;
+      } else if (!emit_groups(c, gs, ngroups, bk->t.ptr<long long>(), err, outs, nrows)) {
+        return false;
       }
     }
     long long herr[2] = {0, 0};
     TQP_CUDA(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
-    if (herr[0]) return false;  // preconditions violated: exact per-instruction path
-    (void)nrows;
-    for (size_t i = 0; i < P.final_slots.size(); ++i) slots[P.final_slots[i]] = outs[P.final_cols[i]];
+    if (herr[0]) {  // preconditions violated: exact per-instruction path
+      if (po) *po = Partial{};
+      return false;
+    }
+    if (po) return true;
+    for (size_t j = 0; j < outs.size(); ++j) outs[j].rows = nrows;
+    for (size_t i = 0; i < P.final_slots.size(); ++i) (*slots)[P.final_slots[i]] = outs[P.final_cols[i]];
     return true;
+  }
+
+  // ---- shared phase-2 pieces -----------------------------------------------------
+  static int out_dtype(const PipeDesc& P, const OutDesc& o) {
+    if (o.fn >= 10) return P.mode == MODE_SMALL ? TQP_STR8 : TQP_I64;
+    if (o.fn == 1) return TQP_I64;
+    if (o.fn == 2) return TQP_F64;
+    return o.is_int ? TQP_I64 : TQP_F64;
+  }
+
+  bool final_spec(const PipeDesc& P_, FinalSpec& fs) const {
+    fs.nacc = static_cast<int>(P_.accs.size());
+    if (fs.nacc > kMaxAcc) return false;
+    for (int a = 0; a < fs.nacc; ++a) fs.acc_is_int[a] = P_.accs[a].is_int;
+    fs.nouts = static_cast<int>(P_.outs.size());
+    if (fs.nouts > 16) return false;
+    for (int j = 0; j < fs.nouts; ++j) fs.outs[j] = {P_.outs[j].fn, P_.outs[j].acc, P_.outs[j].is_int ? 1 : 0};
+    return true;
+  }
+
+  void final_scalar(Ctx& c, const unsigned long long* part, long long nparts, FinalSpec fs, long long* err,
+                    std::vector<Tensor>& outs) const {
+    for (size_t j = 0; j < outs.size(); ++j) {
+      outs[j] = c.alloc(out_dtype(P, P.outs[j]), 1, 1);
+      fs.out_ptr[j] = outs[j].data();
+    }
+    k_final_scalar<<<1, 32, 0, c.stream>>>(part, nparts, fs, err);
+    c.count_launch();
+  }
+
+  long long final_small(Ctx& c, const SmallPart* parts, long long nparts, FinalSpec fs, long long* err,
+                        std::vector<Tensor>& outs) const {
+    auto inv = c.alloc_bytes(sizeof(int) * nparts * kMerged);
+    auto ng = c.alloc_bytes(8);
+    for (size_t j = 0; j < outs.size(); ++j) {
+      outs[j] = c.alloc(out_dtype(P, P.outs[j]), kMerged, 1);
+      fs.out_ptr[j] = outs[j].data();
+    }
+    void* kp[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (size_t j = 0; j < P.outs.size(); ++j)
+      if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = outs[j].data();
+    k_final_small<<<1, kThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
+                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(inv->ptr),
+                                                static_cast<long long*>(ng->ptr), err);
+    c.count_launch();
+    long long nrows = 0;
+    TQP_CUDA(cudaMemcpyAsync(&nrows, ng->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return nrows;
+  }
+
+  static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long ngroups) {
+    Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
+    if (ngroups) {
+      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, ngroups, mask.ptr<uint8_t>());
+      c.count_launch();
+    }
+    return k::compact(c, k::iota(c, ngroups), mask);
+  }
+
+  // group outputs: top-k in the reference's tie order, or every group
+  // ascending by the (unique) build key `bk` (indexed like the key columns)
+  bool emit_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
+                   std::vector<Tensor>& outs, long long& nrows) const {
+    if (P.topk) {
+      gs.nsort = static_cast<int>(P.sort_outs.size());
+      for (int i = 0; i < gs.nsort; ++i) {
+        gs.sort_out[i] = P.sort_outs[i].first;
+        gs.sort_asc[i] = P.sort_outs[i].second;
+      }
+      // reference sort over NaN keys is an error: leave that to the exact path
+      int k = static_cast<int>(P.k);
+      for (size_t j = 0; j < outs.size(); ++j) {
+        outs[j] = c.alloc(out_dtype(P, P.outs[j]), std::max(1, k), 1);
+        gs.f.out_ptr[j] = outs[j].data();
+      }
+      const int nk = gs.nsort + gs.nkeyc;
+      auto cgid = c.alloc_bytes(sizeof(unsigned) * (ngroups + 1));
+      auto ckey = c.alloc_bytes(sizeof(unsigned long long) * nk * (ngroups + 1));
+      auto ncb = c.alloc_bytes(8);
+      TQP_CUDA(cudaMemsetAsync(ncb->ptr, 0, 8, c.stream));
+      if (ngroups) {
+        k_topk_cands<<<(ngroups + kThreads * 8 - 1) / (kThreads * 8), kThreads, 0, c.stream>>>(
+            gs, ngroups, static_cast<unsigned*>(cgid->ptr), static_cast<unsigned long long*>(ckey->ptr),
+            static_cast<unsigned*>(ncb->ptr));
+        c.count_launch();
+      }
+      unsigned ncand = 0;
+      TQP_CUDA(cudaMemcpyAsync(&ncand, ncb->ptr, 4, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      const long long chunk = static_cast<long long>(kThreads) * 4;
+      const long long nblk = (static_cast<long long>(ncand) + chunk - 1) / chunk;
+      const long long nwin = nblk * k;
+      if (nwin > static_cast<long long>(kThreads) * kTopkMaxPerThread) return false;
+      auto win = c.alloc_bytes(sizeof(long long) * std::max<long long>(1, nwin));
+      auto scratch = c.alloc_bytes(sizeof(unsigned long long) * nk * std::max<long long>(1, nwin));
+      auto nout = c.alloc_bytes(8);
+      nrows = 0;
+      if (k > 0 && ncand > 0) {
+        k_topk_local<<<nblk, kThreads, 0, c.stream>>>(static_cast<unsigned long long*>(ckey->ptr), nk, ncand, chunk, k,
+                                                     static_cast<long long*>(win->ptr));
+        k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned long long*>(ckey->ptr),
+                                                   static_cast<unsigned*>(cgid->ptr), static_cast<long long*>(win->ptr),
+                                                   nwin, k, static_cast<unsigned long long*>(scratch->ptr),
+                                                   static_cast<long long*>(nout->ptr), err);
+        c.count_launch(2);
+        TQP_CUDA(cudaMemcpyAsync(&nrows, nout->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
+      }
+      c.sync();
+      return true;
+    }
+    Tensor gids = touched_groups(c, gs.gcnt, ngroups);
+    const long long n = gids.rows;
+    Tensor keys = c.alloc(TQP_I64, n, 1);
+    if (n) {
+      k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_row, gids.ptr<long long>(), n, bk,
+                                                              keys.ptr<long long>());
+      c.count_launch();
+    }
+    Tensor order = k::radix_sort_payload(c, keys, &gids, false);
+    for (size_t j = 0; j < outs.size(); ++j) {
+      outs[j] = c.alloc(out_dtype(P, P.outs[j]), n, 1);
+      gs.f.out_ptr[j] = outs[j].data();
+    }
+    if (n) {
+      k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, order.ptr<long long>(), n, err);
+      c.count_launch();
+    }
+    nrows = n;
+    return true;
+  }
+
+  // ---- phase 2 of a sharded run: merge the parts (in the given order) ----------
+  void finish(Ctx& c, std::vector<std::optional<Tensor>>& slots, const std::vector<PartRef>& parts,
+              const std::string& where) const {
+    FinalSpec fs;
+    if (!final_spec(P, fs)) throw Error(TQP_ERR_EXEC, where + ": unit has no partial form");
+    const int nkeyc = static_cast<int>(P.group_key_root_columns.size());
+    const long long want_words = P.mode == MODE_SCALAR  ? kMaxAcc + 1
+                                 : P.mode == MODE_SMALL ? kSmallPartWords
+                                                        : record_words(nkeyc, fs.nacc);
+    if (parts.empty()) throw Error(TQP_ERR_ARG, where + ": no partials to merge");
+    long long total = 0;
+    std::vector<long long> nrec(parts.size());
+    for (size_t i = 0; i < parts.size(); ++i) {
+      unsigned long long h[kHdrWords];
+      if (!parts[i].ptr || parts[i].words < kHdrWords) throw Error(TQP_ERR_ARG, where + ": partial " + std::to_string(i) + " is truncated");
+      TQP_CUDA(cudaMemcpyAsync(h, parts[i].ptr, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (h[0] != kPartMagic || h[1] != static_cast<unsigned long long>(P.mode) ||
+          h[3] != static_cast<unsigned long long>(want_words) || h[4] != static_cast<unsigned long long>(fs.nacc) ||
+          h[5] != static_cast<unsigned long long>(fs.nouts) || h[6] != P.key_columns.size()) {
+        throw Error(TQP_ERR_ARG, where + ": partial " + std::to_string(i) + " was not produced by this plan");
+      }
+      nrec[i] = static_cast<long long>(h[2]);
+      if (kHdrWords + nrec[i] * want_words > parts[i].words)
+        throw Error(TQP_ERR_ARG, where + ": partial " + std::to_string(i) + " is truncated");
+      total += nrec[i];
+    }
+    auto cat = c.alloc_bytes(sizeof(unsigned long long) * std::max<long long>(1, total * want_words));
+    unsigned long long* catp = static_cast<unsigned long long*>(cat->ptr);
+    long long off = 0;
+    for (size_t i = 0; i < parts.size(); ++i) {
+      if (nrec[i])
+        TQP_CUDA(cudaMemcpyAsync(catp + off * want_words, static_cast<const unsigned long long*>(parts[i].ptr) + kHdrWords,
+                                 sizeof(unsigned long long) * nrec[i] * want_words, cudaMemcpyDeviceToDevice, c.stream));
+      off += nrec[i];
+    }
+    auto err_buf = c.alloc_bytes(16);
+    long long* err = static_cast<long long*>(err_buf->ptr);
+    TQP_CUDA(cudaMemsetAsync(err, 0, 16, c.stream));
+    std::vector<Tensor> outs(P.outs.size());
+    long long nrows = 0;
+    bool ok = true;
+    std::vector<std::shared_ptr<DevBuf>> keep;
+    if (P.mode == MODE_SCALAR) {
+      final_scalar(c, catp, total, fs, err, outs);
+      nrows = 1;
+    } else if (P.mode == MODE_SMALL) {
+      nrows = final_small(c, reinterpret_cast<const SmallPart*>(catp), total, fs, err, outs);
+    } else {
+      // open-addressing table keyed by the build key, at most half full
+      long long cap = 1024;
+      while (cap < 2 * total) cap <<= 1;
+      const int nacc = std::max(1, fs.nacc);
+      auto htag = c.alloc_bytes(sizeof(unsigned long long) * cap);
+      auto hbk = c.alloc_bytes(sizeof(long long) * cap);
+      auto hkeys = c.alloc_bytes(sizeof(long long) * cap * std::max(1, nkeyc));
+      auto hcnt = c.alloc_bytes(sizeof(unsigned long long) * cap);
+      auto hacc = c.alloc_bytes(sizeof(unsigned long long) * 2 * nacc * cap);
+      keep = {htag, hbk, hkeys, hcnt, hacc};
+      for (auto& b : {htag, hcnt, hacc}) TQP_CUDA(cudaMemsetAsync(b->ptr, 0, b->bytes, c.stream));
+      if (total) {
+        k_merge_records<<<c.grid_for(total, 256), 256, 0, c.stream>>>(
+            catp, total, static_cast<int>(want_words), nkeyc, fs.nacc, cap - 1,
+            static_cast<unsigned long long*>(htag->ptr), static_cast<long long*>(hbk->ptr),
+            static_cast<long long*>(hkeys->ptr), static_cast<unsigned long long*>(hcnt->ptr),
+            static_cast<unsigned long long*>(hacc->ptr), err);
+        c.count_launch();
+      }
+      GroupSpec gs;
+      gs.f = fs;
+      gs.gacc = static_cast<unsigned long long*>(hacc->ptr);
+      gs.gcnt = static_cast<unsigned long long*>(hcnt->ptr);
+      gs.group_row = nullptr;
+      gs.nkeyc = nkeyc;
+      for (int i = 0; i < nkeyc; ++i) gs.key_cols[i] = static_cast<const long long*>(hkeys->ptr) + i * cap;
+      ok = emit_groups(c, gs, cap, static_cast<const long long*>(hbk->ptr), err, outs, nrows);
+    }
+    long long herr[2] = {0, 0};
+    TQP_CUDA(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (!ok || herr[0]) {
+      // the local path would re-run these steps per instruction; merged
+      // partials cannot, so report what the exact path raises
+      throw Error(TQP_ERR_EXEC, where + ": merged partials violate the fused preconditions "
+                                        "(AVG over zero rows, more than 256 groups, or an int64 overflow)");
+    }
+    for (size_t j = 0; j < outs.size(); ++j) outs[j].rows = nrows;
+    for (size_t i = 0; i < P.final_slots.size(); ++i) slots[P.final_slots[i]] = outs[P.final_cols[i]];
   }
 };
 
@@ -1962,7 +2173,13 @@ std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
     u.last_step = P.last_step;
     u.name = std::string("fused_") + (P.probes.empty() ? "scan_" : "probe_") + mode + (P.topk ? "_topk" : "");
     u.explain = ex.str();
-    u.run = Runner{P};
+    auto R = std::make_shared<Runner>(Runner{P});
+    u.run = [R](Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& t) { return (*R)(c, slots, t); };
+    u.partial = [R](Ctx& c, const TableSet& t, Partial* out) { return R->run(c, nullptr, t, out); };
+    const std::string where = plan.steps[P.last_step].id;
+    u.finish = [R, where](Ctx& c, std::vector<std::optional<Tensor>>& slots, const std::vector<PartRef>& parts) {
+      R->finish(c, slots, parts, where);
+    };
     units.push_back(std::move(u));
     next_free = P.last_step + 1;
   }

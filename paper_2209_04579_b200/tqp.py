@@ -135,6 +135,9 @@ def _load() -> C.CDLL:
         "tqp_executor_explain": (C.c_char_p, [P]), "tqp_executor_free": (None, [P]),
         "tqp_executor_set_timing": (None, [P, I]), "tqp_executor_timings": (C.c_char_p, [P]),
         "tqp_executor_reset_timings": (None, [P]),
+        "tqp_executor_shardable": (I, [P, C.POINTER(C.c_char_p)]),
+        "tqp_executor_execute_partial": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, S]),
+        "tqp_executor_finish": (P, [P, C.POINTER(P), C.POINTER(I64_), I, S]),
         "tqp_free_str": (None, [P]),
         "tqp_result_rows": (I64_, [P]), "tqp_result_num_columns": (I, [P]),
         "tqp_result_column_name": (C.c_char_p, [P, I]), "tqp_result_column_type": (I, [P, I]),
@@ -254,6 +257,17 @@ class Tensor:
 
     def data_ptr(self) -> int:
         return lib.tqp_tensor_data(self.h) or 0
+
+    @property
+    def __cuda_array_interface__(self) -> dict:
+        """Zero-copy view for torch.as_tensor (fixed-width dtypes only); the
+        producer stream is synchronised before the view is handed out."""
+        if self.dtype == STR8:
+            raise TypeError("STR8 tensors have no fixed-width array view")
+        self.ctx.sync()
+        typestr = {BOOL: "|u1", I32: "<i4", I64: "<i8", F64: "<f8"}[self.dtype]
+        return {"shape": (self.rows, self.cols), "typestr": typestr, "data": (self.data_ptr(), False),
+                "version": 3, "strides": None, "stream": None}
 
     def numpy(self, widen_strings: bool = True) -> np.ndarray:
         """Host copy; STR8 widens to the reference's Int32-per-byte layout."""
@@ -643,6 +657,42 @@ class Executor:
         cn, th, n = self._args(tables)
         st = Status()
         h = lib.tqp_executor_execute(self.h, cn, th, n, C.byref(st))
+        _check(st, bool(h))
+        return Result(h, self.ctx)
+
+    # ---- sharded execution; see distributed.py ----
+    def shardable(self) -> Tuple[bool, str]:
+        why = C.c_char_p()
+        ok = lib.tqp_executor_shardable(self.h, C.byref(why))
+        return bool(ok), (why.value or b"").decode()
+
+    def execute_partial(self, tables: Mapping[str, Table]) -> Tensor:
+        """Phase 1 over this shard's tables: an opaque I64-word device tensor."""
+        cn, th, n = self._args(tables)
+        st = Status()
+        h = lib.tqp_executor_execute_partial(self.h, cn, th, n, C.byref(st))
+        _check(st, bool(h))
+        return Tensor(h, self.ctx)
+
+    def finish(self, parts: Sequence) -> Result:
+        """Phase 2: merge the partials of every shard (in shard order). Each
+        part is a tqp Tensor or a CUDA tensor of int64 words (e.g. from an
+        NCCL all-gather); the caller keeps them alive and synchronised."""
+        ptrs, words = [], []
+        for p in parts:
+            if isinstance(p, Tensor):
+                ptrs.append(p.data_ptr())
+                words.append(p.rows * p.cols)
+            else:  # torch.Tensor on this device
+                if not p.is_cuda or p.dtype.itemsize != 8 or not p.is_contiguous():
+                    raise TypeError("partials must be contiguous 8-byte CUDA tensors")
+                ptrs.append(p.data_ptr())
+                words.append(p.numel())
+        n = len(ptrs)
+        pa = (C.c_void_p * max(1, n))(*ptrs)
+        wa = (C.c_int64 * max(1, n))(*words)
+        st = Status()
+        h = lib.tqp_executor_finish(self.h, pa, wa, n, C.byref(st))
         _check(st, bool(h))
         return Result(h, self.ctx)
 
