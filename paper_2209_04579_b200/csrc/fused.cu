@@ -1820,8 +1820,10 @@ struct Runner {
     long long nrows = 0;
     // phase 1 of a sharded run writes its partial state straight after the
     // header; the local run merges it with the same phase-2 kernels (one part)
+    std::shared_ptr<DevBuf> part_keep;  // alive until the merge has read it
     auto part_buf = [&](long long nrec, int words) {
       auto buf = c.alloc_bytes(sizeof(unsigned long long) * (kHdrWords + nrec * words));
+      part_keep = buf;
       if (po) {
         unsigned long long h[kHdrWords] = {kPartMagic,
                                            static_cast<unsigned long long>(P.mode),
