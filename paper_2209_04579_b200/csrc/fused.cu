@@ -21,6 +21,7 @@
 
 #include "executor.hpp"
 #include "fused_kernels.cuh"
+#include "jit.hpp"
 #include "scan.cuh"
 
 namespace tqp {
@@ -1551,6 +1552,132 @@ const void* tile_kernel(int mode, int nacc) {
   return nullptr;
 }
 
+// ---- run-time specialised pipeline kernels (jit.cu) ------------------------------
+// The generic k_tile reads its pipeline description from shared memory and
+// dispatches per term / factor at run time. For large scans the same pipeline
+// is emitted as straight-line CUDA with every offset, bound and coefficient a
+// literal, compiled once per process by NVRTC and run with the identical
+// staging skeleton and partial layouts (jit_tile.cuh). The generated code keeps
+// k_tile's exact floating-point operation order (__dadd_rn/__dmul_rn, no FMA
+// contraction), so both kernels produce the same bits.
+std::string hex64(unsigned long long v) {
+  char b[40];
+  std::snprintf(b, sizeof(b), "0x%016llxULL", v);
+  return b;
+}
+std::string dlit(double d) {
+  unsigned long long u;
+  std::memcpy(&u, &d, 8);
+  return "__longlong_as_double((long long)" + hex64(u) + ")";
+}
+
+bool jit_wanted(long long rows) {
+  const char* e = std::getenv("TQP_JIT");
+  if (e && (e[0] == '0' || e[0] == 'n')) return false;
+  if (e && (e[0] == '1' || e[0] == 'a' || e[0] == 'y')) return true;
+  return rows >= (1LL << 20);  // below this the NVRTC compile is not worth it
+}
+
+std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<bool>& probe_bitmap) {
+  const ProbeSpec& s = ts.p;
+  std::ostringstream o;
+  unsigned int_mask = 0;
+  for (int a = 0; a < s.nacc; ++a)
+    if (s.acc[a].is_int) int_mask |= 1u << a;
+  o << "#include \"fz_layout.cuh\"\n"
+    << "#define Q_MODE " << mode << "\n#define Q_NA " << s.nacc << "\n#define Q_ROWS " << ts.rows << "\n#define Q_CW "
+    << cw << "\n#define Q_INT_MASK " << int_mask << "u\n"
+    << "namespace tqp { namespace fz {\n"
+    << "__device__ __forceinline__ unsigned long long q_u64(const unsigned char* st, unsigned off, int ri) {\n"
+    << "  return *reinterpret_cast<const unsigned long long*>(st + off + ri * 8); }\n"
+    << "__device__ __forceinline__ double q_f64(const unsigned char* st, unsigned off, int ri) {\n"
+    << "  return __longlong_as_double(static_cast<long long>(q_u64(st, off, ri))); }\n"
+    << "__device__ __forceinline__ bool q_row(const TileSpec& t, const unsigned char* __restrict__ stage, int ri, bool valid,\n"
+    << "    unsigned long long* v, unsigned& code, unsigned& gid, long long& absmax) {\n"
+    << "  bool pass = valid;\n";
+  auto off = [&](int col) { return std::to_string(ts.col_off[col]) + "u"; };
+  for (int i = 0; i < s.nterms; ++i) {
+    const RTerm& t = s.terms[i];
+    switch (t.kind) {
+      case RK_INT:
+        o << "  pass = pass && (q_u64(stage, " << off(t.col) << ", ri) - " << hex64(t.lo) << ") <= " << hex64(t.hi - t.lo)
+          << ";\n";
+        break;
+      case RK_F64: {
+        double lo, hi;
+        std::memcpy(&lo, &t.lo, 8);
+        std::memcpy(&hi, &t.hi, 8);
+        o << "  { const double x = q_f64(stage, " << off(t.col) << ", ri); pass = pass && x >= " << dlit(lo)
+          << " && x <= " << dlit(hi) << "; }\n";
+        break;
+      }
+      case RK_INT_NE: o << "  pass = pass && q_u64(stage, " << off(t.col) << ", ri) != " << hex64(t.lo) << ";\n"; break;
+      case RK_F64_NE: {
+        double k;
+        std::memcpy(&k, &t.lo, 8);
+        o << "  pass = pass && q_f64(stage, " << off(t.col) << ", ri) != " << dlit(k) << ";\n";
+        break;
+      }
+      case RK_TRUE: break;
+      default: o << "  pass = false;\n"; break;
+    }
+  }
+  for (int p = 0; p < s.nprobes; ++p) {
+    // branch-free: the loads of all of a thread's rows issue back to back
+    o << "  unsigned fl" << p << " = 0u, gid" << p << " = 0u;\n"
+      << "  { const Probe& pr = t.p.probes[" << p << "];\n"
+      << "    const long long idx = static_cast<long long>(q_u64(stage, " << off(s.probes[p].key.col) << ", ri)) - pr.kmin;\n"
+      << "    bool in = pass && static_cast<unsigned long long>(idx) < static_cast<unsigned long long>(pr.range);\n";
+    if (probe_bitmap[p])
+      o << "    const unsigned w = in ? __ldg(pr.bitmap + (idx >> 5)) : 0u;\n"
+        << "    in = in && ((w >> (idx & 31)) & 1u);\n";
+    o << "    const unsigned long long e = in ? __ldg(pr.table + idx) : 0ULL;\n"
+      << "    pass = pass && e != 0ULL;\n"
+      << "    gid" << p << " = static_cast<unsigned>((e >> 32) & 0x1ffffffULL);\n"
+      << "    fl" << p << " = static_cast<unsigned>(e >> 57); }\n";
+  }
+  if (mode == MODE_BUILDGRP) {
+    if (s.group_probe < 0 || s.group_probe >= s.nprobes) throw Error(TQP_ERR_EXEC, "internal: build-group pipeline without a group probe");
+    o << "  gid = gid" << s.group_probe << ";\n";
+  }
+  if (mode == MODE_SMALL) {
+    o << "  code = 0u;\n";
+    for (int q = 0; q < s.nkeys; ++q)
+      o << "  code = (code << 8) | stage[" << ts.col_off[s.keys[q].col] << "u + ri];\n";
+  }
+  for (int a = 0; a < s.nacc; ++a) {
+    const Acc& A = s.acc[a];
+    if (A.is_int) {
+      o << "  { const unsigned long long x = pass ? q_u64(stage, " << off(A.f[0].x.col) << ", ri) : 0ULL;\n"
+        << "    long long iv = static_cast<long long>(x); iv = iv < 0 ? -iv : iv; absmax = iv > absmax ? iv : absmax;\n"
+        << "    v[" << a << "] = x; }\n";
+      o << "  const double d" << a << " = 1.0;\n";
+      continue;
+    }
+    std::string prod = A.base >= 0 ? "d" + std::to_string(A.base) : "";
+    for (int i = 0; i < A.nf; ++i) {
+      const Factor& f = A.f[i];
+      std::string x = f.kind != FK_CONST && f.x.col >= 0 ? "q_f64(stage, " + off(f.x.col) + ", ri)" : "0.0";
+      std::string y;
+      if (f.kind == FK_CONST) y = dlit(f.fa + 0.0);  // k_tile: fa + 0 * 0
+      else if (f.fa == 0.0 && f.fb == 1.0) y = x;
+      else if (f.fb == 1.0) y = "__dadd_rn(" + dlit(f.fa) + ", " + x + ")";
+      else if (f.fb == -1.0) y = "__dsub_rn(" + dlit(f.fa) + ", " + x + ")";
+      else y = "__dadd_rn(" + dlit(f.fa) + ", __dmul_rn(" + dlit(f.fb) + ", " + x + "))";
+      prod = prod.empty() ? y : "__dmul_rn(" + prod + ", " + y + ")";
+    }
+    if (prod.empty()) prod = "1.0";
+    o << "  const double d" << a << " = " << prod << ";\n";
+    o << "  { double g = d" << a << ";\n";
+    if (A.gate_probe >= 0)
+      o << "    if (!((fl" << A.gate_probe << " >> " << A.gate_bit << ") & 1u)) g = " << dlit(A.gate_else) << ";\n";
+    o << "    v[" << a << "] = pass ? static_cast<unsigned long long>(__double_as_longlong(g)) : 0ULL; }\n";
+  }
+  o << "  (void)code; (void)gid; (void)absmax;\n  return pass;\n}\n}}  // namespace tqp::fz\n"
+    << "#include \"jit_tile.cuh\"\n";
+  return o.str();
+}
+
 struct Runner {
   PipeDesc P;
 
@@ -1708,6 +1835,7 @@ struct Runner {
       d.gate_else = a.gate_else;
     }
     for (const auto& kcol : P.key_columns) ps.keys[ps.nkeys++] = make_operand(tables, P, {-1, kcol}, &ok);
+    ps.group_probe = P.mode == MODE_BUILDGRP ? P.group_probe : -1;
     if (!ok) return false;
     // prefix sharing: an fp64 accumulator whose leading factors equal another
     // (earlier, ungated) accumulator's whole product starts from that value:
@@ -1789,12 +1917,24 @@ struct Runner {
     const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
     const void* kfn = tile_kernel(P.mode, ps.nacc);
     if (!kfn) return false;
+    const bool jit = jit_wanted(ps.n);
+    if (jit) {
+      // presence bitmaps only pay off in front of filtered build sides
+      std::vector<bool> bm;
+      for (const auto& pd : P.probes) {
+        const BuildDesc& B = P.builds[pd.build];
+        bm.push_back(!B.terms.empty() || !B.children.empty());
+      }
+      ts.p = ps;
+      const int cw = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
+      kfn = jit_kernel(gen_pipeline(ts, P.mode, cw, bm), "q_tile");
+    }
     TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
     if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
     ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
     const size_t smem = fixed + static_cast<size_t>(ts.stages) * ts.stage_bytes;
-    const std::string tile_name = std::string("k_tile<") +
+    const std::string tile_name = std::string(jit ? "q_tile<" : "k_tile<") +
                                   (P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small" : "buildgrp") + "," +
                                   std::to_string(ps.nacc) + ">";
     auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {

@@ -1,0 +1,444 @@
+// Shared layouts and device helpers of the fused fact-scan pipelines.
+// Compiled twice: into libtqp_b200.so (fused_kernels.cuh) and, embedded as a
+// string, into every specialised pipeline kernel NVRTC builds at run time
+// (jit.cu), so the host-filled TileSpec and both kernels share one layout.
+// Self-contained: no CUDA runtime or C++ library headers.
+#pragma once
+
+#include <stdint.h>
+
+#include "tqp_b200.h"
+
+namespace tqp {
+namespace fz {
+
+constexpr int kMaxTerms = 8;
+constexpr int kMaxProbes = 3;
+constexpr int kMaxAcc = 8;
+constexpr int kMaxFactors = 4;
+constexpr int kMaxKeys = 4;
+constexpr int kMaxStrTerms = 4;
+constexpr int kMaxFlags = 7;
+constexpr int kGroups = 8;  // MODE_SMALL per-CTA slot capacity (register accumulators)
+constexpr int kGroupBits = 3;
+constexpr int kMaxAccSmall = 6;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+enum OperandType : int { OT_I64 = 0, OT_F64 = 1, OT_U8 = 2 };
+enum TermKind : int { TK_INT = 0, TK_F64 = 1, TK_TRUE = 2, TK_FALSE = 3 };
+enum FactorKind : int { FK_X = 0, FK_K_MINUS_X, FK_K_PLUS_X, FK_X_MINUS_K, FK_X_PLUS_K, FK_X_TIMES_K, FK_CONST };
+enum Mode : int { MODE_SCALAR = 0, MODE_SMALL = 1, MODE_BUILDGRP = 2 };
+
+// A per-row operand: fact column (src = -1) or a column of the build-side
+// root row matched by probe `src`.
+struct Operand {
+  const void* ptr = nullptr;
+  int type = OT_I64;
+  int src = -1;
+  int col = -1;  // fact operands: column index in the staged tile
+};
+
+struct Term {
+  Operand x;
+  int kind = TK_TRUE;
+  int op = TQP_EQ;
+  long long ik = 0;
+  double fk = 0.0;
+};
+
+// string predicate over STR8 rows: compare with a literal (zero-extended, as
+// string_compare_rows, executor.cpp:72-108) or LIKE (substring_match,
+// kernels.cpp:692-728)
+struct StrTerm {
+  const uint8_t* ptr = nullptr;
+  int width = 1;
+  int is_like = 0;
+  int op = TQP_EQ;      // compare op when !is_like
+  int anchor = TQP_START;
+  int litlen = 0;
+  unsigned char lit[48];
+};
+
+// factor = fa + fb * x, evaluated branch-free (fa/fb derived from `kind`):
+// K - x == K + (-1)x and 1 * x == x exactly; padding factors are 1 + 0 * 0
+struct Factor {
+  Operand x;
+  int kind = FK_X;
+  double k = 0.0;
+  double fa = 1.0, fb = 0.0;
+};
+constexpr int kFixedFactors = 3;
+
+struct Acc {
+  int is_int = 0;
+  int base = -1;  // earlier accumulator whose factor product is this one's prefix
+  int nf = 0;
+  Factor f[kMaxFactors];
+  int gate_probe = -1;  // value counts only if flag bit of probe is set
+  int gate_bit = 0;
+  double gate_else = 0.0;
+};
+
+// dense direct-address build table: entry 0 = empty, else
+//   bits 0-31 rowid+1 | bits 32-56 group id | bits 57-63 flags
+struct Probe {
+  Operand key;
+  long long kmin = 0;
+  long long range = 0;
+  const unsigned long long* table = nullptr;
+  const unsigned* bitmap = nullptr;  // presence bits (L2-resident filter)
+};
+
+// Branch-free predicate term for the fact scan: all compares on one column
+// are merged into lo <= x <= hi (int64: one unsigned compare; fp64: two
+// compares, NaN fails both exactly as the reference's `<`/`>` do).
+enum RangeKind : int { RK_INT = 0, RK_F64 = 1, RK_INT_NE = 2, RK_F64_NE = 3, RK_TRUE = 4, RK_FALSE = 5 };
+struct RTerm {
+  int col = -1;
+  int kind = RK_TRUE;
+  unsigned long long lo = 0, hi = 0;  // bit patterns (int64 or fp64)
+};
+
+__device__ __forceinline__ bool eval_rterm(const RTerm& t, unsigned long long x) {
+  switch (t.kind) {
+    case RK_INT: return x - t.lo <= t.hi - t.lo;
+    case RK_F64: {
+      double d = __longlong_as_double(static_cast<long long>(x));
+      return d >= __longlong_as_double(static_cast<long long>(t.lo)) &&
+             d <= __longlong_as_double(static_cast<long long>(t.hi));
+    }
+    case RK_INT_NE: return x != t.lo;
+    case RK_F64_NE:
+      return __longlong_as_double(static_cast<long long>(x)) != __longlong_as_double(static_cast<long long>(t.lo));
+    case RK_TRUE: return true;
+    default: return false;
+  }
+}
+
+struct ProbeSpec {
+  long long n = 0;
+  int nterms = 0;
+  RTerm terms[kMaxTerms];
+  int nprobes = 0;
+  Probe probes[kMaxProbes];
+  int nacc = 0;
+  Acc acc[kMaxAcc];
+  int nkeys = 0;
+  Operand keys[kMaxKeys];  // MODE_SMALL: 1-byte string columns (fact)
+  int group_probe = -1;    // MODE_BUILDGRP
+  // outputs
+  unsigned long long* part;  // SCALAR: [cta][nacc+1]; SMALL: per-CTA tables
+  unsigned long long* gacc;  // BUILDGRP: [group][nacc] x 2 words (Q64.64 or int64)
+  unsigned long long* gcnt;  // BUILDGRP: [group]
+  long long* err;            // [0] != 0: data violates the fused preconditions
+};
+
+struct BuildSpec {
+  long long n = 0;
+  int nterms = 0;
+  Term terms[kMaxTerms];
+  int nstr = 0;
+  StrTerm str[kMaxStrTerms];
+  int nprobes = 0;
+  Probe probes[kMaxProbes];
+  int nflags = 0;
+  StrTerm flags[kMaxFlags];
+  Operand key;  // root key column (int64)
+  long long kmin = 0;
+  long long range = 0;
+  unsigned long long* table = nullptr;
+  unsigned* bitmap = nullptr;
+  int assign_groups = 0;
+  unsigned int* group_counter = nullptr;
+  int* group_row = nullptr;
+  long long* err = nullptr;
+};
+
+// ---- operand access ----------------------------------------------------------
+__device__ __forceinline__ long long ld_i64(const void* p, long long r) {
+  return __ldg(static_cast<const long long*>(p) + r);
+}
+__device__ __forceinline__ double ld_f64(const void* p, long long r) {
+  return __ldg(static_cast<const double*>(p) + r);
+}
+
+// two consecutive fact rows (row0 even) with one 128-bit load
+__device__ __forceinline__ void ld_pair(const Operand& o, long long row0, unsigned long long& a,
+                                        unsigned long long& b) {
+  if (o.type == OT_U8) {
+    unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(static_cast<const uint8_t*>(o.ptr) + row0));
+    a = v & 0xff;
+    b = v >> 8;
+  } else {
+    ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(static_cast<const unsigned long long*>(o.ptr) + row0));
+    a = v.x;
+    b = v.y;
+  }
+}
+
+__device__ __forceinline__ unsigned long long ld_row(const Operand& o, long long row) {
+  if (o.type == OT_U8) return __ldg(static_cast<const uint8_t*>(o.ptr) + row);
+  return __ldg(static_cast<const unsigned long long*>(o.ptr) + row);
+}
+
+template <typename T>
+__device__ __forceinline__ bool cmp_op(T x, T y, int op) {
+  switch (op) {
+    case TQP_EQ: return x == y;
+    case TQP_NE: return x != y;
+    case TQP_LT: return x < y;
+    case TQP_LE: return x <= y;
+    case TQP_GT: return x > y;
+    default: return x >= y;
+  }
+}
+
+__device__ __forceinline__ bool eval_term(const Term& t, unsigned long long raw) {
+  switch (t.kind) {
+    case TK_INT: return cmp_op<long long>(static_cast<long long>(raw), t.ik, t.op);
+    case TK_F64: return cmp_op<double>(__longlong_as_double(static_cast<long long>(raw)), t.fk, t.op);
+    case TK_TRUE: return true;
+    default: return false;
+  }
+}
+
+__device__ __forceinline__ bool eval_str(const StrTerm& s, long long row) {
+  const uint8_t* p = s.ptr + row * s.width;
+  int len = 0;
+  while (len < s.width && p[len] != 0) ++len;
+  if (s.is_like) {
+    int pl = s.litlen;
+    if (pl > len) return false;
+    auto at = [&](int off) {
+      for (int j = 0; j < pl; ++j)
+        if (p[off + j] != s.lit[j]) return false;
+      return true;
+    };
+    switch (s.anchor) {
+      case TQP_START: return at(0);
+      case TQP_END: return at(len - pl);
+      case TQP_ANY:
+        for (int o = 0; o + pl <= len; ++o)
+          if (at(o)) return true;
+        return false;
+      default: return len == pl && at(0);
+    }
+  }
+  int m = s.width > s.litlen ? s.width : s.litlen;
+  int c = 0;
+  for (int j = 0; j < m && c == 0; ++j) {
+    int x = j < s.width ? p[j] : 0;
+    int y = j < s.litlen ? s.lit[j] : 0;
+    if (x != y) c = x < y ? -1 : 1;
+  }
+  return cmp_op<int>(c, 0, s.op);
+}
+
+__device__ __forceinline__ double apply_factor(const Factor& f, double x) {
+  switch (f.kind) {
+    case FK_X: return x;
+    case FK_K_MINUS_X: return __dsub_rn(f.k, x);
+    case FK_K_PLUS_X: return __dadd_rn(f.k, x);
+    case FK_X_MINUS_K: return __dsub_rn(x, f.k);
+    case FK_X_PLUS_K: return __dadd_rn(x, f.k);
+    case FK_X_TIMES_K: return __dmul_rn(x, f.k);
+    default: return f.k;
+  }
+}
+
+struct RowCtx {
+  long long rid[kMaxProbes];
+  unsigned flags[kMaxProbes];
+  unsigned gid[kMaxProbes];
+};
+
+__device__ __forceinline__ bool probe_lookup(const Probe& p, long long key, long long& rid, unsigned& flags,
+                                             unsigned& gid) {
+  long long idx = key - p.kmin;
+  if (idx < 0 || idx >= p.range) return false;
+  if (p.bitmap && !((__ldg(p.bitmap + (idx >> 5)) >> (idx & 31)) & 1u)) return false;
+  unsigned long long e = __ldg(p.table + idx);
+  if (!e) return false;
+  rid = static_cast<long long>(e & 0xffffffffULL) - 1;
+  gid = static_cast<unsigned>((e >> 32) & 0x1ffffffULL);
+  flags = static_cast<unsigned>(e >> 57);
+  return true;
+}
+
+__device__ __forceinline__ unsigned long long operand_value(const Operand& o, unsigned long long fact_raw,
+                                                            const RowCtx& rc) {
+  if (o.src < 0) return fact_raw;
+  return ld_row(o, rc.rid[o.src]);
+}
+
+// value of accumulator a for one row; fact operands already loaded in fv[]
+__device__ __forceinline__ unsigned long long eval_acc(const Acc& a, const unsigned long long* fv, const RowCtx& rc) {
+  if (a.is_int) return operand_value(a.f[0].x, fv[0], rc);
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxFactors; ++i) {
+    if (i < a.nf) {
+      double x = __longlong_as_double(static_cast<long long>(operand_value(a.f[i].x, fv[i], rc)));
+      double y = apply_factor(a.f[i], x);
+      v = i == 0 ? y : __dmul_rn(v, y);
+    }
+  }
+  if (a.gate_probe >= 0 && !((rc.flags[a.gate_probe] >> a.gate_bit) & 1u)) v = a.gate_else;
+  return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+
+// ---- exact Q64.64 fixed point ----------------------------------------------------
+// x -> round-toward-zero(x * 2^64) as int128. Exact for |x| >= 2^-11 (every
+// money value); false for |x| >= 2^62, NaN, Inf.
+__device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
+  long long bits = __double_as_longlong(x);
+  int ex = static_cast<int>((bits >> 52) & 0x7ff);
+  if (ex == 0x7ff) return false;
+  unsigned long long mant = static_cast<unsigned long long>(bits) & ((1ULL << 52) - 1);
+  if (ex == 0) {
+    ex = 1;
+  } else {
+    mant |= 1ULL << 52;
+  }
+  int shift = ex - 1075 + 64;
+  unsigned __int128 v;
+  if (shift >= 0) {
+    if (shift > 73) return false;
+    v = static_cast<unsigned __int128>(mant) << shift;
+  } else if (shift > -64) {
+    v = static_cast<unsigned __int128>(mant >> (-shift));
+  } else {
+    v = 0;
+  }
+  out = bits < 0 ? -static_cast<__int128>(v) : static_cast<__int128>(v);
+  return true;
+}
+
+__device__ __forceinline__ double q64_to_f64(unsigned long long lo, unsigned long long hi) {
+  __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
+  bool neg = v < 0;
+  unsigned __int128 u = neg ? static_cast<unsigned __int128>(-v) : static_cast<unsigned __int128>(v);
+  double ip = static_cast<double>(static_cast<unsigned long long>(u >> 64));
+  double fp = static_cast<double>(static_cast<unsigned long long>(u)) * 5.421010862427522e-20;  // 2^-64
+  double r = ip + fp;
+  return neg ? -r : r;
+}
+
+__device__ __forceinline__ void atomic_add_q64(unsigned long long* p, __int128 v) {
+  unsigned long long lo = static_cast<unsigned long long>(v);
+  unsigned long long hi = static_cast<unsigned long long>(static_cast<unsigned __int128>(v) >> 64);
+  unsigned long long old = atomicAdd(p, lo);
+  unsigned long long carry = (old + lo < old) ? 1ULL : 0ULL;
+  atomicAdd(p + 1, hi + carry);
+}
+
+// ---- TMA-staged, warp-specialised tile pipeline for the fact scan -----------
+// A persistent CTA per SM streams tiles of kTileRows rows. Warp 0 is the
+// producer: one lane issues, for every distinct fact column, a 1-D bulk async
+// copy (cp.async.bulk.shared::cluster.global -> SASS UBLKCP) of the tile into
+// a multi-stage shared-memory ring, signalling a `full` mbarrier with the
+// expected transaction bytes. Warps 1..16 consume: wait on `full`, evaluate
+// their rows, arrive on the stage's `empty` mbarrier. There is no CTA-wide
+// barrier per tile, ~100-190 KB per SM stay in flight independent of register
+// use, and operands are addressed by runtime column index in shared memory.
+// Predicates, probes and accumulator expressions run as compact runtime
+// loops whose dispatch is amortised over the rows each thread owns.
+constexpr int kTileRows = 2048;  // 16 KB bulk copies per 8-byte column
+constexpr int kMaxStages = 8;
+constexpr int kMaxCols = 10;
+
+// consumer warps per mode (+1 producer warp): small-group keeps 48 register
+// accumulators per thread, so it runs fewer, wider threads
+template <int MODE>
+struct TileShape {
+  // small-group keeps per-thread shared-memory accumulators (groups x
+  // accumulators x threads), so its tiles are half as tall
+  static constexpr int ROWS = MODE == MODE_SMALL ? 1024 : kTileRows;
+  static constexpr int CW = MODE == MODE_SMALL ? 8 : 16;
+  static constexpr int CT = CW * 32;
+  static constexpr int THREADS = CT + 32;
+  static constexpr int R = ROWS / CT;  // rows per consumer thread
+  static constexpr int SUB = R;
+};
+
+struct TileSpec {
+  ProbeSpec p;
+  int ncols = 0;
+  const unsigned char* col_ptr[kMaxCols];
+  int col_w[kMaxCols];
+  int col_off[kMaxCols];  // byte offset of the column inside a stage
+  int stage_bytes = 0;
+  int stages = 3;
+  int rows = kTileRows;   // rows per tile
+  int aux_bytes = 0;      // per-thread accumulator / staging region
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* stage, unsigned long long* bar,
+                                           long long tile) {
+  const long long row0 = tile * t.rows;
+  long long rows = t.p.n - row0;
+  if (rows > t.rows) rows = t.rows;
+  unsigned total = 0;
+  for (int c = 0; c < t.ncols; ++c) total += static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
+  mbar_expect_tx(bar, total);
+  for (int c = 0; c < t.ncols; ++c) {
+    unsigned bytes = static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
+    bulk_g2s(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar);
+  }
+}
+
+__device__ __forceinline__ unsigned long long add_acc(bool is_int, unsigned long long a, unsigned long long b) {
+  if (is_int) return static_cast<unsigned long long>(static_cast<long long>(a) + static_cast<long long>(b));
+  return static_cast<unsigned long long>(__double_as_longlong(
+      __dadd_rn(__longlong_as_double(static_cast<long long>(a)), __longlong_as_double(static_cast<long long>(b)))));
+}
+
+struct SmallPart {  // MODE_SMALL per-CTA partial, in global memory
+  unsigned int codes[kGroups];
+  unsigned long long cnt[kGroups];
+  unsigned long long acc[kGroups][kMaxAcc];
+};
+
+__device__ __forceinline__ unsigned hash_code(unsigned c) { return (c * 2654435761u) >> (32 - kGroupBits); }
+
+// per-thread region: SCALAR running sums [acc][thread]; SMALL accumulators
+// [group][acc + count][thread]
+template <int MODE>
+__host__ __device__ constexpr size_t aux_bytes_for(int nacc) {
+  using S = TileShape<MODE>;
+  return MODE == MODE_SMALL ? sizeof(unsigned long long) * kGroups * (nacc + 1) * S::CT : 0;
+}
+
+}  // namespace fz
+}  // namespace tqp

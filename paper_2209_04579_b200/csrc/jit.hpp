@@ -1,0 +1,18 @@
+// Run-time specialised pipeline kernels: NVRTC compiles a generated kernel
+// (fused.cu's generator + jit_tile.cuh) for sm_100a once per distinct source
+// per process; the cubin is loaded with cudaLibraryLoadData and launched like
+// any other kernel (the handle is a `const void*` for cudaLaunchKernel).
+#pragma once
+
+#include <string>
+
+namespace tqp {
+
+// Compiles (or returns the cached) kernel `entry` of `src`. Throws Error
+// (TQP_ERR_CUDA) with the NVRTC log on failure.
+const void* jit_kernel(const std::string& src, const char* entry);
+
+// Number of distinct kernels compiled in this process (tests/diagnostics).
+int jit_compiled_count();
+
+}  // namespace tqp
