@@ -20,3 +20,17 @@ doc = {"generator": "oracle/make_golden.sh: tqp_ref_runner tables/run (reference
 with gzip.open('../tests/golden/tpch_sf%s.json.gz' % sys.argv[1], 'wt') as f:
     json.dump(doc, f)
 PY
+
+# Full-size results (tables are regenerated bit-identically on the device by
+# include/tqp_gen.h, so only the reference executor's results are committed).
+for SF in 1 10; do
+  ./_ref/tqp_ref_runner run --sf $SF --repeat 0 --warmup 0 --results /tmp/tqp_results_sf$SF.json >/dev/null
+  python3 - "$SF" <<'PY'
+import json, sys
+sf = sys.argv[1]
+r = json.load(open('/tmp/tqp_results_sf%s.json' % sf))
+doc = {"generator": "oracle/make_golden.sh: tqp_ref_runner run (reference executor, par backend)",
+       "sf": float(sf), "seed": 7, "lineitem_rows": r["lineitem_rows"], "results": r["results"]}
+json.dump(doc, open('../tests/golden/tpch_results_sf%s.json' % sf, 'w'), indent=0)
+PY
+done

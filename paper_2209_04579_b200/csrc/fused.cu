@@ -902,7 +902,7 @@ struct Planner {
         ++s;
       }
       if (s + 1 < static_cast<int>(A.rels.size()) && A.rels[s].kind == Rel::SORT && A.rels[s + 1].kind == Rel::LIMIT &&
-          A.rels[s + 1].input == s && A.rels[s + 1].limit >= 0 && A.rels[s + 1].limit <= 64) {
+          A.rels[s + 1].input == s && A.rels[s + 1].limit >= 0 && A.rels[s + 1].limit <= 32) {
         const Rel& S = A.rels[s];
         const Rel& L = A.rels[s + 1];
         bool ok = S.input >= 0;
@@ -946,19 +946,28 @@ struct FinalSpec {
   int acc_is_int[kMaxAcc];
 };
 
+constexpr int kMerged = 256;
+constexpr int kMergeChunk = 256;
+
 __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int nparts, FinalSpec f, long long* err) {
+  // one warp per accumulator (and the count): independent loads into shared
+  // memory, then lane 0 adds in CTA order
   __shared__ unsigned long long s_tot[kMaxAcc + 1];
-  int a = threadIdx.x;
-  if (a <= kMaxAcc && (a < f.nacc || a == kMaxAcc)) {
-    bool is_int = a == kMaxAcc || f.acc_is_int[a];
+  __shared__ unsigned long long s_v[kMaxAcc + 1][kMergeChunk];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int a = warp; a <= kMaxAcc; a += nwarps) {
+    if (a != kMaxAcc && a >= f.nacc) continue;
+    const bool is_int = a == kMaxAcc || f.acc_is_int[a];
     unsigned long long t = 0;
-    for (int c = 0; c < nparts; ++c) {
-      unsigned long long v = part[static_cast<long long>(c) * (kMaxAcc + 1) + a];
-      if (is_int) t = static_cast<unsigned long long>(static_cast<long long>(t) + static_cast<long long>(v));
-      else t = static_cast<unsigned long long>(__double_as_longlong(
-          __dadd_rn(__longlong_as_double(static_cast<long long>(t)), __longlong_as_double(static_cast<long long>(v)))));
+    for (int c0 = 0; c0 < nparts; c0 += kMergeChunk) {
+      const int m = nparts - c0 < kMergeChunk ? nparts - c0 : kMergeChunk;
+      for (int i = lane; i < m; i += 32) s_v[a][i] = part[static_cast<long long>(c0 + i) * (kMaxAcc + 1) + a];
+      __syncwarp();
+      if (lane == 0)
+        for (int i = 0; i < m; ++i) t = add_acc(is_int, t, s_v[a][i]);
+      __syncwarp();
     }
-    s_tot[a] = t;
+    if (lane == 0) s_tot[a] = t;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -982,14 +991,20 @@ __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int 
   }
 }
 
-// MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums in CTA order
-constexpr int kMerged = 256;
-__global__ void k_final_small(const SmallPart* __restrict__ parts, int nparts, FinalSpec f, int nkeys,
-                              void* key_ptr0, void* key_ptr1, void* key_ptr2, void* key_ptr3, int* inv /*[nparts][kMerged]*/,
-                              long long* ngroups_out, long long* err) {
+// MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums in CTA
+// order. One warp per (group, accumulator | count) gathers the CTA values into
+// shared memory with independent loads; lane 0 then adds them in CTA order
+// (absent slots contribute +0.0 / 0, which never changes a sum that starts at
+// +0.0), so the result is the sequential CTA-order sum.
+__global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts, FinalSpec f,
+                                                          int nkeys, void* key_ptr0, void* key_ptr1, void* key_ptr2,
+                                                          void* key_ptr3, int* inv /*[nparts][kMerged]*/,
+                                                          long long* ngroups_out, long long* err) {
   __shared__ unsigned s_set[kMerged];
   __shared__ unsigned s_sorted[kMerged];
-  __shared__ int s_n;
+  __shared__ unsigned long long s_v[kThreads / 32][kMergeChunk];
+  __shared__ unsigned long long s_tot[kMerged][kMaxAcc + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kMerged; i += blockDim.x) s_set[i] = 0xffffffffu;
   __syncthreads();
   for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
@@ -1009,24 +1024,17 @@ __global__ void k_final_small(const SmallPart* __restrict__ parts, int nparts, F
     if (!placed) err[0] = 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int i = 0; i < kMerged; ++i)
-      if (s_set[i] != 0xffffffffu) s_sorted[n++] = s_set[i];
-    for (int i = 1; i < n; ++i) {  // insertion sort (n <= 256)
-      unsigned v = s_sorted[i];
-      int j = i - 1;
-      while (j >= 0 && s_sorted[j] > v) {
-        s_sorted[j + 1] = s_sorted[j];
-        --j;
-      }
-      s_sorted[j + 1] = v;
-    }
-    s_n = n;
-    *ngroups_out = n;
+  // rank sort of the distinct codes (codes are unique)
+  for (int i = threadIdx.x; i < kMerged; i += blockDim.x) {
+    const unsigned v = s_set[i];
+    if (v == 0xffffffffu) continue;
+    int r = 0;
+    for (int j = 0; j < kMerged; ++j) r += s_set[j] < v;
+    s_sorted[r] = v;
   }
-  __syncthreads();
-  const int n = s_n;
+  int n = 0;
+  for (int i = 0; i < kMerged; ++i) n += s_set[i] != 0xffffffffu;  // uniform
+  if (threadIdx.x == 0) *ngroups_out = n;
   for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kMerged; i += blockDim.x) inv[i] = -1;
   __syncthreads();
   for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
@@ -1042,32 +1050,38 @@ __global__ void k_final_small(const SmallPart* __restrict__ parts, int nparts, F
     inv[static_cast<long long>(c) * kMerged + lo] = sl;
   }
   __syncthreads();
+  const int per = f.nacc + 1;
+  for (int p = warp; p < n * per; p += kThreads / 32) {
+    const int g = p / per, a = p % per;  // a == f.nacc: the row count
+    const bool is_int = a == f.nacc || f.acc_is_int[a];
+    unsigned long long tot = 0;
+    for (int c0 = 0; c0 < nparts; c0 += kMergeChunk) {
+      const int m = nparts - c0 < kMergeChunk ? nparts - c0 : kMergeChunk;
+      for (int i = lane; i < m; i += 32) {
+        const int sl = inv[static_cast<long long>(c0 + i) * kMerged + g];
+        s_v[warp][i] = sl < 0 ? 0ULL : (a == f.nacc ? parts[c0 + i].cnt[sl] : parts[c0 + i].acc[sl][a]);
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int i = 0; i < m; ++i) tot = add_acc(is_int, tot, s_v[warp][i]);
+      __syncwarp();
+    }
+    if (lane == 0) s_tot[g][a] = tot;
+  }
+  __syncthreads();
   void* kp[4] = {key_ptr0, key_ptr1, key_ptr2, key_ptr3};
   for (int g = threadIdx.x; g < n; g += blockDim.x) {
     unsigned code = s_sorted[g];
     for (int k = 0; k < nkeys; ++k) static_cast<uint8_t*>(kp[k])[g] = (code >> (8 * (nkeys - 1 - k))) & 0xff;
-    unsigned long long tot[kMaxAcc];
-    long long cnt = 0;
-    for (int a = 0; a < f.nacc; ++a) tot[a] = 0;
-    for (int c = 0; c < nparts; ++c) {
-      int sl = inv[static_cast<long long>(c) * kMerged + g];
-      if (sl < 0) continue;
-      cnt += static_cast<long long>(parts[c].cnt[sl]);
-      for (int a = 0; a < f.nacc; ++a) {
-        unsigned long long v = parts[c].acc[sl][a];
-        if (f.acc_is_int[a]) tot[a] = static_cast<unsigned long long>(static_cast<long long>(tot[a]) + static_cast<long long>(v));
-        else tot[a] = static_cast<unsigned long long>(__double_as_longlong(
-            __dadd_rn(__longlong_as_double(static_cast<long long>(tot[a])), __longlong_as_double(static_cast<long long>(v)))));
-      }
-    }
+    const long long cnt = static_cast<long long>(s_tot[g][f.nacc]);
     for (int j = 0; j < f.nouts; ++j) {
       const OutKind& o = f.outs[j];
       if (o.fn >= 10) continue;
       if (o.fn == 1) static_cast<long long*>(f.out_ptr[j])[g] = cnt;
-      else if (o.fn == 0) static_cast<unsigned long long*>(f.out_ptr[j])[g] = tot[o.acc];
+      else if (o.fn == 0) static_cast<unsigned long long*>(f.out_ptr[j])[g] = s_tot[g][o.acc];
       else {
-        double sum = f.acc_is_int[o.acc] ? static_cast<double>(static_cast<long long>(tot[o.acc]))
-                                         : __longlong_as_double(static_cast<long long>(tot[o.acc]));
+        double sum = f.acc_is_int[o.acc] ? static_cast<double>(static_cast<long long>(s_tot[g][o.acc]))
+                                         : __longlong_as_double(static_cast<long long>(s_tot[g][o.acc]));
         static_cast<double*>(f.out_ptr[j])[g] = __ddiv_rn(sum, static_cast<double>(cnt));
       }
     }
@@ -1085,7 +1099,16 @@ struct GroupSpec {
   int nsort;
   int sort_out[4];  // index into f.outs
   int sort_asc[4];
+  const unsigned* present = nullptr;  // group g exists iff bit g is set (nullptr: every slot, zeroed)
+  int acc_words = 2;                  // per accumulator: 2 = int128 (lo, hi), kLimbWords = limbs
 };
+
+// accumulator a of group g as int128
+__device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, int a) {
+  const unsigned long long* w = s.gacc + (static_cast<long long>(g) * s.f.nacc + a) * s.acc_words;
+  if (s.acc_words == kLimbWords) return limbs_to_i128(w);
+  return static_cast<__int128>((static_cast<unsigned __int128>(w[1]) << 64) | w[0]);
+}
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g) {
   return s.group_row ? s.group_row[g] : static_cast<long long>(g);
@@ -1094,7 +1117,6 @@ __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned 
 __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
                                                 bool& is_f64) {
   const OutKind& o = s.f.outs[j];
-  const unsigned long long* acc = s.gacc + static_cast<long long>(g) * s.f.nacc * 2;
   long long cnt = static_cast<long long>(s.gcnt[g]);
   if (o.fn >= 10) {
     bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][group_src_row(s, g)]);
@@ -1106,36 +1128,41 @@ __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsig
     is_f64 = false;
     return true;
   }
-  const unsigned long long lo = acc[o.acc * 2], hi = acc[o.acc * 2 + 1];
+  const __int128 v128 = group_acc(s, g, o.acc);
+  const unsigned long long lo = static_cast<unsigned long long>(v128);
+  const unsigned long long hi = static_cast<unsigned long long>(static_cast<unsigned __int128>(v128) >> 64);
+  const bool limbs_ok = s.acc_words != kLimbWords || cnt < kLimbMaxRows;
   if (s.f.acc_is_int[o.acc]) {
     long long v = static_cast<long long>(lo);
     bool fits = static_cast<long long>(hi) == (v >> 63);
     if (o.fn == 0) {
       bits = static_cast<unsigned long long>(v);
       is_f64 = false;
-      return fits;
+      return fits && limbs_ok;
     }
     bits = static_cast<unsigned long long>(__double_as_longlong(__ddiv_rn(static_cast<double>(v), static_cast<double>(cnt))));
     is_f64 = true;
-    return fits;
+    return fits && limbs_ok;
   }
   double sum = q64_to_f64(lo, hi);
   is_f64 = true;
   bits = static_cast<unsigned long long>(__double_as_longlong(o.fn == 0 ? sum : __ddiv_rn(sum, static_cast<double>(cnt))));
-  return true;
+  return limbs_ok;
 }
 
 // lexicographic candidate key: sort keys (with direction), then group keys asc
+__device__ __forceinline__ unsigned long long sort_key_word(const GroupSpec& s, int i, unsigned g) {
+  unsigned long long bits;
+  bool f;
+  group_out_value(s, s.sort_out[i], g, bits, f);
+  unsigned long long u = f ? radix_key(__longlong_as_double(static_cast<long long>(bits)))
+                           : radix_key(static_cast<int64_t>(bits));
+  return s.sort_asc[i] ? u : ~u;
+}
+
 __device__ __forceinline__ int cand_keys(const GroupSpec& s, unsigned g, unsigned long long* k) {
   int n = 0;
-  for (int i = 0; i < s.nsort; ++i) {
-    unsigned long long bits;
-    bool f;
-    group_out_value(s, s.sort_out[i], g, bits, f);
-    unsigned long long u = f ? radix_key(__longlong_as_double(static_cast<long long>(bits)))
-                             : radix_key(static_cast<int64_t>(bits));
-    k[n++] = s.sort_asc[i] ? u : ~u;
-  }
+  for (int i = 0; i < s.nsort; ++i) k[n++] = sort_key_word(s, i, g);
   for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(s.key_cols[i][group_src_row(s, g)]));
   return n;
 }
@@ -1146,143 +1173,252 @@ __device__ __forceinline__ bool key_less(const unsigned long long* a, const unsi
   return false;
 }
 
-// Top-k with the reference's tie order. Candidates (groups with rows) get
-// their full key tuple computed once; each CTA then runs k rounds of
-// block-wide "best remaining" over its chunk (each thread keeps a taken-mask
-// over the <= 64 candidates it owns), and one CTA merges the per-CTA winners.
-constexpr int kTopkMaxPerThread = 64;
+// Top-k with the reference's tie order over the groups that have rows, in
+// one launch. The candidate key (sort keys with direction, then the unique
+// group keys ascending) totally orders the groups exactly as the reference's
+// stable sort of the ascending group-by output does. NK (key words) is a
+// template parameter so every key lives in registers.
+//
+// Each warp keeps a sorted list of its k (<= 32) best candidates in registers,
+// one entry per lane. A group whose first key word already loses to the
+// list's k-th key is dropped without computing the rest; a lane that beats it
+// is inserted with one ballot (its position) and one shuffle-up per key word.
+// The block's warp lists meet in warp 0 the same way, and the last block to
+// finish folds every block list in and writes the output rows.
+constexpr int kTopkMaxK = 32;
+constexpr int kTopkUnroll = 4;
+constexpr int kTopkThreads = 512;
 
-__global__ void __launch_bounds__(kThreads) k_topk_cands(GroupSpec s, long long ngroups, unsigned* __restrict__ cand_gid,
-                                                         unsigned long long* __restrict__ cand_key,
-                                                         unsigned* __restrict__ ncand) {
-  // block-aggregated append: one global atomic per 2048 groups
-  __shared__ unsigned long long s_w[33];
-  __shared__ unsigned s_base;
-  constexpr int kPer = 8;
-  const int nk = s.nsort + s.nkeyc;
-  const long long base = static_cast<long long>(blockIdx.x) * kThreads * kPer + threadIdx.x * kPer;
-  bool ok[kPer];
-  unsigned mine = 0;
+template <int NK>
+struct TopkList {
+  unsigned long long e[NK];  // lane i: the i-th best key (i < cnt)
+  unsigned gid = 0;
+  int cnt = 0;
+  unsigned long long thr[NK];  // k-th best key once cnt == k
+
+  __device__ static bool less(const unsigned long long* a, const unsigned long long* b) {
+    bool lt = false, eq = true;
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    ok[j] = base + j < ngroups && s.gcnt[base + j] != 0;
-    mine += ok[j];
+    for (int q = 0; q < NK; ++q) {
+      lt = lt || (eq && a[q] < b[q]);
+      eq = eq && a[q] == b[q];
+    }
+    return lt;
   }
-  unsigned long long total;
-  unsigned long long excl = block_exclusive_scan(mine, s_w, &total);
-  if (threadIdx.x == 0) s_base = total ? atomicAdd(ncand, static_cast<unsigned>(total)) : 0u;
-  __syncthreads();
-  unsigned pos = s_base + static_cast<unsigned>(excl);
+  __device__ bool beats(const unsigned long long* kk, int k) const { return cnt < k || less(kk, thr); }
+  // warp-uniform: insert the key of lane `src` (kk, g valid in that lane)
+  __device__ void insert_from(const unsigned long long* kk, unsigned g, int src, int k) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long bk[NK];
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    if (!ok[j]) continue;
-    const unsigned g = static_cast<unsigned>(base + j);
-    cand_gid[pos] = g;
-    unsigned long long k[9];
-    cand_keys(s, g, k);
-    for (int q = 0; q < nk; ++q) cand_key[static_cast<long long>(pos) * nk + q] = k[q];
-    ++pos;
+    for (int q = 0; q < NK; ++q) bk[q] = __shfl_sync(0xffffffffu, kk[q], src);
+    const unsigned bg = __shfl_sync(0xffffffffu, g, src);
+    if (!beats(bk, k)) return;
+    const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && less(e, bk)));
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+      const unsigned long long up = __shfl_up_sync(0xffffffffu, e[q], 1);
+      e[q] = lane > pos ? up : (lane == pos ? bk[q] : e[q]);
+    }
+    const unsigned upg = __shfl_up_sync(0xffffffffu, gid, 1);
+    gid = lane > pos ? upg : (lane == pos ? bg : gid);
+    if (cnt < k) ++cnt;
+    if (cnt == k) {
+#pragma unroll
+      for (int q = 0; q < NK; ++q) thr[q] = __shfl_sync(0xffffffffu, e[q], k - 1);
+    }
   }
+  // offer one candidate per lane (valid where `cand`)
+  __device__ void offer(bool cand, const unsigned long long* kk, unsigned g, int k) {
+    unsigned mask = __ballot_sync(0xffffffffu, cand && beats(kk, k));
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      insert_from(kk, g, src, k);
+      if (cnt == k) mask &= __ballot_sync(0xffffffffu, cand && less(kk, thr));
+    }
+  }
+};
+
+template <int NK>
+__device__ __forceinline__ void cand_keys_nk(const GroupSpec& s, unsigned g, unsigned long long* k) {
+#pragma unroll
+  for (int q = 0; q < NK; ++q)
+    k[q] = q < s.nsort ? sort_key_word(s, q < 4 ? q : 3, g)
+                       : radix_key(static_cast<int64_t>(s.key_cols[q - s.nsort][group_src_row(s, g)]));
 }
 
-// k rounds over candidates [lo, hi); winners (candidate indices) -> out
-__device__ void block_topk(const unsigned long long* __restrict__ keys, int nk, long long lo, long long hi, int k,
-                           long long* out, int* nout) {
-  __shared__ unsigned long long s_key[kThreads / 32][9];
-  __shared__ long long s_idx[kThreads / 32];
-  __shared__ long long s_win;
+template <int NK>
+__global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long long ngroups, int k,
+                                                          unsigned long long* __restrict__ blk_key,
+                                                          unsigned* __restrict__ blk_gid, int* __restrict__ blk_n,
+                                                          unsigned* __restrict__ ticket,
+                                                          unsigned long long* __restrict__ gthr,
+                                                          long long* __restrict__ nout, long long* __restrict__ err) {
+  constexpr int kSuper = NK > 5 ? 128 : 256;  // slots per presence super-chunk
+  __shared__ unsigned long long s_key[kTopkThreads / 32][kTopkMaxK][NK];
+  __shared__ unsigned s_gid[kTopkThreads / 32][kTopkMaxK];
+  __shared__ unsigned s_slot[kTopkThreads / 32][kSuper];
+  __shared__ int s_cnt[kTopkThreads / 32];
+  __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long taken = 0;
-  for (int round = 0; round < k; ++round) {
-    long long bi = -1;
-    unsigned long long best[9];
-    for (int j = 0; j < kTopkMaxPerThread; ++j) {
-      long long i = lo + threadIdx.x + static_cast<long long>(j) * blockDim.x;
-      if (i >= hi) break;
-      if ((taken >> j) & 1ULL) continue;
-      const unsigned long long* kk = keys + i * nk;
-      if (bi < 0 || key_less(kk, best, nk)) {
-        for (int q = 0; q < nk; ++q) best[q] = kk[q];
-        bi = i;
+  constexpr int kW = kTopkThreads / 32;
+  const long long n = ngroups;
+  TopkList<NK> L;
+  // gthr: the smallest first key word any warp has seen as its k-th best; a
+  // group whose first word is larger is beaten by k distinct groups, so no
+  // warp computes its full key (the expensive dependent gathers).
+  // Groups are walked in super-chunks of kTopkSuper slots: the presence words
+  // of a super-chunk are read with one load and its present slots compacted
+  // into shared memory, then processed kTopkUnroll x 32 at a time.
+  unsigned long long pub = ~0ULL;
+  unsigned* sidx = s_slot[warp];
+  for (long long sb = static_cast<long long>(blockIdx.x) * kW + warp; sb * kSuper < n;
+       sb += static_cast<long long>(gridDim.x) * kW) {
+    const long long base = sb * kSuper;
+    unsigned w = 0;
+    const long long wbase = base + 32LL * lane;
+    if (lane < kSuper / 32 && wbase < n) {
+      w = s.present ? __ldg(s.present + (wbase >> 5)) : ~0u;
+      if (n - wbase < 32) w &= (1u << (n - wbase)) - 1u;
+    }
+    const int c = __popc(w);
+    int off = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, off, o);
+      if (lane >= o) off += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, off, 31);
+    off -= c;
+    while (w) {
+      const int bit = __ffs(w) - 1;
+      w &= w - 1;
+      sidx[off++] = static_cast<unsigned>(wbase - base) + bit;
+    }
+    __syncwarp();
+    const unsigned long long T = __ldcg(gthr);
+    for (int c0 = 0; c0 < total; c0 += 32 * kTopkUnroll) {
+      bool has[kTopkUnroll];
+      unsigned gq[kTopkUnroll];
+      unsigned long long k0[kTopkUnroll];
+#pragma unroll
+      for (int u = 0; u < kTopkUnroll; ++u) {
+        const int i = c0 + u * 32 + lane;
+        gq[u] = i < total ? static_cast<unsigned>(base) + sidx[i] : 0u;
+        const unsigned long long gc = i < total ? s.gcnt[gq[u]] : 0ULL;
+        has[u] = gc != 0;
+        // limb sums are exact below kLimbMaxRows rows per group
+        if (s.acc_words == kLimbWords && gc >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+      }
+#pragma unroll
+      for (int u = 0; u < kTopkUnroll; ++u) k0[u] = has[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
+#pragma unroll
+      for (int u = 0; u < kTopkUnroll; ++u) {
+        const bool maybe = has[u] && k0[u] <= T && (L.cnt < k || k0[u] <= L.thr[0]);
+        unsigned long long kk[NK];
+#pragma unroll
+        for (int q = 0; q < NK; ++q) kk[q] = ~0ULL;
+        if (maybe) cand_keys_nk<NK>(s, gq[u], kk);
+        L.offer(maybe, kk, gq[u], k);
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      unsigned long long ok[9];
-      for (int q = 0; q < nk; ++q) ok[q] = __shfl_xor_sync(0xffffffffu, best[q], o);
-      if (oi >= 0 && (bi < 0 || key_less(ok, best, nk) || (!key_less(best, ok, nk) && oi < bi))) {
-        bi = oi;
-        for (int q = 0; q < nk; ++q) best[q] = ok[q];
+    __syncwarp();
+    if (L.cnt == k && L.thr[0] < pub) {
+      pub = L.thr[0];
+      if (lane == 0) atomicMin(gthr, pub);
+    }
+  }
+  // warp lists -> warp 0
+  if (lane < L.cnt) {
+#pragma unroll
+    for (int q = 0; q < NK; ++q) s_key[warp][lane][q] = L.e[q];
+    s_gid[warp][lane] = L.gid;
+  }
+  if (lane == 0) s_cnt[warp] = L.cnt;
+  __syncthreads();
+  if (warp == 0) {
+    for (int w = 1; w < kW; ++w) {
+      unsigned long long kk[NK];
+      const bool v = lane < s_cnt[w];
+#pragma unroll
+      for (int q = 0; q < NK; ++q) kk[q] = v ? s_key[w][lane][q] : ~0ULL;
+      L.offer(v, kk, v ? s_gid[w][lane] : 0u, k);
+    }
+    if (lane < L.cnt) {
+#pragma unroll
+      for (int q = 0; q < NK; ++q) blk_key[(static_cast<long long>(blockIdx.x) * kTopkMaxK + lane) * NK + q] = L.e[q];
+      blk_gid[static_cast<long long>(blockIdx.x) * kTopkMaxK + lane] = L.gid;
+    }
+    if (lane == 0) blk_n[blockIdx.x] = L.cnt;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last block: every warp folds a share of the block lists (kTopkUnroll
+  // lists per round, loads issued together), then warp 0 folds the warp lists
+  TopkList<NK> F;
+  const int nb = static_cast<int>(gridDim.x);
+  for (int b0 = warp * kTopkUnroll; b0 < nb; b0 += kW * kTopkUnroll) {
+    int bn[kTopkUnroll];
+    unsigned long long kk[kTopkUnroll][NK];
+    unsigned gg[kTopkUnroll];
+#pragma unroll
+    for (int u = 0; u < kTopkUnroll; ++u) {
+      const int b = b0 + u < nb ? b0 + u : nb - 1;
+      bn[u] = b0 + u < nb ? __ldcg(blk_n + b) : 0;
+#pragma unroll
+      for (int q = 0; q < NK; ++q) kk[u][q] = __ldcg(blk_key + (static_cast<long long>(b) * kTopkMaxK + lane) * NK + q);
+      gg[u] = __ldcg(blk_gid + static_cast<long long>(b) * kTopkMaxK + lane);
+    }
+#pragma unroll
+    for (int u = 0; u < kTopkUnroll; ++u) F.offer(lane < bn[u], kk[u], gg[u], k);
+  }
+  __syncthreads();
+  if (lane < F.cnt) {
+#pragma unroll
+    for (int q = 0; q < NK; ++q) s_key[warp][lane][q] = F.e[q];
+    s_gid[warp][lane] = F.gid;
+  }
+  if (lane == 0) s_cnt[warp] = F.cnt;
+  __syncthreads();
+  if (warp == 0) {
+    for (int w = 1; w < kW; ++w) {
+      unsigned long long kk[NK];
+      const bool v = lane < s_cnt[w];
+#pragma unroll
+      for (int q = 0; q < NK; ++q) kk[q] = v ? s_key[w][lane][q] : ~0ULL;
+      F.offer(v, kk, v ? s_gid[w][lane] : 0u, k);
+    }
+    if (lane < F.cnt) {
+      const unsigned g = F.gid;
+      for (int j = 0; j < s.f.nouts; ++j) {
+        unsigned long long bits;
+        bool f;
+        if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
+        static_cast<unsigned long long*>(s.f.out_ptr[j])[lane] = bits;
       }
     }
-    if (lane == 0) {
-      s_idx[warp] = bi;
-      for (int q = 0; q < nk; ++q) s_key[warp][q] = best[q];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int bw = -1;
-      for (int w = 0; w < kThreads / 32; ++w) {
-        if (s_idx[w] < 0) continue;
-        if (bw < 0 || key_less(s_key[w], s_key[bw], nk)) bw = w;
-      }
-      s_win = bw < 0 ? -1 : s_idx[bw];
-      if (s_win >= 0) out[(*nout)++] = s_win;
-    }
-    __syncthreads();
-    const long long win = s_win;
-    if (win < 0) break;
-    const long long rel = win - lo - threadIdx.x;
-    if (rel >= 0 && rel % blockDim.x == 0) taken |= 1ULL << (rel / blockDim.x);
-    __syncthreads();
+    if (lane == 0) *nout = F.cnt;
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_topk_local(const unsigned long long* __restrict__ keys, int nk,
-                                                         long long ncand, long long chunk, int k,
-                                                         long long* __restrict__ winners) {
-  __shared__ long long s_out[64];
-  __shared__ int s_n;
-  if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  const long long lo = chunk * blockIdx.x, hi = lo + chunk < ncand ? lo + chunk : ncand;
-  block_topk(keys, nk, lo, hi > lo ? hi : lo, k, s_out, &s_n);
-  __syncthreads();
-  for (int i = threadIdx.x; i < k; i += blockDim.x) winners[static_cast<long long>(blockIdx.x) * k + i] = i < s_n ? s_out[i] : -1;
-}
-
-__global__ void __launch_bounds__(kThreads) k_topk_final(GroupSpec s, const unsigned long long* __restrict__ keys,
-                                                         const unsigned* __restrict__ cand_gid,
-                                                         const long long* __restrict__ winners, long long nwin, int k,
-                                                         unsigned long long* __restrict__ scratch, long long* nout,
-                                                         long long* err) {
-  __shared__ long long s_out[64];
-  __shared__ int s_n;
-  const int nk = s.nsort + s.nkeyc;
-  // gather the winners' keys into a dense scratch (invalid -> max key)
-  for (long long i = threadIdx.x; i < nwin; i += blockDim.x) {
-    long long w = winners[i];
-    for (int q = 0; q < nk; ++q) scratch[i * nk + q] = w >= 0 ? keys[w * nk + q] : ~0ULL;
-  }
-  if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  block_topk(scratch, nk, 0, nwin, k, s_out, &s_n);
-  __syncthreads();
-  for (int r = threadIdx.x; r < s_n; r += blockDim.x) {
-    long long w = winners[s_out[r]];
-    if (w < 0) continue;
-    const unsigned g = cand_gid[w];
-    for (int j = 0; j < s.f.nouts; ++j) {
-      unsigned long long bits;
-      bool f;
-      if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
-      static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
-    }
-  }
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int r = 0; r < s_n; ++r) n += winners[s_out[r]] >= 0;
-    *nout = n;
+using TopkKernel = void (*)(GroupSpec, long long, int, unsigned long long*, unsigned*, int*, unsigned*,
+                            unsigned long long*, long long*, long long*);
+TopkKernel topk_kernel(int nk) {
+  switch (nk) {
+    case 1: return k_topk_groups<1>;
+    case 2: return k_topk_groups<2>;
+    case 3: return k_topk_groups<3>;
+    case 4: return k_topk_groups<4>;
+    case 5: return k_topk_groups<5>;
+    case 6: return k_topk_groups<6>;
+    case 7: return k_topk_groups<7>;
+    case 8: return k_topk_groups<8>;
+    default: return nullptr;
   }
 }
 
@@ -1298,8 +1434,10 @@ __global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids_sor
   }
 }
 
-__global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long n, uint8_t* __restrict__ mask) {
-  for (long long i = gtid(); i < n; i += gstride()) mask[i] = cnt[i] != 0;
+__global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long n, const unsigned* present,
+                                 uint8_t* __restrict__ mask) {
+  for (long long i = gtid(); i < n; i += gstride())
+    mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i] != 0;
 }
 
 __global__ void k_group_keys(const int* __restrict__ group_row, const long long* __restrict__ gids, long long n,
@@ -1320,7 +1458,8 @@ static_assert(sizeof(SmallPart) % sizeof(unsigned long long) == 0, "SmallPart mu
 constexpr int record_words(int nkeyc, int nacc) { return 2 + nkeyc + 2 * nacc; }
 
 __global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, long long n,
-                               const long long* __restrict__ bkey, int words, unsigned long long* __restrict__ out) {
+                               const long long* __restrict__ bkey, int words, unsigned long long* __restrict__ out,
+                               long long* err) {
   for (long long i = gtid(); i < n; i += gstride()) {
     const unsigned g = static_cast<unsigned>(gids[i]);
     const long long row = group_src_row(s, g);
@@ -1328,8 +1467,12 @@ __global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, 
     w[0] = static_cast<unsigned long long>(bkey[row]);
     for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(s.key_cols[k][row]);
     w[1 + s.nkeyc] = s.gcnt[g];
-    const unsigned long long* acc = s.gacc + static_cast<long long>(g) * s.f.nacc * 2;
-    for (int a = 0; a < 2 * s.f.nacc; ++a) w[2 + s.nkeyc + a] = acc[a];
+    if (s.acc_words == kLimbWords && s.gcnt[g] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+    for (int a = 0; a < s.f.nacc; ++a) {  // records carry int128 (lo, hi)
+      const unsigned __int128 v = static_cast<unsigned __int128>(group_acc(s, g, a));
+      w[2 + s.nkeyc + 2 * a] = static_cast<unsigned long long>(v);
+      w[3 + s.nkeyc + 2 * a] = static_cast<unsigned long long>(v >> 64);
+    }
   }
 }
 
@@ -1633,7 +1776,7 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
         << "    in = in && ((w >> (idx & 31)) & 1u);\n";
     o << "    const unsigned long long e = in ? __ldg(pr.table + idx) : 0ULL;\n"
       << "    pass = pass && e != 0ULL;\n"
-      << "    gid" << p << " = static_cast<unsigned>((e >> 32) & 0x1ffffffULL);\n"
+      << "    gid" << p << " = static_cast<unsigned>(idx);\n"
       << "    fl" << p << " = static_cast<unsigned>(e >> 57); }\n";
   }
   if (mode == MODE_BUILDGRP) {
@@ -1678,6 +1821,114 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
   return o.str();
 }
 
+// Build-side kernel specialised the same way (jit_build.cuh): terms,
+// string terms, LIKE flags and child probes with their constants folded.
+// String predicates keep eval_str's semantics: a START/EXACT pattern or an
+// equality literal without zero bytes compares the leading bytes directly
+// (a zero-padded row shorter than the pattern cannot match a zero-free
+// pattern); anything else calls eval_str.
+constexpr int kJitBuildRows = 4;
+
+std::string str_pred(const StrTerm& t, const std::string& sref, const std::string& row) {
+  bool zero_free = true;
+  for (int i = 0; i < t.litlen; ++i) zero_free = zero_free && t.lit[i] != 0;
+  const std::string p = "(" + sref + ".ptr + " + row + " * " + std::to_string(t.width) + "LL)";
+  auto prefix_eq = [&](int n) {
+    std::string e = "true";
+    for (int i = 0; i < n; ++i) e += " && __ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(t.lit[i]) + "u";
+    return e;
+  };
+  if (t.is_like && zero_free && t.litlen <= t.width) {
+    if (t.anchor == TQP_START) return "(" + prefix_eq(t.litlen) + ")";
+    if (t.anchor == TQP_EXACT) {
+      std::string e = prefix_eq(t.litlen);
+      if (t.litlen < t.width) e += " && __ldg(" + p + " + " + std::to_string(t.litlen) + ") == 0u";
+      return "(" + e + ")";
+    }
+  }
+  if (!t.is_like && t.op == TQP_EQ && t.litlen <= t.width) {
+    // zero-extended equality over max(width, litlen) = width bytes
+    std::string e = "true";
+    for (int i = 0; i < t.width; ++i)
+      e += " && __ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(i < t.litlen ? t.lit[i] : 0) + "u";
+    return "(" + e + ")";
+  }
+  return "eval_str(" + sref + ", " + row + ")";
+}
+
+std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap) {
+  std::ostringstream o;
+  auto ld = [&](const Operand& x, const std::string& ptr, const std::string& row) {
+    if (x.type == OT_U8) return "static_cast<unsigned long long>(__ldg(static_cast<const uint8_t*>(" + ptr + ") + " + row + "))";
+    return "static_cast<unsigned long long>(__ldg(static_cast<const unsigned long long*>(" + ptr + ") + " + row + "))";
+  };
+  static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
+  o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << kJitBuildRows << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0)
+    << "\n#define B_ZACC " << b.zacc_words << "\n"
+    << "namespace tqp { namespace fz {\n"
+    << "__device__ __forceinline__ void b_rows(const BuildSpec& s, long long r0, int stride, bool* pass, long long* key,\n"
+    << "                                       unsigned* flags) {\n"
+    << "  long long r[B_ROWS];\n"
+    << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) { r[j] = r0 + j * stride; pass[j] = r[j] < s.n; flags[j] = 0u; }\n";
+  // every independent column load first
+  o << "  unsigned long long kv[B_ROWS]";
+  for (int t = 0; t < b.nterms; ++t) o << ", tv" << t << "[B_ROWS]";
+  for (int p = 0; p < b.nprobes; ++p) o << ", pv" << p << "[B_ROWS]";
+  o << ";\n#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n"
+    << "    const long long rr = pass[j] ? r[j] : 0;\n"
+    << "    kv[j] = " << ld(b.key, "s.key.ptr", "rr") << ";\n";
+  for (int t = 0; t < b.nterms; ++t)
+    if (b.terms[t].kind == TK_INT || b.terms[t].kind == TK_F64)
+      o << "    tv" << t << "[j] = " << ld(b.terms[t].x, "s.terms[" + std::to_string(t) + "].x.ptr", "rr") << ";\n";
+  for (int p = 0; p < b.nprobes; ++p)
+    o << "    pv" << p << "[j] = " << ld(b.probes[p].key, "s.probes[" + std::to_string(p) + "].key.ptr", "rr") << ";\n";
+  // phase by phase over all B_ROWS rows, so the rows' dependent probe loads
+  // (presence word, then entry) are in flight together
+  o << "  }\n#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n    bool ok = pass[j];\n    key[j] = static_cast<long long>(kv[j]);\n";
+  for (int t = 0; t < b.nterms; ++t) {
+    const Term& T = b.terms[t];
+    const int op = T.op < 0 || T.op > 5 ? 5 : T.op;
+    switch (T.kind) {
+      case TK_INT:
+        o << "    ok = ok && (static_cast<long long>(tv" << t << "[j]) " << ops[op] << " " << T.ik << "LL);\n";
+        break;
+      case TK_F64:
+        o << "    ok = ok && (__longlong_as_double(static_cast<long long>(tv" << t << "[j])) " << ops[op] << " " << dlit(T.fk)
+          << ");\n";
+        break;
+      case TK_TRUE: break;
+      default: o << "    ok = false;\n"; break;
+    }
+  }
+  for (int t = 0; t < b.nstr; ++t)
+    o << "    ok = ok && " << str_pred(b.str[t], "s.str[" + std::to_string(t) + "]", "r[j]") << ";\n";
+  o << "    pass[j] = ok;\n  }\n";
+  for (int p = 0; p < b.nprobes; ++p) {
+    const std::string pr = "s.probes[" + std::to_string(p) + "]";
+    o << "  {\n    long long idx[B_ROWS];\n    bool in[B_ROWS];\n"
+      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) {\n"
+      << "      idx[j] = static_cast<long long>(pv" << p << "[j]) - " << pr << ".kmin;\n"
+      << "      in[j] = pass[j] && static_cast<unsigned long long>(idx[j]) < static_cast<unsigned long long>(" << pr
+      << ".range);\n      if (!in[j]) idx[j] = 0;\n    }\n";
+    if (probe_bitmap[p])
+      o << "    unsigned w[B_ROWS];\n"
+        << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) w[j] = __ldg(" << pr << ".bitmap + (idx[j] >> 5));\n"
+        << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) in[j] = in[j] && ((w[j] >> (idx[j] & 31)) & 1u);\n";
+    o << "    unsigned long long e[B_ROWS];\n"
+      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) e[j] = __ldg(" << pr << ".table + idx[j]);\n"
+      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) pass[j] = in[j] && e[j] != 0ULL;\n  }\n";
+  }
+  if (b.nflags) {
+    o << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n";
+    for (int f = 0; f < b.nflags; ++f)
+      o << "    if (pass[j] && " << str_pred(b.flags[f], "s.flags[" + std::to_string(f) + "]", "r[j]") << ") flags[j] |= "
+        << (1u << f) << "u;\n";
+    o << "  }\n";
+  }
+  o << "}\n}}  // namespace tqp::fz\n#include \"jit_build.cuh\"\n";
+  return o.str();
+}
+
 struct Runner {
   PipeDesc P;
 
@@ -1688,45 +1939,68 @@ struct Runner {
   // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po) const {
     // build sides, children first (builds[] is in post-order by construction)
-    auto err_buf = c.alloc_bytes(16);
+    // err[0]: precondition flag; err[2]: result rows counted on the device
+    auto err_buf = c.alloc_bytes(32);
     long long* err = static_cast<long long*>(err_buf->ptr);
-    TQP_CUDA(cudaMemsetAsync(err, 0, 16, c.stream));
+    TQP_CUDA(cudaMemsetAsync(err, 0, 32, c.stream));
     std::vector<Probe> built(P.builds.size());
     std::vector<std::shared_ptr<DevBuf>> keep;
-    std::vector<long long> build_rows(P.builds.size(), 0);
+    std::vector<long long> build_range(P.builds.size(), 0);
     int* group_row = nullptr;
-    unsigned* group_counter = nullptr;
+    const unsigned* group_present = nullptr;
+    unsigned long long* gacc_p = nullptr;
+    unsigned long long* gcnt_p = nullptr;
+    const int nacc_all = static_cast<int>(P.accs.size());
+    // key ranges of every build side: one launch each, one host round trip
+    const size_t nb = P.builds.size();
+    std::vector<long long> mm(2 * std::max<size_t>(1, nb));
+    std::shared_ptr<DevBuf> mmb;
+    if (nb) {
+      for (size_t bi = 0; bi < nb; ++bi) {
+        mm[2 * bi] = 0x7fffffffffffffffLL;
+        mm[2 * bi + 1] = static_cast<long long>(0x8000000000000000ULL);
+      }
+      mmb = c.alloc_bytes(sizeof(long long) * 2 * nb);
+      TQP_CUDA(cudaMemcpyAsync(mmb->ptr, mm.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, c.stream));
+      for (size_t bi = 0; bi < nb; ++bi) {
+        const BuildDesc& B = P.builds[bi];
+        const Table* tab = bind_table(tables, B.table);
+        const Column* key = tab ? tab->find(B.key_column) : nullptr;
+        if (!key || key->t.dtype != TQP_I64) return false;
+        if (tab->rows) {
+          k_minmax<<<c.grid_for(tab->rows, 256, 8, 16), 256, 0, c.stream>>>(
+              key->t.ptr<long long>(), tab->rows, static_cast<long long*>(mmb->ptr) + 2 * bi);
+          c.count_launch();
+        }
+      }
+      TQP_CUDA(cudaMemcpyAsync(mm.data(), mmb->ptr, sizeof(long long) * 2 * nb, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+    }
     for (size_t bi = 0; bi < P.builds.size(); ++bi) {
       const BuildDesc& B = P.builds[bi];
       const Table* tab = bind_table(tables, B.table);
-      const Column* key = tab ? tab->find(B.key_column) : nullptr;
-      if (!key || key->t.dtype != TQP_I64) return false;
+      const Column* key = tab->find(B.key_column);
       long long n = tab->rows;
-      build_rows[bi] = n;
-      long long mm[2] = {0x7fffffffffffffffLL, static_cast<long long>(0x8000000000000000ULL)};
-      auto mmb = c.alloc_bytes(16);
-      TQP_CUDA(cudaMemcpyAsync(mmb->ptr, mm, 16, cudaMemcpyHostToDevice, c.stream));
-      if (n) {
-        k_minmax<<<c.grid_for(n, 256, 8, 16), 256, 0, c.stream>>>(key->t.ptr<long long>(), n, static_cast<long long*>(mmb->ptr));
-        c.count_launch();
-      }
-      TQP_CUDA(cudaMemcpyAsync(mm, mmb->ptr, 16, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      long long range = n ? mm[1] - mm[0] + 1 : 1;
+      long long range = n ? mm[2 * bi + 1] - mm[2 * bi] + 1 : 1;
       if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
       BuildSpec bs;
       bs.n = n;
-      bs.kmin = n ? mm[0] : 0;
+      bs.kmin = n ? mm[2 * bi] : 0;
       bs.range = range;
       auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
       TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
+      build_range[bi] = range;
       const long long bm_words = (range + 31) / 32;
       auto bitmap = c.alloc_bytes(sizeof(unsigned) * bm_words);
       TQP_CUDA(cudaMemsetAsync(bitmap->ptr, 0, sizeof(unsigned) * bm_words, c.stream));
       keep.push_back(bitmap);
       bs.bitmap = static_cast<unsigned*>(bitmap->ptr);
+      auto counts = c.alloc_bytes(sizeof(unsigned long long) * (kCountSlots + 1));
+      TQP_CUDA(cudaMemsetAsync(counts->ptr, 0, sizeof(unsigned long long) * (kCountSlots + 1), c.stream));
+      keep.push_back(counts);
+      bs.counts = static_cast<unsigned long long*>(counts->ptr);
       bs.err = err;
       bool ok = true;
       bs.key = {key->t.data(), OT_I64, -1};
@@ -1758,21 +2032,45 @@ struct Runner {
         bs.probes[bs.nprobes++] = p;
       }
       if (B.assign_groups) {
-        auto gr = c.alloc_bytes(sizeof(int) * (n + 1) + 16);
+        // the group is the key slot: per-slot build row and accumulators,
+        // written only for the slots a row is inserted into
+        auto gr = c.alloc_bytes(sizeof(int) * (range + 1));
+        auto gacc = c.alloc_bytes(sizeof(unsigned long long) * kLimbWords * std::max(1, nacc_all) * (range + 1));
+        auto gcnt = c.alloc_bytes(sizeof(unsigned long long) * (range + 1));
         keep.push_back(gr);
+        keep.push_back(gacc);
+        keep.push_back(gcnt);
         group_row = static_cast<int*>(gr->ptr);
-        group_counter = reinterpret_cast<unsigned*>(group_row + n + 1);
-        TQP_CUDA(cudaMemsetAsync(group_counter, 0, 4, c.stream));
+        group_present = bs.bitmap;
+        gacc_p = static_cast<unsigned long long*>(gacc->ptr);
+        gcnt_p = static_cast<unsigned long long*>(gcnt->ptr);
         bs.assign_groups = 1;
-        bs.group_counter = group_counter;
         bs.group_row = group_row;
+        bs.zacc = gacc_p;
+        bs.zacc_words = kLimbWords * nacc_all;
+        bs.zcnt = gcnt_p;
       }
       if (!ok) return false;
       if (n) {
-        // one row per thread: the per-row dependent loads (term, probe,
-        // insert) need many warps in flight
-        k_build<<<c.grid_for(n, kThreads, kBuildRows, 1 << 20), kThreads, 0, c.stream>>>(bs);
+        // kBuildRows rows per thread: the per-row dependent loads (term,
+        // probe, insert) need many warps in flight
+        const void* bk = reinterpret_cast<const void*>(&k_build);
+        if (jit_wanted(n)) {
+          std::vector<bool> bm;
+          for (const auto& ch : B.children) {
+            const BuildDesc& CB = P.builds[ch.build];
+            bm.push_back(!CB.terms.empty() || !CB.children.empty());
+          }
+          bk = jit_kernel(gen_build(bs, bm), "q_build");
+        }
+        void* args[] = {&bs};
+        cudaEvent_t ev = c.kernel_begin();
+        TQP_CUDA(cudaLaunchKernel(bk, dim3(c.grid_for(n, kThreads, kBuildRows, 1 << 20)), dim3(kThreads), args, 0, c.stream));
+        c.kernel_end(bk == reinterpret_cast<const void*>(&k_build) ? "k_build" : "q_build", ev);
         c.count_launch();
+        k_bitmap_popc<<<c.grid_for(bm_words / 4 + 1, 256, 4, 4), 256, 0, c.stream>>>(bs.bitmap, bm_words, bs.counts);
+        k_build_verify<<<1, 1, 0, c.stream>>>(bs.counts, err);
+        c.count_launch(2);
       }
       Probe pr;
       pr.kmin = bs.kmin;
@@ -1991,13 +2289,10 @@ struct Runner {
       if (!po) nrows = final_small(c, reinterpret_cast<const SmallPart*>(ps.part), grid, fs, err, outs);
     } else {
       // MODE_BUILDGRP
-      long long ngroups = build_rows[P.probes[P.group_probe].build];
-      auto gacc = c.alloc_bytes(sizeof(unsigned long long) * 2 * std::max(1, ps.nacc) * (ngroups + 1));
-      auto gcnt = c.alloc_bytes(sizeof(unsigned long long) * (ngroups + 1));
-      TQP_CUDA(cudaMemsetAsync(gacc->ptr, 0, gacc->bytes, c.stream));
-      TQP_CUDA(cudaMemsetAsync(gcnt->ptr, 0, gcnt->bytes, c.stream));
-      ps.gacc = static_cast<unsigned long long*>(gacc->ptr);
-      ps.gcnt = static_cast<unsigned long long*>(gcnt->ptr);
+      long long ngroups = build_range[P.probes[P.group_probe].build];
+      if (!gacc_p || !group_present) return false;  // the group build assigns the groups
+      ps.gacc = gacc_p;
+      ps.gcnt = gcnt_p;
       ps.group_probe = P.group_probe;
       launch_tile(kfn, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
@@ -2005,6 +2300,8 @@ struct Runner {
       gs.gacc = ps.gacc;
       gs.gcnt = ps.gcnt;
       gs.group_row = group_row;
+      gs.present = group_present;
+      gs.acc_words = kLimbWords;
       const BuildDesc& gb = P.builds[P.probes[P.group_probe].build];
       const Table* groot = bind_table(tables, gb.table);
       gs.nkeyc = static_cast<int>(P.group_key_root_columns.size());
@@ -2017,27 +2314,28 @@ struct Runner {
       if (po) {
         // the touched groups as self-describing records, keyed by the unique
         // build key: shards may split a group (the merge adds exactly)
-        Tensor gids = touched_groups(c, ps.gcnt, ngroups);
+        Tensor gids = touched_groups(c, ps.gcnt, ngroups, group_present);
         const long long n = gids.rows;
         const int words = record_words(gs.nkeyc, fs.nacc);
         unsigned long long* rec = part_buf(n, words);
         if (n) {
           k_fill_records<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(), n, bk->t.ptr<long long>(),
-                                                                  words, rec);
+                                                                  words, rec, err);
           c.count_launch();
         }
       } else if (!emit_groups(c, gs, ngroups, bk->t.ptr<long long>(), err, outs, nrows)) {
         return false;
       }
     }
-    long long herr[2] = {0, 0};
-    TQP_CUDA(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, c.stream));
+    long long herr[4] = {0, 0, 0, 0};
+    TQP_CUDA(cudaMemcpyAsync(herr, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     if (herr[0]) {  // preconditions violated: exact per-instruction path
       if (po) *po = Partial{};
       return false;
     }
     if (po) return true;
+    if (nrows < 0) nrows = herr[2];
     for (size_t j = 0; j < outs.size(); ++j) outs[j].rows = nrows;
     for (size_t i = 0; i < P.final_slots.size(); ++i) (*slots)[P.final_slots[i]] = outs[P.final_cols[i]];
     return true;
@@ -2067,14 +2365,13 @@ struct Runner {
       outs[j] = c.alloc(out_dtype(P, P.outs[j]), 1, 1);
       fs.out_ptr[j] = outs[j].data();
     }
-    k_final_scalar<<<1, 32, 0, c.stream>>>(part, nparts, fs, err);
+    k_final_scalar<<<1, kThreads, 0, c.stream>>>(part, nparts, fs, err);
     c.count_launch();
   }
 
   long long final_small(Ctx& c, const SmallPart* parts, long long nparts, FinalSpec fs, long long* err,
                         std::vector<Tensor>& outs) const {
     auto inv = c.alloc_bytes(sizeof(int) * nparts * kMerged);
-    auto ng = c.alloc_bytes(8);
     for (size_t j = 0; j < outs.size(); ++j) {
       outs[j] = c.alloc(out_dtype(P, P.outs[j]), kMerged, 1);
       fs.out_ptr[j] = outs[j].data();
@@ -2083,19 +2380,15 @@ struct Runner {
     for (size_t j = 0; j < P.outs.size(); ++j)
       if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = outs[j].data();
     k_final_small<<<1, kThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
-                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(inv->ptr),
-                                                static_cast<long long*>(ng->ptr), err);
+                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(inv->ptr), err + 2, err);
     c.count_launch();
-    long long nrows = 0;
-    TQP_CUDA(cudaMemcpyAsync(&nrows, ng->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    return nrows;
+    return -1;  // on the device (err[2]); read with the error flag
   }
 
-  static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long ngroups) {
+  static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long ngroups, const unsigned* present) {
     Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
     if (ngroups) {
-      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, ngroups, mask.ptr<uint8_t>());
+      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, ngroups, present, mask.ptr<uint8_t>());
       c.count_launch();
     }
     return k::compact(c, k::iota(c, ngroups), mask);
@@ -2111,48 +2404,34 @@ struct Runner {
         gs.sort_out[i] = P.sort_outs[i].first;
         gs.sort_asc[i] = P.sort_outs[i].second;
       }
-      // reference sort over NaN keys is an error: leave that to the exact path
-      int k = static_cast<int>(P.k);
+      const int k = static_cast<int>(P.k);
       for (size_t j = 0; j < outs.size(); ++j) {
         outs[j] = c.alloc(out_dtype(P, P.outs[j]), std::max(1, k), 1);
         gs.f.out_ptr[j] = outs[j].data();
       }
-      const int nk = gs.nsort + gs.nkeyc;
-      auto cgid = c.alloc_bytes(sizeof(unsigned) * (ngroups + 1));
-      auto ckey = c.alloc_bytes(sizeof(unsigned long long) * nk * (ngroups + 1));
-      auto ncb = c.alloc_bytes(8);
-      TQP_CUDA(cudaMemsetAsync(ncb->ptr, 0, 8, c.stream));
-      if (ngroups) {
-        k_topk_cands<<<(ngroups + kThreads * 8 - 1) / (kThreads * 8), kThreads, 0, c.stream>>>(
-            gs, ngroups, static_cast<unsigned*>(cgid->ptr), static_cast<unsigned long long*>(ckey->ptr),
-            static_cast<unsigned*>(ncb->ptr));
-        c.count_launch();
-      }
-      unsigned ncand = 0;
-      TQP_CUDA(cudaMemcpyAsync(&ncand, ncb->ptr, 4, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      const long long chunk = static_cast<long long>(kThreads) * 4;
-      const long long nblk = (static_cast<long long>(ncand) + chunk - 1) / chunk;
-      const long long nwin = nblk * k;
-      if (nwin > static_cast<long long>(kThreads) * kTopkMaxPerThread) return false;
-      auto win = c.alloc_bytes(sizeof(long long) * std::max<long long>(1, nwin));
-      auto scratch = c.alloc_bytes(sizeof(unsigned long long) * nk * std::max<long long>(1, nwin));
-      auto nout = c.alloc_bytes(8);
       nrows = 0;
-      if (k > 0 && ncand > 0) {
-        k_topk_local<<<nblk, kThreads, 0, c.stream>>>(static_cast<unsigned long long*>(ckey->ptr), nk, ncand, chunk, k,
-                                                     static_cast<long long*>(win->ptr));
-        k_topk_final<<<1, kThreads, 0, c.stream>>>(gs, static_cast<unsigned long long*>(ckey->ptr),
-                                                   static_cast<unsigned*>(cgid->ptr), static_cast<long long*>(win->ptr),
-                                                   nwin, k, static_cast<unsigned long long*>(scratch->ptr),
-                                                   static_cast<long long*>(nout->ptr), err);
-        c.count_launch(2);
-        TQP_CUDA(cudaMemcpyAsync(&nrows, nout->ptr, 8, cudaMemcpyDeviceToHost, c.stream));
-      }
-      c.sync();
+      if (k == 0 || ngroups == 0) return true;
+      const int nk = gs.nsort + gs.nkeyc;
+      TopkKernel kern = topk_kernel(nk);
+      if (!kern || k > kTopkMaxK || gs.nsort < 1) return false;
+      const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(2LL * c.num_sms, (ngroups + 4095) / 4096)));
+      auto bkey = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkMaxK * nk);
+      auto bgid = c.alloc_bytes(sizeof(unsigned) * blocks * kTopkMaxK);
+      auto bn = c.alloc_bytes(sizeof(int) * blocks + 32);
+      // [blk_n x blocks][ticket (4 B) + pad][gthr (8 B, all ones)]
+      unsigned char* tail = static_cast<unsigned char*>(bn->ptr) + ((sizeof(int) * blocks + 7) & ~size_t(7));
+      unsigned* ticket = reinterpret_cast<unsigned*>(tail);
+      unsigned long long* gthr = reinterpret_cast<unsigned long long*>(tail + 8);
+      TQP_CUDA(cudaMemsetAsync(ticket, 0, 8, c.stream));
+      TQP_CUDA(cudaMemsetAsync(gthr, 0xff, 8, c.stream));
+      kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bkey->ptr),
+                                              static_cast<unsigned*>(bgid->ptr), static_cast<int*>(bn->ptr), ticket,
+                                              gthr, err + 2, err);
+      c.count_launch();
+      nrows = -1;  // on the device (err[2]); read with the error flag
       return true;
     }
-    Tensor gids = touched_groups(c, gs.gcnt, ngroups);
+    Tensor gids = touched_groups(c, gs.gcnt, ngroups, gs.present);
     const long long n = gids.rows;
     Tensor keys = c.alloc(TQP_I64, n, 1);
     if (n) {
@@ -2209,9 +2488,9 @@ struct Runner {
                                  sizeof(unsigned long long) * nrec[i] * want_words, cudaMemcpyDeviceToDevice, c.stream));
       off += nrec[i];
     }
-    auto err_buf = c.alloc_bytes(16);
+    auto err_buf = c.alloc_bytes(32);
     long long* err = static_cast<long long*>(err_buf->ptr);
-    TQP_CUDA(cudaMemsetAsync(err, 0, 16, c.stream));
+    TQP_CUDA(cudaMemsetAsync(err, 0, 32, c.stream));
     std::vector<Tensor> outs(P.outs.size());
     long long nrows = 0;
     bool ok = true;
@@ -2250,9 +2529,10 @@ struct Runner {
       for (int i = 0; i < nkeyc; ++i) gs.key_cols[i] = static_cast<const long long*>(hkeys->ptr) + i * cap;
       ok = emit_groups(c, gs, cap, static_cast<const long long*>(hbk->ptr), err, outs, nrows);
     }
-    long long herr[2] = {0, 0};
-    TQP_CUDA(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, c.stream));
+    long long herr[4] = {0, 0, 0, 0};
+    TQP_CUDA(cudaMemcpyAsync(herr, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    if (nrows < 0) nrows = herr[2];
     if (!ok || herr[0]) {
       // the local path would re-run these steps per instruction; merged
       // partials cannot, so report what the exact path raises

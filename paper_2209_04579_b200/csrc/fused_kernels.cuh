@@ -27,20 +27,40 @@ namespace tqp {
 namespace fz {
 
 // ---- build kernel ------------------------------------------------------------
-__global__ void k_minmax(const long long* __restrict__ k, long long n, long long* out) {
+// key range of a build side: 128-bit loads, warp then block reduction, one
+// atomic pair per block (a per-warp atomic on one address serialises at L2)
+__global__ void __launch_bounds__(256) k_minmax(const long long* __restrict__ k, long long n, long long* out) {
+  __shared__ long long s_mn[8], s_mx[8];
   long long mn = 0x7fffffffffffffffLL, mx = static_cast<long long>(0x8000000000000000ULL);
-  for (long long i = gtid(); i < n; i += gstride()) {
-    long long v = k[i];
-    mn = v < mn ? v : mn;
-    mx = v > mx ? v : mx;
+  const bool aligned = (reinterpret_cast<uintptr_t>(k) & 15) == 0;
+  const long long npair = aligned ? n / 2 : 0;
+  const longlong2* k2 = reinterpret_cast<const longlong2*>(k);
+  for (long long i = gtid(); i < npair; i += gstride()) {
+    const longlong2 v = __ldg(k2 + i);
+    mn = min(mn, min(v.x, v.y));
+    mx = max(mx, max(v.x, v.y));
+  }
+  for (long long i = 2 * npair + gtid(); i < n; i += gstride()) {
+    const long long v = __ldg(k + i);
+    mn = min(mn, v);
+    mx = max(mx, v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    long long a = __shfl_xor_sync(0xffffffffu, mn, o), b = __shfl_xor_sync(0xffffffffu, mx, o);
-    mn = a < mn ? a : mn;
-    mx = b > mx ? b : mx;
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   }
-  if ((threadIdx.x & 31) == 0) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_mn[warp] = mn;
+    s_mx[warp] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      mn = min(mn, s_mn[w]);
+      mx = max(mx, s_mx[w]);
+    }
     atomicMin(out, mn);
     atomicMax(out + 1, mx);
   }
@@ -49,6 +69,7 @@ __global__ void k_minmax(const long long* __restrict__ k, long long n, long long
 constexpr int kBuildRows = 4;
 __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
   const int lane = threadIdx.x & 31;
+  unsigned inserted = 0;
   // kBuildRows rows per thread (stride blockDim) with every independent column
   // load issued before any dependent work: the per-row chain (filter ->
   // child probe -> insert) is latency-bound otherwise
@@ -93,45 +114,27 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
         }
       }
     }
-    // group ids: one global atomic per block (block scan of per-thread
-    // counts); a per-warp atomic on a single counter serialises at L2
-    unsigned gid_next = 0;
-    if (s.assign_groups) {
-      __shared__ unsigned long long s_w[33];
-      __shared__ unsigned s_gbase;
-      unsigned mine = 0;
-#pragma unroll
-      for (int j = 0; j < kBuildRows; ++j) mine += pass[j] ? 1u : 0u;
-      unsigned long long total;
-      const unsigned long long excl = block_exclusive_scan(mine, s_w, &total);
-      if (threadIdx.x == 0) s_gbase = total ? atomicAdd(s.group_counter, static_cast<unsigned>(total)) : 0u;
-      __syncthreads();
-      gid_next = s_gbase + static_cast<unsigned>(excl);
-      __syncthreads();
-    }
 #pragma unroll
     for (int j = 0; j < kBuildRows; ++j) {
+      if (!__any_sync(0xffffffffu, pass[j])) continue;  // warp-uniform: nothing to insert
       const long long r = base0 + j * blockDim.x + threadIdx.x;
-      unsigned gid = 0;
-      if (s.assign_groups && pass[j]) gid = gid_next++;
       long long idx = -1;
       if (pass[j]) {
         unsigned flags = 0;
         for (int f = 0; f < s.nflags; ++f)
           if (eval_str(s.flags[f], r)) flags |= 1u << f;
         idx = key[j] - s.kmin;
-        if (idx < 0 || idx >= s.range || gid >= (1u << 25)) {
+        if (idx < 0 || idx >= s.range) {
           atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
           idx = -1;
         } else {
-          if (s.assign_groups) s.group_row[gid] = static_cast<int>(r);
-          const unsigned long long e = static_cast<unsigned long long>(r + 1) |
-                                       (static_cast<unsigned long long>(gid) << 32) |
-                                       (static_cast<unsigned long long>(flags) << 57);
-          if (atomicCAS(s.table + idx, 0ULL, e) != 0ULL) {
-            // duplicate build key: the join is 1:N, outside the fused contract
-            atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+          if (s.assign_groups) {  // the group is the key slot
+            s.group_row[idx] = static_cast<int>(r);
+            s.zcnt[idx] = 0ULL;
+            for (int w = 0; w < s.zacc_words; ++w) s.zacc[idx * s.zacc_words + w] = 0ULL;
           }
+          s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags) << 57);
+          ++inserted;
         }
       }
       // presence bits: lanes sharing a bitmap word OR-reduce, one atomic per word
@@ -141,6 +144,37 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
       if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(s.bitmap + word, bits);
     }
   }
+  // per-warp totals spread over kCountSlots words: no block barrier, no hot address
+  inserted = __reduce_add_sync(0xffffffffu, inserted);
+  if (lane == 0 && inserted)
+    atomicAdd(s.counts + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kCountSlots - 1)),
+              static_cast<unsigned long long>(inserted));
+}
+
+// duplicate-key check of a build: set presence bits must equal rows inserted
+__global__ void __launch_bounds__(256) k_bitmap_popc(const unsigned* __restrict__ bm, long long words,
+                                                     unsigned long long* counts) {
+  __shared__ unsigned s_tot;
+  if (threadIdx.x == 0) s_tot = 0;
+  __syncthreads();
+  unsigned c = 0;
+  const long long nq = words / 4;
+  const uint4* b4 = reinterpret_cast<const uint4*>(bm);
+  for (long long i = gtid(); i < nq; i += gstride()) {
+    const uint4 v = __ldg(b4 + i);
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  for (long long i = 4 * nq + gtid(); i < words; i += gstride()) c += __popc(__ldg(bm + i));
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_tot, c);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_tot) atomicAdd(counts + kCountSlots, static_cast<unsigned long long>(s_tot));
+}
+
+__global__ void k_build_verify(const unsigned long long* counts, long long* err) {
+  unsigned long long ins = 0;
+  for (int i = 0; i < kCountSlots; ++i) ins += counts[i];
+  if (ins != counts[kCountSlots]) err[0] = 1;
 }
 
 // value of accumulator `ac` for rows k0..k0+N-1 of this thread (row index
@@ -506,7 +540,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
                 qv = 0;
               }
-              atomic_add_q64(s.gacc + (static_cast<long long>(g[k]) * NAX + a) * 2, qv);
+              atomic_add_limbs(s.gacc + (static_cast<long long>(g[k]) * NAX + a) * kLimbWords, qv);
             }
           }
         }

@@ -24,6 +24,7 @@ constexpr int kGroupBits = 3;
 constexpr int kMaxAccSmall = 6;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+constexpr int kCountSlots = 64;  // build insert counters
 
 enum OperandType : int { OT_I64 = 0, OT_F64 = 1, OT_U8 = 2 };
 enum TermKind : int { TK_INT = 0, TK_F64 = 1, TK_TRUE = 2, TK_FALSE = 3 };
@@ -81,7 +82,8 @@ struct Acc {
 };
 
 // dense direct-address build table: entry 0 = empty, else
-//   bits 0-31 rowid+1 | bits 32-56 group id | bits 57-63 flags
+//   bits 0-31 rowid+1 | bits 57-63 flags; the group of a group-assigning
+//   build is the key slot (key - kmin), valid where the presence bit is set
 struct Probe {
   Operand key;
   long long kmin = 0;
@@ -129,7 +131,7 @@ struct ProbeSpec {
   int group_probe = -1;    // MODE_BUILDGRP
   // outputs
   unsigned long long* part;  // SCALAR: [cta][nacc+1]; SMALL: per-CTA tables
-  unsigned long long* gacc;  // BUILDGRP: [group][nacc] x 2 words (Q64.64 or int64)
+  unsigned long long* gacc;  // BUILDGRP: [group][nacc] x kLimbWords (Q64.64 or int64 as limbs)
   unsigned long long* gcnt;  // BUILDGRP: [group]
   long long* err;            // [0] != 0: data violates the fused preconditions
 };
@@ -150,8 +152,17 @@ struct BuildSpec {
   unsigned long long* table = nullptr;
   unsigned* bitmap = nullptr;
   int assign_groups = 0;
-  unsigned int* group_counter = nullptr;
-  int* group_row = nullptr;
+  int* group_row = nullptr;  // [key slot] -> build row, for the slots inserted
+  // group state zeroed by the row inserted into the slot (no memset over the
+  // whole key range): zacc_words words of zacc and one word of zcnt per slot
+  unsigned long long* zacc = nullptr;
+  int zacc_words = 0;
+  unsigned long long* zcnt = nullptr;
+  // [0, kCountSlots) rows inserted (per-warp totals, spread), [kCountSlots]
+  // presence bits set (k_build_verify): they differ iff
+  // two inserted rows share a key (a 1:N join, outside the fused contract).
+  // Inserts are plain stores so no warp waits on an atomic's return.
+  unsigned long long* counts = nullptr;
   long long* err = nullptr;
 };
 
@@ -261,7 +272,7 @@ __device__ __forceinline__ bool probe_lookup(const Probe& p, long long key, long
   unsigned long long e = __ldg(p.table + idx);
   if (!e) return false;
   rid = static_cast<long long>(e & 0xffffffffULL) - 1;
-  gid = static_cast<unsigned>((e >> 32) & 0x1ffffffULL);
+  gid = static_cast<unsigned>(idx);  // a group-assigning build's group is its key slot
   flags = static_cast<unsigned>(e >> 57);
   return true;
 }
@@ -315,14 +326,11 @@ __device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
   return true;
 }
 
+// Q64.64 -> fp64, correctly rounded (one rounding of the exact value: the
+// int128 conversion rounds to nearest even, the 2^-64 scale is exact)
 __device__ __forceinline__ double q64_to_f64(unsigned long long lo, unsigned long long hi) {
-  __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
-  bool neg = v < 0;
-  unsigned __int128 u = neg ? static_cast<unsigned __int128>(-v) : static_cast<unsigned __int128>(v);
-  double ip = static_cast<double>(static_cast<unsigned long long>(u >> 64));
-  double fp = static_cast<double>(static_cast<unsigned long long>(u)) * 5.421010862427522e-20;  // 2^-64
-  double r = ip + fp;
-  return neg ? -r : r;
+  const __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
+  return static_cast<double>(v) * 5.421010862427522e-20;  // 2^-64
 }
 
 __device__ __forceinline__ void atomic_add_q64(unsigned long long* p, __int128 v) {
@@ -331,6 +339,27 @@ __device__ __forceinline__ void atomic_add_q64(unsigned long long* p, __int128 v
   unsigned long long old = atomicAdd(p, lo);
   unsigned long long carry = (old + lo < old) ? 1ULL : 0ULL;
   atomicAdd(p + 1, hi + carry);
+}
+
+// Carry-free group sums: an int128 is added as three 42-bit limbs
+// (v = l0 + l1 * 2^42 + l2 * 2^84, l0/l1 unsigned, l2 signed) with three
+// non-returning atomic adds, so no thread waits on an atomic's return value.
+// A word takes < 2^21 adds of < 2^42 without overflow; the reader checks the
+// group's row count against kLimbMaxRows and reassembles mod 2^128 (exact
+// whenever the true sum fits, as the int128 it replaces).
+constexpr int kLimbWords = 3;
+constexpr long long kLimbMaxRows = 1LL << 21;
+__device__ __forceinline__ void atomic_add_limbs(unsigned long long* p, __int128 v) {
+  const unsigned __int128 u = static_cast<unsigned __int128>(v);
+  const unsigned long long m = (1ULL << 42) - 1;
+  atomicAdd(p, static_cast<unsigned long long>(u) & m);
+  atomicAdd(p + 1, static_cast<unsigned long long>(u >> 42) & m);
+  atomicAdd(p + 2, static_cast<unsigned long long>(static_cast<long long>(v >> 84)));
+}
+__device__ __forceinline__ __int128 limbs_to_i128(const unsigned long long* w) {
+  const unsigned __int128 u = static_cast<unsigned __int128>(w[0]) + (static_cast<unsigned __int128>(w[1]) << 42) +
+                              (static_cast<unsigned __int128>(static_cast<__int128>(static_cast<long long>(w[2]))) << 84);
+  return static_cast<__int128>(u);
 }
 
 // ---- TMA-staged, warp-specialised tile pipeline for the fact scan -----------

@@ -1,0 +1,68 @@
+// Skeleton of a specialised build-side kernel, compiled at run time by NVRTC
+// (jit.cu) after the generated hook
+//
+//   B_ROWS                                   rows per thread
+//   void b_rows(s, r0, stride, pass, key, flags)
+//        filter terms, string terms, LIKE flags and child probes of rows
+//        r0 + j * stride (j < B_ROWS), straight-line with every constant
+//        folded and every independent load issued first (fused.cu's generator)
+//
+//   B_ASSIGN, B_ZACC                          group-assigning build, words of
+//                                            group state zeroed per slot
+//
+// The rest is k_build's (fused_kernels.cuh): the group of a group-assigning
+// build is its key slot (its state zeroed by the inserted row), the direct-
+// address insert (plain stores; k_build_verify flags a key inserted twice, the
+// 1:N join the fused contract excludes) and the presence bits OR-reduced per
+// warp.
+#pragma once
+
+namespace tqp {
+namespace fz {
+
+extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s) {
+  const int lane = threadIdx.x & 31;
+  unsigned inserted = 0;
+  const long long span = static_cast<long long>(blockDim.x) * B_ROWS;
+  for (long long base0 = static_cast<long long>(blockIdx.x) * span; base0 < s.n;
+       base0 += static_cast<long long>(gridDim.x) * span) {
+    bool pass[B_ROWS];
+    long long key[B_ROWS];
+    unsigned flags[B_ROWS];
+    b_rows(s, base0 + threadIdx.x, blockDim.x, pass, key, flags);
+#pragma unroll
+    for (int j = 0; j < B_ROWS; ++j) {
+      if (!__any_sync(0xffffffffu, pass[j])) continue;  // warp-uniform: nothing to insert
+      const long long r = base0 + j * blockDim.x + threadIdx.x;
+      long long idx = -1;
+      if (pass[j]) {
+        idx = key[j] - s.kmin;
+        if (idx < 0 || idx >= s.range) {
+          atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+          idx = -1;
+        } else {
+#if B_ASSIGN
+          s.group_row[idx] = static_cast<int>(r);  // the group is the key slot
+          s.zcnt[idx] = 0ULL;
+#pragma unroll
+          for (int w = 0; w < B_ZACC; ++w) s.zacc[idx * B_ZACC + w] = 0ULL;
+#endif
+          s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[j]) << 57);
+          ++inserted;
+        }
+      }
+      const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, word);
+      const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
+      if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(s.bitmap + word, bits);
+    }
+  }
+  // per-warp totals spread over kCountSlots words: no block barrier, no hot address
+  inserted = __reduce_add_sync(0xffffffffu, inserted);
+  if (lane == 0 && inserted)
+    atomicAdd(s.counts + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kCountSlots - 1)),
+              static_cast<unsigned long long>(inserted));
+}
+
+}  // namespace fz
+}  // namespace tqp

@@ -150,7 +150,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
               atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
               qv = 0;
             }
-            atomic_add_q64(s.gacc + (static_cast<long long>(gid[k]) * Q_NA + a) * 2, qv);
+            atomic_add_limbs(s.gacc + (static_cast<long long>(gid[k]) * Q_NA + a) * kLimbWords, qv);
           }
         }
       }

@@ -41,6 +41,9 @@ def test_jit_bit_identical_to_generic(ctx, q):
     want, kg = run(tqp, q, tables, False)
     assert any(k.startswith("kernel:q_tile") for k in kj), kj
     assert not any(k.startswith("kernel:q_tile") for k in kg), kg
+    if q in ("q14", "q3"):  # build sides specialised too
+        assert any(k.startswith("kernel:q_build") for k in kj), kj
+        assert any(k.startswith("kernel:k_build") for k in kg), kg
     assert [(n, t) for n, t, _ in got] == [(n, t) for n, t, _ in want]
     for (n, _, g), (_, _, w) in zip(got, want):
         np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=f"{q}.{n}")
@@ -54,3 +57,27 @@ def test_jit_matches_reference_golden(ctx):
     for q in QUERIES:
         got, _ = run(tqp, q, tables, True)
         compare_tables(got, gold["results"][q])
+
+
+def test_jit_golden_plans(ctx, golden_plans):
+    """Every golden plan (string predicates, LIKE anchors, joins, CASE, zero
+    rows, error text) with every fused unit forced onto NVRTC kernels."""
+    from paper_2209_04579_b200 import tqp
+    from test_executor_gpu import as_numpy, device_tables
+    old = os.environ.get("TQP_JIT")
+    os.environ["TQP_JIT"] = "1"
+    try:
+        for case in golden_plans:
+            tables = device_tables(tqp, case["tables"])
+            ex = tqp.Executor(case["opplan"], fuse=True)
+            if "error" in case:
+                with pytest.raises(tqp.ExecError) as ei:
+                    ex.execute(tables)
+                assert str(ei.value) == case["error"], case["name"]
+                continue
+            compare_tables(as_numpy(ex.execute(tables)), case["result"])
+    finally:
+        if old is None:
+            del os.environ["TQP_JIT"]
+        else:
+            os.environ["TQP_JIT"] = old

@@ -1,0 +1,60 @@
+"""Full-size parity (SURVEY.md §8(c) "not pinned in the reference"): TPC-H
+Q1/Q3/Q6/Q14 at SF1 and SF10 on tables generated on the device (bit-identical
+to the host generator the reference ran on, test_executor_gpu.py) against the
+reference executor's own results (tests/golden/tpch_results_sf*.json, made by
+oracle/make_golden.sh). Exact for keys, counts, int64 sums and Q3's ordering;
+fp64 aggregates within 1e-9 relative (BASELINE.json north star).
+
+Covered paths: fused (default), per-instruction (SF1), and the sharded
+execute_partial -> finish merge with 4 order-aligned shards (SF10)."""
+import json
+
+import pytest
+
+from conftest import GOLDEN, ROOT
+from test_oracle import compare_tables
+
+pytestmark = pytest.mark.gpu
+PLANS = ROOT / "paper_2209_04579_b200" / "plans"
+QUERIES = ("q1", "q3", "q6", "q14")
+
+
+def golden(sf):
+    return json.loads((GOLDEN / f"tpch_results_sf{sf}.json").read_text())
+
+
+def plan(q):
+    return json.loads((PLANS / f"{q}.opplan.json").read_text())
+
+
+def generate(tqp, sf, shard=0, nshards=1):
+    sharded = ("lineitem", "orders")
+    return {n: tqp.Table.generate(n, sf, 7, shard=shard if n in sharded else 0,
+                                  nshards=nshards if n in sharded else 1)
+            for n in ("lineitem", "orders", "customer", "part")}
+
+
+@pytest.mark.parametrize("sf,fuse", [(1, True), (1, False), (10, True)])
+def test_tpch_matches_reference_at_scale(ctx, sf, fuse):
+    from paper_2209_04579_b200 import tqp
+    gold = golden(sf)
+    tables = generate(tqp, sf)
+    assert tables["lineitem"].rows == gold["lineitem_rows"]
+    for q in QUERIES:
+        got = tqp.Executor(plan(q), fuse=fuse).execute(tables).to_numpy()
+        compare_tables(got, gold["results"][q])
+    del tables
+    ctx.sync()
+
+
+def test_tpch_sharded_sf10_matches_reference(ctx):
+    from paper_2209_04579_b200 import tqp
+    gold = golden(10)
+    nshards = 4
+    for q in QUERIES:
+        ex = tqp.Executor(plan(q))
+        parts = []
+        for s in range(nshards):
+            parts.append(ex.execute_partial(generate(tqp, 10, s, nshards)))
+            ctx.sync()
+        compare_tables(ex.finish(parts).to_numpy(), gold["results"][q])
