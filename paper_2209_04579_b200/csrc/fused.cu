@@ -1187,7 +1187,7 @@ __device__ __forceinline__ bool key_less(const unsigned long long* a, const unsi
 // finish folds every block list in and writes the output rows.
 constexpr int kTopkMaxK = 32;
 constexpr int kTopkUnroll = 4;
-constexpr int kTopkThreads = 512;
+constexpr int kTopkThreads = 256;
 
 template <int NK>
 struct TopkList {
@@ -1248,37 +1248,78 @@ __device__ __forceinline__ void cand_keys_nk(const GroupSpec& s, unsigned g, uns
                        : radix_key(static_cast<int64_t>(s.key_cols[q - s.nsort][group_src_row(s, g)]));
 }
 
+// Exact top-k in one launch, without per-group full keys. The walk only
+// forms each group's FIRST key word k0 (one accumulator read):
+//   * every warp keeps the k smallest k0 values it has seen (one per lane) and
+//     logs (k0, group) for every group with k0 <= its current k-th value;
+//     since a warp's k-th value only decreases and never drops below the
+//     global k-th value T, every group with k0 <= T is in some warp's log;
+//   * a block merges its warps' values (k-way, heads in lanes) to its own k-th
+//     value T_b >= T and publishes its values and the log entries <= T_b;
+//   * the last block merges the block values into the exact T, keeps the
+//     published entries with k0 <= T (the top k plus ties on k0), computes
+//     their full keys and orders them with TopkList.
+// A warp log that cannot hold the entries still at or below its k-th value
+// (more than kTopkLog ties) flags the unit for the exact per-instruction path.
+constexpr int kTopkLog = 64;
+constexpr int kTopkBlkCand = 128;
+constexpr int kTopkFinal = 128;
+constexpr int kTopkSuperSlots = 1024;
+constexpr int kTopkStage = 2048;  // last block: block values staged in shared memory (nb * k)
+
+// the k smallest u64 values of a warp, ascending, one per lane (lane < cnt)
+struct ValList {
+  unsigned long long v = ~0ULL;
+  int cnt = 0;
+  __device__ unsigned long long thr(int k) const {
+    const unsigned long long t = __shfl_sync(0xffffffffu, v, k - 1);
+    return cnt == k ? t : ~0ULL;
+  }
+  __device__ void insert(unsigned long long x, int k) {  // warp-uniform x
+    const int lane = threadIdx.x & 31;
+    if (cnt == k && x >= thr(k)) return;
+    const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && v <= x));
+    const unsigned long long up = __shfl_up_sync(0xffffffffu, v, 1);
+    v = lane > pos ? up : (lane == pos ? x : v);
+    if (cnt < k) ++cnt;
+  }
+};
+
 template <int NK>
 __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long long ngroups, int k,
-                                                          unsigned long long* __restrict__ blk_key,
-                                                          unsigned* __restrict__ blk_gid, int* __restrict__ blk_n,
-                                                          unsigned* __restrict__ ticket,
-                                                          unsigned long long* __restrict__ gthr,
-                                                          long long* __restrict__ nout, long long* __restrict__ err) {
-  constexpr int kSuper = NK > 5 ? 128 : 256;  // slots per presence super-chunk
-  __shared__ unsigned long long s_key[kTopkThreads / 32][kTopkMaxK][NK];
-  __shared__ unsigned s_gid[kTopkThreads / 32][kTopkMaxK];
-  __shared__ unsigned s_slot[kTopkThreads / 32][kSuper];
-  __shared__ int s_cnt[kTopkThreads / 32];
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                                              unsigned long long* __restrict__ blk_val,
+                                                              int* __restrict__ blk_nval,
+                                                              unsigned long long* __restrict__ blk_ck,
+                                                              unsigned* __restrict__ blk_cg, int* __restrict__ blk_nc,
+                                                              unsigned* __restrict__ ticket,
+                                                              long long* __restrict__ nout, long long* __restrict__ err) {
   constexpr int kW = kTopkThreads / 32;
+  __shared__ unsigned long long s_logk[kW][kTopkLog];
+  __shared__ unsigned s_logg[kW][kTopkLog];
+  __shared__ __align__(16) unsigned s_scratch[kW * kTopkSuperSlots];  // slot compaction; last block: heads / keys
+  __shared__ unsigned long long s_wv[kW][32];
+  __shared__ int s_wn[kW];
+  __shared__ unsigned long long s_T;
+  __shared__ int s_nc, s_last, s_err;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (threadIdx.x == 0) {
+    s_nc = 0;
+    s_err = 0;
+  }
+  __syncthreads();
   const long long n = ngroups;
-  TopkList<NK> L;
-  // gthr: the smallest first key word any warp has seen as its k-th best; a
-  // group whose first word is larger is beaten by k distinct groups, so no
-  // warp computes its full key (the expensive dependent gathers).
-  // Groups are walked in super-chunks of kTopkSuper slots: the presence words
-  // of a super-chunk are read with one load and its present slots compacted
-  // into shared memory, then processed kTopkUnroll x 32 at a time.
-  unsigned long long pub = ~0ULL;
-  unsigned* sidx = s_slot[warp];
-  for (long long sb = static_cast<long long>(blockIdx.x) * kW + warp; sb * kSuper < n;
+  ValList L;
+  int nlog = 0;
+  bool log_ok = true;
+  unsigned* sidx = s_scratch + warp * kTopkSuperSlots;
+
+  for (long long sb = static_cast<long long>(blockIdx.x) * kW + warp; sb * kTopkSuperSlots < n;
        sb += static_cast<long long>(gridDim.x) * kW) {
-    const long long base = sb * kSuper;
+    // present slots of the super-chunk, compacted (one presence word per lane)
+    const long long base = sb * kTopkSuperSlots, wbase = base + 32LL * lane;
     unsigned w = 0;
-    const long long wbase = base + 32LL * lane;
-    if (lane < kSuper / 32 && wbase < n) {
+    if (wbase < n) {
       w = s.present ? __ldg(s.present + (wbase >> 5)) : ~0u;
       if (n - wbase < 32) w &= (1u << (n - wbase)) - 1u;
     }
@@ -1297,101 +1338,209 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
       sidx[off++] = static_cast<unsigned>(wbase - base) + bit;
     }
     __syncwarp();
-    const unsigned long long T = __ldcg(gthr);
     for (int c0 = 0; c0 < total; c0 += 32 * kTopkUnroll) {
-      bool has[kTopkUnroll];
       unsigned gq[kTopkUnroll];
-      unsigned long long k0[kTopkUnroll];
+      unsigned long long gc[kTopkUnroll], k0[kTopkUnroll];
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
         const int i = c0 + u * 32 + lane;
         gq[u] = i < total ? static_cast<unsigned>(base) + sidx[i] : 0u;
-        const unsigned long long gc = i < total ? s.gcnt[gq[u]] : 0ULL;
-        has[u] = gc != 0;
-        // limb sums are exact below kLimbMaxRows rows per group
-        if (s.acc_words == kLimbWords && gc >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+        gc[u] = i < total ? s.gcnt[gq[u]] : 0ULL;
       }
-#pragma unroll
-      for (int u = 0; u < kTopkUnroll; ++u) k0[u] = has[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
-        const bool maybe = has[u] && k0[u] <= T && (L.cnt < k || k0[u] <= L.thr[0]);
-        unsigned long long kk[NK];
+        // limb sums are exact below kLimbMaxRows rows per group
+        if (s.acc_words == kLimbWords && gc[u] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+        k0[u] = gc[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
+      }
 #pragma unroll
-        for (int q = 0; q < NK; ++q) kk[q] = ~0ULL;
-        if (maybe) cand_keys_nk<NK>(s, gq[u], kk);
-        L.offer(maybe, kk, gq[u], k);
+      for (int u = 0; u < kTopkUnroll; ++u) {
+        const unsigned long long t = L.thr(k);  // every lane (shuffle)
+        const bool cand = gc[u] != 0 && k0[u] <= t;
+        unsigned mask = __ballot_sync(0xffffffffu, cand);
+        if (!mask) continue;
+        const int m = __popc(mask);
+        if (log_ok && nlog + m > kTopkLog) {
+          // drop logged entries above the current k-th value (never needed)
+          const unsigned long long t = L.thr(k);
+          int kept = 0;
+          for (int i0 = 0; i0 < nlog; i0 += 32) {
+            const int i = i0 + lane;
+            const unsigned long long lk = i < nlog ? s_logk[warp][i] : ~0ULL;
+            const unsigned lg = i < nlog ? s_logg[warp][i] : 0u;
+            const bool keep = i < nlog && lk <= t;
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (keep) {
+              const int pos = kept + __popc(km & lt_mask);
+              s_logk[warp][pos] = lk;
+              s_logg[warp][pos] = lg;
+            }
+            kept += __popc(km);
+            __syncwarp();
+          }
+          nlog = kept;
+          if (nlog + m > kTopkLog) log_ok = false;  // more ties than the log holds
+        }
+        if (log_ok && cand) {
+          const int pos = nlog + __popc(mask & lt_mask);
+          s_logk[warp][pos] = k0[u];
+          s_logg[warp][pos] = gq[u];
+        }
+        nlog += m;
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          L.insert(__shfl_sync(0xffffffffu, k0[u], src), k);
+        }
       }
     }
     __syncwarp();
-    if (L.cnt == k && L.thr[0] < pub) {
-      pub = L.thr[0];
-      if (lane == 0) atomicMin(gthr, pub);
-    }
   }
-  // warp lists -> warp 0
-  if (lane < L.cnt) {
-#pragma unroll
-    for (int q = 0; q < NK; ++q) s_key[warp][lane][q] = L.e[q];
-    s_gid[warp][lane] = L.gid;
-  }
-  if (lane == 0) s_cnt[warp] = L.cnt;
+  if (!log_ok && lane == 0) s_err = 1;
+  if (lane < L.cnt) s_wv[warp][lane] = L.v;
+  if (lane == 0) s_wn[warp] = L.cnt;
   __syncthreads();
+  // block: k-way merge of the warp lists (lane w < kW holds warp w's head)
   if (warp == 0) {
-    for (int w = 1; w < kW; ++w) {
-      unsigned long long kk[NK];
-      const bool v = lane < s_cnt[w];
+    int hp = 0;
+    ValList B;
+    for (int r = 0; r < k; ++r) {
+      unsigned long long hv = lane < kW && hp < s_wn[lane] ? s_wv[lane][hp] : ~0ULL;
+      int hl = lane < kW && hp < s_wn[lane] ? lane : 32;
 #pragma unroll
-      for (int q = 0; q < NK; ++q) kk[q] = v ? s_key[w][lane][q] : ~0ULL;
-      L.offer(v, kk, v ? s_gid[w][lane] : 0u, k);
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ov = __shfl_xor_sync(0xffffffffu, hv, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, hl, o);
+        if (ov < hv || (ov == hv && ol < hl)) {
+          hv = ov;
+          hl = ol;
+        }
+      }
+      if (hl == 32) break;
+      if (lane == hl) ++hp;
+      if (lane == r) B.v = hv;
+      ++B.cnt;
     }
-    if (lane < L.cnt) {
-#pragma unroll
-      for (int q = 0; q < NK; ++q) blk_key[(static_cast<long long>(blockIdx.x) * kTopkMaxK + lane) * NK + q] = L.e[q];
-      blk_gid[static_cast<long long>(blockIdx.x) * kTopkMaxK + lane] = L.gid;
+    const unsigned long long tb = B.thr(k);
+    if (lane < B.cnt) blk_val[static_cast<long long>(blockIdx.x) * kTopkMaxK + lane] = B.v;
+    if (lane == 0) {
+      blk_nval[blockIdx.x] = B.cnt;
+      s_T = tb;
     }
-    if (lane == 0) blk_n[blockIdx.x] = L.cnt;
+  }
+  __syncthreads();
+  // publish the log entries at or below the block's k-th value
+  {
+    const unsigned long long T = s_T;
+    const int nl = log_ok ? nlog : 0;
+    for (int i0 = 0; i0 < nl; i0 += 32) {
+      const int i = i0 + lane;
+      const bool keep = i < nl && s_logk[warp][i] <= T;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      int basepos = 0;
+      if (lane == 0 && km) basepos = atomicAdd(&s_nc, __popc(km));
+      basepos = __shfl_sync(0xffffffffu, basepos, 0);
+      if (keep) {
+        const int pos = basepos + __popc(km & lt_mask);
+        if (pos < kTopkBlkCand) {
+          blk_ck[static_cast<long long>(blockIdx.x) * kTopkBlkCand + pos] = s_logk[warp][i];
+          blk_cg[static_cast<long long>(blockIdx.x) * kTopkBlkCand + pos] = s_logg[warp][i];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_nc > kTopkBlkCand) s_err = 1;
+    blk_nc[blockIdx.x] = s_nc < kTopkBlkCand ? s_nc : kTopkBlkCand;
+    if (s_err) err[0] = 1;
     __threadfence();
-    __syncwarp();
-    if (lane == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last block: every warp folds a share of the block lists (kTopkUnroll
-  // lists per round, loads issued together), then warp 0 folds the warp lists
-  TopkList<NK> F;
+  // last block: exact T = k-th smallest of every block's values; the lists
+  // are staged in shared memory first (nb * k <= kTopkStage), then merged
+  // k-way by warp 0 with heads in shared memory
   const int nb = static_cast<int>(gridDim.x);
-  for (int b0 = warp * kTopkUnroll; b0 < nb; b0 += kW * kTopkUnroll) {
-    int bn[kTopkUnroll];
-    unsigned long long kk[kTopkUnroll][NK];
-    unsigned gg[kTopkUnroll];
-#pragma unroll
-    for (int u = 0; u < kTopkUnroll; ++u) {
-      const int b = b0 + u < nb ? b0 + u : nb - 1;
-      bn[u] = b0 + u < nb ? __ldcg(blk_n + b) : 0;
-#pragma unroll
-      for (int q = 0; q < NK; ++q) kk[u][q] = __ldcg(blk_key + (static_cast<long long>(b) * kTopkMaxK + lane) * NK + q);
-      gg[u] = __ldcg(blk_gid + static_cast<long long>(b) * kTopkMaxK + lane);
-    }
-#pragma unroll
-    for (int u = 0; u < kTopkUnroll; ++u) F.offer(lane < bn[u], kk[u], gg[u], k);
+  unsigned long long* sv = reinterpret_cast<unsigned long long*>(s_scratch);  // [nb][k]
+  int* hpos = reinterpret_cast<int*>(sv + nb * k);
+  int* hlen = hpos + nb;
+  int* cnb = hlen + nb;  // published candidates per block
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    hlen[b] = __ldcg(blk_nval + b);
+    cnb[b] = __ldcg(blk_nc + b);
+    hpos[b] = 0;
   }
-  __syncthreads();
-  if (lane < F.cnt) {
-#pragma unroll
-    for (int q = 0; q < NK; ++q) s_key[warp][lane][q] = F.e[q];
-    s_gid[warp][lane] = F.gid;
-  }
-  if (lane == 0) s_cnt[warp] = F.cnt;
+  for (int i = threadIdx.x; i < nb * k; i += blockDim.x)
+    sv[i] = __ldcg(blk_val + static_cast<long long>(i / k) * kTopkMaxK + i % k);
   __syncthreads();
   if (warp == 0) {
-    for (int w = 1; w < kW; ++w) {
-      unsigned long long kk[NK];
-      const bool v = lane < s_cnt[w];
+    unsigned long long T = ~0ULL;
+    for (int r = 0; r < k; ++r) {
+      unsigned long long bv = ~0ULL;
+      int bl = -1;
+      for (int b = lane; b < nb; b += 32)
+        if (hpos[b] < hlen[b] && (bl < 0 || sv[b * k + hpos[b]] < bv)) {
+          bv = sv[b * k + hpos[b]];
+          bl = b;
+        }
 #pragma unroll
-      for (int q = 0; q < NK; ++q) kk[q] = v ? s_key[w][lane][q] : ~0ULL;
-      F.offer(v, kk, v ? s_gid[w][lane] : 0u, k);
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (ol >= 0 && (bl < 0 || ov < bv || (ov == bv && ol < bl))) {
+          bv = ov;
+          bl = ol;
+        }
+      }
+      if (bl < 0) break;
+      T = bv;  // after k rounds: the k-th smallest
+      if (lane == 0) ++hpos[bl];
+      __syncwarp();
+    }
+    if (lane == 0) {
+      s_T = T;
+      s_nc = 0;
+    }
+  }
+  __syncthreads();
+  // final candidates: published entries with k0 <= T (one thread per block list)
+  const unsigned long long T = s_T;
+  unsigned* fg = reinterpret_cast<unsigned*>(cnb + nb);
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int ncb = cnb[b];
+    for (int i = 0; i < ncb; ++i) {
+      const long long e = static_cast<long long>(b) * kTopkBlkCand + i;
+      if (__ldcg(blk_ck + e) <= T) {
+        const int pos = atomicAdd(&s_nc, 1);
+        if (pos < kTopkFinal) fg[pos] = __ldcg(blk_cg + e);
+      }
+    }
+  }
+  __syncthreads();
+  const int nfc = s_nc < kTopkFinal ? s_nc : kTopkFinal;
+  if (threadIdx.x == 0 && s_nc > kTopkFinal) err[0] = 1;
+  // full keys of the final candidates, then the exact order (warp 0)
+  unsigned long long* fk = reinterpret_cast<unsigned long long*>(fg + kTopkFinal + 2);
+  fk = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(fk) + 7) & ~uintptr_t(7));
+  for (int i = threadIdx.x; i < nfc; i += blockDim.x) {
+    unsigned long long kk[NK];
+    cand_keys_nk<NK>(s, fg[i], kk);
+#pragma unroll
+    for (int q = 0; q < NK; ++q) fk[i * NK + q] = kk[q];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    TopkList<NK> F;
+    for (int i0 = 0; i0 < nfc; i0 += 32) {
+      const int i = i0 + lane;
+      unsigned long long kk[NK];
+#pragma unroll
+      for (int q = 0; q < NK; ++q) kk[q] = i < nfc ? fk[i * NK + q] : ~0ULL;
+      F.offer(i < nfc, kk, i < nfc ? fg[i] : 0u, k);
     }
     if (lane < F.cnt) {
       const unsigned g = F.gid;
@@ -1406,8 +1555,8 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
   }
 }
 
-using TopkKernel = void (*)(GroupSpec, long long, int, unsigned long long*, unsigned*, int*, unsigned*,
-                            unsigned long long*, long long*, long long*);
+using TopkKernel = void (*)(GroupSpec, long long, int, unsigned long long*, int*, unsigned long long*, unsigned*, int*,
+                            unsigned*, long long*, long long*);
 TopkKernel topk_kernel(int nk) {
   switch (nk) {
     case 1: return k_topk_groups<1>;
@@ -2294,13 +2443,17 @@ struct Runner {
       ps.gacc = gacc_p;
       ps.gcnt = gcnt_p;
       ps.group_probe = P.group_probe;
+      auto touched = c.alloc_bytes(sizeof(unsigned) * ((ngroups + 31) / 32 + 1));
+      TQP_CUDA(cudaMemsetAsync(touched->ptr, 0, touched->bytes, c.stream));
+      keep.push_back(touched);
+      ps.touched = static_cast<unsigned*>(touched->ptr);
       launch_tile(kfn, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
       gs.f = fs;
       gs.gacc = ps.gacc;
       gs.gcnt = ps.gcnt;
       gs.group_row = group_row;
-      gs.present = group_present;
+      gs.present = ps.touched;  // groups with rows (a subset of the inserted slots)
       gs.acc_words = kLimbWords;
       const BuildDesc& gb = P.builds[P.probes[P.group_probe].build];
       const Table* groot = bind_table(tables, gb.table);
@@ -2314,7 +2467,7 @@ struct Runner {
       if (po) {
         // the touched groups as self-describing records, keyed by the unique
         // build key: shards may split a group (the merge adds exactly)
-        Tensor gids = touched_groups(c, ps.gcnt, ngroups, group_present);
+        Tensor gids = touched_groups(c, ps.gcnt, ngroups, ps.touched);
         const long long n = gids.rows;
         const int words = record_words(gs.nkeyc, fs.nacc);
         unsigned long long* rec = part_buf(n, words);
@@ -2414,19 +2567,24 @@ struct Runner {
       const int nk = gs.nsort + gs.nkeyc;
       TopkKernel kern = topk_kernel(nk);
       if (!kern || k > kTopkMaxK || gs.nsort < 1) return false;
-      const int blocks = static_cast<int>(std::max<long long>(1, std::min<long long>(2LL * c.num_sms, (ngroups + 4095) / 4096)));
-      auto bkey = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkMaxK * nk);
-      auto bgid = c.alloc_bytes(sizeof(unsigned) * blocks * kTopkMaxK);
-      auto bn = c.alloc_bytes(sizeof(int) * blocks + 32);
-      // [blk_n x blocks][ticket (4 B) + pad][gthr (8 B, all ones)]
-      unsigned char* tail = static_cast<unsigned char*>(bn->ptr) + ((sizeof(int) * blocks + 7) & ~size_t(7));
-      unsigned* ticket = reinterpret_cast<unsigned*>(tail);
-      unsigned long long* gthr = reinterpret_cast<unsigned long long*>(tail + 8);
-      TQP_CUDA(cudaMemsetAsync(ticket, 0, 8, c.stream));
-      TQP_CUDA(cudaMemsetAsync(gthr, 0xff, 8, c.stream));
-      kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bkey->ptr),
-                                              static_cast<unsigned*>(bgid->ptr), static_cast<int*>(bn->ptr), ticket,
-                                              gthr, err + 2, err);
+      // one wave: as many blocks as are resident at once (the last block
+      // merges one value list per block)
+      int per_sm = 1;
+      TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern), kTopkThreads, 0));
+      const int blocks = static_cast<int>(std::max<long long>(
+          1, std::min<long long>({static_cast<long long>(std::max(1, std::min(per_sm, 2))) * c.num_sms,
+                                  (ngroups + 8191) / 8192, static_cast<long long>(kTopkStage / std::max(1, k))})));
+      auto bval = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkMaxK);
+      auto bck = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkBlkCand);
+      auto bcg = c.alloc_bytes(sizeof(unsigned) * blocks * kTopkBlkCand);
+      auto bn = c.alloc_bytes(sizeof(int) * 2 * blocks + 16);
+      int* bnval = static_cast<int*>(bn->ptr);
+      int* bnc = bnval + blocks;
+      unsigned* ticket = reinterpret_cast<unsigned*>(bnc + blocks);
+      TQP_CUDA(cudaMemsetAsync(ticket, 0, 4, c.stream));
+      kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bval->ptr), bnval,
+                                                  static_cast<unsigned long long*>(bck->ptr),
+                                                  static_cast<unsigned*>(bcg->ptr), bnc, ticket, err + 2, err);
       c.count_launch();
       nrows = -1;  // on the device (err[2]); read with the error flag
       return true;

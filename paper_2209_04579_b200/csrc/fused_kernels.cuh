@@ -456,7 +456,10 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
 #pragma unroll
             for (int p = 1; p < kMaxProbes; ++p) gg = s.group_probe == p ? rc[k].gid[p] : gg;
             g[k] = pass[k] ? gg : 0u;
-            if (pass[k]) atomicAdd(s.gcnt + g[k], 1ULL);
+            if (pass[k]) {
+              atomicAdd(s.gcnt + g[k], 1ULL);
+              atomicOr(s.touched + (g[k] >> 5), 1u << (g[k] & 31));
+            }
           }
         }
         // values, fully unrolled (NA is a template parameter) and branch-free:

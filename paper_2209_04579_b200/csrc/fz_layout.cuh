@@ -133,6 +133,7 @@ struct ProbeSpec {
   unsigned long long* part;  // SCALAR: [cta][nacc+1]; SMALL: per-CTA tables
   unsigned long long* gacc;  // BUILDGRP: [group][nacc] x kLimbWords (Q64.64 or int64 as limbs)
   unsigned long long* gcnt;  // BUILDGRP: [group]
+  unsigned* touched;         // BUILDGRP: bit per group with a row (the top-k walk's index)
   long long* err;            // [0] != 0: data violates the fused preconditions
 };
 

@@ -141,6 +141,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
         for (int k = 0; k < Q_R; ++k) {
           if (!pass[k]) continue;
           atomicAdd(s.gcnt + gid[k], 1ULL);
+          atomicOr(s.touched + (gid[k] >> 5), 1u << (gid[k] & 31));
 #pragma unroll
           for (int a = 0; a < Q_NA; ++a) {
             __int128 qv;
