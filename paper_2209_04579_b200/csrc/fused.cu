@@ -1093,7 +1093,11 @@ struct GroupSpec {
   FinalSpec f;
   const unsigned long long* gacc;
   const unsigned long long* gcnt;
-  const int* group_row;  // group -> build row; nullptr: merged groups (identity)
+  // group -> build row through the build table entry (rowid + 1 in bits
+  // 0-31); nullptr: merged groups (identity)
+  const unsigned long long* group_table;
+  long long cnt_stride = 1;  // words between groups' counts
+  long long acc_stride = 0;  // words between groups' accumulator blocks
   int nkeyc;
   const long long* key_cols[kMaxKeys];  // root columns for the group keys
   int nsort;
@@ -1105,19 +1109,19 @@ struct GroupSpec {
 
 // accumulator a of group g as int128
 __device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, int a) {
-  const unsigned long long* w = s.gacc + (static_cast<long long>(g) * s.f.nacc + a) * s.acc_words;
+  const unsigned long long* w = s.gacc + static_cast<long long>(g) * s.acc_stride + a * s.acc_words;
   if (s.acc_words == kLimbWords) return limbs_to_i128(w);
   return static_cast<__int128>((static_cast<unsigned __int128>(w[1]) << 64) | w[0]);
 }
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g) {
-  return s.group_row ? s.group_row[g] : static_cast<long long>(g);
+  return s.group_table ? static_cast<long long>(s.group_table[g] & 0xffffffffULL) - 1 : static_cast<long long>(g);
 }
 
 __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
                                                 bool& is_f64) {
   const OutKind& o = s.f.outs[j];
-  long long cnt = static_cast<long long>(s.gcnt[g]);
+  long long cnt = static_cast<long long>(s.gcnt[g * s.cnt_stride]);
   if (o.fn >= 10) {
     bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][group_src_row(s, g)]);
     is_f64 = false;
@@ -1345,7 +1349,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
       for (int u = 0; u < kTopkUnroll; ++u) {
         const int i = c0 + u * 32 + lane;
         gq[u] = i < total ? static_cast<unsigned>(base) + sidx[i] : 0u;
-        gc[u] = i < total ? s.gcnt[gq[u]] : 0ULL;
+        gc[u] = i < total ? s.gcnt[gq[u] * s.cnt_stride] : 0ULL;
       }
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
@@ -1583,15 +1587,16 @@ __global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids_sor
   }
 }
 
-__global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long n, const unsigned* present,
-                                 uint8_t* __restrict__ mask) {
+__global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long cnt_stride, long long n,
+                                 const unsigned* present, uint8_t* __restrict__ mask) {
   for (long long i = gtid(); i < n; i += gstride())
-    mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i] != 0;
+    mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i * cnt_stride] != 0;
 }
 
-__global__ void k_group_keys(const int* __restrict__ group_row, const long long* __restrict__ gids, long long n,
+__global__ void k_group_keys(const unsigned long long* __restrict__ group_table, const long long* __restrict__ gids, long long n,
                              const long long* __restrict__ key_col, long long* __restrict__ out) {
-  for (long long i = gtid(); i < n; i += gstride()) out[i] = key_col[group_row ? group_row[gids[i]] : gids[i]];
+  for (long long i = gtid(); i < n; i += gstride())
+    out[i] = key_col[group_table ? static_cast<long long>(group_table[gids[i]] & 0xffffffffULL) - 1 : gids[i]];
 }
 
 // ---- sharded-run partials ------------------------------------------------------
@@ -1615,8 +1620,8 @@ __global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, 
     unsigned long long* w = out + i * words;
     w[0] = static_cast<unsigned long long>(bkey[row]);
     for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(s.key_cols[k][row]);
-    w[1 + s.nkeyc] = s.gcnt[g];
-    if (s.acc_words == kLimbWords && s.gcnt[g] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+    w[1 + s.nkeyc] = s.gcnt[g * s.cnt_stride];
+    if (s.acc_words == kLimbWords && w[1 + s.nkeyc] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
     for (int a = 0; a < s.f.nacc; ++a) {  // records carry int128 (lo, hi)
       const unsigned __int128 v = static_cast<unsigned __int128>(group_acc(s, g, a));
       w[2 + s.nkeyc + 2 * a] = static_cast<unsigned long long>(v);
@@ -1976,7 +1981,14 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
 // equality literal without zero bytes compares the leading bytes directly
 // (a zero-padded row shorter than the pattern cannot match a zero-free
 // pattern); anything else calls eval_str.
-constexpr int kJitBuildRows = 4;
+int jit_build_rows() {
+  static const int r = [] {
+    const char* e = std::getenv("TQP_BUILD_ROWS");  // tuning knob: rows per thread of q_build
+    const int v = e ? std::atoi(e) : 4;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+  }();
+  return r;
+}
 
 std::string str_pred(const StrTerm& t, const std::string& sref, const std::string& row) {
   bool zero_free = true;
@@ -2012,8 +2024,8 @@ std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap)
     return "static_cast<unsigned long long>(__ldg(static_cast<const unsigned long long*>(" + ptr + ") + " + row + "))";
   };
   static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
-  o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << kJitBuildRows << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0)
-    << "\n#define B_ZACC " << b.zacc_words << "\n"
+  o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << jit_build_rows() << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0)
+    << "\n#define B_ZREC " << b.zrec_words << "\n"
     << "namespace tqp { namespace fz {\n"
     << "__device__ __forceinline__ void b_rows(const BuildSpec& s, long long r0, int stride, bool* pass, long long* key,\n"
     << "                                       unsigned* flags) {\n"
@@ -2032,8 +2044,10 @@ std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap)
   for (int p = 0; p < b.nprobes; ++p)
     o << "    pv" << p << "[j] = " << ld(b.probes[p].key, "s.probes[" + std::to_string(p) + "].key.ptr", "rr") << ";\n";
   // phase by phase over all B_ROWS rows, so the rows' dependent probe loads
-  // (presence word, then entry) are in flight together
-  o << "  }\n#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n    bool ok = pass[j];\n    key[j] = static_cast<long long>(kv[j]);\n";
+  // (presence word, then entry) are in flight together; the empty asm keeps
+  // the compiler from sinking the column loads to their first use
+  o << "  }\n  asm volatile(\"\" ::: \"memory\");\n"
+    << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n    bool ok = pass[j];\n    key[j] = static_cast<long long>(kv[j]);\n";
   for (int t = 0; t < b.nterms; ++t) {
     const Term& T = b.terms[t];
     const int op = T.op < 0 || T.op > 5 ? 5 : T.op;
@@ -2095,10 +2109,10 @@ struct Runner {
     std::vector<Probe> built(P.builds.size());
     std::vector<std::shared_ptr<DevBuf>> keep;
     std::vector<long long> build_range(P.builds.size(), 0);
-    int* group_row = nullptr;
+    const unsigned long long* group_table = nullptr;
     const unsigned* group_present = nullptr;
-    unsigned long long* gacc_p = nullptr;
-    unsigned long long* gcnt_p = nullptr;
+    unsigned long long* grec_p = nullptr;
+    int grec_words = 0;
     const int nacc_all = static_cast<int>(P.accs.size());
     // key ranges of every build side: one launch each, one host round trip
     const size_t nb = P.builds.size();
@@ -2181,30 +2195,26 @@ struct Runner {
         bs.probes[bs.nprobes++] = p;
       }
       if (B.assign_groups) {
-        // the group is the key slot: per-slot build row and accumulators,
-        // written only for the slots a row is inserted into
-        auto gr = c.alloc_bytes(sizeof(int) * (range + 1));
-        auto gacc = c.alloc_bytes(sizeof(unsigned long long) * kLimbWords * std::max(1, nacc_all) * (range + 1));
-        auto gcnt = c.alloc_bytes(sizeof(unsigned long long) * (range + 1));
-        keep.push_back(gr);
-        keep.push_back(gacc);
-        keep.push_back(gcnt);
-        group_row = static_cast<int*>(gr->ptr);
+        // the group is the key slot: one record per slot [count, limbs per
+        // accumulator], whole 32-byte sectors, written only for inserted slots
+        grec_words = (1 + kLimbWords * std::max(1, nacc_all) + 3) & ~3;
+        auto grec = c.alloc_bytes(sizeof(unsigned long long) * grec_words * (range + 1));
+        keep.push_back(grec);
+        group_table = bs.table;
         group_present = bs.bitmap;
-        gacc_p = static_cast<unsigned long long*>(gacc->ptr);
-        gcnt_p = static_cast<unsigned long long*>(gcnt->ptr);
+        grec_p = static_cast<unsigned long long*>(grec->ptr);
         bs.assign_groups = 1;
-        bs.group_row = group_row;
-        bs.zacc = gacc_p;
-        bs.zacc_words = kLimbWords * nacc_all;
-        bs.zcnt = gcnt_p;
+        bs.zrec = grec_p;
+        bs.zrec_words = grec_words;
       }
       if (!ok) return false;
       if (n) {
         // kBuildRows rows per thread: the per-row dependent loads (term,
         // probe, insert) need many warps in flight
         const void* bk = reinterpret_cast<const void*>(&k_build);
+        int rows_per_thread = kBuildRows;
         if (jit_wanted(n)) {
+          rows_per_thread = jit_build_rows();
           std::vector<bool> bm;
           for (const auto& ch : B.children) {
             const BuildDesc& CB = P.builds[ch.build];
@@ -2214,7 +2224,8 @@ struct Runner {
         }
         void* args[] = {&bs};
         cudaEvent_t ev = c.kernel_begin();
-        TQP_CUDA(cudaLaunchKernel(bk, dim3(c.grid_for(n, kThreads, kBuildRows, 1 << 20)), dim3(kThreads), args, 0, c.stream));
+        TQP_CUDA(cudaLaunchKernel(bk, dim3(c.grid_for(n, kThreads, rows_per_thread, 1 << 20)), dim3(kThreads), args, 0,
+                                  c.stream));
         c.kernel_end(bk == reinterpret_cast<const void*>(&k_build) ? "k_build" : "q_build", ev);
         c.count_launch();
         k_bitmap_popc<<<c.grid_for(bm_words / 4 + 1, 256, 4, 4), 256, 0, c.stream>>>(bs.bitmap, bm_words, bs.counts);
@@ -2439,9 +2450,10 @@ struct Runner {
     } else {
       // MODE_BUILDGRP
       long long ngroups = build_range[P.probes[P.group_probe].build];
-      if (!gacc_p || !group_present) return false;  // the group build assigns the groups
-      ps.gacc = gacc_p;
-      ps.gcnt = gcnt_p;
+      if (!grec_p || !group_present) return false;  // the group build assigns the groups
+      ps.gcnt = grec_p;
+      ps.gacc = grec_p + 1;
+      ps.gstride = grec_words;
       ps.group_probe = P.group_probe;
       auto touched = c.alloc_bytes(sizeof(unsigned) * ((ngroups + 31) / 32 + 1));
       TQP_CUDA(cudaMemsetAsync(touched->ptr, 0, touched->bytes, c.stream));
@@ -2452,7 +2464,9 @@ struct Runner {
       gs.f = fs;
       gs.gacc = ps.gacc;
       gs.gcnt = ps.gcnt;
-      gs.group_row = group_row;
+      gs.group_table = group_table;
+      gs.cnt_stride = grec_words;
+      gs.acc_stride = grec_words;
       gs.present = ps.touched;  // groups with rows (a subset of the inserted slots)
       gs.acc_words = kLimbWords;
       const BuildDesc& gb = P.builds[P.probes[P.group_probe].build];
@@ -2467,7 +2481,7 @@ struct Runner {
       if (po) {
         // the touched groups as self-describing records, keyed by the unique
         // build key: shards may split a group (the merge adds exactly)
-        Tensor gids = touched_groups(c, ps.gcnt, ngroups, ps.touched);
+        Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, ngroups, ps.touched);
         const long long n = gids.rows;
         const int words = record_words(gs.nkeyc, fs.nacc);
         unsigned long long* rec = part_buf(n, words);
@@ -2538,10 +2552,12 @@ struct Runner {
     return -1;  // on the device (err[2]); read with the error flag
   }
 
-  static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long ngroups, const unsigned* present) {
+  static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long cnt_stride, long long ngroups,
+                               const unsigned* present) {
     Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
     if (ngroups) {
-      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, ngroups, present, mask.ptr<uint8_t>());
+      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, cnt_stride, ngroups, present,
+                                                                       mask.ptr<uint8_t>());
       c.count_launch();
     }
     return k::compact(c, k::iota(c, ngroups), mask);
@@ -2589,11 +2605,11 @@ struct Runner {
       nrows = -1;  // on the device (err[2]); read with the error flag
       return true;
     }
-    Tensor gids = touched_groups(c, gs.gcnt, ngroups, gs.present);
+    Tensor gids = touched_groups(c, gs.gcnt, gs.cnt_stride, ngroups, gs.present);
     const long long n = gids.rows;
     Tensor keys = c.alloc(TQP_I64, n, 1);
     if (n) {
-      k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_row, gids.ptr<long long>(), n, bk,
+      k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gids.ptr<long long>(), n, bk,
                                                               keys.ptr<long long>());
       c.count_launch();
     }
@@ -2682,7 +2698,9 @@ struct Runner {
       gs.f = fs;
       gs.gacc = static_cast<unsigned long long*>(hacc->ptr);
       gs.gcnt = static_cast<unsigned long long*>(hcnt->ptr);
-      gs.group_row = nullptr;
+      gs.group_table = nullptr;
+      gs.cnt_stride = 1;
+      gs.acc_stride = 2LL * fs.nacc;
       gs.nkeyc = nkeyc;
       for (int i = 0; i < nkeyc; ++i) gs.key_cols[i] = static_cast<const long long*>(hkeys->ptr) + i * cap;
       ok = emit_groups(c, gs, cap, static_cast<const long long*>(hbk->ptr), err, outs, nrows);

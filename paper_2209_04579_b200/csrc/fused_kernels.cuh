@@ -128,11 +128,8 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
           atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
           idx = -1;
         } else {
-          if (s.assign_groups) {  // the group is the key slot
-            s.group_row[idx] = static_cast<int>(r);
-            s.zcnt[idx] = 0ULL;
-            for (int w = 0; w < s.zacc_words; ++w) s.zacc[idx * s.zacc_words + w] = 0ULL;
-          }
+          if (s.assign_groups)  // the group is the key slot: zero its record
+            for (int w = 0; w < s.zrec_words; ++w) s.zrec[idx * s.zrec_words + w] = 0ULL;
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags) << 57);
           ++inserted;
         }
@@ -457,7 +454,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             for (int p = 1; p < kMaxProbes; ++p) gg = s.group_probe == p ? rc[k].gid[p] : gg;
             g[k] = pass[k] ? gg : 0u;
             if (pass[k]) {
-              atomicAdd(s.gcnt + g[k], 1ULL);
+              atomicAdd(s.gcnt + static_cast<long long>(g[k]) * s.gstride, 1ULL);
               atomicOr(s.touched + (g[k] >> 5), 1u << (g[k] & 31));
             }
           }
@@ -543,7 +540,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
                 qv = 0;
               }
-              atomic_add_limbs(s.gacc + (static_cast<long long>(g[k]) * NAX + a) * kLimbWords, qv);
+              atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
             }
           }
         }

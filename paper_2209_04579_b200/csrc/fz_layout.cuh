@@ -131,8 +131,11 @@ struct ProbeSpec {
   int group_probe = -1;    // MODE_BUILDGRP
   // outputs
   unsigned long long* part;  // SCALAR: [cta][nacc+1]; SMALL: per-CTA tables
-  unsigned long long* gacc;  // BUILDGRP: [group][nacc] x kLimbWords (Q64.64 or int64 as limbs)
-  unsigned long long* gcnt;  // BUILDGRP: [group]
+  // BUILDGRP group records, gstride words per group (a multiple of 4: whole
+  // 32-byte sectors): [row count, kLimbWords limbs per accumulator]
+  unsigned long long* gacc;  // record + 1
+  unsigned long long* gcnt;  // record
+  int gstride;
   unsigned* touched;         // BUILDGRP: bit per group with a row (the top-k walk's index)
   long long* err;            // [0] != 0: data violates the fused preconditions
 };
@@ -153,12 +156,10 @@ struct BuildSpec {
   unsigned long long* table = nullptr;
   unsigned* bitmap = nullptr;
   int assign_groups = 0;
-  int* group_row = nullptr;  // [key slot] -> build row, for the slots inserted
-  // group state zeroed by the row inserted into the slot (no memset over the
-  // whole key range): zacc_words words of zacc and one word of zcnt per slot
-  unsigned long long* zacc = nullptr;
-  int zacc_words = 0;
-  unsigned long long* zcnt = nullptr;
+  // group records zeroed by the row inserted into the slot (no memset over
+  // the whole key range): zrec_words words per slot (whole sectors)
+  unsigned long long* zrec = nullptr;
+  int zrec_words = 0;
   // [0, kCountSlots) rows inserted (per-warp totals, spread), [kCountSlots]
   // presence bits set (k_build_verify): they differ iff
   // two inserted rows share a key (a 1:N join, outside the fused contract).

@@ -7,8 +7,8 @@
 //        r0 + j * stride (j < B_ROWS), straight-line with every constant
 //        folded and every independent load issued first (fused.cu's generator)
 //
-//   B_ASSIGN, B_ZACC                          group-assigning build, words of
-//                                            group state zeroed per slot
+//   B_ASSIGN, B_ZREC                          group-assigning build, words of
+//                                            the group record zeroed per slot
 //
 // The rest is k_build's (fused_kernels.cuh): the group of a group-assigning
 // build is its key slot (its state zeroed by the inserted row), the direct-
@@ -42,10 +42,11 @@ extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s
           idx = -1;
         } else {
 #if B_ASSIGN
-          s.group_row[idx] = static_cast<int>(r);  // the group is the key slot
-          s.zcnt[idx] = 0ULL;
+          {  // the group is the key slot: zero its record (whole sectors)
+            ulonglong2* rec = reinterpret_cast<ulonglong2*>(s.zrec + idx * B_ZREC);
 #pragma unroll
-          for (int w = 0; w < B_ZACC; ++w) s.zacc[idx * B_ZACC + w] = 0ULL;
+            for (int w = 0; w < B_ZREC / 2; ++w) rec[w] = make_ulonglong2(0ULL, 0ULL);
+          }
 #endif
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[j]) << 57);
           ++inserted;

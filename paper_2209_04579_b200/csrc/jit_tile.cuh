@@ -140,7 +140,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
 #pragma unroll
         for (int k = 0; k < Q_R; ++k) {
           if (!pass[k]) continue;
-          atomicAdd(s.gcnt + gid[k], 1ULL);
+          atomicAdd(s.gcnt + static_cast<long long>(gid[k]) * s.gstride, 1ULL);
           atomicOr(s.touched + (gid[k] >> 5), 1u << (gid[k] & 31));
 #pragma unroll
           for (int a = 0; a < Q_NA; ++a) {
@@ -151,7 +151,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
               atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
               qv = 0;
             }
-            atomic_add_limbs(s.gacc + (static_cast<long long>(gid[k]) * Q_NA + a) * kLimbWords, qv);
+            atomic_add_limbs(s.gacc + static_cast<long long>(gid[k]) * s.gstride + a * kLimbWords, qv);
           }
         }
       }
