@@ -91,7 +91,15 @@ tqp_ctx* tqp_init(int device, tqp_status* st) {
     uint64_t threshold = UINT64_MAX;  // keep freed blocks cached in the pool
     TQP_CUDA(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     TQP_CUDA(cudaMalloc(&c.d_err, 64));
-    TQP_CUDA(cudaMallocHost(&c.h_err, 64));
+    TQP_CUDA(cudaMallocHost(&c.h_err, sizeof(long long) * Ctx::kPinnedWords));
+    // constant sources of small async uploads (see Ctx::kPinned*)
+    c.h_err[Ctx::kPinnedErrInit] = 0x7fffffffffffffffLL;
+    c.h_err[Ctx::kPinnedErrInit + 1] = 0;
+    c.h_err[Ctx::kPinnedErrInit + 2] = 0;
+    for (int i = 0; i < Ctx::kPinnedMinMaxPairs; ++i) {
+      c.h_err[Ctx::kPinnedMinMax + 2 * i] = 0x7fffffffffffffffLL;
+      c.h_err[Ctx::kPinnedMinMax + 2 * i + 1] = static_cast<long long>(0x8000000000000000ULL);
+    }
     return h;
   });
 }

@@ -260,14 +260,13 @@ void Executor::release_after(int s, std::vector<std::optional<Tensor>>& slots) {
 void Executor::time_begin(cudaEvent_t* ev) {
   *ev = nullptr;
   if (!timing_) return;
-  TQP_CUDA(cudaEventCreate(ev));
+  *ev = ctx_.take_event();
   TQP_CUDA(cudaEventRecord(*ev, ctx_.stream));
 }
 
 void Executor::time_end(const std::string& name, cudaEvent_t start) {
   if (!start) return;
-  cudaEvent_t stop;
-  TQP_CUDA(cudaEventCreate(&stop));
+  cudaEvent_t stop = ctx_.take_event();
   TQP_CUDA(cudaEventRecord(stop, ctx_.stream));
   timings_[name].pending.push_back({start, stop});
 }
@@ -287,8 +286,8 @@ void Executor::drain_timings() {
       TQP_CUDA(cudaEventElapsedTime(&ms, a, b));
       t.total_ms += ms;
       t.calls += 1;
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
+      ctx_.give_event(a);
+      ctx_.give_event(b);
     }
     t.pending.clear();
   }
@@ -342,7 +341,7 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
       time_begin(&ev);
       bool ok = unit.run(ctx_, slots, tables);
       if (ok) time_end(unit.name, ev);
-      else if (ev) cudaEventDestroy(ev);
+      else ctx_.give_event(ev);
       if (ok) {
         if (trace) {
           ctx_.sync();
@@ -430,7 +429,7 @@ Partial Executor::execute_partial(const TableSet& tables) {
   time_begin(&ev);
   Partial p;
   if (!u.partial(ctx_, tables, &p)) {
-    if (ev) cudaEventDestroy(ev);
+    ctx_.give_event(ev);
     exec_fail(plan_.steps[u.last_step].id + ": this shard violates the fused path's preconditions "
               "(non-unique or sparse build keys, an int64 overflow, or more than 8 groups per block); "
               "run it unsharded");

@@ -2124,7 +2124,9 @@ struct Runner {
         mm[2 * bi + 1] = static_cast<long long>(0x8000000000000000ULL);
       }
       mmb = c.alloc_bytes(sizeof(long long) * 2 * nb);
-      TQP_CUDA(cudaMemcpyAsync(mmb->ptr, mm.data(), sizeof(long long) * 2 * nb, cudaMemcpyHostToDevice, c.stream));
+      const bool pinned = nb <= static_cast<size_t>(Ctx::kPinnedMinMaxPairs);
+      TQP_CUDA(cudaMemcpyAsync(mmb->ptr, pinned ? c.h_err + Ctx::kPinnedMinMax : mm.data(), sizeof(long long) * 2 * nb,
+                               cudaMemcpyHostToDevice, c.stream));
       for (size_t bi = 0; bi < nb; ++bi) {
         const BuildDesc& B = P.builds[bi];
         const Table* tab = bind_table(tables, B.table);
@@ -2136,8 +2138,10 @@ struct Runner {
           c.count_launch();
         }
       }
-      TQP_CUDA(cudaMemcpyAsync(mm.data(), mmb->ptr, sizeof(long long) * 2 * nb, cudaMemcpyDeviceToHost, c.stream));
+      long long* rd = pinned ? c.h_err + Ctx::kPinnedRead : mm.data();
+      TQP_CUDA(cudaMemcpyAsync(rd, mmb->ptr, sizeof(long long) * 2 * nb, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
+      if (pinned) std::memcpy(mm.data(), rd, sizeof(long long) * 2 * nb);
     }
     for (size_t bi = 0; bi < P.builds.size(); ++bi) {
       const BuildDesc& B = P.builds[bi];
@@ -2396,7 +2400,7 @@ struct Runner {
                                   (P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small" : "buildgrp") + "," +
                                   std::to_string(ps.nacc) + ">";
     auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {
-      cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      cudaError_t e = c.ensure_smem(kernel, static_cast<int>(smem));
       if (e != cudaSuccess) {
         throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e) + " setting " + std::to_string(smem) +
                                       " B dynamic smem (static " + std::to_string(fa.sharedSizeBytes) + ", optin " +
@@ -2495,8 +2499,9 @@ struct Runner {
       }
     }
     long long herr[4] = {0, 0, 0, 0};
-    TQP_CUDA(cudaMemcpyAsync(herr, err, 32, cudaMemcpyDeviceToHost, c.stream));
+    TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedRead, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
     if (herr[0]) {  // preconditions violated: exact per-instruction path
       if (po) *po = Partial{};
       return false;
@@ -2706,8 +2711,9 @@ struct Runner {
       ok = emit_groups(c, gs, cap, static_cast<const long long*>(hbk->ptr), err, outs, nrows);
     }
     long long herr[4] = {0, 0, 0, 0};
-    TQP_CUDA(cudaMemcpyAsync(herr, err, 32, cudaMemcpyDeviceToHost, c.stream));
+    TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedRead, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
     if (nrows < 0) nrows = herr[2];
     if (!ok || herr[0]) {
       // the local path would re-run these steps per instruction; merged

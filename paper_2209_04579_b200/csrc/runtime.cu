@@ -89,8 +89,7 @@ Tensor Ctx::alloc(int dtype, int64_t rows, int64_t cols) {
 void Ctx::sync() { TQP_CUDA(cudaStreamSynchronize(stream)); }
 
 void Ctx::reset_err() {
-  long long init[3] = {kNoBad, 0, 0};
-  TQP_CUDA(cudaMemcpyAsync(d_err, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+  TQP_CUDA(cudaMemcpyAsync(d_err, h_err + kPinnedErrInit, 3 * sizeof(long long), cudaMemcpyHostToDevice, stream));
 }
 
 int64_t Ctx::read_err(long long* aux, long long* kind) {

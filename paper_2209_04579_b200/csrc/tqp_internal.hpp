@@ -70,7 +70,14 @@ struct Ctx {
   // device scratch for kernel error reporting: [0] first bad index
   // (atomicMin, INT64_MAX = none), [1] aux value, [2] error kind
   long long* d_err = nullptr;
-  long long* h_err = nullptr;  // pinned mirror
+  long long* h_err = nullptr;  // pinned: [0, 3) error mirror, then the regions below
+  // pinned host words for small copies (pageable copies stage through the
+  // driver): constant upload sources and a readback area
+  static constexpr int kPinnedWords = 512;
+  static constexpr int kPinnedErrInit = 8;     // {INT64_MAX, 0, 0}
+  static constexpr int kPinnedMinMax = 64;     // kPinnedMinMaxPairs x {INT64_MAX, INT64_MIN}
+  static constexpr int kPinnedMinMaxPairs = 64;
+  static constexpr int kPinnedRead = 256;      // 256 words of readback
   std::atomic<int64_t> launches{0};
 
   Tensor alloc(int dtype, int64_t rows, int64_t cols);
@@ -86,19 +93,42 @@ struct Ctx {
   // the executor's timings
   bool time_kernels = false;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> kernel_events;
+  // timing events are recycled (creating one per launch costs host time
+  // between dependent launches)
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event() {
+    cudaEvent_t e;
+    if (!event_pool.empty()) {
+      e = event_pool.back();
+      event_pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
+  }
+  void give_event(cudaEvent_t e) {
+    if (e) event_pool.push_back(e);
+  }
   cudaEvent_t kernel_begin() {
     if (!time_kernels) return nullptr;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
+    cudaEvent_t e = take_event();
     cudaEventRecord(e, stream);
     return e;
   }
   void kernel_end(const std::string& name, cudaEvent_t start) {
     if (!start) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
+    cudaEvent_t e = take_event();
     cudaEventRecord(e, stream);
     kernel_events.push_back({name, {start, e}});
+  }
+  // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, size)
+  std::map<const void*, int> smem_set;
+  cudaError_t ensure_smem(const void* kernel, int bytes) {
+    auto it = smem_set.find(kernel);
+    if (it != smem_set.end() && it->second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) smem_set[kernel] = bytes;
+    return e;
   }
 };
 
