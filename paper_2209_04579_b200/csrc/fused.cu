@@ -834,8 +834,9 @@ struct Planner {
         P.key_columns.clear();
         int gp = -1;
         for (size_t p = 0; p < P.probes.size() && gp < 0; ++p) {
-          bool ok = true;
+          bool ok = true, has_row_key = false;
           std::vector<std::string> cols;
+          const std::string& bkey = P.builds[P.probes[p].build].key_column;
           for (int k : G.keys) {
             OperandDesc o;
             int lt;
@@ -845,14 +846,18 @@ struct Planner {
             }
             if (o.probe == static_cast<int>(p)) {
               cols.push_back(o.column);
+              has_row_key = has_row_key || iequals(o.column, bkey);
             } else if (o.probe < 0 && iequals(o.column, P.probes[p].fact_column)) {
-              cols.push_back(P.builds[P.probes[p].build].key_column);  // l_orderkey == o_orderkey
+              cols.push_back(bkey);  // l_orderkey == o_orderkey
+              has_row_key = true;
             } else {
               ok = false;
               break;
             }
           }
-          if (ok) {
+          // a group is one build row only if the keys include the build's
+          // (unique) key; other build columns may repeat across build rows
+          if (ok && has_row_key) {
             gp = static_cast<int>(p);
             P.group_key_root_columns = cols;
           }
@@ -1575,9 +1580,10 @@ TopkKernel topk_kernel(int nk) {
   }
 }
 
-__global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids_sorted, long long n, long long* err) {
+__global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids, const long long* __restrict__ order,
+                             long long n, long long* err) {
   for (long long r = gtid(); r < n; r += gstride()) {
-    unsigned g = static_cast<unsigned>(gids_sorted[r]);
+    unsigned g = static_cast<unsigned>(gids[order[r]]);
     for (int j = 0; j < s.f.nouts; ++j) {
       unsigned long long bits;
       bool f;
@@ -2618,13 +2624,14 @@ struct Runner {
                                                               keys.ptr<long long>());
       c.count_launch();
     }
-    Tensor order = k::radix_sort_payload(c, keys, &gids, false);
+    // positions of the touched groups in ascending build-key order
+    Tensor order = k::radix_sort_payload(c, keys, nullptr, false);
     for (size_t j = 0; j < outs.size(); ++j) {
       outs[j] = c.alloc(out_dtype(P, P.outs[j]), n, 1);
       gs.f.out_ptr[j] = outs[j].data();
     }
     if (n) {
-      k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, order.ptr<long long>(), n, err);
+      k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(), order.ptr<long long>(), n, err);
       c.count_launch();
     }
     nrows = n;

@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
 #pragma unroll
         for (int j = 0; j < kBuildRows; ++j) {
           const long long r = base0 + j * blockDim.x + threadIdx.x;
-          v[j] = pass[j] ? ld_row(s.terms[t].x, r) : 0ULL;
+          // constant terms (TK_TRUE / TK_FALSE) have no column
+          v[j] = pass[j] && s.terms[t].kind <= TK_F64 ? ld_row(s.terms[t].x, r) : 0ULL;
         }
 #pragma unroll
         for (int j = 0; j < kBuildRows; ++j) pass[j] = pass[j] && eval_term(s.terms[t], v[j]);
