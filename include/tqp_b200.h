@@ -174,6 +174,21 @@ void tqp_table_free(tqp_table* tab);
 tqp_table* tqp_gen_table(tqp_ctx* ctx, const char* table, double sf, uint64_t seed, int shard,
                          int nshards, tqp_status* st);
 
+/* ---- CSV loader ---------------------------------------
+ * tensql::parse_csv_text (columnar.cpp:453-519): the header line of `text`
+ * must name the schema's columns (case-insensitive); every data line is split
+ * on `delimiter` and parsed on the device into a table with the schema's names
+ * and logical types (TQP_LT_*). Field syntax, rounding and every error message
+ * are the reference's (std::from_chars, encode_date, valid_utf8); errors come
+ * back as EncodingError ("<origin>:<line>: column '<c>' (field k): ..."). */
+tqp_table* tqp_csv_parse(tqp_ctx* ctx, const char* text, int64_t len, const char* const* names,
+                         const int* logical_types, int ncols, char delimiter, const char* origin,
+                         tqp_status* st);
+/* tensql::load_csv (columnar.cpp:521-527): the file is read into pinned host
+ * memory and copied to HBM once; origin = path. */
+tqp_table* tqp_csv_load(tqp_ctx* ctx, const char* path, const char* const* names,
+                        const int* logical_types, int ncols, char delimiter, tqp_status* st);
+
 /* ---- OperatorPlan builder (operator_plan.hpp:16-92) ----------------------
  * op names are the reference's instr_op_name strings (operator_plan.cpp:11-42):
  * "compare", "arith", ..., "load_column", "const", "iota_rows", ... */

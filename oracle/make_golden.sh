@@ -7,6 +7,7 @@ make -j8 >/dev/null
 G=../tests/golden
 ./_ref/golden_cases kernels $G/kernels.json
 ./_ref/golden_cases plans $G/plans.json _ref/queries
+./_ref/csv_cases $G/csv.json
 ./_ref/tqp_ref_runner opplan --out ../paper_2209_04579_b200/plans
 SF=0.005
 ./_ref/tqp_ref_runner tables --sf $SF --out /tmp/tqp_tables.json

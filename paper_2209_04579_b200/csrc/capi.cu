@@ -539,3 +539,58 @@ extern "C" const char* tqp_plan_fusion_explain(const tqp_plan* p) {
   }
   return s.c_str();
 }
+
+// ---- CSV loader -----------------------------------------------
+namespace tqp {
+Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vector<std::pair<std::string, int>>& schema,
+                char delimiter, const std::string& origin);
+Table csv_load(Ctx& c, const std::string& path, const std::vector<std::pair<std::string, int>>& schema, char delimiter);
+}
+
+namespace {
+std::vector<std::pair<std::string, int>> csv_schema(const char* const* names, const int* types, int ncols) {
+  std::vector<std::pair<std::string, int>> s;
+  for (int i = 0; i < ncols; ++i) {
+    if (!names || !names[i] || !types) throw Error(TQP_ERR_ARG, "csv: null schema entry");
+    if (types[i] < TQP_LT_INT64 || types[i] > TQP_LT_BOOL) throw Error(TQP_ERR_ARG, "csv: bad logical type");
+    s.push_back({names[i], types[i]});
+  }
+  return s;
+}
+}  // namespace
+
+extern "C" tqp_table* tqp_csv_parse(tqp_ctx* ctx, const char* text, int64_t len, const char* const* names,
+                                    const int* logical_types, int ncols, char delimiter, const char* origin,
+                                    tqp_status* st) {
+  return guard(st, [&] {
+    if (!text && len) throw Error(TQP_ERR_ARG, "csv: null text");
+    auto schema = csv_schema(names, logical_types, ncols);
+    auto* t = new tqp_table;
+    t->ctx = &C_(ctx);
+    try {
+      t->t = tqp::csv_parse(*t->ctx, reinterpret_cast<const unsigned char*>(text), len, schema, delimiter,
+                            origin ? origin : "<csv>");
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    return t;
+  });
+}
+
+extern "C" tqp_table* tqp_csv_load(tqp_ctx* ctx, const char* path, const char* const* names, const int* logical_types,
+                                   int ncols, char delimiter, tqp_status* st) {
+  return guard(st, [&] {
+    if (!path) throw Error(TQP_ERR_ARG, "csv: null path");
+    auto schema = csv_schema(names, logical_types, ncols);
+    auto* t = new tqp_table;
+    t->ctx = &C_(ctx);
+    try {
+      t->t = tqp::csv_load(*t->ctx, path, schema, delimiter);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    return t;
+  });
+}

@@ -123,6 +123,9 @@ def _load() -> C.CDLL:
         "tqp_table_column_name": (C.c_char_p, [P, I]), "tqp_table_column_type": (I, [P, I]),
         "tqp_table_column": (P, [P, I]), "tqp_table_free": (None, [P]),
         "tqp_gen_table": (P, [P, C.c_char_p, D, U64, I, I, S]),
+        "tqp_csv_parse": (P, [P, C.c_char_p, C.c_int64, C.POINTER(C.c_char_p), C.POINTER(C.c_int), I, C.c_char,
+                              C.c_char_p, S]),
+        "tqp_csv_load": (P, [P, C.c_char_p, C.POINTER(C.c_char_p), C.POINTER(C.c_int), I, C.c_char, S]),
         "tqp_plan_create": (P, [I, S]), "tqp_plan_begin_step": (I, [P, C.c_char_p, C.c_char_p, S]),
         "tqp_plan_add_instr": (I, [P, C.POINTER(InstrDesc), S]),
         "tqp_plan_set_step_outputs": (I, [P, C.POINTER(C.c_int), I, S]),
@@ -492,6 +495,38 @@ class Table:
         ctx = ctx or default_context()
         st = Status()
         h = lib.tqp_gen_table(ctx.h, table.encode(), float(sf), int(seed), shard, nshards, C.byref(st))
+        _check(st, bool(h))
+        return Table(h, ctx)
+
+    @staticmethod
+    def _csv_schema(schema):
+        n = len(schema)
+        names = (C.c_char_p * max(1, n))(*[name.encode() for name, _ in schema])
+        types = (C.c_int * max(1, n))(*[LOGICAL_NAMES[lt] for _, lt in schema])
+        return names, types, n
+
+    @staticmethod
+    def from_csv_text(text, schema: Sequence[Tuple[str, str]], delimiter: str = ",", origin: str = "<csv>",
+                      ctx=None) -> "Table":
+        """tensql::parse_csv_text (columnar.cpp:453-519) on the device:
+        schema is [(name, logical type name)]; errors raise EncodingError
+        with the reference's messages."""
+        ctx = ctx or default_context()
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        names, types, n = Table._csv_schema(schema)
+        st = Status()
+        h = lib.tqp_csv_parse(ctx.h, data, len(data), names, types, n, delimiter.encode(), origin.encode(),
+                              C.byref(st))
+        _check(st, bool(h))
+        return Table(h, ctx)
+
+    @staticmethod
+    def load_csv(path, schema: Sequence[Tuple[str, str]], delimiter: str = ",", ctx=None) -> "Table":
+        """tensql::load_csv (columnar.cpp:521-527): pinned read, one copy to HBM."""
+        ctx = ctx or default_context()
+        names, types, n = Table._csv_schema(schema)
+        st = Status()
+        h = lib.tqp_csv_load(ctx.h, str(path).encode(), names, types, n, delimiter.encode(), C.byref(st))
         _check(st, bool(h))
         return Table(h, ctx)
 
