@@ -185,6 +185,8 @@ def main():
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-csv", action="store_true")
+    ap.add_argument("--csv-sf", type=float, default=1.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -321,6 +323,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args.ref_sf)
 
+    csv_leg = None
+    if rank == 0 and not args.no_csv:
+        csv_leg = run_csv_leg(tqp, ctx, args.csv_sf)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
@@ -334,11 +340,45 @@ def main():
                                        f"whole per rank, partials all-gathered over NCCL" if world > 1
                                        else "single GPU")},
             "queries": queries, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": launches,
+            "clocks": clocks.summary(), "gpu_launches": launches, "csv_load": csv_leg,
         }
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def run_csv_leg(tqp, ctx, sf):
+    """lineitem as a CSV file -> device table through the
+    loader's public call (Table.load_csv: pinned read, one copy to HBM, device
+    parse), against the reference's own load_csv (columnar.cpp:521-527, one
+    host thread) on the same file. The file is written by the oracle's
+    generator (oracle/_ref/csv_cases lineitem)."""
+    tool = ROOT / "oracle" / "_ref" / "csv_cases"
+    if not tool.exists():
+        return {"skipped": "oracle/_ref/csv_cases not built"}
+    path = Path(f"/tmp/tqp_bench_lineitem_sf{sf:g}.csv")
+    if not path.exists():
+        subprocess.run([str(tool), "lineitem", str(sf), str(path)], check=True)
+    nbytes = path.stat().st_size
+    schema = [("l_orderkey", "int64"), ("l_partkey", "int64"), ("l_quantity", "int64"),
+              ("l_extendedprice", "float64"), ("l_discount", "float64"), ("l_tax", "float64"),
+              ("l_returnflag", "utf8"), ("l_linestatus", "utf8"), ("l_shipdate", "date")]
+    for _ in range(2):
+        t = tqp.Table.load_csv(path, schema, ctx=ctx)
+    times = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        t = tqp.Table.load_csv(path, schema, ctx=ctx)
+        ctx.sync()
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.median(times)
+    rows = t.rows
+    ref = subprocess.run([str(tool), "time", str(path), "1"], capture_output=True, text=True, timeout=600)
+    ref_ms = json.loads(ref.stdout.strip().splitlines()[-1])["ms"] if ref.returncode == 0 else None
+    return {"workload": f"lineitem SF{sf:g} CSV file ({nbytes} B, {rows} rows) -> device table (Table.load_csv)",
+            "ms": ms, "rows_per_s": rows / (ms / 1e3), "gb_per_s": nbytes / (ms / 1e3) / 1e9,
+            "reference_ms": ref_ms, "reference_rows_per_s": rows / (ref_ms / 1e3) if ref_ms else None,
+            "reference": "tensql::load_csv (one host thread), same file"}
 
 
 def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist):

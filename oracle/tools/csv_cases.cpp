@@ -9,7 +9,11 @@
 #include <string>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+
 #include "dump.hpp"
+#include "tpch_tables.hpp"
 
 using namespace tqp_oracle;
 
@@ -149,9 +153,48 @@ void random_cases(int n, uint64_t seed) {
 
 }  // namespace
 
+// lineitem of the shared generator as CSV text (two-decimal money, ISO dates)
+int write_lineitem(double sf, const char* path) {
+  TableSet ts = tpch_tables(sf, 7);
+  const EncodedTable& t = ts.at("lineitem");
+  auto rows = decode_table(t);
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return 1;
+  for (size_t c = 0; c < t.columns().size(); ++c) std::fprintf(f, "%s%s", c ? "," : "", t.columns()[c].name.c_str());
+  std::fputc('\n', f);
+  for (const auto& r : rows) {
+    for (size_t c = 0; c < r.size(); ++c) {
+      if (c) std::fputc(',', f);
+      const LogicalType lt = t.columns()[c].logical;
+      if (lt == LogicalType::Float64) std::fprintf(f, "%.2f", std::get<double>(r[c]));
+      else std::fputs(cell_to_text(r[c], lt).c_str(), f);
+    }
+    std::fputc('\n', f);
+  }
+  std::fclose(f);
+  return 0;
+}
+
+// the reference's load_csv on a file (CPU baseline of the loader)
+int time_reference(const char* path, int reps) {
+  double best = 1e30;
+  int64_t rows = 0;
+  for (int i = 0; i < reps; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    EncodedTable t = load_csv(path, lineitem_schema(), ',');
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    best = ms < best ? ms : best;
+    rows = t.row_count();
+  }
+  std::printf("{\"rows\": %lld, \"ms\": %.3f}\n", static_cast<long long>(rows), best);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 4 && std::string(argv[1]) == "lineitem") return write_lineitem(std::stod(argv[2]), argv[3]);
+  if (argc >= 3 && std::string(argv[1]) == "time") return time_reference(argv[2], argc > 3 ? std::stoi(argv[3]) : 1);
   if (argc < 2) {
-    std::cerr << "usage: csv_cases OUT.json\n";
+    std::cerr << "usage: csv_cases OUT.json | csv_cases lineitem SF OUT.csv | csv_cases time FILE.csv [reps]\n";
     return 2;
   }
   fixed_cases();

@@ -109,6 +109,9 @@ void tqp_shutdown(tqp_ctx* ctx) {
   cudaStreamSynchronize(ctx->c.stream);
   cudaFree(ctx->c.d_err);
   cudaFreeHost(ctx->c.h_err);
+  if (ctx->c.csv_ring) cudaFreeHost(ctx->c.csv_ring);
+  for (auto& e : ctx->c.csv_ring_ev)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kNlThreads) k_nl_write(const unsigned char* __
 }
 
 struct CsvSpec {
-  const unsigned char* d;  // data bytes (after the header line)
+  const unsigned char* d;  // the whole text (header line first), padded to 16 B
   int64_t n;
   const long long* nl;     // newline positions
   int64_t n_nl;
@@ -125,9 +125,11 @@ struct CsvSpec {
   long long slow_cap;
 };
 
-__device__ __forceinline__ void line_span(const CsvSpec& s, int64_t i, int64_t& a, int64_t& b) {
-  a = i == 0 ? 0 : s.nl[i - 1] + 1;
-  b = i < s.n_nl ? s.nl[i] : s.n;
+// data line r: after newline r (newline 0 ends the header), up to the next
+// newline or the end of the text; one trailing '\r' stripped
+__device__ __forceinline__ void line_span(const CsvSpec& s, int64_t r, int64_t& a, int64_t& b) {
+  a = s.nl[r] + 1;
+  b = r + 1 < s.n_nl ? s.nl[r + 1] : s.n;
   if (b > a && s.d[b - 1] == '\r') --b;  // "\r\n" line ends
 }
 
@@ -263,26 +265,54 @@ std::string field_error(int type, const std::string& f) {
 
 }  // namespace
 
-Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vector<std::pair<std::string, int>>& schema,
-                char delimiter, const std::string& origin) {
+namespace {
+
+std::vector<std::string> split_line(const std::string& line, char delimiter) {
+  std::vector<std::string> f;
+  for (size_t st = 0;;) {
+    const size_t d = line.find(delimiter, st);
+    if (d == std::string::npos) {
+      f.push_back(line.substr(st));
+      break;
+    }
+    f.push_back(line.substr(st, d - st));
+    st = d + 1;
+  }
+  return f;
+}
+
+std::string device_bytes(Ctx& c, const unsigned char* d, int64_t a, int64_t b) {
+  std::string out(static_cast<size_t>(std::max<int64_t>(0, b - a)), '\0');
+  if (b > a) {
+    TQP_CUDA(cudaMemcpyAsync(&out[0], d + a, static_cast<size_t>(b - a), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  }
+  return out;
+}
+
+long long device_word(Ctx& c, const long long* p) {
+  long long v = 0;
+  TQP_CUDA(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  return v;
+}
+
+}  // namespace
+
+// `d`: the whole CSV text in HBM (16-byte aligned, 32 zero bytes of padding
+// after `len`); `head`: the first `head_len` bytes of it on the host (at
+// least the header line, or all of a text without a newline).
+Table csv_parse_device(Ctx& c, const unsigned char* d, int64_t len, const unsigned char* head, int64_t head_len,
+                       const std::vector<std::pair<std::string, int>>& schema, char delimiter, const std::string& origin) {
   if (schema.empty()) enc_fail(origin + ": schema has no columns");
   if (schema.size() > 64) throw Error(TQP_ERR_ARG, "csv: more than 64 columns");
   // ---- header (host: one line)
   if (len <= 0) enc_fail(origin + ": missing header line");
-  const void* nlp = std::memchr(text, '\n', static_cast<size_t>(len));
-  const int64_t hend = nlp ? static_cast<const unsigned char*>(nlp) - text : len;
-  std::string header(reinterpret_cast<const char*>(text), static_cast<size_t>(hend));
+  const void* nlp = std::memchr(head, '\n', static_cast<size_t>(head_len));
+  const int64_t hend = nlp ? static_cast<const unsigned char*>(nlp) - head : head_len;
+  std::string header(reinterpret_cast<const char*>(head), static_cast<size_t>(hend));
   if (!header.empty() && header.back() == '\r') header.pop_back();
-  std::vector<std::string> hf;
-  for (size_t st = 0;;) {
-    const size_t d = header.find(delimiter, st);
-    if (d == std::string::npos) {
-      hf.push_back(header.substr(st));
-      break;
-    }
-    hf.push_back(header.substr(st, d - st));
-    st = d + 1;
-  }
+  const std::vector<std::string> hf = split_line(header, delimiter);
   const int ncols = static_cast<int>(schema.size());
   if (static_cast<int>(hf.size()) != ncols)
     enc_fail(origin + ":1: header has " + std::to_string(hf.size()) + " columns, schema has " + std::to_string(ncols));
@@ -291,20 +321,13 @@ Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vecto
       enc_fail(origin + ":1: header column " + std::to_string(i + 1) + " is '" + hf[i] + "', schema expects '" +
                schema[i].first + "'");
 
-  // ---- data bytes to HBM
-  const int64_t dstart = nlp ? hend + 1 : len;
-  const int64_t dn = len - dstart;
-  auto dbuf = c.alloc_bytes(static_cast<size_t>(dn) + 32);
-  unsigned char* d = static_cast<unsigned char*>(dbuf->ptr);
-  if (dn) TQP_CUDA(cudaMemcpyAsync(d, text + dstart, static_cast<size_t>(dn), cudaMemcpyHostToDevice, c.stream));
-  TQP_CUDA(cudaMemsetAsync(d + dn, 0, 32, c.stream));
-
-  // ---- newline positions
-  const int64_t nchunks = dn ? (dn + kNlChunk - 1) / kNlChunk : 0;
+  // ---- newline positions over the whole text (newline 0 ends the header)
+  const int64_t dn = len;
+  const int64_t nchunks = (dn + kNlChunk - 1) / kNlChunk;
   Tensor counts = c.alloc(TQP_I64, std::max<int64_t>(1, nchunks), 1);
   int64_t n_nl = 0;
   Tensor pos = c.alloc(TQP_I64, 1, 1);
-  if (nchunks) {
+  if (nlp) {
     k_nl_count<<<static_cast<unsigned>(nchunks), kNlThreads, 0, c.stream>>>(d, dn, counts.ptr<long long>());
     c.count_launch();
     Tensor cc = counts;
@@ -316,30 +339,26 @@ Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vecto
     c.sync();
     n_nl = last[0] + last[1];
     pos = c.alloc(TQP_I64, std::max<int64_t>(1, n_nl), 1);
-    if (n_nl) {
-      k_nl_write<<<static_cast<unsigned>(nchunks), kNlThreads, 0, c.stream>>>(d, dn, offs.ptr<long long>(),
-                                                                              pos.ptr<long long>());
-      c.count_launch();
+    k_nl_write<<<static_cast<unsigned>(nchunks), kNlThreads, 0, c.stream>>>(d, dn, offs.ptr<long long>(),
+                                                                            pos.ptr<long long>());
+    c.count_launch();
+  }
+  // data lines: one after each newline, except after a final newline at the
+  // end of the text; the last one is dropped when it is empty ("trailing
+  // newline", columnar.cpp:504)
+  int64_t rows = 0;
+  if (n_nl) {
+    const long long lastnl = device_word(c, pos.ptr<long long>() + n_nl - 1);
+    rows = n_nl - 1 + (dn > lastnl + 1 ? 1 : 0);
+    if (rows) {
+      const long long a = device_word(c, pos.ptr<long long>() + rows - 1) + 1;
+      const long long b = rows < n_nl ? device_word(c, pos.ptr<long long>() + rows) : dn;
+      const std::string tail = device_bytes(c, d, std::max<long long>(a, b - 1), b);
+      int64_t sl = b - a;
+      if (sl > 0 && tail.back() == '\r') --sl;
+      if (sl == 0) --rows;
     }
   }
-  // lines: n_nl terminated ones plus an unterminated tail; the last line is
-  // dropped when it is empty ("trailing newline", columnar.cpp:504). Its
-  // extent is found on the host text (one memrchr).
-  const unsigned char* hd = text + dstart;
-  int64_t nlines = n_nl + ((dn > 0 && hd[dn - 1] != '\n') ? 1 : 0);
-  if (nlines) {
-    const int64_t end = hd[dn - 1] == '\n' ? dn - 1 : dn;
-    int64_t start = 0;
-    for (int64_t i = end - 1; i >= 0; --i)
-      if (hd[i] == '\n') {
-        start = i + 1;
-        break;
-      }
-    int64_t sl = end - start;
-    if (sl > 0 && hd[end - 1] == '\r') --sl;
-    if (sl == 0) --nlines;
-  }
-  const int64_t rows = nlines;
 
   // ---- parse
   CsvSpec s{};
@@ -387,23 +406,12 @@ Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vecto
   if (hdr[0] != ~0ULL) {
     const int64_t r = static_cast<int64_t>(hdr[0] / (ncols + 1));
     const int field = static_cast<int>(hdr[0] % (ncols + 1)) - 1;
-    long long pr[2] = {-1, dn};
-    if (r >= 1) TQP_CUDA(cudaMemcpyAsync(&pr[0], pos.ptr<long long>() + r - 1, 8, cudaMemcpyDeviceToHost, c.stream));
-    if (r < n_nl) TQP_CUDA(cudaMemcpyAsync(&pr[1], pos.ptr<long long>() + r, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    std::string line(reinterpret_cast<const char*>(text + dstart + pr[0] + 1), static_cast<size_t>(pr[1] - pr[0] - 1));
+    const long long a = device_word(c, pos.ptr<long long>() + r) + 1;
+    const long long b = r + 1 < n_nl ? device_word(c, pos.ptr<long long>() + r + 1) : dn;
+    std::string line = device_bytes(c, d, a, b);
     if (!line.empty() && line.back() == '\r') line.pop_back();
     const std::string where = origin + ":" + std::to_string(r + 2) + ": ";
-    std::vector<std::string> f;
-    for (size_t st = 0;;) {
-      const size_t dd = line.find(delimiter, st);
-      if (dd == std::string::npos) {
-        f.push_back(line.substr(st));
-        break;
-      }
-      f.push_back(line.substr(st, dd - st));
-      st = dd + 1;
-    }
+    const std::vector<std::string> f = split_line(line, delimiter);
     if (field < 0) enc_fail(where + "expected " + std::to_string(ncols) + " fields, got " + std::to_string(f.size()));
     enc_fail(where + "column '" + schema[field].first + "' (field " + std::to_string(field + 1) +
              "): " + field_error(schema[field].second, f[field]));
@@ -427,19 +435,51 @@ Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vecto
   return t;
 }
 
+Table csv_parse(Ctx& c, const unsigned char* text, int64_t len, const std::vector<std::pair<std::string, int>>& schema,
+                char delimiter, const std::string& origin) {
+  auto dbuf = c.alloc_bytes(static_cast<size_t>(std::max<int64_t>(0, len)) + 32);
+  unsigned char* d = static_cast<unsigned char*>(dbuf->ptr);
+  if (len > 0) TQP_CUDA(cudaMemcpyAsync(d, text, static_cast<size_t>(len), cudaMemcpyHostToDevice, c.stream));
+  TQP_CUDA(cudaMemsetAsync(d + std::max<int64_t>(0, len), 0, 32, c.stream));
+  return csv_parse_device(c, d, len, text, len, schema, delimiter, origin);
+}
+
+// load_csv: the file streams through a small ring of pinned buffers straight
+// into one device buffer (reads overlap the copies; no pinned allocation of
+// the file's size), then the device parse
 Table csv_load(Ctx& c, const std::string& path, const std::vector<std::pair<std::string, int>>& schema, char delimiter) {
   std::ifstream in(path, std::ios::binary | std::ios::ate);
   if (!in) enc_fail("csv: cannot open '" + path + "'");
   const int64_t n = static_cast<int64_t>(in.tellg());
   in.seekg(0);
-  unsigned char* buf = nullptr;  // pinned: one DMA straight to HBM
-  TQP_CUDA(cudaMallocHost(&buf, static_cast<size_t>(std::max<int64_t>(1, n))));
-  struct Free {
-    unsigned char* p;
-    ~Free() { cudaFreeHost(p); }
-  } guard{buf};
-  if (n && !in.read(reinterpret_cast<char*>(buf), n)) enc_fail("csv: cannot read '" + path + "'");
-  return csv_parse(c, buf, n, schema, delimiter, path);
+  constexpr int kRing = 4;
+  constexpr int64_t kChunk = 16 << 20;
+  if (!c.csv_ring) {
+    TQP_CUDA(cudaMallocHost(&c.csv_ring, static_cast<size_t>(kRing * kChunk)));
+    for (int i = 0; i < kRing; ++i) TQP_CUDA(cudaEventCreateWithFlags(&c.csv_ring_ev[i], cudaEventDisableTiming));
+  }
+  auto dbuf = c.alloc_bytes(static_cast<size_t>(n) + 32);
+  unsigned char* d = static_cast<unsigned char*>(dbuf->ptr);
+  std::string head;
+  bool have_nl = false;
+  for (int64_t off = 0, k = 0; off < n; off += kChunk, ++k) {
+    const int slot = static_cast<int>(k % kRing);
+    unsigned char* buf = c.csv_ring + slot * kChunk;
+    if (k >= kRing) TQP_CUDA(cudaEventSynchronize(c.csv_ring_ev[slot]));  // its previous copy is done
+    const int64_t m = std::min<int64_t>(kChunk, n - off);
+    if (!in.read(reinterpret_cast<char*>(buf), m)) enc_fail("csv: cannot read '" + path + "'");
+    if (!have_nl) {  // the header line stays on the host
+      const void* p = std::memchr(buf, '\n', static_cast<size_t>(m));
+      const int64_t take = p ? static_cast<const unsigned char*>(p) - buf + 1 : m;
+      head.append(reinterpret_cast<const char*>(buf), static_cast<size_t>(take));
+      have_nl = p != nullptr;
+    }
+    TQP_CUDA(cudaMemcpyAsync(d + off, buf, static_cast<size_t>(m), cudaMemcpyHostToDevice, c.stream));
+    TQP_CUDA(cudaEventRecord(c.csv_ring_ev[slot], c.stream));
+  }
+  TQP_CUDA(cudaMemsetAsync(d + n, 0, 32, c.stream));
+  return csv_parse_device(c, d, n, reinterpret_cast<const unsigned char*>(head.data()),
+                          static_cast<int64_t>(head.size()), schema, delimiter, path);
 }
 
 }  // namespace tqp

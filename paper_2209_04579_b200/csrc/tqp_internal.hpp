@@ -93,6 +93,9 @@ struct Ctx {
   // the executor's timings
   bool time_kernels = false;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> kernel_events;
+  // CSV file loader: pinned ring of upload buffers (csv.cu), kept for reuse
+  unsigned char* csv_ring = nullptr;
+  cudaEvent_t csv_ring_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // timing events are recycled (creating one per launch costs host time
   // between dependent launches)
   std::vector<cudaEvent_t> event_pool;
