@@ -1874,6 +1874,19 @@ std::string dlit(double d) {
   return "__longlong_as_double((long long)" + hex64(u) + ")";
 }
 
+// Small-group scans first run with 4 group slots per CTA: the per-thread
+// shared-memory cells then take half the space, which goes to one more
+// staging buffer (the scan is bound by the bytes each SM keeps in flight:
+// 3 -> 4 stages of 43 KB). A CTA meeting a fifth key flags err[1] and the
+// unit reruns with the 8-slot kernel. Per-thread row order is unchanged, so
+// both give the same bits.
+bool small_wide_wanted() {
+  const char* e = std::getenv("TQP_SMALL_WIDE");
+  return !(e && (e[0] == '0' || e[0] == 'n'));
+}
+constexpr int kWideSlots = 4;
+constexpr int kWideCW = 8;
+
 bool jit_wanted(long long rows) {
   const char* e = std::getenv("TQP_JIT");
   if (e && (e[0] == '0' || e[0] == 'n')) return false;
@@ -1881,7 +1894,8 @@ bool jit_wanted(long long rows) {
   return rows >= (1LL << 20);  // below this the NVRTC compile is not worth it
 }
 
-std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<bool>& probe_bitmap) {
+std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<bool>& probe_bitmap,
+                         int slots = kGroups) {
   const ProbeSpec& s = ts.p;
   std::ostringstream o;
   unsigned int_mask = 0;
@@ -1889,7 +1903,7 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
     if (s.acc[a].is_int) int_mask |= 1u << a;
   o << "#include \"fz_layout.cuh\"\n"
     << "#define Q_MODE " << mode << "\n#define Q_NA " << s.nacc << "\n#define Q_ROWS " << ts.rows << "\n#define Q_CW "
-    << cw << "\n#define Q_INT_MASK " << int_mask << "u\n"
+    << cw << "\n#define Q_INT_MASK " << int_mask << "u\n#define Q_SLOTS " << slots << "\n"
     << "namespace tqp { namespace fz {\n"
     << "__device__ __forceinline__ unsigned long long q_u64(const unsigned char* st, unsigned off, int ri) {\n"
     << "  return *reinterpret_cast<const unsigned long long*>(st + off + ri * 8); }\n"
@@ -2106,7 +2120,9 @@ struct Runner {
   }
 
   // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
-  bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po) const {
+  // narrow: the 8-slot small-group kernel only (after a 4-slot overflow)
+  bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
+           bool narrow = false) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     auto err_buf = c.alloc_bytes(32);
@@ -2373,6 +2389,12 @@ struct Runner {
     ts.aux_bytes = static_cast<int>(P.mode == MODE_SMALL    ? aux_bytes_for<MODE_SMALL>(ps.nacc)
                                     : P.mode == MODE_SCALAR ? aux_bytes_for<MODE_SCALAR>(ps.nacc)
                                                             : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
+    const bool wide = P.mode == MODE_SMALL && !narrow && jit_wanted(ps.n) && small_wide_wanted();
+    int small_threads = TileShape<MODE_SMALL>::THREADS;
+    if (wide) {  // per-thread cells for kWideSlots slots, kWideCW consumer warps
+      ts.aux_bytes = static_cast<int>(sizeof(unsigned long long) * kWideSlots * (ps.nacc + 1) * kWideCW * 32);
+      small_threads = kWideCW * 32 + 32;
+    }
     for (int i = 0; i < ts.ncols; ++i) {
       ts.col_off[i] = ts.stage_bytes;
       ts.stage_bytes += (ts.rows * ts.col_w[i] + 127) & ~127;  // 128 B aligned columns
@@ -2394,8 +2416,8 @@ struct Runner {
         bm.push_back(!B.terms.empty() || !B.children.empty());
       }
       ts.p = ps;
-      const int cw = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
-      kfn = jit_kernel(gen_pipeline(ts, P.mode, cw, bm), "q_tile");
+      const int cw = wide ? kWideCW : P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
+      kfn = jit_kernel(gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups), "q_tile");
     }
     TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
@@ -2455,7 +2477,7 @@ struct Runner {
       nrows = 1;
     } else if (P.mode == MODE_SMALL) {
       ps.part = part_buf(grid, kSmallPartWords);
-      launch_tile(kfn, TileShape<MODE_SMALL>::THREADS, grid);
+      launch_tile(kfn, small_threads, grid);
       if (!po) nrows = final_small(c, reinterpret_cast<const SmallPart*>(ps.part), grid, fs, err, outs);
     } else {
       // MODE_BUILDGRP
@@ -2508,6 +2530,7 @@ struct Runner {
     TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedRead, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
+    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true);  // a fifth key in a CTA
     if (herr[0]) {  // preconditions violated: exact per-instruction path
       if (po) *po = Partial{};
       return false;

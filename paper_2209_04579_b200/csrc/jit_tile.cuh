@@ -18,11 +18,14 @@ namespace fz {
 
 constexpr int Q_CT = Q_CW * 32;
 constexpr int Q_R = Q_ROWS / Q_CT;
+#ifndef Q_SLOTS
+#define Q_SLOTS kGroups  // small-group slots per CTA (<= kGroups)
+#endif
 __device__ __forceinline__ bool q_is_int(int a) { return (Q_INT_MASK >> a) & 1; }
 
 extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec t) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ unsigned long long s_wred[Q_MODE == MODE_SMALL ? kGroups : 1][Q_NA + 1][Q_CW];
+  __shared__ unsigned long long s_wred[Q_MODE == MODE_SMALL ? Q_SLOTS : 1][Q_NA + 1][Q_CW];
   __shared__ unsigned int s_codes[kGroups];
   __shared__ int s_ncodes;
   __shared__ int s_overflow;
@@ -89,20 +92,20 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       } else if constexpr (Q_MODE == MODE_SMALL) {
         // slot of each row's code among the CTA's claimed codes
         const int ncl = *reinterpret_cast<volatile int*>(&s_ncodes);
-        unsigned cr[kGroups];
+        unsigned cr[Q_SLOTS];
 #pragma unroll
-        for (int j = 0; j < kGroups; ++j) cr[j] = s_codes[j];
+        for (int j = 0; j < Q_SLOTS; ++j) cr[j] = s_codes[j];
         int slot[Q_R];
         bool miss = false;
 #pragma unroll
         for (int k = 0; k < Q_R; ++k) {
           slot[k] = -1;
-          if (ncl <= 4) {
+          if (Q_SLOTS <= 4 || ncl <= 4) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) slot[k] = cr[j] == code[k] ? j : slot[k];
+            for (int j = 0; j < (Q_SLOTS < 4 ? Q_SLOTS : 4); ++j) slot[k] = cr[j] == code[k] ? j : slot[k];
           } else {
 #pragma unroll
-            for (int j = 0; j < kGroups; ++j) slot[k] = cr[j] == code[k] ? j : slot[k];
+            for (int j = 0; j < Q_SLOTS; ++j) slot[k] = cr[j] == code[k] ? j : slot[k];
           }
           miss = miss || (pass[k] && slot[k] < 0);
         }
@@ -111,7 +114,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
 #pragma unroll
           for (int k = 0; k < Q_R; ++k) {
             if (!pass[k] || slot[k] >= 0) continue;
-            for (int j = 0; j < kGroups; ++j) {
+            for (int j = 0; j < Q_SLOTS; ++j) {
               const unsigned prev = atomicCAS(&s_codes[j], 0xffffffffu, code[k]);
               if (prev == 0xffffffffu || prev == code[k]) {
                 slot[k] = j;
@@ -163,7 +166,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
     }
     if constexpr (Q_MODE == MODE_SMALL) {
-      for (int gg = 0; gg < kGroups; ++gg) {
+      for (int gg = 0; gg < Q_SLOTS; ++gg) {
 #pragma unroll
         for (int a = 0; a <= Q_NA; ++a) {
           unsigned long long x = s_cell[(gg * (Q_NA + 1) + a) * Q_CT + ct];
@@ -202,9 +205,16 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       out[kMaxAcc] = c;
     }
   } else if constexpr (Q_MODE == MODE_SMALL) {
-    if (s_overflow && threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+    // slot overflow: the 8-slot kernel reruns the scan (err[1]) or, with
+    // every slot in use, the exact per-instruction path does (err[0])
+    if (s_overflow && threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(s.err) + (Q_SLOTS < kGroups ? 1 : 0), 1ULL);
     SmallPart* out = reinterpret_cast<SmallPart*>(s.part) + blockIdx.x;
     for (int sl = threadIdx.x; sl < kGroups; sl += blockDim.x) {
+      if (sl >= Q_SLOTS) {
+        out->codes[sl] = 0xffffffffu;
+        out->cnt[sl] = 0;
+        continue;
+      }
       out->codes[sl] = s_codes[sl];
       unsigned long long c = 0;
       for (int w = 0; w < Q_CW; ++w) c += s_wred[sl][Q_NA][w];

@@ -17,9 +17,11 @@ PLANS = ROOT / "paper_2209_04579_b200" / "plans"
 QUERIES = ("q1", "q6", "q14", "q3")
 
 
-def run(tqp, q, tables, jit):
+def run(tqp, q, tables, jit, wide=False):
     old = os.environ.get("TQP_JIT")
+    old_w = os.environ.get("TQP_SMALL_WIDE")
     os.environ["TQP_JIT"] = "1" if jit else "0"
+    os.environ["TQP_SMALL_WIDE"] = "1" if wide else "0"
     try:
         ex = tqp.Executor(json.loads((PLANS / f"{q}.opplan.json").read_text()))
         ex.set_timing(True)
@@ -31,6 +33,10 @@ def run(tqp, q, tables, jit):
             del os.environ["TQP_JIT"]
         else:
             os.environ["TQP_JIT"] = old
+        if old_w is None:
+            del os.environ["TQP_SMALL_WIDE"]
+        else:
+            os.environ["TQP_SMALL_WIDE"] = old_w
 
 
 @pytest.mark.parametrize("q", QUERIES)
@@ -81,3 +87,38 @@ def test_jit_golden_plans(ctx, golden_plans):
             del os.environ["TQP_JIT"]
         else:
             os.environ["TQP_JIT"] = old
+
+
+def _q1_close(got, want):
+    assert [(n, t) for n, t, _ in got] == [(n, t) for n, t, _ in want]
+    for (n, t, g), (_, _, w) in zip(got, want):
+        np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=n)
+
+
+def test_small_group_wide_kernel(ctx):
+    """The 4-slot small-group kernel (the default for large Q1-shaped scans)
+    against the 8-slot generic kernel: bit-identical (same per-thread row
+    order); with six keys per CTA it flags the overflow and the unit reruns
+    on the 8-slot kernel."""
+    from paper_2209_04579_b200 import tqp
+    tables = {"lineitem": tqp.Table.generate("lineitem", 0.05, 7)}
+    wide, kw = run(tqp, "q1", tables, True, wide=True)
+    generic, _ = run(tqp, "q1", tables, False)
+    assert any(k.startswith("kernel:q_tile") for k in kw)
+    _q1_close(wide, generic)
+    # six (returnflag, linestatus) keys: more than the wide kernel's 4 slots
+    host = tables["lineitem"].to_numpy()
+    rng = np.random.default_rng(3)
+    flags = np.array([ord(c) for c in "ABC"], dtype=np.int32)[rng.integers(0, 3, host["l_returnflag"].shape[0])]
+    cols = []
+    for name, lt in tables["lineitem"].columns():
+        a = host[name]
+        if name == "l_returnflag":
+            a = flags.reshape(-1, 1).astype(a.dtype)
+        cols.append((name, lt, a))
+    six = {"lineitem": tqp.Table.from_columns(cols)}
+    wide6, kw6 = run(tqp, "q1", six, True, wide=True)
+    generic6, _ = run(tqp, "q1", six, False)
+    assert len(wide6[0][2]) == 6
+    assert any(k.startswith("kernel:q_tile") for k in kw6)
+    _q1_close(wide6, generic6)
