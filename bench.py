@@ -199,11 +199,21 @@ def main():
         return
 
     import torch
+    # TQP_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo exchange - a
+    # functional check of the N-rank flow on a one-GPU box (not a measurement)
+    share = os.environ.get("TQP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
+    red_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+            red_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     from paper_2209_04579_b200 import tqp
     ctx = tqp.Context(local_rank)
@@ -219,7 +229,7 @@ def main():
     L, O, P, Cn = (tables[n].rows for n in ("lineitem", "orders", "part", "customer"))
     L_total = L
     if dist:
-        t = torch.tensor([L], device="cuda", dtype=torch.int64)
+        t = torch.tensor([L], device=red_dev, dtype=torch.int64)
         dist.all_reduce(t)
         L_total = int(t.item())
     execs = {}
@@ -272,7 +282,7 @@ def main():
     launches = ctx.launches - launches0
     total_ms = start.elapsed_time(end)
     if dist:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -317,7 +327,7 @@ def main():
     # e2e: host (pinned) columns -> device -> four queries -> result to host
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist)
+        e2e = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -381,7 +391,7 @@ def run_csv_leg(tqp, ctx, sf):
             "reference": "tensql::load_csv (one host thread), same file"}
 
 
-def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist):
+def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev="cuda"):
     """Same suite through the public C ABI with HOST inputs: every step
     uploads the columns from pinned host memory, runs the queries and reads
     the results back; all inside the timed region."""
@@ -437,7 +447,7 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist):
     wall_ms = (time.perf_counter() - t0) * 1e3
     ms = max(start.elapsed_time(end), wall_ms) / steps
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return {"value": len(QUERIES) * L_total / (ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,

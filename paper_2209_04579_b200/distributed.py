@@ -86,6 +86,8 @@ def execute_sharded(executor, tables: Mapping, group=None):
         if err is not None:
             raise err
         raise
+    if parts and not parts[0].is_cuda and hasattr(executor, "ctx") and torch.cuda.is_available():
+        parts = [p.cuda() for p in parts]  # a gloo exchange: the device executor merges device words
     if parts and parts[0].is_cuda:
         torch.cuda.current_stream().synchronize()  # NCCL done before the library stream reads
     del part
