@@ -1359,7 +1359,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
         // limb sums are exact below kLimbMaxRows rows per group
-        if (s.acc_words == kLimbWords && gc[u] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+        if (s.acc_words == kLimbWords && gc[u] >= static_cast<unsigned long long>(kLimbMaxRows)) {
+          err[0] = 1;
+          err[3] = 15;
+        }
         k0[u] = gc[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
       }
 #pragma unroll
@@ -1463,7 +1466,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
   if (threadIdx.x == 0) {
     if (s_nc > kTopkBlkCand) s_err = 1;
     blk_nc[blockIdx.x] = s_nc < kTopkBlkCand ? s_nc : kTopkBlkCand;
-    if (s_err) err[0] = 1;
+    if (s_err) {
+      err[0] = 1;
+      err[3] = 16;
+    }
     __threadfence();
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
@@ -1531,7 +1537,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
   }
   __syncthreads();
   const int nfc = s_nc < kTopkFinal ? s_nc : kTopkFinal;
-  if (threadIdx.x == 0 && s_nc > kTopkFinal) err[0] = 1;
+  if (threadIdx.x == 0 && s_nc > kTopkFinal) {
+    err[0] = 1;
+    err[3] = 17;
+  }
   // full keys of the final candidates, then the exact order (warp 0)
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(fg + kTopkFinal + 2);
   fk = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(fk) + 7) & ~uintptr_t(7));
@@ -1556,7 +1565,10 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
       for (int j = 0; j < s.f.nouts; ++j) {
         unsigned long long bits;
         bool f;
-        if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
+        if (!group_out_value(s, j, g, bits, f)) {
+          err[0] = 1;
+          err[3] = 18;
+        }
         static_cast<unsigned long long*>(s.f.out_ptr[j])[lane] = bits;
       }
     }
@@ -2001,6 +2013,18 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
 // equality literal without zero bytes compares the leading bytes directly
 // (a zero-padded row shorter than the pattern cannot match a zero-free
 // pattern); anything else calls eval_str.
+// The TMA-staged build kernel (jit_build_tile.cuh) is opt-in: on B200 the
+// Q3 orders build measured 144 us staged vs 148 us unstaged - the build is
+// bound by its scattered inserts and dependent probes, not by reading its
+// columns - so the simpler kernel stays the default.
+bool build_tile_wanted(long long rows) {
+  const char* e = std::getenv("TQP_BUILD_TILE");
+  (void)rows;
+  return e && (e[0] == '1' || e[0] == 'y');
+}
+constexpr int kBuildTileRows = 2048;
+constexpr int kBuildTileCW = 16;
+
 int jit_build_rows() {
   static const int r = [] {
     const char* e = std::getenv("TQP_BUILD_ROWS");  // tuning knob: rows per thread of q_build
@@ -2037,32 +2061,54 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
   return "eval_str(" + sref + ", " + row + ")";
 }
 
-std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap) {
+// staged: the TMA-staged skeleton (jit_build_tile.cuh); key / term / probe-key
+// columns are read from the shared-memory tile at byte offsets `off`
+// (indexed key, terms..., probe keys...), string columns from global memory.
+std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap, bool staged = false,
+                      const std::vector<int>& off = {}, int cw = 16, int tile_rows = 2048) {
   std::ostringstream o;
   auto ld = [&](const Operand& x, const std::string& ptr, const std::string& row) {
     if (x.type == OT_U8) return "static_cast<unsigned long long>(__ldg(static_cast<const uint8_t*>(" + ptr + ") + " + row + "))";
     return "static_cast<unsigned long long>(__ldg(static_cast<const unsigned long long*>(" + ptr + ") + " + row + "))";
   };
+  auto lds = [&](const Operand& x, int byte_off) {
+    if (x.type == OT_U8) return "static_cast<unsigned long long>(stage[" + std::to_string(byte_off) + "u + ri[j]])";
+    return "*reinterpret_cast<const unsigned long long*>(stage + " + std::to_string(byte_off) + "u + ri[j] * 8)";
+  };
   static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
-  o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << jit_build_rows() << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0)
-    << "\n#define B_ZREC " << b.zrec_words << "\n"
-    << "namespace tqp { namespace fz {\n"
-    << "__device__ __forceinline__ void b_rows(const BuildSpec& s, long long r0, int stride, bool* pass, long long* key,\n"
-    << "                                       unsigned* flags) {\n"
-    << "  long long r[B_ROWS];\n"
-    << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) { r[j] = r0 + j * stride; pass[j] = r[j] < s.n; flags[j] = 0u; }\n";
+  o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << (staged ? tile_rows / (cw * 32) : jit_build_rows())
+    << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0) << "\n#define B_ZREC " << b.zrec_words << "\n";
+  if (staged) o << "#define QB_CW " << cw << "\n#define QB_ROWS " << tile_rows << "\n";
+  o << "namespace tqp { namespace fz {\n";
+  if (staged) {
+    o << "__device__ __forceinline__ void qb_rows(const TileSpec& t, const BuildSpec& s, const unsigned char* __restrict__ stage,\n"
+      << "    int ct, long long row0, bool* pass, long long* key, unsigned* flags) {\n"
+      << "  long long r[B_ROWS];\n  int ri[B_ROWS];\n"
+      << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) { ri[j] = j * " << cw * 32
+      << " + ct; r[j] = row0 + ri[j]; pass[j] = r[j] < s.n; flags[j] = 0u; }\n";
+  } else {
+    o << "__device__ __forceinline__ void b_rows(const BuildSpec& s, long long r0, int stride, bool* pass, long long* key,\n"
+      << "                                       unsigned* flags) {\n"
+      << "  long long r[B_ROWS];\n"
+      << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) { r[j] = r0 + j * stride; pass[j] = r[j] < s.n; flags[j] = 0u; }\n";
+  }
   // every independent column load first
   o << "  unsigned long long kv[B_ROWS]";
   for (int t = 0; t < b.nterms; ++t) o << ", tv" << t << "[B_ROWS]";
   for (int p = 0; p < b.nprobes; ++p) o << ", pv" << p << "[B_ROWS]";
   o << ";\n#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n"
-    << "    const long long rr = pass[j] ? r[j] : 0;\n"
-    << "    kv[j] = " << ld(b.key, "s.key.ptr", "rr") << ";\n";
+    << "    const long long rr = pass[j] ? r[j] : 0;\n    (void)rr;\n";
+  int oi = 0;
+  o << "    kv[j] = " << (staged ? lds(b.key, off.at(oi++)) : ld(b.key, "s.key.ptr", "rr")) << ";\n";
   for (int t = 0; t < b.nterms; ++t)
     if (b.terms[t].kind == TK_INT || b.terms[t].kind == TK_F64)
-      o << "    tv" << t << "[j] = " << ld(b.terms[t].x, "s.terms[" + std::to_string(t) + "].x.ptr", "rr") << ";\n";
+      o << "    tv" << t << "[j] = "
+        << (staged ? lds(b.terms[t].x, off.at(oi++)) : ld(b.terms[t].x, "s.terms[" + std::to_string(t) + "].x.ptr", "rr"))
+        << ";\n";
   for (int p = 0; p < b.nprobes; ++p)
-    o << "    pv" << p << "[j] = " << ld(b.probes[p].key, "s.probes[" + std::to_string(p) + "].key.ptr", "rr") << ";\n";
+    o << "    pv" << p << "[j] = "
+      << (staged ? lds(b.probes[p].key, off.at(oi++)) : ld(b.probes[p].key, "s.probes[" + std::to_string(p) + "].key.ptr", "rr"))
+      << ";\n";
   // phase by phase over all B_ROWS rows, so the rows' dependent probe loads
   // (presence word, then entry) are in flight together; the empty asm keeps
   // the compiler from sinking the column loads to their first use
@@ -2108,7 +2154,7 @@ std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap)
         << (1u << f) << "u;\n";
     o << "  }\n";
   }
-  o << "}\n}}  // namespace tqp::fz\n#include \"jit_build.cuh\"\n";
+  o << "}\n}}  // namespace tqp::fz\n#include \"" << (staged ? "jit_build_tile.cuh" : "jit_build.cuh") << "\"\n";
   return o.str();
 }
 
@@ -2239,21 +2285,74 @@ struct Runner {
         // probe, insert) need many warps in flight
         const void* bk = reinterpret_cast<const void*>(&k_build);
         int rows_per_thread = kBuildRows;
-        if (jit_wanted(n)) {
-          rows_per_thread = jit_build_rows();
-          std::vector<bool> bm;
-          for (const auto& ch : B.children) {
-            const BuildDesc& CB = P.builds[ch.build];
-            bm.push_back(!CB.terms.empty() || !CB.children.empty());
+        std::vector<bool> bm;
+        for (const auto& ch : B.children) {
+          const BuildDesc& CB = P.builds[ch.build];
+          bm.push_back(!CB.terms.empty() || !CB.children.empty());
+        }
+        if (jit_wanted(n) && build_tile_wanted(n)) {
+          // large build side: TMA-staged scan of its columns (jit_build_tile.cuh)
+          TileSpec bt;
+          bt.p.n = n;
+          std::vector<int> offs;
+          bool stageable = true;
+          auto stage_col = [&](const Operand& o) {
+            const int w = o.type == OT_U8 ? 1 : 8;
+            if (!o.ptr || reinterpret_cast<uintptr_t>(o.ptr) % 16) stageable = false;
+            for (int i = 0; i < bt.ncols; ++i)
+              if (bt.col_ptr[i] == o.ptr) {
+                offs.push_back(bt.col_off[i]);
+                return;
+              }
+            if (bt.ncols >= kMaxCols) {
+              stageable = false;
+              return;
+            }
+            bt.col_ptr[bt.ncols] = static_cast<const unsigned char*>(o.ptr);
+            bt.col_w[bt.ncols] = w;
+            bt.col_off[bt.ncols] = bt.stage_bytes;
+            offs.push_back(bt.stage_bytes);
+            bt.stage_bytes += (kBuildTileRows * w + 127) & ~127;
+            ++bt.ncols;
+          };
+          stage_col(bs.key);
+          for (int t = 0; t < bs.nterms; ++t)
+            if (bs.terms[t].kind == TK_INT || bs.terms[t].kind == TK_F64) stage_col(bs.terms[t].x);
+          for (int p = 0; p < bs.nprobes; ++p) stage_col(bs.probes[p].key);
+          if (stageable) {
+            bt.rows = kBuildTileRows;
+            const void* kfn = jit_kernel(gen_build(bs, bm, true, offs, kBuildTileCW, kBuildTileRows), "q_build_tile");
+            int optin = 0;
+            TQP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+            cudaFuncAttributes fa{};
+            TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
+            const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024 - 256;
+            bt.stages = static_cast<int>(std::min<size_t>(kMaxStages, budget / bt.stage_bytes));
+            if (bt.stages >= 2) {
+              const size_t smem = 256 + static_cast<size_t>(bt.stages) * bt.stage_bytes;
+              cudaError_t e = c.ensure_smem(kfn, static_cast<int>(smem));
+              if (e != cudaSuccess) throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e));
+              void* targs[] = {&bt, &bs};
+              cudaEvent_t ev = c.kernel_begin();
+              TQP_CUDA(cudaLaunchKernel(kfn, dim3(c.num_sms), dim3(kBuildTileCW * 32 + 32), targs, smem, c.stream));
+              c.kernel_end("q_build_tile", ev);
+              c.count_launch();
+              bk = nullptr;
+            }
           }
+        }
+        if (bk && jit_wanted(n)) {
+          rows_per_thread = jit_build_rows();
           bk = jit_kernel(gen_build(bs, bm), "q_build");
         }
-        void* args[] = {&bs};
-        cudaEvent_t ev = c.kernel_begin();
-        TQP_CUDA(cudaLaunchKernel(bk, dim3(c.grid_for(n, kThreads, rows_per_thread, 1 << 20)), dim3(kThreads), args, 0,
-                                  c.stream));
-        c.kernel_end(bk == reinterpret_cast<const void*>(&k_build) ? "k_build" : "q_build", ev);
-        c.count_launch();
+        if (bk) {
+          void* args[] = {&bs};
+          cudaEvent_t ev = c.kernel_begin();
+          TQP_CUDA(cudaLaunchKernel(bk, dim3(c.grid_for(n, kThreads, rows_per_thread, 1 << 20)), dim3(kThreads), args, 0,
+                                    c.stream));
+          c.kernel_end(bk == reinterpret_cast<const void*>(&k_build) ? "k_build" : "q_build", ev);
+          c.count_launch();
+        }
         k_bitmap_popc<<<c.grid_for(bm_words / 4 + 1, 256, 4, 4), 256, 0, c.stream>>>(bs.bitmap, bm_words, bs.counts);
         k_build_verify<<<1, 1, 0, c.stream>>>(bs.counts, err);
         c.count_launch(2);
@@ -2531,6 +2630,8 @@ struct Runner {
     c.sync();
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
     if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true);  // a fifth key in a CTA
+    if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
+      std::fprintf(stderr, "tqp: fused unit left the fused path (reason %lld)\n", herr[3]);
     if (herr[0]) {  // preconditions violated: exact per-instruction path
       if (po) *po = Partial{};
       return false;

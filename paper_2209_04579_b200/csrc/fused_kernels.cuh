@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(256) k_bitmap_popc(const unsigned* __restrict_
 __global__ void k_build_verify(const unsigned long long* counts, long long* err) {
   unsigned long long ins = 0;
   for (int i = 0; i < kCountSlots; ++i) ins += counts[i];
-  if (ins != counts[kCountSlots]) err[0] = 1;
+  if (ins != counts[kCountSlots]) {
+    err[0] = 1;
+    err[3] = 12;  // reason (TQP_DEBUG_FALLBACK)
+  }
 }
 
 // value of accumulator `ac` for rows k0..k0+N-1 of this thread (row index

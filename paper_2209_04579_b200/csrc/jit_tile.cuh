@@ -152,6 +152,8 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
               qv = static_cast<__int128>(static_cast<long long>(v[k][a]));
             } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k][a])), qv)) {
               atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+      atomicExch(reinterpret_cast<unsigned long long*>(s.err) + 3, 14ULL);
+              atomicExch(reinterpret_cast<unsigned long long*>(s.err) + 3, 13ULL);
               qv = 0;
             }
             atomic_add_limbs(s.gacc + static_cast<long long>(gid[k]) * s.gstride + a * kLimbWords, qv);

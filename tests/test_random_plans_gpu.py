@@ -27,3 +27,17 @@ def test_random_plans_match_reference(seed, plans):
     tail = "\n".join(r.stdout.splitlines()[-40:])
     assert r.returncode == 0, tail + r.stderr[-2000:]
     assert "0 failure(s)" in r.stdout, tail
+
+
+@pytest.mark.parametrize("env", [{"TQP_JIT": "1"}, {"TQP_JIT": "1", "TQP_BUILD_TILE": "1"}])
+def test_random_plans_nvrtc_kernels(env):
+    """The same comparison with every fused unit on NVRTC kernels, and with
+    build sides through the TMA-staged build kernel."""
+    import os
+    if not BIN.exists():
+        pytest.fail(f"{BIN} is not built (make -C oracle)")
+    r = subprocess.run([str(BIN), "--seed", "17", "--plans", "120"], capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, **env))
+    tail = "\n".join(r.stdout.splitlines()[-40:])
+    assert r.returncode == 0, tail + r.stderr[-2000:]
+    assert "0 failure(s)" in r.stdout, tail
