@@ -6,6 +6,8 @@
 
 #include <chrono>
 #include <functional>
+#include <memory>
+#include <mutex>
 #include <optional>
 #include <string>
 #include <vector>
@@ -61,10 +63,21 @@ struct Plan {
   std::vector<InputTable> input_tables;
 };
 
+// Min/max of an int64 column, computed on the device the first time a build
+// side keys on it and kept with the column: table columns are immutable once
+// on the device (the reference never mutates an input), so the
+// range is table metadata like its row count, not a per-query result.
+struct KeyRange {
+  std::mutex mu;
+  bool ready = false;
+  long long mn = 0, mx = 0;
+};
+
 struct Column {
   std::string name;
   int type;  // logical
   Tensor t;
+  std::shared_ptr<KeyRange> range = std::make_shared<KeyRange>();
 };
 
 struct Table {

@@ -9,6 +9,7 @@
 // > 64 groups, fixed-point range, int64 near overflow) hands its steps back
 // to the per-instruction path, which reproduces the reference exactly.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -997,13 +998,17 @@ __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int 
 }
 
 // MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums in CTA
-// order. One warp per (group, accumulator | count) gathers the CTA values into
-// shared memory with independent loads; lane 0 then adds them in CTA order
-// (absent slots contribute +0.0 / 0, which never changes a sum that starts at
-// +0.0), so the result is the sequential CTA-order sum.
+// order. One thread per CTA part inserts its codes and later records the
+// group rank of each of its slots (rank[part][slot]); one warp per (group,
+// accumulator | count) then gathers the CTA values into shared memory - each
+// lane's rank words and values for 4 parts in flight at once - and lane 0
+// adds them in CTA order (absent slots contribute +0.0 / 0, which never
+// changes a sum that starts at +0.0), so the result is the sequential
+// CTA-order sum.
+constexpr int kMergeUnroll = 4;
 __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts, FinalSpec f,
                                                           int nkeys, void* key_ptr0, void* key_ptr1, void* key_ptr2,
-                                                          void* key_ptr3, int* inv /*[nparts][kMerged]*/,
+                                                          void* key_ptr3, int* rank /*[nparts][kGroups]*/,
                                                           long long* ngroups_out, long long* err) {
   __shared__ unsigned s_set[kMerged];
   __shared__ unsigned s_sorted[kMerged];
@@ -1012,21 +1017,31 @@ __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __res
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kMerged; i += blockDim.x) s_set[i] = 0xffffffffu;
   __syncthreads();
-  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
-    unsigned c = parts[i / kGroups].codes[i % kGroups];
-    if (c == 0xffffffffu || parts[i / kGroups].cnt[i % kGroups] == 0) continue;
-    unsigned h = (c * 2654435761u) >> 24;
-    bool placed = false;
-    for (int p = 0; p < kMerged; ++p) {
-      unsigned cur = s_set[h];
-      if (cur == c) { placed = true; break; }
-      if (cur == 0xffffffffu) {
-        unsigned prev = atomicCAS(&s_set[h], 0xffffffffu, c);
-        if (prev == 0xffffffffu || prev == c) { placed = true; break; }
-      }
-      h = (h + 1) & (kMerged - 1);
+  for (int c = threadIdx.x; c < nparts; c += blockDim.x) {
+    unsigned code[kGroups];
+    unsigned long long cnt[kGroups];
+#pragma unroll
+    for (int sl = 0; sl < kGroups; ++sl) {
+      code[sl] = parts[c].codes[sl];
+      cnt[sl] = parts[c].cnt[sl];
     }
-    if (!placed) err[0] = 1;
+#pragma unroll
+    for (int sl = 0; sl < kGroups; ++sl) {
+      const unsigned cd = code[sl];
+      if (cd == 0xffffffffu || cnt[sl] == 0) continue;
+      unsigned h = (cd * 2654435761u) >> 24;
+      bool placed = false;
+      for (int p = 0; p < kMerged; ++p) {
+        unsigned cur = s_set[h];
+        if (cur == cd) { placed = true; break; }
+        if (cur == 0xffffffffu) {
+          unsigned prev = atomicCAS(&s_set[h], 0xffffffffu, cd);
+          if (prev == 0xffffffffu || prev == cd) { placed = true; break; }
+        }
+        h = (h + 1) & (kMerged - 1);
+      }
+      if (!placed) err[0] = 1;
+    }
   }
   __syncthreads();
   // rank sort of the distinct codes (codes are unique)
@@ -1040,19 +1055,23 @@ __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __res
   int n = 0;
   for (int i = 0; i < kMerged; ++i) n += s_set[i] != 0xffffffffu;  // uniform
   if (threadIdx.x == 0) *ngroups_out = n;
-  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kMerged; i += blockDim.x) inv[i] = -1;
   __syncthreads();
-  for (long long i = threadIdx.x; i < static_cast<long long>(nparts) * kGroups; i += blockDim.x) {
-    int c = static_cast<int>(i / kGroups), sl = static_cast<int>(i % kGroups);
-    unsigned code = parts[c].codes[sl];
-    if (code == 0xffffffffu || parts[c].cnt[sl] == 0) continue;
-    int lo = 0, hi = n;
-    while (lo < hi) {
-      int m = (lo + hi) / 2;
-      if (s_sorted[m] < code) lo = m + 1;
-      else hi = m;
+  for (int c = threadIdx.x; c < nparts; c += blockDim.x) {
+#pragma unroll
+    for (int sl = 0; sl < kGroups; ++sl) {
+      const unsigned code = parts[c].codes[sl];
+      int r = -1;
+      if (code != 0xffffffffu && parts[c].cnt[sl] != 0) {
+        int lo = 0, hi = n;
+        while (lo < hi) {
+          int m = (lo + hi) / 2;
+          if (s_sorted[m] < code) lo = m + 1;
+          else hi = m;
+        }
+        r = lo;
+      }
+      rank[static_cast<long long>(c) * kGroups + sl] = r;
     }
-    inv[static_cast<long long>(c) * kMerged + lo] = sl;
   }
   __syncthreads();
   const int per = f.nacc + 1;
@@ -1062,9 +1081,27 @@ __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __res
     unsigned long long tot = 0;
     for (int c0 = 0; c0 < nparts; c0 += kMergeChunk) {
       const int m = nparts - c0 < kMergeChunk ? nparts - c0 : kMergeChunk;
-      for (int i = lane; i < m; i += 32) {
-        const int sl = inv[static_cast<long long>(c0 + i) * kMerged + g];
-        s_v[warp][i] = sl < 0 ? 0ULL : (a == f.nacc ? parts[c0 + i].cnt[sl] : parts[c0 + i].acc[sl][a]);
+      for (int i0 = lane; i0 < m; i0 += 32 * kMergeUnroll) {
+        int sl[kMergeUnroll];
+#pragma unroll
+        for (int u = 0; u < kMergeUnroll; ++u) {
+          const int i = i0 + 32 * u;
+          sl[u] = -1;
+          if (i < m) {
+            const int* rk = rank + static_cast<long long>(c0 + i) * kGroups;
+#pragma unroll
+            for (int q = 0; q < kGroups; ++q) sl[u] = rk[q] == g ? q : sl[u];
+          }
+        }
+        unsigned long long v[kMergeUnroll];
+#pragma unroll
+        for (int u = 0; u < kMergeUnroll; ++u) {
+          const int i = i0 + 32 * u;
+          v[u] = sl[u] < 0 ? 0ULL : (a == f.nacc ? parts[c0 + i].cnt[sl[u]] : parts[c0 + i].acc[sl[u]][a]);
+        }
+#pragma unroll
+        for (int u = 0; u < kMergeUnroll; ++u)
+          if (i0 + 32 * u < m) s_v[warp][i0 + 32 * u] = v[u];
       }
       __syncwarp();
       if (lane == 0)
@@ -1906,7 +1943,20 @@ bool jit_wanted(long long rows) {
   return rows >= (1LL << 20);  // below this the NVRTC compile is not worth it
 }
 
-std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<bool>& probe_bitmap,
+// How a generated fact probe asks a build side. Every build fills its
+// presence bitmap; the table entry is only needed for the LIKE flag bits it
+// carries. PM_TABLE: unfiltered build (every in-range key is a table hit or a
+// zero entry), read the entry; PM_BITMAP_TABLE: filtered build with flags,
+// presence word first, entry for the flags; PM_BITMAP: no flags wanted, the
+// presence bit is the answer and the table is never read.
+enum { PM_TABLE = 0, PM_BITMAP_TABLE = 1, PM_BITMAP = 2 };
+bool build_filtered(const BuildDesc& B) { return !B.terms.empty() || !B.children.empty(); }
+int probe_mode_of(const BuildDesc& B) {
+  if (B.flags.empty()) return PM_BITMAP;
+  return build_filtered(B) ? PM_BITMAP_TABLE : PM_TABLE;
+}
+
+std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<int>& probe_mode,
                          int slots = kGroups) {
   const ProbeSpec& s = ts.p;
   std::ostringstream o;
@@ -1957,13 +2007,18 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
       << "  { const Probe& pr = t.p.probes[" << p << "];\n"
       << "    const long long idx = static_cast<long long>(q_u64(stage, " << off(s.probes[p].key.col) << ", ri)) - pr.kmin;\n"
       << "    bool in = pass && static_cast<unsigned long long>(idx) < static_cast<unsigned long long>(pr.range);\n";
-    if (probe_bitmap[p])
+    if (probe_mode[p] != PM_TABLE)
       o << "    const unsigned w = in ? __ldg(pr.bitmap + (idx >> 5)) : 0u;\n"
         << "    in = in && ((w >> (idx & 31)) & 1u);\n";
-    o << "    const unsigned long long e = in ? __ldg(pr.table + idx) : 0ULL;\n"
-      << "    pass = pass && e != 0ULL;\n"
-      << "    gid" << p << " = static_cast<unsigned>(idx);\n"
-      << "    fl" << p << " = static_cast<unsigned>(e >> 57); }\n";
+    if (probe_mode[p] == PM_BITMAP) {
+      // presence is the whole answer: no flags wanted, the group is the slot
+      o << "    pass = pass && in;\n";
+    } else {
+      o << "    const unsigned long long e = in ? __ldg(pr.table + idx) : 0ULL;\n"
+        << "    pass = pass && e != 0ULL;\n"
+        << "    fl" << p << " = static_cast<unsigned>(e >> 57);\n";
+    }
+    o << "    gid" << p << " = static_cast<unsigned>(idx); }\n";
   }
   if (mode == MODE_BUILDGRP) {
     if (s.group_probe < 0 || s.group_probe >= s.nprobes) throw Error(TQP_ERR_EXEC, "internal: build-group pipeline without a group probe");
@@ -2022,8 +2077,23 @@ bool build_tile_wanted(long long rows) {
   (void)rows;
   return e && (e[0] == '1' || e[0] == 'y');
 }
-constexpr int kBuildTileRows = 2048;
-constexpr int kBuildTileCW = 16;
+// staged build shape: consumer warps and rows per tile (TQP_BUILD_TILE_CW /
+// TQP_BUILD_TILE_ROWS tuning knobs; rows a multiple of 32 x warps)
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+int build_tile_cw() {
+  static const int v = [] { const int x = env_int("TQP_BUILD_TILE_CW", 16); return x >= 4 && x <= 31 ? x : 16; }();
+  return v;
+}
+int build_tile_rows() {
+  static const int v = [] {
+    const int x = env_int("TQP_BUILD_TILE_ROWS", 2048);
+    return x >= 32 * build_tile_cw() && x <= 8192 && x % (32 * build_tile_cw()) == 0 ? x : 32 * build_tile_cw() * 4;
+  }();
+  return v;
+}
 
 int jit_build_rows() {
   static const int r = [] {
@@ -2064,7 +2134,7 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
 // staged: the TMA-staged skeleton (jit_build_tile.cuh); key / term / probe-key
 // columns are read from the shared-memory tile at byte offsets `off`
 // (indexed key, terms..., probe keys...), string columns from global memory.
-std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap, bool staged = false,
+std::string gen_build(const BuildSpec& b, bool staged = false,
                       const std::vector<int>& off = {}, int cw = 16, int tile_rows = 2048) {
   std::ostringstream o;
   auto ld = [&](const Operand& x, const std::string& ptr, const std::string& row) {
@@ -2139,13 +2209,11 @@ std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap,
       << "      idx[j] = static_cast<long long>(pv" << p << "[j]) - " << pr << ".kmin;\n"
       << "      in[j] = pass[j] && static_cast<unsigned long long>(idx[j]) < static_cast<unsigned long long>(" << pr
       << ".range);\n      if (!in[j]) idx[j] = 0;\n    }\n";
-    if (probe_bitmap[p])
-      o << "    unsigned w[B_ROWS];\n"
-        << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) w[j] = __ldg(" << pr << ".bitmap + (idx[j] >> 5));\n"
-        << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) in[j] = in[j] && ((w[j] >> (idx[j] & 31)) & 1u);\n";
-    o << "    unsigned long long e[B_ROWS];\n"
-      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) e[j] = __ldg(" << pr << ".table + idx[j]);\n"
-      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) pass[j] = in[j] && e[j] != 0ULL;\n  }\n";
+    // a child probe only asks whether the key was inserted: the presence bit
+    // (filled by every build) answers it without touching the table
+    o << "    unsigned w[B_ROWS];\n"
+      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) w[j] = __ldg(" << pr << ".bitmap + (idx[j] >> 5));\n"
+      << "#pragma unroll\n    for (int j = 0; j < B_ROWS; ++j) pass[j] = in[j] && ((w[j] >> (idx[j] & 31)) & 1u);\n  }\n";
   }
   if (b.nflags) {
     o << "#pragma unroll\n  for (int j = 0; j < B_ROWS; ++j) {\n";
@@ -2157,6 +2225,25 @@ std::string gen_build(const BuildSpec& b, const std::vector<bool>& probe_bitmap,
   o << "}\n}}  // namespace tqp::fz\n#include \"" << (staged ? "jit_build_tile.cuh" : "jit_build.cuh") << "\"\n";
   return o.str();
 }
+
+// TQP_HOST_PROF=1: wall-clock marks of a fused unit's host side, one stderr
+// line per run (where the host time between the unit's kernels goes)
+struct HostProf {
+  bool on;
+  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> m;
+  HostProf() : on(std::getenv("TQP_HOST_PROF") != nullptr) { mark("start"); }
+  void mark(const char* what) {
+    if (on) m.emplace_back(what, std::chrono::steady_clock::now());
+  }
+  ~HostProf() {
+    if (!on || m.size() < 2) return;
+    std::string o = "[tqp host]";
+    for (size_t i = 1; i < m.size(); ++i)
+      o += std::string(" ") + m[i].first + "=" +
+           std::to_string(std::chrono::duration_cast<std::chrono::microseconds>(m[i].second - m[i - 1].second).count());
+    std::fprintf(stderr, "%s us\n", o.c_str());
+  }
+};
 
 struct Runner {
   PipeDesc P;
@@ -2171,6 +2258,7 @@ struct Runner {
            bool narrow = false) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
+    HostProf hp;
     auto err_buf = c.alloc_bytes(32);
     long long* err = static_cast<long long*>(err_buf->ptr);
     TQP_CUDA(cudaMemsetAsync(err, 0, 32, c.stream));
@@ -2182,35 +2270,58 @@ struct Runner {
     unsigned long long* grec_p = nullptr;
     int grec_words = 0;
     const int nacc_all = static_cast<int>(P.accs.size());
-    // key ranges of every build side: one launch each, one host round trip
+    // key ranges of every build side: cached with the column after the first
+    // query that keys on it; otherwise one launch per column and one host
+    // round trip for all of them
     const size_t nb = P.builds.size();
     std::vector<long long> mm(2 * std::max<size_t>(1, nb));
-    std::shared_ptr<DevBuf> mmb;
-    if (nb) {
-      for (size_t bi = 0; bi < nb; ++bi) {
+    std::vector<size_t> todo;
+    for (size_t bi = 0; bi < nb; ++bi) {
+      const BuildDesc& B = P.builds[bi];
+      const Table* tab = bind_table(tables, B.table);
+      const Column* key = tab ? tab->find(B.key_column) : nullptr;
+      if (!key || key->t.dtype != TQP_I64) return false;
+      std::lock_guard<std::mutex> lk(key->range->mu);
+      if (key->range->ready) {
+        mm[2 * bi] = key->range->mn;
+        mm[2 * bi + 1] = key->range->mx;
+      } else {
         mm[2 * bi] = 0x7fffffffffffffffLL;
         mm[2 * bi + 1] = static_cast<long long>(0x8000000000000000ULL);
+        todo.push_back(bi);
       }
+    }
+    std::shared_ptr<DevBuf> mmb;
+    if (!todo.empty()) {
       mmb = c.alloc_bytes(sizeof(long long) * 2 * nb);
       const bool pinned = nb <= static_cast<size_t>(Ctx::kPinnedMinMaxPairs);
       TQP_CUDA(cudaMemcpyAsync(mmb->ptr, pinned ? c.h_err + Ctx::kPinnedMinMax : mm.data(), sizeof(long long) * 2 * nb,
                                cudaMemcpyHostToDevice, c.stream));
-      for (size_t bi = 0; bi < nb; ++bi) {
+      for (size_t bi : todo) {
         const BuildDesc& B = P.builds[bi];
         const Table* tab = bind_table(tables, B.table);
-        const Column* key = tab ? tab->find(B.key_column) : nullptr;
-        if (!key || key->t.dtype != TQP_I64) return false;
+        const Column* key = tab->find(B.key_column);
         if (tab->rows) {
           k_minmax<<<c.grid_for(tab->rows, 256, 8, 16), 256, 0, c.stream>>>(
               key->t.ptr<long long>(), tab->rows, static_cast<long long*>(mmb->ptr) + 2 * bi);
           c.count_launch();
         }
       }
-      long long* rd = pinned ? c.h_err + Ctx::kPinnedRead : mm.data();
+      std::vector<long long> fresh(2 * nb);
+      long long* rd = pinned ? c.h_err + Ctx::kPinnedRead : fresh.data();
       TQP_CUDA(cudaMemcpyAsync(rd, mmb->ptr, sizeof(long long) * 2 * nb, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
-      if (pinned) std::memcpy(mm.data(), rd, sizeof(long long) * 2 * nb);
+      for (size_t bi : todo) {
+        mm[2 * bi] = rd[2 * bi];
+        mm[2 * bi + 1] = rd[2 * bi + 1];
+        const Column* key = bind_table(tables, P.builds[bi].table)->find(P.builds[bi].key_column);
+        std::lock_guard<std::mutex> lk(key->range->mu);
+        key->range->mn = mm[2 * bi];
+        key->range->mx = mm[2 * bi + 1];
+        key->range->ready = true;
+      }
     }
+    hp.mark("ranges");
     for (size_t bi = 0; bi < P.builds.size(); ++bi) {
       const BuildDesc& B = P.builds[bi];
       const Table* tab = bind_table(tables, B.table);
@@ -2223,7 +2334,11 @@ struct Runner {
       bs.kmin = n ? mm[2 * bi] : 0;
       bs.range = range;
       auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
-      TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
+      // a filtered build's table is only read where its presence bit is set
+      // (probe_lookup and every generated probe check the bitmap first), so
+      // only an unfiltered one, read as `entry != 0`, needs zeroed slots
+      if (!build_filtered(B))
+        TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
       build_range[bi] = range;
@@ -2232,10 +2347,6 @@ struct Runner {
       TQP_CUDA(cudaMemsetAsync(bitmap->ptr, 0, sizeof(unsigned) * bm_words, c.stream));
       keep.push_back(bitmap);
       bs.bitmap = static_cast<unsigned*>(bitmap->ptr);
-      auto counts = c.alloc_bytes(sizeof(unsigned long long) * (kCountSlots + 1));
-      TQP_CUDA(cudaMemsetAsync(counts->ptr, 0, sizeof(unsigned long long) * (kCountSlots + 1), c.stream));
-      keep.push_back(counts);
-      bs.counts = static_cast<unsigned long long*>(counts->ptr);
       bs.err = err;
       bool ok = true;
       bs.key = {key->t.data(), OT_I64, -1};
@@ -2285,11 +2396,6 @@ struct Runner {
         // probe, insert) need many warps in flight
         const void* bk = reinterpret_cast<const void*>(&k_build);
         int rows_per_thread = kBuildRows;
-        std::vector<bool> bm;
-        for (const auto& ch : B.children) {
-          const BuildDesc& CB = P.builds[ch.build];
-          bm.push_back(!CB.terms.empty() || !CB.children.empty());
-        }
         if (jit_wanted(n) && build_tile_wanted(n)) {
           // large build side: TMA-staged scan of its columns (jit_build_tile.cuh)
           TileSpec bt;
@@ -2312,7 +2418,7 @@ struct Runner {
             bt.col_w[bt.ncols] = w;
             bt.col_off[bt.ncols] = bt.stage_bytes;
             offs.push_back(bt.stage_bytes);
-            bt.stage_bytes += (kBuildTileRows * w + 127) & ~127;
+            bt.stage_bytes += (build_tile_rows() * w + 127) & ~127;
             ++bt.ncols;
           };
           stage_col(bs.key);
@@ -2320,8 +2426,8 @@ struct Runner {
             if (bs.terms[t].kind == TK_INT || bs.terms[t].kind == TK_F64) stage_col(bs.terms[t].x);
           for (int p = 0; p < bs.nprobes; ++p) stage_col(bs.probes[p].key);
           if (stageable) {
-            bt.rows = kBuildTileRows;
-            const void* kfn = jit_kernel(gen_build(bs, bm, true, offs, kBuildTileCW, kBuildTileRows), "q_build_tile");
+            bt.rows = build_tile_rows();
+            const void* kfn = jit_kernel(gen_build(bs, true, offs, build_tile_cw(), build_tile_rows()), "q_build_tile");
             int optin = 0;
             TQP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
             cudaFuncAttributes fa{};
@@ -2334,7 +2440,7 @@ struct Runner {
               if (e != cudaSuccess) throw Error(TQP_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e));
               void* targs[] = {&bt, &bs};
               cudaEvent_t ev = c.kernel_begin();
-              TQP_CUDA(cudaLaunchKernel(kfn, dim3(c.num_sms), dim3(kBuildTileCW * 32 + 32), targs, smem, c.stream));
+              TQP_CUDA(cudaLaunchKernel(kfn, dim3(c.num_sms), dim3(build_tile_cw() * 32 + 32), targs, smem, c.stream));
               c.kernel_end("q_build_tile", ev);
               c.count_launch();
               bk = nullptr;
@@ -2343,7 +2449,11 @@ struct Runner {
         }
         if (bk && jit_wanted(n)) {
           rows_per_thread = jit_build_rows();
-          bk = jit_kernel(gen_build(bs, bm), "q_build");
+          hp.mark("bprep");
+          const std::string src = gen_build(bs);
+          hp.mark("bgen");
+          bk = jit_kernel(src, "q_build");
+          hp.mark("bjit");
         }
         if (bk) {
           void* args[] = {&bs};
@@ -2352,10 +2462,8 @@ struct Runner {
                                     c.stream));
           c.kernel_end(bk == reinterpret_cast<const void*>(&k_build) ? "k_build" : "q_build", ev);
           c.count_launch();
+          hp.mark("blaunch");
         }
-        k_bitmap_popc<<<c.grid_for(bm_words / 4 + 1, 256, 4, 4), 256, 0, c.stream>>>(bs.bitmap, bm_words, bs.counts);
-        k_build_verify<<<1, 1, 0, c.stream>>>(bs.counts, err);
-        c.count_launch(2);
       }
       Probe pr;
       pr.kmin = bs.kmin;
@@ -2364,6 +2472,7 @@ struct Runner {
       pr.bitmap = bs.bitmap;
       built[bi] = pr;
     }
+    hp.mark("builds");
     // fact probe
     const Table* fact = bind_table(tables, P.fact_table);
     if (!fact) return false;
@@ -2508,16 +2617,16 @@ struct Runner {
     if (!kfn) return false;
     const bool jit = jit_wanted(ps.n);
     if (jit) {
-      // presence bitmaps only pay off in front of filtered build sides
-      std::vector<bool> bm;
-      for (const auto& pd : P.probes) {
-        const BuildDesc& B = P.builds[pd.build];
-        bm.push_back(!B.terms.empty() || !B.children.empty());
-      }
+      std::vector<int> bm;
+      for (const auto& pd : P.probes) bm.push_back(probe_mode_of(P.builds[pd.build]));
       ts.p = ps;
       const int cw = wide ? kWideCW : P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
-      kfn = jit_kernel(gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups), "q_tile");
+      hp.mark("tprep");
+      const std::string src = gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups);
+      hp.mark("tgen");
+      kfn = jit_kernel(src, "q_tile");
     }
+    hp.mark("gen");
     TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
     if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
@@ -2626,8 +2735,10 @@ struct Runner {
       }
     }
     long long herr[4] = {0, 0, 0, 0};
+    hp.mark("launched");
     TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedRead, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
+    hp.mark("sync");
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
     if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true);  // a fifth key in a CTA
     if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
@@ -2673,7 +2784,7 @@ struct Runner {
 
   long long final_small(Ctx& c, const SmallPart* parts, long long nparts, FinalSpec fs, long long* err,
                         std::vector<Tensor>& outs) const {
-    auto inv = c.alloc_bytes(sizeof(int) * nparts * kMerged);
+    auto rank = c.alloc_bytes(sizeof(int) * nparts * kGroups);
     for (size_t j = 0; j < outs.size(); ++j) {
       outs[j] = c.alloc(out_dtype(P, P.outs[j]), kMerged, 1);
       fs.out_ptr[j] = outs[j].data();
@@ -2682,7 +2793,7 @@ struct Runner {
     for (size_t j = 0; j < P.outs.size(); ++j)
       if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = outs[j].data();
     k_final_small<<<1, kThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
-                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(inv->ptr), err + 2, err);
+                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(rank->ptr), err + 2, err);
     c.count_launch();
     return -1;  // on the device (err[2]); read with the error flag
   }

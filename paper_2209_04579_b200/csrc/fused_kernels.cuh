@@ -68,8 +68,7 @@ __global__ void __launch_bounds__(256) k_minmax(const long long* __restrict__ k,
 
 constexpr int kBuildRows = 4;
 __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
-  const int lane = threadIdx.x & 31;
-  unsigned inserted = 0;
+  unsigned dup = 0;
   // kBuildRows rows per thread (stride blockDim) with every independent column
   // load issued before any dependent work: the per-row chain (filter ->
   // child probe -> insert) is latency-bound otherwise
@@ -115,8 +114,10 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
         }
       }
     }
+    unsigned old[kBuildRows], set[kBuildRows];
 #pragma unroll
     for (int j = 0; j < kBuildRows; ++j) {
+      old[j] = set[j] = 0u;
       if (!__any_sync(0xffffffffu, pass[j])) continue;  // warp-uniform: nothing to insert
       const long long r = base0 + j * blockDim.x + threadIdx.x;
       long long idx = -1;
@@ -132,50 +133,14 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
           if (s.assign_groups)  // the group is the key slot: zero its record
             for (int w = 0; w < s.zrec_words; ++w) s.zrec[idx * s.zrec_words + w] = 0ULL;
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags) << 57);
-          ++inserted;
         }
       }
-      // presence bits: lanes sharing a bitmap word OR-reduce, one atomic per word
-      const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(0xffffffffu, word);
-      const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
-      if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(s.bitmap + word, bits);
+      presence_insert(s.bitmap, idx, old[j], set[j], dup);
     }
+#pragma unroll
+    for (int j = 0; j < kBuildRows; ++j) dup |= old[j] & set[j];
   }
-  // per-warp totals spread over kCountSlots words: no block barrier, no hot address
-  inserted = __reduce_add_sync(0xffffffffu, inserted);
-  if (lane == 0 && inserted)
-    atomicAdd(s.counts + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kCountSlots - 1)),
-              static_cast<unsigned long long>(inserted));
-}
-
-// duplicate-key check of a build: set presence bits must equal rows inserted
-__global__ void __launch_bounds__(256) k_bitmap_popc(const unsigned* __restrict__ bm, long long words,
-                                                     unsigned long long* counts) {
-  __shared__ unsigned s_tot;
-  if (threadIdx.x == 0) s_tot = 0;
-  __syncthreads();
-  unsigned c = 0;
-  const long long nq = words / 4;
-  const uint4* b4 = reinterpret_cast<const uint4*>(bm);
-  for (long long i = gtid(); i < nq; i += gstride()) {
-    const uint4 v = __ldg(b4 + i);
-    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-  }
-  for (long long i = 4 * nq + gtid(); i < words; i += gstride()) c += __popc(__ldg(bm + i));
-  c = __reduce_add_sync(0xffffffffu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_tot, c);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_tot) atomicAdd(counts + kCountSlots, static_cast<unsigned long long>(s_tot));
-}
-
-__global__ void k_build_verify(const unsigned long long* counts, long long* err) {
-  unsigned long long ins = 0;
-  for (int i = 0; i < kCountSlots; ++i) ins += counts[i];
-  if (ins != counts[kCountSlots]) {
-    err[0] = 1;
-    err[3] = 12;  // reason (TQP_DEBUG_FALLBACK)
-  }
+  build_dup_check(dup, s.err);
 }
 
 // value of accumulator `ac` for rows k0..k0+N-1 of this thread (row index

@@ -24,7 +24,6 @@ constexpr int kGroupBits = 3;
 constexpr int kMaxAccSmall = 6;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCountSlots = 64;  // build insert counters
 
 enum OperandType : int { OT_I64 = 0, OT_F64 = 1, OT_U8 = 2 };
 enum TermKind : int { TK_INT = 0, TK_F64 = 1, TK_TRUE = 2, TK_FALSE = 3 };
@@ -160,13 +159,36 @@ struct BuildSpec {
   // the whole key range): zrec_words words per slot (whole sectors)
   unsigned long long* zrec = nullptr;
   int zrec_words = 0;
-  // [0, kCountSlots) rows inserted (per-warp totals, spread), [kCountSlots]
-  // presence bits set (k_build_verify): they differ iff
-  // two inserted rows share a key (a 1:N join, outside the fused contract).
-  // Inserts are plain stores so no warp waits on an atomic's return.
-  unsigned long long* counts = nullptr;
   long long* err = nullptr;
 };
+
+// Presence bits of one insert round of a warp: lanes sharing a bitmap word
+// OR-reduce and the first of them sets the bits. Two inserted rows with one
+// key (a 1:N join, outside the fused contract) show up either inside the
+// round (fewer bits than lanes) or as a bit the word already held; the
+// atomic's old word is returned in `old` (with the bits in `set`) and only
+// checked by build_dup_check after the thread's last round, so no round
+// waits on the atomic's return.
+__device__ __forceinline__ void presence_insert(unsigned* bitmap, long long idx, unsigned& old, unsigned& set,
+                                                unsigned& dup) {
+  const int lane = threadIdx.x & 31;
+  const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, word);
+  const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
+  old = 0u;
+  set = 0u;
+  if (idx >= 0 && lane == __ffs(peers) - 1) {
+    old = atomicOr(bitmap + word, bits);
+    set = bits;
+    dup |= __popc(bits) != __popc(peers) ? 1u : 0u;
+  }
+}
+__device__ __forceinline__ void build_dup_check(unsigned dup, long long* err) {
+  if (__any_sync(0xffffffffu, dup != 0u) && (threadIdx.x & 31) == 0) {
+    atomicExch(reinterpret_cast<unsigned long long*>(err), 1ULL);
+    atomicExch(reinterpret_cast<unsigned long long*>(err) + 3, 12ULL);  // reason (TQP_DEBUG_FALLBACK)
+  }
+}
 
 // ---- operand access ----------------------------------------------------------
 __device__ __forceinline__ long long ld_i64(const void* p, long long r) {

@@ -14,15 +14,14 @@
 // build is its key slot (its state zeroed by the inserted row), the direct-
 // address insert (plain stores; k_build_verify flags a key inserted twice, the
 // 1:N join the fused contract excludes) and the presence bits OR-reduced per
-// warp.
+// warp, a key inserted twice flagged from the bitmap words (presence_insert).
 #pragma once
 
 namespace tqp {
 namespace fz {
 
 extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s) {
-  const int lane = threadIdx.x & 31;
-  unsigned inserted = 0;
+  unsigned dup = 0;
   const long long span = static_cast<long long>(blockDim.x) * B_ROWS;
   for (long long base0 = static_cast<long long>(blockIdx.x) * span; base0 < s.n;
        base0 += static_cast<long long>(gridDim.x) * span) {
@@ -30,8 +29,10 @@ extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s
     long long key[B_ROWS];
     unsigned flags[B_ROWS];
     b_rows(s, base0 + threadIdx.x, blockDim.x, pass, key, flags);
+    unsigned old[B_ROWS], set[B_ROWS];
 #pragma unroll
     for (int j = 0; j < B_ROWS; ++j) {
+      old[j] = set[j] = 0u;
       if (!__any_sync(0xffffffffu, pass[j])) continue;  // warp-uniform: nothing to insert
       const long long r = base0 + j * blockDim.x + threadIdx.x;
       long long idx = -1;
@@ -49,20 +50,14 @@ extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s
           }
 #endif
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[j]) << 57);
-          ++inserted;
         }
       }
-      const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(0xffffffffu, word);
-      const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
-      if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(s.bitmap + word, bits);
+      presence_insert(s.bitmap, idx, old[j], set[j], dup);
     }
+#pragma unroll
+    for (int j = 0; j < B_ROWS; ++j) dup |= old[j] & set[j];
   }
-  // per-warp totals spread over kCountSlots words: no block barrier, no hot address
-  inserted = __reduce_add_sync(0xffffffffu, inserted);
-  if (lane == 0 && inserted)
-    atomicAdd(s.counts + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kCountSlots - 1)),
-              static_cast<unsigned long long>(inserted));
+  build_dup_check(dup, s.err);
 }
 
 }  // namespace fz

@@ -54,7 +54,7 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
     return;
   }
   const int ct = threadIdx.x - 32;
-  unsigned inserted = 0;
+  unsigned dup = 0;
   int st = 0;
   unsigned ph = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -65,8 +65,10 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
     long long key[QB_R];
     unsigned flags[QB_R];
     qb_rows(t, b, stage, ct, row0, pass, key, flags);
+    unsigned old[QB_R], set[QB_R];
 #pragma unroll
     for (int k = 0; k < QB_R; ++k) {
+      old[k] = set[k] = 0u;
       if (!__any_sync(0xffffffffu, pass[k])) continue;  // warp-uniform
       const long long r = row0 + k * QB_CT + ct;
       long long idx = -1;
@@ -85,14 +87,12 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
           }
 #endif
           b.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[k]) << 57);
-          ++inserted;
         }
       }
-      const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(0xffffffffu, word);
-      const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
-      if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(b.bitmap + word, bits);
+      presence_insert(b.bitmap, idx, old[k], set[k], dup);
     }
+#pragma unroll
+    for (int k = 0; k < QB_R; ++k) dup |= old[k] & set[k];
     // release the stage only after every value read from it has been used
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -101,10 +101,7 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
       ph ^= 1u;
     }
   }
-  inserted = __reduce_add_sync(0xffffffffu, inserted);
-  if (lane == 0 && inserted)
-    atomicAdd(b.counts + ((blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) & (kCountSlots - 1)),
-              static_cast<unsigned long long>(inserted));
+  build_dup_check(dup, b.err);
 }
 
 }  // namespace fz
