@@ -96,6 +96,10 @@ const char* tqp_backend_name(tqp_ctx* ctx); /* "b200" (KernelBackend::name)  */
 int tqp_device(tqp_ctx* ctx);
 /* Number of this library's kernels launched on ctx since creation. */
 int64_t tqp_launch_count(tqp_ctx* ctx);
+/* NVRTC the run-time specialised kernels compile with (major * 1000 + minor
+ * 10, e.g. 12090), bound from the build's toolkit whatever else the process
+ * loaded; < 0 when it cannot be loaded. */
+int tqp_jit_nvrtc_version(void);
 
 /* ---- tensors (tensql::Tensor, tensor.hpp:49-122) ------------------------ */
 size_t tqp_dtype_size(int dtype);

@@ -7,6 +7,7 @@
 #include <string>
 
 #include "executor.hpp"
+#include "jit.hpp"
 
 using namespace tqp;
 
@@ -100,6 +101,14 @@ tqp_ctx* tqp_init(int device, tqp_status* st) {
       c.h_err[Ctx::kPinnedMinMax + 2 * i] = 0x7fffffffffffffffLL;
       c.h_err[Ctx::kPinnedMinMax + 2 * i + 1] = static_cast<long long>(0x8000000000000000ULL);
     }
+    for (int i = 0; i < Ctx::kMaxDeferred; ++i) {
+      long long* w = c.h_err + Ctx::kPinnedDeferInit + 4 * i;
+      w[0] = 0x7fffffffffffffffLL;
+      w[1] = w[2] = w[3] = 0;
+    }
+    TQP_CUDA(cudaMalloc(&c.d_defer, 4 * sizeof(long long) * Ctx::kMaxDeferred));
+    TQP_CUDA(cudaMemcpy(c.d_defer, c.h_err + Ctx::kPinnedDeferInit, 4 * sizeof(long long) * Ctx::kMaxDeferred,
+                        cudaMemcpyHostToDevice));
     return h;
   });
 }
@@ -108,6 +117,7 @@ void tqp_shutdown(tqp_ctx* ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
   cudaFree(ctx->c.d_err);
+  cudaFree(ctx->c.d_defer);
   cudaFreeHost(ctx->c.h_err);
   if (ctx->c.csv_ring) cudaFreeHost(ctx->c.csv_ring);
   for (auto& e : ctx->c.csv_ring_ev)
@@ -126,6 +136,13 @@ void* tqp_stream(tqp_ctx* ctx) { return ctx ? ctx->c.stream : nullptr; }
 const char* tqp_backend_name(tqp_ctx*) { return "b200"; }
 int tqp_device(tqp_ctx* ctx) { return ctx ? ctx->c.device : -1; }
 int64_t tqp_launch_count(tqp_ctx* ctx) { return ctx ? ctx->c.launches.load() : 0; }
+int tqp_jit_nvrtc_version(void) {
+  try {
+    return tqp::jit_nvrtc_version();
+  } catch (...) {
+    return -1;
+  }
+}
 
 size_t tqp_dtype_size(int dtype) { return dtype_size(dtype); }
 

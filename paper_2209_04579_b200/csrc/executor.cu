@@ -223,16 +223,35 @@ void Executor::run_step(int s, std::vector<std::optional<Tensor>>& slots, const 
   const Step& step = plan_.steps[s];
   int64_t ordinal = step_first_ordinal_[s];
   int64_t step_start = now_ns(), step_bytes = 0, rows_out = 0;
-  for (const auto& in : step.instrs) {
+  // error checks of this step's instructions may be deferred to one readback
+  // at its end (Ctx::check_deferred); a synchronous error first reports any
+  // earlier deferred failure, so the first failing instruction always wins
+  struct DeferScope {
+    Ctx& c;
+    explicit DeferScope(Ctx& c_) : c(c_) { c.defer_checks = true; }
+    ~DeferScope() {
+      c.defer_checks = false;
+      c.deferred.clear();
+    }
+  } defer_scope(ctx_);
+  auto wrap = [&](const Error& e) -> Error {
+    if (e.code == TQP_ERR_KERNEL || e.code == TQP_ERR_ENCODING) return Error(TQP_ERR_EXEC, step.id + ": " + e.what(), e.bad_row);
+    return e;
+  };
+  for (size_t ii = 0; ii < step.instrs.size(); ++ii) {
+    const Instr& in = step.instrs[ii];
     int64_t t0 = now_ns();
     Tensor r;
     try {
       r = exec_instr(in, slots, tables);
+      if (trace || ii + 1 == step.instrs.size()) ctx_.check_deferred();
     } catch (const Error& e) {
-      if (e.code == TQP_ERR_KERNEL || e.code == TQP_ERR_ENCODING) {
-        throw Error(TQP_ERR_EXEC, step.id + ": " + e.what(), e.bad_row);
+      try {
+        ctx_.check_deferred();
+      } catch (const Error& first) {
+        throw wrap(first);
       }
-      throw;
+      throw wrap(e);
     }
     if (trace) ctx_.sync();
     int64_t t1 = now_ns();

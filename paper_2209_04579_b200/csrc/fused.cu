@@ -1935,6 +1935,25 @@ bool small_wide_wanted() {
 }
 constexpr int kWideSlots = 4;
 constexpr int kWideCW = 8;
+// 4-slot kernel with register accumulators (TQP_SMALL_REG=0: shared-memory
+// cells); TQP_SMALL_CW / TQP_SMALL_ROWS: its consumer warps / tile rows.
+// Q1 SF10 per launch (B200): cells 486 us; registers 14 warps x 4 rows per
+// thread (1792-row tiles) 365 us, 12 x 4 402 us, 10 x 4 406 us, 14 x 3 418
+// us, 12 x 2 660 us - four rows per thread keep the staged loads in flight.
+bool small_regacc() {
+  const char* e = std::getenv("TQP_SMALL_REG");
+  return !(e && (e[0] == '0' || e[0] == 'n'));
+}
+int small_reg_cw() {
+  static const int v = [] { const char* e = std::getenv("TQP_SMALL_CW"); const int x = e ? std::atoi(e) : 14;
+                            return x >= 4 && x <= 24 ? x : 14; }();
+  return v;
+}
+int small_reg_rows() {
+  static const int v = [] { const char* e = std::getenv("TQP_SMALL_ROWS"); const int x = e ? std::atoi(e) : 1792;
+                            return x >= 32 * small_reg_cw() && x <= 4096 && x % (32 * small_reg_cw()) == 0 ? x : 32 * small_reg_cw() * 4; }();
+  return v;
+}
 
 bool jit_wanted(long long rows) {
   const char* e = std::getenv("TQP_JIT");
@@ -1957,7 +1976,7 @@ int probe_mode_of(const BuildDesc& B) {
 }
 
 std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector<int>& probe_mode,
-                         int slots = kGroups) {
+                         int slots = kGroups, bool regacc = false) {
   const ProbeSpec& s = ts.p;
   std::ostringstream o;
   unsigned int_mask = 0;
@@ -1965,7 +1984,8 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
     if (s.acc[a].is_int) int_mask |= 1u << a;
   o << "#include \"fz_layout.cuh\"\n"
     << "#define Q_MODE " << mode << "\n#define Q_NA " << s.nacc << "\n#define Q_ROWS " << ts.rows << "\n#define Q_CW "
-    << cw << "\n#define Q_INT_MASK " << int_mask << "u\n#define Q_SLOTS " << slots << "\n"
+    << cw << "\n#define Q_INT_MASK " << int_mask << "u\n#define Q_SLOTS " << slots << "\n#define Q_REGACC "
+    << (regacc ? 1 : 0) << "\n"
     << "namespace tqp { namespace fz {\n"
     << "__device__ __forceinline__ unsigned long long q_u64(const unsigned char* st, unsigned off, int ri) {\n"
     << "  return *reinterpret_cast<const unsigned long long*>(st + off + ri * 8); }\n"
@@ -2098,8 +2118,8 @@ int build_tile_rows() {
 int jit_build_rows() {
   static const int r = [] {
     const char* e = std::getenv("TQP_BUILD_ROWS");  // tuning knob: rows per thread of q_build
-    const int v = e ? std::atoi(e) : 4;
-    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+    const int v = e ? std::atoi(e) : 2;  // Q3 orders build SF10: 108 us at 2, 115 at 4, 150 at 8
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
   }();
   return r;
 }
@@ -2599,7 +2619,13 @@ struct Runner {
                                                             : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
     const bool wide = P.mode == MODE_SMALL && !narrow && jit_wanted(ps.n) && small_wide_wanted();
     int small_threads = TileShape<MODE_SMALL>::THREADS;
-    if (wide) {  // per-thread cells for kWideSlots slots, kWideCW consumer warps
+    const bool regacc = wide && small_regacc();
+    const int wide_cw = regacc ? small_reg_cw() : kWideCW;
+    if (regacc) {  // register accumulators: no cells, taller tiles, more consumer warps
+      ts.aux_bytes = 0;
+      ts.rows = small_reg_rows();
+      small_threads = wide_cw * 32 + 32;
+    } else if (wide) {  // per-thread cells for kWideSlots slots, kWideCW consumer warps
       ts.aux_bytes = static_cast<int>(sizeof(unsigned long long) * kWideSlots * (ps.nacc + 1) * kWideCW * 32);
       small_threads = kWideCW * 32 + 32;
     }
@@ -2620,9 +2646,9 @@ struct Runner {
       std::vector<int> bm;
       for (const auto& pd : P.probes) bm.push_back(probe_mode_of(P.builds[pd.build]));
       ts.p = ps;
-      const int cw = wide ? kWideCW : P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
+      const int cw = wide ? wide_cw : P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
       hp.mark("tprep");
-      const std::string src = gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups);
+      const std::string src = gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups, regacc);
       hp.mark("tgen");
       kfn = jit_kernel(src, "q_tile");
     }

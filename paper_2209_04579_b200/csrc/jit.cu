@@ -1,6 +1,16 @@
 // NVRTC front end for the specialised pipeline kernels (jit.hpp).
+//
+// NVRTC is bound at run time from the toolkit this library was built with
+// (dlopen by absolute path, RTLD_LOCAL), not through the dynamic linker: a
+// process that imported torch first already holds torch's bundled
+// libnvrtc.so.12 (12.8), and an ordinary -lnvrtc would bind to that one by
+// SONAME. The generated kernels must not depend on import order - the Q1
+// register-accumulator kernel measured 365 us with NVRTC 12.9 and 458 us
+// with 12.8 on the same B200.
+#include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -25,11 +35,62 @@ Cache& cache() {
   return c;
 }
 
+#ifndef TQP_NVRTC_PATH
+#define TQP_NVRTC_PATH "/usr/local/cuda/lib64/libnvrtc.so.12"
+#endif
+
+struct Nvrtc {
+  const char* (*GetErrorString)(nvrtcResult);
+  nvrtcResult (*Version)(int*, int*);
+  nvrtcResult (*CreateProgram)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult (*CompileProgram)(nvrtcProgram, int, const char* const*);
+  nvrtcResult (*GetProgramLogSize)(nvrtcProgram, size_t*);
+  nvrtcResult (*GetProgramLog)(nvrtcProgram, char*);
+  nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t*);
+  nvrtcResult (*GetCUBIN)(nvrtcProgram, char*);
+  nvrtcResult (*DestroyProgram)(nvrtcProgram*);
+  int major = 0, minor = 0;
+};
+
+// TQP_NVRTC (environment) overrides the library path
+const Nvrtc& nvrtc() {
+  static const Nvrtc api = [] {
+    const char* env = std::getenv("TQP_NVRTC");
+    const char* path = env && *env ? env : TQP_NVRTC_PATH;
+    void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+    if (!h) throw Error(TQP_ERR_CUDA, std::string("nvrtc: cannot load ") + path + ": " + dlerror());
+    Nvrtc a{};
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) throw Error(TQP_ERR_CUDA, std::string("nvrtc: missing symbol ") + name + " in " + path);
+      return f;
+    };
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("nvrtcGetErrorString"));
+    a.Version = reinterpret_cast<decltype(a.Version)>(sym("nvrtcVersion"));
+    a.CreateProgram = reinterpret_cast<decltype(a.CreateProgram)>(sym("nvrtcCreateProgram"));
+    a.CompileProgram = reinterpret_cast<decltype(a.CompileProgram)>(sym("nvrtcCompileProgram"));
+    a.GetProgramLogSize = reinterpret_cast<decltype(a.GetProgramLogSize)>(sym("nvrtcGetProgramLogSize"));
+    a.GetProgramLog = reinterpret_cast<decltype(a.GetProgramLog)>(sym("nvrtcGetProgramLog"));
+    a.GetCUBINSize = reinterpret_cast<decltype(a.GetCUBINSize)>(sym("nvrtcGetCUBINSize"));
+    a.GetCUBIN = reinterpret_cast<decltype(a.GetCUBIN)>(sym("nvrtcGetCUBIN"));
+    a.DestroyProgram = reinterpret_cast<decltype(a.DestroyProgram)>(sym("nvrtcDestroyProgram"));
+    a.Version(&a.major, &a.minor);
+    return a;
+  }();
+  return api;
+}
+
 void nvrtc_check(nvrtcResult r, const char* what) {
-  if (r != NVRTC_SUCCESS) throw Error(TQP_ERR_CUDA, std::string("nvrtc: ") + nvrtcGetErrorString(r) + " in " + what);
+  if (r != NVRTC_SUCCESS)
+    throw Error(TQP_ERR_CUDA, std::string("nvrtc: ") + nvrtc().GetErrorString(r) + " in " + what);
 }
 
 }  // namespace
+
+int jit_nvrtc_version() {
+  const Nvrtc& a = nvrtc();
+  return a.major * 1000 + a.minor * 10;
+}
 
 const void* jit_kernel(const std::string& src, const char* entry) {
   Cache& c = cache();
@@ -38,25 +99,26 @@ const void* jit_kernel(const std::string& src, const char* entry) {
   auto it = c.kernels.find(key);
   if (it != c.kernels.end()) return it->second;
 
+  const Nvrtc& api = nvrtc();
   nvrtcProgram prog;
-  nvrtc_check(nvrtcCreateProgram(&prog, src.c_str(), "tqp_pipeline.cu", kJitHeaderCount, kJitHeaderSrc, kJitHeaderNames),
+  nvrtc_check(api.CreateProgram(&prog, src.c_str(), "tqp_pipeline.cu", kJitHeaderCount, kJitHeaderSrc, kJitHeaderNames),
               "nvrtcCreateProgram");
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--device-int128", "-lineinfo",
                         "-default-device", "--extra-device-vectorization"};
-  nvrtcResult r = nvrtcCompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
+  nvrtcResult r = api.CompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
-    nvrtcGetProgramLogSize(prog, &n);
+    api.GetProgramLogSize(prog, &n);
     std::string log(n, '\0');
-    if (n) nvrtcGetProgramLog(prog, &log[0]);
-    nvrtcDestroyProgram(&prog);
+    if (n) api.GetProgramLog(prog, &log[0]);
+    api.DestroyProgram(&prog);
     throw Error(TQP_ERR_CUDA, "nvrtc failed to compile a pipeline kernel:\n" + log.substr(0, 1500));
   }
   size_t n = 0;
-  nvrtc_check(nvrtcGetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
+  nvrtc_check(api.GetCUBINSize(prog, &n), "nvrtcGetCUBINSize");
   std::vector<char> cubin(n);
-  nvrtc_check(nvrtcGetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
-  nvrtcDestroyProgram(&prog);
+  nvrtc_check(api.GetCUBIN(prog, cubin.data()), "nvrtcGetCUBIN");
+  api.DestroyProgram(&prog);
 
   cudaLibrary_t lib;
   TQP_CUDA(cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));

@@ -15,4 +15,7 @@ const void* jit_kernel(const std::string& src, const char* entry);
 // Number of distinct kernels compiled in this process (tests/diagnostics).
 int jit_compiled_count();
 
+// Version of the NVRTC the kernels are compiled with (major * 1000 + minor * 10).
+int jit_nvrtc_version();
+
 }  // namespace tqp

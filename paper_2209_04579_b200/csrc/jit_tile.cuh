@@ -21,6 +21,9 @@ constexpr int Q_R = Q_ROWS / Q_CT;
 #ifndef Q_SLOTS
 #define Q_SLOTS kGroups  // small-group slots per CTA (<= kGroups)
 #endif
+#ifndef Q_REGACC
+#define Q_REGACC 0  // small-group accumulators in registers instead of shared-memory cells
+#endif
 __device__ __forceinline__ bool q_is_int(int a) { return (Q_INT_MASK >> a) & 1; }
 
 extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec t) {
@@ -68,6 +71,16 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
     for (int a = 0; a < Q_NA; ++a) acc[a] = 0;  // 0.0 and 0 share bits
     unsigned long long cnt = 0;
     long long absmax = 0;
+    // MODE_SMALL with Q_REGACC: per-thread [slot][acc + count] accumulators in
+    // registers. A row adds to its slot only (predicated), in the same order
+    // as the shared-memory cells, so the sums are bit-identical to them; the
+    // cells' shared-memory traffic (a load and a store of 8 B per accumulator
+    // per row, twice the staged column bytes) is gone.
+    unsigned long long racc[Q_REGACC ? Q_SLOTS : 1][Q_NA + 1];
+#pragma unroll
+    for (int j = 0; j < (Q_REGACC ? Q_SLOTS : 1); ++j)
+#pragma unroll
+      for (int a = 0; a <= Q_NA; ++a) racc[j][a] = 0;
     long long it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int st = static_cast<int>(it % nst);
@@ -132,6 +145,20 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
         }
         // per-thread cells [slot][acc + count][thread]; masked rows add 0 to
         // slot 0 (x + 0 == x), so there is no per-row branch
+#if Q_REGACC
+#pragma unroll
+        for (int k = 0; k < Q_R; ++k) {
+          const int tgt = slot[k] < 0 ? 0 : slot[k];
+#pragma unroll
+          for (int j = 0; j < Q_SLOTS; ++j) {
+            if (tgt == j) {
+#pragma unroll
+              for (int a = 0; a < Q_NA; ++a) racc[j][a] = add_acc(q_is_int(a), racc[j][a], v[k][a]);
+              racc[j][Q_NA] += pass[k] ? 1u : 0u;
+            }
+          }
+        }
+#else
 #pragma unroll
         for (int k = 0; k < Q_R; ++k) {
           unsigned long long* cell = s_cell + (slot[k] < 0 ? 0 : slot[k]) * (Q_NA + 1) * Q_CT + ct;
@@ -139,6 +166,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
           for (int a = 0; a < Q_NA; ++a) cell[a * Q_CT] = add_acc(q_is_int(a), cell[a * Q_CT], v[k][a]);
           cell[Q_NA * Q_CT] += pass[k] ? 1u : 0u;
         }
+#endif
       } else {
 #pragma unroll
         for (int k = 0; k < Q_R; ++k) {
@@ -168,10 +196,15 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
     }
     if constexpr (Q_MODE == MODE_SMALL) {
+#pragma unroll
       for (int gg = 0; gg < Q_SLOTS; ++gg) {
 #pragma unroll
         for (int a = 0; a <= Q_NA; ++a) {
+#if Q_REGACC
+          unsigned long long x = racc[gg][a];
+#else
           unsigned long long x = s_cell[(gg * (Q_NA + 1) + a) * Q_CT + ct];
+#endif
           const bool is_int = a == Q_NA || q_is_int(a);
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) x = add_acc(is_int, x, __shfl_xor_sync(0xffffffffu, x, o));

@@ -80,14 +80,16 @@ __global__ void k_binary(const T* __restrict__ a, const T* __restrict__ b, Out* 
 }
 
 template <typename T, typename Out, typename F>
-Tensor binary(Ctx& c, const char* kernel, const Tensor& a, const Tensor& b, int out_dtype, F f, Bcast* shape = nullptr) {
+Tensor binary(Ctx& c, const char* kernel, const Tensor& a, const Tensor& b, int out_dtype, F f, Bcast* shape = nullptr,
+              long long* err = nullptr) {
   Bcast s = broadcast_shape(kernel, a, b);
   if (shape) *shape = s;
   Tensor o = c.alloc(out_dtype, s.rows, s.cols);
   int64_t n = s.rows * s.cols;
   if (n) {
     k_binary<T, Out><<<c.grid_for(n, kBlock), kBlock, 0, c.stream>>>(
-        a.ptr<T>(), b.ptr<T>(), o.ptr<Out>(), n, s.cols, s.a_scalar, s.a_row, s.b_scalar, s.b_row, f, c.d_err);
+        a.ptr<T>(), b.ptr<T>(), o.ptr<Out>(), n, s.cols, s.a_scalar, s.a_row, s.b_scalar, s.b_row, f,
+        err ? err : c.d_err);
     c.count_launch();
   }
   return o;
@@ -325,24 +327,36 @@ Tensor arith(Ctx& c, const Tensor& a, const Tensor& b, int op) {
   if (a.dtype == TQP_BOOL || a.dtype == TQP_STR8) kernel_fail("arith: bool operands not supported");
   if (op == TQP_DIV && a.dtype != TQP_F64) kernel_fail("arith: div requires float64 operands");
   if (op < TQP_ADD || op > TQP_DIV) kernel_fail("arith: bad op");
-  c.reset_err();
   Bcast s;
   Tensor out;
   if (a.dtype == TQP_F64) {
-    out = binary<double, double>(c, "arith", a, b, TQP_F64, ArithF64{op}, &s);
-    if (op == TQP_DIV) {
+    if (op != TQP_DIV) return binary<double, double>(c, "arith", a, b, TQP_F64, ArithF64{op}, &s);
+    bool dfr = false;
+    long long* err = c.check_slot(&dfr);
+    out = binary<double, double>(c, "arith", a, b, TQP_F64, ArithF64{op}, &s, err);
+    const char* msg = "arith: division by zero at row ";
+    if (dfr) {
+      c.deferred.push_back({msg, s.cols});
+    } else {
       int64_t bad = c.read_err();
-      if (bad >= 0) kernel_fail("arith: division by zero at row " + std::to_string(bad / s.cols), bad / s.cols);
+      if (bad >= 0) kernel_fail(msg + std::to_string(bad / s.cols), bad / s.cols);
     }
     return out;
   }
+  bool dfr = false;
+  long long* err = c.check_slot(&dfr);
   if (a.dtype == TQP_I64) {
-    out = binary<int64_t, int64_t>(c, "arith", a, b, TQP_I64, ArithInt<int64_t>{op}, &s);
+    out = binary<int64_t, int64_t>(c, "arith", a, b, TQP_I64, ArithInt<int64_t>{op}, &s, err);
   } else {
-    out = binary<int32_t, int32_t>(c, "arith", a, b, TQP_I32, ArithInt<int32_t>{op}, &s);
+    out = binary<int32_t, int32_t>(c, "arith", a, b, TQP_I32, ArithInt<int32_t>{op}, &s, err);
   }
-  int64_t bad = c.read_err();
-  if (bad >= 0) kernel_fail("arith: integer overflow at row " + std::to_string(bad / s.cols), bad / s.cols);
+  const char* msg = "arith: integer overflow at row ";
+  if (dfr) {
+    c.deferred.push_back({msg, s.cols});
+  } else {
+    int64_t bad = c.read_err();
+    if (bad >= 0) kernel_fail(msg + std::to_string(bad / s.cols), bad / s.cols);
+  }
   return out;
 }
 

@@ -100,6 +100,34 @@ int64_t Ctx::read_err(long long* aux, long long* kind) {
   return h_err[0] == kNoBad ? -1 : h_err[0];
 }
 
+long long* Ctx::check_slot(bool* is_deferred) {
+  if (defer_checks && deferred.size() < static_cast<size_t>(kMaxDeferred)) {
+    *is_deferred = true;
+    return d_defer + 4 * deferred.size();
+  }
+  *is_deferred = false;
+  reset_err();
+  return d_err;
+}
+
+void Ctx::check_deferred() {
+  if (deferred.empty()) return;
+  const size_t n = deferred.size();
+  std::vector<DeferredCheck> list;
+  list.swap(deferred);
+  TQP_CUDA(cudaMemcpyAsync(h_err + kPinnedRead, d_defer, 4 * n * sizeof(long long), cudaMemcpyDeviceToHost, stream));
+  sync();
+  // slots back to "no error" (ordered before any later use on the stream)
+  TQP_CUDA(cudaMemcpyAsync(d_defer, h_err + kPinnedDeferInit, 4 * n * sizeof(long long), cudaMemcpyHostToDevice, stream));
+  for (size_t i = 0; i < n; ++i) {
+    const long long bad = h_err[kPinnedRead + 4 * i];
+    if (bad != kNoBad) {
+      const int64_t row = bad / list[i].cols;
+      kernel_fail(list[i].msg + std::to_string(row), row);
+    }
+  }
+}
+
 int Ctx::grid_for(int64_t n, int block, int per_thread, int waves) const {
   int64_t need = (n + static_cast<int64_t>(block) * per_thread - 1) / (static_cast<int64_t>(block) * per_thread);
   int64_t cap = static_cast<int64_t>(num_sms) * waves;

@@ -77,7 +77,26 @@ struct Ctx {
   static constexpr int kPinnedErrInit = 8;     // {INT64_MAX, 0, 0}
   static constexpr int kPinnedMinMax = 64;     // kPinnedMinMaxPairs x {INT64_MAX, INT64_MIN}
   static constexpr int kPinnedMinMaxPairs = 64;
+  static constexpr int kPinnedDeferInit = 192;  // kMaxDeferred x {INT64_MAX, 0, 0, 0}
   static constexpr int kPinnedRead = 256;      // 256 words of readback
+  // Deferred checks (executor steps only): an instruction whose one host
+  // interaction is its error check (arith's division by zero / overflow)
+  // gets its own device error slot instead of a round trip; the executor
+  // reads every slot of a step in one readback (check_deferred) before the
+  // step's next synchronous error or its end, and the first failing
+  // instruction in program order is reported, as if checked in place.
+  static constexpr int kMaxDeferred = 16;
+  long long* d_defer = nullptr;  // kMaxDeferred x 4 words
+  bool defer_checks = false;
+  struct DeferredCheck {
+    std::string msg;  // message up to the row number
+    int64_t cols;     // reported row = flat index / cols
+  };
+  std::vector<DeferredCheck> deferred;
+  // error slot of the next check: a fresh deferred slot while deferring
+  // (and one is free), else d_err after reset_err()
+  long long* check_slot(bool* is_deferred);
+  void check_deferred();
   std::atomic<int64_t> launches{0};
 
   Tensor alloc(int dtype, int64_t rows, int64_t cols);

@@ -98,7 +98,7 @@ def _load() -> C.CDLL:
         "tqp_abi_version": (I, []),
         "tqp_init": (P, [I, S]), "tqp_shutdown": (None, [P]), "tqp_sync": (I, [P, S]),
         "tqp_stream": (P, [P]), "tqp_backend_name": (C.c_char_p, [P]), "tqp_device": (I, [P]),
-        "tqp_launch_count": (I64_, [P]), "tqp_dtype_size": (C.c_size_t, [I]),
+        "tqp_launch_count": (I64_, [P]), "tqp_dtype_size": (C.c_size_t, [I]), "tqp_jit_nvrtc_version": (I, []),
         "tqp_tensor_from_host": (P, [P, I, I64_, I64_, P, S]),
         "tqp_tensor_from_host_utf8_i32": (P, [P, I64_, I64_, P, S]),
         "tqp_tensor_from_device": (P, [P, I, I64_, I64_, P, S]),
@@ -194,6 +194,11 @@ class Context:
 
 
 _default: Optional[Context] = None
+
+
+def nvrtc_version() -> int:
+    """NVRTC the run-time specialised kernels compile with (12090 = 12.9)."""
+    return int(lib.tqp_jit_nvrtc_version())
 
 
 def default_context() -> Context:

@@ -54,3 +54,19 @@ def test_plan_builder_without_gpu():
     from paper_2209_04579_b200 import tqp
     p = tqp.Plan.from_file(ROOT / "paper_2209_04579_b200" / "plans" / "q6.opplan.json")
     assert p.h
+
+
+def test_nvrtc_bound_from_build_toolkit():
+    """The specialised kernels compile with the toolkit the library was built
+    with even when torch (bundling an older libnvrtc.so.12) is imported
+    first: kernel speed must not depend on import order."""
+    import subprocess
+    import sys
+    code = ("import torch, sys; sys.path.insert(0, %r); "
+            "from paper_2209_04579_b200 import tqp; print(tqp.nvrtc_version())" % str(ROOT))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    nvcc = subprocess.run(["/usr/local/cuda/bin/nvcc", "--version"], capture_output=True, text=True).stdout
+    rel = nvcc.split("release ")[1].split(",")[0]
+    major, minor = (int(x) for x in rel.split("."))
+    assert int(out.stdout.strip()) == major * 1000 + minor * 10

@@ -17,11 +17,13 @@ PLANS = ROOT / "paper_2209_04579_b200" / "plans"
 QUERIES = ("q1", "q6", "q14", "q3")
 
 
-def run(tqp, q, tables, jit, wide=False):
+def run(tqp, q, tables, jit, wide=False, regacc=True):
     old = os.environ.get("TQP_JIT")
     old_w = os.environ.get("TQP_SMALL_WIDE")
+    old_r = os.environ.get("TQP_SMALL_REG")
     os.environ["TQP_JIT"] = "1" if jit else "0"
     os.environ["TQP_SMALL_WIDE"] = "1" if wide else "0"
+    os.environ["TQP_SMALL_REG"] = "1" if regacc else "0"
     try:
         ex = tqp.Executor(json.loads((PLANS / f"{q}.opplan.json").read_text()))
         ex.set_timing(True)
@@ -37,6 +39,10 @@ def run(tqp, q, tables, jit, wide=False):
             del os.environ["TQP_SMALL_WIDE"]
         else:
             os.environ["TQP_SMALL_WIDE"] = old_w
+        if old_r is None:
+            del os.environ["TQP_SMALL_REG"]
+        else:
+            os.environ["TQP_SMALL_REG"] = old_r
 
 
 @pytest.mark.parametrize("q", QUERIES)
@@ -95,17 +101,35 @@ def _q1_close(got, want):
         np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=n)
 
 
+def _q1_within(got, want, rtol=1e-12):
+    """Keys, integer sums and counts bit for bit; fp64 sums within rtol (a
+    different row-to-thread split changes the fp64 association only)."""
+    assert [(n, t) for n, t, _ in got] == [(n, t) for n, t, _ in want]
+    for (n, t, g), (_, _, w) in zip(got, want):
+        if g.dtype == np.float64:
+            np.testing.assert_allclose(g, w, rtol=rtol, atol=0, err_msg=n)
+        else:
+            np.testing.assert_array_equal(g, w, err_msg=n)
+
+
 def test_small_group_wide_kernel(ctx):
-    """The 4-slot small-group kernel (the default for large Q1-shaped scans)
-    against the 8-slot generic kernel: bit-identical (same per-thread row
-    order); with six keys per CTA it flags the overflow and the unit reruns
-    on the 8-slot kernel."""
+    """The 4-slot small-group kernels (the default for large Q1-shaped scans)
+    against the 8-slot generic kernel: the shared-memory-cell variant is
+    bit-identical (same tile shape, same per-thread row order); the register
+    variant (taller tiles, more warps) matches within 1e-12 and is
+    deterministic; with six keys per CTA both flag the overflow and the unit
+    reruns on the 8-slot kernel."""
     from paper_2209_04579_b200 import tqp
     tables = {"lineitem": tqp.Table.generate("lineitem", 0.05, 7)}
+    cells, kc = run(tqp, "q1", tables, True, wide=True, regacc=False)
     wide, kw = run(tqp, "q1", tables, True, wide=True)
+    again, _ = run(tqp, "q1", tables, True, wide=True)
     generic, _ = run(tqp, "q1", tables, False)
     assert any(k.startswith("kernel:q_tile") for k in kw)
-    _q1_close(wide, generic)
+    assert any(k.startswith("kernel:q_tile") for k in kc)
+    _q1_close(cells, generic)
+    _q1_close(wide, again)
+    _q1_within(wide, generic)
     # six (returnflag, linestatus) keys: more than the wide kernel's 4 slots
     host = tables["lineitem"].to_numpy()
     rng = np.random.default_rng(3)
@@ -118,7 +142,9 @@ def test_small_group_wide_kernel(ctx):
         cols.append((name, lt, a))
     six = {"lineitem": tqp.Table.from_columns(cols)}
     wide6, kw6 = run(tqp, "q1", six, True, wide=True)
+    cells6, _ = run(tqp, "q1", six, True, wide=True, regacc=False)
     generic6, _ = run(tqp, "q1", six, False)
     assert len(wide6[0][2]) == 6
     assert any(k.startswith("kernel:q_tile") for k in kw6)
     _q1_close(wide6, generic6)
+    _q1_close(cells6, generic6)
