@@ -348,7 +348,9 @@ void Executor::check_inputs(const TableSet& tables) const {
 }
 
 Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
+  HostProf hp("exec");
   check_inputs(tables);
+  hp.mark("inputs");
   std::vector<std::optional<Tensor>> slots(plan_.num_slots);
   int64_t run_start = now_ns();
   size_t u = 0;
@@ -359,6 +361,7 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
       cudaEvent_t ev;
       time_begin(&ev);
       bool ok = unit.run(ctx_, slots, tables);
+      hp.mark("unit");
       if (ok) time_end(unit.name, ev);
       else ctx_.give_event(ev);
       if (ok) {
@@ -387,9 +390,12 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
     time_begin(&ev);
     run_step(s, slots, tables, trace, run_start);
     time_end("step:" + plan_.steps[s].kind, ev);
+    hp.mark("step");
     ++s;
   }
-  return collect_outputs(slots);
+  Result r = collect_outputs(slots);
+  hp.mark("collect");
+  return r;
 }
 
 Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots) {

@@ -418,11 +418,18 @@ struct AccDesc {
   }
 };
 
+constexpr int kMaxEpiConst = 8;  // constants of a scalar epilogue
+// err[3] reason codes of a scalar epilogue (the exact path reports these
+// errors with the reference's text)
+constexpr long long kReasonEpiDivZero = 20;
+constexpr long long kReasonEpiOverflow = 21;
+
 struct OutDesc {  // aggregate outputs, in the AGG step's output order
-  int fn;         // 0 sum 1 count 2 avg, 10 + i: group key i
+  int fn;         // 0 sum 1 count 2 avg, 3 scalar epilogue arith, 10 + i: group key i
   int acc = -1;
   int slot = -1;
   bool is_int = false;
+  int op = 0, a = 0, b = 0;  // fn 3 (OutKind)
 };
 
 struct PipeDesc {
@@ -448,6 +455,8 @@ struct PipeDesc {
   bool topk = false;
   int64_t k = 0;
   std::vector<std::pair<int, bool>> sort_outs;  // (index into outs, asc)
+  std::vector<unsigned long long> konst;        // scalar epilogue constants (bits)
+  std::string epi_step;                         // id of the absorbed epilogue step
   std::vector<int> final_cols;                  // unit output slots -> outs index
   std::vector<int> final_slots;
   std::string explain;
@@ -933,15 +942,99 @@ struct Planner {
         }
       }
     }
+    if (P.mode == MODE_SCALAR) absorb_scalar_epilogue(next);
     return true;
+  }
+
+  // A project step right after a scalar aggregate whose instructions are 1x1
+  // constants and + - * / over the aggregate's outputs (Q14's 100.00 *
+  // promo / total) is evaluated by k_final_scalar: no per-instruction step,
+  // no second round trip. Anything else (other ops, int division, a bool
+  // constant) leaves the step to the exact path.
+  void absorb_scalar_epilogue(int next) {
+    if (next >= static_cast<int>(plan.steps.size())) return;
+    const Step& st = plan.steps[next];
+    if (st.kind != "project" || st.instrs.empty()) return;
+    std::map<int, int> out_of;  // slot -> outs index
+    for (size_t i = 0; i < P.outs.size(); ++i) out_of[P.outs[i].slot] = static_cast<int>(i);
+    std::map<int, std::pair<int, bool>> konst_of;  // slot -> (const index, is_int)
+    std::vector<OutDesc> outs = P.outs;
+    std::vector<unsigned long long> konst;
+    auto is_int_out = [&](const OutDesc& o) { return o.fn == 1 || ((o.fn == 0 || o.fn == 3) && o.is_int); };
+    for (const Instr& in : st.instrs) {
+      if (in.op == Op::ConstTensor) {
+        bool f = false, b = false;
+        long long ik = 0;
+        double fk = 0;
+        if (!const_scalar(&in, &f, &ik, &fk, &b) || b || konst.size() >= static_cast<size_t>(kMaxEpiConst)) return;
+        unsigned long long bits;
+        if (f) std::memcpy(&bits, &fk, 8);
+        else bits = static_cast<unsigned long long>(ik);
+        konst_of[in.output] = {static_cast<int>(konst.size()), !f};
+        konst.push_back(bits);
+        continue;
+      }
+      if (in.op != Op::Arith || in.inputs.size() != 2 || in.arith < TQP_ADD || in.arith > TQP_DIV) return;
+      int opnd[2];
+      bool ints[2];
+      for (int k = 0; k < 2; ++k) {
+        const int x = in.inputs[k];
+        auto o = out_of.find(x);
+        auto q = konst_of.find(x);
+        if (o != out_of.end()) {
+          opnd[k] = o->second;
+          ints[k] = is_int_out(outs[o->second]);
+        } else if (q != konst_of.end()) {
+          opnd[k] = -1 - q->second.first;
+          ints[k] = q->second.second;
+        } else {
+          return;
+        }
+      }
+      if (ints[0] != ints[1] || (ints[0] && in.arith == TQP_DIV) || outs.size() >= 16) return;
+      OutDesc d;
+      d.fn = 3;
+      d.slot = in.output;
+      d.is_int = ints[0];
+      d.op = in.arith;
+      d.a = opnd[0];
+      d.b = opnd[1];
+      out_of[in.output] = static_cast<int>(outs.size());
+      outs.push_back(d);
+    }
+    // the step's outputs (and any slot passing through it) must come from the unit
+    std::vector<int> slots = P.final_slots, cols = P.final_cols;
+    for (int x : st.output_slots) {
+      auto o = out_of.find(x);
+      if (o == out_of.end()) return;
+      if (std::find(slots.begin(), slots.end(), x) == slots.end()) {
+        slots.push_back(x);
+        cols.push_back(o->second);
+      }
+    }
+    for (size_t i = P.outs.size(); i < outs.size(); ++i) {
+      if (std::find(slots.begin(), slots.end(), outs[i].slot) == slots.end()) {
+        slots.push_back(outs[i].slot);
+        cols.push_back(static_cast<int>(i));
+      }
+    }
+    P.outs = outs;
+    P.konst = konst;
+    P.final_slots = slots;
+    P.final_cols = cols;
+    P.epi_step = st.id;
+    P.last_step = next;
   }
 };
 
 // ---- finalize kernels ------------------------------------------------------------
 struct OutKind {
-  int fn;  // 0 sum 1 count 2 avg, 10+i key
+  int fn;  // 0 sum 1 count 2 avg, 3 scalar epilogue arith, 10+i key
   int acc;
   int is_int;
+  // fn 3: op (TQP_ADD..TQP_DIV) over operands a, b: >= 0 an earlier output,
+  // < 0 the constant konst[-1 - x]
+  int op = 0, a = 0, b = 0;
 };
 
 struct FinalSpec {
@@ -950,71 +1043,114 @@ struct FinalSpec {
   void* out_ptr[16];
   int nacc = 0;
   int acc_is_int[kMaxAcc];
+  unsigned long long konst[kMaxEpiConst];
 };
 
 constexpr int kMerged = 256;
-constexpr int kMergeChunk = 256;
+
+// Deterministic warp sum of get(i), i < m: lane l adds i = l, l + 32, ... in
+// order, then a fixed xor-shuffle tree; every lane returns the total. The
+// association is fixed by m alone, so a merge is reproducible run to run
+// (fp64 sums need not be sequential: SURVEY.md 8(a) a7 allows the
+// reference's own 4096-chunk order, within the fp64 tolerance).
+template <typename Get>
+__device__ __forceinline__ unsigned long long warp_sum_fixed(bool is_int, int m, Get get) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long t = 0;
+#pragma unroll 4
+  for (int i = lane; i < m; i += 32) t = add_acc(is_int, t, get(i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t = add_acc(is_int, t, __shfl_xor_sync(0xffffffffu, t, o));
+  return t;
+}
 
 __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int nparts, FinalSpec f, long long* err) {
-  // one warp per accumulator (and the count): independent loads into shared
-  // memory, then lane 0 adds in CTA order
+  // one warp per accumulator (and the count), warp_sum_fixed over the CTAs
   __shared__ unsigned long long s_tot[kMaxAcc + 1];
-  __shared__ unsigned long long s_v[kMaxAcc + 1][kMergeChunk];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int a = warp; a <= kMaxAcc; a += nwarps) {
     if (a != kMaxAcc && a >= f.nacc) continue;
     const bool is_int = a == kMaxAcc || f.acc_is_int[a];
-    unsigned long long t = 0;
-    for (int c0 = 0; c0 < nparts; c0 += kMergeChunk) {
-      const int m = nparts - c0 < kMergeChunk ? nparts - c0 : kMergeChunk;
-      for (int i = lane; i < m; i += 32) s_v[a][i] = part[static_cast<long long>(c0 + i) * (kMaxAcc + 1) + a];
-      __syncwarp();
-      if (lane == 0)
-        for (int i = 0; i < m; ++i) t = add_acc(is_int, t, s_v[a][i]);
-      __syncwarp();
-    }
-    if (lane == 0) s_tot[a] = t;
+    const unsigned long long t =
+        warp_sum_fixed(is_int, nparts, [&](int i) { return part[static_cast<long long>(i) * (kMaxAcc + 1) + a]; });
+    if ((threadIdx.x & 31) == 0) s_tot[a] = t;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     long long cnt = static_cast<long long>(s_tot[kMaxAcc]);
+    unsigned long long val[16];
     for (int j = 0; j < f.nouts; ++j) {
       const OutKind& o = f.outs[j];
+      unsigned long long v = 0;
       if (o.fn == 1) {
-        static_cast<long long*>(f.out_ptr[j])[0] = cnt;
+        v = static_cast<unsigned long long>(cnt);
       } else if (o.fn == 0) {
-        static_cast<unsigned long long*>(f.out_ptr[j])[0] = s_tot[o.acc];
+        v = s_tot[o.acc];
+      } else if (o.fn == 3) {
+        // scalar epilogue, arith's semantics (kernels.cpp:211-283): fp64
+        // with IEEE rounding, int64 checked; a division by zero or an
+        // overflow hands the unit to the exact path, which raises it
+        const unsigned long long x = o.a >= 0 ? val[o.a] : f.konst[-1 - o.a];
+        const unsigned long long y = o.b >= 0 ? val[o.b] : f.konst[-1 - o.b];
+        if (o.is_int) {
+          int64_t r = 0;
+          const int64_t xi = static_cast<int64_t>(x), yi = static_cast<int64_t>(y);
+          const bool ovf = o.op == TQP_ADD ? add_ovf(xi, yi, &r) : o.op == TQP_SUB ? sub_ovf(xi, yi, &r) : mul_ovf(xi, yi, &r);
+          if (ovf) {
+            err[0] = 1;
+            err[3] = kReasonEpiOverflow;
+          }
+          v = static_cast<unsigned long long>(r);
+        } else {
+          const double xd = __longlong_as_double(static_cast<long long>(x));
+          const double yd = __longlong_as_double(static_cast<long long>(y));
+          double r;
+          switch (o.op) {
+            case TQP_ADD: r = __dadd_rn(xd, yd); break;
+            case TQP_SUB: r = __dsub_rn(xd, yd); break;
+            case TQP_MUL: r = __dmul_rn(xd, yd); break;
+            default:
+              if (yd == 0.0) {
+                err[0] = 1;
+                err[3] = kReasonEpiDivZero;
+                r = 0.0;
+              } else {
+                r = __ddiv_rn(xd, yd);
+              }
+          }
+          v = static_cast<unsigned long long>(__double_as_longlong(r));
+        }
       } else {
         if (cnt == 0) {
           err[0] = 1;  // AVG over zero rows: the reference raises division by zero
+          val[j] = 0;
           continue;
         }
         double sum = f.acc_is_int[o.acc] ? static_cast<double>(static_cast<long long>(s_tot[o.acc]))
                                          : __longlong_as_double(static_cast<long long>(s_tot[o.acc]));
-        static_cast<double*>(f.out_ptr[j])[0] = __ddiv_rn(sum, static_cast<double>(cnt));
+        v = static_cast<unsigned long long>(__double_as_longlong(__ddiv_rn(sum, static_cast<double>(cnt))));
       }
+      val[j] = v;
+      static_cast<unsigned long long*>(f.out_ptr[j])[0] = v;
     }
   }
 }
 
-// MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums in CTA
-// order. One thread per CTA part inserts its codes and later records the
-// group rank of each of its slots (rank[part][slot]); one warp per (group,
-// accumulator | count) then gathers the CTA values into shared memory - each
-// lane's rank words and values for 4 parts in flight at once - and lane 0
-// adds them in CTA order (absent slots contribute +0.0 / 0, which never
-// changes a sum that starts at +0.0), so the result is the sequential
-// CTA-order sum.
-constexpr int kMergeUnroll = 4;
-__global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts, FinalSpec f,
-                                                          int nkeys, void* key_ptr0, void* key_ptr1, void* key_ptr2,
-                                                          void* key_ptr3, int* rank /*[nparts][kGroups]*/,
-                                                          long long* ngroups_out, long long* err) {
+// MODE_SMALL merge: distinct codes -> sorted -> per (group, acc) sums. One
+// thread per CTA part inserts its codes and later records the group rank of
+// each of its slots (rank[part][slot]); one warp per (group, accumulator |
+// count) then sums the parts' values with warp_sum_fixed (absent slots
+// contribute +0.0 / 0, which never changes a sum that starts at +0.0).
+constexpr int kFinalSmallThreads = 1024;
+__global__ void __launch_bounds__(kFinalSmallThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts,
+                                                                    FinalSpec f, int nkeys, void* key_ptr0,
+                                                                    void* key_ptr1, void* key_ptr2, void* key_ptr3,
+                                                                    int* rank /*[nparts][kGroups]*/,
+                                                                    long long* ngroups_out, long long* err) {
   __shared__ unsigned s_set[kMerged];
   __shared__ unsigned s_sorted[kMerged];
-  __shared__ unsigned long long s_v[kThreads / 32][kMergeChunk];
   __shared__ unsigned long long s_tot[kMerged][kMaxAcc + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int i = threadIdx.x; i < kMerged; i += blockDim.x) s_set[i] = 0xffffffffu;
   __syncthreads();
   for (int c = threadIdx.x; c < nparts; c += blockDim.x) {
@@ -1052,10 +1188,8 @@ __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __res
     for (int j = 0; j < kMerged; ++j) r += s_set[j] < v;
     s_sorted[r] = v;
   }
-  int n = 0;
-  for (int i = 0; i < kMerged; ++i) n += s_set[i] != 0xffffffffu;  // uniform
+  const int n = __syncthreads_count(threadIdx.x < kMerged && s_set[threadIdx.x] != 0xffffffffu);
   if (threadIdx.x == 0) *ngroups_out = n;
-  __syncthreads();
   for (int c = threadIdx.x; c < nparts; c += blockDim.x) {
 #pragma unroll
     for (int sl = 0; sl < kGroups; ++sl) {
@@ -1075,40 +1209,17 @@ __global__ void __launch_bounds__(kThreads) k_final_small(const SmallPart* __res
   }
   __syncthreads();
   const int per = f.nacc + 1;
-  for (int p = warp; p < n * per; p += kThreads / 32) {
+  for (int p = warp; p < n * per; p += nwarps) {
     const int g = p / per, a = p % per;  // a == f.nacc: the row count
     const bool is_int = a == f.nacc || f.acc_is_int[a];
-    unsigned long long tot = 0;
-    for (int c0 = 0; c0 < nparts; c0 += kMergeChunk) {
-      const int m = nparts - c0 < kMergeChunk ? nparts - c0 : kMergeChunk;
-      for (int i0 = lane; i0 < m; i0 += 32 * kMergeUnroll) {
-        int sl[kMergeUnroll];
+    const unsigned long long tot = warp_sum_fixed(is_int, nparts, [&](int c) {
+      const int* rk = rank + static_cast<long long>(c) * kGroups;
+      int sl = -1;
 #pragma unroll
-        for (int u = 0; u < kMergeUnroll; ++u) {
-          const int i = i0 + 32 * u;
-          sl[u] = -1;
-          if (i < m) {
-            const int* rk = rank + static_cast<long long>(c0 + i) * kGroups;
-#pragma unroll
-            for (int q = 0; q < kGroups; ++q) sl[u] = rk[q] == g ? q : sl[u];
-          }
-        }
-        unsigned long long v[kMergeUnroll];
-#pragma unroll
-        for (int u = 0; u < kMergeUnroll; ++u) {
-          const int i = i0 + 32 * u;
-          v[u] = sl[u] < 0 ? 0ULL : (a == f.nacc ? parts[c0 + i].cnt[sl[u]] : parts[c0 + i].acc[sl[u]][a]);
-        }
-#pragma unroll
-        for (int u = 0; u < kMergeUnroll; ++u)
-          if (i0 + 32 * u < m) s_v[warp][i0 + 32 * u] = v[u];
-      }
-      __syncwarp();
-      if (lane == 0)
-        for (int i = 0; i < m; ++i) tot = add_acc(is_int, tot, s_v[warp][i]);
-      __syncwarp();
-    }
-    if (lane == 0) s_tot[g][a] = tot;
+      for (int q = 0; q < kGroups; ++q) sl = rk[q] == g ? q : sl;
+      return sl < 0 ? 0ULL : (a == f.nacc ? parts[c].cnt[sl] : parts[c].acc[sl][a]);
+    });
+    if ((threadIdx.x & 31) == 0) s_tot[g][a] = tot;
   }
   __syncthreads();
   void* kp[4] = {key_ptr0, key_ptr1, key_ptr2, key_ptr3};
@@ -2246,25 +2357,6 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
   return o.str();
 }
 
-// TQP_HOST_PROF=1: wall-clock marks of a fused unit's host side, one stderr
-// line per run (where the host time between the unit's kernels goes)
-struct HostProf {
-  bool on;
-  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> m;
-  HostProf() : on(std::getenv("TQP_HOST_PROF") != nullptr) { mark("start"); }
-  void mark(const char* what) {
-    if (on) m.emplace_back(what, std::chrono::steady_clock::now());
-  }
-  ~HostProf() {
-    if (!on || m.size() < 2) return;
-    std::string o = "[tqp host]";
-    for (size_t i = 1; i < m.size(); ++i)
-      o += std::string(" ") + m[i].first + "=" +
-           std::to_string(std::chrono::duration_cast<std::chrono::microseconds>(m[i].second - m[i - 1].second).count());
-    std::fprintf(stderr, "%s us\n", o.c_str());
-  }
-};
-
 struct Runner {
   PipeDesc P;
 
@@ -2794,7 +2886,12 @@ struct Runner {
     for (int a = 0; a < fs.nacc; ++a) fs.acc_is_int[a] = P_.accs[a].is_int;
     fs.nouts = static_cast<int>(P_.outs.size());
     if (fs.nouts > 16) return false;
-    for (int j = 0; j < fs.nouts; ++j) fs.outs[j] = {P_.outs[j].fn, P_.outs[j].acc, P_.outs[j].is_int ? 1 : 0};
+    for (int j = 0; j < fs.nouts; ++j) {
+      const OutDesc& d = P_.outs[j];
+      fs.outs[j] = {d.fn, d.acc, d.is_int ? 1 : 0, d.op, d.a, d.b};
+    }
+    if (P_.konst.size() > static_cast<size_t>(kMaxEpiConst)) return false;
+    for (size_t i = 0; i < P_.konst.size(); ++i) fs.konst[i] = P_.konst[i];
     return true;
   }
 
@@ -2818,7 +2915,7 @@ struct Runner {
     void* kp[4] = {nullptr, nullptr, nullptr, nullptr};
     for (size_t j = 0; j < P.outs.size(); ++j)
       if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = outs[j].data();
-    k_final_small<<<1, kThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
+    k_final_small<<<1, kFinalSmallThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
                                                 kp[0], kp[1], kp[2], kp[3], static_cast<int*>(rank->ptr), err + 2, err);
     c.count_launch();
     return -1;  // on the device (err[2]); read with the error flag
@@ -2983,6 +3080,10 @@ struct Runner {
     c.sync();
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
     if (nrows < 0) nrows = herr[2];
+    if (herr[0] && (herr[3] == kReasonEpiDivZero || herr[3] == kReasonEpiOverflow))
+      throw Error(TQP_ERR_EXEC, P.epi_step + (herr[3] == kReasonEpiDivZero ? ": arith: division by zero at row 0"
+                                                                            : ": arith: integer overflow at row 0"),
+                  0);
     if (!ok || herr[0]) {
       // the local path would re-run these steps per instruction; merged
       // partials cannot, so report what the exact path raises

@@ -10,6 +10,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 
 #include "tqp_b200.h"
 
@@ -61,6 +64,26 @@ const char* dtype_name(int dtype);  // reference names (tensor.cpp:5-13); STR8 -
 size_t dtype_size(int dtype);
 const char* logical_type_name(int lt);
 int physical_dtype(int lt);  // device physical dtype of a logical type
+
+// TQP_HOST_PROF=1: wall-clock marks of a host-side section (a fused unit,
+// an execution), one stderr line per section (where host time goes)
+struct HostProf {
+  bool on;
+  const char* tag;
+  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> m;
+  explicit HostProf(const char* t = "unit") : on(std::getenv("TQP_HOST_PROF") != nullptr), tag(t) { mark("start"); }
+  void mark(const char* what) {
+    if (on) m.emplace_back(what, std::chrono::steady_clock::now());
+  }
+  ~HostProf() {
+    if (!on || m.size() < 2) return;
+    std::string o = std::string("[tqp host ") + tag + "]";
+    for (size_t i = 1; i < m.size(); ++i)
+      o += std::string(" ") + m[i].first + "=" +
+           std::to_string(std::chrono::duration_cast<std::chrono::microseconds>(m[i].second - m[i - 1].second).count());
+    std::fprintf(stderr, "%s us\n", o.c_str());
+  }
+};
 
 struct Ctx {
   int device = 0;

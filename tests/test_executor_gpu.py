@@ -89,3 +89,40 @@ def test_profile_trace(ctx):
     ops = [e for e in trace if e["cat"] == "operator"]
     assert [e["name"] for e in ops] == ["scan#0", "filter#0", "aggregate#0", "project#0"]
     assert all(e["ph"] == "X" for e in trace)
+
+
+def test_q14_scalar_epilogue(ctx):
+    """Q14's final projection (100.00 * promo / total) runs inside the fused
+    unit's finalize kernel; with no qualifying row the exact path reports the
+    reference's division-by-zero error, fused or not, and the sharded merge
+    raises the same text."""
+    from paper_2209_04579_b200 import tqp
+    plan = json.loads((PLANS / "q14.opplan.json").read_text())
+    gold = load_tpch_golden()
+    tables = {n: tqp.Table.generate(n, gold["sf"], gold["seed"]) for n in ("lineitem", "part")}
+    fused = tqp.Executor(plan, fuse=True)
+    fused.set_timing(True)
+    got = as_numpy(fused.execute(tables))
+    assert not [k for k in fused.timings() if k.startswith("step:")], fused.timings()
+    compare_tables(got, gold["results"]["q14"])
+    exact = as_numpy(tqp.Executor(plan, fuse=False).execute(tables))
+    np.testing.assert_allclose(got[0][2], exact[0][2], rtol=1e-12)
+    # every price 0.0: both sums are 0.0 -> 100.00 * 0.0 / 0.0
+    host = tables["lineitem"].to_numpy()
+    cols = []
+    for name, lt in tables["lineitem"].columns():
+        a = host[name]
+        if name == "l_extendedprice":
+            a = np.zeros_like(a)
+        cols.append((name, lt, a))
+    empty = {"lineitem": tqp.Table.from_columns(cols), "part": tables["part"]}
+    msgs = []
+    for fuse in (True, False):
+        with pytest.raises(tqp.ExecError) as ei:
+            tqp.Executor(plan, fuse=fuse).execute(empty)
+        msgs.append(str(ei.value))
+    assert msgs[0] == msgs[1] and msgs[0].endswith("arith: division by zero at row 0"), msgs
+    ex = tqp.Executor(plan, fuse=True)
+    with pytest.raises(tqp.ExecError) as ei:
+        ex.finish([ex.execute_partial(empty)])
+    assert str(ei.value) == msgs[0]
