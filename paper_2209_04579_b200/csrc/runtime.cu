@@ -17,7 +17,13 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 DevBuf::~DevBuf() {
-  if (ptr && ctx) cudaFreeAsync(ptr, ctx->stream);
+  if (!ptr || !ctx) return;
+  if (bucket >= 0) {
+    std::lock_guard<std::mutex> lk(ctx->small_mu);
+    ctx->small_free[bucket].push_back(ptr);
+    return;
+  }
+  cudaFreeAsync(ptr, ctx->stream);
 }
 
 size_t dtype_size(int dtype) {
@@ -70,8 +76,32 @@ std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
   auto b = std::make_shared<DevBuf>();
   b->ctx = this;
   b->bytes = bytes;
-  if (bytes) TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream));
+  if (!bytes) return b;
+  if (bytes <= (size_t(256) << (kSmallBuckets - 1))) {
+    int i = 0;
+    while ((size_t(256) << i) < bytes) ++i;
+    b->bucket = i;
+    {
+      std::lock_guard<std::mutex> lk(small_mu);
+      if (!small_free[i].empty()) {
+        b->ptr = small_free[i].back();
+        small_free[i].pop_back();
+        return b;
+      }
+    }
+    TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, size_t(256) << i, pool, stream));
+    return b;
+  }
+  TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream));
   return b;
+}
+
+void Ctx::release_small() {
+  std::lock_guard<std::mutex> lk(small_mu);
+  for (auto& v : small_free) {
+    for (void* p : v) cudaFreeAsync(p, stream);
+    v.clear();
+  }
 }
 
 Tensor Ctx::alloc(int dtype, int64_t rows, int64_t cols) {

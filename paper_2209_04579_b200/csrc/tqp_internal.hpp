@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <mutex>
 #include <vector>
 #include <cstdlib>
 #include <cstdio>
@@ -39,6 +40,7 @@ struct DevBuf {
   Ctx* ctx = nullptr;
   void* ptr = nullptr;
   size_t bytes = 0;
+  int bucket = -1;  // >= 0: a small block of the context's host-side cache
   ~DevBuf();
 };
 
@@ -121,6 +123,17 @@ struct Ctx {
   long long* check_slot(bool* is_deferred);
   void check_deferred();
   std::atomic<int64_t> launches{0};
+  // Small blocks (error words, scalars, partials, output columns of a few
+  // rows) are recycled through a host-side free list per power-of-two size
+  // instead of a cudaMallocAsync/cudaFreeAsync pair each: a query makes a
+  // dozen of them and each driver call is host time between its kernels.
+  // Reuse follows the stream order exactly as cudaFreeAsync on `stream`
+  // does (a block freed after its last enqueued use is only handed to work
+  // enqueued later on the same stream).
+  static constexpr int kSmallBuckets = 9;  // 256 B << i, up to 64 KB
+  std::mutex small_mu;
+  std::vector<void*> small_free[kSmallBuckets];
+  void release_small();
 
   Tensor alloc(int dtype, int64_t rows, int64_t cols);
   std::shared_ptr<DevBuf> alloc_bytes(size_t bytes);
