@@ -245,7 +245,8 @@ tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names,
                                  tqp_status* st);
 /* Per-unit device time (CUDA events on the context stream, no host sync
  * until read): unit = fused pipeline name or "step:<kind>". JSON owned by
- * the library, valid until the next call on this thread. */
+ * the library, valid until the next call on this thread. on: 0 off, 1 units,
+ * steps and every kernel, 2 the fused fact-scan kernels only. */
 void tqp_executor_set_timing(tqp_executor* ex, int on);
 const char* tqp_executor_timings(tqp_executor* ex);
 void tqp_executor_reset_timings(tqp_executor* ex);

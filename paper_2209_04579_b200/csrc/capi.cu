@@ -523,7 +523,7 @@ extern "C" tqp_table* tqp_gen_table(tqp_ctx* ctx, const char* table, double sf, 
 }
 
 extern "C" void tqp_executor_set_timing(tqp_executor* ex, int on) {
-  if (ex) ex->ex->set_timing(on != 0);
+  if (ex) ex->ex->set_timing(on < 0 || on > 2 ? 1 : on);
 }
 
 extern "C" const char* tqp_executor_timings(tqp_executor* ex) {

@@ -412,7 +412,7 @@ Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots) {
     }
   }
   ctx_.sync();
-  if (timing_) collect_kernel_events();
+  if (ctx_.time_kernels) collect_kernel_events();
   return res;
 }
 
@@ -461,7 +461,7 @@ Partial Executor::execute_partial(const TableSet& tables) {
   }
   time_end(u.name + ":partial", ev);
   ctx_.sync();
-  if (timing_) collect_kernel_events();
+  if (ctx_.time_kernels) collect_kernel_events();
   return p;
 }
 

@@ -153,9 +153,12 @@ class Executor {
 
   // Device-time accounting per unit (fused pipeline or generic step) with
   // CUDA events on the context stream; no host synchronisation until read.
-  void set_timing(bool on) {
-    timing_ = on;
-    ctx_.time_kernels = on;
+  // mode 1: units, steps and every kernel; 2: the fused fact-scan kernels
+  // only (an event pair costs a few us of host time per launch, so a timed
+  // benchmark region records just the kernel its roofline is quoted on).
+  void set_timing(int mode) {
+    timing_ = mode == 1;
+    ctx_.time_kernels = mode;
   }
   std::string timings_json();
   void reset_timings();

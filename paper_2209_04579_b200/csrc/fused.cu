@@ -2762,7 +2762,7 @@ struct Runner {
       }
       ts.p = ps;
       void* args[] = {&ts};
-      cudaEvent_t ev = c.kernel_begin();
+      cudaEvent_t ev = c.kernel_begin(true);
       TQP_CUDA(cudaLaunchKernel(kernel, dim3(grid_), dim3(threads), args, smem, c.stream));
       c.kernel_end(tile_name, ev);
       TQP_CUDA(cudaGetLastError());

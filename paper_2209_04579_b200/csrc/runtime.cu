@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Runtime: context, stream-ordered device memory, tensor upload/download.
 // Replaces the reference's host-only storage (tensor.hpp:105-121) and the
 // thread-pool backend (backend.cpp:27-178) with one CUDA stream per context
@@ -116,7 +117,17 @@ Tensor Ctx::alloc(int dtype, int64_t rows, int64_t cols) {
   return t;
 }
 
-void Ctx::sync() { TQP_CUDA(cudaStreamSynchronize(stream)); }
+void Ctx::sync() {
+  static const bool poll = std::getenv("TQP_SYNC_POLL") != nullptr;  // experiment: busy-poll the stream
+  if (poll) {
+    cudaError_t e;
+    while ((e = cudaStreamQuery(stream)) == cudaErrorNotReady) {
+    }
+    TQP_CUDA(e);
+    return;
+  }
+  TQP_CUDA(cudaStreamSynchronize(stream));
+}
 
 void Ctx::reset_err() {
   TQP_CUDA(cudaMemcpyAsync(d_err, h_err + kPinnedErrInit, 3 * sizeof(long long), cudaMemcpyHostToDevice, stream));

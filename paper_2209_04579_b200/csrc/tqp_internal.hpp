@@ -146,7 +146,7 @@ struct Ctx {
 
   // optional per-kernel device timing (CUDA events on `stream`), drained by
   // the executor's timings
-  bool time_kernels = false;
+  int time_kernels = 0;  // 0 off, 1 every kernel, 2 fused fact-scan kernels only
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> kernel_events;
   // CSV file loader: pinned ring of upload buffers (csv.cu), kept for reuse
   unsigned char* csv_ring = nullptr;
@@ -167,8 +167,8 @@ struct Ctx {
   void give_event(cudaEvent_t e) {
     if (e) event_pool.push_back(e);
   }
-  cudaEvent_t kernel_begin() {
-    if (!time_kernels) return nullptr;
+  cudaEvent_t kernel_begin(bool fact_scan = false) {
+    if (!time_kernels || (time_kernels == 2 && !fact_scan)) return nullptr;
     cudaEvent_t e = take_event();
     cudaEventRecord(e, stream);
     return e;

@@ -673,8 +673,10 @@ class Executor:
             lib.tqp_executor_free(self.h)
             self.h = None
 
-    def set_timing(self, on: bool = True):
-        lib.tqp_executor_set_timing(self.h, 1 if on else 0)
+    def set_timing(self, on=True):
+        """True: units, steps and every kernel; "scan": the fused fact-scan
+        kernels only (cheapest: one event pair per query); False: off."""
+        lib.tqp_executor_set_timing(self.h, 2 if on == "scan" else (1 if on else 0))
 
     def timings(self) -> dict:
         """{unit: {"calls", "total_ms"}} measured with CUDA events."""

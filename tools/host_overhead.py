@@ -1,6 +1,6 @@
 """Per-query host overhead: wall time of Executor.execute vs the device time
 of its kernels (CUDA events recorded by the library), SF10 device tables."""
-import json, sys, time
+import json, os, sys, time
 from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
@@ -14,7 +14,7 @@ for q in ("q6", "q1", "q14", "q3"):
     for _ in range(5):
         ex.execute(tables)
     ctx.sync()
-    ex.set_timing(True)
+    ex.set_timing(os.environ.get("TQP_HO_TIMING", "1") == "1")
     ex.reset_timings()
     n = 50
     t0 = time.perf_counter()

@@ -1,7 +1,7 @@
 """SF100 on one B200: the four queries unsharded vs 8 order-aligned shards
 merged through execute_partial/finish; integers, keys and
 Q3's exact sums must be bit-identical, fp64 scan sums within 1e-9. Writes
-profiles/r1b_sf100_check.json. (The reference executor needs > 190 GB of host
+profiles/r1c_sf100_check.json. (The reference executor needs > 190 GB of host
 RAM at SF100, so parity there is by this property plus the SF1/SF10 goldens.)"""
 import json, sys, time
 from pathlib import Path
