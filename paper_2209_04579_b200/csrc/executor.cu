@@ -38,6 +38,16 @@ std::string json_escape(const std::string& s) {
   }
   return o;
 }
+void check_result_rows(Result& res) {
+  res.rows = res.cols.empty() ? 0 : res.cols[0].t.rows;
+  for (const auto& c : res.cols) {
+    if (c.t.rows != res.rows) {
+      throw Error(TQP_ERR_ENCODING, "table: column '" + c.name + "' has " + std::to_string(c.t.rows) +
+                                        " rows, expected " + std::to_string(res.rows));
+    }
+  }
+}
+
 }  // namespace
 
 bool op_from_name(const std::string& name, Op* out) {
@@ -347,10 +357,21 @@ void Executor::check_inputs(const TableSet& tables) const {
   }
 }
 
-Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
+Result Executor::execute(const TableSet& tables, ProfileTrace* trace, bool allow_defer) {
   HostProf hp("exec");
   check_inputs(tables);
   hp.mark("inputs");
+  // the last fused unit defers its check when only instruction-free steps
+  // follow it (its outputs are the result)
+  UnitPending pend;
+  int defer_unit = -1;
+  if (allow_defer && !trace && !units_.empty()) {
+    const FusedUnit& last = units_.back();
+    bool tail_free = true;
+    for (size_t q = last.last_step + 1; q < plan_.steps.size(); ++q)
+      if (!plan_.steps[q].instrs.empty()) tail_free = false;
+    if (tail_free) defer_unit = static_cast<int>(units_.size()) - 1;
+  }
   std::vector<std::optional<Tensor>> slots(plan_.num_slots);
   int64_t run_start = now_ns();
   size_t u = 0;
@@ -360,7 +381,7 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
       int64_t t0 = now_ns();
       cudaEvent_t ev;
       time_begin(&ev);
-      bool ok = unit.run(ctx_, slots, tables);
+      bool ok = unit.run(ctx_, slots, tables, static_cast<int>(u) - 1 == defer_unit ? &pend : nullptr);
       hp.mark("unit");
       if (ok) time_end(unit.name, ev);
       else ctx_.give_event(ev);
@@ -393,24 +414,28 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace) {
     hp.mark("step");
     ++s;
   }
-  Result r = collect_outputs(slots);
+  Result r = collect_outputs(slots, !pend.active);
   hp.mark("collect");
+  if (pend.active) {
+    // collect_outputs synchronised: the deferred word is on the host
+    long long herr[4];
+    std::memcpy(herr, ctx_.h_err + Ctx::kPinnedUnitErr, sizeof(herr));
+    if (herr[0] || herr[1]) return execute(tables, trace, false);  // the checked path decides (fallback / 8 slots)
+    const long long nrows = pend.nrows >= 0 ? pend.nrows : herr[2];
+    for (auto& col : r.cols)
+      if (std::find(pend.outs.begin(), pend.outs.end(), col.t.data()) != pend.outs.end()) col.t.rows = nrows;
+    check_result_rows(r);
+  }
   return r;
 }
 
-Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots) {
+Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows) {
   Result res;
   for (const auto& o : plan_.outputs) {
     if (!slots[o.slot]) exec_fail("internal: slot " + std::to_string(o.slot) + " read after release");
     res.cols.push_back({o.name, o.type, *slots[o.slot]});
   }
-  if (!res.cols.empty()) res.rows = res.cols[0].t.rows;
-  for (const auto& c : res.cols) {
-    if (c.t.rows != res.rows) {
-      throw Error(TQP_ERR_ENCODING, "table: column '" + c.name + "' has " + std::to_string(c.t.rows) +
-                                        " rows, expected " + std::to_string(res.rows));
-    }
-  }
+  if (check_rows) check_result_rows(res);
   ctx_.sync();
   if (ctx_.time_kernels) collect_kernel_events();
   return res;

@@ -121,6 +121,17 @@ struct PartRef {
 
 // A fused pipeline replaces a contiguous range of steps [first, last] and
 // writes the slots later instructions (or the plan outputs) read.
+// A fused unit whose outputs go straight to the result (only instruction-free
+// steps follow it) need not wait for its error/row-count word before the
+// executor moves on: the word is copied to pinned memory with the outputs
+// and checked at the result's one synchronisation (Executor::execute).
+struct UnitPending {
+  bool active = false;
+  long long nrows = -1;            // host-known row count, or -1: err[2]
+  std::vector<const void*> outs;   // device buffers of the unit's outputs
+  std::shared_ptr<DevBuf> err;     // the device word (kept until read)
+};
+
 struct FusedUnit {
   int first_step = 0, last_step = 0;
   std::string name;  // e.g. "scan_filter_aggregate"
@@ -128,7 +139,8 @@ struct FusedUnit {
   // returns false when the data violates the fused path's preconditions
   // (e.g. a fixed-point overflow or a non-unique build key); the executor
   // then runs the covered steps through the per-instruction path.
-  std::function<bool(Ctx&, std::vector<std::optional<Tensor>>& slots, const TableSet& tables)> run;
+  // pend != nullptr: deferred check (see UnitPending); returns true
+  std::function<bool(Ctx&, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, UnitPending* pend)> run;
   // sharded runs: phase 1 writes this shard's partial state (false: the data
   // violates the preconditions); phase 2 merges the parts of every shard
   std::function<bool(Ctx&, const TableSet& tables, Partial* out)> partial;
@@ -138,7 +150,7 @@ struct FusedUnit {
 class Executor {
  public:
   Executor(Ctx& ctx, Plan plan, unsigned flags);
-  Result execute(const TableSet& tables, ProfileTrace* trace = nullptr);
+  Result execute(const TableSet& tables, ProfileTrace* trace = nullptr, bool allow_defer = true);
 
   // Sharded execution: every shard runs phase 1 over its
   // rows of the fact table; the concatenated partials of all shards (rank
@@ -181,7 +193,7 @@ class Executor {
                 int64_t run_start);
   void release_after(int s, std::vector<std::optional<Tensor>>& slots);
   void check_inputs(const TableSet& tables) const;
-  Result collect_outputs(std::vector<std::optional<Tensor>>& slots);
+  Result collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows = true);
 
   Ctx& ctx_;
   Plan plan_;

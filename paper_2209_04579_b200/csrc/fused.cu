@@ -2360,14 +2360,14 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
 struct Runner {
   PipeDesc P;
 
-  bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables) const {
-    return run(c, &slots, tables, nullptr);
+  bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, UnitPending* pend) const {
+    return run(c, &slots, tables, nullptr, false, pend);
   }
 
   // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
   // narrow: the 8-slot small-group kernel only (after a 4-slot overflow)
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
-           bool narrow = false) const {
+           bool narrow = false, UnitPending* pend = nullptr) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
@@ -2854,6 +2854,18 @@ struct Runner {
     }
     long long herr[4] = {0, 0, 0, 0};
     hp.mark("launched");
+    if (pend && !po) {
+      // deferred: the word travels with the outputs and is checked at the
+      // result's synchronisation; rows are patched there when device-side
+      TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedUnitErr, err, 32, cudaMemcpyDeviceToHost, c.stream));
+      pend->active = true;
+      pend->nrows = nrows;
+      pend->err = err_buf;
+      pend->outs.clear();
+      for (auto& o : outs) pend->outs.push_back(o.data());
+      for (size_t i = 0; i < P.final_slots.size(); ++i) (*slots)[P.final_slots[i]] = outs[P.final_cols[i]];
+      return true;
+    }
     TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedRead, err, 32, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     hp.mark("sync");
@@ -3147,7 +3159,9 @@ std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
     u.name = std::string("fused_") + (P.probes.empty() ? "scan_" : "probe_") + mode + (P.topk ? "_topk" : "");
     u.explain = ex.str();
     auto R = std::make_shared<Runner>(Runner{P});
-    u.run = [R](Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& t) { return (*R)(c, slots, t); };
+    u.run = [R](Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& t, UnitPending* pend) {
+      return (*R)(c, slots, t, pend);
+    };
     u.partial = [R](Ctx& c, const TableSet& t, Partial* out) { return R->run(c, nullptr, t, out); };
     const std::string where = plan.steps[P.last_step].id;
     u.finish = [R, where](Ctx& c, std::vector<std::optional<Tensor>>& slots, const std::vector<PartRef>& parts) {

@@ -104,6 +104,7 @@ struct Ctx {
   static constexpr int kPinnedMinMaxPairs = 64;
   static constexpr int kPinnedDeferInit = 192;  // kMaxDeferred x {INT64_MAX, 0, 0, 0}
   static constexpr int kPinnedRead = 256;      // 256 words of readback
+  static constexpr int kPinnedUnitErr = 480;   // a deferred fused unit's error words (4)
   // Deferred checks (executor steps only): an instruction whose one host
   // interaction is its error check (arith's division by zero / overflow)
   // gets its own device error slot instead of a round trip; the executor
