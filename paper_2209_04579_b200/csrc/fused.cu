@@ -2371,9 +2371,6 @@ struct Runner {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
-    auto err_buf = c.alloc_bytes(32);
-    long long* err = static_cast<long long*>(err_buf->ptr);
-    TQP_CUDA(cudaMemsetAsync(err, 0, 32, c.stream));
     std::vector<Probe> built(P.builds.size());
     std::vector<std::shared_ptr<DevBuf>> keep;
     std::vector<long long> build_range(P.builds.size(), 0);
@@ -2434,6 +2431,27 @@ struct Runner {
       }
     }
     hp.mark("ranges");
+    // one zeroed arena for the unit's small state - the error words, every
+    // build's presence bitmap and the touched-group bitmap - so one memset
+    // replaces one per buffer (each is host time between the unit's kernels)
+    std::vector<size_t> bm_off(nb, 0);
+    size_t arena = 256, touched_off = 0;
+    for (size_t bi = 0; bi < nb; ++bi) {
+      const long long n = bind_table(tables, P.builds[bi].table)->rows;
+      const long long range = n ? mm[2 * bi + 1] - mm[2 * bi] + 1 : 1;
+      if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
+      bm_off[bi] = arena;
+      arena += (sizeof(unsigned) * static_cast<size_t>((range + 31) / 32) + 255) & ~size_t(255);
+      if (P.mode == MODE_BUILDGRP && P.group_probe >= 0 && P.group_probe < static_cast<int>(P.probes.size()) &&
+          P.probes[P.group_probe].build == static_cast<int>(bi)) {
+        touched_off = arena;
+        arena += (sizeof(unsigned) * static_cast<size_t>((range + 31) / 32 + 1) + 255) & ~size_t(255);
+      }
+    }
+    auto err_buf = c.alloc_bytes(arena);
+    TQP_CUDA(cudaMemsetAsync(err_buf->ptr, 0, arena, c.stream));
+    long long* err = static_cast<long long*>(err_buf->ptr);
+    unsigned char* arena_p = static_cast<unsigned char*>(err_buf->ptr);
     for (size_t bi = 0; bi < P.builds.size(); ++bi) {
       const BuildDesc& B = P.builds[bi];
       const Table* tab = bind_table(tables, B.table);
@@ -2454,11 +2472,7 @@ struct Runner {
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
       build_range[bi] = range;
-      const long long bm_words = (range + 31) / 32;
-      auto bitmap = c.alloc_bytes(sizeof(unsigned) * bm_words);
-      TQP_CUDA(cudaMemsetAsync(bitmap->ptr, 0, sizeof(unsigned) * bm_words, c.stream));
-      keep.push_back(bitmap);
-      bs.bitmap = static_cast<unsigned*>(bitmap->ptr);
+      bs.bitmap = reinterpret_cast<unsigned*>(arena_p + bm_off[bi]);
       bs.err = err;
       bool ok = true;
       bs.key = {key->t.data(), OT_I64, -1};
@@ -2813,10 +2827,8 @@ struct Runner {
       ps.gacc = grec_p + 1;
       ps.gstride = grec_words;
       ps.group_probe = P.group_probe;
-      auto touched = c.alloc_bytes(sizeof(unsigned) * ((ngroups + 31) / 32 + 1));
-      TQP_CUDA(cudaMemsetAsync(touched->ptr, 0, touched->bytes, c.stream));
-      keep.push_back(touched);
-      ps.touched = static_cast<unsigned*>(touched->ptr);
+      if (!touched_off) return false;
+      ps.touched = reinterpret_cast<unsigned*>(arena_p + touched_off);
       launch_tile(kfn, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
       gs.f = fs;
@@ -2977,8 +2989,8 @@ struct Runner {
       auto bn = c.alloc_bytes(sizeof(int) * 2 * blocks + 16);
       int* bnval = static_cast<int*>(bn->ptr);
       int* bnc = bnval + blocks;
-      unsigned* ticket = reinterpret_cast<unsigned*>(bnc + blocks);
-      TQP_CUDA(cudaMemsetAsync(ticket, 0, 4, c.stream));
+      // the last-block ticket lives after the error words (zeroed with them)
+      unsigned* ticket = reinterpret_cast<unsigned*>(err + 4);
       kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bval->ptr), bnval,
                                                   static_cast<unsigned long long*>(bck->ptr),
                                                   static_cast<unsigned*>(bcg->ptr), bnc, ticket, err + 2, err);
@@ -3044,9 +3056,9 @@ struct Runner {
                                  sizeof(unsigned long long) * nrec[i] * want_words, cudaMemcpyDeviceToDevice, c.stream));
       off += nrec[i];
     }
-    auto err_buf = c.alloc_bytes(32);
+    auto err_buf = c.alloc_bytes(64);  // error words + the top-k ticket
     long long* err = static_cast<long long*>(err_buf->ptr);
-    TQP_CUDA(cudaMemsetAsync(err, 0, 32, c.stream));
+    TQP_CUDA(cudaMemsetAsync(err, 0, 64, c.stream));
     std::vector<Tensor> outs(P.outs.size());
     long long nrows = 0;
     bool ok = true;
