@@ -282,6 +282,7 @@ def main():
         ctx.sync()
         torch.cuda.synchronize()
     launches = ctx.launches - launches0
+    fallbacks = sum(ex.fallbacks for ex in execs.values())
     total_ms = start.elapsed_time(end)
     if dist:
         t = torch.tensor([total_ms], device=red_dev)
@@ -367,7 +368,7 @@ def main():
                                        f"whole per rank, partials all-gathered over NCCL" if world > 1
                                        else "single GPU")},
             "queries": queries, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": launches, "csv_load": csv_leg,
+            "clocks": clocks.summary(), "gpu_launches": launches, "fused_fallbacks": fallbacks, "csv_load": csv_leg,
         }
         print(json.dumps(line))
     if dist:

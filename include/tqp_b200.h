@@ -269,6 +269,10 @@ tqp_result* tqp_executor_finish(tqp_executor* ex, const void* const* parts, cons
 
 /* Description of the fused pipelines chosen for this plan (JSON). */
 const char* tqp_executor_explain(tqp_executor* ex);
+/* Fused units that met data outside their contract (duplicate build keys,
+ * too many groups, fixed-point or int64 range, ...) and ran the exact
+ * per-instruction path instead, since the executor was created. */
+int64_t tqp_executor_fallbacks(tqp_executor* ex);
 void tqp_executor_free(tqp_executor* ex);
 void tqp_free_str(char* s);
 

@@ -487,6 +487,7 @@ int tqp_executor_shardable(tqp_executor* ex, const char** why) {
 }
 
 const char* tqp_executor_explain(tqp_executor* ex) { return ex ? ex->explain.c_str() : ""; }
+int64_t tqp_executor_fallbacks(tqp_executor* ex) { return ex ? ex->ex->fallbacks() : 0; }
 void tqp_executor_free(tqp_executor* ex) { delete ex; }
 void tqp_free_str(char* s) { std::free(s); }
 

@@ -385,6 +385,7 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace, bool allow
       hp.mark("unit");
       if (ok) time_end(unit.name, ev);
       else ctx_.give_event(ev);
+      if (!ok) ++fallbacks_;
       if (ok) {
         if (trace) {
           ctx_.sync();

@@ -173,6 +173,9 @@ class Executor {
     ctx_.time_kernels = mode;
   }
   std::string timings_json();
+  // fused units that met data outside their contract and ran the exact
+  // per-instruction path instead (since creation)
+  int64_t fallbacks() const { return fallbacks_; }
   void reset_timings();
 
  private:
@@ -186,6 +189,7 @@ class Executor {
   void drain_timings();
   void collect_kernel_events();
   bool timing_ = false;
+  int64_t fallbacks_ = 0;
   std::map<std::string, UnitTiming> timings_;
 
   Tensor exec_instr(const Instr& in, std::vector<std::optional<Tensor>>& slots, const TableSet& tables);

@@ -136,6 +136,7 @@ def _load() -> C.CDLL:
         "tqp_executor_execute": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, S]),
         "tqp_executor_profile": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, C.POINTER(C.c_void_p), S]),
         "tqp_executor_explain": (C.c_char_p, [P]), "tqp_executor_free": (None, [P]),
+        "tqp_executor_fallbacks": (I64_, [P]),
         "tqp_executor_set_timing": (None, [P, I]), "tqp_executor_timings": (C.c_char_p, [P]),
         "tqp_executor_reset_timings": (None, [P]),
         "tqp_executor_shardable": (I, [P, C.POINTER(C.c_char_p)]),
@@ -681,6 +682,11 @@ class Executor:
     def timings(self) -> dict:
         """{unit: {"calls", "total_ms"}} measured with CUDA events."""
         return json.loads(lib.tqp_executor_timings(self.h).decode())
+
+    @property
+    def fallbacks(self) -> int:
+        """Fused units that ran the exact per-instruction path instead."""
+        return int(lib.tqp_executor_fallbacks(self.h))
 
     def reset_timings(self):
         lib.tqp_executor_reset_timings(self.h)

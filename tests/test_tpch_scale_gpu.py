@@ -41,8 +41,12 @@ def test_tpch_matches_reference_at_scale(ctx, sf, fuse):
     tables = generate(tqp, sf)
     assert tables["lineitem"].rows == gold["lineitem_rows"]
     for q in QUERIES:
-        got = tqp.Executor(plan(q), fuse=fuse).execute(tables).to_numpy()
+        ex = tqp.Executor(plan(q), fuse=fuse)
+        got = ex.execute(tables).to_numpy()
         compare_tables(got, gold["results"][q])
+        # the fused path itself must produce it: an exact-path fallback would
+        # pass the comparison and hide a fused-kernel defect
+        assert ex.fallbacks == 0, q
     del tables
     ctx.sync()
 
