@@ -345,7 +345,9 @@ def main():
     # e2e: host (pinned) columns -> device -> four queries -> result to host
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev)
+        e2e = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev, encoded=True)
+        e2e["raw_layout"] = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev,
+                                    encoded=False)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -409,19 +411,30 @@ def run_csv_leg(tqp, ctx, sf):
             "reference": "tensql::load_csv (one host thread), same file"}
 
 
-def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev="cuda"):
+def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev="cuda", encoded=True):
     """Same suite through the public C ABI with HOST inputs: every step
     uploads the columns from pinned host memory, runs the queries and reads
-    the results back; all inside the timed region."""
+    the results back; all inside the timed region. encoded: the host columns
+    are in the compressed columnar format (tqp_codec_encode, once, when the
+    host copy is made - the loader's storage format); each step copies the
+    encoded bytes and decodes them on the device (tqp_tensor_from_encoded).
+    Otherwise the reference's layout is copied as is (tqp_tensor_from_host)."""
     host = {}
     h2d = 0
+    codecs = {}
     for name, t in tables.items():
         cols = []
         for cname, lt in t.columns():
             dev = t.column(cname)
             arr = dev.numpy(widen_strings=False)
-            pin = torch.from_numpy(arr).pin_memory()
-            cols.append((cname, lt, dev.dtype, pin))
+            if encoded:
+                codec, payload = tqp.encode_column(arr, dev.dtype)
+                pin = torch.from_numpy(payload).pin_memory()
+                codecs[f"{name}.{cname}"] = f"{codec.name}{codec.width if codec.name in ('for', 'dec') else ''}"
+                cols.append((cname, lt, dev.dtype, arr.shape, codec, pin))
+            else:
+                pin = torch.from_numpy(arr).pin_memory()
+                cols.append((cname, lt, dev.dtype, arr.shape, None, pin))
             h2d += pin.numel() * pin.element_size()
         host[name] = cols
 
@@ -429,12 +442,15 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red
         out = {}
         for name, cols in host.items():
             tab = tqp.Table.create(ctx)
-            for cname, lt, dt, pin in cols:
-                st = tqp.Status()
-                h = tqp.lib.tqp_tensor_from_host(ctx.h, dt, pin.shape[0], pin.shape[1], pin.data_ptr(),
-                                                 tqp.C.byref(st))
-                tqp._check(st, bool(h))
-                tab.add_column(cname, lt, tqp.Tensor(h, ctx))
+            for cname, lt, dt, shape, codec, pin in cols:
+                if codec is not None:
+                    t = tqp.Tensor.from_encoded(codec, pin, dt, shape[0], shape[1], ctx=ctx)
+                else:
+                    st = tqp.Status()
+                    h = tqp.lib.tqp_tensor_from_host(ctx.h, dt, shape[0], shape[1], pin.data_ptr(), tqp.C.byref(st))
+                    tqp._check(st, bool(h))
+                    t = tqp.Tensor(h, ctx)
+                tab.add_column(cname, lt, t)
             out[name] = tab
         return out
 
@@ -468,9 +484,15 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red
         t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    return {"value": len(QUERIES) * L_total / (ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
-            "path": "pinned host columns -> tqp_tensor_from_host (C ABI) -> tqp_executor_execute x4 -> results to host"}
+    out = {"value": len(QUERIES) * L_total / (ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
+    if encoded:
+        out["path"] = ("pinned host columns in the compressed columnar format -> tqp_tensor_from_encoded (C ABI: "
+                       "H2D of the encoded bytes + device decode) -> tqp_executor_execute x4 -> results to host")
+        out["codecs"] = codecs
+    else:
+        out["path"] = "pinned host columns (reference layout) -> tqp_tensor_from_host (C ABI) -> tqp_executor_execute x4 -> results to host"
+    return out
 
 
 if __name__ == "__main__":

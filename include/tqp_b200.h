@@ -112,6 +112,45 @@ tqp_tensor* tqp_tensor_from_host_utf8_i32(tqp_ctx* ctx, int64_t rows, int64_t co
 /* Wraps an existing device buffer (copied; the caller keeps ownership). */
 tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols,
                                    const void* dev, tqp_status* st);
+
+/* ---- compressed columnar host format (the loader) -------
+ * The reference loads columns only from CSV text (columnar.cpp:453-527).
+ * This binary host format keeps a column losslessly compressed in (pinned)
+ * host memory, so an upload moves fewer bytes over PCIe and the device
+ * decodes at HBM speed. Codecs (one per column, chosen by tqp_codec_encode):
+ *   RAW   the reference layout as is (any dtype / shape)
+ *   FOR   int64/date vector: v = base + scale * u, u unsigned of `width`
+ *         bytes (frame of reference; scale = gcd of v - min, e.g. one day
+ *         in ns for dates)
+ *   DICT  float64 vector with <= 256 distinct bit patterns: dict_n patterns
+ *         (8 B each, ascending) then one byte per row
+ *   DEC   float64 vector whose every value is exactly (base + u) / scale
+ *         for an integer u of `width` bytes and scale = 10^d (d <= 4): the
+ *         decode (an IEEE division) reproduces the original bits; -0.0,
+ *         NaN and inf excluded.
+ * Lossless by construction: the encoder verifies every value. */
+typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3 } tqp_codec_kind;
+typedef struct {
+  int32_t codec;  /* tqp_codec_kind */
+  int32_t width;  /* FOR / DEC: bytes per code (1, 2, 4); DICT: 1 */
+  int64_t base;   /* FOR: value of code 0; DEC: integer numerator of code 0 */
+  int64_t scale;  /* FOR: value step of one code; DEC: the denominator 10^d */
+  int32_t dict_n; /* DICT: dictionary entries at the start of the payload */
+  int32_t reserved;
+} tqp_codec;
+/* Upper bound of an encoded payload's bytes (the RAW size plus a dictionary). */
+int64_t tqp_codec_bound(int dtype, int64_t rows, int64_t cols);
+/* Encodes a host column (device dtype layout: int64/date and float64 8 B
+ * per row, STR8 one byte per byte) into `out` (cap bytes); returns the
+ * payload bytes and fills *codec, or -1 (status set). Runs on the host's
+ * cores. */
+int64_t tqp_codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, void* out, int64_t cap,
+                         tqp_codec* codec, tqp_status* st);
+/* Uploads an encoded payload (pinned host memory for an asynchronous copy)
+ * and decodes it on the device into a new tensor of the original dtype and
+ * shape, bit-identical to the encoded column. */
+tqp_tensor* tqp_tensor_from_encoded(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols, const tqp_codec* codec,
+                                    const void* payload, int64_t bytes, tqp_status* st);
 int tqp_tensor_dtype(const tqp_tensor* t);
 int64_t tqp_tensor_rows(const tqp_tensor* t);
 int64_t tqp_tensor_cols(const tqp_tensor* t);

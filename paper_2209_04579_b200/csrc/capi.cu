@@ -164,6 +164,31 @@ tqp_tensor* tqp_tensor_from_host_utf8_i32(tqp_ctx* ctx, int64_t rows, int64_t co
   });
 }
 
+int64_t tqp_codec_bound(int dtype, int64_t rows, int64_t cols) {
+  if (dtype < TQP_BOOL || dtype > TQP_STR8 || rows < 0 || cols < 1) return -1;
+  return tqp::codec_bound(dtype, rows, cols);
+}
+
+int64_t tqp_codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, void* out, int64_t cap,
+                         tqp_codec* codec, tqp_status* st) {
+  int64_t n = -1;
+  guard(st, [&] {
+    if (!out || !codec || (!host && rows * cols)) throw Error(TQP_ERR_ARG, "codec: null argument");
+    n = tqp::codec_encode(dtype, rows, cols, host, out, cap, codec);
+    return 0;
+  });
+  return n;
+}
+
+tqp_tensor* tqp_tensor_from_encoded(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols, const tqp_codec* codec,
+                                    const void* payload, int64_t bytes, tqp_status* st) {
+  return guard(st, [&] {
+    if (!codec || (!payload && bytes)) throw Error(TQP_ERR_ARG, "codec: null argument");
+    if (dtype < TQP_BOOL || dtype > TQP_STR8) throw Error(TQP_ERR_ARG, "bad dtype");
+    return wrap(tqp::decode_column(C_(ctx), dtype, rows, cols, *codec, payload, bytes));
+  });
+}
+
 tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols, const void* dev,
                                    tqp_status* st) {
   return guard(st, [&] {

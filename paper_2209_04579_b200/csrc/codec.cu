@@ -1,0 +1,290 @@
+// Compressed columnar host format (tqp_b200.h, "compressed columnar host
+// format"): a lossless per-column codec chosen on the host and decoded on
+// the device. The reference's loader only parses CSV text
+// (proj/src/columnar.cpp:453-527); SURVEY.md 8(f)1 names a binary columnar
+// format with pinned-staging DMA as the next step of the loader, so that an
+// end-to-end run (host columns -> device -> query) is not bound by moving the
+// reference's 8-byte values over PCIe.
+//
+// Encoding runs once per column (when the host copy is made), on the host's
+// cores; every value is verified, so a column that does not fit a codec
+// exactly stays RAW. Decoding is one grid-stride kernel per column.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "device.cuh"
+#include "tqp_internal.hpp"
+
+namespace tqp {
+namespace {
+
+// ---- host: parallel helpers --------------------------------------------------
+int host_threads(int64_t n) {
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(hw, n / (1 << 20) + 1)));
+}
+
+template <typename F>
+void parallel_chunks(int64_t n, F&& f) {  // f(thread, lo, hi)
+  const int nt = host_threads(n);
+  if (nt == 1) {
+    f(0, 0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+    th.emplace_back([&f, t, lo, hi] { f(t, lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+int width_for(uint64_t max_code) {
+  if (max_code < (1ull << 8)) return 1;
+  if (max_code < (1ull << 16)) return 2;
+  if (max_code < (1ull << 32)) return 4;
+  return 0;
+}
+
+void put_code(void* out, int width, int64_t i, uint64_t u) {
+  switch (width) {
+    case 1: static_cast<uint8_t*>(out)[i] = static_cast<uint8_t>(u); break;
+    case 2: static_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(u); break;
+    default: static_cast<uint32_t*>(out)[i] = static_cast<uint32_t>(u); break;
+  }
+}
+
+// ---- host: codecs --------------------------------------------------------------
+// FOR over int64: base = min, scale = gcd of (v - min) (unsigned), codes of
+// the narrowest width that holds (max - min) / scale. Returns payload bytes
+// or -1 when no width below 8 bytes fits.
+int64_t try_for(const int64_t* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
+  if (n == 0) return -1;
+  const int nt = host_threads(n);
+  std::vector<int64_t> mn(nt, INT64_MAX), mx(nt, INT64_MIN);
+  parallel_chunks(n, [&](int t, int64_t lo, int64_t hi) {
+    int64_t a = INT64_MAX, b = INT64_MIN;
+    for (int64_t i = lo; i < hi; ++i) {
+      a = std::min(a, v[i]);
+      b = std::max(b, v[i]);
+    }
+    mn[t] = a;
+    mx[t] = b;
+  });
+  const int64_t lo = *std::min_element(mn.begin(), mn.end()), hi = *std::max_element(mx.begin(), mx.end());
+  const uint64_t range = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
+  std::vector<uint64_t> g(nt, 0);
+  parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
+    uint64_t x = 0;
+    for (int64_t i = a; i < b && x != 1; ++i) {
+      const uint64_t d = static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(lo);
+      if (x == 0 ? d != 0 : d % x != 0) x = std::gcd(x, d);
+    }
+    g[t] = x;
+  });
+  uint64_t scale = 0;
+  for (uint64_t x : g) scale = std::gcd(scale, x);
+  if (scale == 0) scale = 1;  // every value equal
+  const int w = width_for(range / scale);
+  if (!w || w * n > cap) return -1;
+  parallel_chunks(n, [&](int, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) put_code(out, w, i, (static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(lo)) / scale);
+  });
+  c->codec = TQP_CODEC_FOR;
+  c->width = w;
+  c->base = lo;
+  c->scale = static_cast<int64_t>(scale);
+  return w * n;
+}
+
+// DICT over float64 bit patterns (<= 256 distinct).
+int64_t try_dict(const uint64_t* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
+  if (n == 0) return -1;
+  const int nt = host_threads(n);
+  std::vector<std::vector<uint64_t>> sets(nt);
+  std::vector<char> over(nt, 0);
+  parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
+    std::vector<uint64_t>& s = sets[t];
+    uint64_t last = 0;
+    bool have = false;
+    for (int64_t i = a; i < b; ++i) {
+      if (have && v[i] == last) continue;
+      if (std::find(s.begin(), s.end(), v[i]) == s.end()) {
+        if (s.size() >= 256) {
+          over[t] = 1;
+          return;
+        }
+        s.push_back(v[i]);
+      }
+      last = v[i];
+      have = true;
+    }
+  });
+  for (char o : over)
+    if (o) return -1;
+  std::vector<uint64_t> dict;
+  for (auto& s : sets) dict.insert(dict.end(), s.begin(), s.end());
+  std::sort(dict.begin(), dict.end());
+  dict.erase(std::unique(dict.begin(), dict.end()), dict.end());
+  if (dict.size() > 256) return -1;
+  const int64_t bytes = 8 * static_cast<int64_t>(dict.size()) + n;
+  if (bytes > cap) return -1;
+  std::memcpy(out, dict.data(), 8 * dict.size());
+  uint8_t* codes = static_cast<uint8_t*>(out) + 8 * dict.size();
+  parallel_chunks(n, [&](int, int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i)
+      codes[i] = static_cast<uint8_t>(std::lower_bound(dict.begin(), dict.end(), v[i]) - dict.begin());
+  });
+  c->codec = TQP_CODEC_DICT;
+  c->width = 1;
+  c->dict_n = static_cast<int32_t>(dict.size());
+  return bytes;
+}
+
+// DEC over float64: v == (double)k / 10^d exactly for an integer k, every row.
+int64_t try_dec(const double* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
+  if (n == 0) return -1;
+  const int nt = host_threads(n);
+  for (int d : {0, 1, 2, 3, 4}) {  // the first exact one has the smallest code range
+    const double scale = std::pow(10.0, d);
+    std::vector<int64_t> mn(nt, INT64_MAX), mx(nt, INT64_MIN);
+    std::vector<char> bad(nt, 0);
+    parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
+      int64_t lo = INT64_MAX, hi = INT64_MIN;
+      for (int64_t i = a; i < b; ++i) {
+        const double x = v[i];
+        if (!std::isfinite(x) || std::fabs(x) * scale >= 9.0e15) {
+          bad[t] = 1;
+          return;
+        }
+        const int64_t k = std::llrint(x * scale);
+        const double back = static_cast<double>(k) / scale;
+        uint64_t bx, bb;
+        std::memcpy(&bx, &x, 8);
+        std::memcpy(&bb, &back, 8);
+        if (bx != bb) {
+          bad[t] = 1;
+          return;
+        }
+        lo = std::min(lo, k);
+        hi = std::max(hi, k);
+      }
+      mn[t] = lo;
+      mx[t] = hi;
+    });
+    if (std::find(bad.begin(), bad.end(), 1) != bad.end()) continue;
+    const int64_t lo = *std::min_element(mn.begin(), mn.end()), hi = *std::max_element(mx.begin(), mx.end());
+    const int w = width_for(static_cast<uint64_t>(hi - lo));
+    if (!w || w * n > cap) return -1;
+    parallel_chunks(n, [&](int, int64_t a, int64_t b) {
+      for (int64_t i = a; i < b; ++i) put_code(out, w, i, static_cast<uint64_t>(std::llrint(v[i] * scale) - lo));
+    });
+    c->codec = TQP_CODEC_DEC;
+    c->width = w;
+    c->base = lo;
+    c->scale = static_cast<int64_t>(scale);
+    return w * n;
+  }
+  return -1;
+}
+
+// ---- device: decoders ------------------------------------------------------------
+template <typename U>
+__global__ void k_decode_for(const U* __restrict__ codes, int64_t n, int64_t base, int64_t scale, int64_t* __restrict__ out) {
+  for (int64_t i = gtid(); i < n; i += gstride())
+    out[i] = static_cast<int64_t>(static_cast<uint64_t>(base) + static_cast<uint64_t>(scale) * static_cast<uint64_t>(codes[i]));
+}
+
+template <typename U>
+__global__ void k_decode_dec(const U* __restrict__ codes, int64_t n, int64_t base, double scale, double* __restrict__ out) {
+  for (int64_t i = gtid(); i < n; i += gstride())
+    out[i] = __ddiv_rn(static_cast<double>(base + static_cast<int64_t>(codes[i])), scale);
+}
+
+__global__ void k_decode_dict(const unsigned long long* __restrict__ dict, int nd, const uint8_t* __restrict__ codes,
+                              int64_t n, unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long s_dict[256];
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) s_dict[i] = dict[i];
+  __syncthreads();
+  for (int64_t i = gtid(); i < n; i += gstride()) out[i] = s_dict[codes[i]];
+}
+
+}  // namespace
+
+int64_t codec_bound(int dtype, int64_t rows, int64_t cols) {
+  return rows * cols * static_cast<int64_t>(dtype_size(dtype)) + 8 * 256 + 64;
+}
+
+int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, void* out, int64_t cap, tqp_codec* c) {
+  if (rows < 0 || cols < 1 || dtype < TQP_BOOL || dtype > TQP_STR8) throw Error(TQP_ERR_ARG, "codec: bad column shape");
+  *c = tqp_codec{};
+  c->codec = TQP_CODEC_RAW;
+  const int64_t raw = rows * cols * static_cast<int64_t>(dtype_size(dtype));
+  // each attempt writes straight into `out`; a failed one leaves it to the
+  // next, and RAW (below) overwrites whatever a failed attempt wrote
+  if (cols == 1 && rows > 0 && dtype == TQP_I64) {
+    const int64_t b = try_for(static_cast<const int64_t*>(host), rows, out, std::min(cap, raw - 1), c);
+    if (b >= 0) return b;
+  }
+  if (cols == 1 && rows > 0 && dtype == TQP_F64) {
+    // DICT first (8 B x entries + 1 B per row); DEC can only beat it at one
+    // byte per row too, so it is tried when DICT does not apply
+    int64_t b = try_dict(static_cast<const uint64_t*>(host), rows, out, std::min(cap, raw - 1), c);
+    if (b >= 0) return b;
+    b = try_dec(static_cast<const double*>(host), rows, out, std::min(cap, raw - 1), c);
+    if (b >= 0) return b;
+  }
+  *c = tqp_codec{};
+  c->codec = TQP_CODEC_RAW;
+  if (raw > cap) throw Error(TQP_ERR_ARG, "codec: output buffer too small");
+  if (raw) std::memcpy(out, host, static_cast<size_t>(raw));
+  return raw;
+}
+
+Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_codec& k, const void* payload,
+                     int64_t bytes) {
+  if (rows < 0 || cols < 1) throw Error(TQP_ERR_ARG, "codec: bad column shape");
+  if (k.codec == TQP_CODEC_RAW) {
+    if (bytes != rows * cols * static_cast<int64_t>(dtype_size(dtype))) throw Error(TQP_ERR_ARG, "codec: payload size");
+    return upload(c, dtype, rows, cols, payload);
+  }
+  const bool vec = cols == 1;
+  const bool w_ok = k.width == 1 || k.width == 2 || k.width == 4;
+  if (k.codec == TQP_CODEC_FOR && !(vec && dtype == TQP_I64 && w_ok && bytes == k.width * rows))
+    throw Error(TQP_ERR_ARG, "codec: bad FOR column");
+  if (k.codec == TQP_CODEC_DEC && !(vec && dtype == TQP_F64 && w_ok && bytes == k.width * rows && k.scale > 0))
+    throw Error(TQP_ERR_ARG, "codec: bad DEC column");
+  if (k.codec == TQP_CODEC_DICT &&
+      !(vec && dtype == TQP_F64 && k.dict_n >= 1 && k.dict_n <= 256 && bytes == 8LL * k.dict_n + rows))
+    throw Error(TQP_ERR_ARG, "codec: bad DICT column");
+  if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_DEC) throw Error(TQP_ERR_ARG, "codec: unknown codec");
+  Tensor out = c.alloc(dtype, rows, cols);
+  auto staged = c.alloc_bytes(static_cast<size_t>(bytes));
+  if (bytes) TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, c.stream));
+  if (!rows) return out;
+  const int grid = c.grid_for(rows, 256, 4);
+  if (k.codec == TQP_CODEC_FOR) {
+    int64_t* o = out.ptr<int64_t>();
+    if (k.width == 1) k_decode_for<uint8_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint8_t*>(staged->ptr), rows, k.base, k.scale, o);
+    else if (k.width == 2) k_decode_for<uint16_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint16_t*>(staged->ptr), rows, k.base, k.scale, o);
+    else k_decode_for<uint32_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(staged->ptr), rows, k.base, k.scale, o);
+  } else if (k.codec == TQP_CODEC_DEC) {
+    double* o = out.ptr<double>();
+    const double sc = static_cast<double>(k.scale);
+    if (k.width == 1) k_decode_dec<uint8_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint8_t*>(staged->ptr), rows, k.base, sc, o);
+    else if (k.width == 2) k_decode_dec<uint16_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint16_t*>(staged->ptr), rows, k.base, sc, o);
+    else k_decode_dec<uint32_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(staged->ptr), rows, k.base, sc, o);
+  } else {
+    const auto* dict = static_cast<const unsigned long long*>(staged->ptr);
+    k_decode_dict<<<grid, 256, 0, c.stream>>>(dict, k.dict_n, reinterpret_cast<const uint8_t*>(dict + k.dict_n), rows,
+                                              out.ptr<unsigned long long>());
+  }
+  c.count_launch();
+  return out;
+}
+
+}  // namespace tqp

@@ -192,6 +192,11 @@ struct Ctx {
 };
 
 Tensor upload(Ctx& c, int dtype, int64_t rows, int64_t cols, const void* host);
+// compressed columnar host format (codec.cu)
+int64_t codec_bound(int dtype, int64_t rows, int64_t cols);
+int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, void* out, int64_t cap, tqp_codec* c);
+Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_codec& k, const void* payload,
+                     int64_t bytes);
 void download(Ctx& c, const Tensor& t, void* host);
 template <typename T>
 T read_scalar(Ctx& c, const Tensor& t, int64_t index = 0) {

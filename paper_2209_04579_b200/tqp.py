@@ -75,6 +75,18 @@ class Status(C.Structure):
     _fields_ = [("code", C.c_int), ("bad_row", C.c_int64), ("msg", C.c_char * 1024)]
 
 
+class Codec(C.Structure):
+    """tqp_codec: the per-column codec of the compressed host format."""
+    _fields_ = [("codec", C.c_int32), ("width", C.c_int32), ("base", C.c_int64), ("scale", C.c_int64),
+                ("dict_n", C.c_int32), ("reserved", C.c_int32)]
+
+    NAMES = {0: "raw", 1: "for", 2: "dict", 3: "dec"}
+
+    @property
+    def name(self) -> str:
+        return self.NAMES.get(self.codec, "?")
+
+
 class InstrDesc(C.Structure):
     _fields_ = [
         ("op", C.c_char_p), ("inputs", C.POINTER(C.c_int)), ("num_inputs", C.c_int), ("output", C.c_int),
@@ -100,6 +112,9 @@ def _load() -> C.CDLL:
         "tqp_stream": (P, [P]), "tqp_backend_name": (C.c_char_p, [P]), "tqp_device": (I, [P]),
         "tqp_launch_count": (I64_, [P]), "tqp_dtype_size": (C.c_size_t, [I]), "tqp_jit_nvrtc_version": (I, []),
         "tqp_tensor_from_host": (P, [P, I, I64_, I64_, P, S]),
+        "tqp_codec_bound": (I64_, [I, I64_, I64_]),
+        "tqp_codec_encode": (I64_, [I, I64_, I64_, P, P, I64_, P, S]),
+        "tqp_tensor_from_encoded": (P, [P, I, I64_, I64_, P, P, I64_, S]),
         "tqp_tensor_from_host_utf8_i32": (P, [P, I64_, I64_, P, S]),
         "tqp_tensor_from_device": (P, [P, I, I64_, I64_, P, S]),
         "tqp_tensor_dtype": (I, [P]), "tqp_tensor_rows": (I64_, [P]), "tqp_tensor_cols": (I64_, [P]),
@@ -197,6 +212,21 @@ class Context:
 _default: Optional[Context] = None
 
 
+def encode_column(a: np.ndarray, dtype: int) -> Tuple["Codec", np.ndarray]:
+    """Compressed host format of one column (device dtype layout): the codec
+    and its payload bytes (tqp_codec_encode; lossless, verified per value)."""
+    a = np.asarray(a)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    a = np.ascontiguousarray(a, dtype=NP_OF[dtype] if dtype != STR8 else np.uint8)
+    rows, cols = a.shape
+    out = np.empty(max(1, lib.tqp_codec_bound(dtype, rows, cols)), dtype=np.uint8)
+    codec, st = Codec(), Status()
+    n = lib.tqp_codec_encode(dtype, rows, cols, a.ctypes.data, out.ctypes.data, out.nbytes, C.byref(codec), C.byref(st))
+    _check(st, n >= 0)
+    return codec, out[:n].copy()
+
+
 def nvrtc_version() -> int:
     """NVRTC the run-time specialised kernels compile with (12090 = 12.9)."""
     return int(lib.tqp_jit_nvrtc_version())
@@ -241,6 +271,22 @@ class Tensor:
         else:
             a = np.ascontiguousarray(a, dtype=NP_OF[dtype])
             h = lib.tqp_tensor_from_host(ctx.h, dtype, a.shape[0], a.shape[1], a.ctypes.data, C.byref(st))
+        _check(st, bool(h))
+        return Tensor(h, ctx)
+
+    @staticmethod
+    def from_encoded(codec: "Codec", payload, dtype: int, rows: int, cols: int = 1,
+                     ctx: Optional[Context] = None) -> "Tensor":
+        """Uploads an encoded payload (numpy array or a pinned torch tensor:
+        anything with a data pointer) and decodes it on the device."""
+        ctx = ctx or default_context()
+        if hasattr(payload, "data_ptr"):
+            ptr, nbytes = payload.data_ptr(), payload.numel() * payload.element_size()
+        else:
+            payload = np.ascontiguousarray(payload)
+            ptr, nbytes = payload.ctypes.data, payload.nbytes
+        st = Status()
+        h = lib.tqp_tensor_from_encoded(ctx.h, dtype, rows, cols, C.byref(codec), ptr, nbytes, C.byref(st))
         _check(st, bool(h))
         return Tensor(h, ctx)
 

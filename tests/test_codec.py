@@ -1,0 +1,98 @@
+"""Compressed columnar host format (tqp_codec_encode / tqp_tensor_from_encoded,
+SURVEY.md 8(f)1): the encoder picks a lossless codec per column; a numpy
+decoder here (CPU) and the device decoder (GPU) must both give back the
+column bit for bit."""
+import numpy as np
+import pytest
+
+from conftest import ROOT  # noqa: F401  (sys.path)
+
+
+def np_decode(codec, payload, dtype, rows):
+    from paper_2209_04579_b200 import tqp
+    if codec.name == "raw":
+        return payload.view(tqp.NP_OF[dtype]).reshape(rows, -1) if rows else payload.view(tqp.NP_OF[dtype])
+    if codec.name == "dict":
+        d = payload[:8 * codec.dict_n].view(np.uint64)
+        return d[payload[8 * codec.dict_n:]].view(np.float64).reshape(-1, 1)
+    u = payload.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[codec.width]).astype(np.uint64)
+    if codec.name == "for":
+        v = np.uint64(codec.base & 0xFFFFFFFFFFFFFFFF) + np.uint64(codec.scale) * u
+        return v.view(np.int64).reshape(-1, 1)
+    return ((codec.base + u.astype(np.int64)).astype(np.float64) / np.float64(codec.scale)).reshape(-1, 1)
+
+
+def cases():
+    rng = np.random.default_rng(11)
+    day = 86_400 * 10**9
+    n = 200_003
+    yield "dates", 2, (rng.integers(8035, 10561, n) * day), "for", 2
+    yield "qty", 2, rng.integers(1, 51, n), "for", 1
+    yield "keys", 2, rng.integers(1, 2_000_001, n), "for", 4
+    yield "negative", 2, rng.integers(-(2**40), -(2**40) + 70_000, n), "for", 4
+    yield "const", 2, np.full(n, -7, dtype=np.int64), "for", 1
+    yield "extremes", 2, np.array([-(2**63), 2**63 - 1, 0], dtype=np.int64), "raw", 0
+    yield "discount", 3, rng.integers(0, 11, n) / 100.0, "dict", 1
+    yield "price", 3, np.round(rng.uniform(900, 105000, n), 2), "dec", 4
+    yield "price_neg", 3, -np.round(rng.uniform(0.01, 300, n), 2), "dec", 2
+    yield "integral_f64", 3, rng.integers(-100, 100, n).astype(np.float64) * 3.0 + 0.5 * 0, "dict", 1
+    yield "random_f64", 3, rng.standard_normal(n), "raw", 0
+    zneg = np.round(rng.uniform(1, 20, n), 2)
+    zneg[5] = -0.0
+    yield "neg_zero_many", 3, zneg, "raw", 0  # -0.0 breaks DEC; > 256 values rule DICT out
+    nan = rng.integers(0, 5, n).astype(np.float64)
+    nan[7] = np.nan
+    yield "nan_dict", 3, nan, "dict", 1  # DICT keeps bit patterns, NaN included
+    yield "empty", 2, np.zeros(0, dtype=np.int64), "raw", 0
+
+
+@pytest.mark.parametrize("name,dtype,arr,want,width", list(cases()), ids=[c[0] for c in cases()])
+def test_encoder_lossless(name, dtype, arr, want, width):
+    from paper_2209_04579_b200 import tqp
+    arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
+    codec, payload = tqp.encode_column(arr, dtype)
+    assert codec.name == want, (name, codec.name)
+    if want in ("for", "dec"):
+        assert codec.width == width
+    if want != "raw":
+        assert payload.nbytes < arr.nbytes
+    back = np_decode(codec, payload, dtype, len(arr))
+    np.testing.assert_array_equal(back.reshape(-1).view(np.uint64 if arr.dtype.itemsize == 8 else arr.dtype),
+                                  arr.view(np.uint64 if arr.dtype.itemsize == 8 else arr.dtype))
+
+
+@pytest.mark.gpu
+def test_device_decode_bit_identical(ctx):
+    from paper_2209_04579_b200 import tqp
+    for name, dtype, arr, _, _ in cases():
+        arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
+        codec, payload = tqp.encode_column(arr, dtype)
+        t = tqp.Tensor.from_encoded(codec, payload, dtype, len(arr), 1)
+        got = t.numpy().reshape(-1)
+        np.testing.assert_array_equal(got.view(np.uint64), arr.view(np.uint64), err_msg=name)
+
+
+@pytest.mark.gpu
+def test_tpch_from_encoded_columns(ctx):
+    """The four queries over tables uploaded in the compressed format match
+    the golden results (and the columns decode to the generator's bits)."""
+    import json
+    from conftest import load_tpch_golden
+    from test_oracle import compare_tables
+    from paper_2209_04579_b200 import tqp
+    gold = load_tpch_golden()
+    tables = {}
+    for n in ("lineitem", "orders", "customer", "part"):
+        src = tqp.Table.generate(n, gold["sf"], gold["seed"])
+        tab = tqp.Table.create(ctx)
+        for cname, lt in src.columns():
+            dev = src.column(cname)
+            host = dev.numpy(widen_strings=False)
+            codec, payload = tqp.encode_column(host, dev.dtype)
+            t = tqp.Tensor.from_encoded(codec, payload, dev.dtype, host.shape[0], host.shape[1])
+            np.testing.assert_array_equal(t.numpy(widen_strings=False), host, err_msg=f"{n}.{cname}")
+            tab.add_column(cname, lt, t)
+        tables[n] = tab
+    for q in ("q1", "q6", "q14", "q3"):
+        plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
+        compare_tables(tqp.Executor(plan).execute(tables).to_numpy(), gold["results"][q])
