@@ -119,20 +119,21 @@ tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_
  * host memory, so an upload moves fewer bytes over PCIe and the device
  * decodes at HBM speed. Codecs (one per column, chosen by tqp_codec_encode):
  *   RAW   the reference layout as is (any dtype / shape)
- *   FOR   int64/date vector: v = base + scale * u, u unsigned of `width`
- *         bytes (frame of reference; scale = gcd of v - min, e.g. one day
- *         in ns for dates)
+ *   FOR   int64/date or one-byte (STR8/BOOL, one column) vector:
+ *         v = base + scale * u (frame of reference; scale = gcd of v - min,
+ *         e.g. one day in ns for dates)
  *   DICT  float64 vector with <= 256 distinct bit patterns: dict_n patterns
- *         (8 B each, ascending) then one byte per row
+ *         (8 B each, ascending) then the codes
  *   DEC   float64 vector whose every value is exactly (base + u) / scale
- *         for an integer u of `width` bytes and scale = 10^d (d <= 4): the
- *         decode (an IEEE division) reproduces the original bits; -0.0,
- *         NaN and inf excluded.
+ *         for an integer u and scale = 10^d (d <= 4): the decode (an IEEE
+ *         division) reproduces the original bits; -0.0, NaN, inf excluded.
+ * Codes u are bit-packed, `width` bits each (1..32), little endian in
+ * 32-bit words, plus one spare word: 4 * (ceil(rows * width / 32) + 1) B.
  * Lossless by construction: the encoder verifies every value. */
 typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3 } tqp_codec_kind;
 typedef struct {
   int32_t codec;  /* tqp_codec_kind */
-  int32_t width;  /* FOR / DEC: bytes per code (1, 2, 4); DICT: 1 */
+  int32_t width;  /* bits per code (1..32), FOR / DICT / DEC */
   int64_t base;   /* FOR: value of code 0; DEC: integer numerator of code 0 */
   int64_t scale;  /* FOR: value step of one code; DEC: the denominator 10^d */
   int32_t dict_n; /* DICT: dictionary entries at the start of the payload */

@@ -43,34 +43,48 @@ void parallel_chunks(int64_t n, F&& f) {  // f(thread, lo, hi)
   for (auto& x : th) x.join();
 }
 
-int width_for(uint64_t max_code) {
-  if (max_code < (1ull << 8)) return 1;
-  if (max_code < (1ull << 16)) return 2;
-  if (max_code < (1ull << 32)) return 4;
-  return 0;
+// codes are bit-packed little-endian into 32-bit words: code i occupies
+// bits [i * w, (i + 1) * w) of the stream (w = 1..32); one spare word at the
+// end lets a decoder always read two words
+int bits_for(uint64_t max_code) {
+  int b = 1;
+  while (b < 32 && (max_code >> b) != 0) ++b;
+  return (max_code >> b) != 0 ? 0 : b;  // 0: does not fit 32 bits
 }
+int64_t packed_bytes(int64_t n, int w) { return 4 * ((n * w + 31) / 32 + 1); }
 
-void put_code(void* out, int width, int64_t i, uint64_t u) {
-  switch (width) {
-    case 1: static_cast<uint8_t*>(out)[i] = static_cast<uint8_t>(u); break;
-    case 2: static_cast<uint16_t*>(out)[i] = static_cast<uint16_t>(u); break;
-    default: static_cast<uint32_t*>(out)[i] = static_cast<uint32_t>(u); break;
-  }
+// packs code(i) for i in [0, n) in parallel; chunks start on 32-code
+// boundaries so no two threads share a word
+template <typename Code>
+void pack_codes(int64_t n, int w, uint32_t* words, Code&& code) {
+  std::memset(words, 0, static_cast<size_t>(packed_bytes(n, w)));
+  const int64_t groups = (n + 31) / 32;
+  parallel_chunks(groups, [&](int, int64_t g0, int64_t g1) {
+    for (int64_t i = g0 * 32; i < std::min(n, g1 * 32); ++i) {
+      const uint64_t u = code(i);
+      const int64_t bit = i * w;
+      const int64_t wi = bit >> 5;
+      const int sh = static_cast<int>(bit & 31);
+      words[wi] |= static_cast<uint32_t>(u << sh);
+      if (sh + w > 32) words[wi + 1] |= static_cast<uint32_t>(u >> (32 - sh));
+    }
+  });
 }
 
 // ---- host: codecs --------------------------------------------------------------
-// FOR over int64: base = min, scale = gcd of (v - min) (unsigned), codes of
-// the narrowest width that holds (max - min) / scale. Returns payload bytes
-// or -1 when no width below 8 bytes fits.
-int64_t try_for(const int64_t* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
+// FOR over integers (int64 or byte values): base = min, scale = gcd of
+// (v - min) (unsigned), codes of the fewest bits that hold (max - min) /
+// scale. Returns payload bytes or -1.
+template <typename T>
+int64_t try_for(const T* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
   if (n == 0) return -1;
   const int nt = host_threads(n);
   std::vector<int64_t> mn(nt, INT64_MAX), mx(nt, INT64_MIN);
   parallel_chunks(n, [&](int t, int64_t lo, int64_t hi) {
     int64_t a = INT64_MAX, b = INT64_MIN;
     for (int64_t i = lo; i < hi; ++i) {
-      a = std::min(a, v[i]);
-      b = std::max(b, v[i]);
+      a = std::min<int64_t>(a, v[i]);
+      b = std::max<int64_t>(b, v[i]);
     }
     mn[t] = a;
     mx[t] = b;
@@ -81,7 +95,7 @@ int64_t try_for(const int64_t* v, int64_t n, void* out, int64_t cap, tqp_codec* 
   parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
     uint64_t x = 0;
     for (int64_t i = a; i < b && x != 1; ++i) {
-      const uint64_t d = static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(lo);
+      const uint64_t d = static_cast<uint64_t>(static_cast<int64_t>(v[i])) - static_cast<uint64_t>(lo);
       if (x == 0 ? d != 0 : d % x != 0) x = std::gcd(x, d);
     }
     g[t] = x;
@@ -89,16 +103,16 @@ int64_t try_for(const int64_t* v, int64_t n, void* out, int64_t cap, tqp_codec* 
   uint64_t scale = 0;
   for (uint64_t x : g) scale = std::gcd(scale, x);
   if (scale == 0) scale = 1;  // every value equal
-  const int w = width_for(range / scale);
-  if (!w || w * n > cap) return -1;
-  parallel_chunks(n, [&](int, int64_t a, int64_t b) {
-    for (int64_t i = a; i < b; ++i) put_code(out, w, i, (static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(lo)) / scale);
+  const int w = bits_for(range / scale);
+  if (!w || packed_bytes(n, w) > cap) return -1;
+  pack_codes(n, w, static_cast<uint32_t*>(out), [&](int64_t i) {
+    return (static_cast<uint64_t>(static_cast<int64_t>(v[i])) - static_cast<uint64_t>(lo)) / scale;
   });
   c->codec = TQP_CODEC_FOR;
   c->width = w;
   c->base = lo;
   c->scale = static_cast<int64_t>(scale);
-  return w * n;
+  return packed_bytes(n, w);
 }
 
 // DICT over float64 bit patterns (<= 256 distinct).
@@ -131,16 +145,15 @@ int64_t try_dict(const uint64_t* v, int64_t n, void* out, int64_t cap, tqp_codec
   std::sort(dict.begin(), dict.end());
   dict.erase(std::unique(dict.begin(), dict.end()), dict.end());
   if (dict.size() > 256) return -1;
-  const int64_t bytes = 8 * static_cast<int64_t>(dict.size()) + n;
+  const int w = bits_for(dict.size() - 1);
+  const int64_t bytes = 8 * static_cast<int64_t>(dict.size()) + packed_bytes(n, w);
   if (bytes > cap) return -1;
   std::memcpy(out, dict.data(), 8 * dict.size());
-  uint8_t* codes = static_cast<uint8_t*>(out) + 8 * dict.size();
-  parallel_chunks(n, [&](int, int64_t a, int64_t b) {
-    for (int64_t i = a; i < b; ++i)
-      codes[i] = static_cast<uint8_t>(std::lower_bound(dict.begin(), dict.end(), v[i]) - dict.begin());
+  pack_codes(n, w, reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(out) + 8 * dict.size()), [&](int64_t i) {
+    return static_cast<uint64_t>(std::lower_bound(dict.begin(), dict.end(), v[i]) - dict.begin());
   });
   c->codec = TQP_CODEC_DICT;
-  c->width = 1;
+  c->width = w;
   c->dict_n = static_cast<int32_t>(dict.size());
   return bytes;
 }
@@ -178,39 +191,46 @@ int64_t try_dec(const double* v, int64_t n, void* out, int64_t cap, tqp_codec* c
     });
     if (std::find(bad.begin(), bad.end(), 1) != bad.end()) continue;
     const int64_t lo = *std::min_element(mn.begin(), mn.end()), hi = *std::max_element(mx.begin(), mx.end());
-    const int w = width_for(static_cast<uint64_t>(hi - lo));
-    if (!w || w * n > cap) return -1;
-    parallel_chunks(n, [&](int, int64_t a, int64_t b) {
-      for (int64_t i = a; i < b; ++i) put_code(out, w, i, static_cast<uint64_t>(std::llrint(v[i] * scale) - lo));
-    });
+    const int w = bits_for(static_cast<uint64_t>(hi - lo));
+    if (!w || packed_bytes(n, w) > cap) return -1;
+    pack_codes(n, w, static_cast<uint32_t*>(out),
+               [&](int64_t i) { return static_cast<uint64_t>(std::llrint(v[i] * scale) - lo); });
     c->codec = TQP_CODEC_DEC;
     c->width = w;
     c->base = lo;
     c->scale = static_cast<int64_t>(scale);
-    return w * n;
+    return packed_bytes(n, w);
   }
   return -1;
 }
 
 // ---- device: decoders ------------------------------------------------------------
-template <typename U>
-__global__ void k_decode_for(const U* __restrict__ codes, int64_t n, int64_t base, int64_t scale, int64_t* __restrict__ out) {
-  for (int64_t i = gtid(); i < n; i += gstride())
-    out[i] = static_cast<int64_t>(static_cast<uint64_t>(base) + static_cast<uint64_t>(scale) * static_cast<uint64_t>(codes[i]));
+__device__ __forceinline__ uint32_t unpack(const uint32_t* __restrict__ words, int64_t i, int w) {
+  const int64_t bit = i * w;
+  const int64_t wi = bit >> 5;
+  const uint64_t two = static_cast<uint64_t>(__ldg(words + wi)) | (static_cast<uint64_t>(__ldg(words + wi + 1)) << 32);
+  return static_cast<uint32_t>((two >> (bit & 31)) & ((w == 32 ? 0x100000000ull : (1ull << w)) - 1));
 }
 
-template <typename U>
-__global__ void k_decode_dec(const U* __restrict__ codes, int64_t n, int64_t base, double scale, double* __restrict__ out) {
+template <typename T>
+__global__ void k_decode_for(const uint32_t* __restrict__ words, int w, int64_t n, int64_t base, int64_t scale,
+                             T* __restrict__ out) {
   for (int64_t i = gtid(); i < n; i += gstride())
-    out[i] = __ddiv_rn(static_cast<double>(base + static_cast<int64_t>(codes[i])), scale);
+    out[i] = static_cast<T>(static_cast<uint64_t>(base) + static_cast<uint64_t>(scale) * unpack(words, i, w));
 }
 
-__global__ void k_decode_dict(const unsigned long long* __restrict__ dict, int nd, const uint8_t* __restrict__ codes,
-                              int64_t n, unsigned long long* __restrict__ out) {
+__global__ void k_decode_dec(const uint32_t* __restrict__ words, int w, int64_t n, int64_t base, double scale,
+                             double* __restrict__ out) {
+  for (int64_t i = gtid(); i < n; i += gstride())
+    out[i] = __ddiv_rn(static_cast<double>(base + static_cast<int64_t>(unpack(words, i, w))), scale);
+}
+
+__global__ void k_decode_dict(const unsigned long long* __restrict__ dict, int nd, const uint32_t* __restrict__ words,
+                              int w, int64_t n, unsigned long long* __restrict__ out) {
   __shared__ unsigned long long s_dict[256];
   for (int i = threadIdx.x; i < nd; i += blockDim.x) s_dict[i] = dict[i];
   __syncthreads();
-  for (int64_t i = gtid(); i < n; i += gstride()) out[i] = s_dict[codes[i]];
+  for (int64_t i = gtid(); i < n; i += gstride()) out[i] = s_dict[unpack(words, i, w)];
 }
 
 }  // namespace
@@ -228,6 +248,10 @@ int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, vo
   // next, and RAW (below) overwrites whatever a failed attempt wrote
   if (cols == 1 && rows > 0 && dtype == TQP_I64) {
     const int64_t b = try_for(static_cast<const int64_t*>(host), rows, out, std::min(cap, raw - 1), c);
+    if (b >= 0) return b;
+  }
+  if (cols == 1 && rows > 0 && (dtype == TQP_STR8 || dtype == TQP_BOOL)) {  // one-byte values (flags, codes)
+    const int64_t b = try_for(static_cast<const uint8_t*>(host), rows, out, std::min(cap, raw - 1), c);
     if (b >= 0) return b;
   }
   if (cols == 1 && rows > 0 && dtype == TQP_F64) {
@@ -253,13 +277,14 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
     return upload(c, dtype, rows, cols, payload);
   }
   const bool vec = cols == 1;
-  const bool w_ok = k.width == 1 || k.width == 2 || k.width == 4;
-  if (k.codec == TQP_CODEC_FOR && !(vec && dtype == TQP_I64 && w_ok && bytes == k.width * rows))
+  const bool w_ok = k.width >= 1 && k.width <= 32;
+  const bool byte_col = dtype == TQP_STR8 || dtype == TQP_BOOL;
+  if (k.codec == TQP_CODEC_FOR && !(vec && (dtype == TQP_I64 || byte_col) && w_ok && bytes == packed_bytes(rows, k.width)))
     throw Error(TQP_ERR_ARG, "codec: bad FOR column");
-  if (k.codec == TQP_CODEC_DEC && !(vec && dtype == TQP_F64 && w_ok && bytes == k.width * rows && k.scale > 0))
+  if (k.codec == TQP_CODEC_DEC && !(vec && dtype == TQP_F64 && w_ok && bytes == packed_bytes(rows, k.width) && k.scale > 0))
     throw Error(TQP_ERR_ARG, "codec: bad DEC column");
-  if (k.codec == TQP_CODEC_DICT &&
-      !(vec && dtype == TQP_F64 && k.dict_n >= 1 && k.dict_n <= 256 && bytes == 8LL * k.dict_n + rows))
+  if (k.codec == TQP_CODEC_DICT && !(vec && dtype == TQP_F64 && w_ok && k.dict_n >= 1 && k.dict_n <= 256 &&
+                                     bytes == 8LL * k.dict_n + packed_bytes(rows, k.width)))
     throw Error(TQP_ERR_ARG, "codec: bad DICT column");
   if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_DEC) throw Error(TQP_ERR_ARG, "codec: unknown codec");
   Tensor out = c.alloc(dtype, rows, cols);
@@ -267,21 +292,18 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
   if (bytes) TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, c.stream));
   if (!rows) return out;
   const int grid = c.grid_for(rows, 256, 4);
+  const auto* words = static_cast<const uint32_t*>(staged->ptr);
   if (k.codec == TQP_CODEC_FOR) {
-    int64_t* o = out.ptr<int64_t>();
-    if (k.width == 1) k_decode_for<uint8_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint8_t*>(staged->ptr), rows, k.base, k.scale, o);
-    else if (k.width == 2) k_decode_for<uint16_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint16_t*>(staged->ptr), rows, k.base, k.scale, o);
-    else k_decode_for<uint32_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(staged->ptr), rows, k.base, k.scale, o);
+    if (byte_col)
+      k_decode_for<uint8_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, k.scale, out.ptr<uint8_t>());
+    else
+      k_decode_for<int64_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, k.scale, out.ptr<int64_t>());
   } else if (k.codec == TQP_CODEC_DEC) {
-    double* o = out.ptr<double>();
-    const double sc = static_cast<double>(k.scale);
-    if (k.width == 1) k_decode_dec<uint8_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint8_t*>(staged->ptr), rows, k.base, sc, o);
-    else if (k.width == 2) k_decode_dec<uint16_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint16_t*>(staged->ptr), rows, k.base, sc, o);
-    else k_decode_dec<uint32_t><<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(staged->ptr), rows, k.base, sc, o);
+    k_decode_dec<<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, static_cast<double>(k.scale), out.ptr<double>());
   } else {
     const auto* dict = static_cast<const unsigned long long*>(staged->ptr);
-    k_decode_dict<<<grid, 256, 0, c.stream>>>(dict, k.dict_n, reinterpret_cast<const uint8_t*>(dict + k.dict_n), rows,
-                                              out.ptr<unsigned long long>());
+    k_decode_dict<<<grid, 256, 0, c.stream>>>(dict, k.dict_n, reinterpret_cast<const uint32_t*>(dict + k.dict_n), k.width,
+                                              rows, out.ptr<unsigned long long>());
   }
   c.count_launch();
   return out;

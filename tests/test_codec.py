@@ -12,13 +12,19 @@ def np_decode(codec, payload, dtype, rows):
     from paper_2209_04579_b200 import tqp
     if codec.name == "raw":
         return payload.view(tqp.NP_OF[dtype]).reshape(rows, -1) if rows else payload.view(tqp.NP_OF[dtype])
+    off = 8 * codec.dict_n if codec.name == "dict" else 0
+    words = payload[off:].view(np.uint32).astype(np.uint64)
+    w = codec.width
+    bit = np.arange(rows, dtype=np.uint64) * np.uint64(w)
+    wi = (bit >> np.uint64(5)).astype(np.int64)
+    two = words[wi] | (words[wi + 1] << np.uint64(32))
+    u = (two >> (bit & np.uint64(31))) & np.uint64((1 << w) - 1)
     if codec.name == "dict":
-        d = payload[:8 * codec.dict_n].view(np.uint64)
-        return d[payload[8 * codec.dict_n:]].view(np.float64).reshape(-1, 1)
-    u = payload.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[codec.width]).astype(np.uint64)
+        d = payload[:off].view(np.uint64)
+        return d[u.astype(np.int64)].view(np.float64).reshape(-1, 1)
     if codec.name == "for":
         v = np.uint64(codec.base & 0xFFFFFFFFFFFFFFFF) + np.uint64(codec.scale) * u
-        return v.view(np.int64).reshape(-1, 1)
+        return (v.view(np.int64) if dtype == 2 else v.astype(np.uint8)).reshape(-1, 1)
     return ((codec.base + u.astype(np.int64)).astype(np.float64) / np.float64(codec.scale)).reshape(-1, 1)
 
 
@@ -26,23 +32,25 @@ def cases():
     rng = np.random.default_rng(11)
     day = 86_400 * 10**9
     n = 200_003
-    yield "dates", 2, (rng.integers(8035, 10561, n) * day), "for", 2
-    yield "qty", 2, rng.integers(1, 51, n), "for", 1
-    yield "keys", 2, rng.integers(1, 2_000_001, n), "for", 4
-    yield "negative", 2, rng.integers(-(2**40), -(2**40) + 70_000, n), "for", 4
+    yield "dates", 2, (rng.integers(8035, 10561, n) * day), "for", 12
+    yield "qty", 2, rng.integers(1, 51, n), "for", 6
+    yield "keys", 2, rng.integers(1, 2_000_001, n), "for", 21
+    yield "negative", 2, rng.integers(-(2**40), -(2**40) + 70_000, n), "for", 17
     yield "const", 2, np.full(n, -7, dtype=np.int64), "for", 1
+    yield "wide32", 2, rng.integers(0, 2**32, n), "for", 32
+    yield "flags", 4, np.array([65, 78, 82], dtype=np.uint8)[rng.integers(0, 3, n)], "for", 5
     yield "extremes", 2, np.array([-(2**63), 2**63 - 1, 0], dtype=np.int64), "raw", 0
-    yield "discount", 3, rng.integers(0, 11, n) / 100.0, "dict", 1
-    yield "price", 3, np.round(rng.uniform(900, 105000, n), 2), "dec", 4
-    yield "price_neg", 3, -np.round(rng.uniform(0.01, 300, n), 2), "dec", 2
-    yield "integral_f64", 3, rng.integers(-100, 100, n).astype(np.float64) * 3.0 + 0.5 * 0, "dict", 1
+    yield "discount", 3, rng.integers(0, 11, n) / 100.0, "dict", 4
+    yield "price", 3, np.round(rng.uniform(900, 105000, n), 2), "dec", 24
+    yield "price_neg", 3, -np.round(rng.uniform(0.01, 300, n), 2), "dec", 15
+    yield "integral_f64", 3, rng.integers(-100, 100, n).astype(np.float64) * 3.0, "dict", 8
     yield "random_f64", 3, rng.standard_normal(n), "raw", 0
     zneg = np.round(rng.uniform(1, 20, n), 2)
     zneg[5] = -0.0
     yield "neg_zero_many", 3, zneg, "raw", 0  # -0.0 breaks DEC; > 256 values rule DICT out
     nan = rng.integers(0, 5, n).astype(np.float64)
     nan[7] = np.nan
-    yield "nan_dict", 3, nan, "dict", 1  # DICT keeps bit patterns, NaN included
+    yield "nan_dict", 3, nan, "dict", 3  # DICT keeps bit patterns, NaN included
     yield "empty", 2, np.zeros(0, dtype=np.int64), "raw", 0
 
 
@@ -52,8 +60,8 @@ def test_encoder_lossless(name, dtype, arr, want, width):
     arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
     codec, payload = tqp.encode_column(arr, dtype)
     assert codec.name == want, (name, codec.name)
-    if want in ("for", "dec"):
-        assert codec.width == width
+    if want in ("for", "dec", "dict"):
+        assert codec.width == width, (name, codec.width)
     if want != "raw":
         assert payload.nbytes < arr.nbytes
     back = np_decode(codec, payload, dtype, len(arr))
@@ -68,8 +76,9 @@ def test_device_decode_bit_identical(ctx):
         arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
         codec, payload = tqp.encode_column(arr, dtype)
         t = tqp.Tensor.from_encoded(codec, payload, dtype, len(arr), 1)
-        got = t.numpy().reshape(-1)
-        np.testing.assert_array_equal(got.view(np.uint64), arr.view(np.uint64), err_msg=name)
+        got = t.numpy(widen_strings=False).reshape(-1)
+        view = np.uint64 if arr.dtype.itemsize == 8 else arr.dtype
+        np.testing.assert_array_equal(got.view(view), arr.view(view), err_msg=name)
 
 
 @pytest.mark.gpu
