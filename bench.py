@@ -479,13 +479,15 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red
     end.record(stream)
     end.synchronize()
     wall_ms = (time.perf_counter() - t0) * 1e3
-    ms = max(start.elapsed_time(end), wall_ms) / steps
+    ev_ms = start.elapsed_time(end)
+    ms = max(ev_ms, wall_ms) / steps
     if dist:
         t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     out = {"value": len(QUERIES) * L_total / (ms / 1e3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps}
+           "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": steps,
+           "device_ms_per_step": ev_ms / steps, "wall_ms_per_step": wall_ms / steps}
     if encoded:
         out["path"] = ("pinned host columns in the compressed columnar format -> tqp_tensor_from_encoded (C ABI: "
                        "H2D of the encoded bytes + device decode) -> tqp_executor_execute x4 -> results to host")

@@ -127,15 +127,18 @@ tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_
  *   DEC   float64 vector whose every value is exactly (base + u) / scale
  *         for an integer u and scale = 10^d (d <= 4): the decode (an IEEE
  *         division) reproduces the original bits; -0.0, NaN, inf excluded.
+ *   DELTA int64 vector in non-decreasing order (sorted keys): code i is
+ *         (v_i - v_(i-1)) / scale (code 0 is 0), base = v_0; decoded by a
+ *         device prefix sum
  * Codes u are bit-packed, `width` bits each (1..32), little endian in
  * 32-bit words, plus one spare word: 4 * (ceil(rows * width / 32) + 1) B.
  * Lossless by construction: the encoder verifies every value. */
-typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3 } tqp_codec_kind;
+typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3, TQP_CODEC_DELTA = 4 } tqp_codec_kind;
 typedef struct {
   int32_t codec;  /* tqp_codec_kind */
   int32_t width;  /* bits per code (1..32), FOR / DICT / DEC */
-  int64_t base;   /* FOR: value of code 0; DEC: integer numerator of code 0 */
-  int64_t scale;  /* FOR: value step of one code; DEC: the denominator 10^d */
+  int64_t base;   /* FOR: value of code 0; DEC: integer numerator of code 0; DELTA: v_0 */
+  int64_t scale;  /* FOR / DELTA: value step of one code; DEC: the denominator 10^d */
   int32_t dict_n; /* DICT: dictionary entries at the start of the payload */
   int32_t reserved;
 } tqp_codec;

@@ -11,6 +11,7 @@
 // exactly stays RAW. Decoding is one grid-stride kernel per column.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -74,10 +75,17 @@ void pack_codes(int64_t n, int w, uint32_t* words, Code&& code) {
 // ---- host: codecs --------------------------------------------------------------
 // FOR over integers (int64 or byte values): base = min, scale = gcd of
 // (v - min) (unsigned), codes of the fewest bits that hold (max - min) /
-// scale. Returns payload bytes or -1.
+// scale.
+struct ForPlan {
+  int64_t base = 0;
+  uint64_t scale = 1;
+  int bits = 0;  // 0: does not fit
+};
+
 template <typename T>
-int64_t try_for(const T* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
-  if (n == 0) return -1;
+ForPlan plan_for(const T* v, int64_t n) {
+  ForPlan p;
+  if (n == 0) return p;
   const int nt = host_threads(n);
   std::vector<int64_t> mn(nt, INT64_MAX), mx(nt, INT64_MIN);
   parallel_chunks(n, [&](int t, int64_t lo, int64_t hi) {
@@ -103,16 +111,78 @@ int64_t try_for(const T* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
   uint64_t scale = 0;
   for (uint64_t x : g) scale = std::gcd(scale, x);
   if (scale == 0) scale = 1;  // every value equal
-  const int w = bits_for(range / scale);
-  if (!w || packed_bytes(n, w) > cap) return -1;
-  pack_codes(n, w, static_cast<uint32_t*>(out), [&](int64_t i) {
-    return (static_cast<uint64_t>(static_cast<int64_t>(v[i])) - static_cast<uint64_t>(lo)) / scale;
+  p.base = lo;
+  p.scale = scale;
+  p.bits = bits_for(range / scale);
+  return p;
+}
+
+template <typename T>
+int64_t pack_for(const T* v, int64_t n, const ForPlan& p, void* out, tqp_codec* c) {
+  pack_codes(n, p.bits, static_cast<uint32_t*>(out), [&](int64_t i) {
+    return (static_cast<uint64_t>(static_cast<int64_t>(v[i])) - static_cast<uint64_t>(p.base)) / p.scale;
   });
   c->codec = TQP_CODEC_FOR;
-  c->width = w;
-  c->base = lo;
-  c->scale = static_cast<int64_t>(scale);
-  return packed_bytes(n, w);
+  c->width = p.bits;
+  c->base = p.base;
+  c->scale = static_cast<int64_t>(p.scale);
+  return packed_bytes(n, p.bits);
+}
+
+template <typename T>
+int64_t try_for(const T* v, int64_t n, void* out, int64_t cap, tqp_codec* c) {
+  const ForPlan p = plan_for(v, n);
+  if (!p.bits || packed_bytes(n, p.bits) > cap) return -1;
+  return pack_for(v, n, p, out, c);
+}
+
+// DELTA over a non-decreasing int64 vector (sorted keys): e_0 = 0,
+// e_i = v_i - v_(i-1) >= 0, codes e_i / scale (scale = gcd of the e_i);
+// v_i = v_0 + scale * (sum of codes up to i). Returns the plan (bits 0: not
+// sorted or does not fit).
+ForPlan plan_delta(const int64_t* v, int64_t n) {
+  ForPlan p;
+  if (n < 2) return p;
+  const int nt = host_threads(n);
+  std::vector<uint64_t> g(nt, 0), mx(nt, 0);
+  std::vector<char> unsorted(nt, 0);
+  parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
+    uint64_t x = 0, m = 0;
+    for (int64_t i = std::max<int64_t>(a, 1); i < b; ++i) {
+      if (v[i] < v[i - 1]) {
+        unsorted[t] = 1;
+        return;
+      }
+      const uint64_t d = static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(v[i - 1]);
+      m = std::max(m, d);
+      if (x != 1 && (x == 0 ? d != 0 : d % x != 0)) x = std::gcd(x, d);
+    }
+    g[t] = x;
+    mx[t] = m;
+  });
+  for (char u : unsorted)
+    if (u) return p;
+  uint64_t scale = 0, m = 0;
+  for (int t = 0; t < nt; ++t) {
+    scale = std::gcd(scale, g[t]);
+    m = std::max(m, mx[t]);
+  }
+  if (scale == 0) scale = 1;
+  p.base = v[0];
+  p.scale = scale;
+  p.bits = bits_for(m / scale);
+  return p;
+}
+
+int64_t pack_delta(const int64_t* v, int64_t n, const ForPlan& p, void* out, tqp_codec* c) {
+  pack_codes(n, p.bits, static_cast<uint32_t*>(out), [&](int64_t i) {
+    return i == 0 ? 0ull : (static_cast<uint64_t>(v[i]) - static_cast<uint64_t>(v[i - 1])) / p.scale;
+  });
+  c->codec = TQP_CODEC_DELTA;
+  c->width = p.bits;
+  c->base = p.base;
+  c->scale = static_cast<int64_t>(p.scale);
+  return packed_bytes(n, p.bits);
 }
 
 // DICT over float64 bit patterns (<= 256 distinct).
@@ -219,6 +289,12 @@ __global__ void k_decode_for(const uint32_t* __restrict__ words, int w, int64_t 
     out[i] = static_cast<T>(static_cast<uint64_t>(base) + static_cast<uint64_t>(scale) * unpack(words, i, w));
 }
 
+__global__ void k_delta_finish(const int64_t* __restrict__ excl, const int64_t* __restrict__ step, int64_t n,
+                               int64_t base, int64_t* __restrict__ out) {
+  for (int64_t i = gtid(); i < n; i += gstride())
+    out[i] = static_cast<int64_t>(static_cast<uint64_t>(base) + static_cast<uint64_t>(excl[i]) + static_cast<uint64_t>(step[i]));
+}
+
 __global__ void k_decode_dec(const uint32_t* __restrict__ words, int w, int64_t n, int64_t base, double scale,
                              double* __restrict__ out) {
   for (int64_t i = gtid(); i < n; i += gstride())
@@ -247,8 +323,12 @@ int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, vo
   // each attempt writes straight into `out`; a failed one leaves it to the
   // next, and RAW (below) overwrites whatever a failed attempt wrote
   if (cols == 1 && rows > 0 && dtype == TQP_I64) {
-    const int64_t b = try_for(static_cast<const int64_t*>(host), rows, out, std::min(cap, raw - 1), c);
-    if (b >= 0) return b;
+    const auto* v = static_cast<const int64_t*>(host);
+    static const bool no_delta = std::getenv("TQP_CODEC_NO_DELTA") != nullptr;  // experiment knob
+    const ForPlan f = plan_for(v, rows), d = no_delta ? ForPlan{} : plan_delta(v, rows);
+    const int64_t lim = std::min(cap, raw - 1);
+    if (d.bits && (!f.bits || d.bits < f.bits) && packed_bytes(rows, d.bits) <= lim) return pack_delta(v, rows, d, out, c);
+    if (f.bits && packed_bytes(rows, f.bits) <= lim) return pack_for(v, rows, f, out, c);
   }
   if (cols == 1 && rows > 0 && (dtype == TQP_STR8 || dtype == TQP_BOOL)) {  // one-byte values (flags, codes)
     const int64_t b = try_for(static_cast<const uint8_t*>(host), rows, out, std::min(cap, raw - 1), c);
@@ -286,7 +366,9 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
   if (k.codec == TQP_CODEC_DICT && !(vec && dtype == TQP_F64 && w_ok && k.dict_n >= 1 && k.dict_n <= 256 &&
                                      bytes == 8LL * k.dict_n + packed_bytes(rows, k.width)))
     throw Error(TQP_ERR_ARG, "codec: bad DICT column");
-  if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_DEC) throw Error(TQP_ERR_ARG, "codec: unknown codec");
+  if (k.codec == TQP_CODEC_DELTA && !(vec && dtype == TQP_I64 && w_ok && bytes == packed_bytes(rows, k.width)))
+    throw Error(TQP_ERR_ARG, "codec: bad DELTA column");
+  if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_DELTA) throw Error(TQP_ERR_ARG, "codec: unknown codec");
   Tensor out = c.alloc(dtype, rows, cols);
   auto staged = c.alloc_bytes(static_cast<size_t>(bytes));
   if (bytes) TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, c.stream));
@@ -298,6 +380,15 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
       k_decode_for<uint8_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, k.scale, out.ptr<uint8_t>());
     else
       k_decode_for<int64_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, k.scale, out.ptr<int64_t>());
+  } else if (k.codec == TQP_CODEC_DELTA) {
+    // the steps, then their inclusive scan (exclusive scan + the step)
+    Tensor steps = c.alloc(TQP_I64, rows, 1);
+    k_decode_for<int64_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, 0, k.scale, steps.ptr<int64_t>());
+    c.count_launch();
+    int64_t ovf = -1;
+    Tensor excl = k::prefix_sum_raw(c, steps, &ovf);
+    if (ovf >= 0) throw Error(TQP_ERR_ARG, "codec: DELTA column overflows int64");
+    k_delta_finish<<<grid, 256, 0, c.stream>>>(excl.ptr<int64_t>(), steps.ptr<int64_t>(), rows, k.base, out.ptr<int64_t>());
   } else if (k.codec == TQP_CODEC_DEC) {
     k_decode_dec<<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, static_cast<double>(k.scale), out.ptr<double>());
   } else {

@@ -25,6 +25,9 @@ def np_decode(codec, payload, dtype, rows):
     if codec.name == "for":
         v = np.uint64(codec.base & 0xFFFFFFFFFFFFFFFF) + np.uint64(codec.scale) * u
         return (v.view(np.int64) if dtype == 2 else v.astype(np.uint8)).reshape(-1, 1)
+    if codec.name == "delta":
+        v = np.uint64(codec.base & 0xFFFFFFFFFFFFFFFF) + np.cumsum(np.uint64(codec.scale) * u, dtype=np.uint64)
+        return v.view(np.int64).reshape(-1, 1)
     return ((codec.base + u.astype(np.int64)).astype(np.float64) / np.float64(codec.scale)).reshape(-1, 1)
 
 
@@ -37,6 +40,10 @@ def cases():
     yield "keys", 2, rng.integers(1, 2_000_001, n), "for", 21
     yield "negative", 2, rng.integers(-(2**40), -(2**40) + 70_000, n), "for", 17
     yield "const", 2, np.full(n, -7, dtype=np.int64), "for", 1
+    yield "sorted_runs", 2, np.repeat(np.arange(1, n // 4 + 2), 4)[:n], "delta", 1  # lineitem's l_orderkey
+    yield "dense_seq", 2, np.arange(5, n + 5), "delta", 1
+    yield "sorted_gaps", 2, np.cumsum(rng.integers(0, 4, n)) * 8 - 2**62, "delta", 2
+    yield "one_row", 2, np.array([123456789], dtype=np.int64), "raw", 0  # packed would not be smaller
     yield "wide32", 2, rng.integers(0, 2**32, n), "for", 32
     yield "flags", 4, np.array([65, 78, 82], dtype=np.uint8)[rng.integers(0, 3, n)], "for", 5
     yield "extremes", 2, np.array([-(2**63), 2**63 - 1, 0], dtype=np.int64), "raw", 0
@@ -60,7 +67,7 @@ def test_encoder_lossless(name, dtype, arr, want, width):
     arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
     codec, payload = tqp.encode_column(arr, dtype)
     assert codec.name == want, (name, codec.name)
-    if want in ("for", "dec", "dict"):
+    if want in ("for", "dec", "dict", "delta"):
         assert codec.width == width, (name, codec.width)
     if want != "raw":
         assert payload.nbytes < arr.nbytes
