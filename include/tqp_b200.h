@@ -130,10 +130,13 @@ tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_
  *   DELTA int64 vector in non-decreasing order (sorted keys): code i is
  *         (v_i - v_(i-1)) / scale (code 0 is 0), base = v_0; decoded by a
  *         device prefix sum
+ *   ROWDICT STR8 / BOOL rows of any width with <= 256 distinct rows: the
+ *         dict_n rows (ascending bytes, padded to 8 B) then the codes
  * Codes u are bit-packed, `width` bits each (1..32), little endian in
  * 32-bit words, plus one spare word: 4 * (ceil(rows * width / 32) + 1) B.
  * Lossless by construction: the encoder verifies every value. */
-typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3, TQP_CODEC_DELTA = 4 } tqp_codec_kind;
+typedef enum { TQP_CODEC_RAW = 0, TQP_CODEC_FOR = 1, TQP_CODEC_DICT = 2, TQP_CODEC_DEC = 3, TQP_CODEC_DELTA = 4,
+               TQP_CODEC_ROWDICT = 5 } tqp_codec_kind;
 typedef struct {
   int32_t codec;  /* tqp_codec_kind */
   int32_t width;  /* bits per code (1..32), FOR / DICT / DEC */

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -274,6 +275,51 @@ int64_t try_dec(const double* v, int64_t n, void* out, int64_t cap, tqp_codec* c
   return -1;
 }
 
+// ROWDICT over byte rows (STR8 / BOOL, any width): <= 256 distinct rows of
+// `cols` bytes, the dictionary rows (ascending bytes) then the codes.
+int64_t try_rowdict(const uint8_t* v, int64_t n, int64_t cols, void* out, int64_t cap, tqp_codec* c) {
+  if (n == 0) return -1;
+  const int nt = host_threads(n);
+  std::vector<std::vector<std::string>> sets(nt);
+  std::vector<char> over(nt, 0);
+  parallel_chunks(n, [&](int t, int64_t a, int64_t b) {
+    std::vector<std::string>& s = sets[t];
+    std::string row(static_cast<size_t>(cols), '\0');
+    for (int64_t i = a; i < b; ++i) {
+      row.assign(reinterpret_cast<const char*>(v + i * cols), static_cast<size_t>(cols));
+      if (std::find(s.begin(), s.end(), row) == s.end()) {
+        if (s.size() >= 256) {
+          over[t] = 1;
+          return;
+        }
+        s.push_back(row);
+      }
+    }
+  });
+  for (char o : over)
+    if (o) return -1;
+  std::vector<std::string> dict;
+  for (auto& s : sets) dict.insert(dict.end(), s.begin(), s.end());
+  std::sort(dict.begin(), dict.end());
+  dict.erase(std::unique(dict.begin(), dict.end()), dict.end());
+  if (dict.size() > 256) return -1;
+  const int w = bits_for(dict.size() - 1);
+  const int64_t dict_bytes = (static_cast<int64_t>(dict.size()) * cols + 7) & ~int64_t(7);
+  const int64_t bytes = dict_bytes + packed_bytes(n, w);
+  if (bytes > cap) return -1;
+  unsigned char* o = static_cast<unsigned char*>(out);
+  std::memset(o, 0, static_cast<size_t>(dict_bytes));
+  for (size_t d = 0; d < dict.size(); ++d) std::memcpy(o + d * cols, dict[d].data(), static_cast<size_t>(cols));
+  pack_codes(n, w, reinterpret_cast<uint32_t*>(o + dict_bytes), [&](int64_t i) {
+    const std::string row(reinterpret_cast<const char*>(v + i * cols), static_cast<size_t>(cols));
+    return static_cast<uint64_t>(std::lower_bound(dict.begin(), dict.end(), row) - dict.begin());
+  });
+  c->codec = TQP_CODEC_ROWDICT;
+  c->width = w;
+  c->dict_n = static_cast<int32_t>(dict.size());
+  return bytes;
+}
+
 // ---- device: decoders ------------------------------------------------------------
 __device__ __forceinline__ uint32_t unpack(const uint32_t* __restrict__ words, int64_t i, int w) {
   const int64_t bit = i * w;
@@ -293,6 +339,14 @@ __global__ void k_delta_finish(const int64_t* __restrict__ excl, const int64_t* 
                                int64_t base, int64_t* __restrict__ out) {
   for (int64_t i = gtid(); i < n; i += gstride())
     out[i] = static_cast<int64_t>(static_cast<uint64_t>(base) + static_cast<uint64_t>(excl[i]) + static_cast<uint64_t>(step[i]));
+}
+
+__global__ void k_decode_rowdict(const uint8_t* __restrict__ dict, const uint32_t* __restrict__ words, int w,
+                                 int64_t n, int64_t cols, uint8_t* __restrict__ out) {
+  for (int64_t e = gtid(); e < n * cols; e += gstride()) {
+    const int64_t r = e / cols;
+    out[e] = dict[static_cast<int64_t>(unpack(words, r, w)) * cols + (e - r * cols)];
+  }
 }
 
 __global__ void k_decode_dec(const uint32_t* __restrict__ words, int w, int64_t n, int64_t base, double scale,
@@ -330,9 +384,16 @@ int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, vo
     if (d.bits && (!f.bits || d.bits < f.bits) && packed_bytes(rows, d.bits) <= lim) return pack_delta(v, rows, d, out, c);
     if (f.bits && packed_bytes(rows, f.bits) <= lim) return pack_for(v, rows, f, out, c);
   }
-  if (cols == 1 && rows > 0 && (dtype == TQP_STR8 || dtype == TQP_BOOL)) {  // one-byte values (flags, codes)
-    const int64_t b = try_for(static_cast<const uint8_t*>(host), rows, out, std::min(cap, raw - 1), c);
+  if (rows > 0 && (dtype == TQP_STR8 || dtype == TQP_BOOL)) {
+    // byte rows: a row dictionary (<= 256 distinct rows), else one-byte
+    // values by FOR
+    const auto* v = static_cast<const uint8_t*>(host);
+    int64_t b = try_rowdict(v, rows, cols, out, std::min(cap, raw - 1), c);
     if (b >= 0) return b;
+    if (cols == 1) {
+      b = try_for(v, rows, out, std::min(cap, raw - 1), c);
+      if (b >= 0) return b;
+    }
   }
   if (cols == 1 && rows > 0 && dtype == TQP_F64) {
     // DICT first (8 B x entries + 1 B per row); DEC can only beat it at one
@@ -368,7 +429,11 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
     throw Error(TQP_ERR_ARG, "codec: bad DICT column");
   if (k.codec == TQP_CODEC_DELTA && !(vec && dtype == TQP_I64 && w_ok && bytes == packed_bytes(rows, k.width)))
     throw Error(TQP_ERR_ARG, "codec: bad DELTA column");
-  if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_DELTA) throw Error(TQP_ERR_ARG, "codec: unknown codec");
+  const int64_t rd_bytes = (static_cast<int64_t>(k.dict_n) * cols + 7) & ~int64_t(7);
+  if (k.codec == TQP_CODEC_ROWDICT && !(byte_col && w_ok && k.dict_n >= 1 && k.dict_n <= 256 &&
+                                        bytes == rd_bytes + packed_bytes(rows, k.width)))
+    throw Error(TQP_ERR_ARG, "codec: bad ROWDICT column");
+  if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_ROWDICT) throw Error(TQP_ERR_ARG, "codec: unknown codec");
   Tensor out = c.alloc(dtype, rows, cols);
   auto staged = c.alloc_bytes(static_cast<size_t>(bytes));
   if (bytes) TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, c.stream));
@@ -389,6 +454,10 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
     Tensor excl = k::prefix_sum_raw(c, steps, &ovf);
     if (ovf >= 0) throw Error(TQP_ERR_ARG, "codec: DELTA column overflows int64");
     k_delta_finish<<<grid, 256, 0, c.stream>>>(excl.ptr<int64_t>(), steps.ptr<int64_t>(), rows, k.base, out.ptr<int64_t>());
+  } else if (k.codec == TQP_CODEC_ROWDICT) {
+    const auto* dict = static_cast<const uint8_t*>(staged->ptr);
+    k_decode_rowdict<<<c.grid_for(rows * cols, 256, 4), 256, 0, c.stream>>>(
+        dict, reinterpret_cast<const uint32_t*>(dict + rd_bytes), k.width, rows, cols, out.ptr<uint8_t>());
   } else if (k.codec == TQP_CODEC_DEC) {
     k_decode_dec<<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, static_cast<double>(k.scale), out.ptr<double>());
   } else {

@@ -80,7 +80,7 @@ class Codec(C.Structure):
     _fields_ = [("codec", C.c_int32), ("width", C.c_int32), ("base", C.c_int64), ("scale", C.c_int64),
                 ("dict_n", C.c_int32), ("reserved", C.c_int32)]
 
-    NAMES = {0: "raw", 1: "for", 2: "dict", 3: "dec", 4: "delta"}
+    NAMES = {0: "raw", 1: "for", 2: "dict", 3: "dec", 4: "delta", 5: "rowdict"}
 
     @property
     def name(self) -> str:

@@ -8,17 +8,20 @@ import pytest
 from conftest import ROOT  # noqa: F401  (sys.path)
 
 
-def np_decode(codec, payload, dtype, rows):
+def np_decode(codec, payload, dtype, rows, cols=1):
     from paper_2209_04579_b200 import tqp
     if codec.name == "raw":
         return payload.view(tqp.NP_OF[dtype]).reshape(rows, -1) if rows else payload.view(tqp.NP_OF[dtype])
-    off = 8 * codec.dict_n if codec.name == "dict" else 0
+    off = 8 * codec.dict_n if codec.name == "dict" else (((codec.dict_n * cols + 7) // 8) * 8 if codec.name == "rowdict" else 0)
     words = payload[off:].view(np.uint32).astype(np.uint64)
     w = codec.width
     bit = np.arange(rows, dtype=np.uint64) * np.uint64(w)
     wi = (bit >> np.uint64(5)).astype(np.int64)
     two = words[wi] | (words[wi + 1] << np.uint64(32))
     u = (two >> (bit & np.uint64(31))) & np.uint64((1 << w) - 1)
+    if codec.name == "rowdict":
+        d = payload[:codec.dict_n * cols].reshape(codec.dict_n, cols)
+        return d[u.astype(np.int64)]
     if codec.name == "dict":
         d = payload[:off].view(np.uint64)
         return d[u.astype(np.int64)].view(np.float64).reshape(-1, 1)
@@ -45,7 +48,8 @@ def cases():
     yield "sorted_gaps", 2, np.cumsum(rng.integers(0, 4, n)) * 8 - 2**62, "delta", 2
     yield "one_row", 2, np.array([123456789], dtype=np.int64), "raw", 0  # packed would not be smaller
     yield "wide32", 2, rng.integers(0, 2**32, n), "for", 32
-    yield "flags", 4, np.array([65, 78, 82], dtype=np.uint8)[rng.integers(0, 3, n)], "for", 5
+    yield "flags", 4, np.array([65, 78, 82], dtype=np.uint8)[rng.integers(0, 3, n)], "rowdict", 2
+    yield "bytes_many", 4, (np.arange(n) % 251).astype(np.uint8), "raw", 0  # 8-bit codes would not be smaller
     yield "extremes", 2, np.array([-(2**63), 2**63 - 1, 0], dtype=np.int64), "raw", 0
     yield "discount", 3, rng.integers(0, 11, n) / 100.0, "dict", 4
     yield "price", 3, np.round(rng.uniform(900, 105000, n), 2), "dec", 24
@@ -67,7 +71,7 @@ def test_encoder_lossless(name, dtype, arr, want, width):
     arr = np.ascontiguousarray(arr, dtype=tqp.NP_OF[dtype])
     codec, payload = tqp.encode_column(arr, dtype)
     assert codec.name == want, (name, codec.name)
-    if want in ("for", "dec", "dict", "delta"):
+    if want in ("for", "dec", "dict", "delta", "rowdict"):
         assert codec.width == width, (name, codec.width)
     if want != "raw":
         assert payload.nbytes < arr.nbytes
@@ -112,3 +116,35 @@ def test_tpch_from_encoded_columns(ctx):
     for q in ("q1", "q6", "q14", "q3"):
         plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
         compare_tables(tqp.Executor(plan).execute(tables).to_numpy(), gold["results"][q])
+
+
+def test_row_dictionary_multibyte():
+    """ROWDICT over multi-byte string rows (p_type / c_mktsegment shaped):
+    <= 256 distinct rows -> dictionary + codes; more -> RAW."""
+    from paper_2209_04579_b200 import tqp
+    rng = np.random.default_rng(5)
+    words = [w.encode() for w in ("STANDARD", "SMALL", "MEDIUM", "LARGE", "ECONOMY", "PROMO")]
+    rows = np.zeros((100_000, 25), dtype=np.uint8)
+    pick = rng.integers(0, len(words), (rows.shape[0], 3))
+    for i in range(rows.shape[0]):
+        s = b" ".join(words[j] for j in pick[i])[:25]
+        rows[i, :len(s)] = np.frombuffer(s, dtype=np.uint8)
+    codec, payload = tqp.encode_column(rows, tqp.STR8)
+    assert codec.name == "rowdict" and codec.dict_n <= 216
+    np.testing.assert_array_equal(np_decode(codec, payload, tqp.STR8, rows.shape[0], 25), rows)
+    noisy = rng.integers(0, 256, (5000, 10)).astype(np.uint8)
+    codec, payload = tqp.encode_column(noisy, tqp.STR8)
+    assert codec.name == "raw"
+    np.testing.assert_array_equal(payload.reshape(noisy.shape), noisy)
+
+
+@pytest.mark.gpu
+def test_row_dictionary_device(ctx):
+    from paper_2209_04579_b200 import tqp
+    rng = np.random.default_rng(6)
+    rows = np.array([list(b"BUILDING\0\0"), list(b"MACHINERY\0"), list(b"AUTOMOBILE")], dtype=np.uint8)[
+        rng.integers(0, 3, 70_001)]
+    codec, payload = tqp.encode_column(rows, tqp.STR8)
+    assert codec.name == "rowdict"
+    t = tqp.Tensor.from_encoded(codec, payload, tqp.STR8, rows.shape[0], rows.shape[1])
+    np.testing.assert_array_equal(t.numpy(widen_strings=False), rows)
