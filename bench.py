@@ -65,8 +65,10 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled (NVML, every 10 ms) during the
-    timed region; falls back to nvidia-smi when NVML is unavailable."""
+    """SM clocks + throttle reasons sampled (NVML, every 5 ms, plus one sample
+    as the timed region starts and one as it ends) during the timed region;
+    falls back to nvidia-smi when NVML is unavailable. NVML is initialised
+    before the region so the first sample is not lost to its start-up."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
@@ -77,37 +79,50 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
         self.max_mhz = None
-
-    def _run(self):
+        self._nvml = None
         try:
             import pynvml
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((sm, rs))
-                self._stop.wait(0.01)
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nvml = pynvml
         except Exception:  # noqa: BLE001
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip().split(",")
-                    self.max_mhz = float(out[1])
-                    self.samples.append((float(out[0]), int(out[2], 16)))
-                except Exception:  # noqa: BLE001
-                    pass
-                self._stop.wait(0.2)
+            self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            sm = self._nvml.nvmlDeviceGetClockInfo(self._h, self._nvml.NVML_CLOCK_SM)
+            rs = self._nvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.samples.append((sm, rs))
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                              "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip().split(",")
+        self.max_mhz = float(out[1])
+        self.samples.append((float(out[0]), int(out[2], 16)))
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.005 if self._nvml is not None else 0.2)
 
     def __enter__(self):
+        try:
+            self._sample()
+        except Exception:  # noqa: BLE001
+            pass
         self._t.start()
-        time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
+        try:
+            self._sample()
+        except Exception:  # noqa: BLE001
+            pass
         self._stop.set()
         self._t.join(timeout=10)
 
@@ -177,7 +192,7 @@ def cpu_baseline_sample(sf: float):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--ref-sf", type=float, default=1.0)
