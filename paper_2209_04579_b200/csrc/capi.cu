@@ -123,6 +123,10 @@ void tqp_shutdown(tqp_ctx* ctx) {
   if (ctx->c.csv_ring) cudaFreeHost(ctx->c.csv_ring);
   for (auto& e : ctx->c.csv_ring_ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->c.copy_stream) {
+    cudaStreamSynchronize(ctx->c.copy_stream);
+    cudaStreamDestroy(ctx->c.copy_stream);
+  }
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

@@ -436,7 +436,20 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
   if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_ROWDICT) throw Error(TQP_ERR_ARG, "codec: unknown codec");
   Tensor out = c.alloc(dtype, rows, cols);
   auto staged = c.alloc_bytes(static_cast<size_t>(bytes));
-  if (bytes) TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, c.stream));
+  if (bytes) {
+    // the copy runs on the context's copy stream so the uploads of later
+    // columns overlap this column's decode (and whatever else `stream` runs):
+    // copy stream waits for the staging allocation, `stream` for the copy
+    cudaStream_t cs = c.copies();
+    cudaEvent_t ready = c.take_event(), landed = c.take_event();
+    TQP_CUDA(cudaEventRecord(ready, c.stream));
+    TQP_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+    TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, cs));
+    TQP_CUDA(cudaEventRecord(landed, cs));
+    TQP_CUDA(cudaStreamWaitEvent(c.stream, landed, 0));
+    c.give_event(ready);
+    c.give_event(landed);
+  }
   if (!rows) return out;
   const int grid = c.grid_for(rows, 256, 4);
   const auto* words = static_cast<const uint32_t*>(staged->ptr);
@@ -450,9 +463,9 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
     Tensor steps = c.alloc(TQP_I64, rows, 1);
     k_decode_for<int64_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, 0, k.scale, steps.ptr<int64_t>());
     c.count_launch();
-    int64_t ovf = -1;
-    Tensor excl = k::prefix_sum_raw(c, steps, &ovf);
-    if (ovf >= 0) throw Error(TQP_ERR_ARG, "codec: DELTA column overflows int64");
+    // no overflow readback (and so no host round trip): the encoder has
+    // verified that every prefix is a value of the column
+    Tensor excl = k::prefix_sum_unchecked(c, steps);
     k_delta_finish<<<grid, 256, 0, c.stream>>>(excl.ptr<int64_t>(), steps.ptr<int64_t>(), rows, k.base, out.ptr<int64_t>());
   } else if (k.codec == TQP_CODEC_ROWDICT) {
     const auto* dict = static_cast<const uint8_t*>(staged->ptr);

@@ -177,6 +177,21 @@ Tensor prefix_sum_raw(Ctx& c, const Tensor& x, int64_t* first_overflow) {
   return o;
 }
 
+// Exclusive scan without the overflow readback (callers that know the sums fit).
+Tensor prefix_sum_unchecked(Ctx& c, const Tensor& x) {
+  int64_t n = x.rows;
+  Tensor o = c.alloc(TQP_I64, n, 1);
+  if (!n) return o;
+  int64_t tiles = (n + kTile - 1) / kTile;
+  auto s = scan_scratch(c, tiles);
+  auto scratch_err = c.alloc_bytes(32);  // the kernel's overflow word, never read
+  TQP_CUDA(cudaMemsetAsync(scratch_err->ptr, 0x7f, 8, c.stream));
+  k_prefix_sum<<<tiles, kThreads, 0, c.stream>>>(x.ptr<int64_t>(), o.ptr<int64_t>(), n, s.desc, s.counter,
+                                                 static_cast<long long*>(scratch_err->ptr));
+  c.count_launch();
+  return o;
+}
+
 Tensor prefix_sum_exclusive(Ctx& c, const Tensor& x) {
   require(x.is_vector(), "prefix_sum_exclusive: expected a vector (m=1)");
   if (x.dtype != TQP_I64) {

@@ -155,6 +155,13 @@ struct Ctx {
   // timing events are recycled (creating one per launch costs host time
   // between dependent launches)
   std::vector<cudaEvent_t> event_pool;
+  // a second stream for host->device copies that may overlap the work of
+  // `stream` (compressed column uploads); created on first use
+  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copies() {
+    if (!copy_stream) TQP_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    return copy_stream;
+  }
   cudaEvent_t take_event() {
     cudaEvent_t e;
     if (!event_pool.empty()) {
@@ -241,6 +248,7 @@ Tensor str8_to_i32(Ctx&, const Tensor& t);
 Tensor radix_sort_payload(Ctx&, const Tensor& keys, const Tensor* perm, bool descending);
 // exclusive int64 scan; *first_overflow = first overflowing row or -1
 Tensor prefix_sum_raw(Ctx&, const Tensor& x, int64_t* first_overflow);
+Tensor prefix_sum_unchecked(Ctx&, const Tensor& x);
 }  // namespace k
 
 }  // namespace tqp
