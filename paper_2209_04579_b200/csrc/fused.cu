@@ -1142,6 +1142,7 @@ __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int 
 // count) then sums the parts' values with warp_sum_fixed (absent slots
 // contribute +0.0 / 0, which never changes a sum that starts at +0.0).
 constexpr int kFinalSmallThreads = 1024;
+static_assert(kFinalSmallThreads >= kMerged, "one thread per merge slot when compacting the codes");
 __global__ void __launch_bounds__(kFinalSmallThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts,
                                                                     FinalSpec f, int nkeys, void* key_ptr0,
                                                                     void* key_ptr1, void* key_ptr2, void* key_ptr3,
@@ -1180,16 +1181,23 @@ __global__ void __launch_bounds__(kFinalSmallThreads) k_final_small(const SmallP
     }
   }
   __syncthreads();
-  // rank sort of the distinct codes (codes are unique)
-  for (int i = threadIdx.x; i < kMerged; i += blockDim.x) {
-    const unsigned v = s_set[i];
-    if (v == 0xffffffffu) continue;
+  // rank sort of the distinct codes (codes are unique): the occupied slots
+  // are compacted first, so each code is compared with the n codes only
+  __shared__ unsigned s_list[kMerged];
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  if (threadIdx.x < kMerged && s_set[threadIdx.x] != 0xffffffffu) s_list[atomicAdd(&s_n, 1)] = s_set[threadIdx.x];
+  __syncthreads();
+  const int n = s_n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned v = s_list[i];
     int r = 0;
-    for (int j = 0; j < kMerged; ++j) r += s_set[j] < v;
+    for (int j = 0; j < n; ++j) r += s_list[j] < v;
     s_sorted[r] = v;
   }
-  const int n = __syncthreads_count(threadIdx.x < kMerged && s_set[threadIdx.x] != 0xffffffffu);
   if (threadIdx.x == 0) *ngroups_out = n;
+  __syncthreads();
   for (int c = threadIdx.x; c < nparts; c += blockDim.x) {
 #pragma unroll
     for (int sl = 0; sl < kGroups; ++sl) {
@@ -2239,16 +2247,18 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
   bool zero_free = true;
   for (int i = 0; i < t.litlen; ++i) zero_free = zero_free && t.lit[i] != 0;
   const std::string p = "(" + sref + ".ptr + " + row + " * " + std::to_string(t.width) + "LL)";
+  // byte compares joined with `&` (no short circuit): every byte load of
+  // the row is independent and in flight at once (the row is in bounds)
   auto prefix_eq = [&](int n) {
     std::string e = "true";
-    for (int i = 0; i < n; ++i) e += " && __ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(t.lit[i]) + "u";
+    for (int i = 0; i < n; ++i) e += " & (__ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(t.lit[i]) + "u)";
     return e;
   };
   if (t.is_like && zero_free && t.litlen <= t.width) {
     if (t.anchor == TQP_START) return "(" + prefix_eq(t.litlen) + ")";
     if (t.anchor == TQP_EXACT) {
       std::string e = prefix_eq(t.litlen);
-      if (t.litlen < t.width) e += " && __ldg(" + p + " + " + std::to_string(t.litlen) + ") == 0u";
+      if (t.litlen < t.width) e += " & (__ldg(" + p + " + " + std::to_string(t.litlen) + ") == 0u)";
       return "(" + e + ")";
     }
   }
@@ -2256,7 +2266,7 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
     // zero-extended equality over max(width, litlen) = width bytes
     std::string e = "true";
     for (int i = 0; i < t.width; ++i)
-      e += " && __ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(i < t.litlen ? t.lit[i] : 0) + "u";
+      e += " & (__ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(i < t.litlen ? t.lit[i] : 0) + "u)";
     return "(" + e + ")";
   }
   return "eval_str(" + sref + ", " + row + ")";
