@@ -741,10 +741,16 @@ class Executor:
         return json.loads(lib.tqp_executor_explain(self.h).decode())
 
     def _args(self, tables: Mapping[str, Table]):
-        names = list(tables.keys())
-        n = len(names)
-        cn = (C.c_char_p * max(1, n))(*[x.encode() for x in names])
-        th = (C.c_void_p * max(1, n))(*[tables[x].h for x in names])
+        # the ctypes arrays are rebuilt only when the table set changes (a
+        # repeated query over the same tables skips their construction)
+        key = tuple((name, t.h) for name, t in tables.items())
+        cached = getattr(self, "_args_cache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        n = len(key)
+        cn = (C.c_char_p * max(1, n))(*[name.encode() for name, _ in key])
+        th = (C.c_void_p * max(1, n))(*[h for _, h in key])
+        self._args_cache = (key, (cn, th, n))
         return cn, th, n
 
     def execute(self, tables: Mapping[str, Table]) -> Result:
