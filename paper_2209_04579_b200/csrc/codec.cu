@@ -15,6 +15,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <string_view>
 #include <thread>
 #include <vector>
 
@@ -311,8 +312,10 @@ int64_t try_rowdict(const uint8_t* v, int64_t n, int64_t cols, void* out, int64_
   std::memset(o, 0, static_cast<size_t>(dict_bytes));
   for (size_t d = 0; d < dict.size(); ++d) std::memcpy(o + d * cols, dict[d].data(), static_cast<size_t>(cols));
   pack_codes(n, w, reinterpret_cast<uint32_t*>(o + dict_bytes), [&](int64_t i) {
-    const std::string row(reinterpret_cast<const char*>(v + i * cols), static_cast<size_t>(cols));
-    return static_cast<uint64_t>(std::lower_bound(dict.begin(), dict.end(), row) - dict.begin());
+    const std::string_view row(reinterpret_cast<const char*>(v + i * cols), static_cast<size_t>(cols));
+    return static_cast<uint64_t>(
+        std::lower_bound(dict.begin(), dict.end(), row, [](const std::string& a, std::string_view b) { return a < b; }) -
+        dict.begin());
   });
   c->codec = TQP_CODEC_ROWDICT;
   c->width = w;
@@ -378,8 +381,7 @@ int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, vo
   // next, and RAW (below) overwrites whatever a failed attempt wrote
   if (cols == 1 && rows > 0 && dtype == TQP_I64) {
     const auto* v = static_cast<const int64_t*>(host);
-    static const bool no_delta = std::getenv("TQP_CODEC_NO_DELTA") != nullptr;  // experiment knob
-    const ForPlan f = plan_for(v, rows), d = no_delta ? ForPlan{} : plan_delta(v, rows);
+    const ForPlan f = plan_for(v, rows), d = plan_delta(v, rows);
     const int64_t lim = std::min(cap, raw - 1);
     if (d.bits && (!f.bits || d.bits < f.bits) && packed_bytes(rows, d.bits) <= lim) return pack_delta(v, rows, d, out, c);
     if (f.bits && packed_bytes(rows, f.bits) <= lim) return pack_for(v, rows, f, out, c);

@@ -117,17 +117,7 @@ Tensor Ctx::alloc(int dtype, int64_t rows, int64_t cols) {
   return t;
 }
 
-void Ctx::sync() {
-  static const bool poll = std::getenv("TQP_SYNC_POLL") != nullptr;  // experiment: busy-poll the stream
-  if (poll) {
-    cudaError_t e;
-    while ((e = cudaStreamQuery(stream)) == cudaErrorNotReady) {
-    }
-    TQP_CUDA(e);
-    return;
-  }
-  TQP_CUDA(cudaStreamSynchronize(stream));
-}
+void Ctx::sync() { TQP_CUDA(cudaStreamSynchronize(stream)); }
 
 void Ctx::reset_err() {
   TQP_CUDA(cudaMemcpyAsync(d_err, h_err + kPinnedErrInit, 3 * sizeof(long long), cudaMemcpyHostToDevice, stream));
