@@ -17,6 +17,9 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <new>
+#include <type_traits>
+#include <mutex>
 #include <set>
 #include <sstream>
 
@@ -2367,8 +2370,72 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
   return o.str();
 }
 
+// Memo of the last kernel generated per call site of a fused unit. The
+// generators are pure functions of their arguments, so byte-identical
+// arguments (the same query over the same tables: pointers, ranges and
+// constants all equal) reuse the kernel without generating its source
+// again; any difference - or a padding byte that differs - regenerates.
+struct JitMemo {
+  std::mutex mu;
+  std::map<int, std::pair<std::string, const void*>> last;  // site -> (argument bytes, kernel)
+  template <typename Make>
+  const void* get(int site, const std::string& key, Make&& make) {
+    std::lock_guard<std::mutex> l(mu);
+    auto it = last.find(site);
+    if (it != last.end() && it->second.first == key) return it->second.second;
+    const void* fn = make();
+    last[site] = {key, fn};
+    return fn;
+  }
+};
+template <typename T>
+void append_bytes(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+// re-creates a default-initialised spec over zeroed storage, so the padding
+// between its members is zero and stays zero (member assignments do not
+// touch it): byte-identical specs then compare equal
+template <typename T>
+void zero_padding(T& v) {
+  static_assert(std::is_trivially_copyable_v<T> && std::is_trivially_destructible_v<T>, "plain spec structs only");
+  std::memset(static_cast<void*>(&v), 0, sizeof(T));
+  ::new (static_cast<void*>(&v)) T();
+}
+
+// memo keys: the generators' argument bytes without the per-execution
+// buffers (partials, group records, build tables, presence bitmaps, error
+// words), which the generated code only reaches through the kernel
+// parameter, never as literals
+std::string tile_key(TileSpec t) {
+  t.p.part = nullptr;
+  t.p.gacc = t.p.gcnt = nullptr;
+  t.p.touched = nullptr;
+  t.p.err = nullptr;
+  for (auto& pr : t.p.probes) {
+    pr.table = nullptr;
+    pr.bitmap = nullptr;
+  }
+  std::string k;
+  append_bytes(k, t);
+  return k;
+}
+std::string build_key(BuildSpec b) {
+  b.table = nullptr;
+  b.bitmap = nullptr;
+  b.zrec = nullptr;
+  b.err = nullptr;
+  for (auto& pr : b.probes) {
+    pr.table = nullptr;
+    pr.bitmap = nullptr;
+  }
+  std::string k;
+  append_bytes(k, b);
+  return k;
+}
+
 struct Runner {
   PipeDesc P;
+  std::shared_ptr<JitMemo> memo = std::make_shared<JitMemo>();
 
   bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, UnitPending* pend) const {
     return run(c, &slots, tables, nullptr, false, pend);
@@ -2470,6 +2537,7 @@ struct Runner {
       long long range = n ? mm[2 * bi + 1] - mm[2 * bi] + 1 : 1;
       if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
       BuildSpec bs;
+      zero_padding(bs);  // its bytes key the kernel memo
       bs.n = n;
       bs.kmin = n ? mm[2 * bi] : 0;
       bs.range = range;
@@ -2586,9 +2654,9 @@ struct Runner {
         if (bk && jit_wanted(n)) {
           rows_per_thread = jit_build_rows();
           hp.mark("bprep");
-          const std::string src = gen_build(bs);
-          hp.mark("bgen");
-          bk = jit_kernel(src, "q_build");
+          std::string key = build_key(bs);
+          append_bytes(key, rows_per_thread);
+          bk = memo->get(static_cast<int>(bi), key, [&] { return jit_kernel(gen_build(bs), "q_build"); });
           hp.mark("bjit");
         }
         if (bk) {
@@ -2613,6 +2681,7 @@ struct Runner {
     const Table* fact = bind_table(tables, P.fact_table);
     if (!fact) return false;
     ProbeSpec ps;
+    zero_padding(ps);
     ps.n = fact->rows;
     ps.err = err;
     bool ok = true;
@@ -2702,6 +2771,7 @@ struct Runner {
         if (ps.acc[a].f[i].kind != FK_CONST && ps.acc[a].f[i].x.src >= 0) return false;
     // distinct fact columns staged per tile; operands address them by index
     TileSpec ts;
+    zero_padding(ts);
     auto col_index = [&](Operand& o) {
       if (o.src >= 0 || !o.ptr) return true;
       const int w = o.type == OT_U8 ? 1 : 8;
@@ -2751,8 +2821,7 @@ struct Runner {
     }
     if (ts.stage_bytes == 0) ts.stage_bytes = 128;
     // as many stages as fit next to the fixed (static + staging) parts
-    int optin = 0;
-    TQP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    const int optin = c.smem_optin();
     cudaFuncAttributes fa{};
     const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
     const void* kfn = tile_kernel(P.mode, ps.nacc);
@@ -2764,12 +2833,15 @@ struct Runner {
       ts.p = ps;
       const int cw = wide ? wide_cw : P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::CW : TileShape<MODE_SCALAR>::CW;
       hp.mark("tprep");
-      const std::string src = gen_pipeline(ts, P.mode, cw, bm, wide ? kWideSlots : kGroups, regacc);
+      const int slots = wide ? kWideSlots : kGroups;
+      std::string key = tile_key(ts);
+      for (int v : {static_cast<int>(P.mode), cw, slots, regacc ? 1 : 0}) append_bytes(key, v);
+      for (int v : bm) append_bytes(key, v);
+      kfn = memo->get(-1, key, [&] { return jit_kernel(gen_pipeline(ts, P.mode, cw, bm, slots, regacc), "q_tile"); });
       hp.mark("tgen");
-      kfn = jit_kernel(src, "q_tile");
     }
     hp.mark("gen");
-    TQP_CUDA(cudaFuncGetAttributes(&fa, kfn));
+    fa.sharedSizeBytes = c.static_smem(kfn);
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
     if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
     ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
@@ -2988,8 +3060,7 @@ struct Runner {
       if (!kern || k > kTopkMaxK || gs.nsort < 1) return false;
       // one wave: as many blocks as are resident at once (the last block
       // merges one value list per block)
-      int per_sm = 1;
-      TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern), kTopkThreads, 0));
+      const int per_sm = c.blocks_per_sm(reinterpret_cast<const void*>(kern), kTopkThreads);
       const int blocks = static_cast<int>(std::max<long long>(
           1, std::min<long long>({static_cast<long long>(std::max(1, std::min(per_sm, 2))) * c.num_sms,
                                   (ngroups + 8191) / 8192, static_cast<long long>(kTopkStage / std::max(1, k))})));

@@ -187,6 +187,30 @@ struct Ctx {
     cudaEventRecord(e, stream);
     kernel_events.push_back({name, {start, e}});
   }
+  // per-device opt-in shared memory and per-kernel static shared memory,
+  // queried once (driver calls between a unit's kernels are host time)
+  int smem_optin_ = -1;
+  std::map<const void*, size_t> static_smem_;
+  int smem_optin() {
+    if (smem_optin_ < 0) TQP_CUDA(cudaDeviceGetAttribute(&smem_optin_, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    return smem_optin_;
+  }
+  size_t static_smem(const void* kernel) {
+    auto it = static_smem_.find(kernel);
+    if (it != static_smem_.end()) return it->second;
+    cudaFuncAttributes fa{};
+    TQP_CUDA(cudaFuncGetAttributes(&fa, kernel));
+    return static_smem_[kernel] = fa.sharedSizeBytes;
+  }
+  std::map<std::pair<const void*, int>, int> occupancy_;
+  int blocks_per_sm(const void* kernel, int threads) {  // no dynamic shared memory
+    auto key = std::make_pair(kernel, threads);
+    auto it = occupancy_.find(key);
+    if (it != occupancy_.end()) return it->second;
+    int n = 1;
+    TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, 0));
+    return occupancy_[key] = n;
+  }
   // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, size)
   std::map<const void*, int> smem_set;
   cudaError_t ensure_smem(const void* kernel, int bytes) {
