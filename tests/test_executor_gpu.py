@@ -126,3 +126,30 @@ def test_q14_scalar_epilogue(ctx):
     with pytest.raises(tqp.ExecError) as ei:
         ex.finish([ex.execute_partial(empty)])
     assert str(ei.value) == msgs[0]
+
+
+def test_one_executor_over_several_table_sets(ctx):
+    """An executor reused across table sets (its per-unit kernel memo keyed by
+    the generator arguments) gives each table set the result a fresh executor
+    gives it, in either order and repeatedly."""
+    from paper_2209_04579_b200 import tqp
+    import os
+    old = os.environ.get("TQP_JIT")
+    os.environ["TQP_JIT"] = "1"  # the NVRTC kernels (and their memo) at test sizes
+    try:
+        sets = [{n: tqp.Table.generate(n, sf, seed) for n in ("lineitem", "orders", "customer", "part")}
+                for sf, seed in ((0.02, 7), (0.02, 8), (0.03, 7))]
+        for q in ("q1", "q6", "q14", "q3"):
+            plan = json.loads((PLANS / f"{q}.opplan.json").read_text())
+            fresh = [as_numpy(tqp.Executor(plan).execute(t)) for t in sets]
+            ex = tqp.Executor(plan)
+            for i in (0, 1, 2, 1, 0, 0, 2):
+                got = as_numpy(ex.execute(sets[i]))
+                for (n, _, g), (_, _, w) in zip(got, fresh[i]):
+                    np.testing.assert_array_equal(g, w, err_msg=f"{q} set {i} {n}")
+            assert ex.fallbacks == 0
+    finally:
+        if old is None:
+            del os.environ["TQP_JIT"]
+        else:
+            os.environ["TQP_JIT"] = old
