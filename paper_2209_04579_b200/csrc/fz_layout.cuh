@@ -162,21 +162,37 @@ struct BuildSpec {
   long long* err = nullptr;
 };
 
-// Presence bit of one inserted row: one atomicOr per row (measured faster
-// than OR-reducing the lanes that share a word with __match_any_sync: the
-// Q3 orders build 110 -> 104 us). Two inserted rows with one key (a 1:N
-// join, outside the fused contract) show up as a bit the word already held,
-// whichever lane or warp comes second; the atomic's old word is returned in
-// `old` (with the bit in `set`) and only checked by build_dup_check after
-// the thread's last row, so no row waits on the atomic's return.
+// Presence bits of one insert round of a warp. Sparse rounds (few lanes
+// inserting, e.g. Q3's orders build at a 10 % pass rate) issue one atomicOr
+// per row; dense rounds (every row of an unfiltered build, e.g. Q14's part)
+// first OR-reduce the lanes that share a word (__match_any_sync) so one
+// lane sets them - per-row atomics there would hit one word 32 times. Two
+// inserted rows with one key (a 1:N join, outside the fused contract) show
+// up as a bit the word already held, or inside a dense round as fewer bits
+// than lanes; the atomic's old word is returned in `old` (with the bits in
+// `set`) and only checked by build_dup_check after the thread's last round,
+// so no round waits on the atomic's return. Orders build 110 -> 104 us with
+// the sparse form; the part build keeps the dense one.
 __device__ __forceinline__ void presence_insert(unsigned* bitmap, long long idx, unsigned& old, unsigned& set,
                                                 unsigned& dup) {
-  (void)dup;
   old = 0u;
   set = 0u;
-  if (idx >= 0) {  // one atomic per inserted row: a repeated key sees its bit set
-    set = 1u << (idx & 31);
-    old = atomicOr(bitmap + (idx >> 5), set);
+  const unsigned active = __ballot_sync(0xffffffffu, idx >= 0);
+  if (__popc(active) < 8) {  // warp-uniform
+    if (idx >= 0) {
+      set = 1u << (idx & 31);
+      old = atomicOr(bitmap + (idx >> 5), set);
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, word);
+  const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
+  if (idx >= 0 && lane == __ffs(peers) - 1) {
+    old = atomicOr(bitmap + word, bits);
+    set = bits;
+    dup |= __popc(bits) != __popc(peers) ? 1u : 0u;
   }
 }
 __device__ __forceinline__ void build_dup_check(unsigned dup, long long* err) {
