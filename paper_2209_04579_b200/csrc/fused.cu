@@ -1145,12 +1145,30 @@ __global__ void k_final_scalar(const unsigned long long* __restrict__ part, int 
 // count) then sums the parts' values with warp_sum_fixed (absent slots
 // contribute +0.0 / 0, which never changes a sum that starts at +0.0).
 constexpr int kFinalSmallThreads = 1024;
+constexpr size_t kFinalSmallStageMax = 180 * 1024;  // dynamic shared memory for staged parts
 static_assert(kFinalSmallThreads >= kMerged, "one thread per merge slot when compacting the codes");
-__global__ void __launch_bounds__(kFinalSmallThreads) k_final_small(const SmallPart* __restrict__ parts, int nparts,
+// kStaged: the parts (and the rank table) are first copied into dynamic
+// shared memory with every load in flight at once, so the phases below make
+// no further global round trips (Q1: 148 parts, 90 KB); otherwise (many
+// shards' parts) they are read from global memory in place.
+template <bool kStaged>
+__global__ void __launch_bounds__(kFinalSmallThreads) k_final_small(const SmallPart* __restrict__ parts_g, int nparts,
                                                                     FinalSpec f, int nkeys, void* key_ptr0,
                                                                     void* key_ptr1, void* key_ptr2, void* key_ptr3,
-                                                                    int* rank /*[nparts][kGroups]*/,
+                                                                    int* rank_g /*[nparts][kGroups]*/,
                                                                     long long* ngroups_out, long long* err) {
+  extern __shared__ __align__(16) unsigned char s_parts_raw[];
+  const SmallPart* parts = parts_g;
+  int* rank = rank_g;
+  if constexpr (kStaged) {
+    const int n16 = static_cast<int>(nparts * sizeof(SmallPart) / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(parts_g);
+    uint4* dst = reinterpret_cast<uint4*>(s_parts_raw);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+    parts = reinterpret_cast<const SmallPart*>(s_parts_raw);
+    rank = reinterpret_cast<int*>(s_parts_raw + nparts * sizeof(SmallPart));
+    __syncthreads();
+  }
   __shared__ unsigned s_set[kMerged];
   __shared__ unsigned s_sorted[kMerged];
   __shared__ unsigned long long s_tot[kMerged][kMaxAcc + 1];
@@ -3021,8 +3039,19 @@ struct Runner {
     void* kp[4] = {nullptr, nullptr, nullptr, nullptr};
     for (size_t j = 0; j < P.outs.size(); ++j)
       if (P.outs[j].fn >= 10) kp[P.outs[j].fn - 10] = outs[j].data();
-    k_final_small<<<1, kFinalSmallThreads, 0, c.stream>>>(parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()),
-                                                kp[0], kp[1], kp[2], kp[3], static_cast<int*>(rank->ptr), err + 2, err);
+    const size_t staged = nparts * (sizeof(SmallPart) + sizeof(int) * kGroups);
+    static_assert(sizeof(SmallPart) % 16 == 0, "staged copy moves 16-byte vectors");
+    const bool stage = staged <= kFinalSmallStageMax && reinterpret_cast<uintptr_t>(parts) % 16 == 0 &&
+                       c.ensure_smem(reinterpret_cast<const void*>(&k_final_small<true>), static_cast<int>(staged)) ==
+                           cudaSuccess;
+    if (stage)
+      k_final_small<true><<<1, kFinalSmallThreads, staged, c.stream>>>(
+          parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()), kp[0], kp[1], kp[2], kp[3],
+          static_cast<int*>(rank->ptr), err + 2, err);
+    else
+      k_final_small<false><<<1, kFinalSmallThreads, 0, c.stream>>>(
+          parts, static_cast<int>(nparts), fs, static_cast<int>(P.key_columns.size()), kp[0], kp[1], kp[2], kp[3],
+          static_cast<int*>(rank->ptr), err + 2, err);
     c.count_launch();
     return -1;  // on the device (err[2]); read with the error flag
   }
