@@ -2268,13 +2268,23 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
   bool zero_free = true;
   for (int i = 0; i < t.litlen; ++i) zero_free = zero_free && t.lit[i] != 0;
   const std::string p = "(" + sref + ".ptr + " + row + " * " + std::to_string(t.width) + "LL)";
-  // byte compares joined with `&` (no short circuit): every byte load of
-  // the row is independent and in flight at once (the row is in bounds)
-  auto prefix_eq = [&](int n) {
+  // compares joined with `&` (no short circuit): every load of the row is
+  // independent and in flight at once (the row is in bounds). With an even
+  // row width every row starts 2-byte aligned (columns are 256-byte
+  // aligned), so byte pairs load as one 16-bit word
+  const bool even = t.width % 2 == 0;
+  auto byte_at = [&](int i) { return i < t.litlen ? static_cast<unsigned>(t.lit[i]) : 0u; };
+  auto bytes_eq = [&](int n, auto&& want) {
     std::string e = "true";
-    for (int i = 0; i < n; ++i) e += " & (__ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(t.lit[i]) + "u)";
+    int i = 0;
+    if (even)
+      for (; i + 1 < n; i += 2)
+        e += " & (__ldg(reinterpret_cast<const unsigned short*>(" + p + " + " + std::to_string(i) + ")) == " +
+             std::to_string(want(i) | (want(i + 1) << 8)) + "u)";
+    for (; i < n; ++i) e += " & (__ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(want(i)) + "u)";
     return e;
   };
+  auto prefix_eq = [&](int n) { return bytes_eq(n, byte_at); };
   if (t.is_like && zero_free && t.litlen <= t.width) {
     if (t.anchor == TQP_START) return "(" + prefix_eq(t.litlen) + ")";
     if (t.anchor == TQP_EXACT) {
@@ -2285,10 +2295,7 @@ std::string str_pred(const StrTerm& t, const std::string& sref, const std::strin
   }
   if (!t.is_like && t.op == TQP_EQ && t.litlen <= t.width) {
     // zero-extended equality over max(width, litlen) = width bytes
-    std::string e = "true";
-    for (int i = 0; i < t.width; ++i)
-      e += " & (__ldg(" + p + " + " + std::to_string(i) + ") == " + std::to_string(i < t.litlen ? t.lit[i] : 0) + "u)";
-    return "(" + e + ")";
+    return "(" + bytes_eq(t.width, byte_at) + ")";
   }
   return "eval_str(" + sref + ", " + row + ")";
 }
