@@ -148,3 +148,20 @@ def test_row_dictionary_device(ctx):
     assert codec.name == "rowdict"
     t = tqp.Tensor.from_encoded(codec, payload, tqp.STR8, rows.shape[0], rows.shape[1])
     np.testing.assert_array_equal(t.numpy(widen_strings=False), rows)
+
+
+def test_codec_argument_errors():
+    """Bad shapes, a too-small output buffer and a mismatched payload fail
+    with a status instead of writing out of bounds."""
+    from paper_2209_04579_b200 import tqp
+    import ctypes as C
+    a = np.arange(1000, dtype=np.int64)
+    out = np.empty(16, dtype=np.uint8)
+    codec, st = tqp.Codec(), tqp.Status()
+    n = tqp.lib.tqp_codec_encode(tqp.I64, 1000, 1, a.ctypes.data, out.ctypes.data, out.nbytes, C.byref(codec),
+                                 C.byref(st))
+    assert n == -1 and st.code != 0  # RAW would need 8000 bytes; packed codes need more than 16
+    n = tqp.lib.tqp_codec_encode(tqp.I64, -1, 1, a.ctypes.data, out.ctypes.data, out.nbytes, C.byref(codec),
+                                 C.byref(st))
+    assert n == -1 and b"shape" in st.msg
+    assert tqp.lib.tqp_codec_bound(tqp.I64, 10, 0) == -1
