@@ -2569,8 +2569,11 @@ struct Runner {
       auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
       // a filtered build's table is only read where its presence bit is set
       // (probe_lookup and every generated probe check the bitmap first), so
-      // only an unfiltered one, read as `entry != 0`, needs zeroed slots
-      if (!build_filtered(B))
+      // only an unfiltered one, read as `entry != 0`, needs zeroed slots -
+      // and not even that when its n unique keys fill all n slots of the
+      // range (a repeated key leaves a slot unwritten, but it is flagged as
+      // a duplicate and the unit is discarded)
+      if (!build_filtered(B) && range != n)
         TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
