@@ -6,5 +6,5 @@ run() {  # seed jit
   echo "$out" | grep -q " 0 failure(s)" || echo "$out" > gpurun_out/rand_fail_$1_$2.txt
 }
 export -f run
-( for s in $(seq 300 339); do echo "$s 0"; echo "$s 1"; done ) | xargs -P 8 -n 2 bash -c 'run "$0" "$1"' | sort -t= -k2 -n > gpurun_out/random_sweep.txt
+( for s in $(seq ${SEED0:-300} $(( ${SEED0:-300} + 39 ))); do echo "$s 0"; echo "$s 1"; done ) | xargs -P 8 -n 2 bash -c 'run "$0" "$1"' | sort -t= -k2 -n > gpurun_out/random_sweep.txt
 grep -c " 0 failure" gpurun_out/random_sweep.txt; grep -v " 0 failure" gpurun_out/random_sweep.txt | head
