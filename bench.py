@@ -9,7 +9,14 @@ scanned per second over the four queries (4 x rows per step / step time).
 Inputs per query are 1.9-2.5 GB, far larger than the 126 MB L2, so no L2
 flush is needed between steps. `--impl reference` times the reference's own
 CPU executor (oracle/_ref/tqp_ref_runner, built from /root/reference's
-sources, `par` backend on every host core) on a bounded SF1 sample.
+sources, `par` backend on every host core) on the same configuration (SF10
+suite, same generated tables; --ref-sf overrides), with the step count cut to
+fit --ref-budget-s if needed.
+
+Extra legs on the b200 line (rank 0, N=1): `cold_first_execution_ms` (each
+query's first execution in the process: NVRTC compile included), `q6_sf1`
+(BASELINE config 1), `per_instruction` (the suite with fuse=False),
+`e2e.encode_once_ms` (host encode of the compressed columnar format).
 """
 from __future__ import annotations
 
@@ -136,7 +143,10 @@ class ClockSampler:
 
 
 def run_reference(args, rank: int) -> None:
-    """Reference arm: the reference's CPU executor (par backend, all cores)."""
+    """Reference arm: the reference's CPU executor (par backend, all cores) on
+    the b200 arm's own configuration (the suite at --sf, same generated
+    tables). One SF10 step is ~12 s on 16 cores; if K + W steps would exceed
+    --ref-budget-s the timed count is reduced (stated in the line)."""
     if rank != 0:
         return
     sample_sf = args.ref_sf
@@ -144,26 +154,40 @@ def run_reference(args, rank: int) -> None:
     if not REF_RUNNER.exists():
         print(json.dumps({"impl": "reference", "unavailable": f"{REF_RUNNER} not built (make -C oracle)"}))
         return
+    steps, warmup = args.steps, args.warmup
+    # one untimed probe step sizes the run (its table generation included)
+    probe = subprocess.run([str(REF_RUNNER), "run", "--sf", str(sample_sf), "--queries", ",".join(QUERIES),
+                            "--backend", "par", "--threads", str(cores), "--repeat", "1", "--warmup", "0"],
+                           capture_output=True, text=True, check=True).stdout
+    probe_ms = sum(json.loads(x)["median_ms"] for x in probe.splitlines() if x.startswith("{"))
+    fit = max(2, int(args.ref_budget_s * 1e3 / max(probe_ms, 1.0)))
+    if steps + warmup > fit:
+        warmup = min(warmup, max(1, fit // 4))
+        steps = max(1, fit - warmup)
     cmd = [str(REF_RUNNER), "run", "--sf", str(sample_sf), "--queries", ",".join(QUERIES), "--backend", "par",
-           "--threads", str(cores), "--repeat", str(args.steps), "--warmup", str(args.warmup)]
+           "--threads", str(cores), "--repeat", str(steps), "--warmup", str(warmup)]
     out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
     lines = [json.loads(x) for x in out.splitlines() if x.startswith("{")]
     per_q = {d["query"]: d for d in lines}
     L = lines[0]["lineitem_rows"]
-    step_ms = [sum(per_q[q]["times_ms"][i] for q in QUERIES) for i in range(args.steps)]
+    step_ms = [sum(per_q[q]["times_ms"][i] for q in QUERIES) for i in range(steps)]
     ms = statistics.median(step_ms)
     value = len(QUERIES) * L / (ms / 1e3)
+    same = sample_sf == args.sf
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic",
-        "config": {"workload": f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf} (reference timed on an SF{sample_sf} sample)",
-                   "sf": args.sf, "sample_sf": sample_sf, "queries": list(QUERIES), "lineitem_rows": L},
+        "config": {"workload": (f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf:g}" if same else
+                                f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf:g} (reference timed on an SF{sample_sf:g} sample)"),
+                   "sf": args.sf, "sample_sf": sample_sf, "same_config": same, "queries": list(QUERIES),
+                   "lineitem_rows": L, "requested_steps": args.steps, "requested_warmup": args.warmup,
+                   "budget_s": args.ref_budget_s},
         "queries": {q: {"latency_ms": per_q[q]["median_ms"], "rows_per_s": L / (per_q[q]["median_ms"] / 1e3)}
                     for q in QUERIES},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "reference",
-                         "sample": f"tensql Executor(par, {cores} threads) on SF{sample_sf} ({L} lineitem rows), "
-                                   f"median of {args.steps} after {args.warmup} warmups"},
+                         "sample": f"tensql Executor(par, {cores} threads) on SF{sample_sf:g} ({L} lineitem rows), "
+                                   f"median of {steps} after {warmup} warmups"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -175,7 +199,7 @@ def cpu_baseline_sample(sf: float):
     if not REF_RUNNER.exists():
         return None
     cmd = [str(REF_RUNNER), "run", "--sf", str(sf), "--queries", ",".join(QUERIES), "--backend", "par",
-           "--threads", str(cores), "--repeat", "3", "--warmup", "1"]
+           "--threads", str(cores), "--repeat", "1", "--warmup", "1"]
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, check=True, timeout=600).stdout
     except Exception as e:  # noqa: BLE001
@@ -184,8 +208,8 @@ def cpu_baseline_sample(sf: float):
     L = lines[0]["lineitem_rows"]
     ms = sum(d["median_ms"] for d in lines)
     return {"value": len(QUERIES) * L / (ms / 1e3), "unit": "rows/s", "cores": cores, "kind": "reference",
-            "sample": f"tensql Executor(par, {cores} threads), Q1+Q6+Q14+Q3 on SF{sf} ({L} lineitem rows), "
-                      f"median of 3 after 1 warmup",
+            "sample": f"tensql Executor(par, {cores} threads), Q1+Q6+Q14+Q3 on SF{sf:g} ({L} lineitem rows), "
+                      f"one timed run after 1 warmup (about 25 s of CPU work at SF10)",
             "queries_ms": {d["query"]: d["median_ms"] for d in lines}}
 
 
@@ -195,7 +219,9 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sf", type=float, default=10.0)
-    ap.add_argument("--ref-sf", type=float, default=1.0)
+    ap.add_argument("--ref-sf", type=float, default=None, help="reference arm / cpu_baseline SF (default: --sf)")
+    ap.add_argument("--ref-budget-s", type=float, default=900.0)
+    ap.add_argument("--no-extra", action="store_true", help="skip the cold, Q6@SF1 and per-instruction legs")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -204,6 +230,8 @@ def main():
     ap.add_argument("--csv-sf", type=float, default=1.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.ref_sf is None:
+        args.ref_sf = args.sf
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -275,6 +303,15 @@ def main():
                 e1.record(stream)
                 timing[q].append((e0, e1))
 
+    # cold latency: each query's first execution in this process (NVRTC
+    # compile of its specialised kernels, key ranges, allocations), wall clock
+    cold = {}
+    for q in QUERIES:
+        ctx.sync()
+        t0 = time.perf_counter()
+        run_query(q, tables)
+        ctx.sync()
+        cold[q] = (time.perf_counter() - t0) * 1e3
     for _ in range(args.warmup):
         step()
     for ex in execs.values():
@@ -364,6 +401,11 @@ def main():
         e2e["raw_layout"] = run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red_dev,
                                     encoded=False)
 
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra["q6_sf1"] = run_q6_sf1(args, tqp, torch, ctx, stream)
+        extra["per_instruction"] = run_per_instruction(args, tqp, torch, ctx, stream, tables, L)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample(args.ref_sf)
@@ -379,6 +421,7 @@ def main():
             "vs_baseline": None, "dtype": "f64+int64", "data": "synthetic (counter-based TPC-H generator, seed 7)",
             "config": {"workload": f"TPC-H Q1+Q6+Q14+Q3 suite, SF{args.sf:g} per GPU (SF{args.sf * world:g} total), device-resident columns",
                        "sf": args.sf, "queries": list(QUERIES), "lineitem_rows_per_gpu": L,
+                       "cold_ms": cold,
                        "fused": not args.no_fuse,
                        "l2": "inputs larger than L2 (1.9-2.5 GB per query vs 126 MB)",
                        "parallelism": (f"lineitem+orders cut on order boundaries x{world}, part/customer "
@@ -386,10 +429,64 @@ def main():
                                        else "single GPU")},
             "queries": queries, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks.summary(), "gpu_launches": launches, "fused_fallbacks": fallbacks, "csv_load": csv_leg,
+            "cold_first_execution_ms": cold,
         }
+        line.update(extra)
         print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
+
+
+def timed_queries(torch, stream, run, queries, steps):
+    """median device latency (CUDA events on the library's stream) per query"""
+    per = {q: [] for q in queries}
+    for _ in range(steps):
+        for q in queries:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            run(q)
+            e1.record(stream)
+            per[q].append((e0, e1))
+    torch.cuda.synchronize()
+    return {q: statistics.median([a.elapsed_time(b) for a, b in v]) for q, v in per.items()}
+
+
+def run_q6_sf1(args, tqp, torch, ctx, stream):
+    """BASELINE.json config 1: TPC-H Q6 at SF1 (6 M lineitem rows), fused,
+    device-resident, median of K after W warmups."""
+    plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / "q6.opplan.json").read_text())
+    li = tqp.Table.generate("lineitem", 1.0, 7, ctx=ctx)
+    ex = tqp.Executor(plan, ctx=ctx)
+    for _ in range(args.warmup):
+        ex.execute({"lineitem": li})
+    ms = timed_queries(torch, stream, lambda q: ex.execute({"lineitem": li}), ["q6"], max(5, args.steps))["q6"]
+    peak, _ = measured_peaks()
+    return {"workload": "TPC-H Q6 at SF1 (BASELINE config 1), fused, device-resident", "latency_ms": ms,
+            "rows_per_s": li.rows / (ms / 1e3), "algorithmic_bytes": 32 * li.rows,
+            "hbm_frac": 32 * li.rows / (ms / 1e3) / 1e9 / peak, "fallbacks": ex.fallbacks}
+
+
+def run_per_instruction(args, tqp, torch, ctx, stream, tables, L):
+    """The per-instruction device path (fuse=False: one kernel family per
+    InstrOp, the reference's lowering executed as written - radix sorts,
+    compactions, sort joins, segmented reductions) on the same SF tables: the
+    path every plan outside the fused contract takes."""
+    execs = {}
+    for q in QUERIES:
+        plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
+        execs[q] = tqp.Executor(plan, fuse=False, ctx=ctx)
+    for q in QUERIES:
+        execs[q].execute(tables)
+    ctx.sync()
+    ms = timed_queries(torch, stream, lambda q: execs[q].execute(tables), list(QUERIES), 3)
+    launches0 = ctx.launches
+    for q in QUERIES:
+        execs[q].execute(tables)
+    ctx.sync()
+    return {"workload": f"suite per instruction (fuse=False), SF{args.sf:g}", "latency_ms": ms,
+            "rows_per_s": {q: L / (v / 1e3) for q, v in ms.items()}, "suite_ms": sum(ms.values()),
+            "launches_per_suite": ctx.launches - launches0}
 
 
 def run_csv_leg(tqp, ctx, sf):
@@ -437,13 +534,16 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red
     host = {}
     h2d = 0
     codecs = {}
+    encode_s = 0.0
     for name, t in tables.items():
         cols = []
         for cname, lt in t.columns():
             dev = t.column(cname)
             arr = dev.numpy(widen_strings=False)
             if encoded:
+                t0 = time.perf_counter()
                 codec, payload = tqp.encode_column(arr, dev.dtype)
+                encode_s += time.perf_counter() - t0
                 pin = torch.from_numpy(payload).pin_memory()
                 codecs[f"{name}.{cname}"] = f"{codec.name}{codec.width if codec.name in ('for', 'dec') else ''}"
                 cols.append((cname, lt, dev.dtype, arr.shape, codec, pin))
@@ -507,6 +607,10 @@ def run_e2e(args, tqp, torch, ctx, stream, tables, run_query, L_total, dist, red
         out["path"] = ("pinned host columns in the compressed columnar format -> tqp_tensor_from_encoded (C ABI: "
                        "H2D of the encoded bytes + device decode) -> tqp_executor_execute x4 -> results to host")
         out["codecs"] = codecs
+        out["encode_once_ms"] = encode_s * 1e3
+        out["encode_note"] = ("host-side encode of every column, done once when the host copy is made (the "
+                              "loader's storage format), outside the timed region; tqp_codec_encode on the "
+                              "host cores")
     else:
         out["path"] = "pinned host columns (reference layout) -> tqp_tensor_from_host (C ABI) -> tqp_executor_execute x4 -> results to host"
     return out

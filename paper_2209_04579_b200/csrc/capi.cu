@@ -374,6 +374,7 @@ int tqp_plan_add_instr(tqp_plan* p, const tqp_instr_desc* d, tqp_status* st) {
     if (p->p.steps.empty()) throw Error(TQP_ERR_ARG, "tqp_plan_add_instr before tqp_plan_begin_step");
     Instr in;
     if (!op_from_name(d->op ? d->op : "", &in.op)) throw Error(TQP_ERR_PLAN, std::string("unknown instruction ") + d->op);
+    if (d->num_inputs < 0 || (d->num_inputs > 0 && !d->inputs)) throw Error(TQP_ERR_ARG, "tqp_plan_add_instr: bad inputs");
     in.inputs.assign(d->inputs, d->inputs + d->num_inputs);
     in.output = d->output;
     in.cmp = d->cmp;
@@ -388,10 +389,13 @@ int tqp_plan_add_instr(tqp_plan* p, const tqp_instr_desc* d, tqp_status* st) {
     if (d->column) in.column = d->column;
     in.param = d->param;
     if (in.op == Op::ConstTensor) {
+      if (d->const_dtype < TQP_BOOL || d->const_dtype > TQP_STR8 || d->const_rows < 0 || d->const_cols < 0)
+        throw Error(TQP_ERR_ARG, "tqp_plan_add_instr: bad constant dtype or shape");
       in.const_dtype = d->const_dtype;
       in.const_rows = d->const_rows;
       in.const_cols = d->const_cols;
       size_t bytes = static_cast<size_t>(d->const_rows * d->const_cols) * dtype_size(d->const_dtype);
+      if (bytes && !d->const_data) throw Error(TQP_ERR_ARG, "tqp_plan_add_instr: null constant data");
       in.const_host.resize(bytes);
       if (bytes) std::memcpy(in.const_host.data(), d->const_data, bytes);
     }
@@ -401,6 +405,8 @@ int tqp_plan_add_instr(tqp_plan* p, const tqp_instr_desc* d, tqp_status* st) {
 }
 int tqp_plan_set_step_outputs(tqp_plan* p, const int* slots, int n, tqp_status* st) {
   return guard(st, [&] {
+    if (p->p.steps.empty()) throw Error(TQP_ERR_ARG, "tqp_plan_set_step_outputs before tqp_plan_begin_step");
+    if (n < 0 || (n > 0 && !slots)) throw Error(TQP_ERR_ARG, "tqp_plan_set_step_outputs: bad slot array");
     p->p.steps.back().output_slots.assign(slots, slots + n);
     return 0;
   });

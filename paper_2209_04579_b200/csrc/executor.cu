@@ -188,6 +188,7 @@ Tensor Executor::exec_instr(const Instr& in, std::vector<std::optional<Tensor>>&
       if (num < 0) {
         const Tensor& t = arg(2);
         if (t.size() != 1) kernel_fail("tensor: item() requires exactly one element");
+        check_i64_access(t);
         num = std::max<int64_t>(0, read_scalar<int64_t>(c, t));
       }
       return k::segmented_reduce(c, arg(0), arg(1), num, in.reduce);
@@ -210,6 +211,7 @@ Tensor Executor::exec_instr(const Instr& in, std::vector<std::optional<Tensor>>&
     case Op::IotaLen: {
       const Tensor& t = arg(0);
       if (t.size() != 1) kernel_fail("tensor: item() requires exactly one element");
+      check_i64_access(t);
       return k::iota(c, read_scalar<int64_t>(c, t));
     }
     case Op::Cast: return k::cast(c, arg(0), in.cast_to);

@@ -1538,7 +1538,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
         // limb sums are exact below kLimbMaxRows rows per group
         if (s.acc_words == kLimbWords && gc[u] >= static_cast<unsigned long long>(kLimbMaxRows)) {
           err[0] = 1;
-          err[3] = 15;
+          err[3] = FR_LIMB_ROWS;
         }
         k0[u] = gc[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
       }
@@ -1645,7 +1645,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
     blk_nc[blockIdx.x] = s_nc < kTopkBlkCand ? s_nc : kTopkBlkCand;
     if (s_err) {
       err[0] = 1;
-      err[3] = 16;
+      err[3] = FR_TOPK_BLOCK;
     }
     __threadfence();
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
@@ -1716,7 +1716,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
   const int nfc = s_nc < kTopkFinal ? s_nc : kTopkFinal;
   if (threadIdx.x == 0 && s_nc > kTopkFinal) {
     err[0] = 1;
-    err[3] = 17;
+    err[3] = FR_TOPK_FINAL;
   }
   // full keys of the final candidates, then the exact order (warp 0)
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(fg + kTopkFinal + 2);
@@ -1744,7 +1744,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
         bool f;
         if (!group_out_value(s, j, g, bits, f)) {
           err[0] = 1;
-          err[3] = 18;
+          err[3] = FR_GROUP_VALUE;
         }
         static_cast<unsigned long long*>(s.f.out_ptr[j])[lane] = bits;
       }
@@ -1855,6 +1855,10 @@ __global__ void k_merge_records(const unsigned long long* __restrict__ rec, long
     for (int a = 0; a < nacc; ++a) {
       const unsigned long long lo = r[2 + nkeyc + 2 * a], hi = r[3 + nkeyc + 2 * a];
       const __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
+      // a shard's sum is < 2^62 (q64_range_check) so |v| < 2^126; partials
+      // at or above 2^122 could wrap the int128 once 32 shards are added
+      const __int128 lim = static_cast<__int128>(1) << 122;
+      if (v >= lim || v <= -lim) err[0] = 1;
       atomic_add_q64(&hacc[(h * nacc + a) * 2], v);
     }
   }

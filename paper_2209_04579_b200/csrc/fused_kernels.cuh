@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       for (int a = 0; a < NA; ++a) acc[g][a] = 0;  // 0.0 and 0 share bits
     }
     long long absmax = 0;  // int accumulators: exactness guard
+    double fabsmax = 0.0;  // build-group fp64 values: Q64.64 range guard
     long long it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int st = static_cast<int>(it % nst);
@@ -505,9 +506,13 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
               __int128 qv;
               if (is_int) {
                 qv = static_cast<__int128>(static_cast<long long>(v[k]));
-              } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k])), qv)) {
-                atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-                qv = 0;
+              } else {
+                const double dv = __longlong_as_double(static_cast<long long>(v[k]));
+                fabsmax = fmax(fabsmax, fabs(dv));
+                if (!f64_to_q64(dv, qv)) {
+                  set_fallback(s.err, FR_Q64_CONVERT);
+                  qv = 0;
+                }
               }
               atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
             }
@@ -519,9 +524,8 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     }
     // int64 sums are exact only while |v| * rows < 2^63 (the reference
     // errors on the first overflowing prefix): otherwise the exact path
-    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-    }
+    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) set_fallback(s.err, FR_INT_RANGE);
+    if constexpr (MODE == MODE_BUILDGRP) q64_range_check(fabsmax, s.n, s.err);
     if constexpr (MODE == MODE_SMALL) {
       for (int gg = 0; gg < kGroups; ++gg) {
         for (int a = 0; a <= s.nacc; ++a) {

@@ -30,6 +30,22 @@ enum TermKind : int { TK_INT = 0, TK_F64 = 1, TK_TRUE = 2, TK_FALSE = 3 };
 enum FactorKind : int { FK_X = 0, FK_K_MINUS_X, FK_K_PLUS_X, FK_X_MINUS_K, FK_X_PLUS_K, FK_X_TIMES_K, FK_CONST };
 enum Mode : int { MODE_SCALAR = 0, MODE_SMALL = 1, MODE_BUILDGRP = 2 };
 
+// err[3]: why a fused unit handed its steps to the exact per-instruction path
+// (err[0] != 0). Diagnostic only (TQP_DEBUG_FALLBACK prints it); the exact
+// path then produces the reference's result or error.
+enum FallbackReason : long long {
+  FR_BUILD_RANGE = 11,     // build key outside the direct-address range
+  FR_DUP_KEY = 12,         // a build key inserted twice (1:N join)
+  FR_Q64_CONVERT = 13,     // an fp64 group value not exactly representable in Q64.64
+  FR_Q64_RANGE = 14,       // max|value| x rows may reach 2^62: a Q64.64 group sum could wrap
+  FR_LIMB_ROWS = 15,       // a group has >= kLimbMaxRows rows (limb words could overflow)
+  FR_TOPK_BLOCK = 16,      // top-k: a block's candidate log overflowed
+  FR_TOPK_FINAL = 17,      // top-k: too many final candidates (ties)
+  FR_GROUP_VALUE = 18,     // a group output (AVG / epilogue) left the exact form
+  FR_INT_RANGE = 19,       // int64 sum may overflow (|v| x rows >= 2^63)
+  FR_HASH_FULL = 22,       // hash group / join table probe sequence exhausted
+};
+
 // A per-row operand: fact column (src = -1) or a column of the build-side
 // root row matched by probe `src`.
 struct Operand {
@@ -195,11 +211,12 @@ __device__ __forceinline__ void presence_insert(unsigned* bitmap, long long idx,
     dup |= __popc(bits) != __popc(peers) ? 1u : 0u;
   }
 }
+__device__ __forceinline__ void set_fallback(long long* err, long long reason) {
+  atomicExch(reinterpret_cast<unsigned long long*>(err), 1ULL);
+  atomicExch(reinterpret_cast<unsigned long long*>(err) + 3, static_cast<unsigned long long>(reason));
+}
 __device__ __forceinline__ void build_dup_check(unsigned dup, long long* err) {
-  if (__any_sync(0xffffffffu, dup != 0u) && (threadIdx.x & 31) == 0) {
-    atomicExch(reinterpret_cast<unsigned long long*>(err), 1ULL);
-    atomicExch(reinterpret_cast<unsigned long long*>(err) + 3, 12ULL);  // reason (TQP_DEBUG_FALLBACK)
-  }
+  if (__any_sync(0xffffffffu, dup != 0u) && (threadIdx.x & 31) == 0) set_fallback(err, FR_DUP_KEY);
 }
 
 // ---- operand access ----------------------------------------------------------
@@ -336,8 +353,10 @@ __device__ __forceinline__ unsigned long long eval_acc(const Acc& a, const unsig
 }
 
 // ---- exact Q64.64 fixed point ----------------------------------------------------
-// x -> round-toward-zero(x * 2^64) as int128. Exact for |x| >= 2^-11 (every
-// money value); false for |x| >= 2^62, NaN, Inf.
+// x -> x * 2^64 as int128, exactly: false for NaN, Inf, |x| >= 2^62 and for
+// any x with a nonzero bit below 2^-64 (it would be truncated), so a group
+// sum built from these values is exact or the unit falls back (FR_Q64_*).
+// Every money value (a multiple of 2^-40 or coarser) converts.
 __device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
   long long bits = __double_as_longlong(x);
   int ex = static_cast<int>((bits >> 52) & 0x7ff);
@@ -354,12 +373,21 @@ __device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
     if (shift > 73) return false;
     v = static_cast<unsigned __int128>(mant) << shift;
   } else if (shift > -64) {
+    if (mant & ((1ULL << (-shift)) - 1)) return false;  // bits below 2^-64
     v = static_cast<unsigned __int128>(mant >> (-shift));
   } else {
+    if (mant) return false;
     v = 0;
   }
   out = bits < 0 ? -static_cast<__int128>(v) : static_cast<__int128>(v);
   return true;
+}
+
+// Q64.64 group sums cannot wrap while max|value| x rows < 2^62 (the limb
+// words are bounded separately by kLimbMaxRows); checked once per thread
+// after its last row with the largest |value| it converted
+__device__ __forceinline__ void q64_range_check(double fabsmax, long long rows, long long* err) {
+  if (fabsmax * static_cast<double>(rows) >= 4.6116860184273879e18) set_fallback(err, FR_Q64_RANGE);
 }
 
 // Q64.64 -> fp64, correctly rounded (one rounding of the exact value: the

@@ -75,8 +75,7 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
       if (pass[k]) {
         idx = key[k] - b.kmin;
         if (idx < 0 || idx >= b.range) {
-          atomicExch(reinterpret_cast<unsigned long long*>(b.err), 1ULL);
-          atomicExch(reinterpret_cast<unsigned long long*>(b.err) + 3, 11ULL);
+          set_fallback(b.err, FR_BUILD_RANGE);
           idx = -1;
         } else {
 #if B_ASSIGN

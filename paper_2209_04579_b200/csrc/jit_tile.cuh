@@ -71,6 +71,7 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
     for (int a = 0; a < Q_NA; ++a) acc[a] = 0;  // 0.0 and 0 share bits
     unsigned long long cnt = 0;
     long long absmax = 0;
+    double fabsmax = 0.0;  // build-group fp64 values: Q64.64 range guard
     // MODE_SMALL with Q_REGACC: per-thread [slot][acc + count] accumulators in
     // registers. A row adds to its slot only (predicated), in the same order
     // as the shared-memory cells, so the sums are bit-identical to them; the
@@ -178,11 +179,13 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
             __int128 qv;
             if (q_is_int(a)) {
               qv = static_cast<__int128>(static_cast<long long>(v[k][a]));
-            } else if (!f64_to_q64(__longlong_as_double(static_cast<long long>(v[k][a])), qv)) {
-              atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err) + 3, 14ULL);
-              atomicExch(reinterpret_cast<unsigned long long*>(s.err) + 3, 13ULL);
-              qv = 0;
+            } else {
+              const double dv = __longlong_as_double(static_cast<long long>(v[k][a]));
+              fabsmax = fmax(fabsmax, fabs(dv));
+              if (!f64_to_q64(dv, qv)) {
+                set_fallback(s.err, FR_Q64_CONVERT);
+                qv = 0;
+              }
             }
             atomic_add_limbs(s.gacc + static_cast<long long>(gid[k]) * s.gstride + a * kLimbWords, qv);
           }
@@ -192,9 +195,8 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     // int64 sums are exact only while |v| * rows < 2^63: otherwise the exact path
-    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
-      atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-    }
+    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) set_fallback(s.err, FR_INT_RANGE);
+    if constexpr (Q_MODE == MODE_BUILDGRP) q64_range_check(fabsmax, s.n, s.err);
     if constexpr (Q_MODE == MODE_SMALL) {
 #pragma unroll
       for (int gg = 0; gg < Q_SLOTS; ++gg) {

@@ -523,6 +523,7 @@ Tensor exp_f64(Ctx& c, const Tensor& t) {
 }
 
 Tensor last_or_zero(Ctx& c, const Tensor& t) {
+  check_i64_access(t);  // executor.cpp:239-242 reads data<int64_t>()
   Tensor o = c.alloc(TQP_I64, 1, 1);
   if (t.size() == 0) {
     TQP_CUDA(cudaMemsetAsync(o.data(), 0, 8, c.stream));

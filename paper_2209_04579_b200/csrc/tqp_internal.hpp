@@ -229,6 +229,11 @@ int64_t codec_encode(int dtype, int64_t rows, int64_t cols, const void* host, vo
 Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_codec& k, const void* payload,
                      int64_t bytes);
 void download(Ctx& c, const Tensor& t, void* host);
+// Tensor::data<int64_t>() / item<int64_t>() of the reference (tensor.hpp:
+// 84-100, tensor.cpp:35-39): a typed host access checks the dtype first
+inline void check_i64_access(const Tensor& t) {
+  if (t.dtype != TQP_I64) kernel_fail(std::string("tensor: dtype is ") + dtype_name(t.dtype) + ", accessed as int64");
+}
 template <typename T>
 T read_scalar(Ctx& c, const Tensor& t, int64_t index = 0) {
   T v{};

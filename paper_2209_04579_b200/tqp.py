@@ -276,9 +276,11 @@ class Tensor:
 
     @staticmethod
     def from_encoded(codec: "Codec", payload, dtype: int, rows: int, cols: int = 1,
-                     ctx: Optional[Context] = None) -> "Tensor":
+                     ctx: Optional[Context] = None, sync: bool = True) -> "Tensor":
         """Uploads an encoded payload (numpy array or a pinned torch tensor:
-        anything with a data pointer) and decodes it on the device."""
+        anything with a data pointer) and decodes it on the device. With
+        sync=False the host->device copy may still be reading `payload` when
+        this returns: keep it alive and unmodified until ctx.sync()."""
         ctx = ctx or default_context()
         if hasattr(payload, "data_ptr"):
             ptr, nbytes = payload.data_ptr(), payload.numel() * payload.element_size()
@@ -288,6 +290,11 @@ class Tensor:
         st = Status()
         h = lib.tqp_tensor_from_encoded(ctx.h, dtype, rows, cols, C.byref(codec), ptr, nbytes, C.byref(st))
         _check(st, bool(h))
+        if not sync:
+            # the copy from `payload` is asynchronous (truly so for pinned
+            # memory): the caller keeps it alive and unchanged until ctx.sync()
+            return Tensor(h, ctx)
+        ctx.sync()
         return Tensor(h, ctx)
 
     @staticmethod
@@ -316,7 +323,16 @@ class Tensor:
     @property
     def __cuda_array_interface__(self) -> dict:
         """Zero-copy view for torch.as_tensor (fixed-width dtypes only); the
-        producer stream is synchronised before the view is handed out."""
+        producer stream is synchronised before the view is handed out.
+
+        The view must be treated as READ-ONLY. Tensors are immutable and
+        shared by reference (a table column is aliased by LoadColumn results
+        and result columns, and its min/max key range is cached with the
+        column, executor.hpp Column::range), so an in-place write would change
+        every alias and leave the cached range stale. The interface cannot say
+        so itself: torch rejects `data: (ptr, True)` ("the read only flag is
+        not supported"), so the flag stays False; copy (`.clone()`) before
+        writing."""
         if self.dtype == STR8:
             raise TypeError("STR8 tensors have no fixed-width array view")
         self.ctx.sync()

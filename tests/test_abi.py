@@ -70,3 +70,30 @@ def test_nvrtc_bound_from_build_toolkit():
     rel = nvcc.split("release ")[1].split(",")[0]
     major, minor = (int(x) for x in rel.split("."))
     assert int(out.stdout.strip()) == major * 1000 + minor * 10
+
+
+def test_plan_builder_rejects_bad_arguments():
+    """The plan builder validates what crosses the C ABI (no step yet, bad
+    constant dtype, null constant data) instead of dereferencing it."""
+    import ctypes as C
+    from paper_2209_04579_b200 import tqp
+    st = tqp.Status()
+    h = tqp.lib.tqp_plan_create(4, C.byref(st))
+    assert h
+    slots = (C.c_int * 1)(0)
+    assert tqp.lib.tqp_plan_set_step_outputs(h, slots, 1, C.byref(st)) != 0
+    assert b"before tqp_plan_begin_step" in st.msg
+    assert tqp.lib.tqp_plan_begin_step(h, b"s#0", b"scan", C.byref(st)) == 0
+    d = tqp.InstrDesc()
+    d.op = b"const"
+    d.num_inputs = 0
+    d.output = 0
+    d.const_dtype = 9
+    d.const_rows = d.const_cols = 1
+    assert tqp.lib.tqp_plan_add_instr(h, C.byref(d), C.byref(st)) != 0
+    assert b"bad constant dtype" in st.msg
+    d.const_dtype = tqp.I64
+    d.const_data = None
+    assert tqp.lib.tqp_plan_add_instr(h, C.byref(d), C.byref(st)) != 0
+    assert b"null constant data" in st.msg
+    tqp.lib.tqp_plan_free(h)

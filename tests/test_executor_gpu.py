@@ -153,3 +153,44 @@ def test_one_executor_over_several_table_sets(ctx):
             del os.environ["TQP_JIT"]
         else:
             os.environ["TQP_JIT"] = old
+
+
+def _with_column(tqp, table, name, fn):
+    host = table.to_numpy()
+    return tqp.Table.from_columns([(c, lt, fn(host[c]) if c == name else host[c]) for c, lt in table.columns()])
+
+
+@pytest.mark.parametrize("scale", [1e-25, 1e15])
+def test_buildgroup_fixed_point_guards(ctx, scale):
+    """Q3's build-group sums are exact Q64.64 fixed point. A value with bits
+    below 2^-64 (scale 1e-25) or a column whose max|v| x rows may reach 2^62
+    (scale 1e15) must not be summed there: the unit hands its steps to the
+    exact path (one fallback) and the result is the per-instruction one."""
+    from paper_2209_04579_b200 import tqp
+    plan = json.loads((PLANS / "q3.opplan.json").read_text())
+    base = {n: tqp.Table.generate(n, 0.005, 7) for n in ("lineitem", "orders", "customer")}
+    tables = dict(base, lineitem=_with_column(tqp, base["lineitem"], "l_extendedprice", lambda a: a * scale))
+    fused = tqp.Executor(plan, fuse=True)
+    got = as_numpy(fused.execute(tables))
+    assert fused.fallbacks == 1
+    want = as_numpy(tqp.Executor(plan, fuse=False).execute(tables))
+    for (n, _, g), (_, _, w) in zip(got, want):
+        np.testing.assert_array_equal(g, w, err_msg=n)
+    # the unscaled tables stay on the fused path
+    ok = tqp.Executor(plan, fuse=True)
+    ok.execute(base)
+    assert ok.fallbacks == 0
+
+
+def test_typed_scalar_access_checks_dtype(ctx):
+    """last_or_zero / iota_len / segmented_reduce's count read a 1x1 int64
+    (Tensor::data<int64_t>, tensor.cpp:35-39): other dtypes raise the
+    reference's KernelError instead of reading 8 bytes of something else."""
+    from paper_2209_04579_b200 import tqp
+    for arr, dt, name in ((np.array([[1.5]]), tqp.F64, "float64"), (np.array([[1]], np.int32), tqp.I32, "int32"),
+                          (np.array([[1]], np.uint8), tqp.BOOL, "bool")):
+        t = tqp.Tensor.from_numpy(arr, dt)
+        with pytest.raises(tqp.KernelError, match=f"tensor: dtype is {name}, accessed as int64"):
+            tqp.last_or_zero(t)
+    np.testing.assert_array_equal(tqp.last_or_zero(tqp.Tensor.from_numpy(np.array([[3], [9]], np.int64))).numpy(),
+                                  [[9]])
