@@ -190,6 +190,9 @@ class B200Executor {
   const tensql::OperatorPlan& plan() const { return plan_; }
   std::string_view backend_name() const { return "b200"; }
   std::string explain() const { return tqp_executor_explain(ex_); }
+  // fused units that handed their steps to the exact per-instruction path
+  // (their data left the fused contract) over this executor's runs
+  long long fallbacks() const { return static_cast<long long>(tqp_executor_fallbacks(ex_)); }
 
   // Executor::execute (executor.cpp:346): uploads the tables, runs on device
   // and returns the result as an EncodedTable.

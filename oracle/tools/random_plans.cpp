@@ -48,12 +48,29 @@ std::string iso_day(int64_t day) {  // days since 1970-01-01 -> ISO text
 struct Shape {
   int64_t n_fact, n_dim;
   bool dim_dups, huge_ints, nans;
+  // --profile groups: group-key columns k (Int64 over [0, k_range), sparse
+  // when k_sparse) and c (short Utf8 codes), dim keys spread over
+  // [0, n_dim * dim_spread)
+  bool groups = false;
+  int64_t k_range = 0;
+  bool k_sparse = false;
+  int64_t dim_spread = 1;
 };
 
 // fact(fk, a, x, d, s, b), dim(dk, y, t, e)
 void make_tables(Rng& r, const Shape& sh, Catalog& cat, TableSet& tables) {
   TableSchema fs = {{"fk", LogicalType::Int64}, {"a", LogicalType::Int64}, {"x", LogicalType::Float64},
                     {"d", LogicalType::Date},   {"s", LogicalType::Utf8},  {"b", LogicalType::Bool}};
+  if (sh.groups) {
+    fs.push_back({"k", LogicalType::Int64});
+    fs.push_back({"c", LogicalType::Utf8});
+  }
+  static const std::vector<std::string> kCodes = {"", "A", "B", "AB", "BA", "ZZ", "Q7", "AIR", "MAIL", "SHIP", "TRUCK",
+                                                  "RAIL", "REG", "FOB", "X", "XYZW"};
+  // sparse k values: a fixed pool of wide-range keys
+  std::vector<int64_t> kpool;
+  if (sh.groups && sh.k_sparse)
+    for (int64_t i = 0; i < sh.k_range; ++i) kpool.push_back(static_cast<int64_t>(r() >> 20) - (int64_t{1} << 42));
   TableSchema ds = {{"dk", LogicalType::Int64}, {"y", LogicalType::Float64}, {"t", LogicalType::Utf8},
                     {"e", LogicalType::Date}};
   const int64_t d0 = days_from_civil(1992, 1, 1), d1 = days_from_civil(1998, 12, 31);
@@ -64,12 +81,20 @@ void make_tables(Rng& r, const Shape& sh, Catalog& cat, TableSet& tables) {
     double x = static_cast<double>(static_cast<int64_t>(pick(r, 20001)) - 10000) / 100.0;
     if (chance(r, 0.03)) x = -0.0;
     if (sh.nans && chance(r, 0.02)) x = std::nan("");
-    fr.push_back({Cell{static_cast<int64_t>(pick(r, static_cast<int>(sh.n_dim) + 4))}, Cell{a}, Cell{x},
+    const int64_t fk_span = sh.n_dim * sh.dim_spread + 4;
+    fr.push_back({Cell{static_cast<int64_t>(r() % static_cast<uint64_t>(fk_span))}, Cell{a}, Cell{x},
                   Cell{iso_day(d0 + pick(r, static_cast<int>(d1 - d0 + 1)))}, Cell{kWords[pick(r, kWords.size())]},
                   Cell{chance(r, 0.5)}});
+    if (sh.groups) {
+      const int64_t kv = sh.k_sparse ? kpool[r() % kpool.size()] : static_cast<int64_t>(r() % static_cast<uint64_t>(sh.k_range));
+      fr.back().push_back(Cell{kv});
+      fr.back().push_back(Cell{kCodes[pick(r, kCodes.size())]});
+    }
   }
   std::vector<int64_t> keys(sh.n_dim);
-  for (int64_t i = 0; i < sh.n_dim; ++i) keys[i] = sh.dim_dups ? pick(r, static_cast<int>(sh.n_dim / 2 + 1)) : i;
+  for (int64_t i = 0; i < sh.n_dim; ++i)
+    keys[i] = sh.dim_dups ? static_cast<int64_t>(r() % static_cast<uint64_t>(sh.n_dim * sh.dim_spread / 2 + 1))
+                          : i * sh.dim_spread + (sh.dim_spread > 1 ? pick(r, static_cast<int>(sh.dim_spread)) : 0);
   std::shuffle(keys.begin(), keys.end(), r);
   for (int64_t i = 0; i < sh.n_dim; ++i) {
     dr.push_back({Cell{keys[i]}, Cell{static_cast<double>(pick(r, 100001)) / 100.0}, Cell{kWords[pick(r, kWords.size())]},
@@ -260,6 +285,79 @@ Built random_plan(Rng& r, const Catalog& cat) {
   return b;
 }
 
+// --profile groups: scan(fact) > [filter] > [join(dim)] > aggregate over 1-3
+// group keys drawn from the int64 / date / short-string columns (k, c, d, a,
+// fk and the dim's dk, e) with SUM / COUNT / AVG (the fused hash-group
+// family; MIN/MAX now and then) > [sort > limit]
+Built random_group_plan(Rng& r, const Catalog& cat) {
+  Built b;
+  Gen g{r};
+  PlanPtr p = make_scan("fact");
+  Schema sch = infer_schema(p, cat);
+  std::string txt = "scan(fact)";
+  auto refresh = [&] { sch = infer_schema(p, cat); };
+  g.schema = &sch;
+  if (chance(r, 0.5)) {
+    g.budget = 4;
+    p = make_filter(p, g.predicate(2));
+    txt += " > filter";
+    refresh();
+  }
+  bool joined = false;
+  if (chance(r, 0.4)) {
+    PlanPtr right = make_scan("dim");
+    if (chance(r, 0.3)) {
+      Schema ds = infer_schema(right, cat);
+      Gen gd{r, &ds, 3};
+      right = make_filter(right, gd.predicate(2));
+    }
+    p = make_join(p, right, "fk", "dk");
+    txt += " > join(dim)";
+    joined = true;
+    refresh();
+  }
+  std::vector<std::string> pool = {"k", "k", "c", "d", "a", "fk"};
+  if (joined) {
+    pool.push_back("dk");
+    pool.push_back("e");
+  }
+  std::vector<std::string> keys;
+  const int nk = 1 + pick(r, 3);
+  for (int i = 0; i < nk; ++i) {
+    const std::string k = pool[pick(r, pool.size())];
+    if (std::find(keys.begin(), keys.end(), k) == keys.end()) keys.push_back(k);
+  }
+  std::vector<std::string> vals = {"a", "x", "k"};
+  if (joined) vals.push_back("y");
+  std::vector<AggregateNode::Agg> aggs;
+  std::vector<std::string> exact_sort_cols = keys;
+  const int na = 1 + pick(r, 3);
+  for (int i = 0; i < na; ++i) {
+    const std::string name = "g" + std::to_string(i);
+    const std::string c = vals[pick(r, vals.size())];
+    AggFn fs[] = {AggFn::Sum, AggFn::Sum, AggFn::Count, AggFn::Avg, AggFn::Min};
+    AggFn fn = fs[pick(r, chance(r, 0.9) ? 4 : 5)];
+    if (fn == AggFn::Count || fn == AggFn::Min || c == "a" || c == "k") exact_sort_cols.push_back(name);
+    aggs.push_back({name, fn, col(c)});
+  }
+  p = make_aggregate(p, keys, std::move(aggs));
+  txt += " > aggregate(" + std::to_string(keys.size()) + " keys)";
+  if (chance(r, 0.35)) {
+    std::vector<SortNode::Key> sk;
+    const int ns = 1 + pick(r, 2);
+    for (int i = 0; i < ns; ++i) sk.push_back({exact_sort_cols[pick(r, exact_sort_cols.size())], chance(r, 0.5)});
+    p = make_sort(p, sk);
+    txt += " > sort(" + std::to_string(ns) + ")";
+    if (chance(r, 0.7)) {
+      p = make_limit(p, 1 + pick(r, 20));
+      txt += " > limit";
+    }
+  }
+  b.plan = p;
+  b.text = txt;
+  return b;
+}
+
 // ---- comparison (tables_diff_ordered, tests/support/table_compare.hpp:37-64) ----
 bool close(double a, double b) {
   if (std::isnan(a) || std::isnan(b)) return std::isnan(a) && std::isnan(b);
@@ -300,6 +398,12 @@ int main(int argc, char** argv) {
   // --only N: run just plan N of the seeded sequence (the sequence is still
   // generated, so N is the same plan as in the full run) and dump it
   const int only = fl.count("--only") ? std::stoi(fl["--only"]) : -1;
+  // --profile groups: wide group-by / join key shapes (random_group_plan);
+  // --require-fused 1: a fused unit handing its steps to the exact path counts
+  // as a failure (the fused contract must cover these shapes)
+  const bool groups = fl.count("--profile") && fl["--profile"] == "groups";
+  const bool require_fused = fl.count("--require-fused") && fl["--require-fused"] != "0";
+  long long fallbacks = 0;
   Rng r(seed);
   int failures = 0, compared = 0, invalid = 0, errors_matched = 0;
   std::map<std::string, int> shapes;
@@ -308,6 +412,20 @@ int main(int argc, char** argv) {
   int plans_per_table = 10;
   for (int done = 0; done < nplans;) {
     Shape sh{sizes[pick(r, 7)], dsizes[pick(r, 6)], chance(r, 0.3), chance(r, 0.2), chance(r, 0.2)};
+    if (groups) {
+      // 1 k .. 10 M distinct k values over up to 1 M fact rows; dim keys
+      // dense, spread (non-dense) or duplicated
+      static const int64_t gsizes[] = {0, 1, 1000, 20000, 200000, 1000000};
+      static const int64_t granges[] = {7, 1000, 50000, 1000000, 10000000};
+      static const int64_t gdims[] = {0, 5, 500, 20000, 200000};
+      sh = Shape{gsizes[pick(r, 6)], gdims[pick(r, 5)], chance(r, 0.2), false, chance(r, 0.1)};
+      sh.groups = true;
+      sh.k_range = granges[pick(r, 5)];
+      sh.k_sparse = chance(r, 0.3);
+      if (sh.k_sparse) sh.k_range = std::min<int64_t>(sh.k_range, 200000);
+      static const int64_t spreads[] = {1, 1, 3, 1000, 1000000};
+      sh.dim_spread = spreads[pick(r, 5)];
+    }
     Catalog cat;
     TableSet tables;
     make_tables(r, sh, cat, tables);
@@ -315,7 +433,7 @@ int main(int argc, char** argv) {
       Built b;
       OperatorPlan op;
       try {
-        b = random_plan(r, cat);
+        b = groups ? random_group_plan(r, cat) : random_plan(r, cat);
         op = plan_operators(optimize(b.plan, cat), cat);
       } catch (const std::exception& e) {
         ++invalid;  // rejected by the reference's own planner: nothing to compare
@@ -347,12 +465,23 @@ int main(int argc, char** argv) {
       for (bool fuse : {true, false}) {
         std::string got_err;
         EncodedTable got;
+        long long fb = 0;
         try {
           tqp_integration::B200Executor ex(op, fuse);
-          got = ex.execute(tables);
+          try {
+            got = ex.execute(tables);
+          } catch (...) {
+            fb = ex.fallbacks();
+            throw;
+          }
+          fb = ex.fallbacks();
         } catch (const std::exception& e) {
           got_err = e.what();
         }
+        fallbacks += fb;
+        if (fb && (verbose || require_fused))
+          std::printf("FALLBACK plan %d (%lld fused unit(s) to the exact path) [%s] %s\n", done, fb,
+                      fuse ? "fused" : "per-instruction", b.text.c_str());
         std::string d = !want_err.empty() || !got_err.empty()
                             ? (want_err == got_err ? "" : "error '" + got_err + "' vs '" + want_err + "'")
                             : diff(got, want);
@@ -386,11 +515,13 @@ int main(int argc, char** argv) {
                       b.text.c_str(), d.empty() ? "" : ": ", d.c_str());
         }
         if (!d.empty()) ++failures;
+        if (require_fused && fb && want_err.empty()) ++failures;
       }
     }
   }
   std::printf("random plans: seed %llu, %d plans, %d comparisons (%d matched errors), %d rejected by the planner, "
-              "%zu distinct shapes, %d failure(s)\n",
-              static_cast<unsigned long long>(seed), nplans, compared, errors_matched, invalid, shapes.size(), failures);
+              "%zu distinct shapes, %lld fused fallback(s), %d failure(s)\n",
+              static_cast<unsigned long long>(seed), nplans, compared, errors_matched, invalid, shapes.size(), fallbacks,
+              failures);
   return failures ? 1 : 0;
 }

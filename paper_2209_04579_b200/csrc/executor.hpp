@@ -71,6 +71,7 @@ struct KeyRange {
   std::mutex mu;
   bool ready = false;
   long long mn = 0, mx = 0;
+  int day = -1;  // Date keys: 1 every value is a whole day in ns, 0 not, -1 not computed
 };
 
 struct Column {

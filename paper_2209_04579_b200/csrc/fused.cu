@@ -454,6 +454,12 @@ struct PipeDesc {
   // MODE_BUILDGRP: keys resolved to root columns of probes[group_probe]
   int group_probe = -1;
   std::vector<std::string> group_key_root_columns;
+  // MODE_HASH: group keys (fact or probe root columns) with their logical
+  // types; a MODE_SMALL unit with hash_alt reruns as MODE_HASH when a CTA
+  // meets more codes than its slots
+  std::vector<OperandDesc> hkeys;
+  std::vector<int> hkey_lt;
+  bool hash_alt = false;
   // fused sort + limit (MODE_BUILDGRP)
   bool topk = false;
   int64_t k = 0;
@@ -840,8 +846,27 @@ struct Planner {
         if (!operand(k, o, &lt) || o.probe >= 0 || lt != TQP_LT_UTF8) small = false;
         else P.key_columns.push_back(o.column);
       }
+      // hashable: <= kMaxKeys int64 / date / string keys, each a fact column
+      // or a probe's root column
+      bool hashable = G.keys.size() <= static_cast<size_t>(kMaxKeys);
+      for (int k : G.keys) {
+        OperandDesc o;
+        int lt;
+        if (!hashable) break;
+        if (!operand(k, o, &lt) || (lt != TQP_LT_INT64 && lt != TQP_LT_DATE && lt != TQP_LT_UTF8)) {
+          hashable = false;
+          break;
+        }
+        P.hkeys.push_back(o);
+        P.hkey_lt.push_back(lt);
+      }
+      if (!hashable) {
+        P.hkeys.clear();
+        P.hkey_lt.clear();
+      }
       if (small) {
         P.mode = MODE_SMALL;
+        P.hash_alt = hashable;
       } else {
         // group = matched build row of one probe
         P.key_columns.clear();
@@ -875,10 +900,16 @@ struct Planner {
             P.group_key_root_columns = cols;
           }
         }
-        if (gp < 0) return fail("group keys are neither small byte keys nor a build row");
-        P.mode = MODE_BUILDGRP;
-        P.group_probe = gp;
-        P.builds[P.probes[gp].build].assign_groups = true;
+        if (gp >= 0) {
+          P.mode = MODE_BUILDGRP;
+          P.group_probe = gp;
+          P.builds[P.probes[gp].build].assign_groups = true;
+        } else if (hashable) {
+          P.mode = MODE_HASH;
+          P.group_key_root_columns.clear();
+        } else {
+          return fail("group keys are neither small byte keys, a build row, nor hashable int/date/string columns");
+        }
       }
     }
     // aggregates
@@ -901,6 +932,20 @@ struct Planner {
       P.outs.push_back(o);
     }
     if (P.accs.size() > static_cast<size_t>(kMaxAcc)) return fail("too many accumulators");
+    // accumulator operands on a probe's root row: only the hash-group kernel
+    // reads them (at the matched row); other modes stage fact columns only
+    bool probe_operand = false;
+    for (const auto& a : P.accs)
+      for (const auto& f : a.f) probe_operand = probe_operand || (f.kind != FK_CONST && f.x.probe >= 0);
+    if (probe_operand && P.mode != MODE_HASH) {
+      if (P.hkeys.empty()) return fail("aggregate operand on a build-side row outside a hash-group unit");
+      if (P.mode == MODE_BUILDGRP) P.builds[P.probes[P.group_probe].build].assign_groups = false;
+      P.mode = MODE_HASH;
+      P.group_probe = -1;
+      P.hash_alt = false;
+      P.key_columns.clear();
+      P.group_key_root_columns.clear();
+    }
     // the unit must cover a contiguous step range
     P.first_step = *covered.begin();
     P.last_step = agg_step;
@@ -912,7 +957,7 @@ struct Planner {
     int next = agg_step + 1;
     std::map<int, int> slot_to_out;
     for (size_t i = 0; i < P.outs.size(); ++i) slot_to_out[P.outs[i].slot] = static_cast<int>(i);
-    if (P.mode == MODE_BUILDGRP && next + 1 < static_cast<int>(A.rels.size())) {
+    if ((P.mode == MODE_BUILDGRP || P.mode == MODE_HASH) && next + 1 < static_cast<int>(A.rels.size())) {
       int s = next;
       std::vector<int> proj_cols = G.cols;
       if (A.rels[s].kind == Rel::PROJECT && A.rels[s].input == agg_step) {
@@ -1287,7 +1332,37 @@ struct GroupSpec {
   int sort_asc[4];
   const unsigned* present = nullptr;  // group g exists iff bit g is set (nullptr: every slot, zeroed)
   int acc_words = 2;                  // per accumulator: 2 = int128 (lo, hi), kLimbWords = limbs
+  // MODE_HASH: group keys decoded from the group's code (tag - 1, ProbeSpec
+  // GKey), counts packed as rows | adds << 40
+  const unsigned long long* codes = nullptr;
+  long long kmin[kMaxKeys] = {0, 0, 0, 0}, kstep[kMaxKeys] = {1, 1, 1, 1};
+  unsigned long long krange[kMaxKeys] = {1, 1, 1, 1}, kstride[kMaxKeys] = {1, 1, 1, 1};
+  int key_w[kMaxKeys] = {0, 0, 0, 0};  // output width of key i: 0 int64, else STR8 bytes
+  int cnt_packed = 0;
+  const long long* absmax = nullptr;  // MODE_HASH: int sums exact iff absmax x rows < 2^63
+  int flag_word = -1;                 // MODE_HASH special run: record word of the NaN/Inf bits
 };
+
+__device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g);
+
+// group key i of group g (STR8 keys: the row's bytes big-endian)
+__device__ __forceinline__ long long group_key_value(const GroupSpec& s, int i, unsigned g) {
+  if (s.codes) {
+    const unsigned long long dg = ((s.codes[g] - 1ULL) / s.kstride[i]) % s.krange[i];
+    return s.key_w[i] ? static_cast<long long>(dg) : s.kmin[i] + static_cast<long long>(dg * static_cast<unsigned long long>(s.kstep[i]));
+  }
+  return s.key_cols[i][group_src_row(s, g)];
+}
+__device__ __forceinline__ long long group_count(const GroupSpec& s, unsigned g) {
+  const unsigned long long w = s.gcnt[g * s.cnt_stride];
+  return static_cast<long long>(s.cnt_packed ? (w & kCntMask) : w);
+}
+// limb words exact: fewer than kLimbMaxRows adds reached them
+__device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
+  if (s.acc_words != kLimbWords) return true;
+  const unsigned long long w = s.gcnt[g * s.cnt_stride];
+  return (s.cnt_packed ? (w >> 40) : w) < static_cast<unsigned long long>(kLimbMaxRows);
+}
 
 // accumulator a of group g as int128
 __device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, int a) {
@@ -1303,9 +1378,9 @@ __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned 
 __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
                                                 bool& is_f64) {
   const OutKind& o = s.f.outs[j];
-  long long cnt = static_cast<long long>(s.gcnt[g * s.cnt_stride]);
+  long long cnt = group_count(s, g);
   if (o.fn >= 10) {
-    bits = static_cast<unsigned long long>(s.key_cols[o.fn - 10][group_src_row(s, g)]);
+    bits = static_cast<unsigned long long>(group_key_value(s, o.fn - 10, g));
     is_f64 = false;
     return true;
   }
@@ -1317,10 +1392,11 @@ __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsig
   const __int128 v128 = group_acc(s, g, o.acc);
   const unsigned long long lo = static_cast<unsigned long long>(v128);
   const unsigned long long hi = static_cast<unsigned long long>(static_cast<unsigned __int128>(v128) >> 64);
-  const bool limbs_ok = s.acc_words != kLimbWords || cnt < kLimbMaxRows;
+  const bool limbs_ok = group_limbs_ok(s, g);
   if (s.f.acc_is_int[o.acc]) {
     long long v = static_cast<long long>(lo);
     bool fits = static_cast<long long>(hi) == (v >> 63);
+    if (s.absmax && static_cast<double>(*s.absmax) * static_cast<double>(cnt) >= 9.0e18) fits = false;
     if (o.fn == 0) {
       bits = static_cast<unsigned long long>(v);
       is_f64 = false;
@@ -1331,9 +1407,27 @@ __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsig
     return fits && limbs_ok;
   }
   double sum = q64_to_f64(lo, hi);
+  if (s.flag_word >= 0) {  // NaN / +Inf / -Inf among the group's values (IEEE sum)
+    const unsigned f = static_cast<unsigned>(s.gcnt[g * s.cnt_stride + s.flag_word] >> (3 * o.acc)) & 7u;
+    if ((f & 1u) || (f & 6u) == 6u) sum = __longlong_as_double(0x7ff8000000000000LL);
+    else if (f & 2u) sum = __longlong_as_double(0x7ff0000000000000LL);
+    else if (f & 4u) sum = __longlong_as_double(static_cast<long long>(0xfff0000000000000ULL));
+  }
   is_f64 = true;
   bits = static_cast<unsigned long long>(__double_as_longlong(o.fn == 0 ? sum : __ddiv_rn(sum, static_cast<double>(cnt))));
   return limbs_ok;
+}
+
+// output row r of group output j (a hash unit's STR8 key: the big-endian
+// bytes of its digit)
+__device__ __forceinline__ void store_group_out(const GroupSpec& s, int j, long long r, unsigned long long bits) {
+  const int w = s.f.outs[j].fn >= 10 ? s.key_w[s.f.outs[j].fn - 10] : 0;
+  if (w) {
+    uint8_t* o = static_cast<uint8_t*>(s.f.out_ptr[j]) + r * w;
+    for (int b = 0; b < w; ++b) o[b] = static_cast<uint8_t>(bits >> (8 * (w - 1 - b)));
+  } else {
+    static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
+  }
 }
 
 // lexicographic candidate key: sort keys (with direction), then group keys asc
@@ -1349,7 +1443,7 @@ __device__ __forceinline__ unsigned long long sort_key_word(const GroupSpec& s, 
 __device__ __forceinline__ int cand_keys(const GroupSpec& s, unsigned g, unsigned long long* k) {
   int n = 0;
   for (int i = 0; i < s.nsort; ++i) k[n++] = sort_key_word(s, i, g);
-  for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(s.key_cols[i][group_src_row(s, g)]));
+  for (int i = 0; i < s.nkeyc; ++i) k[n++] = radix_key(static_cast<int64_t>(group_key_value(s, i, g)));
   return n;
 }
 
@@ -1431,7 +1525,7 @@ __device__ __forceinline__ void cand_keys_nk(const GroupSpec& s, unsigned g, uns
 #pragma unroll
   for (int q = 0; q < NK; ++q)
     k[q] = q < s.nsort ? sort_key_word(s, q < 4 ? q : 3, g)
-                       : radix_key(static_cast<int64_t>(s.key_cols[q - s.nsort][group_src_row(s, g)]));
+                       : radix_key(static_cast<int64_t>(group_key_value(s, q - s.nsort, g)));
 }
 
 // Exact top-k in one launch, without per-group full keys. The walk only
@@ -1536,7 +1630,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
         // limb sums are exact below kLimbMaxRows rows per group
-        if (s.acc_words == kLimbWords && gc[u] >= static_cast<unsigned long long>(kLimbMaxRows)) {
+        if (gc[u] && !group_limbs_ok(s, gq[u])) {
           err[0] = 1;
           err[3] = FR_LIMB_ROWS;
         }
@@ -1746,7 +1840,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
           err[0] = 1;
           err[3] = FR_GROUP_VALUE;
         }
-        static_cast<unsigned long long*>(s.f.out_ptr[j])[lane] = bits;
+        store_group_out(s, j, lane, bits);
       }
     }
     if (lane == 0) *nout = F.cnt;
@@ -1777,7 +1871,7 @@ __global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids, co
       unsigned long long bits;
       bool f;
       if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
-      static_cast<unsigned long long*>(s.f.out_ptr[j])[r] = bits;
+      store_group_out(s, j, r, bits);
     }
   }
 }
@@ -1788,6 +1882,14 @@ __global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, lon
     mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i * cnt_stride] != 0;
 }
 
+// MODE_HASH: bit per claimed slot of the group table
+__global__ void k_hash_present(const unsigned long long* __restrict__ tag, long long cap, unsigned* __restrict__ present) {
+  const long long n32 = (cap + 31) & ~31LL;  // warp-uniform trip count (blockDim % 32 == 0)
+  for (long long i = gtid(); i < n32; i += gstride()) {
+    const unsigned bits = __ballot_sync(0xffffffffu, i < cap && tag[i] != 0ULL);
+    if ((threadIdx.x & 31) == 0) present[i >> 5] = bits;
+  }
+}
 __global__ void k_group_keys(const unsigned long long* __restrict__ group_table, const long long* __restrict__ gids, long long n,
                              const long long* __restrict__ key_col, long long* __restrict__ out) {
   for (long long i = gtid(); i < n; i += gstride())
@@ -1813,10 +1915,10 @@ __global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, 
     const unsigned g = static_cast<unsigned>(gids[i]);
     const long long row = group_src_row(s, g);
     unsigned long long* w = out + i * words;
-    w[0] = static_cast<unsigned long long>(bkey[row]);
-    for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(s.key_cols[k][row]);
-    w[1 + s.nkeyc] = s.gcnt[g * s.cnt_stride];
-    if (s.acc_words == kLimbWords && w[1 + s.nkeyc] >= static_cast<unsigned long long>(kLimbMaxRows)) err[0] = 1;
+    w[0] = s.codes ? s.codes[g] - 1ULL : static_cast<unsigned long long>(bkey[row]);
+    for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(group_key_value(s, k, g));
+    w[1 + s.nkeyc] = static_cast<unsigned long long>(group_count(s, g));
+    if (!group_limbs_ok(s, g)) err[0] = 1;
     for (int a = 0; a < s.f.nacc; ++a) {  // records carry int128 (lo, hi)
       const unsigned __int128 v = static_cast<unsigned __int128>(group_acc(s, g, a));
       w[2 + s.nkeyc + 2 * a] = static_cast<unsigned long long>(v);
@@ -2040,10 +2142,11 @@ bool merge_range_terms(const std::vector<Term>& in, ProbeSpec& ps, std::vector<O
 const void* tile_kernel(int mode, int nacc) {
 #define TQP_TK(M, N) \
   if (mode == M && nacc == N) return reinterpret_cast<const void*>(&k_tile<M, N>);
-  TQP_TK(MODE_SCALAR, 1) TQP_TK(MODE_SCALAR, 2) TQP_TK(MODE_SCALAR, 3) TQP_TK(MODE_SCALAR, 4)
+  TQP_TK(MODE_SCALAR, 0) TQP_TK(MODE_SCALAR, 1) TQP_TK(MODE_SCALAR, 2) TQP_TK(MODE_SCALAR, 3) TQP_TK(MODE_SCALAR, 4)
   TQP_TK(MODE_SMALL, 1) TQP_TK(MODE_SMALL, 2) TQP_TK(MODE_SMALL, 3) TQP_TK(MODE_SMALL, 4) TQP_TK(MODE_SMALL, 5)
   TQP_TK(MODE_SMALL, 6)
   TQP_TK(MODE_BUILDGRP, 1) TQP_TK(MODE_BUILDGRP, 2) TQP_TK(MODE_BUILDGRP, 3) TQP_TK(MODE_BUILDGRP, 4)
+  TQP_TK(MODE_HASH, 0) TQP_TK(MODE_HASH, 1) TQP_TK(MODE_HASH, 2) TQP_TK(MODE_HASH, 3) TQP_TK(MODE_HASH, 4)
 #undef TQP_TK
   return nullptr;
 }
@@ -2462,9 +2565,112 @@ std::string build_key(BuildSpec b) {
   return k;
 }
 
+// min / max (and, for Date keys, day alignment) of int64 key columns, cached
+// with the column (input columns are immutable): one launch per missing
+// column and one host round trip for all of them
+void ensure_key_info(Ctx& c, const std::vector<std::pair<const Column*, long long>>& cols, const std::vector<bool>& day) {
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < cols.size(); ++i) {
+    std::lock_guard<std::mutex> lk(cols[i].first->range->mu);
+    const KeyRange& r = *cols[i].first->range;
+    if (!r.ready || (day[i] && r.day < 0)) todo.push_back(i);
+  }
+  if (todo.empty()) return;
+  std::vector<long long> init(3 * todo.size());
+  for (size_t j = 0; j < todo.size(); ++j) {
+    init[3 * j] = 0x7fffffffffffffffLL;
+    init[3 * j + 1] = static_cast<long long>(0x8000000000000000ULL);
+    init[3 * j + 2] = 0;
+  }
+  auto buf = c.alloc_bytes(sizeof(long long) * init.size());
+  TQP_CUDA(cudaMemcpyAsync(buf->ptr, init.data(), sizeof(long long) * init.size(), cudaMemcpyHostToDevice, c.stream));
+  for (size_t j = 0; j < todo.size(); ++j) {
+    const auto& [col, rows] = cols[todo[j]];
+    long long* out = static_cast<long long*>(buf->ptr) + 3 * j;
+    if (rows <= 0) continue;
+    if (day[todo[j]])
+      k_minmax<true><<<c.grid_for(rows, 256, 8, 16), 256, 0, c.stream>>>(col->t.ptr<long long>(), rows, out);
+    else
+      k_minmax<false><<<c.grid_for(rows, 256, 8, 16), 256, 0, c.stream>>>(col->t.ptr<long long>(), rows, out);
+    c.count_launch();
+  }
+  std::vector<long long> got(init.size());
+  TQP_CUDA(cudaMemcpyAsync(got.data(), buf->ptr, sizeof(long long) * got.size(), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  for (size_t j = 0; j < todo.size(); ++j) {
+    KeyRange& r = *cols[todo[j]].first->range;
+    std::lock_guard<std::mutex> lk(r.mu);
+    r.mn = got[3 * j];
+    r.mx = got[3 * j + 1];
+    r.ready = true;
+    if (day[todo[j]]) r.day = got[3 * j + 2] ? 0 : 1;
+  }
+}
+
+// MODE_HASH table shape: shared-memory records per CTA when the whole code
+// range fits kHashPrivBytes, a direct-address global table (slot = code)
+// while the range is at most 4 slots per fact row (and <= 2^26), otherwise
+// open addressing at load <= 1/2
+// STR8 key widths of a MODE_HASH unit, 8 bits each (partial header word 7)
+unsigned long long hash_key_widths(const ProbeSpec& ps) {
+  unsigned long long w = 0;
+  for (int i = 0; i < ps.nhkeys; ++i) w |= static_cast<unsigned long long>(ps.hkeys[i].width & 0xff) << (8 * i);
+  return w;
+}
+
+GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsigned* present) {
+  GroupSpec gs;
+  gs.f = fs;
+  gs.gacc = ps.gacc;
+  gs.gcnt = ps.gcnt;
+  gs.group_table = nullptr;
+  gs.cnt_stride = ps.gstride;
+  gs.acc_stride = ps.gstride;
+  gs.present = present;
+  gs.acc_words = kLimbWords;
+  gs.nkeyc = ps.nhkeys;
+  gs.nsort = 0;
+  gs.codes = ps.htag;
+  gs.cnt_packed = 1;
+  gs.absmax = ps.absmax_out;
+  gs.flag_word = ps.hflags;
+  for (int i = 0; i < ps.nhkeys; ++i) {
+    gs.key_cols[i] = nullptr;
+    gs.kmin[i] = ps.hkeys[i].kmin;
+    gs.kstep[i] = ps.hkeys[i].step;
+    gs.krange[i] = ps.hkeys[i].range;
+    gs.kstride[i] = ps.hkeys[i].stride;
+    gs.key_w[i] = ps.hkeys[i].width;
+  }
+  return gs;
+}
+
+__global__ void k_fill_u64(unsigned long long* __restrict__ p, long long n, unsigned long long v) {
+  for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
+}
+void fill_u64(Ctx& c, unsigned long long* p, long long n, unsigned long long v) {
+  if (n <= 0) return;
+  k_fill_u64<<<c.grid_for(n, 256), 256, 0, c.stream>>>(p, n, v);
+  c.count_launch();
+}
+
+// a fused unit that cannot take this data (host-side contract check): the
+// executor runs its steps per instruction; TQP_DEBUG_FALLBACK names the check
+bool nofuse(int line) {
+  if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: fused unit not run (fused.cu:%d)\n", line);
+  return false;
+}
+
+constexpr size_t kHashPrivBytes = 48 * 1024;
+constexpr unsigned long long kHashDirectMax = 1ULL << 26;
+constexpr size_t kHashMaxBytes = 24ULL << 30;
+
 struct Runner {
   PipeDesc P;
   std::shared_ptr<JitMemo> memo = std::make_shared<JitMemo>();
+  // MODE_SMALL units with hashable keys: the MODE_HASH unit a CTA overflow
+  // (more distinct codes than slots) reruns as, instead of the exact path
+  std::shared_ptr<const Runner> alt;
 
   bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, UnitPending* pend) const {
     return run(c, &slots, tables, nullptr, false, pend);
@@ -2472,8 +2678,13 @@ struct Runner {
 
   // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
   // narrow: the 8-slot small-group kernel only (after a 4-slot overflow)
+  // weighted: re-run after a build met a repeated key (1:N join): builds sum
+  // row weights per key and the fact scan counts rows by multiplicity
+  // special: re-run after a hash-group fp64 value was NaN or +-Inf: those are
+  // flagged per group (IEEE sum semantics) instead of summed in fixed point
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
-           bool narrow = false, UnitPending* pend = nullptr) const {
+           bool narrow = false, UnitPending* pend = nullptr, bool weighted = false, bool fullsort = false,
+           bool special = false) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
@@ -2495,7 +2706,7 @@ struct Runner {
       const BuildDesc& B = P.builds[bi];
       const Table* tab = bind_table(tables, B.table);
       const Column* key = tab ? tab->find(B.key_column) : nullptr;
-      if (!key || key->t.dtype != TQP_I64) return false;
+      if (!key || key->t.dtype != TQP_I64) return nofuse(__LINE__);
       std::lock_guard<std::mutex> lk(key->range->mu);
       if (key->range->ready) {
         mm[2 * bi] = key->range->mn;
@@ -2517,7 +2728,7 @@ struct Runner {
         const Table* tab = bind_table(tables, B.table);
         const Column* key = tab->find(B.key_column);
         if (tab->rows) {
-          k_minmax<<<c.grid_for(tab->rows, 256, 8, 16), 256, 0, c.stream>>>(
+          k_minmax<false><<<c.grid_for(tab->rows, 256, 8, 16), 256, 0, c.stream>>>(
               key->t.ptr<long long>(), tab->rows, static_cast<long long*>(mmb->ptr) + 2 * bi);
           c.count_launch();
         }
@@ -2540,14 +2751,32 @@ struct Runner {
     // one zeroed arena for the unit's small state - the error words, every
     // build's presence bitmap and the touched-group bitmap - so one memset
     // replaces one per buffer (each is host time between the unit's kernels)
+    // a build whose key range is too wide for direct addressing (or would
+    // overflow the range arithmetic) is an open-addressing table of `cap`
+    // slots; the group of a group-assigning hashed build is its slot
     std::vector<size_t> bm_off(nb, 0);
+    std::vector<char> hashed(nb, 0);
+    std::vector<long long> slots_of(nb, 0);  // direct: key range; hashed: capacity
     size_t arena = 256, touched_off = 0;
+    bool generic_only = weighted;  // the NVRTC kernels address dense, unweighted builds only
     for (size_t bi = 0; bi < nb; ++bi) {
       const long long n = bind_table(tables, P.builds[bi].table)->rows;
-      const long long range = n ? mm[2 * bi + 1] - mm[2 * bi] + 1 : 1;
-      if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
+      const long long mn = mm[2 * bi], mx = mm[2 * bi + 1];
+      const unsigned long long span = static_cast<unsigned long long>(mx) - static_cast<unsigned long long>(mn);
+      const bool wide = n && (span > static_cast<unsigned long long>(16LL * n + (1LL << 22)) || span >= (1ULL << 31));
+      long long range = n ? static_cast<long long>(span) + 1 : 1;
+      if (wide) {
+        if (mn == static_cast<long long>(0x8000000000000000ULL)) return nofuse(__LINE__);  // no empty-slot marker
+        if (n >= (1LL << 31)) return nofuse(__LINE__);
+        long long cap = 1024;
+        while (cap < 2 * n) cap <<= 1;
+        hashed[bi] = 1;
+        range = cap;
+        generic_only = true;
+      }
+      slots_of[bi] = range;
       bm_off[bi] = arena;
-      arena += (sizeof(unsigned) * static_cast<size_t>((range + 31) / 32) + 255) & ~size_t(255);
+      if (!wide) arena += (sizeof(unsigned) * static_cast<size_t>((range + 31) / 32) + 255) & ~size_t(255);
       if (P.mode == MODE_BUILDGRP && P.group_probe >= 0 && P.group_probe < static_cast<int>(P.probes.size()) &&
           P.probes[P.group_probe].build == static_cast<int>(bi)) {
         touched_off = arena;
@@ -2563,8 +2792,7 @@ struct Runner {
       const Table* tab = bind_table(tables, B.table);
       const Column* key = tab->find(B.key_column);
       long long n = tab->rows;
-      long long range = n ? mm[2 * bi + 1] - mm[2 * bi] + 1 : 1;
-      if (range <= 0 || range > (16LL * n + (1LL << 22)) || range > (1LL << 31)) return false;  // not dense
+      const long long range = slots_of[bi];
       BuildSpec bs;
       zero_padding(bs);  // its bytes key the kernel memo
       bs.n = n;
@@ -2576,9 +2804,23 @@ struct Runner {
       // only an unfiltered one, read as `entry != 0`, needs zeroed slots -
       // and not even that when its n unique keys fill all n slots of the
       // range (a repeated key leaves a slot unwritten, but it is flagged as
-      // a duplicate and the unit is discarded)
-      if (!build_filtered(B) && range != n)
+      // a duplicate and the unit is discarded). A hashed table's entries are
+      // only read where the slot's key matched (written by the claiming row).
+      if (!hashed[bi] && ((!build_filtered(B) && range != n) || weighted))
         TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
+      if (hashed[bi]) {
+        auto hk = c.alloc_bytes(sizeof(long long) * range);
+        keep.push_back(hk);
+        fill_u64(c, static_cast<unsigned long long*>(hk->ptr), range, static_cast<unsigned long long>(bs.kmin - 1));
+        bs.hkeys = static_cast<long long*>(hk->ptr);
+        bs.hmask = static_cast<unsigned long long>(range - 1);
+      }
+      if (weighted) {
+        auto mu = c.alloc_bytes(sizeof(unsigned) * range);
+        keep.push_back(mu);
+        TQP_CUDA(cudaMemsetAsync(mu->ptr, 0, mu->bytes, c.stream));
+        bs.mult = static_cast<unsigned*>(mu->ptr);
+      }
       keep.push_back(table);
       bs.table = static_cast<unsigned long long*>(table->ptr);
       build_range[bi] = range;
@@ -2590,12 +2832,12 @@ struct Runner {
         Term nt;
         StrTerm st;
         bool is_str;
-        if (!make_term(tables, B.table, t, &nt, &st, &is_str)) return false;
+        if (!make_term(tables, B.table, t, &nt, &st, &is_str)) return nofuse(__LINE__);
         if (is_str) {
-          if (bs.nstr >= kMaxStrTerms) return false;
+          if (bs.nstr >= kMaxStrTerms) return nofuse(__LINE__);
           bs.str[bs.nstr++] = st;
         } else {
-          if (bs.nterms >= kMaxTerms) return false;
+          if (bs.nterms >= kMaxTerms) return nofuse(__LINE__);
           bs.terms[bs.nterms++] = nt;
         }
       }
@@ -2603,12 +2845,12 @@ struct Runner {
         Term nt;
         StrTerm st;
         bool is_str;
-        if (!make_term(tables, B.table, t, &nt, &st, &is_str) || !is_str) return false;
+        if (!make_term(tables, B.table, t, &nt, &st, &is_str) || !is_str) return nofuse(__LINE__);
         bs.flags[bs.nflags++] = st;
       }
       for (const auto& ch : B.children) {
         const Column* kc = tab->find(ch.fact_column);
-        if (!kc || kc->t.dtype != TQP_I64) return false;
+        if (!kc || kc->t.dtype != TQP_I64) return nofuse(__LINE__);
         Probe p = built[ch.build];
         p.key = {kc->t.data(), OT_I64, -1};
         bs.probes[bs.nprobes++] = p;
@@ -2626,13 +2868,13 @@ struct Runner {
         bs.zrec = grec_p;
         bs.zrec_words = grec_words;
       }
-      if (!ok) return false;
+      if (!ok) return nofuse(__LINE__);
       if (n) {
         // kBuildRows rows per thread: the per-row dependent loads (term,
         // probe, insert) need many warps in flight
         const void* bk = reinterpret_cast<const void*>(&k_build);
         int rows_per_thread = kBuildRows;
-        if (jit_wanted(n) && build_tile_wanted(n)) {
+        if (jit_wanted(n) && build_tile_wanted(n) && !generic_only) {
           // large build side: TMA-staged scan of its columns (jit_build_tile.cuh)
           TileSpec bt;
           bt.p.n = n;
@@ -2683,7 +2925,7 @@ struct Runner {
             }
           }
         }
-        if (bk && jit_wanted(n)) {
+        if (bk && jit_wanted(n) && !generic_only) {
           rows_per_thread = jit_build_rows();
           hp.mark("bprep");
           std::string key = build_key(bs);
@@ -2705,13 +2947,16 @@ struct Runner {
       pr.kmin = bs.kmin;
       pr.range = range;
       pr.table = bs.table;
-      pr.bitmap = bs.bitmap;
+      pr.bitmap = hashed[bi] ? nullptr : bs.bitmap;
+      pr.hkeys = bs.hkeys;
+      pr.hmask = bs.hmask;
+      pr.mult = bs.mult;
       built[bi] = pr;
     }
     hp.mark("builds");
     // fact probe
     const Table* fact = bind_table(tables, P.fact_table);
-    if (!fact) return false;
+    if (!fact) return nofuse(__LINE__);
     ProbeSpec ps;
     zero_padding(ps);
     ps.n = fact->rows;
@@ -2723,23 +2968,23 @@ struct Runner {
       Term nt;
       StrTerm st;
       bool is_str;
-      if (!make_term(tables, P.fact_table, t, &nt, &st, &is_str) || is_str) return false;
-      if (nt.kind <= TK_F64 && reinterpret_cast<uintptr_t>(nt.x.ptr) % 16) return false;
+      if (!make_term(tables, P.fact_table, t, &nt, &st, &is_str) || is_str) return nofuse(__LINE__);
+      if (nt.kind <= TK_F64 && reinterpret_cast<uintptr_t>(nt.x.ptr) % 16) return nofuse(__LINE__);
       raw_terms.push_back(nt);
     }
     std::vector<Operand> term_cols;
-    if (!merge_range_terms(raw_terms, ps, term_cols)) return false;
+    if (!merge_range_terms(raw_terms, ps, term_cols)) return nofuse(__LINE__);
     for (const auto& p : P.probes) {
       Probe pr = built[p.build];
       pr.key = make_operand(tables, P, {-1, p.fact_column}, &ok);
-      if (pr.key.type != OT_I64) return false;
+      if (pr.key.type != OT_I64) return nofuse(__LINE__);
       ps.probes[ps.nprobes++] = pr;
     }
     for (const auto& a : P.accs) {
       Acc& d = ps.acc[ps.nacc++];
       d.is_int = a.is_int;
       d.nf = static_cast<int>(a.f.size());
-      if (!a.is_int && a.f.size() > static_cast<size_t>(kFixedFactors)) return false;
+      if (!a.is_int && a.f.size() > static_cast<size_t>(kFixedFactors)) return nofuse(__LINE__);
       for (size_t i = 0; i < a.f.size(); ++i) {
         if (a.f[i].kind != FK_CONST) d.f[i].x = make_operand(tables, P, a.f[i].x, &ok);
         d.f[i].kind = a.f[i].kind;
@@ -2765,7 +3010,114 @@ struct Runner {
     }
     for (const auto& kcol : P.key_columns) ps.keys[ps.nkeys++] = make_operand(tables, P, {-1, kcol}, &ok);
     ps.group_probe = P.mode == MODE_BUILDGRP ? P.group_probe : -1;
-    if (!ok) return false;
+    // small-group keys are 1-byte strings; wider ones (or an accumulator
+    // count without a small-group kernel) run as the hash-group unit
+    if (P.mode == MODE_SMALL && alt && (!ok || !tile_kernel(MODE_SMALL, ps.nacc)))
+      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special);
+    if (!ok) return nofuse(__LINE__);
+    // probes whose matched root row is read: with repeated build keys such a
+    // probe must match exactly one row (checked per row in a weighted run)
+    ps.weighted = weighted ? 1 : 0;
+    ps.root_mask = 0;
+    for (int a = 0; a < ps.nacc; ++a) {
+      if (ps.acc[a].gate_probe >= 0) ps.root_mask |= 1u << ps.acc[a].gate_probe;
+      for (int i = 0; i < ps.acc[a].nf; ++i)
+        if (ps.acc[a].f[i].kind != FK_CONST && ps.acc[a].f[i].x.src >= 0) ps.root_mask |= 1u << ps.acc[a].f[i].x.src;
+    }
+    if (P.mode == MODE_BUILDGRP && P.group_probe >= 0) ps.root_mask |= 1u << P.group_probe;
+    for (const auto& hk : P.hkeys)
+      if (hk.probe >= 0) ps.root_mask |= 1u << hk.probe;
+    // MODE_HASH: key digits from the key columns' ranges, the code's mixed
+    // radix, and the table shape (private / direct / open addressing)
+    std::shared_ptr<DevBuf> htag_buf, hrec_buf;
+    unsigned long long hcap = 0;
+    int hrec_words = 0;
+    if (P.mode == MODE_HASH) {
+      const int nk = static_cast<int>(P.hkeys.size());
+      if (nk < 1 || nk > kMaxKeys) return nofuse(__LINE__);
+      std::vector<const Column*> kc(nk);
+      std::vector<std::pair<const Column*, long long>> icols;
+      std::vector<bool> iday;
+      for (int i = 0; i < nk; ++i) {
+        const OperandDesc& o = P.hkeys[i];
+        const std::string& tname = o.probe < 0 ? P.fact_table : P.builds[P.probes[o.probe].build].table;
+        const Table* tab = bind_table(tables, tname);
+        kc[i] = tab ? tab->find(o.column) : nullptr;
+        if (!kc[i]) return nofuse(__LINE__);
+        GKey& K = ps.hkeys[i];
+        K.x.ptr = kc[i]->t.data();
+        K.x.src = o.probe;
+        K.x.col = -1;
+        if (P.hkey_lt[i] == TQP_LT_UTF8) {
+          if (kc[i]->t.dtype != TQP_STR8 || kc[i]->t.cols < 1 || kc[i]->t.cols > 7) return nofuse(__LINE__);
+          K.x.type = OT_U8;
+          K.width = static_cast<int>(kc[i]->t.cols);
+          K.range = 1ULL << (8 * K.width);
+        } else {
+          if (kc[i]->t.dtype != TQP_I64 || kc[i]->t.cols != 1) return nofuse(__LINE__);
+          if (reinterpret_cast<uintptr_t>(K.x.ptr) % 16) return nofuse(__LINE__);
+          K.x.type = OT_I64;
+          icols.push_back({kc[i], tab->rows});
+          iday.push_back(P.hkey_lt[i] == TQP_LT_DATE);
+        }
+      }
+      ensure_key_info(c, icols, iday);
+      unsigned __int128 total = 1;
+      for (int i = 0; i < nk; ++i) {
+        GKey& K = ps.hkeys[i];
+        if (K.width) {
+          total *= K.range;
+          continue;
+        }
+        const KeyRange& r = *kc[i]->range;
+        if (r.mn > r.mx) {  // empty key column: no row reaches the table
+          K.kmin = 0;
+          K.range = 1;
+        } else {
+          K.kmin = r.mn;
+          K.step = (P.hkey_lt[i] == TQP_LT_DATE && r.day == 1) ? 86400000000000LL : 1;
+          K.range = (static_cast<unsigned long long>(r.mx) - static_cast<unsigned long long>(r.mn)) /
+                        static_cast<unsigned long long>(K.step) + 1ULL;
+          if (K.range == 0) return nofuse(__LINE__);  // the full 2^64 span
+        }
+        total *= K.range;
+        if (total > (static_cast<unsigned __int128>(1) << 62)) return nofuse(__LINE__);
+      }
+      if (total > (static_cast<unsigned __int128>(1) << 62)) return nofuse(__LINE__);
+      unsigned long long stride = 1;
+      for (int i = nk - 1; i >= 0; --i) {
+        ps.hkeys[i].stride = stride;
+        stride *= ps.hkeys[i].range;
+      }
+      ps.nhkeys = nk;
+      const unsigned long long R = static_cast<unsigned long long>(total);
+      // special: one more word per record, NaN / +Inf / -Inf bits per accumulator
+      hrec_words = (1 + kLimbWords * std::max(1, nacc_all) + (special ? 1 : 0) + 3) & ~3;
+      ps.hflags = special ? 1 + kLimbWords * std::max(1, nacc_all) : -1;
+      const size_t priv_bytes = static_cast<size_t>(R) * (1 + kLimbWords * nacc_all) * sizeof(unsigned long long);
+      ps.hpriv = priv_bytes <= kHashPrivBytes && !std::getenv("TQP_HASH_NOPRIV");
+      ps.hdirect = ps.hpriv || (R <= kHashDirectMax && R <= 4ULL * static_cast<unsigned long long>(ps.n) + (1ULL << 20));
+      if (ps.hdirect) {
+        hcap = R;
+      } else {
+        const unsigned long long want = 2ULL * std::min<unsigned long long>(static_cast<unsigned long long>(std::max<long long>(ps.n, 1)), R);
+        hcap = 1024;
+        while (hcap < want) hcap <<= 1;
+      }
+      if (static_cast<double>(hcap) * (8.0 + 8.0 * hrec_words) > static_cast<double>(kHashMaxBytes)) return nofuse(__LINE__);
+      // direct tables are indexed by code: hmask + 1 is the slot count
+      ps.hmask = hcap - 1;
+      htag_buf = c.alloc_bytes(sizeof(unsigned long long) * hcap);
+      hrec_buf = c.alloc_bytes(sizeof(unsigned long long) * hrec_words * hcap);
+      TQP_CUDA(cudaMemsetAsync(htag_buf->ptr, 0, htag_buf->bytes, c.stream));
+      // private runs flush into zeroed records; otherwise the claiming row zeroes
+      if (ps.hpriv) TQP_CUDA(cudaMemsetAsync(hrec_buf->ptr, 0, hrec_buf->bytes, c.stream));
+      ps.htag = static_cast<unsigned long long*>(htag_buf->ptr);
+      ps.absmax_out = po ? nullptr : err + 5;  // sharded partials keep the whole-scan bound
+      ps.gcnt = static_cast<unsigned long long*>(hrec_buf->ptr);
+      ps.gacc = ps.gcnt + 1;
+      ps.gstride = hrec_words;
+    }
     // prefix sharing: an fp64 accumulator whose leading factors equal another
     // (earlier, ungated) accumulator's whole product starts from that value:
     // ((p*(1-d))*(1+t)) reuses p*(1-d) with identical rounding
@@ -2796,11 +3148,12 @@ struct Runner {
       }
     }
 
-    if (ps.nacc > max_acc_for(P.mode)) return false;
-    // the tile kernels read accumulator operands from the staged fact tile
+    if (ps.nacc > max_acc_for(P.mode)) return nofuse(__LINE__);
+    // the tile kernels read accumulator operands from the staged fact tile;
+    // MODE_HASH (generic kernel) also reads probe-root columns at the match
     for (int a = 0; a < ps.nacc; ++a)
       for (int i = 0; i < kFixedFactors; ++i)
-        if (ps.acc[a].f[i].kind != FK_CONST && ps.acc[a].f[i].x.src >= 0) return false;
+        if (ps.acc[a].f[i].kind != FK_CONST && ps.acc[a].f[i].x.src >= 0 && P.mode != MODE_HASH) return nofuse(__LINE__);
     // distinct fact columns staged per tile; operands address them by index
     TileSpec ts;
     zero_padding(ts);
@@ -2813,7 +3166,7 @@ struct Runner {
           return true;
         }
       }
-      if (ts.ncols >= kMaxCols) return false;
+      if (ts.ncols >= kMaxCols) return nofuse(__LINE__);
       ts.col_ptr[ts.ncols] = static_cast<const unsigned char*>(o.ptr);
       ts.col_w[ts.ncols] = w;
       o.col = ts.ncols++;
@@ -2821,21 +3174,25 @@ struct Runner {
     };
     for (int i = 0; i < ps.nterms; ++i) {
       if (ps.terms[i].kind >= RK_TRUE) continue;
-      if (!col_index(term_cols[i])) return false;
+      if (!col_index(term_cols[i])) return nofuse(__LINE__);
       ps.terms[i].col = term_cols[i].col;
     }
     for (int i = 0; i < ps.nprobes; ++i)
-      if (!col_index(ps.probes[i].key)) return false;
+      if (!col_index(ps.probes[i].key)) return nofuse(__LINE__);
     for (int a = 0; a < ps.nacc; ++a)
       for (int i = 0; i < ps.acc[a].nf; ++i)
-        if (ps.acc[a].f[i].kind != FK_CONST && !col_index(ps.acc[a].f[i].x)) return false;
+        if (ps.acc[a].f[i].kind != FK_CONST && !col_index(ps.acc[a].f[i].x)) return nofuse(__LINE__);
     for (int i = 0; i < ps.nkeys; ++i)
-      if (!col_index(ps.keys[i])) return false;
+      if (!col_index(ps.keys[i])) return nofuse(__LINE__);
+    for (int i = 0; i < ps.nhkeys; ++i)  // int64 fact keys come from the staged tile
+      if (!ps.hkeys[i].width && ps.hkeys[i].x.src < 0 && !col_index(ps.hkeys[i].x)) return nofuse(__LINE__);
     ts.rows = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::ROWS : kTileRows;
     ts.aux_bytes = static_cast<int>(P.mode == MODE_SMALL    ? aux_bytes_for<MODE_SMALL>(ps.nacc)
                                     : P.mode == MODE_SCALAR ? aux_bytes_for<MODE_SCALAR>(ps.nacc)
                                                             : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
-    const bool wide = P.mode == MODE_SMALL && !narrow && jit_wanted(ps.n) && small_wide_wanted();
+    if (P.mode == MODE_HASH && ps.hpriv)  // the CTA's records [code][count, limbs per accumulator]
+      ts.aux_bytes = static_cast<int>(((ps.hmask + 1) * (1 + kLimbWords * ps.nacc) * sizeof(unsigned long long) + 15) & ~15ULL);
+    const bool wide = P.mode == MODE_SMALL && !narrow && jit_wanted(ps.n) && small_wide_wanted() && !generic_only;
     int small_threads = TileShape<MODE_SMALL>::THREADS;
     const bool regacc = wide && small_regacc();
     const int wide_cw = regacc ? small_reg_cw() : kWideCW;
@@ -2857,8 +3214,8 @@ struct Runner {
     cudaFuncAttributes fa{};
     const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
     const void* kfn = tile_kernel(P.mode, ps.nacc);
-    if (!kfn) return false;
-    const bool jit = jit_wanted(ps.n);
+    if (!kfn) return nofuse(__LINE__);
+    const bool jit = jit_wanted(ps.n) && P.mode != MODE_HASH && !generic_only && ps.nacc > 0;
     if (jit) {
       std::vector<int> bm;
       for (const auto& pd : P.probes) bm.push_back(probe_mode_of(P.builds[pd.build]));
@@ -2875,11 +3232,14 @@ struct Runner {
     hp.mark("gen");
     fa.sharedSizeBytes = c.static_smem(kfn);
     const size_t budget = static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024;
-    if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return false;
+    if (fixed + 2 * static_cast<size_t>(ts.stage_bytes) > budget) return nofuse(__LINE__);
     ts.stages = static_cast<int>(std::min<size_t>(kMaxStages, (budget - fixed) / ts.stage_bytes));
     const size_t smem = fixed + static_cast<size_t>(ts.stages) * ts.stage_bytes;
     const std::string tile_name = std::string(jit ? "q_tile<" : "k_tile<") +
-                                  (P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small" : "buildgrp") + "," +
+                                  (P.mode == MODE_SCALAR  ? "scalar"
+                                   : P.mode == MODE_SMALL ? "small"
+                                   : P.mode == MODE_HASH  ? (ps.hpriv ? "hash-priv" : ps.hdirect ? "hash-direct" : "hash")
+                                                          : "buildgrp") + "," +
                                   std::to_string(ps.nacc) + ">";
     auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {
       cudaError_t e = c.ensure_smem(kernel, static_cast<int>(smem));
@@ -2898,7 +3258,7 @@ struct Runner {
     };
 
     FinalSpec fs;
-    if (!final_spec(P, fs)) return false;
+    if (!final_spec(P, fs)) return nofuse(__LINE__);
     const int grid = c.num_sms;  // persistent: one CTA per SM
     std::vector<Tensor> outs(P.outs.size());
     long long nrows = 0;
@@ -2915,8 +3275,8 @@ struct Runner {
                                            static_cast<unsigned long long>(words),
                                            static_cast<unsigned long long>(fs.nacc),
                                            static_cast<unsigned long long>(fs.nouts),
-                                           static_cast<unsigned long long>(P.key_columns.size()),
-                                           0};
+                                           static_cast<unsigned long long>(P.mode == MODE_HASH ? ps.nhkeys : static_cast<int>(P.key_columns.size())),
+                                           hash_key_widths(ps)};
         TQP_CUDA(cudaMemcpyAsync(buf->ptr, h, sizeof(h), cudaMemcpyHostToDevice, c.stream));
         po->buf = buf;
         po->words = kHdrWords + nrec * words;
@@ -2933,15 +3293,38 @@ struct Runner {
       ps.part = part_buf(grid, kSmallPartWords);
       launch_tile(kfn, small_threads, grid);
       if (!po) nrows = final_small(c, reinterpret_cast<const SmallPart*>(ps.part), grid, fs, err, outs);
+    } else if (P.mode == MODE_HASH) {
+      launch_tile(kfn, TileShape<MODE_HASH>::THREADS, grid);
+      auto pres = c.alloc_bytes(sizeof(unsigned) * ((hcap + 31) / 32 + 1));
+      keep.push_back(pres);
+      keep.push_back(htag_buf);
+      keep.push_back(hrec_buf);
+      k_hash_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
+          ps.htag, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
+      c.count_launch();
+      GroupSpec gs = hash_group_spec(ps, fs, static_cast<const unsigned*>(pres->ptr));
+      if (po) {
+        Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, static_cast<long long>(hcap), gs.present);
+        const long long n = gids.rows;
+        const int words = record_words(gs.nkeyc, fs.nacc);
+        unsigned long long* rec = part_buf(n, words);
+        if (n) {
+          k_fill_records<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(), n, nullptr, words, rec, err);
+          c.count_launch();
+        }
+      } else if (!emit_groups(c, gs, static_cast<long long>(hcap), reinterpret_cast<const long long*>(ps.htag), err, outs,
+                              nrows, fullsort)) {
+        return nofuse(__LINE__);
+      }
     } else {
       // MODE_BUILDGRP
       long long ngroups = build_range[P.probes[P.group_probe].build];
-      if (!grec_p || !group_present) return false;  // the group build assigns the groups
+      if (!grec_p || !group_present) return nofuse(__LINE__);  // the group build assigns the groups
       ps.gcnt = grec_p;
       ps.gacc = grec_p + 1;
       ps.gstride = grec_words;
       ps.group_probe = P.group_probe;
-      if (!touched_off) return false;
+      if (!touched_off) return nofuse(__LINE__);
       ps.touched = reinterpret_cast<unsigned*>(arena_p + touched_off);
       launch_tile(kfn, TileShape<MODE_BUILDGRP>::THREADS, grid);
       GroupSpec gs;
@@ -2958,7 +3341,7 @@ struct Runner {
       gs.nkeyc = static_cast<int>(P.group_key_root_columns.size());
       for (int i = 0; i < gs.nkeyc; ++i) {
         const Column* kc = groot->find(P.group_key_root_columns[i]);
-        if (!kc || kc->t.dtype != TQP_I64) return false;
+        if (!kc || kc->t.dtype != TQP_I64) return nofuse(__LINE__);
         gs.key_cols[i] = kc->t.ptr<long long>();
       }
       const Column* bk = groot->find(gb.key_column);
@@ -2974,8 +3357,8 @@ struct Runner {
                                                                   words, rec, err);
           c.count_launch();
         }
-      } else if (!emit_groups(c, gs, ngroups, bk->t.ptr<long long>(), err, outs, nrows)) {
-        return false;
+      } else if (!emit_groups(c, gs, ngroups, bk->t.ptr<long long>(), err, outs, nrows, fullsort)) {
+        return nofuse(__LINE__);
       }
     }
     long long herr[4] = {0, 0, 0, 0};
@@ -2996,12 +3379,28 @@ struct Runner {
     c.sync();
     hp.mark("sync");
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
-    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true);  // a fifth key in a CTA
+    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special);  // a fifth key in a CTA
+    if (herr[0] && herr[3] == FR_DUP_KEY && !weighted) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: repeated build keys: unit reruns weighted\n");
+      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special);
+    }
+    if (herr[0] && (herr[3] == FR_TOPK_BLOCK || herr[3] == FR_TOPK_FINAL) && !fullsort && P.topk && !po) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: top-k ties overflow: unit reruns with a full group sort\n");
+      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special);
+    }
+    if (herr[0] && herr[3] == FR_Q64_CONVERT && P.mode == MODE_HASH && !special && !po) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: NaN/Inf group values: unit reruns with special flags\n");
+      return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true);
+    }
+    if (herr[0] && alt && P.mode == MODE_SMALL) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: small-group unit reruns as hash-group (reason %lld)\n", herr[3]);
+      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special);
+    }
     if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
       std::fprintf(stderr, "tqp: fused unit left the fused path (reason %lld)\n", herr[3]);
     if (herr[0]) {  // preconditions violated: exact per-instruction path
       if (po) *po = Partial{};
-      return false;
+      return nofuse(__LINE__);
     }
     if (po) return true;
     if (nrows < 0) nrows = herr[2];
@@ -3081,10 +3480,35 @@ struct Runner {
     return k::compact(c, k::iota(c, ngroups), mask);
   }
 
+  // a group output column: STR8 (rows, width) for a string key of a hash
+  // unit, else per out_dtype
+  Tensor alloc_out(Ctx& c, const GroupSpec& gs, size_t j, long long rows) const {
+    const OutDesc& o = P.outs[j];
+    if (o.fn >= 10 && gs.key_w[o.fn - 10]) return c.alloc(TQP_STR8, rows, gs.key_w[o.fn - 10]);
+    return c.alloc(out_dtype(P, o), rows, 1);
+  }
+
   // group outputs: top-k in the reference's tie order, or every group
   // ascending by the (unique) build key `bk` (indexed like the key columns)
+  // fullsort: the top-k kernel met more ties than it keeps candidates for;
+  // every group is emitted in ascending key order and the ORDER BY + LIMIT
+  // run as the reference lowers them (stable SortPermRows per key, last key
+  // first, then the first k rows), on the device
   bool emit_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
-                   std::vector<Tensor>& outs, long long& nrows) const {
+                   std::vector<Tensor>& outs, long long& nrows, bool fullsort = false) const {
+    if (P.topk && fullsort) {
+      GroupSpec all = gs;
+      std::vector<Tensor> rows(outs.size());
+      if (!emit_all_groups(c, all, ngroups, bk, err, rows, nrows)) return false;
+      Tensor perm = k::iota(c, nrows);
+      for (int i = static_cast<int>(P.sort_outs.size()) - 1; i >= 0; --i)
+        perm = k::sort_perm_rows(c, rows[P.sort_outs[i].first], perm, P.sort_outs[i].second);
+      const long long m = std::min<long long>(nrows, P.k);
+      perm.rows = m;
+      for (size_t j = 0; j < outs.size(); ++j) outs[j] = k::gather(c, rows[j], perm);
+      nrows = m;
+      return true;
+    }
     if (P.topk) {
       gs.nsort = static_cast<int>(P.sort_outs.size());
       for (int i = 0; i < gs.nsort; ++i) {
@@ -3093,7 +3517,7 @@ struct Runner {
       }
       const int k = static_cast<int>(P.k);
       for (size_t j = 0; j < outs.size(); ++j) {
-        outs[j] = c.alloc(out_dtype(P, P.outs[j]), std::max(1, k), 1);
+        outs[j] = alloc_out(c, gs, j, std::max(1, k));
         gs.f.out_ptr[j] = outs[j].data();
       }
       nrows = 0;
@@ -3122,6 +3546,12 @@ struct Runner {
       nrows = -1;  // on the device (err[2]); read with the error flag
       return true;
     }
+    return emit_all_groups(c, gs, ngroups, bk, err, outs, nrows);
+  }
+
+  // every group with rows, ascending by its (unique) key `bk`
+  bool emit_all_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
+                       std::vector<Tensor>& outs, long long& nrows) const {
     Tensor gids = touched_groups(c, gs.gcnt, gs.cnt_stride, ngroups, gs.present);
     const long long n = gids.rows;
     Tensor keys = c.alloc(TQP_I64, n, 1);
@@ -3133,7 +3563,7 @@ struct Runner {
     // positions of the touched groups in ascending build-key order
     Tensor order = k::radix_sort_payload(c, keys, nullptr, false);
     for (size_t j = 0; j < outs.size(); ++j) {
-      outs[j] = c.alloc(out_dtype(P, P.outs[j]), n, 1);
+      outs[j] = alloc_out(c, gs, j, n);
       gs.f.out_ptr[j] = outs[j].data();
     }
     if (n) {
@@ -3149,11 +3579,20 @@ struct Runner {
               const std::string& where) const {
     FinalSpec fs;
     if (!final_spec(P, fs)) throw Error(TQP_ERR_EXEC, where + ": unit has no partial form");
-    const int nkeyc = static_cast<int>(P.group_key_root_columns.size());
+    const int nkeyc = static_cast<int>(P.mode == MODE_HASH ? P.hkeys.size() : P.group_key_root_columns.size());
+    const size_t hdr_keys = P.mode == MODE_HASH ? P.hkeys.size() : P.key_columns.size();
+    unsigned long long key_widths = 0;
     const long long want_words = P.mode == MODE_SCALAR  ? kMaxAcc + 1
                                  : P.mode == MODE_SMALL ? kSmallPartWords
                                                         : record_words(nkeyc, fs.nacc);
     if (parts.empty()) throw Error(TQP_ERR_ARG, where + ": no partials to merge");
+    if (alt && P.mode == MODE_SMALL && parts[0].ptr && parts[0].words >= kHdrWords) {
+      // shards whose small-group run overflowed produced hash-group partials
+      unsigned long long h[kHdrWords];
+      TQP_CUDA(cudaMemcpyAsync(h, parts[0].ptr, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (h[0] == kPartMagic && h[1] == static_cast<unsigned long long>(MODE_HASH)) return alt->finish(c, slots, parts, where);
+    }
     long long total = 0;
     std::vector<long long> nrec(parts.size());
     for (size_t i = 0; i < parts.size(); ++i) {
@@ -3163,9 +3602,10 @@ struct Runner {
       c.sync();
       if (h[0] != kPartMagic || h[1] != static_cast<unsigned long long>(P.mode) ||
           h[3] != static_cast<unsigned long long>(want_words) || h[4] != static_cast<unsigned long long>(fs.nacc) ||
-          h[5] != static_cast<unsigned long long>(fs.nouts) || h[6] != P.key_columns.size()) {
+          h[5] != static_cast<unsigned long long>(fs.nouts) || h[6] != hdr_keys || (i > 0 && h[7] != key_widths)) {
         throw Error(TQP_ERR_ARG, where + ": partial " + std::to_string(i) + " was not produced by this plan");
       }
+      key_widths = h[7];
       nrec[i] = static_cast<long long>(h[2]);
       if (kHdrWords + nrec[i] * want_words > parts[i].words)
         throw Error(TQP_ERR_ARG, where + ": partial " + std::to_string(i) + " is truncated");
@@ -3221,6 +3661,7 @@ struct Runner {
       gs.acc_stride = 2LL * fs.nacc;
       gs.nkeyc = nkeyc;
       for (int i = 0; i < nkeyc; ++i) gs.key_cols[i] = static_cast<const long long*>(hkeys->ptr) + i * cap;
+      for (int i = 0; i < nkeyc; ++i) gs.key_w[i] = static_cast<int>((key_widths >> (8 * i)) & 0xff);
       ok = emit_groups(c, gs, cap, static_cast<const long long*>(hbk->ptr), err, outs, nrows);
     }
     long long herr[4] = {0, 0, 0, 0};
@@ -3285,7 +3726,10 @@ std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
     }
     if (!ok) continue;
     std::ostringstream ex;
-    const char* mode = P.mode == MODE_SCALAR ? "scalar" : P.mode == MODE_SMALL ? "small-group" : "build-group";
+    const char* mode = P.mode == MODE_SCALAR  ? "scalar"
+                       : P.mode == MODE_SMALL ? "small-group"
+                       : P.mode == MODE_HASH  ? "hash-group"
+                                              : "build-group";
     ex << "fact=" << P.fact_table << " terms=" << P.terms.size() << " probes=" << P.probes.size()
        << " builds=" << P.builds.size() << " accumulators=" << P.accs.size() << " mode=" << mode
        << (P.topk ? " topk=" + std::to_string(P.k) : std::string());
@@ -3295,6 +3739,12 @@ std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
     u.name = std::string("fused_") + (P.probes.empty() ? "scan_" : "probe_") + mode + (P.topk ? "_topk" : "");
     u.explain = ex.str();
     auto R = std::make_shared<Runner>(Runner{P});
+    if (P.mode == MODE_SMALL && P.hash_alt) {
+      PipeDesc H = P;
+      H.mode = MODE_HASH;
+      H.key_columns.clear();
+      R->alt = std::make_shared<const Runner>(Runner{H});
+    }
     u.run = [R](Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& t, UnitPending* pend) {
       return (*R)(c, slots, t, pend);
     };

@@ -29,9 +29,14 @@ namespace fz {
 // ---- build kernel ------------------------------------------------------------
 // key range of a build side: 128-bit loads, warp then block reduction, one
 // atomic pair per block (a per-warp atomic on one address serialises at L2)
+// DAY: also out[2] |= 1 if a value is not a whole number of days in ns (a
+// Date column keyed by day digits, MODE_HASH)
+template <bool DAY = false>
 __global__ void __launch_bounds__(256) k_minmax(const long long* __restrict__ k, long long n, long long* out) {
   __shared__ long long s_mn[8], s_mx[8];
   long long mn = 0x7fffffffffffffffLL, mx = static_cast<long long>(0x8000000000000000ULL);
+  bool odd = false;
+  constexpr long long kDay = 86400000000000LL;
   const bool aligned = (reinterpret_cast<uintptr_t>(k) & 15) == 0;
   const long long npair = aligned ? n / 2 : 0;
   const longlong2* k2 = reinterpret_cast<const longlong2*>(k);
@@ -39,12 +44,15 @@ __global__ void __launch_bounds__(256) k_minmax(const long long* __restrict__ k,
     const longlong2 v = __ldg(k2 + i);
     mn = min(mn, min(v.x, v.y));
     mx = max(mx, max(v.x, v.y));
+    if (DAY) odd = odd || (v.x % kDay) != 0 || (v.y % kDay) != 0;
   }
   for (long long i = 2 * npair + gtid(); i < n; i += gstride()) {
     const long long v = __ldg(k + i);
     mn = min(mn, v);
     mx = max(mx, v);
+    if (DAY) odd = odd || (v % kDay) != 0;
   }
+  if (DAY && __any_sync(0xffffffffu, odd) && (threadIdx.x & 31) == 0) atomicOr(reinterpret_cast<unsigned long long*>(out + 2), 1ULL);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -103,14 +111,18 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
 #pragma unroll
       for (int j = 0; j < kBuildRows; ++j)
         if (pass[j]) pass[j] = eval_str(s.str[t], base0 + j * blockDim.x + threadIdx.x);
+    unsigned wgt[kBuildRows];  // row weight: product of the child probes' multiplicities
+#pragma unroll
+    for (int j = 0; j < kBuildRows; ++j) wgt[j] = 1u;
 #pragma unroll
     for (int p = 0; p < kMaxProbes; ++p) {
       if (p < s.nprobes) {
 #pragma unroll
         for (int j = 0; j < kBuildRows; ++j) {
           long long rid;
-          unsigned fl, g;
-          if (pass[j]) pass[j] = probe_lookup(s.probes[p], pk[j][p], rid, fl, g);
+          unsigned fl, g, m = 1u;
+          if (pass[j]) pass[j] = probe_lookup(s.probes[p], pk[j][p], rid, fl, g, &m);
+          wgt[j] *= m;
         }
       }
     }
@@ -125,20 +137,45 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
         unsigned flags = 0;
         for (int f = 0; f < s.nflags; ++f)
           if (eval_str(s.flags[f], r)) flags |= 1u << f;
-        idx = key[j] - s.kmin;
-        if (idx < 0 || idx >= s.range) {
-          atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
-          idx = -1;
+        const unsigned long long entry = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags) << 57);
+        if (s.hkeys) {
+          // open addressing: the first row with a key claims its slot
+          bool seen = false;
+          const long long sl = build_hash_insert(s, key[j], seen);
+          if (sl < 0) {
+            set_fallback(s.err, FR_HASH_FULL);
+          } else {
+            if (!seen) {
+              if (s.assign_groups)  // the group is the slot: zero its record
+                for (int w = 0; w < s.zrec_words; ++w) s.zrec[sl * s.zrec_words + w] = 0ULL;
+              s.table[sl] = entry;
+            } else if (!s.mult) {
+              dup = 1u;  // a repeated key: the unit reruns weighted
+            }
+            if (s.mult) atomicAdd(s.mult + sl, wgt[j]);
+          }
+          idx = -1;  // no presence bits
         } else {
-          if (s.assign_groups)  // the group is the key slot: zero its record
-            for (int w = 0; w < s.zrec_words; ++w) s.zrec[idx * s.zrec_words + w] = 0ULL;
-          s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags) << 57);
+          idx = key[j] - s.kmin;
+          if (idx < 0 || idx >= s.range) {
+            atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);
+            idx = -1;
+          } else {
+            if (s.assign_groups)  // the group is the key slot: zero its record
+              for (int w = 0; w < s.zrec_words; ++w) s.zrec[idx * s.zrec_words + w] = 0ULL;
+            s.table[idx] = entry;
+            if (s.mult) atomicAdd(s.mult + idx, wgt[j]);
+          }
         }
       }
-      presence_insert(s.bitmap, idx, old[j], set[j], dup);
+      if (!s.hkeys) presence_insert(s.bitmap, idx, old[j], set[j], dup);
     }
+    if (!s.mult) {
 #pragma unroll
-    for (int j = 0; j < kBuildRows; ++j) dup |= old[j] & set[j];
+      for (int j = 0; j < kBuildRows; ++j) dup |= old[j] & set[j];
+    } else {
+      dup = 0u;  // weighted: repeated keys are summed, not flagged
+    }
   }
   build_dup_check(dup, s.err);
 }
@@ -212,6 +249,7 @@ struct TileDesc {
   int a_src[kMaxAcc][kFixedFactors];
   int a_mode[kMaxAcc][kFixedFactors];  // FM_* (uniform fast forms)
   int a_base[kMaxAcc];                 // earlier accumulator whose product is a prefix, or -1
+  const void* a_ptr[kMaxAcc][kFixedFactors];  // MODE_HASH: probe-root operand columns (a_src >= 0)
   double a_fa[kMaxAcc][kFixedFactors], a_fb[kMaxAcc][kFixedFactors];
   unsigned k_off[kMaxKeys];
   unsigned p_off[kMaxProbes];
@@ -238,6 +276,7 @@ __device__ void load_desc(const TileSpec& t, TileDesc& d) {
     for (int i = 0; i < kFixedFactors; ++i) {
       const Factor& f = ac.f[i];
       d.a_src[a][i] = f.x.src;
+      d.a_ptr[a][i] = f.x.ptr;
       d.a_off[a][i] = (f.x.src < 0 && f.x.col >= 0) ? static_cast<unsigned>(t.col_off[f.x.col]) : kNoCol;
       d.a_fa[a][i] = ac.is_int ? 0.0 : f.fa;
       d.a_fb[a][i] = ac.is_int ? 0.0 : f.fb;
@@ -363,7 +402,23 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
           const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.p_off[p]);
 #pragma unroll
           for (int k = 0; k < R; ++k)
-            if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p]);
+            if (pass[k]) pass[k] = probe_lookup(pr, static_cast<long long>(col[k * CT + ct]), rc[k].rid[p], rc[k].flags[p], rc[k].gid[p], &rc[k].mult[p]);
+        }
+      }
+      // weighted run (repeated build keys): the row counts prod(mult) times;
+      // a probe whose root row is read must have matched exactly one row
+      unsigned wt[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        wt[k] = 1u;
+        if (s.weighted && pass[k]) {
+#pragma unroll
+          for (int p = 0; p < kMaxProbes; ++p) {
+            if (p < d.nprobes) {
+              wt[k] *= rc[k].mult[p];
+              if (((s.root_mask >> p) & 1u) && rc[k].mult[p] != 1u) set_fallback(s.err, FR_DUP_KEY);
+            }
+          }
         }
       }
       bool any = MODE == MODE_SMALL;  // small-group runs warp-collective slot claims: no per-thread skip
@@ -410,12 +465,54 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
           }
 #pragma unroll
           for (int k = 0; k < R; ++k)
-            if (pass[k]) s_stage_val[(slot[k] * (NA_ + 1) + NA_) * CT + ct] += 1;
+            if (pass[k]) s_stage_val[(slot[k] * (NA_ + 1) + NA_) * CT + ct] += wt[k];
         } else {
 #pragma unroll
-          for (int k = 0; k < R; ++k) gcnt_local[0] += pass[k] ? 1u : 0u;
+          for (int k = 0; k < R; ++k) gcnt_local[0] += pass[k] ? wt[k] : 0u;
         }
         unsigned g[R];
+        if constexpr (MODE == MODE_HASH) {
+          // group code per row (mixed radix over the key digits), then its
+          // slot: the CTA's shared-memory records (hpriv) or the global table
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            g[k] = 0u;
+            if (!pass[k]) continue;
+            const long long row = row0 + k * CT + ct;
+            unsigned long long code = 0;
+            bool bad = false;
+#pragma unroll
+            for (int q = 0; q < kMaxKeys; ++q) {
+              if (q < s.nhkeys) {
+                const GKey& K = s.hkeys[q];
+                long long rid = rc[k].rid[0];  // static select keeps rc in registers
+#pragma unroll
+                for (int p = 1; p < kMaxProbes; ++p) rid = K.x.src == p ? rc[k].rid[p] : rid;
+                const long long krow = K.x.src < 0 ? row : rid;
+                unsigned long long raw = 0;
+                if (!K.width)
+                  raw = K.x.src < 0 ? reinterpret_cast<const unsigned long long*>(stage + t.col_off[K.x.col])[k * CT + ct]
+                                    : ld_row(K.x, rid);
+                const unsigned long long dg = gkey_digit(K, raw, krow);
+                bad = bad || dg >= K.range;
+                code += dg * K.stride;
+              }
+            }
+            long long slot = -1;
+            if (bad) {
+              set_fallback(s.err, FR_KEY_RANGE);
+            } else if (s.hpriv) {
+              slot = static_cast<long long>(code);
+              atomicAdd(s_stage_val + slot * (1 + kLimbWords * NA_), static_cast<unsigned long long>(wt[k]));
+            } else {
+              slot = hash_claim(s, code);
+              if (slot < 0) set_fallback(s.err, FR_HASH_FULL);
+              else atomicAdd(s.gcnt + slot * s.gstride, static_cast<unsigned long long>(wt[k]) + kCntAdd);
+            }
+            if (slot < 0) pass[k] = false;
+            g[k] = static_cast<unsigned>(slot < 0 ? 0 : slot);
+          }
+        }
         if constexpr (MODE == MODE_BUILDGRP) {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -424,7 +521,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             for (int p = 1; p < kMaxProbes; ++p) gg = s.group_probe == p ? rc[k].gid[p] : gg;
             g[k] = pass[k] ? gg : 0u;
             if (pass[k]) {
-              atomicAdd(s.gcnt + static_cast<long long>(g[k]) * s.gstride, 1ULL);
+              atomicAdd(s.gcnt + static_cast<long long>(g[k]) * s.gstride, static_cast<unsigned long long>(wt[k]));
               atomicOr(s.touched + (g[k] >> 5), 1u << (g[k] & 31));
             }
           }
@@ -434,16 +531,29 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
         // start = 1.0 (1 * f0 == f0 exactly) or an earlier accumulator's
         // product (prefix sharing); a missing operand reads as 0 and a
         // padding factor is 1 + 0 * 0, so every slot runs the same code
-        double dvals[NAX][R];
+        double dvals[NAX > 0 ? NAX : 1][R];
 #pragma unroll
         for (int a = 0; a < NAX; ++a) {
           const bool is_int = d.a_int[a];
           unsigned long long v[R];
           if (is_int) {
             const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.a_off[a][0]);
+            const int isrc = MODE == MODE_HASH ? d.a_src[a][0] : -1;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-              v[k] = pass[k] ? col[k * CT + ct] : 0ULL;
+              if (MODE == MODE_HASH && isrc >= 0) {  // a probe's root column at the matched row
+                long long rid = rc[k].rid[0];
+#pragma unroll
+                for (int p = 1; p < kMaxProbes; ++p) rid = isrc == p ? rc[k].rid[p] : rid;
+                v[k] = pass[k] ? static_cast<unsigned long long>(ld_i64(d.a_ptr[a][0], rid)) : 0ULL;
+              } else {
+                v[k] = pass[k] ? col[k * CT + ct] : 0ULL;
+              }
+              if (s.weighted && wt[k] != 1u) {  // v * weight, exactly or the exact path
+                const __int128 pw = static_cast<__int128>(static_cast<long long>(v[k])) * wt[k];
+                if (pw != static_cast<__int128>(static_cast<long long>(pw))) set_fallback(s.err, FR_INT_RANGE);
+                v[k] = static_cast<unsigned long long>(static_cast<long long>(pw));
+              }
               long long iv = static_cast<long long>(v[k]);
               iv = iv < 0 ? -iv : iv;
               absmax = iv > absmax ? iv : absmax;
@@ -464,9 +574,16 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
               const bool has = off != kNoCol;
               const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + (has ? off : 0u));
               const double fa = d.a_fa[a][i], fb = d.a_fb[a][i];
+              const int fsrc = MODE == MODE_HASH ? d.a_src[a][i] : -1;
 #pragma unroll
               for (int k = 0; k < R; ++k) {
-                const double x = has ? __longlong_as_double(static_cast<long long>(col[k * CT + ct])) : 0.0;
+                double x = has ? __longlong_as_double(static_cast<long long>(col[k * CT + ct])) : 0.0;
+                if (MODE == MODE_HASH && fsrc >= 0) {  // a probe's root column at the matched row
+                  long long rid = rc[k].rid[0];
+#pragma unroll
+                  for (int p = 1; p < kMaxProbes; ++p) rid = fsrc == p ? rc[k].rid[p] : rid;
+                  x = pass[k] ? ld_f64(d.a_ptr[a][i], rid) : 0.0;
+                }
                 dv[k] = __dmul_rn(dv[k], __dadd_rn(fa, __dmul_rn(fb, x)));
               }
             }
@@ -486,6 +603,13 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             }
 #pragma unroll
             for (int k = 0; k < R; ++k) v[k] = pass[k] ? static_cast<unsigned long long>(__double_as_longlong(dv[k])) : 0ULL;
+          }
+          if ((MODE == MODE_SCALAR || MODE == MODE_SMALL) && !is_int && s.weighted) {
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+              if (wt[k] != 1u)
+                v[k] = static_cast<unsigned long long>(__double_as_longlong(
+                    __dmul_rn(__longlong_as_double(static_cast<long long>(v[k])), static_cast<double>(wt[k]))));
           }
           if constexpr (MODE == MODE_SCALAR) {
 #pragma unroll
@@ -508,13 +632,26 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 qv = static_cast<__int128>(static_cast<long long>(v[k]));
               } else {
                 const double dv = __longlong_as_double(static_cast<long long>(v[k]));
-                fabsmax = fmax(fabsmax, fabs(dv));
                 if (!f64_to_q64(dv, qv)) {
-                  set_fallback(s.err, FR_Q64_CONVERT);
                   qv = 0;
+                  if (MODE == MODE_HASH && s.hflags >= 0 && (isnan(dv) || isinf(dv))) {
+                    const unsigned long long bit = isnan(dv) ? 1ULL : dv > 0 ? 2ULL : 4ULL;
+                    atomicOr(s.gcnt + static_cast<long long>(g[k]) * s.gstride + s.hflags, bit << (3 * a));
+                  } else {
+                    set_fallback(s.err, FR_Q64_CONVERT);
+                  }
+                } else {
+                  fabsmax = fmax(fabsmax, fabs(dv));
+                }
+                if (wt[k] != 1u) {  // exact: the weight multiplies the fixed-point value
+                  qv *= static_cast<__int128>(wt[k]);
+                  fabsmax = fmax(fabsmax, fabs(dv) * static_cast<double>(wt[k]));
                 }
               }
-              atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
+              if (MODE == MODE_HASH && s.hpriv)
+                atomic_add_limbs(s_stage_val + static_cast<long long>(g[k]) * (1 + kLimbWords * NA_) + 1 + a * kLimbWords, qv);
+              else
+                atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
             }
           }
         }
@@ -524,8 +661,12 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     }
     // int64 sums are exact only while |v| * rows < 2^63 (the reference
     // errors on the first overflowing prefix): otherwise the exact path
-    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) set_fallback(s.err, FR_INT_RANGE);
-    if constexpr (MODE == MODE_BUILDGRP) q64_range_check(fabsmax, s.n, s.err);
+    if (MODE == MODE_HASH && s.absmax_out) {
+      if (absmax) atomicMax(s.absmax_out, absmax);
+    } else if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
+      set_fallback(s.err, FR_INT_RANGE);
+    }
+    if constexpr (MODE == MODE_BUILDGRP || MODE == MODE_HASH) q64_range_check(fabsmax, s.n, s.err);
     if constexpr (MODE == MODE_SMALL) {
       for (int gg = 0; gg < kGroups; ++gg) {
         for (int a = 0; a <= s.nacc; ++a) {
@@ -570,6 +711,24 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       unsigned long long c = 0;
       for (int w = 0; w < CW; ++w) c += s_wred[0][kMaxAcc][w];
       out[kMaxAcc] = c;
+    }
+  } else if constexpr (MODE == MODE_HASH) {
+    if (s.hpriv) {
+      // flush the CTA's records into the (direct) global table: one add per
+      // word per CTA, limbs re-split so every added limb is < 2^42; the
+      // packed count carries the adds for the reader's limb bound
+      constexpr int RW = 1 + kLimbWords * NA_;
+      const long long ncode = static_cast<long long>(s.hmask) + 1;
+      for (long long code = threadIdx.x; code < ncode; code += blockDim.x) {
+        const unsigned long long* r = s_stage_val + code * RW;
+        const unsigned long long c = r[0];
+        if (!c) continue;
+        if (c >= static_cast<unsigned long long>(kLimbMaxRows)) set_fallback(s.err, FR_LIMB_ROWS);
+        s.htag[code] = static_cast<unsigned long long>(code) + 1;
+        atomicAdd(s.gcnt + code * s.gstride, c + kCntAdd);
+#pragma unroll
+        for (int a = 0; a < NA_; ++a) atomic_add_limbs(s.gacc + code * s.gstride + a * kLimbWords, limbs_to_i128(r + 1 + a * kLimbWords));
+      }
     }
   } else if constexpr (MODE == MODE_SMALL) {
     if (s_overflow && threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(s.err), 1ULL);

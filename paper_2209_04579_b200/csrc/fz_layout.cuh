@@ -28,7 +28,7 @@ constexpr int kWarps = kThreads / 32;
 enum OperandType : int { OT_I64 = 0, OT_F64 = 1, OT_U8 = 2 };
 enum TermKind : int { TK_INT = 0, TK_F64 = 1, TK_TRUE = 2, TK_FALSE = 3 };
 enum FactorKind : int { FK_X = 0, FK_K_MINUS_X, FK_K_PLUS_X, FK_X_MINUS_K, FK_X_PLUS_K, FK_X_TIMES_K, FK_CONST };
-enum Mode : int { MODE_SCALAR = 0, MODE_SMALL = 1, MODE_BUILDGRP = 2 };
+enum Mode : int { MODE_SCALAR = 0, MODE_SMALL = 1, MODE_BUILDGRP = 2, MODE_HASH = 3 };
 
 // err[3]: why a fused unit handed its steps to the exact per-instruction path
 // (err[0] != 0). Diagnostic only (TQP_DEBUG_FALLBACK prints it); the exact
@@ -44,6 +44,7 @@ enum FallbackReason : long long {
   FR_GROUP_VALUE = 18,     // a group output (AVG / epilogue) left the exact form
   FR_INT_RANGE = 19,       // int64 sum may overflow (|v| x rows >= 2^63)
   FR_HASH_FULL = 22,       // hash group / join table probe sequence exhausted
+  FR_KEY_RANGE = 23,       // a group key digit outside its range (stale key range)
 };
 
 // A per-row operand: fact column (src = -1) or a column of the build-side
@@ -99,13 +100,29 @@ struct Acc {
 // dense direct-address build table: entry 0 = empty, else
 //   bits 0-31 rowid+1 | bits 57-63 flags; the group of a group-assigning
 //   build is the key slot (key - kmin), valid where the presence bit is set
+// A build whose key range is too wide for direct addressing is an
+// open-addressing table instead (hkeys != nullptr): slot = hash(key) with
+// linear probing at load <= 1/2, hkeys[slot] the key (kmin - 1 marks an
+// empty slot: no key of the column is below kmin), table[slot] the entry.
+// A build whose keys repeat (a 1:N join) is re-run with mult != nullptr:
+// mult[slot] = the summed weight of the build rows with that key (a row's
+// weight is the product of its own child probes' multiplicities); the fact
+// scan then counts a row mult times and adds its values times mult.
 struct Probe {
   Operand key;
   long long kmin = 0;
   long long range = 0;
   const unsigned long long* table = nullptr;
   const unsigned* bitmap = nullptr;  // presence bits (L2-resident filter)
+  const long long* hkeys = nullptr;  // open addressing: keys per slot
+  unsigned long long hmask = 0;
+  const unsigned* mult = nullptr;    // weighted (1:N) builds: multiplicity per slot
 };
+
+__device__ __forceinline__ unsigned long long build_hslot(long long key, unsigned long long mask) {
+  unsigned long long h = static_cast<unsigned long long>(key) * 0x9E3779B97F4A7C15ULL;
+  return (h ^ (h >> 31)) & mask;
+}
 
 // Branch-free predicate term for the fact scan: all compares on one column
 // are merged into lo <= x <= hi (int64: one unsigned compare; fp64: two
@@ -133,6 +150,24 @@ __device__ __forceinline__ bool eval_rterm(const RTerm& t, unsigned long long x)
   }
 }
 
+// MODE_HASH group key: a fact column or a probe's root column. Every key
+// maps to a digit (v - kmin) / step in [0, range) (int64 / date: step 86400e9
+// for day-aligned dates; STR8 rows of width <= 7: the bytes big-endian, so
+// digit order is the reference's byte order of zero-padded rows), and the
+// group code is the mixed-radix number of the digits, first key most
+// significant: ascending codes are the reference's ascending key order.
+struct GKey {
+  Operand x;
+  int width = 0;  // 0: int64 / date; 1..7: STR8 bytes per row
+  long long kmin = 0;
+  long long step = 1;
+  unsigned long long range = 1;
+  unsigned long long stride = 1;
+};
+constexpr unsigned long long kHashBusy = ~0ULL;       // tag of a slot being claimed
+constexpr unsigned long long kCntAdd = 1ULL << 40;    // packed count: rows | adds << 40
+constexpr unsigned long long kCntMask = kCntAdd - 1;
+
 struct ProbeSpec {
   long long n = 0;
   int nterms = 0;
@@ -153,6 +188,26 @@ struct ProbeSpec {
   int gstride;
   unsigned* touched;         // BUILDGRP: bit per group with a row (the top-k walk's index)
   long long* err;            // [0] != 0: data violates the fused preconditions
+  // MODE_HASH: group table of hcap slots; tag = code + 1 (0 empty,
+  // kHashBusy while the claiming thread zeroes the slot's record); hdirect:
+  // slot = code (the code range fits), else multiplicative hash + linear
+  // probing; hpriv: the whole code range fits one CTA's shared memory (the
+  // CTA accumulates there and flushes once)
+  int nhkeys;
+  GKey hkeys[kMaxKeys];
+  unsigned long long* htag;
+  unsigned long long hmask;
+  int hdirect, hpriv;
+  // weighted run (some build keys repeat): a row counts prod(mult) times;
+  // probes whose root row is read (operands, keys, flags, groups) must match
+  // exactly one build row (root_mask bit p), else the exact path
+  int weighted;
+  unsigned root_mask;
+  // MODE_HASH: max |int64 value| over the scan (atomicMax); each group's
+  // int sums are checked against it at output (max x rows < 2^63: no prefix
+  // of the reference's sequential sum can overflow), not the whole scan's rows
+  long long* absmax_out;
+  int hflags;  // >= 0: record word of per-accumulator NaN / +Inf / -Inf bits (special run)
 };
 
 struct BuildSpec {
@@ -170,6 +225,9 @@ struct BuildSpec {
   long long range = 0;
   unsigned long long* table = nullptr;
   unsigned* bitmap = nullptr;
+  long long* hkeys = nullptr;  // open-addressing build (see Probe)
+  unsigned long long hmask = 0;
+  unsigned* mult = nullptr;    // weighted build: summed row weights per slot
   int assign_groups = 0;
   // group records zeroed by the row inserted into the slot (no memset over
   // the whole key range): zrec_words words per slot (whole sectors)
@@ -315,19 +373,51 @@ struct RowCtx {
   long long rid[kMaxProbes];
   unsigned flags[kMaxProbes];
   unsigned gid[kMaxProbes];
+  unsigned mult[kMaxProbes];
 };
 
 __device__ __forceinline__ bool probe_lookup(const Probe& p, long long key, long long& rid, unsigned& flags,
-                                             unsigned& gid) {
-  long long idx = key - p.kmin;
-  if (idx < 0 || idx >= p.range) return false;
-  if (p.bitmap && !((__ldg(p.bitmap + (idx >> 5)) >> (idx & 31)) & 1u)) return false;
+                                             unsigned& gid, unsigned* mult = nullptr) {
+  long long idx;
+  if (p.hkeys) {
+    unsigned long long sl = build_hslot(key, p.hmask);
+    const long long empty = p.kmin - 1;
+    for (;;) {
+      const long long k = __ldg(p.hkeys + sl);
+      if (k == key) break;
+      if (k == empty) return false;
+      sl = (sl + 1) & p.hmask;
+    }
+    idx = static_cast<long long>(sl);
+  } else {
+    idx = key - p.kmin;
+    if (idx < 0 || idx >= p.range) return false;
+    if (p.bitmap && !((__ldg(p.bitmap + (idx >> 5)) >> (idx & 31)) & 1u)) return false;
+  }
   unsigned long long e = __ldg(p.table + idx);
   if (!e) return false;
   rid = static_cast<long long>(e & 0xffffffffULL) - 1;
   gid = static_cast<unsigned>(idx);  // a group-assigning build's group is its key slot
   flags = static_cast<unsigned>(e >> 57);
+  if (mult) *mult = p.mult ? __ldg(p.mult + idx) : 1u;
   return true;
+}
+
+// open-addressing insert of `key` (build side): the slot, and whether the key
+// was already there (a repeated build key)
+__device__ __forceinline__ long long build_hash_insert(const BuildSpec& s, long long key, bool& seen) {
+  unsigned long long sl = build_hslot(key, s.hmask);
+  const unsigned long long empty = static_cast<unsigned long long>(s.kmin - 1);
+  for (unsigned long long i = 0; i <= s.hmask; ++i) {
+    const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(s.hkeys) + sl, empty,
+                                             static_cast<unsigned long long>(key));
+    if (old == empty || old == static_cast<unsigned long long>(key)) {
+      seen = old != empty;
+      return static_cast<long long>(sl);
+    }
+    sl = (sl + 1) & s.hmask;
+  }
+  return -1;
 }
 
 __device__ __forceinline__ unsigned long long operand_value(const Operand& o, unsigned long long fact_raw,
@@ -426,6 +516,56 @@ __device__ __forceinline__ __int128 limbs_to_i128(const unsigned long long* w) {
   return static_cast<__int128>(u);
 }
 
+// ---- MODE_HASH group table --------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// digit of key K for one row: `raw` is the loaded int64 (width 0); STR8 keys
+// read their `width` bytes at `row` (big-endian, so digit order = byte order)
+__device__ __forceinline__ unsigned long long gkey_digit(const GKey& K, unsigned long long raw, long long row) {
+  if (K.width) {
+    const uint8_t* p = static_cast<const uint8_t*>(K.x.ptr) + row * K.width;
+    unsigned long long d = 0;
+    for (int j = 0; j < K.width; ++j) d = (d << 8) | __ldg(p + j);
+    return d;
+  }
+  unsigned long long d = raw - static_cast<unsigned long long>(K.kmin);
+  if (K.step != 1) d /= static_cast<unsigned long long>(K.step);
+  return d;
+}
+
+// slot of group `code` in the global table, claimed (record zeroed, then the
+// tag published) by the first row that meets it; -1: table full
+__device__ __forceinline__ long long hash_claim(const ProbeSpec& s, unsigned long long code) {
+  const unsigned long long want = code + 1;
+  unsigned long long slot = code;
+  if (!s.hdirect) {
+    unsigned long long h = code * 0x9E3779B97F4A7C15ULL;
+    slot = (h ^ (h >> 29)) & s.hmask;
+  }
+  for (unsigned long long probe = 0; probe <= s.hmask; ++probe) {
+    unsigned long long* tp = s.htag + slot;
+    unsigned long long t = ld_acquire_u64(tp);
+    if (t == 0ULL) {
+      t = atomicCAS(tp, 0ULL, kHashBusy);
+      if (t == 0ULL) {
+        unsigned long long* rec = s.gcnt + static_cast<long long>(slot) * s.gstride;
+        for (int w = 0; w < s.gstride; ++w) rec[w] = 0ULL;
+        __threadfence();
+        atomicExch(tp, want);
+        return static_cast<long long>(slot);
+      }
+    }
+    while (t == kHashBusy) t = ld_acquire_u64(tp);
+    if (t == want) return static_cast<long long>(slot);
+    slot = (slot + 1) & s.hmask;
+  }
+  return -1;
+}
+
 // ---- TMA-staged, warp-specialised tile pipeline for the fact scan -----------
 // A persistent CTA per SM streams tiles of kTileRows rows. Warp 0 is the
 // producer: one lane issues, for every distinct fact column, a 1-D bulk async
@@ -447,7 +587,7 @@ template <int MODE>
 struct TileShape {
   // small-group keeps per-thread shared-memory accumulators (groups x
   // accumulators x threads), so its tiles are half as tall
-  static constexpr int ROWS = MODE == MODE_SMALL ? 1024 : kTileRows;
+  static constexpr int ROWS = MODE == MODE_SMALL ? 1024 : kTileRows;  // MODE_HASH: as SCALAR
   static constexpr int CW = MODE == MODE_SMALL ? 8 : 16;
   static constexpr int CT = CW * 32;
   static constexpr int THREADS = CT + 32;
