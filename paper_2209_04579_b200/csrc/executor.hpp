@@ -74,11 +74,25 @@ struct KeyRange {
   int day = -1;  // Date keys: 1 every value is a whole day in ns, 0 not, -1 not computed
 };
 
+// Dictionary of an int64 key column (MODE_HASH keys whose value range is too
+// wide to pack): the distinct values ascending, and an open-addressing map
+// value -> rank; cached with the (immutable) column like its KeyRange.
+struct KeyDict {
+  std::mutex mu;
+  bool ready = false;
+  long long d = 0;                      // distinct values
+  Tensor vals;                          // (d, 1) int64, ascending
+  std::shared_ptr<DevBuf> hkeys, hranks;
+  unsigned long long mask = 0;
+  long long empty = 0;                  // marker of an empty map slot (column min - 1)
+};
+
 struct Column {
   std::string name;
   int type;  // logical
   Tensor t;
   std::shared_ptr<KeyRange> range = std::make_shared<KeyRange>();
+  std::shared_ptr<KeyDict> dict = std::make_shared<KeyDict>();
 };
 
 struct Table {

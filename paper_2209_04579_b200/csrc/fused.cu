@@ -556,7 +556,9 @@ bool term_of(Analysis& A, int e, int scan, const Plan& plan, TermDesc& t) {
     } else {
       return false;
     }
+    // Bool-column compares are not fused terms (either operand order)
     if (A.ex[x.b].k == SExpr::CONST && A.ex[x.b].cinstr->const_dtype == TQP_BOOL) return false;
+    if (A.ex[x.a].k == SExpr::CONST && A.ex[x.a].cinstr->const_dtype == TQP_BOOL) return false;
     t.kind = 0;
     t.f64 = f;
     t.ik = ik;
@@ -856,6 +858,12 @@ struct Planner {
         if (!operand(k, o, &lt) || (lt != TQP_LT_INT64 && lt != TQP_LT_DATE && lt != TQP_LT_UTF8)) {
           hashable = false;
           break;
+        }
+        // a key equal to a probe's build key is the fact probe column itself
+        // (no read of the matched root row, so it survives repeated build keys)
+        if (o.probe >= 0 && iequals(o.column, P.builds[P.probes[o.probe].build].key_column)) {
+          o.column = P.probes[o.probe].fact_column;
+          o.probe = -1;
         }
         P.hkeys.push_back(o);
         P.hkey_lt.push_back(lt);
@@ -1339,8 +1347,10 @@ struct GroupSpec {
   unsigned long long krange[kMaxKeys] = {1, 1, 1, 1}, kstride[kMaxKeys] = {1, 1, 1, 1};
   int key_w[kMaxKeys] = {0, 0, 0, 0};  // output width of key i: 0 int64, else STR8 bytes
   int cnt_packed = 0;
+  const long long* dvals[kMaxKeys] = {nullptr, nullptr, nullptr, nullptr};  // dictionary keys: value by rank
   const long long* absmax = nullptr;  // MODE_HASH: int sums exact iff absmax x rows < 2^63
   int flag_word = -1;                 // MODE_HASH special run: record word of the NaN/Inf bits
+  int qfrac = 64;                     // fixed-point fraction bits of the sums
 };
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g);
@@ -1349,6 +1359,7 @@ __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned 
 __device__ __forceinline__ long long group_key_value(const GroupSpec& s, int i, unsigned g) {
   if (s.codes) {
     const unsigned long long dg = ((s.codes[g] - 1ULL) / s.kstride[i]) % s.krange[i];
+    if (s.dvals[i]) return s.dvals[i][dg];
     return s.key_w[i] ? static_cast<long long>(dg) : s.kmin[i] + static_cast<long long>(dg * static_cast<unsigned long long>(s.kstep[i]));
   }
   return s.key_cols[i][group_src_row(s, g)];
@@ -1406,7 +1417,8 @@ __device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsig
     is_f64 = true;
     return fits && limbs_ok;
   }
-  double sum = q64_to_f64(lo, hi);
+  double sum = s.qfrac == 64 ? q64_to_f64(lo, hi)
+                             : ldexp(static_cast<double>(static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo)), -s.qfrac);
   if (s.flag_word >= 0) {  // NaN / +Inf / -Inf among the group's values (IEEE sum)
     const unsigned f = static_cast<unsigned>(s.gcnt[g * s.cnt_stride + s.flag_word] >> (3 * o.acc)) & 7u;
     if ((f & 1u) || (f & 6u) == 6u) sum = __longlong_as_double(0x7ff8000000000000LL);
@@ -2145,7 +2157,7 @@ const void* tile_kernel(int mode, int nacc) {
   TQP_TK(MODE_SCALAR, 0) TQP_TK(MODE_SCALAR, 1) TQP_TK(MODE_SCALAR, 2) TQP_TK(MODE_SCALAR, 3) TQP_TK(MODE_SCALAR, 4)
   TQP_TK(MODE_SMALL, 1) TQP_TK(MODE_SMALL, 2) TQP_TK(MODE_SMALL, 3) TQP_TK(MODE_SMALL, 4) TQP_TK(MODE_SMALL, 5)
   TQP_TK(MODE_SMALL, 6)
-  TQP_TK(MODE_BUILDGRP, 1) TQP_TK(MODE_BUILDGRP, 2) TQP_TK(MODE_BUILDGRP, 3) TQP_TK(MODE_BUILDGRP, 4)
+  TQP_TK(MODE_BUILDGRP, 0) TQP_TK(MODE_BUILDGRP, 1) TQP_TK(MODE_BUILDGRP, 2) TQP_TK(MODE_BUILDGRP, 3) TQP_TK(MODE_BUILDGRP, 4)
   TQP_TK(MODE_HASH, 0) TQP_TK(MODE_HASH, 1) TQP_TK(MODE_HASH, 2) TQP_TK(MODE_HASH, 3) TQP_TK(MODE_HASH, 4)
 #undef TQP_TK
   return nullptr;
@@ -2607,6 +2619,80 @@ void ensure_key_info(Ctx& c, const std::vector<std::pair<const Column*, long lon
   }
 }
 
+__global__ void k_fill_u64(unsigned long long* __restrict__ p, long long n, unsigned long long v) {
+  for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
+}
+void fill_u64(Ctx& c, unsigned long long* p, long long n, unsigned long long v) {
+  if (n <= 0) return;
+  k_fill_u64<<<c.grid_for(n, 256), 256, 0, c.stream>>>(p, n, v);
+  c.count_launch();
+}
+
+__global__ void k_dict_insert(const long long* __restrict__ vals, long long d, long long* __restrict__ hk,
+                              unsigned* __restrict__ hr, unsigned long long mask, long long empty) {
+  for (long long i = gtid(); i < d; i += gstride()) {
+    const long long v = vals[i];
+    unsigned long long h = static_cast<unsigned long long>(v) * 0x9E3779B97F4A7C15ULL;
+    unsigned long long sl = (h ^ (h >> 31)) & mask;
+    while (atomicCAS(reinterpret_cast<unsigned long long*>(hk) + sl, static_cast<unsigned long long>(empty),
+                     static_cast<unsigned long long>(v)) != static_cast<unsigned long long>(empty))
+      sl = (sl + 1) & mask;
+    hr[sl] = static_cast<unsigned>(i);
+  }
+}
+
+// the column's KeyDict (distinct values by a device sort, then the value ->
+// rank map), built once and kept with the column; false: not buildable
+// (the column holds INT64_MIN, or more than 2^32 distinct values)
+__global__ void k_pack_str8(const uint8_t* __restrict__ p, long long n, int w, long long* __restrict__ out) {
+  for (long long i = gtid(); i < n; i += gstride()) {
+    unsigned long long d = 0;
+    for (int j = 0; j < w; ++j) d = (d << 8) | p[i * w + j];
+    out[i] = static_cast<long long>(d);
+  }
+}
+
+bool ensure_dict(Ctx& c, const Column* col, long long rows, long long mn) {
+  KeyDict& D = *col->dict;
+  std::lock_guard<std::mutex> lk(D.mu);
+  if (D.ready) return true;
+  Tensor t = col->t;
+  t.rows = rows;
+  if (t.dtype == TQP_STR8) {  // rows of <= 7 bytes, packed big-endian (>= 0)
+    if (t.cols > 7) return false;
+    Tensor packed = c.alloc(TQP_I64, rows, 1);
+    if (rows) {
+      k_pack_str8<<<c.grid_for(rows, 256), 256, 0, c.stream>>>(t.ptr<uint8_t>(), rows, static_cast<int>(t.cols),
+                                                              packed.ptr<long long>());
+      c.count_launch();
+    }
+    t = packed;
+    mn = 0;
+  }
+  if (mn == static_cast<long long>(0x8000000000000000ULL)) return false;
+  Tensor order = k::argsort_stable(c, t);
+  Tensor sorted = k::gather(c, t, order);
+  Tensor distinct = k::compact(c, sorted, k::segment_starts(c, sorted));
+  const long long d = distinct.rows;
+  if (d >= (1LL << 32)) return false;
+  unsigned long long cap = 1024;
+  while (cap < 2ULL * static_cast<unsigned long long>(d)) cap <<= 1;
+  D.hkeys = c.alloc_bytes(sizeof(long long) * cap);
+  D.hranks = c.alloc_bytes(sizeof(unsigned) * cap);
+  fill_u64(c, static_cast<unsigned long long*>(D.hkeys->ptr), static_cast<long long>(cap), static_cast<unsigned long long>(mn - 1));
+  if (d) {
+    k_dict_insert<<<c.grid_for(d, 256), 256, 0, c.stream>>>(distinct.ptr<long long>(), d, static_cast<long long*>(D.hkeys->ptr),
+                                                            static_cast<unsigned*>(D.hranks->ptr), cap - 1, mn - 1);
+    c.count_launch();
+  }
+  D.vals = distinct;
+  D.d = d;
+  D.mask = cap - 1;
+  D.empty = mn - 1;
+  D.ready = true;
+  return true;
+}
+
 // MODE_HASH table shape: shared-memory records per CTA when the whole code
 // range fits kHashPrivBytes, a direct-address global table (slot = code)
 // while the range is at most 4 slots per fact row (and <= 2^26), otherwise
@@ -2618,7 +2704,8 @@ unsigned long long hash_key_widths(const ProbeSpec& ps) {
   return w;
 }
 
-GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsigned* present) {
+GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsigned* present,
+                          const std::vector<const long long*>& dict_vals) {
   GroupSpec gs;
   gs.f = fs;
   gs.gacc = ps.gacc;
@@ -2634,6 +2721,7 @@ GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsign
   gs.cnt_packed = 1;
   gs.absmax = ps.absmax_out;
   gs.flag_word = ps.hflags;
+  gs.qfrac = ps.qfrac;
   for (int i = 0; i < ps.nhkeys; ++i) {
     gs.key_cols[i] = nullptr;
     gs.kmin[i] = ps.hkeys[i].kmin;
@@ -2641,17 +2729,9 @@ GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsign
     gs.krange[i] = ps.hkeys[i].range;
     gs.kstride[i] = ps.hkeys[i].stride;
     gs.key_w[i] = ps.hkeys[i].width;
+    gs.dvals[i] = dict_vals[i];
   }
   return gs;
-}
-
-__global__ void k_fill_u64(unsigned long long* __restrict__ p, long long n, unsigned long long v) {
-  for (long long i = gtid(); i < n; i += gstride()) p[i] = v;
-}
-void fill_u64(Ctx& c, unsigned long long* p, long long n, unsigned long long v) {
-  if (n <= 0) return;
-  k_fill_u64<<<c.grid_for(n, 256), 256, 0, c.stream>>>(p, n, v);
-  c.count_launch();
 }
 
 // a fused unit that cannot take this data (host-side contract check): the
@@ -2684,7 +2764,7 @@ struct Runner {
   // flagged per group (IEEE sum semantics) instead of summed in fixed point
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
            bool narrow = false, UnitPending* pend = nullptr, bool weighted = false, bool fullsort = false,
-           bool special = false) const {
+           bool special = false, int qfrac = 64) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
@@ -3013,7 +3093,7 @@ struct Runner {
     // small-group keys are 1-byte strings; wider ones (or an accumulator
     // count without a small-group kernel) run as the hash-group unit
     if (P.mode == MODE_SMALL && alt && (!ok || !tile_kernel(MODE_SMALL, ps.nacc)))
-      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special);
+      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special, qfrac);
     if (!ok) return nofuse(__LINE__);
     // probes whose matched root row is read: with repeated build keys such a
     // probe must match exactly one row (checked per row in a weighted run)
@@ -3030,6 +3110,7 @@ struct Runner {
     // MODE_HASH: key digits from the key columns' ranges, the code's mixed
     // radix, and the table shape (private / direct / open addressing)
     std::shared_ptr<DevBuf> htag_buf, hrec_buf;
+    std::vector<const long long*> hdict_vals(kMaxKeys, nullptr);
     unsigned long long hcap = 0;
     int hrec_words = 0;
     if (P.mode == MODE_HASH) {
@@ -3062,10 +3143,47 @@ struct Runner {
         }
       }
       ensure_key_info(c, icols, iday);
+      // int keys whose ranges multiply past 2^62: the widest ones take
+      // dictionary digits (rank among the column's distinct values)
+      std::vector<char> use_dict(nk, 0);
+      {
+        auto range_of = [&](int i) -> long double {
+          const GKey& K = ps.hkeys[i];
+          if (K.width) return use_dict[i] ? static_cast<long double>(std::max<long long>(1, kc[i]->dict->d))
+                                          : static_cast<long double>(K.range);
+          const KeyRange& r = *kc[i]->range;
+          if (r.mn > r.mx) return 1.0L;
+          if (use_dict[i]) return static_cast<long double>(std::max<long long>(1, kc[i]->dict->d));
+          const long double step = (P.hkey_lt[i] == TQP_LT_DATE && r.day == 1) ? 86400000000000.0L : 1.0L;
+          return (static_cast<long double>(r.mx) - static_cast<long double>(r.mn)) / step + 1.0L;
+        };
+        for (;;) {
+          long double prod = 1.0L;
+          for (int i = 0; i < nk; ++i) prod *= range_of(i);
+          if (prod <= 4.0e18L) break;  // < 2^62
+          int widest = -1;
+          for (int i = 0; i < nk; ++i)
+            if (!use_dict[i] && (widest < 0 || range_of(i) > range_of(widest))) widest = i;
+          if (widest < 0) break;
+          const std::string& tname = P.hkeys[widest].probe < 0 ? P.fact_table : P.builds[P.probes[P.hkeys[widest].probe].build].table;
+          if (!ensure_dict(c, kc[widest], bind_table(tables, tname)->rows, ps.hkeys[widest].width ? 0 : kc[widest]->range->mn))
+            return nofuse(__LINE__);
+          use_dict[widest] = 1;
+        }
+      }
       unsigned __int128 total = 1;
       for (int i = 0; i < nk; ++i) {
         GKey& K = ps.hkeys[i];
         if (K.width) {
+          if (use_dict[i]) {
+            const KeyDict& D = *kc[i]->dict;
+            K.range = static_cast<unsigned long long>(std::max<long long>(1, D.d));
+            K.dkeys = static_cast<const long long*>(D.hkeys->ptr);
+            K.dranks = static_cast<const unsigned*>(D.hranks->ptr);
+            K.dmask = D.mask;
+            K.dempty = D.empty;
+            hdict_vals[i] = D.vals.ptr<long long>();
+          }
           total *= K.range;
           continue;
         }
@@ -3073,6 +3191,15 @@ struct Runner {
         if (r.mn > r.mx) {  // empty key column: no row reaches the table
           K.kmin = 0;
           K.range = 1;
+        } else if (use_dict[i]) {
+          const KeyDict& D = *kc[i]->dict;
+          K.kmin = 0;
+          K.range = static_cast<unsigned long long>(std::max<long long>(1, D.d));
+          K.dkeys = static_cast<const long long*>(D.hkeys->ptr);
+          K.dranks = static_cast<const unsigned*>(D.hranks->ptr);
+          K.dmask = D.mask;
+          K.dempty = D.empty;
+          hdict_vals[i] = D.vals.ptr<long long>();
         } else {
           K.kmin = r.mn;
           K.step = (P.hkey_lt[i] == TQP_LT_DATE && r.day == 1) ? 86400000000000LL : 1;
@@ -3114,6 +3241,8 @@ struct Runner {
       if (ps.hpriv) TQP_CUDA(cudaMemsetAsync(hrec_buf->ptr, 0, hrec_buf->bytes, c.stream));
       ps.htag = static_cast<unsigned long long*>(htag_buf->ptr);
       ps.absmax_out = po ? nullptr : err + 5;  // sharded partials keep the whole-scan bound
+      ps.qfrac = qfrac;
+      ps.qstats = po ? nullptr : err + 6;
       ps.gcnt = static_cast<unsigned long long*>(hrec_buf->ptr);
       ps.gacc = ps.gcnt + 1;
       ps.gstride = hrec_words;
@@ -3302,7 +3431,7 @@ struct Runner {
       k_hash_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
           ps.htag, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
       c.count_launch();
-      GroupSpec gs = hash_group_spec(ps, fs, static_cast<const unsigned*>(pres->ptr));
+      GroupSpec gs = hash_group_spec(ps, fs, static_cast<const unsigned*>(pres->ptr), hdict_vals);
       if (po) {
         Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, static_cast<long long>(hcap), gs.present);
         const long long n = gids.rows;
@@ -3379,22 +3508,31 @@ struct Runner {
     c.sync();
     hp.mark("sync");
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
-    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special);  // a fifth key in a CTA
+    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special, qfrac);  // a fifth key in a CTA
     if (herr[0] && herr[3] == FR_DUP_KEY && !weighted) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: repeated build keys: unit reruns weighted\n");
-      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special);
+      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special, qfrac);
     }
     if (herr[0] && (herr[3] == FR_TOPK_BLOCK || herr[3] == FR_TOPK_FINAL) && !fullsort && P.topk && !po) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: top-k ties overflow: unit reruns with a full group sort\n");
-      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special);
+      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special, qfrac);
     }
-    if (herr[0] && herr[3] == FR_Q64_CONVERT && P.mode == MODE_HASH && !special && !po) {
-      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: NaN/Inf group values: unit reruns with special flags\n");
-      return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true);
+    if (herr[0] && herr[3] == FR_Q64_CONVERT && P.mode == MODE_HASH && !po && (!special || qfrac == 64)) {
+      // NaN / Inf values: flagged per group; finite values with bits below
+      // 2^-64: more fraction bits (exact while the sums' range allows)
+      long long lowneg = 0;
+      TQP_CUDA(cudaMemcpyAsync(&lowneg, err + 6, sizeof(lowneg), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      const int F = std::max<long long>(64, lowneg) > 120 ? -1 : static_cast<int>(std::max<long long>(64, lowneg));
+      if (F > 0 && (!special || F > qfrac)) {
+        if (std::getenv("TQP_DEBUG_FALLBACK"))
+          std::fprintf(stderr, "tqp: NaN/Inf or fine fp64 group values: unit reruns with special flags, %d fraction bits\n", F);
+        return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true, F);
+      }
     }
-    if (herr[0] && alt && P.mode == MODE_SMALL) {
-      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: small-group unit reruns as hash-group (reason %lld)\n", herr[3]);
-      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special);
+    if (herr[0] && alt && (P.mode == MODE_SMALL || P.mode == MODE_BUILDGRP)) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: unit reruns as hash-group (reason %lld)\n", herr[3]);
+      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special, qfrac);
     }
     if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
       std::fprintf(stderr, "tqp: fused unit left the fused path (reason %lld)\n", herr[3]);
@@ -3586,7 +3724,7 @@ struct Runner {
                                  : P.mode == MODE_SMALL ? kSmallPartWords
                                                         : record_words(nkeyc, fs.nacc);
     if (parts.empty()) throw Error(TQP_ERR_ARG, where + ": no partials to merge");
-    if (alt && P.mode == MODE_SMALL && parts[0].ptr && parts[0].words >= kHdrWords) {
+    if (alt && (P.mode == MODE_SMALL || P.mode == MODE_BUILDGRP) && parts[0].ptr && parts[0].words >= kHdrWords) {
       // shards whose small-group run overflowed produced hash-group partials
       unsigned long long h[kHdrWords];
       TQP_CUDA(cudaMemcpyAsync(h, parts[0].ptr, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
@@ -3739,10 +3877,15 @@ std::vector<FusedUnit> plan_fusion(Ctx& ctx, const Plan& plan) {
     u.name = std::string("fused_") + (P.probes.empty() ? "scan_" : "probe_") + mode + (P.topk ? "_topk" : "");
     u.explain = ex.str();
     auto R = std::make_shared<Runner>(Runner{P});
-    if (P.mode == MODE_SMALL && P.hash_alt) {
+    if ((P.mode == MODE_SMALL && P.hash_alt) || (P.mode == MODE_BUILDGRP && !P.hkeys.empty())) {
+      // the hash-group unit a small-group overflow or a build-group unit whose
+      // group build meets repeated keys (or unconvertible values) reruns as
       PipeDesc H = P;
       H.mode = MODE_HASH;
       H.key_columns.clear();
+      H.group_key_root_columns.clear();
+      if (P.mode == MODE_BUILDGRP) H.builds[H.probes[H.group_probe].build].assign_groups = false;
+      H.group_probe = -1;
       R->alt = std::make_shared<const Runner>(Runner{H});
     }
     u.run = [R](Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& t, UnitPending* pend) {

@@ -632,13 +632,15 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 qv = static_cast<__int128>(static_cast<long long>(v[k]));
               } else {
                 const double dv = __longlong_as_double(static_cast<long long>(v[k]));
-                if (!f64_to_q64(dv, qv)) {
+                if (!f64_to_qf(dv, MODE == MODE_HASH ? s.qfrac : 64, qv)) {
                   qv = 0;
                   if (MODE == MODE_HASH && s.hflags >= 0 && (isnan(dv) || isinf(dv))) {
                     const unsigned long long bit = isnan(dv) ? 1ULL : dv > 0 ? 2ULL : 4ULL;
                     atomicOr(s.gcnt + static_cast<long long>(g[k]) * s.gstride + s.hflags, bit << (3 * a));
                   } else {
                     set_fallback(s.err, FR_Q64_CONVERT);
+                    if (MODE == MODE_HASH && s.qstats && !isnan(dv) && !isinf(dv))
+                      atomicMax(s.qstats, static_cast<long long>(-lowbit_exp(dv)));
                   }
                 } else {
                   fabsmax = fmax(fabsmax, fabs(dv));
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
     } else if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
       set_fallback(s.err, FR_INT_RANGE);
     }
-    if constexpr (MODE == MODE_BUILDGRP || MODE == MODE_HASH) q64_range_check(fabsmax, s.n, s.err);
+    if constexpr (MODE == MODE_BUILDGRP || MODE == MODE_HASH) q64_range_check(fabsmax, s.n, s.err, MODE == MODE_HASH ? s.qfrac : 64);
     if constexpr (MODE == MODE_SMALL) {
       for (int gg = 0; gg < kGroups; ++gg) {
         for (int a = 0; a <= s.nacc; ++a) {

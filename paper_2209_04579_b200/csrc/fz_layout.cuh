@@ -163,6 +163,12 @@ struct GKey {
   long long step = 1;
   unsigned long long range = 1;
   unsigned long long stride = 1;
+  // dictionary digit (wide int64 keys): rank of the value among the column's
+  // distinct values, looked up in an open-addressing map (dkeys / dranks)
+  const long long* dkeys = nullptr;
+  const unsigned* dranks = nullptr;
+  unsigned long long dmask = 0;
+  long long dempty = 0;
 };
 constexpr unsigned long long kHashBusy = ~0ULL;       // tag of a slot being claimed
 constexpr unsigned long long kCntAdd = 1ULL << 40;    // packed count: rows | adds << 40
@@ -208,6 +214,8 @@ struct ProbeSpec {
   // of the reference's sequential sum can overflow), not the whole scan's rows
   long long* absmax_out;
   int hflags;  // >= 0: record word of per-accumulator NaN / +Inf / -Inf bits (special run)
+  int qfrac;          // MODE_HASH fixed-point fraction bits (64, or more after a re-run)
+  long long* qstats;  // MODE_HASH: max of -(lowest set bit exponent) over unconvertible finite values
 };
 
 struct BuildSpec {
@@ -447,7 +455,9 @@ __device__ __forceinline__ unsigned long long eval_acc(const Acc& a, const unsig
 // any x with a nonzero bit below 2^-64 (it would be truncated), so a group
 // sum built from these values is exact or the unit falls back (FR_Q64_*).
 // Every money value (a multiple of 2^-40 or coarser) converts.
-__device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
+// Q(128-F).F generalisation (F fraction bits; MODE_HASH re-runs with F > 64
+// when a value has bits below 2^-64): exact or false
+__device__ __forceinline__ bool f64_to_qf(double x, int F, __int128& out) {
   long long bits = __double_as_longlong(x);
   int ex = static_cast<int>((bits >> 52) & 0x7ff);
   if (ex == 0x7ff) return false;
@@ -457,7 +467,7 @@ __device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
   } else {
     mant |= 1ULL << 52;
   }
-  int shift = ex - 1075 + 64;
+  int shift = ex - 1075 + F;
   unsigned __int128 v;
   if (shift >= 0) {
     if (shift > 73) return false;
@@ -472,12 +482,23 @@ __device__ __forceinline__ bool f64_to_q64(double x, __int128& out) {
   out = bits < 0 ? -static_cast<__int128>(v) : static_cast<__int128>(v);
   return true;
 }
+__device__ __forceinline__ bool f64_to_q64(double x, __int128& out) { return f64_to_qf(x, 64, out); }
+
+// binary exponent of the lowest set bit of a finite nonzero x
+__device__ __forceinline__ int lowbit_exp(double x) {
+  const long long bits = __double_as_longlong(x);
+  int ex = static_cast<int>((bits >> 52) & 0x7ff);
+  unsigned long long mant = static_cast<unsigned long long>(bits) & ((1ULL << 52) - 1);
+  if (ex == 0) ex = 1;
+  else mant |= 1ULL << 52;
+  return ex - 1075 + (mant ? __ffsll(static_cast<long long>(mant)) - 1 : 0);
+}
 
 // Q64.64 group sums cannot wrap while max|value| x rows < 2^62 (the limb
 // words are bounded separately by kLimbMaxRows); checked once per thread
 // after its last row with the largest |value| it converted
-__device__ __forceinline__ void q64_range_check(double fabsmax, long long rows, long long* err) {
-  if (fabsmax * static_cast<double>(rows) >= 4.6116860184273879e18) set_fallback(err, FR_Q64_RANGE);
+__device__ __forceinline__ void q64_range_check(double fabsmax, long long rows, long long* err, int F = 64) {
+  if (fabsmax * static_cast<double>(rows) >= ldexp(4.6116860184273879e18, 64 - F)) set_fallback(err, FR_Q64_RANGE);
 }
 
 // Q64.64 -> fp64, correctly rounded (one rounding of the exact value: the
@@ -530,7 +551,19 @@ __device__ __forceinline__ unsigned long long gkey_digit(const GKey& K, unsigned
     const uint8_t* p = static_cast<const uint8_t*>(K.x.ptr) + row * K.width;
     unsigned long long d = 0;
     for (int j = 0; j < K.width; ++j) d = (d << 8) | __ldg(p + j);
-    return d;
+    if (!K.dkeys) return d;
+    raw = d;  // dictionary over the packed rows
+  }
+  if (K.dkeys) {
+    const long long v = static_cast<long long>(raw);
+    unsigned long long h = static_cast<unsigned long long>(v) * 0x9E3779B97F4A7C15ULL;
+    unsigned long long sl = (h ^ (h >> 31)) & K.dmask;
+    for (;;) {
+      const long long k = __ldg(K.dkeys + sl);
+      if (k == v) return __ldg(K.dranks + sl);
+      if (k == K.dempty) return ~0ULL;  // not in the dictionary: flagged as out of range
+      sl = (sl + 1) & K.dmask;
+    }
   }
   unsigned long long d = raw - static_cast<unsigned long long>(K.kmin);
   if (K.step != 1) d /= static_cast<unsigned long long>(K.step);

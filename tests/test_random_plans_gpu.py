@@ -41,3 +41,20 @@ def test_random_plans_nvrtc_kernels(env):
     tail = "\n".join(r.stdout.splitlines()[-40:])
     assert r.returncode == 0, tail + r.stderr[-2000:]
     assert "0 failure(s)" in r.stdout, tail
+
+
+# --profile groups (oracle/tools/random_plans.cpp): group-by over int / date /
+# short-string keys with 1 .. 10 M distinct values (dense, sparse, from the
+# fact or the joined dim), joins with dense, non-dense (spread keys) and
+# repeated (1:N) build keys, NaN / -0.0 values, ORDER BY + LIMIT with ties.
+# Every plan must match the reference AND every fused unit must stay on the
+# fused path (--require-fused: an exact-path fallback counts as a failure).
+@pytest.mark.parametrize("seed", [1, 4])
+def test_random_group_plans_stay_fused(seed):
+    if not BIN.exists():
+        pytest.fail(f"{BIN} is not built (make -C oracle)")
+    r = subprocess.run([str(BIN), "--profile", "groups", "--seed", str(seed), "--plans", "60", "--require-fused", "1"],
+                       capture_output=True, text=True, timeout=900)
+    tail = "\n".join(r.stdout.splitlines()[-40:])
+    assert r.returncode == 0, tail + r.stderr[-2000:]
+    assert "0 fused fallback(s), 0 failure(s)" in r.stdout, tail
