@@ -405,6 +405,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_extra:
         extra["q6_sf1"] = run_q6_sf1(args, tqp, torch, ctx, stream)
         extra["per_instruction"] = run_per_instruction(args, tqp, torch, ctx, stream, tables, L)
+        extra["hash_group"] = run_hash_group(args, tqp, torch, ctx, stream, tables, L)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -487,6 +488,45 @@ def run_per_instruction(args, tqp, torch, ctx, stream, tables, L):
     return {"workload": f"suite per instruction (fuse=False), SF{args.sf:g}", "latency_ms": ms,
             "rows_per_s": {q: L / (v / 1e3) for q, v in ms.items()}, "suite_ms": sum(ms.values()),
             "launches_per_suite": ctx.launches - launches0}
+
+
+def run_hash_group(args, tqp, torch, ctx, stream, tables, L):
+    """queries/qg.sql: GROUP BY l_partkey (200 k groups per SF) with a date
+    filter, SUM(price*(1-disc)), SUM(qty), COUNT(*) - the fused hash-group
+    unit (direct-address group table, exact Q64.64 limb sums), and the same
+    plan per instruction (the reference's sort-based lowering on the device).
+    Algorithmic bytes: l_shipdate, l_partkey, l_extendedprice, l_discount,
+    l_quantity = 40 B per lineitem row."""
+    plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / "qg.opplan.json").read_text())
+    ex = tqp.Executor(plan, ctx=ctx)
+    li = {"lineitem": tables["lineitem"]}
+    t0 = time.perf_counter()
+    ex.execute(li)
+    ctx.sync()
+    cold = (time.perf_counter() - t0) * 1e3
+    for _ in range(args.warmup):
+        ex.execute(li)
+    ms = timed_queries(torch, stream, lambda q: ex.execute(li), ["qg"], max(5, args.steps))["qg"]
+    ex.set_timing(True)
+    ex.reset_timings()
+    ex.execute(li)
+    ctx.sync()
+    units = ex.timings()
+    ex.set_timing(False)
+    groups = ex.execute(li).to_numpy()[0][2].shape[0]
+    nf = tqp.Executor(plan, fuse=False, ctx=ctx)
+    nf.execute(li)
+    ms_nf = timed_queries(torch, stream, lambda q: nf.execute(li), ["qg"], 3)["qg"]
+    peak, _ = measured_peaks()
+    b = 40 * L
+    kern = {k: v["total_ms"] / max(1, v["calls"]) for k, v in units.items() if k.startswith("kernel:")}
+    scan_ms = max(kern.values()) if kern else None
+    return {"workload": f"qg: GROUP BY l_partkey, SF{args.sf:g} ({groups} groups), fused hash-group, device-resident",
+            "latency_ms": ms, "rows_per_s": L / (ms / 1e3), "algorithmic_bytes": b,
+            "hbm_frac": b / (ms / 1e3) / 1e9 / peak, "scan_kernel_ms": scan_ms,
+            "scan_kernel_hbm_frac": (b / (scan_ms / 1e3) / 1e9 / peak) if scan_ms else None,
+            "units": units, "explain": ex.explain(), "cold_ms": cold, "fallbacks": ex.fallbacks,
+            "per_instruction_ms": ms_nf, "speedup_vs_per_instruction": ms_nf / ms}
 
 
 def run_csv_leg(tqp, ctx, sf):

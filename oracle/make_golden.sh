@@ -35,3 +35,17 @@ doc = {"generator": "oracle/make_golden.sh: tqp_ref_runner run (reference execut
 json.dump(doc, open('../tests/golden/tpch_results_sf%s.json' % sf, 'w'), indent=0)
 PY
 done
+
+# qg (GROUP BY l_partkey, the hash-group workload): reference results at SF0.05 and SF1
+for SF in 0.05 1; do
+  ./_ref/tqp_ref_runner run --sf $SF --queries qg --repeat 0 --warmup 0 --results /tmp/tqp_qg_sf$SF.json >/dev/null
+  python3 - "$SF" <<'PY'
+import gzip, json, sys
+sf = sys.argv[1]
+r = json.load(open('/tmp/tqp_qg_sf%s.json' % sf))
+doc = {"generator": "oracle/make_golden.sh: tqp_ref_runner run --queries qg (reference executor, par backend)",
+       "sf": float(sf), "seed": 7, "lineitem_rows": r["lineitem_rows"], "results": r["results"]}
+with gzip.open('../tests/golden/qg_results_sf%s.json.gz' % sf, 'wt') as f:
+    json.dump(doc, f)
+PY
+done

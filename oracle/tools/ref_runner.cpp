@@ -80,7 +80,8 @@ int main(int argc, char** argv) {
   try {
     if (mode == "opplan") {
       std::string out = get("--out", ".");
-      for (const std::string q : {"q1", "q3", "q6", "q14"}) {
+      // qg: GROUP BY l_partkey (2 M groups at SF10), the hash-group workload
+      for (const std::string q : {"q1", "q3", "q6", "q14", "qg"}) {
         PlanPtr plan = optimize(query_plan(qdir, q, cat), cat);
         OperatorPlan op = plan_operators(plan, cat);
         std::ofstream f(out + "/" + q + ".opplan.json");

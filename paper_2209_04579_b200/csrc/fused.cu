@@ -1351,14 +1351,18 @@ struct GroupSpec {
   const long long* absmax = nullptr;  // MODE_HASH: int sums exact iff absmax x rows < 2^63
   int flag_word = -1;                 // MODE_HASH special run: record word of the NaN/Inf bits
   int qfrac = 64;                     // fixed-point fraction bits of the sums
+  int limb2 = 0;                      // MODE_HASH 2-limb sums (checked per group against fmax)
+  const long long* fmax = nullptr;    // max |fp64 value| (bits) of the scan
+  int direct_codes = 0;               // MODE_HASH direct table: the group's code is its slot
 };
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g);
 
 // group key i of group g (STR8 keys: the row's bytes big-endian)
 __device__ __forceinline__ long long group_key_value(const GroupSpec& s, int i, unsigned g) {
-  if (s.codes) {
-    const unsigned long long dg = ((s.codes[g] - 1ULL) / s.kstride[i]) % s.krange[i];
+  if (s.codes || s.direct_codes) {
+    const unsigned long long code = s.direct_codes ? static_cast<unsigned long long>(g) : s.codes[g] - 1ULL;
+    const unsigned long long dg = (code / s.kstride[i]) % s.krange[i];
     if (s.dvals[i]) return s.dvals[i][dg];
     return s.key_w[i] ? static_cast<long long>(dg) : s.kmin[i] + static_cast<long long>(dg * static_cast<unsigned long long>(s.kstep[i]));
   }
@@ -1370,6 +1374,11 @@ __device__ __forceinline__ long long group_count(const GroupSpec& s, unsigned g)
 }
 // limb words exact: fewer than kLimbMaxRows adds reached them
 __device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
+  if (s.limb2) {
+    const unsigned long long w = s.gcnt[g * s.cnt_stride];
+    const double fm = s.fmax ? __longlong_as_double(*s.fmax) : 0.0;
+    return (w >> 40) < (1ULL << 22) && fm * static_cast<double>(w & kCntMask) < 2.1990232555520000e12;  // 2^41
+  }
   if (s.acc_words != kLimbWords) return true;
   const unsigned long long w = s.gcnt[g * s.cnt_stride];
   return (s.cnt_packed ? (w >> 40) : w) < static_cast<unsigned long long>(kLimbMaxRows);
@@ -1377,6 +1386,7 @@ __device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
 
 // accumulator a of group g as int128
 __device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, int a) {
+  if (s.limb2) return limbs2_to_i128(s.gacc + static_cast<long long>(g) * s.acc_stride + a * 2);
   const unsigned long long* w = s.gacc + static_cast<long long>(g) * s.acc_stride + a * s.acc_words;
   if (s.acc_words == kLimbWords) return limbs_to_i128(w);
   return static_cast<__int128>((static_cast<unsigned __int128>(w[1]) << 64) | w[0]);
@@ -1882,7 +1892,10 @@ __global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids, co
     for (int j = 0; j < s.f.nouts; ++j) {
       unsigned long long bits;
       bool f;
-      if (!group_out_value(s, j, g, bits, f)) err[0] = 1;
+      if (!group_out_value(s, j, g, bits, f)) {
+        err[0] = 1;
+        err[3] = FR_GROUP_VALUE;
+      }
       store_group_out(s, j, r, bits);
     }
   }
@@ -1894,6 +1907,15 @@ __global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, lon
     mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i * cnt_stride] != 0;
 }
 
+// MODE_HASH direct tables: bit per slot with rows
+__global__ void k_count_present(const unsigned long long* __restrict__ cnt, long long stride, long long cap,
+                                unsigned* __restrict__ present) {
+  const long long n32 = (cap + 31) & ~31LL;
+  for (long long i = gtid(); i < n32; i += gstride()) {
+    const unsigned bits = __ballot_sync(0xffffffffu, i < cap && cnt[i * stride] != 0ULL);
+    if ((threadIdx.x & 31) == 0) present[i >> 5] = bits;
+  }
+}
 // MODE_HASH: bit per claimed slot of the group table
 __global__ void k_hash_present(const unsigned long long* __restrict__ tag, long long cap, unsigned* __restrict__ present) {
   const long long n32 = (cap + 31) & ~31LL;  // warp-uniform trip count (blockDim % 32 == 0)
@@ -1905,7 +1927,8 @@ __global__ void k_hash_present(const unsigned long long* __restrict__ tag, long 
 __global__ void k_group_keys(const unsigned long long* __restrict__ group_table, const long long* __restrict__ gids, long long n,
                              const long long* __restrict__ key_col, long long* __restrict__ out) {
   for (long long i = gtid(); i < n; i += gstride())
-    out[i] = key_col[group_table ? static_cast<long long>(group_table[gids[i]] & 0xffffffffULL) - 1 : gids[i]];
+    out[i] = key_col ? key_col[group_table ? static_cast<long long>(group_table[gids[i]] & 0xffffffffULL) - 1 : gids[i]]
+                     : gids[i];
 }
 
 // ---- sharded-run partials ------------------------------------------------------
@@ -1927,10 +1950,15 @@ __global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, 
     const unsigned g = static_cast<unsigned>(gids[i]);
     const long long row = group_src_row(s, g);
     unsigned long long* w = out + i * words;
-    w[0] = s.codes ? s.codes[g] - 1ULL : static_cast<unsigned long long>(bkey[row]);
+    w[0] = s.direct_codes ? static_cast<unsigned long long>(g)
+           : s.codes      ? s.codes[g] - 1ULL
+                          : static_cast<unsigned long long>(bkey[row]);
     for (int k = 0; k < s.nkeyc; ++k) w[1 + k] = static_cast<unsigned long long>(group_key_value(s, k, g));
     w[1 + s.nkeyc] = static_cast<unsigned long long>(group_count(s, g));
-    if (!group_limbs_ok(s, g)) err[0] = 1;
+    if (!group_limbs_ok(s, g)) {
+      err[0] = 1;
+      err[3] = FR_GROUP_VALUE;
+    }
     for (int a = 0; a < s.f.nacc; ++a) {  // records carry int128 (lo, hi)
       const unsigned __int128 v = static_cast<unsigned __int128>(group_acc(s, g, a));
       w[2 + s.nkeyc + 2 * a] = static_cast<unsigned long long>(v);
@@ -2718,10 +2746,13 @@ GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsign
   gs.nkeyc = ps.nhkeys;
   gs.nsort = 0;
   gs.codes = ps.htag;
+  gs.direct_codes = ps.htag ? 0 : 1;
   gs.cnt_packed = 1;
   gs.absmax = ps.absmax_out;
   gs.flag_word = ps.hflags;
   gs.qfrac = ps.qfrac;
+  gs.limb2 = ps.hlimbs == 2 ? 1 : 0;
+  gs.fmax = ps.fmax_out;
   for (int i = 0; i < ps.nhkeys; ++i) {
     gs.key_cols[i] = nullptr;
     gs.kmin[i] = ps.hkeys[i].kmin;
@@ -2762,9 +2793,11 @@ struct Runner {
   // row weights per key and the fact scan counts rows by multiplicity
   // special: re-run after a hash-group fp64 value was NaN or +-Inf: those are
   // flagged per group (IEEE sum semantics) instead of summed in fixed point
+  // hlimbs: hash-group sums in 2 limbs (re-run with 3 when a group's range
+  // check fails)
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
            bool narrow = false, UnitPending* pend = nullptr, bool weighted = false, bool fullsort = false,
-           bool special = false, int qfrac = 64) const {
+           bool special = false, int qfrac = 64, int hlimbs = 2) const {
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
@@ -3093,7 +3126,7 @@ struct Runner {
     // small-group keys are 1-byte strings; wider ones (or an accumulator
     // count without a small-group kernel) run as the hash-group unit
     if (P.mode == MODE_SMALL && alt && (!ok || !tile_kernel(MODE_SMALL, ps.nacc)))
-      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special, qfrac);
+      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special, qfrac, hlimbs);
     if (!ok) return nofuse(__LINE__);
     // probes whose matched root row is read: with repeated build keys such a
     // probe must match exactly one row (checked per row in a weighted run)
@@ -3218,9 +3251,14 @@ struct Runner {
       }
       ps.nhkeys = nk;
       const unsigned long long R = static_cast<unsigned long long>(total);
-      // special: one more word per record, NaN / +Inf / -Inf bits per accumulator
-      hrec_words = (1 + kLimbWords * std::max(1, nacc_all) + (special ? 1 : 0) + 3) & ~3;
-      ps.hflags = special ? 1 + kLimbWords * std::max(1, nacc_all) : -1;
+      // special: one more word per record, NaN / +Inf / -Inf bits per accumulator;
+      // 3-limb records are padded to whole 32-byte sectors, 2-limb ones are
+      // kept dense (an L2-resident table is worth more than aligned records)
+      const int L = (hlimbs == 2 && !po) ? 2 : kLimbWords;  // sharded partials: 3 limbs (no per-group fmax check)
+      hrec_words = 1 + L * std::max(1, nacc_all) + (special ? 1 : 0);
+      if (L == kLimbWords) hrec_words = (hrec_words + 3) & ~3;
+      ps.hflags = special ? 1 + L * std::max(1, nacc_all) : -1;
+      ps.hlimbs = L;
       const size_t priv_bytes = static_cast<size_t>(R) * (1 + kLimbWords * nacc_all) * sizeof(unsigned long long);
       ps.hpriv = priv_bytes <= kHashPrivBytes && !std::getenv("TQP_HASH_NOPRIV");
       ps.hdirect = ps.hpriv || (R <= kHashDirectMax && R <= 4ULL * static_cast<unsigned long long>(ps.n) + (1ULL << 20));
@@ -3232,14 +3270,20 @@ struct Runner {
         while (hcap < want) hcap <<= 1;
       }
       if (static_cast<double>(hcap) * (8.0 + 8.0 * hrec_words) > static_cast<double>(kHashMaxBytes)) return nofuse(__LINE__);
-      // direct tables are indexed by code: hmask + 1 is the slot count
+      // direct tables are indexed by code (hmask + 1 slots) and zeroed up
+      // front: no tags; open-addressing tables claim slots by tag and the
+      // claiming row zeroes the record
       ps.hmask = hcap - 1;
-      htag_buf = c.alloc_bytes(sizeof(unsigned long long) * hcap);
       hrec_buf = c.alloc_bytes(sizeof(unsigned long long) * hrec_words * hcap);
-      TQP_CUDA(cudaMemsetAsync(htag_buf->ptr, 0, htag_buf->bytes, c.stream));
-      // private runs flush into zeroed records; otherwise the claiming row zeroes
-      if (ps.hpriv) TQP_CUDA(cudaMemsetAsync(hrec_buf->ptr, 0, hrec_buf->bytes, c.stream));
-      ps.htag = static_cast<unsigned long long*>(htag_buf->ptr);
+      if (ps.hdirect) {
+        TQP_CUDA(cudaMemsetAsync(hrec_buf->ptr, 0, hrec_buf->bytes, c.stream));
+        ps.htag = nullptr;
+      } else {
+        htag_buf = c.alloc_bytes(sizeof(unsigned long long) * hcap);
+        TQP_CUDA(cudaMemsetAsync(htag_buf->ptr, 0, htag_buf->bytes, c.stream));
+        ps.htag = static_cast<unsigned long long*>(htag_buf->ptr);
+      }
+      ps.fmax_out = po ? nullptr : err + 7;
       ps.absmax_out = po ? nullptr : err + 5;  // sharded partials keep the whole-scan bound
       ps.qfrac = qfrac;
       ps.qstats = po ? nullptr : err + 6;
@@ -3319,6 +3363,7 @@ struct Runner {
     ts.aux_bytes = static_cast<int>(P.mode == MODE_SMALL    ? aux_bytes_for<MODE_SMALL>(ps.nacc)
                                     : P.mode == MODE_SCALAR ? aux_bytes_for<MODE_SCALAR>(ps.nacc)
                                                             : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
+    ts.evict_first = (P.mode == MODE_HASH && !ps.hpriv && !std::getenv("TQP_NO_EVICT_FIRST")) ? 1 : 0;
     if (P.mode == MODE_HASH && ps.hpriv)  // the CTA's records [code][count, limbs per accumulator]
       ts.aux_bytes = static_cast<int>(((ps.hmask + 1) * (1 + kLimbWords * ps.nacc) * sizeof(unsigned long long) + 15) & ~15ULL);
     const bool wide = P.mode == MODE_SMALL && !narrow && jit_wanted(ps.n) && small_wide_wanted() && !generic_only;
@@ -3428,8 +3473,12 @@ struct Runner {
       keep.push_back(pres);
       keep.push_back(htag_buf);
       keep.push_back(hrec_buf);
-      k_hash_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
-          ps.htag, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
+      if (ps.htag)
+        k_hash_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
+            ps.htag, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
+      else
+        k_count_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
+            ps.gcnt, ps.gstride, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
       c.count_launch();
       GroupSpec gs = hash_group_spec(ps, fs, static_cast<const unsigned*>(pres->ptr), hdict_vals);
       if (po) {
@@ -3442,7 +3491,7 @@ struct Runner {
           c.count_launch();
         }
       } else if (!emit_groups(c, gs, static_cast<long long>(hcap), reinterpret_cast<const long long*>(ps.htag), err, outs,
-                              nrows, fullsort)) {
+                              nrows, fullsort, !ps.htag)) {
         return nofuse(__LINE__);
       }
     } else {
@@ -3508,14 +3557,18 @@ struct Runner {
     c.sync();
     hp.mark("sync");
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
-    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special, qfrac);  // a fifth key in a CTA
+    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special, qfrac, hlimbs);  // a fifth key in a CTA
     if (herr[0] && herr[3] == FR_DUP_KEY && !weighted) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: repeated build keys: unit reruns weighted\n");
-      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special, qfrac);
+      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special, qfrac, hlimbs);
     }
     if (herr[0] && (herr[3] == FR_TOPK_BLOCK || herr[3] == FR_TOPK_FINAL) && !fullsort && P.topk && !po) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: top-k ties overflow: unit reruns with a full group sort\n");
-      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special, qfrac);
+      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special, qfrac, hlimbs);
+    }
+    if (herr[0] && (herr[3] == FR_LIMB2 || herr[3] == FR_GROUP_VALUE) && P.mode == MODE_HASH && hlimbs == 2) {
+      if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: 2-limb group sums out of range: unit reruns with 3 limbs\n");
+      return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, special, qfrac, 3);
     }
     if (herr[0] && herr[3] == FR_Q64_CONVERT && P.mode == MODE_HASH && !po && (!special || qfrac == 64)) {
       // NaN / Inf values: flagged per group; finite values with bits below
@@ -3527,12 +3580,12 @@ struct Runner {
       if (F > 0 && (!special || F > qfrac)) {
         if (std::getenv("TQP_DEBUG_FALLBACK"))
           std::fprintf(stderr, "tqp: NaN/Inf or fine fp64 group values: unit reruns with special flags, %d fraction bits\n", F);
-        return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true, F);
+        return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true, F, hlimbs);
       }
     }
     if (herr[0] && alt && (P.mode == MODE_SMALL || P.mode == MODE_BUILDGRP)) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: unit reruns as hash-group (reason %lld)\n", herr[3]);
-      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special, qfrac);
+      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special, qfrac, hlimbs);
     }
     if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
       std::fprintf(stderr, "tqp: fused unit left the fused path (reason %lld)\n", herr[3]);
@@ -3632,12 +3685,13 @@ struct Runner {
   // every group is emitted in ascending key order and the ORDER BY + LIMIT
   // run as the reference lowers them (stable SortPermRows per key, last key
   // first, then the first k rows), on the device
+  // gids_sorted: slot order is key order (direct hash-group tables)
   bool emit_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
-                   std::vector<Tensor>& outs, long long& nrows, bool fullsort = false) const {
+                   std::vector<Tensor>& outs, long long& nrows, bool fullsort = false, bool gids_sorted = false) const {
     if (P.topk && fullsort) {
       GroupSpec all = gs;
       std::vector<Tensor> rows(outs.size());
-      if (!emit_all_groups(c, all, ngroups, bk, err, rows, nrows)) return false;
+      if (!emit_all_groups(c, all, ngroups, bk, err, rows, nrows, gids_sorted)) return false;
       Tensor perm = k::iota(c, nrows);
       for (int i = static_cast<int>(P.sort_outs.size()) - 1; i >= 0; --i)
         perm = k::sort_perm_rows(c, rows[P.sort_outs[i].first], perm, P.sort_outs[i].second);
@@ -3684,22 +3738,27 @@ struct Runner {
       nrows = -1;  // on the device (err[2]); read with the error flag
       return true;
     }
-    return emit_all_groups(c, gs, ngroups, bk, err, outs, nrows);
+    return emit_all_groups(c, gs, ngroups, bk, err, outs, nrows, gids_sorted);
   }
 
   // every group with rows, ascending by its (unique) key `bk`
   bool emit_all_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
-                       std::vector<Tensor>& outs, long long& nrows) const {
+                       std::vector<Tensor>& outs, long long& nrows, bool gids_sorted = false) const {
     Tensor gids = touched_groups(c, gs.gcnt, gs.cnt_stride, ngroups, gs.present);
     const long long n = gids.rows;
-    Tensor keys = c.alloc(TQP_I64, n, 1);
-    if (n) {
-      k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gids.ptr<long long>(), n, bk,
-                                                              keys.ptr<long long>());
-      c.count_launch();
+    Tensor order;
+    if (gids_sorted) {
+      order = k::iota(c, n);
+    } else {
+      Tensor keys = c.alloc(TQP_I64, n, 1);
+      if (n) {
+        k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gids.ptr<long long>(), n, bk,
+                                                                keys.ptr<long long>());
+        c.count_launch();
+      }
+      // positions of the touched groups in ascending build-key order
+      order = k::radix_sort_payload(c, keys, nullptr, false);
     }
-    // positions of the touched groups in ascending build-key order
-    Tensor order = k::radix_sort_payload(c, keys, nullptr, false);
     for (size_t j = 0; j < outs.size(); ++j) {
       outs[j] = alloc_out(c, gs, j, n);
       gs.f.out_ptr[j] = outs[j].data();

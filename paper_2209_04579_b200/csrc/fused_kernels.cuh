@@ -505,9 +505,10 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
               slot = static_cast<long long>(code);
               atomicAdd(s_stage_val + slot * (1 + kLimbWords * NA_), static_cast<unsigned long long>(wt[k]));
             } else {
-              slot = hash_claim(s, code);
+              // direct tables are zeroed up front (no tag, no claim)
+              slot = s.htag ? hash_claim(s, code) : static_cast<long long>(code);
               if (slot < 0) set_fallback(s.err, FR_HASH_FULL);
-              else atomicAdd(s.gcnt + slot * s.gstride, static_cast<unsigned long long>(wt[k]) + kCntAdd);
+              else red_add_hint(s.gcnt + slot * s.gstride, static_cast<unsigned long long>(wt[k]) + kCntAdd, l2_policy_evict_last());
             }
             if (slot < 0) pass[k] = false;
             g[k] = static_cast<unsigned>(slot < 0 ? 0 : slot);
@@ -650,10 +651,13 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                   fabsmax = fmax(fabsmax, fabs(dv) * static_cast<double>(wt[k]));
                 }
               }
-              if (MODE == MODE_HASH && s.hpriv)
+              if (MODE == MODE_HASH && s.hpriv) {
                 atomic_add_limbs(s_stage_val + static_cast<long long>(g[k]) * (1 + kLimbWords * NA_) + 1 + a * kLimbWords, qv);
-              else
+              } else if (MODE == MODE_HASH && s.hlimbs == 2) {
+                if (!atomic_add_limbs2(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * 2, qv, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
+              } else {
                 atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
+              }
             }
           }
         }
@@ -669,6 +673,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       set_fallback(s.err, FR_INT_RANGE);
     }
     if constexpr (MODE == MODE_BUILDGRP || MODE == MODE_HASH) q64_range_check(fabsmax, s.n, s.err, MODE == MODE_HASH ? s.qfrac : 64);
+    if (MODE == MODE_HASH && s.fmax_out && fabsmax > 0.0) atomicMax(s.fmax_out, __double_as_longlong(fabsmax));
     if constexpr (MODE == MODE_SMALL) {
       for (int gg = 0; gg < kGroups; ++gg) {
         for (int a = 0; a <= s.nacc; ++a) {
@@ -726,10 +731,16 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
         const unsigned long long c = r[0];
         if (!c) continue;
         if (c >= static_cast<unsigned long long>(kLimbMaxRows)) set_fallback(s.err, FR_LIMB_ROWS);
-        s.htag[code] = static_cast<unsigned long long>(code) + 1;
         atomicAdd(s.gcnt + code * s.gstride, c + kCntAdd);
 #pragma unroll
-        for (int a = 0; a < NA_; ++a) atomic_add_limbs(s.gacc + code * s.gstride + a * kLimbWords, limbs_to_i128(r + 1 + a * kLimbWords));
+        for (int a = 0; a < NA_; ++a) {
+          const __int128 v = limbs_to_i128(r + 1 + a * kLimbWords);
+          if (s.hlimbs == 2) {
+            if (!atomic_add_limbs2(s.gacc + code * s.gstride + a * 2, v, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
+          } else {
+            atomic_add_limbs(s.gacc + code * s.gstride + a * kLimbWords, v);
+          }
+        }
       }
     }
   } else if constexpr (MODE == MODE_SMALL) {

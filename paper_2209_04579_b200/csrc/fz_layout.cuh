@@ -45,6 +45,7 @@ enum FallbackReason : long long {
   FR_INT_RANGE = 19,       // int64 sum may overflow (|v| x rows >= 2^63)
   FR_HASH_FULL = 22,       // hash group / join table probe sequence exhausted
   FR_KEY_RANGE = 23,       // a group key digit outside its range (stale key range)
+  FR_LIMB2 = 24,           // a value too wide for the 2-limb group sums (re-run with 3 limbs)
 };
 
 // A per-row operand: fact column (src = -1) or a column of the build-side
@@ -216,6 +217,11 @@ struct ProbeSpec {
   int hflags;  // >= 0: record word of per-accumulator NaN / +Inf / -Inf bits (special run)
   int qfrac;          // MODE_HASH fixed-point fraction bits (64, or more after a re-run)
   long long* qstats;  // MODE_HASH: max of -(lowest set bit exponent) over unconvertible finite values
+  // MODE_HASH sums as 2 limbs (l0 42-bit unsigned, l1 signed: v = l0 + l1 * 2^42)
+  // while every value fits 105 bits; the reader checks per group that
+  // adds < 2^22 and fmax x rows < 2^41 (else the unit re-runs with 3 limbs)
+  int hlimbs;
+  long long* fmax_out;  // max |fp64 value| (bit pattern, atomicMax) over the scan
 };
 
 struct BuildSpec {
@@ -531,6 +537,20 @@ __device__ __forceinline__ void atomic_add_limbs(unsigned long long* p, __int128
   atomicAdd(p + 1, static_cast<unsigned long long>(u >> 42) & m);
   atomicAdd(p + 2, static_cast<unsigned long long>(static_cast<long long>(v >> 84)));
 }
+// 2-limb form (MODE_HASH): false if v needs more than 105 bits
+__device__ __forceinline__ bool atomic_add_limbs2(unsigned long long* p, __int128 v, unsigned long long pol) {
+  const __int128 hi = v >> 42;
+  if (hi != static_cast<__int128>(static_cast<long long>(hi))) return false;
+  unsigned long long lo = static_cast<unsigned long long>(v) & ((1ULL << 42) - 1);
+  unsigned long long h = static_cast<unsigned long long>(static_cast<long long>(hi));
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(lo), "l"(pol) : "memory");
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p + 1), "l"(h), "l"(pol) : "memory");
+  return true;
+}
+__device__ __forceinline__ __int128 limbs2_to_i128(const unsigned long long* w) {
+  return static_cast<__int128>(static_cast<unsigned __int128>(w[0]) +
+                               static_cast<unsigned __int128>(static_cast<__int128>(static_cast<long long>(w[1])) << 42));
+}
 __device__ __forceinline__ __int128 limbs_to_i128(const unsigned long long* w) {
   const unsigned __int128 u = static_cast<unsigned __int128>(w[0]) + (static_cast<unsigned __int128>(w[1]) << 42) +
                               (static_cast<unsigned __int128>(static_cast<__int128>(static_cast<long long>(w[2]))) << 84);
@@ -638,6 +658,8 @@ struct TileSpec {
   int stages = 3;
   int rows = kTileRows;   // rows per tile
   int aux_bytes = 0;      // per-thread accumulator / staging region
+  int evict_first = 0;    // stream the fact tiles with an L2 evict-first policy (keeps a
+                          // hash-group table resident in L2 under the stream)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -670,6 +692,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// non-returning u64 add with an L2 cache policy (hash-group table words)
+__device__ __forceinline__ void red_add_hint(unsigned long long* p, unsigned long long v, unsigned long long pol) {
+  asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* stage, unsigned long long* bar,
                                            long long tile) {
   const long long row0 = tile * t.rows;
@@ -678,9 +723,11 @@ __device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* sta
   unsigned total = 0;
   for (int c = 0; c < t.ncols; ++c) total += static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
   mbar_expect_tx(bar, total);
+  const unsigned long long pol = t.evict_first ? l2_policy_evict_first() : 0ULL;
   for (int c = 0; c < t.ncols; ++c) {
     unsigned bytes = static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
-    bulk_g2s(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar);
+    if (t.evict_first) bulk_g2s_hint(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar, pol);
+    else bulk_g2s(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar);
   }
 }
 
