@@ -313,6 +313,39 @@ tqp_tensor* tqp_executor_execute_partial(tqp_executor* ex, const char* const* na
 tqp_result* tqp_executor_finish(tqp_executor* ex, const void* const* parts, const int64_t* words,
                                 int nparts, tqp_status* st);
 
+/* ---- communicators and one-call sharded execution ----
+ * One rank per GPU. tqp_executor_execute_sharded runs phase 1 on this rank's
+ * tables with the build-side exchanges their layout needs (row-shard
+ * dimension tables: presence / flag bitmaps all-gathered over the global key
+ * range; row-shard tables whose rows the scan reads: rows re-aligned to the
+ * fact shards' key ranges with a grouped send/recv all-to-all), all-gathers
+ * the partials and merges them on every rank: every rank returns the whole
+ * result. Plans that cannot shard, or shards whose data leave the fused
+ * contract, run on the tables all-gathered to every rank, so the result and
+ * errors are the reference's either way (executor.cpp:346 is the unsharded
+ * equivalent; the reference has no sharded entry point). */
+typedef struct tqp_comm tqp_comm;
+typedef enum { TQP_SHARD_REPLICATED = 0, TQP_SHARD_COPARTITIONED = 1, TQP_SHARD_ROWS = 2 } tqp_shard_kind;
+/* 128-byte NCCL unique id, made on one rank and sent to the others by the
+ * caller (e.g. torch.distributed broadcast); NCCL is bound at run time. */
+int tqp_comm_nccl_unique_id(void* out128, tqp_status* st);
+tqp_comm* tqp_comm_init_nccl(tqp_ctx* ctx, const void* id128, int nranks, int rank, tqp_status* st);
+/* n ranks that are threads of this process (out[0..n)); each thread uses its
+ * own context. For single-GPU tests of the sharded paths (NCCL needs one
+ * GPU per rank). */
+int tqp_comm_init_local(int n, tqp_comm** out, tqp_status* st);
+int tqp_comm_rank(const tqp_comm* comm);
+int tqp_comm_size(const tqp_comm* comm);
+const char* tqp_comm_kind(const tqp_comm* comm);
+void tqp_comm_free(tqp_comm* comm);
+/* kinds[i]: tqp_shard_kind of tables[i] (lineitem / orders cut on order
+ * boundaries: COPARTITIONED; part / customer row-sharded: ROWS) */
+tqp_result* tqp_executor_execute_sharded(tqp_executor* ex, tqp_comm* comm, const char* const* names,
+                                         tqp_table* const* tables, const int* kinds, int ntables, tqp_status* st);
+/* JSON of this executor's last sharded run: {"path": "fused" | "gathered" |
+ * "unsharded", "ranks", "bitmap_merges", "shuffled_tables", "exchange_bytes"} */
+const char* tqp_executor_shard_stats(tqp_executor* ex);
+
 /* Description of the fused pipelines chosen for this plan (JSON). */
 const char* tqp_executor_explain(tqp_executor* ex);
 /* Fused units that met data outside their contract (duplicate build keys,

@@ -1,11 +1,13 @@
 // extern "C" boundary (include/tqp_b200.h): converts C++ errors into
 // tqp_status and owns the opaque handles.
+#include <cctype>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <string>
 
+#include "comm.hpp"
 #include "executor.hpp"
 #include "jit.hpp"
 
@@ -511,6 +513,78 @@ tqp_result* tqp_executor_finish(tqp_executor* ex, const void* const* parts, cons
     return r;
   });
 }
+
+struct tqp_comm {
+  std::unique_ptr<Comm> c;
+};
+
+int tqp_comm_nccl_unique_id(void* out128, tqp_status* st) {
+  return guard(st, [&] {
+    if (!out128) throw Error(TQP_ERR_ARG, "null id buffer");
+    nccl_unique_id(out128);
+    return 0;
+  });
+}
+
+tqp_comm* tqp_comm_init_nccl(tqp_ctx* ctx, const void* id128, int nranks, int rank, tqp_status* st) {
+  return guard(st, [&]() -> tqp_comm* {
+    if (!ctx || !id128) throw Error(TQP_ERR_ARG, "null context or id");
+    auto* h = new tqp_comm;
+    try {
+      h->c = make_nccl_comm(ctx->c, id128, nranks, rank);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    return h;
+  });
+}
+
+int tqp_comm_init_local(int n, tqp_comm** out, tqp_status* st) {
+  return guard(st, [&] {
+    if (!out) throw Error(TQP_ERR_ARG, "null output array");
+    auto g = make_local_group(n);
+    for (int i = 0; i < n; ++i) {
+      out[i] = new tqp_comm;
+      out[i]->c = std::move(g[i]);
+    }
+    return 0;
+  });
+}
+
+int tqp_comm_rank(const tqp_comm* comm) { return comm ? comm->c->rank : -1; }
+int tqp_comm_size(const tqp_comm* comm) { return comm ? comm->c->size : -1; }
+const char* tqp_comm_kind(const tqp_comm* comm) { return comm ? comm->c->kind() : ""; }
+void tqp_comm_free(tqp_comm* comm) { delete comm; }
+
+tqp_result* tqp_executor_execute_sharded(tqp_executor* ex, tqp_comm* comm, const char* const* names,
+                                         tqp_table* const* tables, const int* kinds, int n, tqp_status* st) {
+  return guard(st, [&] {
+    if (!ex || !comm) throw Error(TQP_ERR_ARG, "null executor or communicator");
+    if (n < 0 || (n > 0 && (!names || !tables || !kinds))) throw Error(TQP_ERR_ARG, "bad table arrays");
+    TableSet ts;
+    ShardEnv env;
+    env.comm = comm->c.get();
+    for (int i = 0; i < n; ++i) {
+      if (kinds[i] < TQP_SHARD_REPLICATED || kinds[i] > TQP_SHARD_ROWS) throw Error(TQP_ERR_ARG, "bad shard kind");
+      ts.push_back({names[i], &tables[i]->t});
+      std::string lower = names[i];
+      for (auto& ch : lower) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+      env.kinds[lower] = kinds[i];
+    }
+    auto* r = new tqp_result;
+    try {
+      r->r = ex->ex->execute_sharded(ts, env);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    for (auto& c : r->r.cols) r->handles.push_back(wrap(c.t));
+    return r;
+  });
+}
+
+const char* tqp_executor_shard_stats(tqp_executor* ex) { return ex ? ex->ex->shard_stats().c_str() : "{}"; }
 
 int tqp_executor_shardable(tqp_executor* ex, const char** why) {
   static thread_local std::string msg;

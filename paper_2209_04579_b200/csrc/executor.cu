@@ -11,6 +11,7 @@
 #include <set>
 #include <sstream>
 
+#include "comm.hpp"
 #include "executor.hpp"
 
 namespace tqp {
@@ -491,6 +492,132 @@ Partial Executor::execute_partial(const TableSet& tables) {
   ctx_.sync();
   if (ctx_.time_kernels) collect_kernel_events();
   return p;
+}
+
+int ShardEnv::kind_of(const std::string& table) const {
+  for (const auto& [name, k] : kinds)
+    if (iequals(name, table)) return k;
+  return SHARD_REPLICATED;
+}
+
+// Every row-shard / co-partitioned table all-gathered to every rank (rank
+// order), then the plan runs unsharded: the fallback for plans that do not
+// shard and for shards that leave the fused contract.
+Result Executor::gather_and_execute(const TableSet& tables, const ShardEnv& env) {
+  Comm& comm = *env.comm;
+  std::vector<std::shared_ptr<Table>> hold;
+  TableSet full;
+  for (const auto& [name, t] : tables) {
+    if (env.kind_of(name) == SHARD_REPLICATED) {
+      full.push_back({name, t});
+      continue;
+    }
+    const std::vector<long long> rows = allgather_host(ctx_, comm, {t->rows});
+    long long total = 0, mx = 0;
+    for (long long r : rows) {
+      total += r;
+      mx = std::max(mx, r);
+    }
+    auto g = std::make_shared<Table>();
+    g->rows = total;
+    for (const Column& col : t->cols) {
+      const size_t rowb = col.t.elem_size() * static_cast<size_t>(col.t.cols);
+      auto pad = ctx_.alloc_bytes(std::max<size_t>(1, rowb * mx));
+      auto all = ctx_.alloc_bytes(std::max<size_t>(1, rowb * mx * comm.size));
+      if (t->rows) TQP_CUDA(cudaMemcpyAsync(pad->ptr, col.t.data(), rowb * t->rows, cudaMemcpyDeviceToDevice, ctx_.stream));
+      comm.allgather(ctx_, pad->ptr, all->ptr, rowb * mx);
+      Column nc;
+      nc.name = col.name;
+      nc.type = col.type;
+      nc.t = ctx_.alloc(col.t.dtype, total, col.t.cols);
+      long long off = 0;
+      for (int r = 0; r < comm.size; ++r) {
+        if (rows[r])
+          TQP_CUDA(cudaMemcpyAsync(static_cast<char*>(nc.t.data()) + rowb * off, static_cast<char*>(all->ptr) + rowb * mx * r,
+                                   rowb * rows[r], cudaMemcpyDeviceToDevice, ctx_.stream));
+        off += rows[r];
+      }
+      g->cols.push_back(std::move(nc));
+    }
+    hold.push_back(g);
+    full.push_back({name, g.get()});
+  }
+  Result r = execute(full);
+  ctx_.sync();
+  return r;
+}
+
+Result Executor::execute_sharded(const TableSet& tables, const ShardEnv& env) {
+  if (!env.comm) throw Error(TQP_ERR_ARG, "execute_sharded: no communicator");
+  Comm& comm = *env.comm;
+  check_inputs(tables);
+  bool any_sharded = false;
+  for (const auto& [name, t] : tables) any_sharded = any_sharded || env.kind_of(name) != SHARD_REPLICATED;
+  shard_stats_ = "{\"path\": \"unsharded\"}";
+  env.bitmap_merges = env.shuffled_tables = env.exchange_bytes = 0;
+  if (!any_sharded || comm.size == 1) return execute(tables);
+  std::string why;
+  bool fact_sharded = false;
+  if (shardable(&why)) {
+    // the fact table of the unit must be sharded (a replicated fact would be
+    // counted once per rank)
+    const auto& fus = units_[0];
+    for (int s = fus.first_step; s <= fus.last_step && !fact_sharded; ++s)
+      for (const auto& in : plan_.steps[s].instrs)
+        if (in.op == Op::LoadColumn && env.kind_of(in.table) != SHARD_REPLICATED) fact_sharded = true;
+  }
+  // phase 1 on every rank, then agree: any rank off the fused path -> gather
+  Partial p;
+  p.env = &env;
+  bool ok = false;
+  if (fact_sharded && shardable(&why)) {
+    cudaEvent_t ev;
+    time_begin(&ev);
+    ok = units_[0].partial(ctx_, tables, &p);
+    if (ok) time_end(units_[0].name + ":partial", ev);
+    else ctx_.give_event(ev);
+  }
+  const std::vector<long long> oks = allgather_host(ctx_, comm, {ok ? 1LL : 0LL, ok ? p.words : 0LL});
+  long long maxw = 0;
+  bool all_ok = true;
+  for (int r = 0; r < comm.size; ++r) {
+    all_ok = all_ok && oks[2 * r] == 1;
+    maxw = std::max(maxw, oks[2 * r + 1]);
+  }
+  auto stats = [&](const char* path) {
+    std::ostringstream os;
+    os << "{\"path\": \"" << path << "\", \"ranks\": " << comm.size << ", \"bitmap_merges\": " << env.bitmap_merges
+       << ", \"shuffled_tables\": " << env.shuffled_tables << ", \"exchange_bytes\": " << env.exchange_bytes << "}";
+    shard_stats_ = os.str();
+  };
+  if (!all_ok) {
+    if (fact_sharded && shardable()) ++fallbacks_;
+    env.gathered = true;
+    stats("gathered");
+    return gather_and_execute(tables, env);
+  }
+  // exchange the partials (padded to the longest), merge on every rank
+  auto pad = ctx_.alloc_bytes(sizeof(long long) * maxw);
+  auto all = ctx_.alloc_bytes(sizeof(long long) * maxw * comm.size);
+  TQP_CUDA(cudaMemcpyAsync(pad->ptr, p.buf->ptr, sizeof(long long) * p.words, cudaMemcpyDeviceToDevice, ctx_.stream));
+  comm.allgather(ctx_, pad->ptr, all->ptr, sizeof(long long) * maxw);
+  env.exchange_bytes += static_cast<long long>(sizeof(long long) * maxw * comm.size);
+  stats("fused");
+  std::vector<PartRef> refs;
+  for (int r = 0; r < comm.size; ++r)
+    refs.push_back({static_cast<const long long*>(all->ptr) + maxw * r, oks[2 * r + 1]});
+  try {
+    Result res = finish(refs);
+    ctx_.sync();
+    return res;
+  } catch (const Error& e) {
+    // merged partials outside the fused contract (e.g. more groups than the
+    // merge keeps): every rank sees the same parts, so every rank gathers
+    if (std::string(e.what()).find("merged partials violate") == std::string::npos) throw;
+    ++fallbacks_;
+    stats("gathered");
+    return gather_and_execute(tables, env);
+  }
 }
 
 Result Executor::finish(const std::vector<PartRef>& parts) {

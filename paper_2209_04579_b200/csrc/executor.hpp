@@ -6,6 +6,7 @@
 
 #include <chrono>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -124,9 +125,25 @@ struct Result {
 };
 
 // Phase-1 state of a sharded run (fused.cu describes the word layout).
+struct Comm;
+// How a sharded run's tables are laid out across the ranks: 0 replicated
+// (every rank holds the whole table), 1 co-partitioned with the fact table
+// (rows cut on the join key's boundaries, e.g. orders with lineitem: joins
+// stay local), 2 row shard (any rows: dimension build sides are exchanged -
+// presence / flag bitmaps all-gathered, or rows re-aligned to the fact shards).
+enum ShardKind : int { SHARD_REPLICATED = 0, SHARD_COPARTITIONED = 1, SHARD_ROWS = 2 };
+struct ShardEnv {
+  Comm* comm = nullptr;
+  std::map<std::string, int> kinds;  // lower-case table name -> ShardKind (default SHARD_REPLICATED)
+  int kind_of(const std::string& table) const;
+  // what the run did (reported by Executor::shard_stats)
+  mutable long long bitmap_merges = 0, shuffled_tables = 0, exchange_bytes = 0;
+  mutable bool gathered = false;
+};
 struct Partial {
   std::shared_ptr<DevBuf> buf;
   int64_t words = 0;
+  const ShardEnv* env = nullptr;  // set by execute_sharded: exchanges inside phase 1
 };
 // a partial as handed back for the merge (device pointer, any owner)
 struct PartRef {
@@ -174,6 +191,15 @@ class Executor {
   // outputs; shardable() says why not otherwise.
   Partial execute_partial(const TableSet& tables);
   Result finish(const std::vector<PartRef>& parts);
+  // One call per rank (every rank gets the whole result): phase 1 with the
+  // build-side exchanges the table layout needs, an all-gather of the
+  // partials, phase 2 on every rank. Plans that cannot shard, or shards that
+  // leave the fused contract, run on the tables gathered to every rank (the
+  // reference's result and errors either way).
+  Result execute_sharded(const TableSet& tables, const ShardEnv& env);
+  // JSON of the last execute_sharded: path ("fused" or "gathered"), build
+  // sides merged as bitmaps, tables re-aligned, bytes this rank exchanged
+  const std::string& shard_stats() const { return shard_stats_; }
   bool shardable(std::string* why = nullptr) const;
   const Plan& plan() const { return plan_; }
   std::string explain() const;
@@ -205,6 +231,7 @@ class Executor {
   void collect_kernel_events();
   bool timing_ = false;
   int64_t fallbacks_ = 0;
+  std::string shard_stats_ = "{}";
   std::map<std::string, UnitTiming> timings_;
 
   Tensor exec_instr(const Instr& in, std::vector<std::optional<Tensor>>& slots, const TableSet& tables);
@@ -213,6 +240,7 @@ class Executor {
   void release_after(int s, std::vector<std::optional<Tensor>>& slots);
   void check_inputs(const TableSet& tables) const;
   Result collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows = true);
+  Result gather_and_execute(const TableSet& tables, const ShardEnv& env);
 
   Ctx& ctx_;
   Plan plan_;

@@ -23,6 +23,7 @@
 #include <set>
 #include <sstream>
 
+#include "comm.hpp"
 #include "executor.hpp"
 #include "fused_kernels.cuh"
 #include "jit.hpp"
@@ -2721,6 +2722,110 @@ bool ensure_dict(Ctx& c, const Column* col, long long rows, long long mn) {
   return true;
 }
 
+// ---- sharded build sides ---------------------------------------------------------
+// per-flag bitmaps of a local build (flag f of slot i where present)
+__global__ void k_flag_bits(const unsigned long long* __restrict__ table, const unsigned* __restrict__ present,
+                            long long range, int nflags, unsigned* __restrict__ out) {
+  const long long nw = (range + 31) / 32;
+  for (long long w = gtid(); w < nw; w += gstride()) {
+    const unsigned p = present[w];
+    unsigned f[kMaxFlags] = {0, 0, 0, 0, 0, 0, 0};
+    for (unsigned m = p; m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const unsigned fl = static_cast<unsigned>(table[w * 32 + b] >> 57);
+      for (int i = 0; i < nflags; ++i) f[i] |= ((fl >> i) & 1u) << b;
+    }
+    for (int i = 0; i < nflags; ++i) out[i * nw + w] = f[i];
+  }
+}
+
+// all-gathered [presence | flag bitmaps] of every rank -> the merged presence
+// bitmap and table entries (1 | flags << 57 where present, 0 elsewhere); a
+// key present on two ranks is a repeated build key (err FR_DUP_KEY)
+__global__ void k_merge_build_bits(const unsigned* __restrict__ all, int nranks, long long nw, int nflags, long long range,
+                                   unsigned* __restrict__ present, unsigned long long* __restrict__ table, long long* err) {
+  const long long per = nw * (1 + nflags);
+  for (long long w = gtid(); w < nw; w += gstride()) {
+    unsigned orp = 0, f[kMaxFlags] = {0, 0, 0, 0, 0, 0, 0};
+    int pops = 0;
+    for (int r = 0; r < nranks; ++r) {
+      const unsigned pr = all[r * per + w];
+      orp |= pr;
+      pops += __popc(pr);
+      for (int i = 0; i < nflags; ++i) f[i] |= all[r * per + (1 + i) * nw + w];
+    }
+    if (pops != __popc(orp)) set_fallback(err, FR_DUP_KEY);
+    present[w] = orp;
+    for (int b = 0; b < 32; ++b) {
+      const long long slot = w * 32 + b;
+      if (slot >= range) break;
+      unsigned long long e = 0;
+      if ((orp >> b) & 1u) {
+        e = 1ULL;
+        for (int i = 0; i < nflags; ++i) e |= static_cast<unsigned long long>((f[i] >> b) & 1u) << (57 + i);
+      }
+      table[slot] = e;
+    }
+  }
+}
+
+__global__ void k_range_mask(const long long* __restrict__ k, long long n, long long lo, long long hi,
+                             uint8_t* __restrict__ out) {
+  for (long long i = gtid(); i < n; i += gstride()) out[i] = k[i] >= lo && k[i] <= hi;
+}
+
+// Re-aligns a row-shard table to the fact shards: every row goes to each rank
+// whose fact shard's probe-key range [lo_r, hi_r] holds its key (a row whose
+// key no fact row can match goes nowhere); the received rows, in source-rank
+// order, make this rank's copy, co-partitioned with its fact rows.
+std::shared_ptr<Table> shuffle_table(Ctx& c, Comm& comm, const Table& t, const std::string& key_col,
+                                     const std::vector<long long>& lo, const std::vector<long long>& hi) {
+  const int G = comm.size;
+  const Column* kc = t.find(key_col);
+  if (!kc || kc->t.dtype != TQP_I64) throw Error(TQP_ERR_EXEC, "shuffle: key column " + key_col + " is not int64");
+  std::vector<Tensor> idx(G);
+  std::vector<long long> cnt(G, 0);
+  for (int r = 0; r < G; ++r) {
+    Tensor mask = c.alloc(TQP_BOOL, t.rows, 1);
+    if (t.rows) {
+      k_range_mask<<<c.grid_for(t.rows, 256), 256, 0, c.stream>>>(kc->t.ptr<long long>(), t.rows, lo[r], hi[r],
+                                                                   mask.ptr<uint8_t>());
+      c.count_launch();
+    }
+    idx[r] = k::compact(c, k::iota(c, t.rows), mask);
+    cnt[r] = idx[r].rows;
+  }
+  const std::vector<long long> m = allgather_host(c, comm, cnt);  // m[src * G + dst]
+  long long total = 0;
+  for (int r = 0; r < G; ++r) total += m[r * G + comm.rank];
+  auto out = std::make_shared<Table>();
+  out->rows = total;
+  for (const Column& col : t.cols) {
+    std::vector<Tensor> parts(G);
+    std::vector<const void*> send(G);
+    std::vector<size_t> sb(G), rb(G);
+    std::vector<void*> recv(G);
+    const size_t rowb = col.t.elem_size() * static_cast<size_t>(col.t.cols);
+    Column nc;
+    nc.name = col.name;
+    nc.type = col.type;
+    nc.t = c.alloc(col.t.dtype, total, col.t.cols);
+    long long off = 0;
+    for (int r = 0; r < G; ++r) {
+      parts[r] = k::gather(c, col.t, idx[r]);
+      send[r] = parts[r].data();
+      sb[r] = rowb * static_cast<size_t>(cnt[r]);
+      recv[r] = static_cast<char*>(nc.t.data()) + rowb * static_cast<size_t>(off);
+      rb[r] = rowb * static_cast<size_t>(m[r * G + comm.rank]);
+      off += m[r * G + comm.rank];
+    }
+    comm.alltoallv(c, send, sb, recv, rb);
+    c.sync();  // the gathered parts stay alive until the copies are done
+    out->cols.push_back(std::move(nc));
+  }
+  return out;
+}
+
 // MODE_HASH table shape: shared-memory records per CTA when the whole code
 // range fits kHashPrivBytes, a direct-address global table (slot = code)
 // while the range is at most 4 slots per fact row (and <= 2^26), otherwise
@@ -2776,6 +2881,22 @@ constexpr size_t kHashPrivBytes = 48 * 1024;
 constexpr unsigned long long kHashDirectMax = 1ULL << 26;
 constexpr size_t kHashMaxBytes = 24ULL << 30;
 
+// re-run options of a fused unit (each set by the check that failed)
+struct RunOpts {
+  bool narrow = false;    // the 8-slot small-group kernel only (after a 4-slot overflow)
+  bool weighted = false;  // repeated build keys: builds sum row weights, the scan counts by multiplicity
+  bool fullsort = false;  // top-k ties: every group, then the reference's sort + limit
+  bool special = false;   // NaN / Inf hash-group values flagged per group
+  int qfrac = 64;         // hash-group fixed-point fraction bits
+  int hlimbs = 2;         // hash-group sums in 2 limbs, or 3
+  bool shuffled = false;  // sharded run: row-shard build sides already realigned to the fact shards
+  RunOpts with_narrow(bool v) const {
+    RunOpts r = *this;
+    r.narrow = v;
+    return r;
+  }
+};
+
 struct Runner {
   PipeDesc P;
   std::shared_ptr<JitMemo> memo = std::make_shared<JitMemo>();
@@ -2784,7 +2905,7 @@ struct Runner {
   std::shared_ptr<const Runner> alt;
 
   bool operator()(Ctx& c, std::vector<std::optional<Tensor>>& slots, const TableSet& tables, UnitPending* pend) const {
-    return run(c, &slots, tables, nullptr, false, pend);
+    return run(c, &slots, tables, nullptr, RunOpts{}, pend);
   }
 
   // po != nullptr: phase 1 of a sharded run (partial state into *po, no slots)
@@ -2796,8 +2917,71 @@ struct Runner {
   // hlimbs: hash-group sums in 2 limbs (re-run with 3 when a group's range
   // check fails)
   bool run(Ctx& c, std::vector<std::optional<Tensor>>* slots, const TableSet& tables, Partial* po,
-           bool narrow = false, UnitPending* pend = nullptr, bool weighted = false, bool fullsort = false,
-           bool special = false, int qfrac = 64, int hlimbs = 2) const {
+           RunOpts o = RunOpts{}, UnitPending* pend = nullptr) const {
+    const bool narrow = o.narrow, weighted = o.weighted, fullsort = o.fullsort, special = o.special;
+    const int qfrac = o.qfrac, hlimbs = o.hlimbs;
+    // sharded phase 1 (execute_sharded): the communicator and table layout
+    const ShardEnv* env = po ? po->env : nullptr;
+    Comm* comm = env ? env->comm : nullptr;
+    auto is_rows = [&](const std::string& t) { return comm && env->kind_of(t) == SHARD_ROWS; };
+    if (comm && !o.shuffled) {
+      // row-shard build sides the scan reads root rows of (the group build,
+      // operand / key columns) are re-aligned to the fact shards by key
+      // range first; the others exchange presence / flag bitmaps below
+      std::vector<std::pair<int, int>> sh;  // (build, fact probe)
+      for (size_t p = 0; p < P.probes.size(); ++p) {
+        const int bi = P.probes[p].build;
+        bool rid = P.builds[bi].assign_groups;
+        for (const auto& a : P.accs)
+          for (const auto& f : a.f) rid = rid || (f.kind != FK_CONST && f.x.probe == static_cast<int>(p));
+        for (const auto& k : P.hkeys) rid = rid || k.probe == static_cast<int>(p);
+        if (rid && is_rows(P.builds[bi].table)) sh.push_back({bi, static_cast<int>(p)});
+      }
+      if (!sh.empty()) {
+        const Table* fact = bind_table(tables, P.fact_table);
+        if (!fact) return nofuse(__LINE__);
+        std::vector<std::pair<const Column*, long long>> fcols;
+        for (auto [bi, p] : sh) {
+          const Column* fc = fact->find(P.probes[p].fact_column);
+          if (!fc || fc->t.dtype != TQP_I64) return nofuse(__LINE__);
+          fcols.push_back({fc, fact->rows});
+        }
+        ensure_key_info(c, fcols, std::vector<bool>(fcols.size(), false));
+        std::vector<long long> mine;
+        for (auto& [fc, rows] : fcols) {
+          mine.push_back(rows ? fc->range->mn : 1);
+          mine.push_back(rows ? fc->range->mx : 0);  // empty shard: an empty range
+        }
+        const std::vector<long long> all = allgather_host(c, *comm, mine);
+        TableSet t2 = tables;
+        ShardEnv env2 = *env;
+        std::vector<std::shared_ptr<Table>> hold;
+        for (size_t i = 0; i < sh.size(); ++i) {
+          const BuildDesc& B = P.builds[sh[i].first];
+          std::vector<long long> lo(comm->size), hi(comm->size);
+          for (int r = 0; r < comm->size; ++r) {
+            lo[r] = all[r * mine.size() + 2 * i];
+            hi[r] = all[r * mine.size() + 2 * i + 1];
+          }
+          const Table* bt = bind_table(tables, B.table);
+          if (!bt) return nofuse(__LINE__);
+          hold.push_back(shuffle_table(c, *comm, *bt, B.key_column, lo, hi));
+          env->shuffled_tables += 1;
+          for (auto& [name, tp] : t2)
+            if (iequals(name, B.table)) tp = hold.back().get();
+          std::string lower = B.table;
+          for (auto& ch : lower) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+          env2.kinds[lower] = SHARD_COPARTITIONED;
+        }
+        const ShardEnv* saved = po->env;
+        po->env = &env2;
+        RunOpts r = o;
+        r.shuffled = true;
+        const bool ok = run(c, slots, t2, po, r, pend);
+        po->env = saved;
+        return ok;
+      }
+    }
     // build sides, children first (builds[] is in post-order by construction)
     // err[0]: precondition flag; err[2]: result rows counted on the device
     HostProf hp;
@@ -2861,6 +3045,40 @@ struct Runner {
       }
     }
     hp.mark("ranges");
+    // row-shard build sides: the global key range and row count (one
+    // all-gather for all of them; every rank then makes the same table shape)
+    std::vector<long long> gn(nb, -1);
+    bool exchange = false;
+    if (comm) {
+      std::vector<long long> mine;
+      for (size_t bi = 0; bi < nb; ++bi) {
+        if (!is_rows(P.builds[bi].table)) continue;
+        if (P.builds[bi].assign_groups) return nofuse(__LINE__);  // (re-aligned above)
+        mine.push_back(bind_table(tables, P.builds[bi].table)->rows);
+        mine.push_back(mm[2 * bi]);
+        mine.push_back(mm[2 * bi + 1]);
+      }
+      if (!mine.empty()) {
+        exchange = true;
+        const std::vector<long long> all = allgather_host(c, *comm, mine);
+        size_t j = 0;
+        for (size_t bi = 0; bi < nb; ++bi) {
+          if (!is_rows(P.builds[bi].table)) continue;
+          long long n = 0, mn = 0x7fffffffffffffffLL, mx = static_cast<long long>(0x8000000000000000ULL);
+          for (int r = 0; r < comm->size; ++r) {
+            const long long* v = &all[r * mine.size() + j];
+            if (v[0] <= 0) continue;
+            n += v[0];
+            mn = std::min(mn, v[1]);
+            mx = std::max(mx, v[2]);
+          }
+          gn[bi] = n;
+          mm[2 * bi] = n ? mn : 0;
+          mm[2 * bi + 1] = n ? mx : 0;
+          j += 3;
+        }
+      }
+    }
     // one zeroed arena for the unit's small state - the error words, every
     // build's presence bitmap and the touched-group bitmap - so one memset
     // replaces one per buffer (each is host time between the unit's kernels)
@@ -2873,12 +3091,13 @@ struct Runner {
     size_t arena = 256, touched_off = 0;
     bool generic_only = weighted;  // the NVRTC kernels address dense, unweighted builds only
     for (size_t bi = 0; bi < nb; ++bi) {
-      const long long n = bind_table(tables, P.builds[bi].table)->rows;
+      const long long n = gn[bi] >= 0 ? gn[bi] : bind_table(tables, P.builds[bi].table)->rows;
       const long long mn = mm[2 * bi], mx = mm[2 * bi + 1];
       const unsigned long long span = static_cast<unsigned long long>(mx) - static_cast<unsigned long long>(mn);
       const bool wide = n && (span > static_cast<unsigned long long>(16LL * n + (1LL << 22)) || span >= (1ULL << 31));
       long long range = n ? static_cast<long long>(span) + 1 : 1;
       if (wide) {
+        if (gn[bi] >= 0) return nofuse(__LINE__);  // a row-shard build side exchanges direct-address bitmaps only
         if (mn == static_cast<long long>(0x8000000000000000ULL)) return nofuse(__LINE__);  // no empty-slot marker
         if (n >= (1LL << 31)) return nofuse(__LINE__);
         long long cap = 1024;
@@ -2909,7 +3128,7 @@ struct Runner {
       BuildSpec bs;
       zero_padding(bs);  // its bytes key the kernel memo
       bs.n = n;
-      bs.kmin = n ? mm[2 * bi] : 0;
+      bs.kmin = (n || gn[bi] > 0) ? mm[2 * bi] : 0;
       bs.range = range;
       auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
       // a filtered build's table is only read where its presence bit is set
@@ -3056,6 +3275,32 @@ struct Runner {
           hp.mark("blaunch");
         }
       }
+      if (gn[bi] >= 0) {
+        // row-shard build side: all-gather every rank's presence and flag
+        // bitmaps over the global key range and merge them into this rank's
+        // bitmap and table entries (the north star's "part build side
+        // all-gathered": 2.5 MB of bits at SF100 instead of the table)
+        const long long nw = (range + 31) / 32;
+        const int nf = bs.nflags;
+        auto mine = c.alloc_bytes(sizeof(unsigned) * nw * (1 + nf));
+        auto all = c.alloc_bytes(sizeof(unsigned) * nw * (1 + nf) * comm->size);
+        TQP_CUDA(cudaMemcpyAsync(mine->ptr, bs.bitmap, sizeof(unsigned) * nw, cudaMemcpyDeviceToDevice, c.stream));
+        if (nf && nw) {
+          k_flag_bits<<<c.grid_for(nw, 256), 256, 0, c.stream>>>(bs.table, bs.bitmap, range, nf,
+                                                                 static_cast<unsigned*>(mine->ptr) + nw);
+          c.count_launch();
+        }
+        comm->allgather(c, mine->ptr, all->ptr, sizeof(unsigned) * nw * (1 + nf));
+        env->bitmap_merges += 1;
+        env->exchange_bytes += static_cast<long long>(sizeof(unsigned) * nw * (1 + nf) * comm->size);
+        if (nw) {
+          k_merge_build_bits<<<c.grid_for(nw, 256), 256, 0, c.stream>>>(static_cast<const unsigned*>(all->ptr), comm->size,
+                                                                        nw, nf, range, bs.bitmap, bs.table, err);
+          c.count_launch();
+        }
+        keep.push_back(mine);
+        keep.push_back(all);
+      }
       Probe pr;
       pr.kmin = bs.kmin;
       pr.range = range;
@@ -3126,7 +3371,7 @@ struct Runner {
     // small-group keys are 1-byte strings; wider ones (or an accumulator
     // count without a small-group kernel) run as the hash-group unit
     if (P.mode == MODE_SMALL && alt && (!ok || !tile_kernel(MODE_SMALL, ps.nacc)))
-      return alt->run(c, slots, tables, po, false, pend, weighted, fullsort, special, qfrac, hlimbs);
+      return alt->run(c, slots, tables, po, o.with_narrow(false), pend);
     if (!ok) return nofuse(__LINE__);
     // probes whose matched root row is read: with repeated build keys such a
     // probe must match exactly one row (checked per row in a weighted run)
@@ -3557,18 +3802,24 @@ struct Runner {
     c.sync();
     hp.mark("sync");
     std::memcpy(herr, c.h_err + Ctx::kPinnedRead, 32);
-    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, true, nullptr, weighted, fullsort, special, qfrac, hlimbs);  // a fifth key in a CTA
+    if (exchange && (herr[0] || herr[1])) {
+      // a re-run would repeat this rank's collectives alone: the caller
+      // agrees across ranks and gathers the tables instead
+      if (po) *po = Partial{};
+      return nofuse(__LINE__);
+    }
+    if (wide && herr[1] && !herr[0]) return run(c, slots, tables, po, o.with_narrow(true));  // a fifth key in a CTA
     if (herr[0] && herr[3] == FR_DUP_KEY && !weighted) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: repeated build keys: unit reruns weighted\n");
-      return run(c, slots, tables, po, narrow, nullptr, true, fullsort, special, qfrac, hlimbs);
+      { RunOpts r = o; r.weighted = true; return run(c, slots, tables, po, r); }
     }
     if (herr[0] && (herr[3] == FR_TOPK_BLOCK || herr[3] == FR_TOPK_FINAL) && !fullsort && P.topk && !po) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: top-k ties overflow: unit reruns with a full group sort\n");
-      return run(c, slots, tables, po, narrow, nullptr, weighted, true, special, qfrac, hlimbs);
+      { RunOpts r = o; r.fullsort = true; return run(c, slots, tables, po, r); }
     }
     if (herr[0] && (herr[3] == FR_LIMB2 || herr[3] == FR_GROUP_VALUE) && P.mode == MODE_HASH && hlimbs == 2) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: 2-limb group sums out of range: unit reruns with 3 limbs\n");
-      return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, special, qfrac, 3);
+      { RunOpts r = o; r.hlimbs = 3; return run(c, slots, tables, po, r); }
     }
     if (herr[0] && herr[3] == FR_Q64_CONVERT && P.mode == MODE_HASH && !po && (!special || qfrac == 64)) {
       // NaN / Inf values: flagged per group; finite values with bits below
@@ -3580,12 +3831,12 @@ struct Runner {
       if (F > 0 && (!special || F > qfrac)) {
         if (std::getenv("TQP_DEBUG_FALLBACK"))
           std::fprintf(stderr, "tqp: NaN/Inf or fine fp64 group values: unit reruns with special flags, %d fraction bits\n", F);
-        return run(c, slots, tables, po, narrow, nullptr, weighted, fullsort, true, F, hlimbs);
+        { RunOpts r = o; r.special = true; r.qfrac = F; return run(c, slots, tables, po, r); }
       }
     }
     if (herr[0] && alt && (P.mode == MODE_SMALL || P.mode == MODE_BUILDGRP)) {
       if (std::getenv("TQP_DEBUG_FALLBACK")) std::fprintf(stderr, "tqp: unit reruns as hash-group (reason %lld)\n", herr[3]);
-      return alt->run(c, slots, tables, po, false, nullptr, weighted, fullsort, special, qfrac, hlimbs);
+      return alt->run(c, slots, tables, po, o.with_narrow(false));
     }
     if (herr[0] && std::getenv("TQP_DEBUG_FALLBACK"))
       std::fprintf(stderr, "tqp: fused unit left the fused path (reason %lld)\n", herr[3]);

@@ -158,6 +158,11 @@ def _load() -> C.CDLL:
         "tqp_executor_execute_partial": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, S]),
         "tqp_executor_finish": (P, [P, C.POINTER(P), C.POINTER(I64_), I, S]),
         "tqp_free_str": (None, [P]),
+        "tqp_comm_nccl_unique_id": (I, [P, S]), "tqp_comm_init_nccl": (P, [P, P, I, I, S]),
+        "tqp_comm_init_local": (I, [I, C.POINTER(P), S]), "tqp_comm_rank": (I, [P]), "tqp_comm_size": (I, [P]),
+        "tqp_comm_kind": (C.c_char_p, [P]), "tqp_comm_free": (None, [P]),
+        "tqp_executor_execute_sharded": (P, [P, P, C.POINTER(C.c_char_p), C.POINTER(P), C.POINTER(I), I, S]),
+        "tqp_executor_shard_stats": (C.c_char_p, [P]),
         "tqp_result_rows": (I64_, [P]), "tqp_result_num_columns": (I, [P]),
         "tqp_result_column_name": (C.c_char_p, [P, I]), "tqp_result_column_type": (I, [P, I]),
         "tqp_result_column": (P, [P, I]), "tqp_result_free": (None, [P]),
@@ -720,6 +725,62 @@ class Result:
         return [(n, t, self.column(i).numpy()) for i, (n, t) in enumerate(self.columns())]
 
 
+SHARD_REPLICATED, SHARD_COPARTITIONED, SHARD_ROWS = 0, 1, 2
+# layout of the generator's sharded TPC-H tables (tqp_gen_table shard/nshards):
+# lineitem and orders cut on order boundaries, part and customer by rows
+TPCH_SHARD_KINDS = {"lineitem": SHARD_COPARTITIONED, "orders": SHARD_COPARTITIONED,
+                    "part": SHARD_ROWS, "customer": SHARD_ROWS}
+
+
+class Comm:
+    """A rank of a communicator for Executor.execute_sharded: NCCL (one
+    process per GPU; `nccl_unique_id()` on one rank, sent to the others by
+    the caller) or an in-process group of thread ranks (`local_group(n)`)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = Status()
+        _check(st, lib.tqp_comm_nccl_unique_id(buf, C.byref(st)) == 0)
+        return buf.raw
+
+    @staticmethod
+    def nccl(uid: bytes, nranks: int, rank: int, ctx: Optional[Context] = None) -> "Comm":
+        ctx = ctx or default_context()
+        idb = C.create_string_buffer(bytes(uid), 128)
+        st = Status()
+        h = lib.tqp_comm_init_nccl(ctx.h, idb, nranks, rank, C.byref(st))
+        _check(st, bool(h))
+        return Comm(h)
+
+    @staticmethod
+    def local_group(n: int) -> list:
+        arr = (C.c_void_p * n)()
+        st = Status()
+        _check(st, lib.tqp_comm_init_local(n, arr, C.byref(st)) == 0)
+        return [Comm(arr[i]) for i in range(n)]
+
+    @property
+    def rank(self) -> int:
+        return lib.tqp_comm_rank(self.h)
+
+    @property
+    def size(self) -> int:
+        return lib.tqp_comm_size(self.h)
+
+    @property
+    def kind(self) -> str:
+        return lib.tqp_comm_kind(self.h).decode()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.tqp_comm_free(self.h)
+            self.h = None
+
+
 class Executor:
     """tensql::Executor over device tables; fuse=False runs one device kernel
     per instruction (the reference's dispatch loop, executor.cpp:378-408)."""
@@ -811,6 +872,23 @@ class Executor:
         h = lib.tqp_executor_finish(self.h, pa, wa, n, C.byref(st))
         _check(st, bool(h))
         return Result(h, self.ctx)
+
+    def execute_sharded(self, tables: Mapping[str, Table], comm: Comm, kinds: Optional[Mapping[str, int]] = None) -> "Result":
+        """One call per rank (tqp_executor_execute_sharded); every rank gets
+        the whole result. kinds: table -> SHARD_* (default TPCH_SHARD_KINDS,
+        replicated for other names)."""
+        kinds = kinds if kinds is not None else TPCH_SHARD_KINDS
+        cn, th, n = self._args(tables)
+        ka = (C.c_int * max(1, n))(*[int(kinds.get(name.lower(), SHARD_REPLICATED)) for name in tables])
+        st = Status()
+        h = lib.tqp_executor_execute_sharded(self.h, comm.h, cn, th, ka, n, C.byref(st))
+        _check(st, bool(h))
+        return Result(h, self.ctx)
+
+    def shard_stats(self) -> dict:
+        """What the last execute_sharded did (path, bitmap merges, re-aligned
+        tables, bytes exchanged by this rank)."""
+        return json.loads(lib.tqp_executor_shard_stats(self.h).decode())
 
     def profile_execute(self, tables: Mapping[str, Table]) -> Tuple[Result, list]:
         cn, th, n = self._args(tables)
