@@ -264,8 +264,10 @@ def main():
     seed = 7
     # weak scaling: the dataset is SF(sf x N); lineitem and orders are cut on order
     # boundaries (co-partitioned, so Q3's groups stay on one rank); part and
-    # customer are whole on every rank (their builds are rebuilt locally)
-    sharded = ("lineitem", "orders")
+    # customer are cut by rows (row shards: their build sides are exchanged as
+    # presence / flag bitmaps through the library's NCCL communicator). The
+    # shared-GPU functional mode keeps them whole (the torch/gloo exchange).
+    sharded = ("lineitem", "orders") if share else ("lineitem", "orders", "customer", "part")
     tables = {n: tqp.Table.generate(n, args.sf * world, seed,
                                     shard=rank if n in sharded else 0, nshards=world if n in sharded else 1, ctx=ctx)
               for n in ("lineitem", "orders", "customer", "part")}
@@ -283,7 +285,17 @@ def main():
         # CUDA events (the roofline kernel); per-query latencies and the
         # per-unit breakdown come from separate passes after it
         execs[q].set_timing("scan")
-    if dist:
+    comm = None
+    if dist and not share:
+        # NCCL inside the library (tqp_comm_init_nccl): the unique id travels
+        # over torch.distributed, every exchange runs on the library's stream
+        uid = [tqp.Comm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = tqp.Comm.nccl(uid[0], world, rank, ctx)
+
+        def run_query(q, tabs):
+            return execs[q].execute_sharded(tabs, comm, tqp.TPCH_SHARD_KINDS)
+    elif dist:
         from paper_2209_04579_b200.distributed import execute_sharded
 
         def run_query(q, tabs):
@@ -425,11 +437,14 @@ def main():
                        "cold_ms": cold,
                        "fused": not args.no_fuse,
                        "l2": "inputs larger than L2 (1.9-2.5 GB per query vs 126 MB)",
-                       "parallelism": (f"lineitem+orders cut on order boundaries x{world}, part/customer "
-                                       f"whole per rank, partials all-gathered over NCCL" if world > 1
-                                       else "single GPU")},
+                       "parallelism": ((f"lineitem+orders cut on order boundaries x{world}, part/customer row "
+                                        f"shards (build bitmaps all-gathered), partials all-gathered; NCCL in "
+                                        f"the library (tqp_executor_execute_sharded)") if world > 1 and not share
+                                       else (f"x{world} ranks sharing cuda:0 (functional check, gloo)" if world > 1
+                                             else "single GPU"))},
             "queries": queries, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks.summary(), "gpu_launches": launches, "fused_fallbacks": fallbacks, "csv_load": csv_leg,
+            "shard_stats": {q: execs[q].shard_stats() for q in QUERIES} if comm is not None else None,
             "cold_first_execution_ms": cold,
         }
         line.update(extra)
