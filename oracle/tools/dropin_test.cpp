@@ -16,6 +16,7 @@
 #include "tensql/plan_json.hpp"
 #include "tensql/sql.hpp"
 #include "tensql_b200_executor.hpp"
+#include "tensql_sql_ext.hpp"
 #include "tpch_tables.hpp"
 
 using namespace tensql;
@@ -94,6 +95,20 @@ int main(int argc, char** argv) {
     TableSet tables = tqp_oracle::tpch_tables(sf, 7);
     for (const std::string q : {"q6", "q14", "q1"}) check(q, sql::parse_and_plan(read_file(qdir + "/" + q + ".sql"), cat), cat, tables);
     check("q3", plan_from_json(read_file(qdir + "/q3.json")), cat, tables);
+    // the SQL frontend extension (ORDER BY, n-way joins): Q3 written in SQL,
+    // and ORDER BY over grouped / joined statements, through the same path
+    check("q3.sql (tensql_sql_ext)", tqp_sqlx::parse_and_plan(read_file(qdir + "/q3.sql"), cat), cat, tables);
+    for (const char* q : {
+             "SELECT l_returnflag, l_linestatus, SUM(l_quantity) AS q, COUNT(*) AS n FROM lineitem GROUP BY "
+             "l_returnflag, l_linestatus ORDER BY q DESC",
+             "SELECT c_mktsegment, SUM(l_extendedprice * (1 - l_discount)) AS rev, COUNT(*) AS n FROM customer JOIN "
+             "orders ON o_custkey = c_custkey JOIN lineitem ON l_orderkey = o_orderkey WHERE o_orderdate < DATE "
+             "'1995-03-15' GROUP BY c_mktsegment ORDER BY rev DESC",
+             "SELECT o_orderkey, o_orderdate FROM orders JOIN customer ON o_custkey = c_custkey WHERE c_mktsegment = "
+             "'MACHINERY' ORDER BY o_orderdate DESC, o_orderkey LIMIT 20",
+         }) {
+      check(std::string("sqlx: ") + q, tqp_sqlx::parse_and_plan(q, cat), cat, tables);
+    }
     // ad-hoc SQL the reference frontend accepts, through the same path
     for (const char* q : {
              "SELECT l_returnflag, COUNT(*) AS n, SUM(l_quantity) AS q FROM lineitem WHERE l_discount > 0.05 GROUP BY l_returnflag",
