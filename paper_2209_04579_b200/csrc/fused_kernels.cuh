@@ -335,7 +335,8 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = static_cast<int>(it % nst);
         if (it >= nst) mbar_wait(&empty[st], static_cast<unsigned>(((it / nst) - 1) & 1));
-        issue_tile(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
+        if (MODE == MODE_HASH && t.evict_first) issue_tile<true>(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
+        else issue_tile(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
       }
     }
   } else {

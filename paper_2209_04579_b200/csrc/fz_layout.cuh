@@ -715,6 +715,10 @@ __device__ __forceinline__ void red_add_hint(unsigned long long* p, unsigned lon
   asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
+// HINT: the copies carry an L2 evict-first policy (hash-group scans, which
+// keep their table resident under the stream); a compile-time choice, so the
+// other pipelines' producer loop is exactly the unhinted one
+template <bool HINT = false>
 __device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* stage, unsigned long long* bar,
                                            long long tile) {
   const long long row0 = tile * t.rows;
@@ -723,10 +727,9 @@ __device__ __forceinline__ void issue_tile(const TileSpec& t, unsigned char* sta
   unsigned total = 0;
   for (int c = 0; c < t.ncols; ++c) total += static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
   mbar_expect_tx(bar, total);
-  const unsigned long long pol = t.evict_first ? l2_policy_evict_first() : 0ULL;
   for (int c = 0; c < t.ncols; ++c) {
     unsigned bytes = static_cast<unsigned>((rows * t.col_w[c] + 15) & ~15LL);
-    if (t.evict_first) bulk_g2s_hint(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar, pol);
+    if constexpr (HINT) bulk_g2s_hint(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar, l2_policy_evict_first());
     else bulk_g2s(stage + t.col_off[c], t.col_ptr[c] + row0 * t.col_w[c], bytes, bar);
   }
 }
