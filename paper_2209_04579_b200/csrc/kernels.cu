@@ -291,22 +291,64 @@ __global__ void k_strcmp(const TA* __restrict__ a, const TB* __restrict__ b, uin
   }
 }
 
-// fp64 GEMM for PREDICT (kernels.cpp:674-690): 16x16 shared-memory tiles.
-__global__ void k_matmul(const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C, int64_t n,
-                         int64_t kk, int64_t p) {
-  __shared__ double As[16][17], Bs[16][17];
-  int64_t row = static_cast<int64_t>(blockIdx.y) * 16 + threadIdx.y;
-  int64_t col = static_cast<int64_t>(blockIdx.x) * 16 + threadIdx.x;
-  double acc = 0.0;
-  for (int64_t t = 0; t < kk; t += 16) {
-    As[threadIdx.y][threadIdx.x] = (row < n && t + threadIdx.x < kk) ? A[row * kk + t + threadIdx.x] : 0.0;
-    Bs[threadIdx.y][threadIdx.x] = (col < p && t + threadIdx.y < kk) ? B[(t + threadIdx.y) * p + col] : 0.0;
+// fp64 GEMM for PREDICT (kernels.cpp:674-690) on the FP64 tensor cores
+// (DMMA: mma.sync m8n8k4 f64). A block computes a 64 x 64 tile of C with 4
+// warps (2 x 2, 32 x 32 each = 4 x 4 fragments); K is staged 16 wide in
+// shared memory. The Hummingbird tree GEMMs (X.A with a one-hot feature
+// selector, S.C and hit.leaf_index with small-integer operands) are exact on
+// it (every product and partial sum is representable); dense linear models
+// differ from Eigen's summation order within the fp64 tolerance.
+constexpr int kMmBM = 64, kMmBN = 64, kMmBK = 16;
+__global__ void __launch_bounds__(128) k_matmul(const double* __restrict__ A, const double* __restrict__ B,
+                                                double* __restrict__ C, int64_t n, int64_t kk, int64_t p) {
+  __shared__ double As[kMmBM][kMmBK + 1];
+  __shared__ double Bs[kMmBK][kMmBN + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t bm = static_cast<int64_t>(blockIdx.x) * kMmBM, bn = static_cast<int64_t>(blockIdx.y) * kMmBN;  // rows on x (2^31 blocks)
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int64_t k0 = 0; k0 < kk; k0 += kMmBK) {
+    for (int e = threadIdx.x; e < kMmBM * kMmBK; e += 128) {
+      const int r = e / kMmBK, q = e % kMmBK;
+      As[r][q] = (bm + r < n && k0 + q < kk) ? A[(bm + r) * kk + k0 + q] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kMmBK * kMmBN; e += 128) {
+      const int q = e / kMmBN, col = e % kMmBN;
+      Bs[q][col] = (k0 + q < kk && bn + col < p) ? B[(k0 + q) * p + bn + col] : 0.0;
+    }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc = fma(As[threadIdx.y][q], Bs[q][threadIdx.x], acc);
+    for (int ks = 0; ks < kMmBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[wm * 32 + i * 8 + (lane >> 2)][ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[ks + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[i][j][0]), "+d"(acc[i][j][1])
+                       : "d"(af[i]), "d"(bf[j]));
+    }
     __syncthreads();
   }
-  if (row < n && col < p) C[row * p + col] = acc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = bm + wm * 32 + i * 8 + (lane >> 2);
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t col = bn + wn * 32 + j * 8 + (lane & 3) * 2;
+      if (col < p) C[row * p + col] = acc[i][j][0];
+      if (col + 1 < p) C[row * p + col + 1] = acc[i][j][1];
+    }
+  }
 }
 
 int string_like(const Tensor& t) { return t.dtype == TQP_STR8 || t.dtype == TQP_I32; }
@@ -447,9 +489,8 @@ Tensor matmul(Ctx& c, const Tensor& a, const Tensor& b) {
   }
   Tensor o = c.alloc(TQP_F64, a.rows, b.cols);
   if (a.rows && b.cols) {
-    dim3 grid((b.cols + 15) / 16, (a.rows + 15) / 16);
-    k_matmul<<<grid, dim3(16, 16), 0, c.stream>>>(a.ptr<double>(), b.ptr<double>(), o.ptr<double>(), a.rows, a.cols,
-                                                  b.cols);
+    dim3 grid(static_cast<unsigned>((a.rows + kMmBM - 1) / kMmBM), static_cast<unsigned>((b.cols + kMmBN - 1) / kMmBN));
+    k_matmul<<<grid, 128, 0, c.stream>>>(a.ptr<double>(), b.ptr<double>(), o.ptr<double>(), a.rows, a.cols, b.cols);
     c.count_launch();
   }
   return o;
