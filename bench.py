@@ -418,6 +418,7 @@ def main():
         extra["q6_sf1"] = run_q6_sf1(args, tqp, torch, ctx, stream)
         extra["per_instruction"] = run_per_instruction(args, tqp, torch, ctx, stream, tables, L)
         extra["hash_group"] = run_hash_group(args, tqp, torch, ctx, stream, tables, L)
+        extra["dropin_e2e"] = run_dropin_leg()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -542,6 +543,25 @@ def run_hash_group(args, tqp, torch, ctx, stream, tables, L):
             "scan_kernel_hbm_frac": (b / (scan_ms / 1e3) / 1e9 / peak) if scan_ms else None,
             "units": units, "explain": ex.explain(), "cold_ms": cold, "fallbacks": ex.fallbacks,
             "per_instruction_ms": ms_nf, "speedup_vs_per_instruction": ms_nf / ms}
+
+
+def run_dropin_leg(sf: float = 1.0):
+    """The path a tensql caller gets, timed from C++ (oracle/tools/
+    dropin_bench.cpp): host EncodedTables in the reference's layout ->
+    tqp_integration::B200Executor::execute(TableSet) (columns the plan loads,
+    page-locked in place once and DMA'd every call; Utf8 narrowed on the host)
+    -> EncodedTable, median wall ms per query, beside tensql::Executor (par) on
+    the same tables and host cores."""
+    exe = ROOT / "oracle" / "_ref" / "tqp_dropin_bench"
+    if not exe.exists():
+        return {"unavailable": "oracle/_ref/tqp_dropin_bench not built"}
+    r = subprocess.run([str(exe), "--sf", str(sf), "--reps", "5"], capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"error": r.stderr[-500:]}
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    d["path"] = ("host EncodedTable (reference layout) -> B200Executor::execute(TableSet): H2D of the loaded columns "
+                 "(registered host memory), device run, D2H of the result; wall clock per query")
+    return d
 
 
 def run_csv_leg(tqp, ctx, sf):

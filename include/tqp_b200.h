@@ -211,6 +211,11 @@ tqp_table* tqp_table_create(tqp_ctx* ctx, tqp_status* st);
 /* Adds a column; takes a reference to t (the caller may free its handle). */
 int tqp_table_add_column(tqp_table* tab, const char* name, int logical_type, tqp_tensor* t,
                          tqp_status* st);
+/* A column the plan's input schema names (the reference binds every catalog
+ * column, executor.cpp:355-371) but no LoadColumn reads: name, logical type
+ * and row count only, no device data (a drop-in upload skips the bytes). A
+ * plan that does load it fails with an ExecError. */
+int tqp_table_declare_column(tqp_table* tab, const char* name, int logical_type, int64_t rows, tqp_status* st);
 int64_t tqp_table_rows(const tqp_table* tab);
 int tqp_table_num_columns(const tqp_table* tab);
 const char* tqp_table_column_name(const tqp_table* tab, int i);

@@ -55,6 +55,7 @@ std::string diff(const EncodedTable& a, const EncodedTable& b) {
 }
 
 int failures = 0;
+int g_gpus = 1;  // --gpus: ranks of the sharded drop-in executor
 
 void check(const std::string& name, const PlanPtr& plan, const Catalog& cat, const TableSet& tables) {
   OperatorPlan op = plan_operators(optimize(plan, cat), cat);
@@ -66,17 +67,28 @@ void check(const std::string& name, const PlanPtr& plan, const Catalog& cat, con
   } catch (const std::exception& e) {
     want_err = e.what();
   }
-  for (bool fuse : {true, false}) {
+  for (int mode = 0; mode < 3; ++mode) {
+    // 0 fused, 1 per instruction, 2 fused over g_gpus ranks (row shards of
+    // every table, tqp_executor_execute_sharded), when g_gpus > 1
+    if (mode == 2 && g_gpus < 2) break;
+    const bool fuse = mode != 1;
     try {
-      tqp_integration::B200Executor ex(op, fuse);
-      got = ex.execute(tables);
+      tqp_integration::B200Executor ex(op, mode == 2 ? g_gpus : 1, fuse);
+      if (mode == 0) {
+        ProfileTrace tr;
+        got = ex.profile_execute(tables, tr);
+        if (tr.backend != "b200" || tr.operators.empty()) throw std::runtime_error("profile_execute left the trace empty");
+      } else {
+        got = ex.execute(tables);
+      }
       got_err.clear();
     } catch (const std::exception& e) {
       got_err = e.what();
     }
     std::string d = !want_err.empty() || !got_err.empty() ? (want_err == got_err ? "" : "error '" + got_err + "' vs '" + want_err + "'")
                                                           : diff(got, want);
-    std::printf("%s %s [%s]%s%s\n", d.empty() ? "PASS" : "FAIL", name.c_str(), fuse ? "fused" : "per-instruction",
+    std::printf("%s %s [%s]%s%s\n", d.empty() ? "PASS" : "FAIL", name.c_str(),
+                mode == 2 ? ("fused x" + std::to_string(g_gpus) + " ranks").c_str() : fuse ? "fused" : "per-instruction",
                 d.empty() ? "" : ": ", d.c_str());
     if (!d.empty()) ++failures;
   }
@@ -88,6 +100,7 @@ int main(int argc, char** argv) {
   std::map<std::string, std::string> fl;
   for (int i = 1; i + 1 < argc; i += 2) fl[argv[i]] = argv[i + 1];
   const double sf = fl.count("--sf") ? std::stod(fl["--sf"]) : 0.01;
+  g_gpus = fl.count("--gpus") ? std::stoi(fl["--gpus"]) : 1;
   std::string exe = argv[0];
   const std::string qdir = fl.count("--qdir") ? fl["--qdir"] : exe.substr(0, exe.rfind('/')) + "/queries";
   try {

@@ -6,6 +6,8 @@
 #include <cstring>
 #include <sstream>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "comm.hpp"
 #include "executor.hpp"
@@ -165,8 +167,23 @@ tqp_tensor* tqp_tensor_from_host_utf8_i32(tqp_ctx* ctx, int64_t rows, int64_t co
                                           tqp_status* st) {
   return guard(st, [&] {
     Ctx& c = C_(ctx);
-    Tensor wide = upload(c, TQP_I32, rows, cols, host);
-    return wrap(k::utf8_i32_to_str8(c, wide));
+    if (rows < 0 || cols < 1) kernel_fail("tensor: buffer length does not match shape");
+    // narrowed to 1 byte per UTF-8 byte on the host (the reference keeps one
+    // Int32 per byte, columnar.cpp:161-175): a quarter of the PCIe bytes;
+    // large columns are narrowed by several host threads
+    const int64_t n = rows * cols;
+    std::vector<uint8_t> bytes(static_cast<size_t>(n));
+    const int nt = n >= (int64_t{1} << 22) ? static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency()))) : 1;
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+        for (int64_t i = lo; i < hi; ++i) bytes[static_cast<size_t>(i)] = static_cast<uint8_t>(host[i]);
+      });
+    for (auto& x : th) x.join();
+    Tensor o = upload(c, TQP_STR8, rows, cols, bytes.data());
+    c.sync();  // `bytes` is a pageable host buffer: the copy has read it
+    return wrap(std::move(o));
   });
 }
 
@@ -343,6 +360,24 @@ int tqp_table_add_column(tqp_table* tab, const char* name, int lt, tqp_tensor* t
     return 0;
   });
 }
+int tqp_table_declare_column(tqp_table* tab, const char* name, int lt, int64_t rows, tqp_status* st) {
+  return guard(st, [&] {
+    if (!tab || !name) throw Error(TQP_ERR_ARG, "null table or name");
+    if (lt < TQP_LT_INT64 || lt > TQP_LT_BOOL) throw Error(TQP_ERR_ARG, "bad logical type");
+    if (tab->t.find(name)) throw Error(TQP_ERR_ENCODING, std::string("table: duplicate column name '") + name + "'");
+    if (!tab->t.cols.empty() && rows != tab->t.rows)
+      throw Error(TQP_ERR_ENCODING, std::string("table: column '") + name + "' has " + std::to_string(rows) +
+                                        " rows, expected " + std::to_string(tab->t.rows));
+    Tensor x;  // no device buffer: a column the plan binds but never loads
+    x.dtype = physical_dtype(lt);
+    x.rows = rows;
+    x.cols = 1;
+    if (tab->t.cols.empty()) tab->t.rows = rows;
+    tab->t.cols.push_back({name, lt, x});
+    return 0;
+  });
+}
+
 int64_t tqp_table_rows(const tqp_table* tab) { return tab ? tab->t.rows : -1; }
 int tqp_table_num_columns(const tqp_table* tab) { return tab ? static_cast<int>(tab->t.cols.size()) : -1; }
 const char* tqp_table_column_name(const tqp_table* tab, int i) { return tab->t.cols.at(i).name.c_str(); }

@@ -201,6 +201,8 @@ Tensor Executor::exec_instr(const Instr& in, std::vector<std::optional<Tensor>>&
       if (!t) exec_fail("no input table named '" + in.table + "'");
       const Column* col = t->find(in.column);
       if (!col) throw Error(TQP_ERR_ENCODING, "table: no column named '" + in.column + "'");
+      if (!col->t.buf && col->t.size() > 0)  // tqp_table_declare_column: bound, never uploaded
+        exec_fail("column '" + in.column + "' of table '" + in.table + "' was declared without data");
       return col->t;
     }
     case Op::ConstTensor: return in.constant;
@@ -521,6 +523,12 @@ Result Executor::gather_and_execute(const TableSet& tables, const ShardEnv& env)
     auto g = std::make_shared<Table>();
     g->rows = total;
     for (const Column& col : t->cols) {
+      if (!col.t.buf) {  // declared without data (never loaded): declared here too
+        Column nc = col;
+        nc.t.rows = total;
+        g->cols.push_back(std::move(nc));
+        continue;
+      }
       const size_t rowb = col.t.elem_size() * static_cast<size_t>(col.t.cols);
       auto pad = ctx_.alloc_bytes(std::max<size_t>(1, rowb * mx));
       auto all = ctx_.alloc_bytes(std::max<size_t>(1, rowb * mx * comm.size));

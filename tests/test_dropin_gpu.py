@@ -14,7 +14,7 @@ BIN = ROOT / "oracle" / "_ref" / "tqp_dropin_test"
 
 def test_reference_frontend_to_b200_executor():
     assert BIN.exists(), "build it with `make -C oracle` (needs /root/reference at build time)"
-    r = subprocess.run([str(BIN), "--sf", "0.01"], capture_output=True, text=True, timeout=600)
+    r = subprocess.run([str(BIN), "--sf", "0.01", "--gpus", "2"], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
