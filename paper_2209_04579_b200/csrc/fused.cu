@@ -2550,14 +2550,20 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
 // again; any difference - or a padding byte that differs - regenerates.
 struct JitMemo {
   std::mutex mu;
-  std::map<int, std::pair<std::string, const void*>> last;  // site -> (argument bytes, kernel)
+  struct Hit {
+    std::string key;  // argument bytes
+    const void* fn;
+    long long epoch;  // jit_epoch() when stored: an unloaded library invalidates it
+  };
+  std::map<int, Hit> last;  // site -> last kernel
   template <typename Make>
   const void* get(int site, const std::string& key, Make&& make) {
     std::lock_guard<std::mutex> l(mu);
     auto it = last.find(site);
-    if (it != last.end() && it->second.first == key) return it->second.second;
+    if (it != last.end() && it->second.key == key && it->second.epoch == jit_epoch()) return it->second.fn;
+    const long long e = jit_epoch();
     const void* fn = make();
-    last[site] = {key, fn};
+    last[site] = {key, fn, e == jit_epoch() ? e : -1};
     return fn;
   }
 };

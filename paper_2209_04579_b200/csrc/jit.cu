@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <atomic>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -25,10 +26,25 @@ namespace {
 // kJitHeaderNames / kJitHeaderSrc / kJitHeaderCount
 #include "jit_embed.inc"
 
+// Compiled kernels, least-recently-used bounded: a long-lived process that
+// keeps meeting new predicates (every literal is part of a kernel's source)
+// would otherwise keep every code object loaded. At the bound (TQP_JIT_CACHE
+// libraries, default 512) the least recently requested library is unloaded
+// after a device synchronisation (no launch of it can be in flight); the
+// epoch counter tells kernel-pointer caches (the per-unit memo, Ctx's
+// attribute caches) to drop what they hold.
+struct Entry {
+  const void* fn = nullptr;
+  cudaLibrary_t lib = nullptr;
+  unsigned long long tick = 0;
+};
 struct Cache {
   std::mutex mu;
-  std::map<std::string, const void*> kernels;  // key: entry + '\0' + source
+  std::map<std::string, Entry> kernels;  // key: entry + '\0' + source
+  unsigned long long tick = 0;
+  size_t cap = 0;
 };
+std::atomic<long long> g_epoch{0};
 
 Cache& cache() {
   static Cache c;
@@ -97,7 +113,23 @@ const void* jit_kernel(const std::string& src, const char* entry) {
   std::lock_guard<std::mutex> lock(c.mu);
   const std::string key = std::string(entry) + '\0' + src;
   auto it = c.kernels.find(key);
-  if (it != c.kernels.end()) return it->second;
+  if (it != c.kernels.end()) {
+    it->second.tick = ++c.tick;
+    return it->second.fn;
+  }
+  if (!c.cap) {
+    const char* e = std::getenv("TQP_JIT_CACHE");
+    c.cap = e && std::atoi(e) > 0 ? static_cast<size_t>(std::atoi(e)) : 512;
+  }
+  while (c.kernels.size() >= c.cap) {
+    auto lru = c.kernels.begin();
+    for (auto j = c.kernels.begin(); j != c.kernels.end(); ++j)
+      if (j->second.tick < lru->second.tick) lru = j;
+    TQP_CUDA(cudaDeviceSynchronize());
+    TQP_CUDA(cudaLibraryUnload(lru->second.lib));
+    c.kernels.erase(lru);
+    ++g_epoch;
+  }
 
   const Nvrtc& api = nvrtc();
   nvrtcProgram prog;
@@ -125,9 +157,11 @@ const void* jit_kernel(const std::string& src, const char* entry) {
   cudaKernel_t k;
   TQP_CUDA(cudaLibraryGetKernel(&k, lib, entry));
   const void* fn = reinterpret_cast<const void*>(k);
-  c.kernels[key] = fn;  // libraries live for the process
+  c.kernels[key] = Entry{fn, lib, ++c.tick};
   return fn;
 }
+
+long long jit_epoch() { return g_epoch.load(); }
 
 int jit_compiled_count() {
   Cache& c = cache();

@@ -12,8 +12,12 @@ namespace tqp {
 // (TQP_ERR_CUDA) with the NVRTC log on failure.
 const void* jit_kernel(const std::string& src, const char* entry);
 
-// Number of distinct kernels compiled in this process (tests/diagnostics).
+// Number of kernels currently loaded (at most TQP_JIT_CACHE, default 512).
 int jit_compiled_count();
+
+// Incremented whenever a least-recently-used kernel library is unloaded:
+// holders of kernel pointers re-fetch (jit_kernel) when it changed.
+long long jit_epoch();
 
 // Version of the NVRTC the kernels are compiled with (major * 1000 + minor * 10).
 int jit_nvrtc_version();

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "device.cuh"
+#include "jit.hpp"
 
 namespace tqp {
 
@@ -71,6 +72,15 @@ int physical_dtype(int lt) {
     case TQP_LT_BOOL: return TQP_BOOL;
   }
   return -1;
+}
+
+void Ctx::jit_epoch_check() {
+  const long long e = jit_epoch();
+  if (e == jit_epoch_seen_) return;
+  jit_epoch_seen_ = e;
+  static_smem_.clear();
+  occupancy_.clear();
+  smem_set.clear();
 }
 
 std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {

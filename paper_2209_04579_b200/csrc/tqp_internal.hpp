@@ -195,7 +195,12 @@ struct Ctx {
     if (smem_optin_ < 0) TQP_CUDA(cudaDeviceGetAttribute(&smem_optin_, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     return smem_optin_;
   }
+  // the kernel-pointer caches below drop their entries when a JIT library
+  // was unloaded (jit_epoch): a new kernel may reuse an old handle
+  long long jit_epoch_seen_ = 0;
+  void jit_epoch_check();
   size_t static_smem(const void* kernel) {
+    jit_epoch_check();
     auto it = static_smem_.find(kernel);
     if (it != static_smem_.end()) return it->second;
     cudaFuncAttributes fa{};
@@ -204,6 +209,7 @@ struct Ctx {
   }
   std::map<std::pair<const void*, int>, int> occupancy_;
   int blocks_per_sm(const void* kernel, int threads) {  // no dynamic shared memory
+    jit_epoch_check();
     auto key = std::make_pair(kernel, threads);
     auto it = occupancy_.find(key);
     if (it != occupancy_.end()) return it->second;
@@ -214,6 +220,7 @@ struct Ctx {
   // cudaFuncAttributeMaxDynamicSharedMemorySize, set once per (kernel, size)
   std::map<const void*, int> smem_set;
   cudaError_t ensure_smem(const void* kernel, int bytes) {
+    jit_epoch_check();
     auto it = smem_set.find(kernel);
     if (it != smem_set.end() && it->second >= bytes) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
