@@ -493,10 +493,11 @@ def run_per_instruction(args, tqp, torch, ctx, stream, tables, L):
     for q in QUERIES:
         plan = json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text())
         execs[q] = tqp.Executor(plan, fuse=False, ctx=ctx)
-    for q in QUERIES:
-        execs[q].execute(tables)
+    for _ in range(3):  # the pool grows to the path's working set during the first runs
+        for q in QUERIES:
+            execs[q].execute(tables)
     ctx.sync()
-    ms = timed_queries(torch, stream, lambda q: execs[q].execute(tables), list(QUERIES), 3)
+    ms = timed_queries(torch, stream, lambda q: execs[q].execute(tables), list(QUERIES), 5)
     launches0 = ctx.launches
     for q in QUERIES:
         execs[q].execute(tables)
