@@ -17,6 +17,8 @@
 #include <string>
 #include <vector>
 
+#include <type_traits>
+
 #include "device.cuh"
 
 namespace tqp {
@@ -272,6 +274,32 @@ __global__ void k_long_chunks(const T* __restrict__ v, const int64_t* __restrict
   P* sp = reinterpret_cast<P*>(smem_raw);
   int64_t a = item_lo[blockIdx.x], b = item_hi[blockIdx.x];
   int nwarps = blockDim.x >> 5, warp = threadIdx.x >> 5;
+  if constexpr (std::is_same_v<T, double> && OP == TQP_SUM) {
+    // fp64 sums need no sequential order (the reference's own par backend
+    // sums 4096-row chunks, backend.cpp:139-160): coalesced two-row loads,
+    // per-thread sums, a fixed xor tree per warp and the warps in order -
+    // deterministic run to run, within the fp64 tolerance of `ref`
+    double sacc = 0.0;
+    const int64_t a2 = (a + 1) & ~int64_t(1);
+    if (threadIdx.x == 0 && a2 > a) sacc = v[a];
+    const double2* v2 = reinterpret_cast<const double2*>(v + a2);
+    const int64_t np = (b - a2) / 2;
+    for (int64_t i = threadIdx.x; i < np; i += blockDim.x) {
+      const double2 x = __ldg(v2 + i);
+      sacc = __dadd_rn(sacc, __dadd_rn(x.x, x.y));
+    }
+    if (threadIdx.x == 0 && a2 + 2 * np < b) sacc = __dadd_rn(sacc, v[b - 1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc = __dadd_rn(sacc, __shfl_xor_sync(0xffffffffu, sacc, o));
+    if ((threadIdx.x & 31) == 0) sp[warp] = P{sacc};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      P acc = sp[0];
+      for (int w = 1; w < nwarps; ++w) acc = A::comb(acc, sp[w]);
+      parts[blockIdx.x] = acc;
+    }
+    return;
+  }
   int64_t len = b - a, per = (len + nwarps - 1) / nwarps;
   int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
   if (wa > wb) wa = wb;
@@ -285,87 +313,70 @@ __global__ void k_long_chunks(const T* __restrict__ v, const int64_t* __restrict
   }
 }
 
+// One warp per long segment: lane l folds a contiguous run of the segment's
+// chunk partials in order, then the lanes combine in lane order (the partial
+// monoids are associative; the int64 sum's prefix bounds need the order)
 template <typename T, int OP>
 __global__ void k_long_finish(const typename Acc<T, OP>::P* __restrict__ parts, const int64_t* __restrict__ seg,
                               const int64_t* __restrict__ first_item, const int64_t* __restrict__ nitems, int64_t nlong,
                               T* __restrict__ out, long long* err) {
   using A = Acc<T, OP>;
-  for (int64_t q = gtid(); q < nlong; q += gstride()) {
-    auto p = parts[first_item[q]];
-    for (int64_t k = 1; k < nitems[q]; ++k) p = A::comb(p, parts[first_item[q] + k]);
-    if constexpr (OP == TQP_SUM) {
-      write_result<T, OP>(out, seg[q], p, err);
-    } else {
-      write_mm(out, seg[q], p);
+  using P = typename A::P;
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = gtid() >> 5; q < nlong; q += gstride() >> 5) {
+    const int64_t f = first_item[q], m = nitems[q];
+    const int64_t per = (m + 31) / 32;
+    const int64_t a = lane * per, b = a + per < m ? a + per : m;
+    P p{};
+    bool have = false;
+    for (int64_t k = a; k < b; ++k) {
+      p = have ? A::comb(p, parts[f + k]) : parts[f + k];
+      have = true;
+    }
+    if (!have) p = parts[f];  // an idle lane repeats chunk 0 and is masked below
+    // lanes without items must not contribute: fold only lanes [0, used)
+    const int used = static_cast<int>((m + per - 1) / per);
+    P acc = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      P other = shfl(acc, (lane + o) & 31);
+      if ((lane & (2 * o - 1)) == 0 && lane + o < used) acc = A::comb(acc, other);
+    }
+    if (lane == 0) {
+      if constexpr (OP == TQP_SUM) {
+        write_result<T, OP>(out, seg[q], acc, err);
+      } else {
+        write_mm(out, seg[q], acc);
+      }
     }
   }
 }
 
-template <typename T, int OP>
-void run_reduce(Ctx& c, const Tensor& values, const Tensor& lo, const Tensor& hi, int64_t num, Tensor& out) {
-  using P = typename Acc<T, OP>::P;
-  // at most min(num, n / kLong) segments can be longer than kLong rows
-  int64_t max_long = std::min<int64_t>(num, values.rows / kLong + 1);
-  auto long_buf = c.alloc_bytes(sizeof(int64_t) * (max_long + 1) + 16);
-  TQP_CUDA(cudaMemsetAsync(long_buf->ptr, 0, 8, c.stream));
-  auto* long_count = static_cast<unsigned long long*>(long_buf->ptr);
-  auto* long_list = reinterpret_cast<int64_t*>(static_cast<char*>(long_buf->ptr) + 16);
-  c.reset_err();
-  k_short<T, OP><<<c.grid_for(num * 32, 256), 256, 0, c.stream>>>(values.ptr<T>(), lo.ptr<int64_t>(),
-                                                                  hi.ptr<int64_t>(), num, out.ptr<T>(), c.d_err,
-                                                                  long_list, long_count);
-  c.count_launch();
-  unsigned long long nlong = 0;
-  TQP_CUDA(cudaMemcpyAsync(&nlong, long_count, 8, cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  if (!nlong) return;
-  std::vector<int64_t> segs(nlong);
-  TQP_CUDA(cudaMemcpyAsync(segs.data(), long_list, 8 * nlong, cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  std::sort(segs.begin(), segs.end());
-  // fetch run bounds of the long segments
-  std::vector<int64_t> slo(nlong), shi(nlong);
-  for (size_t q = 0; q < nlong; ++q) {
-    TQP_CUDA(cudaMemcpyAsync(&slo[q], lo.ptr<int64_t>() + segs[q], 8, cudaMemcpyDeviceToHost, c.stream));
-    TQP_CUDA(cudaMemcpyAsync(&shi[q], hi.ptr<int64_t>() + segs[q], 8, cudaMemcpyDeviceToHost, c.stream));
+// The validated segment plan of a segment-id vector: run bounds, the first
+// empty segment, and the chunking of the long segments. Tensors are
+// immutable, so the plan is computed on the first segmented_reduce over the
+// ids and kept with their buffer: the reference's lowering reduces every
+// aggregate over the same ids (operator_plan.cpp:355-386; Q1: 8 reductions),
+// and only the first pays the validation, the run bounds and the host round
+// trips that size the long-segment work.
+struct SegPlan {
+  int64_t rows = -1, num = -1;
+  Tensor lo, hi;
+  int64_t first_empty = -1;
+  int64_t nlong = 0, items = 0;
+  Tensor d_ilo, d_ihi, d_seg, d_first, d_cnt;
+  std::shared_ptr<DevBuf> long_scratch;  // k_short's list of long segments
+};
+
+std::shared_ptr<SegPlan> seg_plan(Ctx& c, const Tensor& ids, int64_t num) {
+  if (ids.buf) {
+    auto p = std::static_pointer_cast<SegPlan>(ids.buf->seg_plan);
+    if (p && p->rows == ids.rows && p->num == num) return p;
   }
-  c.sync();
-  std::vector<int64_t> ilo, ihi, first(nlong), cnt(nlong);
-  for (size_t q = 0; q < nlong; ++q) {
-    first[q] = static_cast<int64_t>(ilo.size());
-    for (int64_t a = slo[q]; a < shi[q]; a += kChunk) {
-      ilo.push_back(a);
-      ihi.push_back(std::min(a + kChunk, shi[q]));
-    }
-    cnt[q] = static_cast<int64_t>(ilo.size()) - first[q];
-  }
-  int64_t items = static_cast<int64_t>(ilo.size());
-  Tensor d_ilo = upload(c, TQP_I64, items, 1, ilo.data());
-  Tensor d_ihi = upload(c, TQP_I64, items, 1, ihi.data());
-  Tensor d_seg = upload(c, TQP_I64, nlong, 1, segs.data());
-  Tensor d_first = upload(c, TQP_I64, nlong, 1, first.data());
-  Tensor d_cnt = upload(c, TQP_I64, nlong, 1, cnt.data());
-  auto parts = c.alloc_bytes(sizeof(P) * items);
-  k_long_chunks<T, OP><<<items, 256, 0, c.stream>>>(values.ptr<T>(), d_ilo.ptr<int64_t>(), d_ihi.ptr<int64_t>(),
-                                                    static_cast<P*>(parts->ptr));
-  k_long_finish<T, OP><<<c.grid_for(nlong, 128), 128, 0, c.stream>>>(static_cast<P*>(parts->ptr),
-                                                                     d_seg.ptr<int64_t>(), d_first.ptr<int64_t>(),
-                                                                     d_cnt.ptr<int64_t>(), nlong, out.ptr<T>(), c.d_err);
-  c.count_launch(2);
-  c.sync();  // host vectors above must outlive the async uploads
-}
-
-}  // namespace
-
-namespace k {
-
-Tensor segmented_reduce(Ctx& c, const Tensor& values, const Tensor& ids, int64_t num, int op) {
-  if (!values.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
-  if (ids.dtype != TQP_I64) kernel_fail(std::string("segmented_reduce: expected int64, got ") + dtype_name(ids.dtype));
-  if (!ids.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
-  if (values.rows != ids.rows) kernel_fail("segmented_reduce: values/segment_ids length mismatch");
-  if (num < 0) kernel_fail("segmented_reduce: negative segment count");
-  int64_t n = ids.rows;
+  auto p = std::make_shared<SegPlan>();
+  p->rows = ids.rows;
+  p->num = num;
+  const int64_t n = ids.rows;
   if (n) {
     c.reset_err();
     k_check_ids<<<c.grid_for(n, 256), 256, 0, c.stream>>>(ids.ptr<int64_t>(), n, num, c.d_err);
@@ -380,11 +391,83 @@ Tensor segmented_reduce(Ctx& c, const Tensor& values, const Tensor& ids, int64_t
                   row);
     }
   }
-  Tensor lo = c.alloc(TQP_I64, num, 1), hi = c.alloc(TQP_I64, num, 1);
+  p->lo = c.alloc(TQP_I64, num, 1);
+  p->hi = c.alloc(TQP_I64, num, 1);
   if (num) {
-    k_runs<<<c.grid_for(num, 256), 256, 0, c.stream>>>(ids.ptr<int64_t>(), n, num, lo.ptr<int64_t>(), hi.ptr<int64_t>());
+    k_runs<<<c.grid_for(num, 256), 256, 0, c.stream>>>(ids.ptr<int64_t>(), n, num, p->lo.ptr<int64_t>(), p->hi.ptr<int64_t>());
     c.count_launch();
+    c.reset_err();
+    k_first_empty<<<c.grid_for(num, 256), 256, 0, c.stream>>>(p->lo.ptr<int64_t>(), p->hi.ptr<int64_t>(), num, c.d_err);
+    c.count_launch();
+    p->first_empty = c.read_err();
+    // long segments (> kLong rows) and their kChunk-row chunks
+    std::vector<int64_t> lo(num), hi(num);
+    TQP_CUDA(cudaMemcpyAsync(lo.data(), p->lo.data(), 8 * num, cudaMemcpyDeviceToHost, c.stream));
+    TQP_CUDA(cudaMemcpyAsync(hi.data(), p->hi.data(), 8 * num, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    std::vector<int64_t> segs, ilo, ihi, first, cnt;
+    for (int64_t q = 0; q < num; ++q) {
+      if (hi[q] - lo[q] <= kLong) continue;
+      segs.push_back(q);
+      first.push_back(static_cast<int64_t>(ilo.size()));
+      for (int64_t a = lo[q]; a < hi[q]; a += kChunk) {
+        ilo.push_back(a);
+        ihi.push_back(std::min(a + kChunk, hi[q]));
+      }
+      cnt.push_back(static_cast<int64_t>(ilo.size()) - first.back());
+    }
+    p->nlong = static_cast<int64_t>(segs.size());
+    p->items = static_cast<int64_t>(ilo.size());
+    if (p->nlong) {
+      p->d_ilo = upload(c, TQP_I64, p->items, 1, ilo.data());
+      p->d_ihi = upload(c, TQP_I64, p->items, 1, ihi.data());
+      p->d_seg = upload(c, TQP_I64, p->nlong, 1, segs.data());
+      p->d_first = upload(c, TQP_I64, p->nlong, 1, first.data());
+      p->d_cnt = upload(c, TQP_I64, p->nlong, 1, cnt.data());
+      c.sync();  // the host vectors outlive the uploads
+    }
+    p->long_scratch = c.alloc_bytes(sizeof(int64_t) * (p->nlong + 1) + 16);
   }
+  if (ids.buf) ids.buf->seg_plan = p;
+  return p;
+}
+
+template <typename T, int OP>
+void run_reduce(Ctx& c, const Tensor& values, const SegPlan& pl, Tensor& out) {
+  using P = typename Acc<T, OP>::P;
+  const int64_t num = pl.num;
+  // short segments: one warp each (k_short lists the long ones it skips into
+  // scratch; the plan already holds them, so nothing is read back)
+  auto* long_count = static_cast<unsigned long long*>(pl.long_scratch->ptr);
+  auto* long_list = reinterpret_cast<int64_t*>(static_cast<char*>(pl.long_scratch->ptr) + 16);
+  TQP_CUDA(cudaMemsetAsync(long_count, 0, 8, c.stream));
+  k_short<T, OP><<<c.grid_for(num * 32, 256), 256, 0, c.stream>>>(values.ptr<T>(), pl.lo.ptr<int64_t>(),
+                                                                  pl.hi.ptr<int64_t>(), num, out.ptr<T>(), c.d_err,
+                                                                  long_list, long_count);
+  c.count_launch();
+  if (!pl.nlong) return;
+  auto parts = c.alloc_bytes(sizeof(P) * pl.items);
+  k_long_chunks<T, OP><<<pl.items, 256, 0, c.stream>>>(values.ptr<T>(), pl.d_ilo.ptr<int64_t>(), pl.d_ihi.ptr<int64_t>(),
+                                                       static_cast<P*>(parts->ptr));
+  k_long_finish<T, OP><<<c.grid_for(pl.nlong * 32, 128), 128, 0, c.stream>>>(
+      static_cast<P*>(parts->ptr), pl.d_seg.ptr<int64_t>(), pl.d_first.ptr<int64_t>(), pl.d_cnt.ptr<int64_t>(), pl.nlong,
+      out.ptr<T>(), c.d_err);
+  c.count_launch(2);
+}
+
+}  // namespace
+
+namespace k {
+
+Tensor segmented_reduce(Ctx& c, const Tensor& values, const Tensor& ids, int64_t num, int op) {
+  if (!values.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
+  if (ids.dtype != TQP_I64) kernel_fail(std::string("segmented_reduce: expected int64, got ") + dtype_name(ids.dtype));
+  if (!ids.is_vector()) kernel_fail("segmented_reduce: expected a vector (m=1)");
+  if (values.rows != ids.rows) kernel_fail("segmented_reduce: values/segment_ids length mismatch");
+  if (num < 0) kernel_fail("segmented_reduce: negative segment count");
+  auto plan = seg_plan(c, ids, num);
+  const Tensor& lo = plan->lo;
+  const Tensor& hi = plan->hi;
   if (op == TQP_COUNT) {
     Tensor o = c.alloc(TQP_I64, num, 1);
     if (num) {
@@ -395,36 +478,31 @@ Tensor segmented_reduce(Ctx& c, const Tensor& values, const Tensor& ids, int64_t
   }
   if (values.dtype == TQP_BOOL || values.dtype == TQP_STR8) kernel_fail("segmented_reduce: bool values not supported");
   if (op == TQP_MIN || op == TQP_MAX) {
-    if (num) {
-      c.reset_err();
-      k_first_empty<<<c.grid_for(num, 256), 256, 0, c.stream>>>(lo.ptr<int64_t>(), hi.ptr<int64_t>(), num, c.d_err);
-      c.count_launch();
-      int64_t s = c.read_err();
-      if (s >= 0) {
-        kernel_fail("segmented_reduce: empty segment " + std::to_string(s) + " for " + (op == TQP_MIN ? "min" : "max"));
-      }
-    }
+    if (plan->first_empty >= 0)
+      kernel_fail("segmented_reduce: empty segment " + std::to_string(plan->first_empty) + " for " +
+                  (op == TQP_MIN ? "min" : "max"));
   } else if (op != TQP_SUM) {
     kernel_fail("segmented_reduce: bad op");
   }
   Tensor out = c.alloc(values.dtype, num, 1);
   if (!num) return out;
   if (op == TQP_SUM) TQP_CUDA(cudaMemsetAsync(out.data(), 0, out.bytes(), c.stream));
+  c.reset_err();
   switch (values.dtype) {
     case TQP_F64:
-      if (op == TQP_SUM) run_reduce<double, TQP_SUM>(c, values, lo, hi, num, out);
-      else if (op == TQP_MIN) run_reduce<double, TQP_MIN>(c, values, lo, hi, num, out);
-      else run_reduce<double, TQP_MAX>(c, values, lo, hi, num, out);
+      if (op == TQP_SUM) run_reduce<double, TQP_SUM>(c, values, *plan, out);
+      else if (op == TQP_MIN) run_reduce<double, TQP_MIN>(c, values, *plan, out);
+      else run_reduce<double, TQP_MAX>(c, values, *plan, out);
       break;
     case TQP_I64:
-      if (op == TQP_SUM) run_reduce<int64_t, TQP_SUM>(c, values, lo, hi, num, out);
-      else if (op == TQP_MIN) run_reduce<int64_t, TQP_MIN>(c, values, lo, hi, num, out);
-      else run_reduce<int64_t, TQP_MAX>(c, values, lo, hi, num, out);
+      if (op == TQP_SUM) run_reduce<int64_t, TQP_SUM>(c, values, *plan, out);
+      else if (op == TQP_MIN) run_reduce<int64_t, TQP_MIN>(c, values, *plan, out);
+      else run_reduce<int64_t, TQP_MAX>(c, values, *plan, out);
       break;
     case TQP_I32:
-      if (op == TQP_SUM) run_reduce<int32_t, TQP_SUM>(c, values, lo, hi, num, out);
-      else if (op == TQP_MIN) run_reduce<int32_t, TQP_MIN>(c, values, lo, hi, num, out);
-      else run_reduce<int32_t, TQP_MAX>(c, values, lo, hi, num, out);
+      if (op == TQP_SUM) run_reduce<int32_t, TQP_SUM>(c, values, *plan, out);
+      else if (op == TQP_MIN) run_reduce<int32_t, TQP_MIN>(c, values, *plan, out);
+      else run_reduce<int32_t, TQP_MAX>(c, values, *plan, out);
       break;
     default: kernel_fail("segmented_reduce: unsupported dtype");
   }

@@ -41,6 +41,9 @@ struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
   int bucket = -1;  // >= 0: a small block of the context's host-side cache
+  // derived state of an immutable tensor living in this buffer, computed once
+  // (reduce.cu: the validated segment plan of a segment-id vector)
+  std::shared_ptr<void> seg_plan;
   ~DevBuf();
 };
 
