@@ -66,41 +66,42 @@ __global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restri
   }
 }
 
-// Pass 1 of compact: selected-row count per tile.
-__global__ void __launch_bounds__(kThreads) k_mask_count(const uint8_t* __restrict__ mask, int64_t n,
-                                                         int64_t* __restrict__ counts) {
-  __shared__ unsigned long long s_warp[33];
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  unsigned long long local = 0;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) local += (base + j < n && mask[base + j]) ? 1 : 0;
-  unsigned long long total;
-  block_exclusive_scan(local, s_warp, &total);
-  if (threadIdx.x == 0) counts[blockIdx.x] = static_cast<int64_t>(total);
-}
-
-// Pass 3 of compact: order-preserving scatter of whole rows.
+// Single-pass order-preserving compaction: a tile (dynamic id, so the
+// lookback always waits on tiles already running) counts its selected rows
+// (one 8-byte mask load per thread, a popcount of the nonzero bytes), takes
+// its output offset from the decoupled lookback and scatters whole rows.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_compact_scatter(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
-                                                              int64_t n, int64_t m, const int64_t* __restrict__ offs,
-                                                              T* __restrict__ out) {
+__global__ void __launch_bounds__(kThreads) k_compact_onepass(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
+                                                              int64_t n, int64_t m, T* __restrict__ out, longlong2* desc,
+                                                              int* counter) {
+  __shared__ int s_tile;
   __shared__ unsigned long long s_warp[33];
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  uint8_t sel[kItems];
-  unsigned long long local = 0;
+  __shared__ long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t base = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  unsigned sel = 0;  // bit j: row base + j selected
+  if (base + kItems <= n) {
+    const unsigned long long w = *reinterpret_cast<const unsigned long long*>(mask + base);
 #pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    sel[j] = (base + j < n && mask[base + j]) ? 1 : 0;
-    local += sel[j];
+    for (int j = 0; j < kItems; ++j) sel |= ((w >> (8 * j)) & 0xffULL) ? (1u << j) : 0u;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) sel |= (base + j < n && mask[base + j]) ? (1u << j) : 0u;
   }
   unsigned long long total;
-  unsigned long long w = block_exclusive_scan(local, s_warp, &total) + static_cast<unsigned long long>(offs[blockIdx.x]);
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    if (sel[j]) {
-      for (int64_t q = 0; q < m; ++q) out[w * m + q] = vals[(base + j) * m + q];
-      ++w;
-    }
+  const unsigned long long texcl = block_exclusive_scan(__popc(sel), s_warp, &total);
+  if (threadIdx.x < 32) {
+    const long long p = tile_lookback(desc, tile, static_cast<long long>(total));
+    if (threadIdx.x == 0) s_prefix = p;
+  }
+  __syncthreads();
+  unsigned long long w = static_cast<unsigned long long>(s_prefix) + texcl;
+  for (unsigned b = sel; b; b &= b - 1) {
+    const int j = __ffs(b) - 1;
+    for (int64_t q = 0; q < m; ++q) out[w * m + q] = vals[(base + j) * m + q];
+    ++w;
   }
 }
 
@@ -212,24 +213,27 @@ Tensor compact(Ctx& c, const Tensor& values, const Tensor& mask) {
   }
   int64_t n = values.rows, m = values.cols;
   if (n == 0) return c.alloc(values.dtype, 0, m);
-  int64_t tiles = (n + kTile - 1) / kTile;
-  Tensor counts = c.alloc(TQP_I64, tiles, 1);
-  k_mask_count<<<tiles, kThreads, 0, c.stream>>>(mask.ptr<uint8_t>(), n, counts.ptr<int64_t>());
+  // one pass (k_compact_onepass) into an output sized for every row; the
+  // count comes back with the last tile's inclusive prefix (the one host
+  // round trip: the result's shape), and a sparse result moves to a buffer
+  // of its own size so the n-row buffer is not held
+  const int64_t tiles = (n + kTile - 1) / kTile;
+  ScanScratch sc = scan_scratch(c, tiles);
+  Tensor o = c.alloc(values.dtype, n, m);
+  TQP_DISPATCH(values.dtype, T,
+               k_compact_onepass<T><<<tiles, kThreads, 0, c.stream>>>(values.ptr<T>(), mask.ptr<uint8_t>(), n, m,
+                                                                      o.ptr<T>(), sc.desc, sc.counter));
   c.count_launch();
-  int64_t ovf;
-  Tensor offs = prefix_sum_raw(c, counts, &ovf);
-  int64_t last_off = 0, last_cnt = 0;
-  TQP_CUDA(cudaMemcpyAsync(&last_off, offs.ptr<int64_t>() + tiles - 1, 8, cudaMemcpyDeviceToHost, c.stream));
-  TQP_CUDA(cudaMemcpyAsync(&last_cnt, counts.ptr<int64_t>() + tiles - 1, 8, cudaMemcpyDeviceToHost, c.stream));
+  long long* h = c.h_err + Ctx::kPinnedRead;
+  TQP_CUDA(cudaMemcpyAsync(h, sc.desc + tiles - 1, sizeof(longlong2), cudaMemcpyDeviceToHost, c.stream));
   c.sync();
-  int64_t total = last_off + last_cnt;
-  Tensor o = c.alloc(values.dtype, total, m);
-  if (total) {
-    TQP_DISPATCH(values.dtype, T,
-                 k_compact_scatter<T><<<tiles, kThreads, 0, c.stream>>>(values.ptr<T>(), mask.ptr<uint8_t>(), n, m,
-                                                                        offs.ptr<int64_t>(), o.ptr<T>()));
-    c.count_launch();
+  const int64_t total = h[1];
+  if (total * 2 < n) {
+    Tensor t = c.alloc(values.dtype, total, m);
+    if (total) TQP_CUDA(cudaMemcpyAsync(t.data(), o.data(), t.bytes(), cudaMemcpyDeviceToDevice, c.stream));
+    return t;
   }
+  o.rows = total;
   return o;
 }
 
