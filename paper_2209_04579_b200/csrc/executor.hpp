@@ -73,6 +73,10 @@ struct KeyRange {
   bool ready = false;
   long long mn = 0, mx = 0;
   int day = -1;  // Date keys: 1 every value is a whole day in ns, 0 not, -1 not computed
+  // 1: no value repeats (checked once, on the device, the first time a
+  // direct-addressed build keys on the column), 0: some value repeats,
+  // -1: not checked
+  int unique = -1;
 };
 
 // Dictionary of an int64 key column (MODE_HASH keys whose value range is too

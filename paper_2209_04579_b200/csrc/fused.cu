@@ -1397,7 +1397,12 @@ __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned 
   return s.group_table ? static_cast<long long>(s.group_table[g] & 0xffffffffULL) - 1 : static_cast<long long>(g);
 }
 
-__device__ __forceinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
+// not inlined: its int128 / limb / division cases are several thousand
+// instructions, and the top-k kernel calls it from many sites - inlined
+// copies made k_topk_groups ~26 k instructions and its walk instruction-fetch
+// bound (kernels passing a GroupSpec take it as __grid_constant__, so a call
+// does not copy the struct to local memory)
+__device__ __noinline__ bool group_out_value(const GroupSpec& s, int j, unsigned g, unsigned long long& bits,
                                                 bool& is_f64) {
   const OutKind& o = s.f.outs[j];
   long long cnt = group_count(s, g);
@@ -1543,12 +1548,17 @@ struct TopkList {
   }
 };
 
+// key word q of group g's candidate key (not inlined: one copy for every
+// call site of the top-k kernel)
+__device__ __noinline__ unsigned long long cand_key_word(const GroupSpec& s, int q, unsigned g) {
+  return q < s.nsort ? sort_key_word(s, q < 4 ? q : 3, g)
+                     : radix_key(static_cast<int64_t>(group_key_value(s, q - s.nsort, g)));
+}
+
 template <int NK>
 __device__ __forceinline__ void cand_keys_nk(const GroupSpec& s, unsigned g, unsigned long long* k) {
 #pragma unroll
-  for (int q = 0; q < NK; ++q)
-    k[q] = q < s.nsort ? sort_key_word(s, q < 4 ? q : 3, g)
-                       : radix_key(static_cast<int64_t>(group_key_value(s, q - s.nsort, g)));
+  for (int q = 0; q < NK; ++q) k[q] = cand_key_word(s, q, g);
 }
 
 // Exact top-k in one launch, without per-group full keys. The walk only
@@ -1559,91 +1569,146 @@ __device__ __forceinline__ void cand_keys_nk(const GroupSpec& s, unsigned g, uns
 //     global k-th value T, every group with k0 <= T is in some warp's log;
 //   * a block merges its warps' values (k-way, heads in lanes) to its own k-th
 //     value T_b >= T and publishes its values and the log entries <= T_b;
-//   * the last block merges the block values into the exact T, keeps the
-//     published entries with k0 <= T (the top k plus ties on k0), computes
-//     their full keys and orders them with TopkList.
+//   * the last block finds the exact T (every warp keeps the k smallest of a
+//     share of the block values, warp 0 merges the 8 lists), keeps the
+//     published entries with k0 <= T (the top k plus ties on k0; one flat pass
+//     over all blocks' entries through a prefix of their counts), computes
+//     their full keys in parallel, orders them with TopkList and writes the
+//     output values with one thread per (row, column).
+// Every step of the last block is a few rounds of independent loads: the
+// tail no longer grows with the block count, so the walk runs 4 blocks per
+// SM (more warps in flight for its dependent presence -> count -> limb loads)
+// and each warp takes 4 presence words per lane (4096 slots) per round.
 // A warp log that cannot hold the entries still at or below its k-th value
 // (more than kTopkLog ties) flags the unit for the exact per-instruction path.
 constexpr int kTopkLog = 64;
 constexpr int kTopkBlkCand = 128;
 constexpr int kTopkFinal = 128;
-constexpr int kTopkSuperSlots = 1024;
-constexpr int kTopkStage = 2048;  // last block: block values staged in shared memory (nb * k)
+constexpr int kTopkSuperSlots = 512;   // compaction buffer per warp (slots)
+constexpr int kTopkWords = 4;          // presence words per lane per round
+constexpr int kTopkMaxBlocks = 1024;   // last block: prefix of the published counts in shared memory
+constexpr int kTopkCollect = 1024;     // last block: published entries <= T1 held at once
 
-// the k smallest u64 values of a warp, ascending, one per lane (lane < cnt)
-struct ValList {
-  unsigned long long v = ~0ULL;
-  int cnt = 0;
-  __device__ unsigned long long thr(int k) const {
-    const unsigned long long t = __shfl_sync(0xffffffffu, v, k - 1);
-    return cnt == k ? t : ~0ULL;
+// k-th smallest (k >= 1) of a warp's vals[0..m) in shared memory, ~0 when
+// m < k (rank selection, as block_kth); every lane calls it
+__device__ __noinline__ unsigned long long warp_kth(const unsigned long long* vals, int m, int k) {
+  unsigned long long best = 0;
+  for (int i = static_cast<int>(threadIdx.x & 31); i < m; i += 32) {
+    const unsigned long long v = vals[i];
+    int less = 0;
+#pragma unroll 8
+    for (int j = 0; j < m; ++j) less += vals[j] < v ? 1 : 0;
+    if (less < k && v > best) best = v;
   }
-  __device__ void insert(unsigned long long x, int k) {  // warp-uniform x
-    const int lane = threadIdx.x & 31;
-    if (cnt == k && x >= thr(k)) return;
-    const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && v <= x));
-    const unsigned long long up = __shfl_up_sync(0xffffffffu, v, 1);
-    v = lane > pos ? up : (lane == pos ? x : v);
-    if (cnt < k) ++cnt;
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  return m < k ? ~0ULL : best;
+}
+
+// k-th smallest (k >= 1) of vals[0..m) in shared memory, ~0 when m < k:
+// the largest v_i with fewer than k values below it (rank selection, all
+// threads in parallel, no serial insert chain). Every thread of the block
+// calls it; red holds one word per warp. Not inlined: the top-k kernel's
+// last block runs its code cold (each new instruction line is an L2 fetch,
+// ~0.15 us), and one copy shared by every call site is already in the
+// instruction cache from the block phase.
+__device__ __noinline__ unsigned long long block_kth(const unsigned long long* vals, int m, int k, unsigned long long* red) {
+  unsigned long long best = 0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const unsigned long long v = vals[i];
+    int less = 0;
+#pragma unroll 8
+    for (int j = 0; j < m; ++j) less += vals[j] < v ? 1 : 0;
+    if (less < k && v > best) best = v;
   }
-};
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  unsigned long long r = 0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) r = max(r, red[w]);
+  __syncthreads();
+  return m < k ? ~0ULL : r;
+}
 
 template <int NK>
-__global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long long ngroups, int k,
-                                                              unsigned long long* __restrict__ blk_val,
-                                                              int* __restrict__ blk_nval,
+__global__ void __launch_bounds__(kTopkThreads) k_topk_groups(const __grid_constant__ GroupSpec s, long long ngroups, int k,
                                                               unsigned long long* __restrict__ blk_ck,
                                                               unsigned* __restrict__ blk_cg, int* __restrict__ blk_nc,
                                                               unsigned* __restrict__ ticket,
-                                                              long long* __restrict__ nout, long long* __restrict__ err) {
+                                                              long long* __restrict__ nout, long long* __restrict__ err,
+                                                              unsigned long long* __restrict__ trace) {
   constexpr int kW = kTopkThreads / 32;
+  // TQP_TOPK_TRACE: %globaltimer at the phase boundaries (debug aid)
+  auto stamp = [&](long long at) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[at] = t;
+    }
+  };
+  stamp(8LL * blockIdx.x);
+  constexpr long long kSuper = 32LL * 32 * kTopkWords;  // slots per warp round
   __shared__ unsigned long long s_logk[kW][kTopkLog];
   __shared__ unsigned s_logg[kW][kTopkLog];
-  __shared__ __align__(16) unsigned s_scratch[kW * kTopkSuperSlots];  // slot compaction; last block: heads / keys
-  __shared__ unsigned long long s_wv[kW][32];
-  __shared__ int s_wn[kW];
-  __shared__ unsigned long long s_T;
-  __shared__ int s_nc, s_last, s_err;
+  __shared__ __align__(16) unsigned s_scratch[kW * kTopkSuperSlots];  // slot compaction; last block: prefix / keys
+  __shared__ unsigned long long s_k0[kW][32 * kTopkUnroll];
+  __shared__ unsigned s_gq[kW][32 * kTopkUnroll];
+  __shared__ unsigned long long s_red[kW];
+  __shared__ int s_nc, s_np, s_last, s_err;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   if (threadIdx.x == 0) {
     s_nc = 0;
+    s_np = 0;
     s_err = 0;
   }
   __syncthreads();
   const long long n = ngroups;
-  ValList L;
+  // the warp's log: every group it has seen with k0 <= tw; tw starts at ~0
+  // and drops to the log's k-th value whenever the log fills (a parallel
+  // rank selection, then the entries above it dropped), so it never falls
+  // below the global k-th value T and no per-group serial list insert runs
+  unsigned long long tw = ~0ULL;
   int nlog = 0;
   bool log_ok = true;
   unsigned* sidx = s_scratch + warp * kTopkSuperSlots;
+  // keep the log entries <= the log's k-th value; tw = that value
+  auto prune = [&]() {
+    const unsigned long long t = warp_kth(s_logk[warp], nlog, k);
+    int kept = 0;
+    for (int i0 = 0; i0 < nlog; i0 += 32) {
+      const int i = i0 + lane;
+      const unsigned long long lk = i < nlog ? s_logk[warp][i] : ~0ULL;
+      const unsigned lg = i < nlog ? s_logg[warp][i] : 0u;
+      const bool keep = i < nlog && lk <= t;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();
+      if (keep) {
+        const int pos = kept + __popc(km & lt_mask);
+        s_logk[warp][pos] = lk;
+        s_logg[warp][pos] = lg;
+      }
+      kept += __popc(km);
+      __syncwarp();
+    }
+    nlog = kept;
+    tw = t;
+  };
 
-  for (long long sb = static_cast<long long>(blockIdx.x) * kW + warp; sb * kTopkSuperSlots < n;
-       sb += static_cast<long long>(gridDim.x) * kW) {
-    // present slots of the super-chunk, compacted (one presence word per lane)
-    const long long base = sb * kTopkSuperSlots, wbase = base + 32LL * lane;
-    unsigned w = 0;
-    if (wbase < n) {
-      w = s.present ? __ldg(s.present + (wbase >> 5)) : ~0u;
-      if (n - wbase < 32) w &= (1u << (n - wbase)) - 1u;
-    }
-    const int c = __popc(w);
-    int off = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, off, o);
-      if (lane >= o) off += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, off, 31);
-    off -= c;
-    while (w) {
-      const int bit = __ffs(w) - 1;
-      w &= w - 1;
-      sidx[off++] = static_cast<unsigned>(wbase - base) + bit;
-    }
+  // the groups whose slots (relative to `base`) are sidx[0..total): their
+  // counts and first key words are formed kTopkUnroll x 32 at a time (loads
+  // together), then logged one 32-lane batch at a time
+  long long cy_load = 0, cy_key = 0, cy_offer = 0, cy_t = 0;  // TQP_TOPK_TRACE: warp 0's cycles per walk part
+  auto walk = [&](long long base, int total) {
     __syncwarp();
     for (int c0 = 0; c0 < total; c0 += 32 * kTopkUnroll) {
+      if (trace) cy_t = clock64();
       unsigned gq[kTopkUnroll];
-      unsigned long long gc[kTopkUnroll], k0[kTopkUnroll];
+      unsigned long long gc[kTopkUnroll];
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
         const int i = c0 + u * 32 + lane;
@@ -1652,114 +1717,154 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
       }
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
+        if (c0 + u * 32 >= total) break;  // warp-uniform: no slots left
         // limb sums are exact below kLimbMaxRows rows per group
         if (gc[u] && !group_limbs_ok(s, gq[u])) {
           err[0] = 1;
           err[3] = FR_LIMB_ROWS;
         }
-        k0[u] = gc[u] ? sort_key_word(s, 0, gq[u]) : ~0ULL;
-      }
-#pragma unroll
-      for (int u = 0; u < kTopkUnroll; ++u) {
-        const unsigned long long t = L.thr(k);  // every lane (shuffle)
-        const bool cand = gc[u] != 0 && k0[u] <= t;
-        unsigned mask = __ballot_sync(0xffffffffu, cand);
+        const unsigned long long k0 = gc[u] ? cand_key_word(s, 0, gq[u]) : ~0ULL;
+        // reconverge: after a call from divergent lanes the warp stayed
+        // split and every later shuffle took the slow (diverged) path -
+        // measured 10x on a warp merge
+        __syncwarp();
+        if (trace && u == 0) {
+          const long long t1 = clock64();
+          cy_key += t1 - cy_t;
+          cy_t = t1;
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, gc[u] != 0 && k0 <= tw);
         if (!mask) continue;
-        const int m = __popc(mask);
+        int m = __popc(mask);
         if (log_ok && nlog + m > kTopkLog) {
-          // drop logged entries above the current k-th value (never needed)
-          const unsigned long long t = L.thr(k);
-          int kept = 0;
-          for (int i0 = 0; i0 < nlog; i0 += 32) {
-            const int i = i0 + lane;
-            const unsigned long long lk = i < nlog ? s_logk[warp][i] : ~0ULL;
-            const unsigned lg = i < nlog ? s_logg[warp][i] : 0u;
-            const bool keep = i < nlog && lk <= t;
-            const unsigned km = __ballot_sync(0xffffffffu, keep);
-            __syncwarp();
-            if (keep) {
-              const int pos = kept + __popc(km & lt_mask);
-              s_logk[warp][pos] = lk;
-              s_logg[warp][pos] = lg;
-            }
-            kept += __popc(km);
-            __syncwarp();
-          }
-          nlog = kept;
+          prune();  // tw drops: only the lanes still at or below it are logged
+          mask = __ballot_sync(0xffffffffu, gc[u] != 0 && k0 <= tw);
+          m = __popc(mask);
           if (nlog + m > kTopkLog) log_ok = false;  // more ties than the log holds
         }
-        if (log_ok && cand) {
+        if (log_ok && ((mask >> lane) & 1u)) {
           const int pos = nlog + __popc(mask & lt_mask);
-          s_logk[warp][pos] = k0[u];
+          s_logk[warp][pos] = k0;
           s_logg[warp][pos] = gq[u];
         }
         nlog += m;
-        while (mask) {
-          const int src = __ffs(mask) - 1;
-          mask &= mask - 1;
-          L.insert(__shfl_sync(0xffffffffu, k0[u], src), k);
-        }
+        __syncwarp();
       }
+      if (trace) cy_offer += clock64() - cy_t;
     }
-    __syncwarp();
-  }
-  if (!log_ok && lane == 0) s_err = 1;
-  if (lane < L.cnt) s_wv[warp][lane] = L.v;
-  if (lane == 0) s_wn[warp] = L.cnt;
-  __syncthreads();
-  // block: k-way merge of the warp lists (lane w < kW holds warp w's head)
-  if (warp == 0) {
-    int hp = 0;
-    ValList B;
-    for (int r = 0; r < k; ++r) {
-      unsigned long long hv = lane < kW && hp < s_wn[lane] ? s_wv[lane][hp] : ~0ULL;
-      int hl = lane < kW && hp < s_wn[lane] ? lane : 32;
+  };
+
+  long long sb = static_cast<long long>(blockIdx.x) * kW + warp;
+  const long long sb_step = static_cast<long long>(gridDim.x) * kW;
+  // kTopkWords presence words per lane per round, the next round's loaded
+  // while this one is walked
+  auto load_words = [&](long long sbx, unsigned* w) {
+    const long long base = sbx * kSuper;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long ov = __shfl_xor_sync(0xffffffffu, hv, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, hl, o);
-        if (ov < hv || (ov == hv && ol < hl)) {
-          hv = ov;
-          hl = ol;
-        }
+    for (int u = 0; u < kTopkWords; ++u) {
+      const long long wb = base + 32LL * (u * 32 + lane);
+      w[u] = 0u;
+      if (wb < n) {
+        w[u] = s.present ? __ldg(s.present + (wb >> 5)) : ~0u;
+        if (n - wb < 32) w[u] &= (1u << (n - wb)) - 1u;
       }
-      if (hl == 32) break;
-      if (lane == hl) ++hp;
-      if (lane == r) B.v = hv;
-      ++B.cnt;
     }
-    const unsigned long long tb = B.thr(k);
-    if (lane < B.cnt) blk_val[static_cast<long long>(blockIdx.x) * kTopkMaxK + lane] = B.v;
-    if (lane == 0) {
-      blk_nval[blockIdx.x] = B.cnt;
-      s_T = tb;
+  };
+  unsigned wnext[kTopkWords];
+  load_words(sb, wnext);
+  for (; sb * kSuper < n; sb += sb_step) {
+    // this round's present slots compacted into sidx, handed to walk() (one
+    // call site) whenever the next word's slots would overflow it, and after
+    // the last word
+    const long long base = sb * kSuper;
+    const long long cl0 = trace ? clock64() : 0;
+    unsigned w[kTopkWords];
+#pragma unroll
+    for (int u = 0; u < kTopkWords; ++u) w[u] = wnext[u];
+    load_words(sb + sb_step, wnext);
+    // half a word-round (16 lanes' words, <= 512 slots) at a time, so one
+    // step never exceeds the compaction buffer
+    static_assert(kTopkSuperSlots >= 16 * 32, "compaction buffer below half a word-round");
+    int fill = 0;
+#pragma unroll 1
+    for (int h = 0; h <= 2 * kTopkWords; ++h) {
+      const bool last = h == 2 * kTopkWords;
+      const unsigned xw = w[0];
+      if (h & 1) {
+#pragma unroll
+        for (int v = 0; v + 1 < kTopkWords; ++v) w[v] = w[v + 1];  // next word to the front
+        w[kTopkWords - 1] = 0u;
+      }
+      const unsigned x0 = !last && (lane >> 4) == (h & 1) ? xw : 0u;
+      const int c = __popc(x0);
+      int off = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, off, o);
+        if (lane >= o) off += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, off, 31);
+      if (fill && (last || fill + total > kTopkSuperSlots)) {
+        if (trace && last) cy_load += clock64() - cl0;
+        walk(base, fill);
+        fill = 0;
+      }
+      if (last) break;
+      off += fill - c;
+      unsigned x = x0;
+      const unsigned rel = static_cast<unsigned>(32 * ((h >> 1) * 32 + lane));
+      while (x) {
+        const int bit = __ffs(x) - 1;
+        x &= x - 1;
+        sidx[off++] = rel + bit;
+      }
+      __syncwarp();
+      fill += total;
     }
   }
+  if (trace && threadIdx.x == 0) {
+    trace[8LL * blockIdx.x + 5] = static_cast<unsigned long long>(cy_load);
+    trace[8LL * blockIdx.x + 6] = static_cast<unsigned long long>(cy_key);
+    trace[8LL * blockIdx.x + 7] = static_cast<unsigned long long>(cy_offer);
+  }
+  // the warp's own k-th value: its log shrinks to <= k entries plus ties
+  if (log_ok && nlog > k) prune();
+  if (!log_ok && lane == 0) s_err = 1;
   __syncthreads();
-  // publish the log entries at or below the block's k-th value
+  stamp(8LL * blockIdx.x + 1);
+  unsigned long long* cv = &s_k0[0][0];  // collection: values (kTopkCollect)
+  unsigned* cg = &s_gq[0][0];            // collection: groups
+  // block: every warp's log in one list, T_b = its k-th value (rank
+  // selection), and the entries <= T_b published sorted by value
   {
-    const unsigned long long T = s_T;
     const int nl = log_ok ? nlog : 0;
-    for (int i0 = 0; i0 < nl; i0 += 32) {
-      const int i = i0 + lane;
-      const bool keep = i < nl && s_logk[warp][i] <= T;
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      int basepos = 0;
-      if (lane == 0 && km) basepos = atomicAdd(&s_nc, __popc(km));
-      basepos = __shfl_sync(0xffffffffu, basepos, 0);
-      if (keep) {
-        const int pos = basepos + __popc(km & lt_mask);
-        if (pos < kTopkBlkCand) {
-          blk_ck[static_cast<long long>(blockIdx.x) * kTopkBlkCand + pos] = s_logk[warp][i];
-          blk_cg[static_cast<long long>(blockIdx.x) * kTopkBlkCand + pos] = s_logg[warp][i];
-        }
-      }
+    int basepos = 0;
+    if (lane == 0 && nl) basepos = atomicAdd(&s_nc, nl);
+    basepos = __shfl_sync(0xffffffffu, basepos, 0);
+    for (int i = lane; i < nl; i += 32) {
+      cv[basepos + i] = s_logk[warp][i];
+      cg[basepos + i] = s_logg[warp][i];
     }
+    __syncthreads();
+    const int ncv = s_nc;  // <= kW * kTopkLog <= kTopkCollect
+    const unsigned long long tb = block_kth(cv, ncv, k, s_red);
+    for (int t = threadIdx.x; t < ncv; t += kTopkThreads) {
+      const unsigned long long v = cv[t];
+      if (v > tb) continue;
+      int r = 0;  // rank by (value, position) among the entries <= T_b
+#pragma unroll 8
+      for (int j = 0; j < ncv; ++j) r += cv[j] <= tb && (cv[j] < v || (cv[j] == v && j < t)) ? 1 : 0;
+      if (r < kTopkBlkCand) {
+        blk_ck[static_cast<long long>(blockIdx.x) * kTopkBlkCand + r] = v;
+        blk_cg[static_cast<long long>(blockIdx.x) * kTopkBlkCand + r] = cg[t];
+      }
+      atomicAdd(&s_np, 1);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_nc > kTopkBlkCand) s_err = 1;
-    blk_nc[blockIdx.x] = s_nc < kTopkBlkCand ? s_nc : kTopkBlkCand;
+    if (s_np > kTopkBlkCand) s_err = 1;
+    blk_nc[blockIdx.x] = s_np < kTopkBlkCand ? s_np : kTopkBlkCand;
     if (s_err) {
       err[0] = 1;
       err[3] = FR_TOPK_BLOCK;
@@ -1767,111 +1872,182 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(GroupSpec s, long 
     __threadfence();
     s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
+  stamp(8LL * blockIdx.x + 2);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last block: exact T = k-th smallest of every block's values; the lists
-  // are staged in shared memory first (nb * k <= kTopkStage), then merged
-  // k-way by warp 0 with heads in shared memory
   const int nb = static_cast<int>(gridDim.x);
-  unsigned long long* sv = reinterpret_cast<unsigned long long*>(s_scratch);  // [nb][k]
-  int* hpos = reinterpret_cast<int*>(sv + nb * k);
-  int* hlen = hpos + nb;
-  int* cnb = hlen + nb;  // published candidates per block
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    hlen[b] = __ldcg(blk_nval + b);
-    cnb[b] = __ldcg(blk_nc + b);
-    hpos[b] = 0;
+  const long long tl = 8LL * nb;
+  // last block. Every block published its groups with k0 <= T_b sorted, and
+  // T (the global k-th value) <= every T_b, so the groups with k0 <= T are
+  // all published. T1 = the k-th smallest of the first kTopkThreads blocks'
+  // minima is >= T (k distinct groups at or below it); the published entries
+  // <= T1 (a short sorted prefix per block) hold every group <= T, and T is
+  // their k-th smallest.
+  static_assert(sizeof(int) * kTopkMaxBlocks + sizeof(unsigned long long) * kTopkThreads +
+                        sizeof(unsigned) * (kTopkFinal + 2) + 8 + sizeof(unsigned long long) * kTopkFinal * 8 +
+                        sizeof(unsigned) * kTopkMaxK <=
+                    sizeof(unsigned) * kTopkThreads / 32 * kTopkSuperSlots,
+                "last-block scratch exceeds the compaction buffers");
+  static_assert(kTopkThreads / 32 * 32 * kTopkUnroll >= kTopkCollect, "collection exceeds the staging buffers");
+  static_assert(kTopkThreads / 32 * kTopkLog <= kTopkCollect, "block logs exceed the collection");
+  int* cnb = reinterpret_cast<int*>(s_scratch);                        // [nb]
+  unsigned long long* bmin = reinterpret_cast<unsigned long long*>(cnb + kTopkMaxBlocks);  // [kTopkThreads]
+  for (int b = threadIdx.x; b < nb; b += kTopkThreads) cnb[b] = __ldcg(blk_nc + b);
+  if (threadIdx.x < kTopkThreads) {
+    const int b = threadIdx.x;
+    bmin[b] = b < nb && __ldcg(blk_nc + b) > 0 ? __ldcg(blk_ck + static_cast<long long>(b) * kTopkBlkCand) : ~0ULL;
   }
-  for (int i = threadIdx.x; i < nb * k; i += blockDim.x)
-    sv[i] = __ldcg(blk_val + static_cast<long long>(i / k) * kTopkMaxK + i % k);
+  if (threadIdx.x == 0) s_nc = 0;
   __syncthreads();
-  if (warp == 0) {
-    unsigned long long T = ~0ULL;
-    for (int r = 0; r < k; ++r) {
-      unsigned long long bv = ~0ULL;
-      int bl = -1;
-      for (int b = lane; b < nb; b += 32)
-        if (hpos[b] < hlen[b] && (bl < 0 || sv[b * k + hpos[b]] < bv)) {
-          bv = sv[b * k + hpos[b]];
-          bl = b;
-        }
+  stamp(tl + 6);
+  const unsigned long long T1 = block_kth(bmin, min(nb, kTopkThreads), k, s_red);
+  for (int b = threadIdx.x; b < nb; b += kTopkThreads) {
+    const int nc = cnb[b];
+    for (int i0 = 0; i0 < nc; i0 += 4) {
+      unsigned long long v[4];
+      unsigned g[4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-        if (ol >= 0 && (bl < 0 || ov < bv || (ov == bv && ol < bl))) {
-          bv = ov;
-          bl = ol;
+      for (int u = 0; u < 4; ++u) {  // keys and groups loaded together
+        v[u] = i0 + u < nc ? __ldcg(blk_ck + static_cast<long long>(b) * kTopkBlkCand + i0 + u) : ~0ULL;
+        g[u] = i0 + u < nc ? __ldcg(blk_cg + static_cast<long long>(b) * kTopkBlkCand + i0 + u) : 0u;
+      }
+      bool more = true;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u < nc && v[u] <= T1) {
+          const int pos = atomicAdd(&s_nc, 1);
+          if (pos < kTopkCollect) {
+            cv[pos] = v[u];
+            cg[pos] = g[u];
+          }
+        } else {
+          more = false;
         }
       }
-      if (bl < 0) break;
-      T = bv;  // after k rounds: the k-th smallest
-      if (lane == 0) ++hpos[bl];
-      __syncwarp();
-    }
-    if (lane == 0) {
-      s_T = T;
-      s_nc = 0;
+      if (!more) break;  // sorted: the rest is above T1
     }
   }
   __syncthreads();
-  // final candidates: published entries with k0 <= T (one thread per block list)
-  const unsigned long long T = s_T;
-  unsigned* fg = reinterpret_cast<unsigned*>(cnb + nb);
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    const int ncb = cnb[b];
-    for (int i = 0; i < ncb; ++i) {
-      const long long e = static_cast<long long>(b) * kTopkBlkCand + i;
-      if (__ldcg(blk_ck + e) <= T) {
-        const int pos = atomicAdd(&s_nc, 1);
-        if (pos < kTopkFinal) fg[pos] = __ldcg(blk_cg + e);
-      }
+  stamp(tl + 7);
+  const int m = s_nc;
+  if (m > kTopkCollect) {  // ties: more entries at or below T1 than the collection holds
+    if (threadIdx.x == 0) {
+      err[0] = 1;
+      err[3] = FR_TOPK_FINAL;
+      *nout = 0;
+    }
+    return;
+  }
+  const unsigned long long T = block_kth(cv, m, k, s_red);
+  stamp(tl);
+  // final candidates: the collected entries <= T (the top k plus ties on k0)
+  unsigned* fg = reinterpret_cast<unsigned*>(bmin + kTopkThreads);
+  if (threadIdx.x == 0) s_nc = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += kTopkThreads) {
+    if (cv[i] <= T) {
+      const int pos = atomicAdd(&s_nc, 1);
+      if (pos < kTopkFinal) fg[pos] = cg[i];
     }
   }
   __syncthreads();
+  stamp(tl + 1);
   const int nfc = s_nc < kTopkFinal ? s_nc : kTopkFinal;
   if (threadIdx.x == 0 && s_nc > kTopkFinal) {
     err[0] = 1;
     err[3] = FR_TOPK_FINAL;
   }
-  // full keys of the final candidates, then the exact order (warp 0)
+  // full keys, one thread per (candidate, key word); then each candidate's
+  // rank among the candidates (keys are unique: the group keys end them)
   unsigned long long* fk = reinterpret_cast<unsigned long long*>(fg + kTopkFinal + 2);
   fk = reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(fk) + 7) & ~uintptr_t(7));
-  for (int i = threadIdx.x; i < nfc; i += blockDim.x) {
-    unsigned long long kk[NK];
-    cand_keys_nk<NK>(s, fg[i], kk);
-#pragma unroll
-    for (int q = 0; q < NK; ++q) fk[i * NK + q] = kk[q];
+  unsigned* og = reinterpret_cast<unsigned*>(fk + kTopkFinal * NK);  // output groups in order
+  for (int t = threadIdx.x; t < nfc * NK; t += kTopkThreads) {
+    const int i = t % nfc, q = t / nfc;
+    fk[i * NK + q] = cand_key_word(s, q, fg[i]);
   }
   __syncthreads();
-  if (warp == 0) {
-    TopkList<NK> F;
-    for (int i0 = 0; i0 < nfc; i0 += 32) {
-      const int i = i0 + lane;
-      unsigned long long kk[NK];
+  for (int i = threadIdx.x; i < nfc; i += kTopkThreads) {
+    int r = 0;
+    for (int j = 0; j < nfc; ++j) {
+      bool lt = false, eq = true;
 #pragma unroll
-      for (int q = 0; q < NK; ++q) kk[q] = i < nfc ? fk[i * NK + q] : ~0ULL;
-      F.offer(i < nfc, kk, i < nfc ? fg[i] : 0u, k);
-    }
-    if (lane < F.cnt) {
-      const unsigned g = F.gid;
-      for (int j = 0; j < s.f.nouts; ++j) {
-        unsigned long long bits;
-        bool f;
-        if (!group_out_value(s, j, g, bits, f)) {
-          err[0] = 1;
-          err[3] = FR_GROUP_VALUE;
-        }
-        store_group_out(s, j, lane, bits);
+      for (int q = 0; q < NK; ++q) {
+        const unsigned long long a = fk[j * NK + q], c = fk[i * NK + q];
+        lt = lt || (eq && a < c);
+        eq = eq && a == c;
       }
+      r += lt;
     }
-    if (lane == 0) *nout = F.cnt;
+    if (r < k) og[r] = fg[i];
+  }
+  __syncthreads();
+  stamp(tl + 2);
+  // output values: a thread per (row, column)
+  const int nrow = min(nfc, k);
+  if (threadIdx.x == 0) *nout = nrow;
+  for (int t = threadIdx.x; t < nrow * s.f.nouts; t += blockDim.x) {
+    const int r = t % nrow, j = t / nrow;
+    unsigned long long bits;
+    bool f;
+    if (!group_out_value(s, j, og[r], bits, f)) {
+      err[0] = 1;
+      err[3] = FR_GROUP_VALUE;
+    }
+    store_group_out(s, j, r, bits);
+  }
+  __syncthreads();
+  stamp(tl + 3);
+  if (trace && threadIdx.x == 0) {
+    trace[tl + 4] = static_cast<unsigned long long>(m);
+    trace[tl + 5] = static_cast<unsigned long long>(nfc);
   }
 }
 
-using TopkKernel = void (*)(GroupSpec, long long, int, unsigned long long*, int*, unsigned long long*, unsigned*, int*,
-                            unsigned*, long long*, long long*);
+// TQP_TOPK_TRACE: phase times of one k_topk_groups launch (stderr, us from
+// the first block's start): walk end and publish end over the blocks
+// (median / max), warp 0's walk cycles by part, then the last block's phases
+void topk_trace_report(Ctx& c, const std::shared_ptr<DevBuf>& tb, int nb) {
+  std::vector<unsigned long long> t(8 * nb + 12);
+  TQP_CUDA(cudaMemcpyAsync(t.data(), tb->ptr, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  unsigned long long t0 = ~0ULL;
+  for (int b = 0; b < nb; ++b) t0 = std::min(t0, t[8 * b]);
+  std::vector<double> we, pe, w5, w6, w7;
+  for (int b = 0; b < nb; ++b) {
+    we.push_back((t[8 * b + 1] - t0) / 1e3);
+    pe.push_back((t[8 * b + 2] - t0) / 1e3);
+    w5.push_back(t[8 * b + 5] / 1.965e3);
+    w6.push_back(t[8 * b + 6] / 1.965e3);
+    w7.push_back(t[8 * b + 7] / 1.965e3);
+  }
+  auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+  auto mx = [](const std::vector<double>& v) { return *std::max_element(v.begin(), v.end()); };
+  const long long tl = 8LL * nb;
+  auto at = [&](long long i) { return (t[tl + i] - t0) / 1e3; };
+  std::fprintf(stderr,
+               "topk trace nb=%d walk end med %.1f max %.1f | publish end med %.1f max %.1f | warp0 walk: presence "
+               "%.2f keys %.2f offers %.2f us\n",
+               nb, med(we), mx(we), med(pe), mx(pe), med(w5), med(w6), med(w7));
+  std::fprintf(stderr,
+               "topk trace last block: loads %.1f collect %.1f T %.1f finals %.1f keys+rank %.1f out %.1f | "
+               "collected %llu finals %llu\n",
+               at(6), at(7), at(0), at(1), at(2), at(3), t[tl + 4], t[tl + 5]);
+}
+
+// walk blocks per SM (TQP_TOPK_BPS tuning knob)
+int topk_bps() {
+  static const int v = [] {
+    const char* e = std::getenv("TQP_TOPK_BPS");
+    const int x = e ? std::atoi(e) : 4;
+    return x >= 1 && x <= 8 ? x : 4;
+  }();
+  return v;
+}
+
+using TopkKernel = void (*)(GroupSpec, long long, int, unsigned long long*, unsigned*, int*, unsigned*, long long*,
+                            long long*, unsigned long long*);
 TopkKernel topk_kernel(int nk) {
   switch (nk) {
     case 1: return k_topk_groups<1>;
@@ -1886,7 +2062,7 @@ TopkKernel topk_kernel(int nk) {
   }
 }
 
-__global__ void k_group_rows(GroupSpec s, const long long* __restrict__ gids, const long long* __restrict__ order,
+__global__ void k_group_rows(const __grid_constant__ GroupSpec s, const long long* __restrict__ gids, const long long* __restrict__ order,
                              long long n, long long* err) {
   for (long long r = gtid(); r < n; r += gstride()) {
     unsigned g = static_cast<unsigned>(gids[order[r]]);
@@ -1944,7 +2120,7 @@ constexpr int kSmallPartWords = static_cast<int>(sizeof(SmallPart) / sizeof(unsi
 static_assert(sizeof(SmallPart) % sizeof(unsigned long long) == 0, "SmallPart must be word-sized");
 constexpr int record_words(int nkeyc, int nacc) { return 2 + nkeyc + 2 * nacc; }
 
-__global__ void k_fill_records(GroupSpec s, const long long* __restrict__ gids, long long n,
+__global__ void k_fill_records(const __grid_constant__ GroupSpec s, const long long* __restrict__ gids, long long n,
                                const long long* __restrict__ bkey, int words, unsigned long long* __restrict__ out,
                                long long* err) {
   for (long long i = gtid(); i < n; i += gstride()) {
@@ -2464,7 +2640,8 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
   };
   static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
   o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << (staged ? tile_rows / (cw * 32) : jit_build_rows())
-    << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0) << "\n#define B_ZREC " << b.zrec_words << "\n";
+    << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0) << "\n#define B_ZREC " << b.zrec_words
+    << "\n#define B_UNIQUE " << (b.unique ? 1 : 0) << "\n";
   if (staged) o << "#define QB_CW " << cw << "\n#define QB_ROWS " << tile_rows << "\n";
   o << "namespace tqp { namespace fz {\n";
   if (staged) {
@@ -3121,6 +3298,50 @@ struct Runner {
         arena += (sizeof(unsigned) * static_cast<size_t>((range + 31) / 32 + 1) + 255) & ~size_t(255);
       }
     }
+    // does a direct-addressed build's key column repeat a value? Checked once
+    // per column (one bitmap pass and one host round trip for all of them)
+    // and cached with its range: a build over a unique key sets its presence
+    // bits fire-and-forget (presence_insert_unique) instead of checking every
+    // returned word for a repeated key
+    {
+      std::vector<size_t> uq;
+      for (size_t bi = 0; bi < nb; ++bi) {
+        if (hashed[bi] || gn[bi] >= 0) continue;
+        const Table* tab = bind_table(tables, P.builds[bi].table);
+        if (!tab->rows) continue;
+        const Column* key = tab->find(P.builds[bi].key_column);
+        std::lock_guard<std::mutex> lk(key->range->mu);
+        if (key->range->unique < 0) uq.push_back(bi);
+      }
+      if (!uq.empty()) {
+        size_t bytes = 256;
+        std::vector<size_t> off;
+        for (size_t bi : uq) {
+          off.push_back(bytes);
+          bytes += (sizeof(unsigned) * static_cast<size_t>((slots_of[bi] + 31) / 32) + 255) & ~size_t(255);
+        }
+        if (uq.size() > 64) return nofuse(__LINE__);
+        auto ub = c.alloc_bytes(bytes);
+        TQP_CUDA(cudaMemsetAsync(ub->ptr, 0, bytes, c.stream));
+        unsigned char* up = static_cast<unsigned char*>(ub->ptr);
+        for (size_t j = 0; j < uq.size(); ++j) {
+          const Table* tab = bind_table(tables, P.builds[uq[j]].table);
+          const Column* key = tab->find(P.builds[uq[j]].key_column);
+          k_key_unique<<<c.grid_for(tab->rows, 256, 4, 16), 256, 0, c.stream>>>(
+              key->t.ptr<long long>(), tab->rows, mm[2 * uq[j]], reinterpret_cast<unsigned*>(up + off[j]),
+              reinterpret_cast<int*>(up) + j);
+          c.count_launch();
+        }
+        std::vector<int> dupf(uq.size());
+        TQP_CUDA(cudaMemcpyAsync(dupf.data(), up, sizeof(int) * uq.size(), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        for (size_t j = 0; j < uq.size(); ++j) {
+          const Column* key = bind_table(tables, P.builds[uq[j]].table)->find(P.builds[uq[j]].key_column);
+          std::lock_guard<std::mutex> lk(key->range->mu);
+          key->range->unique = dupf[j] ? 0 : 1;
+        }
+      }
+    }
     auto err_buf = c.alloc_bytes(arena);
     TQP_CUDA(cudaMemsetAsync(err_buf->ptr, 0, arena, c.stream));
     long long* err = static_cast<long long*>(err_buf->ptr);
@@ -3136,6 +3357,10 @@ struct Runner {
       bs.n = n;
       bs.kmin = (n || gn[bi] > 0) ? mm[2 * bi] : 0;
       bs.range = range;
+      if (!hashed[bi] && gn[bi] < 0 && n) {
+        std::lock_guard<std::mutex> lk(key->range->mu);
+        bs.unique = key->range->unique == 1 ? 1 : 0;
+      }
       auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
       // a filtered build's table is only read where its presence bit is set
       // (probe_lookup and every generated probe check the bitmap first), so
@@ -3974,24 +4199,29 @@ struct Runner {
       const int nk = gs.nsort + gs.nkeyc;
       TopkKernel kern = topk_kernel(nk);
       if (!kern || k > kTopkMaxK || gs.nsort < 1) return false;
-      // one wave: as many blocks as are resident at once (the last block
-      // merges one value list per block)
+      // one wave: as many blocks as are resident at once, up to topk_bps()
+      // per SM (the last block reads one value list per block)
       const int per_sm = c.blocks_per_sm(reinterpret_cast<const void*>(kern), kTopkThreads);
       const int blocks = static_cast<int>(std::max<long long>(
-          1, std::min<long long>({static_cast<long long>(std::max(1, std::min(per_sm, 2))) * c.num_sms,
-                                  (ngroups + 8191) / 8192, static_cast<long long>(kTopkStage / std::max(1, k))})));
-      auto bval = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkMaxK);
+          1, std::min<long long>({static_cast<long long>(std::max(1, std::min(per_sm, topk_bps()))) * c.num_sms,
+                                  (ngroups + 8191) / 8192, static_cast<long long>(kTopkMaxBlocks)})));
       auto bck = c.alloc_bytes(sizeof(unsigned long long) * blocks * kTopkBlkCand);
       auto bcg = c.alloc_bytes(sizeof(unsigned) * blocks * kTopkBlkCand);
-      auto bn = c.alloc_bytes(sizeof(int) * 2 * blocks + 16);
-      int* bnval = static_cast<int*>(bn->ptr);
-      int* bnc = bnval + blocks;
+      auto bn = c.alloc_bytes(sizeof(int) * blocks + 16);
+      int* bnc = static_cast<int*>(bn->ptr);
       // the last-block ticket lives after the error words (zeroed with them)
       unsigned* ticket = reinterpret_cast<unsigned*>(err + 4);
-      kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bval->ptr), bnval,
-                                                  static_cast<unsigned long long*>(bck->ptr),
-                                                  static_cast<unsigned*>(bcg->ptr), bnc, ticket, err + 2, err);
+      static const bool tracing = std::getenv("TQP_TOPK_TRACE") != nullptr;
+      std::shared_ptr<DevBuf> tb;
+      if (tracing) {
+        tb = c.alloc_bytes(sizeof(unsigned long long) * (8 * blocks + 12));
+        TQP_CUDA(cudaMemsetAsync(tb->ptr, 0, tb->bytes, c.stream));
+      }
+      kern<<<blocks, kTopkThreads, 0, c.stream>>>(gs, ngroups, k, static_cast<unsigned long long*>(bck->ptr),
+                                                  static_cast<unsigned*>(bcg->ptr), bnc, ticket, err + 2, err,
+                                                  tb ? static_cast<unsigned long long*>(tb->ptr) : nullptr);
       c.count_launch();
+      if (tracing) topk_trace_report(c, tb, blocks);
       nrows = -1;  // on the device (err[2]); read with the error flag
       return true;
     }

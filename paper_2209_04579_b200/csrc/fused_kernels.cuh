@@ -27,6 +27,20 @@ namespace tqp {
 namespace fz {
 
 // ---- build kernel ------------------------------------------------------------
+// Does a key column repeat a value? One pass setting a bit per key over its
+// (known) range; a bit already set flags the column (*dup = 1). Run once per
+// column, the first time a direct-addressed build keys on it (KeyRange::unique).
+__global__ void __launch_bounds__(256) k_key_unique(const long long* __restrict__ k, long long n, long long kmin,
+                                                    unsigned* __restrict__ bits, int* __restrict__ dup) {
+  bool rep = false;
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const unsigned long long idx = static_cast<unsigned long long>(__ldg(k + i) - kmin);
+    const unsigned b = 1u << (idx & 31);
+    rep = rep || (atomicOr(bits + (idx >> 5), b) & b) != 0u;
+  }
+  if (__any_sync(0xffffffffu, rep) && (threadIdx.x & 31) == 0) atomicExch(dup, 1);
+}
+
 // key range of a build side: 128-bit loads, warp then block reduction, one
 // atomic pair per block (a per-warp atomic on one address serialises at L2)
 // DAY: also out[2] |= 1 if a value is not a whole number of days in ns (a
@@ -168,7 +182,10 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
           }
         }
       }
-      if (!s.hkeys) presence_insert(s.bitmap, idx, old[j], set[j], dup);
+      if (!s.hkeys) {
+        if (s.unique) presence_insert_unique(s.bitmap, idx);
+        else presence_insert(s.bitmap, idx, old[j], set[j], dup);
+      }
     }
     if (!s.mult) {
 #pragma unroll

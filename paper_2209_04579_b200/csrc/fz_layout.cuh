@@ -248,6 +248,9 @@ struct BuildSpec {
   unsigned long long* zrec = nullptr;
   int zrec_words = 0;
   long long* err = nullptr;
+  // the key column holds no repeated value (KeyRange::unique): presence bits
+  // are set fire-and-forget, nothing to check (presence_insert_unique)
+  int unique = 0;
 };
 
 // Presence bits of one insert round of a warp. Sparse rounds (few lanes
@@ -282,6 +285,23 @@ __device__ __forceinline__ void presence_insert(unsigned* bitmap, long long idx,
     set = bits;
     dup |= __popc(bits) != __popc(peers) ? 1u : 0u;
   }
+}
+// Presence bits over a key column known to hold no repeated value: the same
+// sparse / warp-aggregated rounds as presence_insert, but the old words are
+// never needed, so the atomics do not return (RED) and no thread waits on one
+// (Q3's orders build: the wait on the returned words at the end of every
+// thread was part of its latency chain).
+__device__ __forceinline__ void presence_insert_unique(unsigned* bitmap, long long idx) {
+  const unsigned active = __ballot_sync(0xffffffffu, idx >= 0);
+  if (__popc(active) < 8) {  // warp-uniform
+    if (idx >= 0) atomicOr(bitmap + (idx >> 5), 1u << (idx & 31));
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const unsigned word = idx >= 0 ? static_cast<unsigned>(idx >> 5) : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, word);
+  const unsigned bits = __reduce_or_sync(peers, idx >= 0 ? 1u << (idx & 31) : 0u);
+  if (idx >= 0 && lane == __ffs(peers) - 1) atomicOr(bitmap + word, bits);
 }
 __device__ __forceinline__ void set_fallback(long long* err, long long reason) {
   atomicExch(reinterpret_cast<unsigned long long*>(err), 1ULL);

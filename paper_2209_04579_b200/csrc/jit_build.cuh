@@ -52,7 +52,11 @@ extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[j]) << 57);
         }
       }
+#if B_UNIQUE
+      presence_insert_unique(s.bitmap, idx);
+#else
       presence_insert(s.bitmap, idx, old[j], set[j], dup);
+#endif
     }
 #pragma unroll
     for (int j = 0; j < B_ROWS; ++j) dup |= old[j] & set[j];

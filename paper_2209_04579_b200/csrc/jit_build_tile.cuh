@@ -88,7 +88,11 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
           b.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[k]) << 57);
         }
       }
+#if B_UNIQUE
+      presence_insert_unique(b.bitmap, idx);
+#else
       presence_insert(b.bitmap, idx, old[k], set[k], dup);
+#endif
     }
 #pragma unroll
     for (int k = 0; k < QB_R; ++k) dup |= old[k] & set[k];
