@@ -1355,6 +1355,7 @@ struct GroupSpec {
   int limb2 = 0;                      // MODE_HASH 2-limb sums (checked per group against fmax)
   const long long* fmax = nullptr;    // max |fp64 value| (bits) of the scan
   int direct_codes = 0;               // MODE_HASH direct table: the group's code is its slot
+  int row_in_cnt = 0;                 // BUILDGRP row_rec build: count word = (row + 1) << 32 | rows
 };
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g);
@@ -1371,7 +1372,7 @@ __device__ __forceinline__ long long group_key_value(const GroupSpec& s, int i, 
 }
 __device__ __forceinline__ long long group_count(const GroupSpec& s, unsigned g) {
   const unsigned long long w = s.gcnt[g * s.cnt_stride];
-  return static_cast<long long>(s.cnt_packed ? (w & kCntMask) : w);
+  return static_cast<long long>(s.cnt_packed ? (w & kCntMask) : s.row_in_cnt ? (w & 0xffffffffULL) : w);
 }
 // limb words exact: fewer than kLimbMaxRows adds reached them
 __device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
@@ -1382,7 +1383,7 @@ __device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
   }
   if (s.acc_words != kLimbWords) return true;
   const unsigned long long w = s.gcnt[g * s.cnt_stride];
-  return (s.cnt_packed ? (w >> 40) : w) < static_cast<unsigned long long>(kLimbMaxRows);
+  return (s.cnt_packed ? (w >> 40) : s.row_in_cnt ? (w & 0xffffffffULL) : w) < static_cast<unsigned long long>(kLimbMaxRows);
 }
 
 // accumulator a of group g as int128
@@ -1394,6 +1395,7 @@ __device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, in
 }
 
 __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned g) {
+  if (s.row_in_cnt) return static_cast<long long>(s.gcnt[g * s.cnt_stride] >> 32) - 1;
   return s.group_table ? static_cast<long long>(s.group_table[g] & 0xffffffffULL) - 1 : static_cast<long long>(g);
 }
 
@@ -1714,6 +1716,7 @@ __global__ void __launch_bounds__(kTopkThreads) k_topk_groups(const __grid_const
         const int i = c0 + u * 32 + lane;
         gq[u] = i < total ? static_cast<unsigned>(base) + sidx[i] : 0u;
         gc[u] = i < total ? s.gcnt[gq[u] * s.cnt_stride] : 0ULL;
+        if (s.row_in_cnt) gc[u] &= 0xffffffffULL;
       }
 #pragma unroll
       for (int u = 0; u < kTopkUnroll; ++u) {
@@ -2079,9 +2082,9 @@ __global__ void k_group_rows(const __grid_constant__ GroupSpec s, const long lon
 }
 
 __global__ void k_nonzero_groups(const unsigned long long* __restrict__ cnt, long long cnt_stride, long long n,
-                                 const unsigned* present, uint8_t* __restrict__ mask) {
+                                 const unsigned* present, unsigned long long cmask, uint8_t* __restrict__ mask) {
   for (long long i = gtid(); i < n; i += gstride())
-    mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && cnt[i * cnt_stride] != 0;
+    mask[i] = (!present || ((__ldg(present + (i >> 5)) >> (i & 31)) & 1u)) && (cnt[i * cnt_stride] & cmask) != 0;
 }
 
 // MODE_HASH direct tables: bit per slot with rows
@@ -2101,11 +2104,18 @@ __global__ void k_hash_present(const unsigned long long* __restrict__ tag, long 
     if ((threadIdx.x & 31) == 0) present[i >> 5] = bits;
   }
 }
-__global__ void k_group_keys(const unsigned long long* __restrict__ group_table, const long long* __restrict__ gids, long long n,
+// the build key of each group: through the group table, or (row_rec) the
+// row kept in bits 32-63 of the group's count word
+__global__ void k_group_keys(const unsigned long long* __restrict__ group_table, const unsigned long long* __restrict__ rowcnt,
+                             long long cnt_stride, const long long* __restrict__ gids, long long n,
                              const long long* __restrict__ key_col, long long* __restrict__ out) {
-  for (long long i = gtid(); i < n; i += gstride())
-    out[i] = key_col ? key_col[group_table ? static_cast<long long>(group_table[gids[i]] & 0xffffffffULL) - 1 : gids[i]]
-                     : gids[i];
+  for (long long i = gtid(); i < n; i += gstride()) {
+    const long long g = gids[i];
+    const long long row = group_table ? static_cast<long long>(group_table[g] & 0xffffffffULL) - 1
+                          : rowcnt    ? static_cast<long long>(rowcnt[g * cnt_stride] >> 32) - 1
+                                      : g;
+    out[i] = key_col ? key_col[row] : g;
+  }
 }
 
 // ---- sharded-run partials ------------------------------------------------------
@@ -2582,7 +2592,9 @@ int build_tile_rows() {
 int jit_build_rows() {
   static const int r = [] {
     const char* e = std::getenv("TQP_BUILD_ROWS");  // tuning knob: rows per thread of q_build
-    const int v = e ? std::atoi(e) : 2;  // Q3 orders build SF10: 108 us at 2, 115 at 4, 150 at 8
+    // Q3 orders build SF10: 108 us at 2, 115 at 4, 150 at 8 with a table
+    // entry per row; with the row in the group record: 89 us at 2, 81 at 4
+    const int v = e ? std::atoi(e) : 4;
     return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
   }();
   return r;
@@ -2641,7 +2653,7 @@ std::string gen_build(const BuildSpec& b, bool staged = false,
   static const char* ops[] = {"==", "!=", "<", "<=", ">", ">="};
   o << "#include \"fz_layout.cuh\"\n#define B_ROWS " << (staged ? tile_rows / (cw * 32) : jit_build_rows())
     << "\n#define B_ASSIGN " << (b.assign_groups ? 1 : 0) << "\n#define B_ZREC " << b.zrec_words
-    << "\n#define B_UNIQUE " << (b.unique ? 1 : 0) << "\n";
+    << "\n#define B_UNIQUE " << (b.unique ? 1 : 0) << "\n#define B_ROWREC " << (b.row_rec ? 1 : 0) << "\n";
   if (staged) o << "#define QB_CW " << cw << "\n#define QB_ROWS " << tile_rows << "\n";
   o << "namespace tqp { namespace fz {\n";
   if (staged) {
@@ -2770,6 +2782,7 @@ std::string tile_key(TileSpec t) {
   for (auto& pr : t.p.probes) {
     pr.table = nullptr;
     pr.bitmap = nullptr;
+    pr.rowrec = nullptr;
   }
   std::string k;
   append_bytes(k, t);
@@ -2783,6 +2796,7 @@ std::string build_key(BuildSpec b) {
   for (auto& pr : b.probes) {
     pr.table = nullptr;
     pr.bitmap = nullptr;
+    pr.rowrec = nullptr;
   }
   std::string k;
   append_bytes(k, b);
@@ -3172,6 +3186,7 @@ struct Runner {
     std::vector<std::shared_ptr<DevBuf>> keep;
     std::vector<long long> build_range(P.builds.size(), 0);
     const unsigned long long* group_table = nullptr;
+    bool row_rec_grp = false;
     const unsigned* group_present = nullptr;
     unsigned long long* grec_p = nullptr;
     int grec_words = 0;
@@ -3361,7 +3376,10 @@ struct Runner {
         std::lock_guard<std::mutex> lk(key->range->mu);
         bs.unique = key->range->unique == 1 ? 1 : 0;
       }
-      auto table = c.alloc_bytes(sizeof(unsigned long long) * range);
+      // a flagless group-assigning direct build keeps its rows in the group
+      // records (BuildSpec::row_rec): no table at all
+      const bool row_rec = B.assign_groups && B.flags.empty() && !hashed[bi] && gn[bi] < 0;
+      auto table = c.alloc_bytes(row_rec ? 0 : sizeof(unsigned long long) * range);
       // a filtered build's table is only read where its presence bit is set
       // (probe_lookup and every generated probe check the bitmap first), so
       // only an unfiltered one, read as `entry != 0`, needs zeroed slots -
@@ -3369,7 +3387,7 @@ struct Runner {
       // range (a repeated key leaves a slot unwritten, but it is flagged as
       // a duplicate and the unit is discarded). A hashed table's entries are
       // only read where the slot's key matched (written by the claiming row).
-      if (!hashed[bi] && ((!build_filtered(B) && range != n) || weighted))
+      if (!row_rec && !hashed[bi] && ((!build_filtered(B) && range != n) || weighted))
         TQP_CUDA(cudaMemsetAsync(table->ptr, 0, sizeof(unsigned long long) * range, c.stream));
       if (hashed[bi]) {
         auto hk = c.alloc_bytes(sizeof(long long) * range);
@@ -3385,7 +3403,8 @@ struct Runner {
         bs.mult = static_cast<unsigned*>(mu->ptr);
       }
       keep.push_back(table);
-      bs.table = static_cast<unsigned long long*>(table->ptr);
+      bs.table = row_rec ? nullptr : static_cast<unsigned long long*>(table->ptr);
+      bs.row_rec = row_rec ? 1 : 0;
       build_range[bi] = range;
       bs.bitmap = reinterpret_cast<unsigned*>(arena_p + bm_off[bi]);
       bs.err = err;
@@ -3424,7 +3443,8 @@ struct Runner {
         grec_words = (1 + kLimbWords * std::max(1, nacc_all) + 3) & ~3;
         auto grec = c.alloc_bytes(sizeof(unsigned long long) * grec_words * (range + 1));
         keep.push_back(grec);
-        group_table = bs.table;
+        group_table = bs.table;  // nullptr for a row_rec build (rows in the records)
+        row_rec_grp = row_rec;
         group_present = bs.bitmap;
         grec_p = static_cast<unsigned long long*>(grec->ptr);
         bs.assign_groups = 1;
@@ -3536,6 +3556,10 @@ struct Runner {
       pr.kmin = bs.kmin;
       pr.range = range;
       pr.table = bs.table;
+      if (bs.row_rec) {
+        pr.rowrec = bs.zrec;
+        pr.rstride = bs.zrec_words;
+      }
       pr.bitmap = hashed[bi] ? nullptr : bs.bitmap;
       pr.hkeys = bs.hkeys;
       pr.hmask = bs.hmask;
@@ -3986,6 +4010,7 @@ struct Runner {
       gs.gacc = ps.gacc;
       gs.gcnt = ps.gcnt;
       gs.group_table = group_table;
+      gs.row_in_cnt = row_rec_grp ? 1 : 0;
       gs.cnt_stride = grec_words;
       gs.acc_stride = grec_words;
       gs.present = ps.touched;  // groups with rows (a subset of the inserted slots)
@@ -4002,7 +4027,7 @@ struct Runner {
       if (po) {
         // the touched groups as self-describing records, keyed by the unique
         // build key: shards may split a group (the merge adds exactly)
-        Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, ngroups, ps.touched);
+        Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, ngroups, ps.touched, row_rec_grp ? 0xffffffffULL : ~0ULL);
         const long long n = gids.rows;
         const int words = record_words(gs.nkeyc, fs.nacc);
         unsigned long long* rec = part_buf(n, words);
@@ -4142,11 +4167,12 @@ struct Runner {
     return -1;  // on the device (err[2]); read with the error flag
   }
 
+  // cmask: the count bits of a count word (row_in_cnt: the low 32)
   static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long cnt_stride, long long ngroups,
-                               const unsigned* present) {
+                               const unsigned* present, unsigned long long cmask = ~0ULL) {
     Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
     if (ngroups) {
-      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, cnt_stride, ngroups, present,
+      k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, cnt_stride, ngroups, present, cmask,
                                                                        mask.ptr<uint8_t>());
       c.count_launch();
     }
@@ -4231,7 +4257,8 @@ struct Runner {
   // every group with rows, ascending by its (unique) key `bk`
   bool emit_all_groups(Ctx& c, GroupSpec gs, long long ngroups, const long long* bk, long long* err,
                        std::vector<Tensor>& outs, long long& nrows, bool gids_sorted = false) const {
-    Tensor gids = touched_groups(c, gs.gcnt, gs.cnt_stride, ngroups, gs.present);
+    Tensor gids = touched_groups(c, gs.gcnt, gs.cnt_stride, ngroups, gs.present,
+                                 gs.row_in_cnt ? 0xffffffffULL : ~0ULL);
     const long long n = gids.rows;
     Tensor order;
     if (gids_sorted) {
@@ -4239,7 +4266,8 @@ struct Runner {
     } else {
       Tensor keys = c.alloc(TQP_I64, n, 1);
       if (n) {
-        k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gids.ptr<long long>(), n, bk,
+        k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gs.row_in_cnt ? gs.gcnt : nullptr,
+                                                                gs.cnt_stride, gids.ptr<long long>(), n, bk,
                                                                 keys.ptr<long long>());
         c.count_launch();
       }

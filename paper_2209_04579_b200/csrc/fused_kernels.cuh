@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(kThreads) k_build(const BuildSpec s) {
           } else {
             if (s.assign_groups)  // the group is the key slot: zero its record
               for (int w = 0; w < s.zrec_words; ++w) s.zrec[idx * s.zrec_words + w] = 0ULL;
-            s.table[idx] = entry;
+            if (s.row_rec) s.zrec[idx * s.zrec_words] = static_cast<unsigned long long>(entry & 0xffffffffULL) << 32;
+            else s.table[idx] = entry;
             if (s.mult) atomicAdd(s.mult + idx, wgt[j]);
           }
         }

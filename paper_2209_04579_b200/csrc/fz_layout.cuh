@@ -118,6 +118,9 @@ struct Probe {
   const long long* hkeys = nullptr;  // open addressing: keys per slot
   unsigned long long hmask = 0;
   const unsigned* mult = nullptr;    // weighted (1:N) builds: multiplicity per slot
+  // row_rec builds (no table): the row is bits 32-63 of rowrec[slot * rstride]
+  const unsigned long long* rowrec = nullptr;
+  long long rstride = 0;
 };
 
 __device__ __forceinline__ unsigned long long build_hslot(long long key, unsigned long long mask) {
@@ -251,6 +254,10 @@ struct BuildSpec {
   // the key column holds no repeated value (KeyRange::unique): presence bits
   // are set fire-and-forget, nothing to check (presence_insert_unique)
   int unique = 0;
+  // a flagless group-assigning build keeps the row in its record's count
+  // word (bits 32-63 = row + 1) instead of a table entry: one 32-byte
+  // sector written per inserted row instead of two
+  int row_rec = 0;
 };
 
 // Presence bits of one insert round of a warp. Sparse rounds (few lanes
@@ -428,7 +435,7 @@ __device__ __forceinline__ bool probe_lookup(const Probe& p, long long key, long
     if (idx < 0 || idx >= p.range) return false;
     if (p.bitmap && !((__ldg(p.bitmap + (idx >> 5)) >> (idx & 31)) & 1u)) return false;
   }
-  unsigned long long e = __ldg(p.table + idx);
+  unsigned long long e = p.table ? __ldg(p.table + idx) : p.rowrec[idx * p.rstride] >> 32;
   if (!e) return false;
   rid = static_cast<long long>(e & 0xffffffffULL) - 1;
   gid = static_cast<unsigned>(idx);  // a group-assigning build's group is its key slot

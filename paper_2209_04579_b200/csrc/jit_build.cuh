@@ -49,7 +49,12 @@ extern "C" __global__ void __launch_bounds__(kThreads) q_build(const BuildSpec s
             for (int w = 0; w < B_ZREC / 2; ++w) rec[w] = make_ulonglong2(0ULL, 0ULL);
           }
 #endif
+#if B_ROWREC
+          // the row is kept in the record's count word (bits 32-63), no table
+          reinterpret_cast<unsigned long long*>(s.zrec)[idx * B_ZREC] = static_cast<unsigned long long>(r + 1) << 32;
+#else
           s.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[j]) << 57);
+#endif
         }
       }
 #if B_UNIQUE

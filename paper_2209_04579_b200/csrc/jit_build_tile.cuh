@@ -85,7 +85,11 @@ extern "C" __global__ void __launch_bounds__(QB_CT + 32, 1) q_build_tile(const T
             for (int w = 0; w < B_ZREC / 2; ++w) rec[w] = make_ulonglong2(0ULL, 0ULL);
           }
 #endif
+#if B_ROWREC
+          b.zrec[idx * B_ZREC] = static_cast<unsigned long long>(r + 1) << 32;
+#else
           b.table[idx] = static_cast<unsigned long long>(r + 1) | (static_cast<unsigned long long>(flags[k]) << 57);
+#endif
         }
       }
 #if B_UNIQUE
