@@ -10,7 +10,7 @@ namespace tqp {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
+constexpr int kItems = 8;  // rows per thread (warp-striped): 2048-row tiles
 constexpr int kTile = kThreads * kItems;
 
 struct ScanScratch {
@@ -31,77 +31,126 @@ ScanScratch scan_scratch(Ctx& c, int64_t tiles) {
 
 // Exclusive int64 scan; reports the first row where the sequential
 // accumulation overflows (the reference's check order, kernels.cpp:356-359).
+// Warp-striped tiles: warp w of a tile owns rows [w * 32 * kItems, ...) of
+// it, item j of lane l is row j * 32 + l, so every load and store of a warp
+// is one contiguous 256-byte run (a blocked layout - kItems consecutive rows
+// per thread - ran the scans at 0.3 of HBM bandwidth: each warp access
+// touched 32 lines). Within a warp the rows are scanned item by item with
+// shuffles, carrying the running total; warps combine through shared
+// memory, tiles through the decoupled lookback.
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+// per-warp totals -> exclusive warp offsets (s_warp[w]) and the tile total
+// (s_warp[kThreads / 32]); the tile's exclusive prefix from the lookback in
+// *s_prefix. Called by every thread.
+__device__ __forceinline__ void tile_offsets(unsigned long long wtotal, unsigned long long* s_warp, long long* s_prefix,
+                                             longlong2* desc, int tile) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kW = kThreads / 32;
+  if (lane == 0) s_warp[warp] = wtotal;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long w = lane < kW ? s_warp[lane] : 0ULL;
+    const unsigned long long wi = warp_incl_scan(w);
+    __syncwarp();
+    if (lane < kW) s_warp[lane] = wi - w;
+    const unsigned long long total = __shfl_sync(0xffffffffu, wi, kW - 1);
+    const long long pfx = tile_lookback(desc, tile, static_cast<long long>(total));
+    if (lane == 0) {
+      s_warp[kW] = total;
+      *s_prefix = pfx;
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restrict__ x, int64_t* __restrict__ out,
                                                          int64_t n, longlong2* desc, int* counter, long long* err) {
   __shared__ int s_tile;
-  __shared__ unsigned long long s_warp[33];
+  __shared__ unsigned long long s_warp[kThreads / 32 + 1];
   __shared__ long long s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t base = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(warp) * 32 * kItems + lane;
   int64_t v[kItems];
-  unsigned long long local = 0;
+  unsigned long long ex[kItems];  // exclusive prefix within the warp
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) v[j] = wbase + j * 32 < n ? x[wbase + j * 32] : 0;
+  unsigned long long carry = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    v[j] = base + j < n ? x[base + j] : 0;
-    local += static_cast<unsigned long long>(v[j]);
+    const unsigned long long is = warp_incl_scan(static_cast<unsigned long long>(v[j]));
+    ex[j] = carry + is - static_cast<unsigned long long>(v[j]);
+    carry += __shfl_sync(0xffffffffu, is, 31);
   }
-  unsigned long long total;
-  unsigned long long texcl = block_exclusive_scan(local, s_warp, &total);
-  if (threadIdx.x < 32) {
-    long long p = tile_lookback(desc, tile, static_cast<long long>(total));
-    if (threadIdx.x == 0) s_prefix = p;
-  }
-  __syncthreads();
-  unsigned long long acc = static_cast<unsigned long long>(s_prefix) + texcl;
+  tile_offsets(carry, s_warp, &s_prefix, desc, tile);
+  const unsigned long long off = static_cast<unsigned long long>(s_prefix) + s_warp[warp];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    if (base + j < n) {
-      out[base + j] = static_cast<int64_t>(acc);
+    const int64_t i = wbase + j * 32;
+    if (i < n) {
+      const unsigned long long acc = off + ex[j];
+      out[i] = static_cast<int64_t>(acc);
       int64_t r;
-      if (add_ovf(static_cast<int64_t>(acc), v[j], &r)) note_bad(err, base + j);
-      acc += static_cast<unsigned long long>(v[j]);
+      if (add_ovf(static_cast<int64_t>(acc), v[j], &r)) note_bad(err, i);
     }
   }
 }
 
 // Single-pass order-preserving compaction: a tile (dynamic id, so the
-// lookback always waits on tiles already running) counts its selected rows
-// (one 8-byte mask load per thread, a popcount of the nonzero bytes), takes
-// its output offset from the decoupled lookback and scatters whole rows.
+// lookback always waits on tiles already running) ranks its selected rows
+// with one ballot + popcount per warp item, takes its output offset from the
+// decoupled lookback, and each warp item's selected rows go to consecutive
+// output rows (coalesced, warp-striped as the prefix sum). Rows of several
+// columns (m > 1) are copied column by column per selected row.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_compact_onepass(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
                                                               int64_t n, int64_t m, T* __restrict__ out, longlong2* desc,
                                                               int* counter) {
   __shared__ int s_tile;
-  __shared__ unsigned long long s_warp[33];
+  __shared__ unsigned long long s_warp[kThreads / 32 + 1];
   __shared__ long long s_prefix;
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
   __syncthreads();
   const int tile = s_tile;
-  const int64_t base = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(threadIdx.x) * kItems;
-  unsigned sel = 0;  // bit j: row base + j selected
-  if (base + kItems <= n) {
-    const unsigned long long w = *reinterpret_cast<const unsigned long long*>(mask + base);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t wbase = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(warp) * 32 * kItems + lane;
+  unsigned ball[kItems];
+  T v[kItems];
+  unsigned carry = 0;
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) sel |= ((w >> (8 * j)) & 0xffULL) ? (1u << j) : 0u;
-  } else {
+  for (int j = 0; j < kItems; ++j) {
+    const int64_t i = wbase + j * 32;
+    const bool sel = i < n && mask[i] != 0;
+    if (m == 1) v[j] = i < n ? vals[i] : T{};
+    ball[j] = __ballot_sync(0xffffffffu, sel);
+    carry += __popc(ball[j]);
+  }
+  tile_offsets(carry, s_warp, &s_prefix, desc, tile);
+  unsigned long long w = static_cast<unsigned long long>(s_prefix) + s_warp[warp];
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) sel |= (base + j < n && mask[base + j]) ? (1u << j) : 0u;
-  }
-  unsigned long long total;
-  const unsigned long long texcl = block_exclusive_scan(__popc(sel), s_warp, &total);
-  if (threadIdx.x < 32) {
-    const long long p = tile_lookback(desc, tile, static_cast<long long>(total));
-    if (threadIdx.x == 0) s_prefix = p;
-  }
-  __syncthreads();
-  unsigned long long w = static_cast<unsigned long long>(s_prefix) + texcl;
-  for (unsigned b = sel; b; b &= b - 1) {
-    const int j = __ffs(b) - 1;
-    for (int64_t q = 0; q < m; ++q) out[w * m + q] = vals[(base + j) * m + q];
-    ++w;
+  for (int j = 0; j < kItems; ++j) {
+    if ((ball[j] >> lane) & 1u) {
+      const unsigned long long pos = w + __popc(ball[j] & lt_mask);
+      if (m == 1) {
+        out[pos] = v[j];
+      } else {
+        const int64_t i = wbase + j * 32;
+        for (int64_t q = 0; q < m; ++q) out[pos * m + q] = vals[i * m + q];
+      }
+    }
+    w += __popc(ball[j]);
   }
 }
 
@@ -139,19 +188,81 @@ __global__ void k_sorted_check(const T* __restrict__ v, int64_t n, long long* er
     if (v[i] < v[i - 1]) note_bad(err, i);
 }
 
+// Binary search with the top of the tree in shared memory: every block
+// stages kSearchPivots evenly spaced keys, and a probe first finds its pivot
+// interval there, then searches only that interval (n / kSearchPivots keys)
+// in global memory. Each warp takes a contiguous run of probes (lane l: rows
+// run + 32 t + l), so a lane's consecutive probes are 32 rows apart: when a
+// probe is not below the lane's previous one (sorted probe columns, e.g.
+// lineitem's l_orderkey), its answer is at or after the previous answer and
+// an exponential search from there finds it in a step or two; otherwise (or
+// after kGallop doublings) the pivot search runs. Result: the first index
+// whose key does not go right (left: s[k] < x, right: s[k] <= x).
+constexpr int kSearchPivots = 2048;
+constexpr int kGallop = 8;
 template <typename T>
-__global__ void k_searchsorted(const T* __restrict__ s, int64_t n, const T* __restrict__ p, int64_t np, bool left,
-                               int64_t* __restrict__ out) {
-  for (int64_t i = gtid(); i < np; i += gstride()) {
-    T x = p[i];
+__global__ void __launch_bounds__(256) k_searchsorted(const T* __restrict__ s, int64_t n, const T* __restrict__ p,
+                                                      int64_t np, bool left, int64_t* __restrict__ out) {
+  __shared__ T piv[kSearchPivots];
+  const int64_t stride = n > kSearchPivots ? (n + kSearchPivots - 1) / kSearchPivots : 1;
+  const int npiv = static_cast<int>((n + stride - 1) / stride);  // pivot j = s[j * stride]
+  for (int j = threadIdx.x; j < npiv; j += blockDim.x) piv[j] = s[static_cast<int64_t>(j) * stride];
+  __syncthreads();
+  auto go_right = [&](T key, T x) { return left ? (key < x) : !(x < key); };
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t run = ((np + nwarps - 1) / nwarps + 31) & ~int64_t(31);
+  const int64_t r0 = gw * run, r1 = r0 + run < np ? r0 + run : np;
+  bool have = false;
+  T px{};
+  int64_t pans = 0;
+  for (int64_t i = r0 + lane; i < r1; i += 32) {
+    const T x = p[i];
     int64_t lo = 0, hi = n;
+    bool found = false;
+    if (have && !(x < px)) {
+      // answer >= pans: gallop pans, pans + 1, pans + 3, pans + 7, ...
+      lo = pans;
+      int64_t step = 1;
+      int d = 0;
+      for (; d < kGallop; ++d) {
+        const int64_t probe = lo + step - 1;
+        if (probe >= n) {
+          hi = n;
+          found = true;
+          break;
+        }
+        if (!go_right(s[probe], x)) {
+          hi = probe;
+          found = true;
+          break;
+        }
+        lo = probe + 1;
+        step <<= 1;
+      }
+    }
+    if (!found) {
+      // pivot interval, then the interval in global memory (within [lo, n))
+      int plo = 0, phi = npiv;
+      while (plo < phi) {
+        const int mid = (plo + phi) >> 1;
+        if (go_right(piv[mid], x)) plo = mid + 1;
+        else phi = mid;
+      }
+      const int64_t a = plo == 0 ? 0 : static_cast<int64_t>(plo - 1) * stride + 1;
+      hi = plo >= npiv ? n : static_cast<int64_t>(plo) * stride;
+      lo = lo > a ? lo : a;
+    }
     while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      bool go_right = left ? (s[mid] < x) : !(x < s[mid]);
-      if (go_right) lo = mid + 1;
+      const int64_t mid = (lo + hi) >> 1;
+      if (go_right(s[mid], x)) lo = mid + 1;
       else hi = mid;
     }
     out[i] = lo;
+    have = true;
+    px = x;
+    pans = lo;
   }
 }
 
