@@ -120,7 +120,6 @@ tqp_ctx* tqp_init(int device, tqp_status* st) {
 void tqp_shutdown(tqp_ctx* ctx) {
   if (!ctx) return;
   ctx->c.release_small();
-  ctx->c.release_large();
   cudaStreamSynchronize(ctx->c.stream);
   cudaFree(ctx->c.d_err);
   cudaFree(ctx->c.d_defer);

@@ -25,14 +25,6 @@ DevBuf::~DevBuf() {
     ctx->small_free[bucket].push_back(ptr);
     return;
   }
-  {
-    std::lock_guard<std::mutex> lk(ctx->small_mu);
-    if (ctx->large_cached + bytes <= Ctx::kLargeCacheBytes) {
-      ctx->large_free.emplace(bytes, ptr);
-      ctx->large_cached += bytes;
-      return;
-    }
-  }
   cudaFreeAsync(ptr, ctx->stream);
 }
 
@@ -111,32 +103,8 @@ std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
     TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, size_t(256) << i, pool, stream));
     return b;
   }
-  {
-    std::lock_guard<std::mutex> lk(small_mu);
-    auto it = large_free.find(bytes);
-    if (it != large_free.end()) {
-      b->ptr = it->second;
-      large_free.erase(it);
-      large_cached -= bytes;
-      return b;
-    }
-  }
-  cudaError_t e = cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream);
-  if (e == cudaErrorMemoryAllocation) {  // cached blocks back to the pool, once
-    cudaGetLastError();
-    release_large();
-    release_small();
-    e = cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream);
-  }
-  TQP_CUDA(e);
+  TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream));
   return b;
-}
-
-void Ctx::release_large() {
-  std::lock_guard<std::mutex> lk(small_mu);
-  for (auto& kv : large_free) cudaFreeAsync(kv.second, stream);
-  large_free.clear();
-  large_cached = 0;
 }
 
 void Ctx::release_small() {

@@ -138,14 +138,10 @@ struct Ctx {
   std::mutex small_mu;
   std::vector<void*> small_free[kSmallBuckets];
   void release_small();
-  // Larger blocks are kept by exact size (a repeated query asks for the same
-  // sizes: Q3's 480 MB orders table, 1.9 GB group records, ...), up to
-  // kLargeCacheBytes in total, under the same stream-order argument; the
-  // cache is handed back to the pool when an allocation fails.
-  static constexpr size_t kLargeCacheBytes = size_t(8) << 30;
-  std::multimap<size_t, void*> large_free;
-  size_t large_cached = 0;
-  void release_large();
+  // Larger blocks go straight back to the stream-ordered pool, which reuses
+  // them for any size (an exact-size host cache of them was tried: it kept
+  // memory from the pool, which then grew for every new size - the
+  // per-instruction path's temporaries, 11.8 -> 59 ms for Q1).
 
   Tensor alloc(int dtype, int64_t rows, int64_t cols);
   std::shared_ptr<DevBuf> alloc_bytes(size_t bytes);
