@@ -155,9 +155,18 @@ int64_t tqp_codec_encode(int dtype, int64_t rows, int64_t cols, const void* host
                          tqp_codec* codec, tqp_status* st);
 /* Uploads an encoded payload (pinned host memory for an asynchronous copy)
  * and decodes it on the device into a new tensor of the original dtype and
- * shape, bit-identical to the encoded column. */
+ * shape, bit-identical to the encoded column. Returns at once: the copy runs
+ * on the context's copy stream and the decode on its decode stream, so the
+ * payload must stay alive and unchanged until the tensor has been used on
+ * the context stream (every entry point taking the tensor, or a table
+ * holding it, orders the context stream after the decode) or
+ * tqp_tensor_wait + tqp_ctx_sync. Replaces the load step of
+ * columnar.cpp:453-527 (EncodedTable columns from host memory). */
 tqp_tensor* tqp_tensor_from_encoded(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols, const tqp_codec* codec,
                                     const void* payload, int64_t bytes, tqp_status* st);
+/* Orders the context stream after the tensor's producer (a decode still
+ * running on the decode stream); no-op otherwise. 0 or -1 (status set). */
+int tqp_tensor_wait(const tqp_tensor* t, tqp_status* st);
 int tqp_tensor_dtype(const tqp_tensor* t);
 int64_t tqp_tensor_rows(const tqp_tensor* t);
 int64_t tqp_tensor_cols(const tqp_tensor* t);

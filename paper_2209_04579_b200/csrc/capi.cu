@@ -69,9 +69,25 @@ tqp_tensor* wrap(Tensor t) {
   return h;
 }
 
+// every entry point reaches a tensor through T_, so a tensor still being
+// decoded on the decode stream is waited for here (on the context stream)
 const Tensor& T_(const tqp_tensor* t) {
   if (!t) throw Error(TQP_ERR_ARG, "null tensor handle");
+  if (t->t.buf && t->t.buf->ready && t->t.buf->ctx) t->t.buf->ctx->wait_ready(*t->t.buf);
   return t->t;
+}
+// the tensor without waiting (metadata only: a table column is added while
+// its decode may still run)
+const Tensor& TH_(const tqp_tensor* t) {
+  if (!t) throw Error(TQP_ERR_ARG, "null tensor handle");
+  return t->t;
+}
+// the same for every column of the tables an executor call binds
+void wait_tables(const TableSet& ts) {
+  for (const auto& nt : ts)
+    if (nt.second)
+      for (const auto& col : nt.second->cols)
+        if (col.t.buf && col.t.buf->ready && col.t.buf->ctx) col.t.buf->ctx->wait_ready(*col.t.buf);
 }
 Ctx& C_(tqp_ctx* c) {
   if (!c) throw Error(TQP_ERR_ARG, "null context");
@@ -121,6 +137,9 @@ void tqp_shutdown(tqp_ctx* ctx) {
   if (!ctx) return;
   ctx->c.release_small();
   cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.copy_stream) cudaStreamSynchronize(ctx->c.copy_stream);
+  if (ctx->c.decode_stream) cudaStreamSynchronize(ctx->c.decode_stream);
+  ctx->c.release_stages();
   cudaFree(ctx->c.d_err);
   cudaFree(ctx->c.d_defer);
   cudaFreeHost(ctx->c.h_err);
@@ -131,6 +150,7 @@ void tqp_shutdown(tqp_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.copy_stream);
     cudaStreamDestroy(ctx->c.copy_stream);
   }
+  if (ctx->c.decode_stream) cudaStreamDestroy(ctx->c.decode_stream);
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }
@@ -212,6 +232,13 @@ tqp_tensor* tqp_tensor_from_encoded(tqp_ctx* ctx, int dtype, int64_t rows, int64
   });
 }
 
+int tqp_tensor_wait(const tqp_tensor* t, tqp_status* st) {
+  return guard(st, [&] {
+    T_(t);
+    return 0;
+  });
+}
+
 tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_t cols, const void* dev,
                                    tqp_status* st) {
   return guard(st, [&] {
@@ -225,7 +252,14 @@ tqp_tensor* tqp_tensor_from_device(tqp_ctx* ctx, int dtype, int64_t rows, int64_
 int tqp_tensor_dtype(const tqp_tensor* t) { return t ? t->t.dtype : -1; }
 int64_t tqp_tensor_rows(const tqp_tensor* t) { return t ? t->t.rows : -1; }
 int64_t tqp_tensor_cols(const tqp_tensor* t) { return t ? t->t.cols : -1; }
-const void* tqp_tensor_data(const tqp_tensor* t) { return t ? t->t.data() : nullptr; }
+const void* tqp_tensor_data(const tqp_tensor* t) {
+  if (!t) return nullptr;
+  try {
+    T_(t);  // ordered after a pending decode on the context stream
+  } catch (...) {
+  }
+  return t->t.data();
+}
 
 int tqp_tensor_to_host(tqp_ctx* ctx, const tqp_tensor* t, void* host, tqp_status* st) {
   return guard(st, [&] {
@@ -345,7 +379,7 @@ tqp_table* tqp_table_create(tqp_ctx* ctx, tqp_status* st) {
 int tqp_table_add_column(tqp_table* tab, const char* name, int lt, tqp_tensor* t, tqp_status* st) {
   return guard(st, [&] {
     if (!tab || !name) throw Error(TQP_ERR_ARG, "null table or name");
-    const Tensor& x = T_(t);
+    const Tensor& x = TH_(t);
     if (tab->t.find(name)) throw Error(TQP_ERR_ENCODING, std::string("table: duplicate column name '") + name + "'");
     if (!tab->t.cols.empty() && x.rows != tab->t.rows) {
       throw Error(TQP_ERR_ENCODING, std::string("table: column '") + name + "' has " + std::to_string(x.rows) +
@@ -488,6 +522,7 @@ static tqp_result* run_exec(tqp_executor* ex, const char* const* names, tqp_tabl
                             ProfileTrace* trace) {
   TableSet ts;
   for (int i = 0; i < n; ++i) ts.push_back({names[i], &tables[i]->t});
+  wait_tables(ts);
   auto* r = new tqp_result;
   try {
     r->r = ex->ex->execute(ts, trace);
@@ -520,6 +555,7 @@ tqp_tensor* tqp_executor_execute_partial(tqp_executor* ex, const char* const* na
     if (!ex) throw Error(TQP_ERR_ARG, "null executor");
     TableSet ts;
     for (int i = 0; i < n; ++i) ts.push_back({names[i], &tables[i]->t});
+    wait_tables(ts);
     Partial p = ex->ex->execute_partial(ts);
     Tensor t;
     t.dtype = TQP_I64;
@@ -607,6 +643,7 @@ tqp_result* tqp_executor_execute_sharded(tqp_executor* ex, tqp_comm* comm, const
       for (auto& ch : lower) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
       env.kinds[lower] = kinds[i];
     }
+    wait_tables(ts);
     auto* r = new tqp_result;
     try {
       r->r = ex->ex->execute_sharded(ts, env);

@@ -436,25 +436,62 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
                                         bytes == rd_bytes + packed_bytes(rows, k.width)))
     throw Error(TQP_ERR_ARG, "codec: bad ROWDICT column");
   if (k.codec < TQP_CODEC_RAW || k.codec > TQP_CODEC_ROWDICT) throw Error(TQP_ERR_ARG, "codec: unknown codec");
+  // The copy runs on the context's copy stream into a staging slot (Ctx::
+  // Stage): it waits only for the decode that last read the slot, so the
+  // copies of consecutive columns run back to back. The decode runs on the
+  // decode stream (allocations included: `stream` is swapped for this
+  // function), which waits for the copy only; the tensor carries a ready
+  // event that the context stream waits for at its first use (Ctx::
+  // wait_ready), so work already queued there - a query over the previous
+  // tables - overlaps this upload.
+  struct StreamSwap {
+    Ctx& c;
+    cudaStream_t old;
+    StreamSwap(Ctx& c_, cudaStream_t s) : c(c_), old(c_.stream) { c.stream = s; }
+    ~StreamSwap() { c.stream = old; }
+  } swap(c, c.decodes());
   Tensor out = c.alloc(dtype, rows, cols);
-  auto staged = c.alloc_bytes(static_cast<size_t>(bytes));
+  Ctx::Stage* slot = nullptr;
   if (bytes) {
-    // the copy runs on the context's copy stream so the uploads of later
-    // columns overlap this column's decode (and whatever else `stream` runs):
-    // copy stream waits for the staging allocation, `stream` for the copy
     cudaStream_t cs = c.copies();
-    cudaEvent_t ready = c.take_event(), landed = c.take_event();
-    TQP_CUDA(cudaEventRecord(ready, c.stream));
-    TQP_CUDA(cudaStreamWaitEvent(cs, ready, 0));
-    TQP_CUDA(cudaMemcpyAsync(staged->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, cs));
+    slot = &c.stages[c.stage_next];
+    c.stage_next = (c.stage_next + 1) % Ctx::kStages;
+    if (slot->freed) TQP_CUDA(cudaStreamWaitEvent(cs, slot->freed, 0));
+    if (slot->cap < static_cast<size_t>(bytes)) {
+      if (slot->ptr) {
+        TQP_CUDA(cudaStreamSynchronize(cs));  // the slot's last reader is done
+        TQP_CUDA(cudaFree(slot->ptr));
+      }
+      const size_t cap = (std::max(static_cast<size_t>(bytes), 2 * slot->cap) + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1);
+      TQP_CUDA(cudaMalloc(&slot->ptr, cap));
+      slot->cap = cap;
+    }
+    TQP_CUDA(cudaMemcpyAsync(slot->ptr, payload, static_cast<size_t>(bytes), cudaMemcpyHostToDevice, cs));
+    cudaEvent_t landed = c.take_event();
     TQP_CUDA(cudaEventRecord(landed, cs));
     TQP_CUDA(cudaStreamWaitEvent(c.stream, landed, 0));
-    c.give_event(ready);
     c.give_event(landed);
+    if (!slot->freed) TQP_CUDA(cudaEventCreateWithFlags(&slot->freed, cudaEventDisableTiming));
   }
-  if (!rows) return out;
+  struct SlotRelease {  // the slot is free again once the decode stream has run this column's decode
+    Ctx& c;
+    Ctx::Stage* s;
+    ~SlotRelease() {
+      if (s) cudaEventRecord(s->freed, c.stream);
+    }
+  } release{c, slot};
+  // the decoded tensor's ready event, recorded after its last decode kernel
+  auto ready = [&]() -> Tensor {
+    if (out.buf && !out.buf->ready) {
+      TQP_CUDA(cudaEventCreateWithFlags(&out.buf->ready, cudaEventDisableTiming));
+      TQP_CUDA(cudaEventRecord(out.buf->ready, c.stream));
+    }
+    return out;
+  };
+  if (!rows) return ready();
   const int grid = c.grid_for(rows, 256, 4);
-  const auto* words = static_cast<const uint32_t*>(staged->ptr);
+  const void* staged_ptr = slot ? slot->ptr : nullptr;
+  const auto* words = static_cast<const uint32_t*>(staged_ptr);
   if (k.codec == TQP_CODEC_FOR) {
     if (byte_col)
       k_decode_for<uint8_t><<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, k.scale, out.ptr<uint8_t>());
@@ -470,18 +507,18 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
     Tensor excl = k::prefix_sum_unchecked(c, steps);
     k_delta_finish<<<grid, 256, 0, c.stream>>>(excl.ptr<int64_t>(), steps.ptr<int64_t>(), rows, k.base, out.ptr<int64_t>());
   } else if (k.codec == TQP_CODEC_ROWDICT) {
-    const auto* dict = static_cast<const uint8_t*>(staged->ptr);
+    const auto* dict = static_cast<const uint8_t*>(staged_ptr);
     k_decode_rowdict<<<c.grid_for(rows * cols, 256, 4), 256, 0, c.stream>>>(
         dict, reinterpret_cast<const uint32_t*>(dict + rd_bytes), k.width, rows, cols, out.ptr<uint8_t>());
   } else if (k.codec == TQP_CODEC_DEC) {
     k_decode_dec<<<grid, 256, 0, c.stream>>>(words, k.width, rows, k.base, static_cast<double>(k.scale), out.ptr<double>());
   } else {
-    const auto* dict = static_cast<const unsigned long long*>(staged->ptr);
+    const auto* dict = static_cast<const unsigned long long*>(staged_ptr);
     k_decode_dict<<<grid, 256, 0, c.stream>>>(dict, k.dict_n, reinterpret_cast<const uint32_t*>(dict + k.dict_n), k.width,
                                               rows, out.ptr<unsigned long long>());
   }
   c.count_launch();
-  return out;
+  return ready();
 }
 
 }  // namespace tqp

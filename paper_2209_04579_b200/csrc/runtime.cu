@@ -19,6 +19,11 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 DevBuf::~DevBuf() {
+  if (ready) {  // never used on the context stream: free after the producer
+    if (ctx) cudaStreamWaitEvent(ctx->stream, ready, 0);
+    cudaEventDestroy(ready);
+    ready = nullptr;
+  }
   if (!ptr || !ctx) return;
   if (bucket >= 0) {
     std::lock_guard<std::mutex> lk(ctx->small_mu);
@@ -105,6 +110,14 @@ std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
   }
   TQP_CUDA(cudaMallocFromPoolAsync(&b->ptr, bytes, pool, stream));
   return b;
+}
+
+void Ctx::release_stages() {
+  for (auto& s : stages) {
+    if (s.ptr) cudaFree(s.ptr);
+    if (s.freed) cudaEventDestroy(s.freed);
+    s = Stage{};
+  }
 }
 
 void Ctx::release_small() {

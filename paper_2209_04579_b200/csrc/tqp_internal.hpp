@@ -44,6 +44,10 @@ struct DevBuf {
   // derived state of an immutable tensor living in this buffer, computed once
   // (reduce.cu: the validated segment plan of a segment-id vector)
   std::shared_ptr<void> seg_plan;
+  // written on another stream (a column decoded on the context's decode
+  // stream): `ctx->stream` waits for this event before the first use
+  // (Ctx::wait_ready), then it is dropped
+  cudaEvent_t ready = nullptr;
   ~DevBuf();
 };
 
@@ -165,6 +169,34 @@ struct Ctx {
   // a second stream for host->device copies that may overlap the work of
   // `stream` (compressed column uploads); created on first use
   cudaStream_t copy_stream = nullptr;
+  // Staging slots for encoded column uploads (codec.cu decode_column): a
+  // column's host->device copy waits only for the decode that last read its
+  // slot, not for everything queued on `stream`, so consecutive columns'
+  // copies run back to back on the copy engine while earlier columns decode.
+  struct Stage {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    cudaEvent_t freed = nullptr;  // recorded on `stream` after the slot's decode
+  };
+  static constexpr int kStages = 3;
+  Stage stages[kStages];
+  int stage_next = 0;
+  void release_stages();
+  // decodes of encoded uploads run here, so the context stream's queued
+  // work (a query over the previous tables) does not hold them up; the
+  // decoded tensor carries a ready event (DevBuf::ready)
+  cudaStream_t decode_stream = nullptr;
+  cudaStream_t decodes() {
+    if (!decode_stream) TQP_CUDA(cudaStreamCreateWithFlags(&decode_stream, cudaStreamNonBlocking));
+    return decode_stream;
+  }
+  // orders `stream` after the producer of b (if one is still pending)
+  void wait_ready(DevBuf& b) {
+    if (!b.ready) return;
+    TQP_CUDA(cudaStreamWaitEvent(stream, b.ready, 0));
+    cudaEventDestroy(b.ready);  // released once the wait has consumed it
+    b.ready = nullptr;
+  }
   cudaStream_t copies() {
     if (!copy_stream) TQP_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
     return copy_stream;

@@ -115,6 +115,7 @@ def _load() -> C.CDLL:
         "tqp_codec_bound": (I64_, [I, I64_, I64_]),
         "tqp_codec_encode": (I64_, [I, I64_, I64_, P, P, I64_, P, S]),
         "tqp_tensor_from_encoded": (P, [P, I, I64_, I64_, P, P, I64_, S]),
+        "tqp_tensor_wait": (I, [P, S]),
         "tqp_tensor_from_host_utf8_i32": (P, [P, I64_, I64_, P, S]),
         "tqp_tensor_from_device": (P, [P, I, I64_, I64_, P, S]),
         "tqp_tensor_dtype": (I, [P]), "tqp_tensor_rows": (I64_, [P]), "tqp_tensor_cols": (I64_, [P]),
@@ -283,9 +284,11 @@ class Tensor:
     def from_encoded(codec: "Codec", payload, dtype: int, rows: int, cols: int = 1,
                      ctx: Optional[Context] = None, sync: bool = True) -> "Tensor":
         """Uploads an encoded payload (numpy array or a pinned torch tensor:
-        anything with a data pointer) and decodes it on the device. With
-        sync=False the host->device copy may still be reading `payload` when
-        this returns: keep it alive and unmodified until ctx.sync()."""
+        anything with a data pointer) and decodes it on the device (copy
+        stream + decode stream; the context stream waits for the decode at
+        the tensor's first use). With sync=False the host->device copy may
+        still be reading `payload` when this returns: keep it alive and
+        unmodified until the tensor has been used (or wait() + ctx.sync())."""
         ctx = ctx or default_context()
         if hasattr(payload, "data_ptr"):
             ptr, nbytes = payload.data_ptr(), payload.numel() * payload.element_size()
@@ -295,12 +298,21 @@ class Tensor:
         st = Status()
         h = lib.tqp_tensor_from_encoded(ctx.h, dtype, rows, cols, C.byref(codec), ptr, nbytes, C.byref(st))
         _check(st, bool(h))
+        t = Tensor(h, ctx)
         if not sync:
             # the copy from `payload` is asynchronous (truly so for pinned
-            # memory): the caller keeps it alive and unchanged until ctx.sync()
-            return Tensor(h, ctx)
+            # memory): the caller keeps it alive and unchanged until used
+            return t
+        t.wait()
         ctx.sync()
-        return Tensor(h, ctx)
+        return t
+
+    def wait(self) -> None:
+        """Orders the context stream after this tensor's producer (a decode
+        still running on the decode stream)."""
+        st = Status()
+        lib.tqp_tensor_wait(self.h, C.byref(st))
+        _check(st, True)
 
     @staticmethod
     def from_strings(values: Sequence[str], ctx: Optional[Context] = None) -> "Tensor":
@@ -340,6 +352,7 @@ class Tensor:
         writing."""
         if self.dtype == STR8:
             raise TypeError("STR8 tensors have no fixed-width array view")
+        self.wait()  # a decode still running on the decode stream
         self.ctx.sync()
         typestr = {BOOL: "|u1", I32: "<i4", I64: "<i8", F64: "<f8"}[self.dtype]
         return {"shape": (self.rows, self.cols), "typestr": typestr, "data": (self.data_ptr(), False),
