@@ -142,3 +142,39 @@ def test_string_compare_and_plumbing(ctx):
     w = tqp.pad_width_like(tqp.Tensor.from_numpy(lit, utf8=True), tqp.Tensor.from_numpy(chars, utf8=True))
     assert w.cols == chars.shape[1]
     np.testing.assert_array_equal(tqp.iota(5).numpy().ravel(), np.arange(5))
+
+
+def test_searchsorted_large(ctx):
+    """Pivot-staged search with galloping (scan.cu k_searchsorted): sorted
+    probes (the gallop path), random probes (the pivot path), duplicates,
+    probes below / above every key, both sides, int64 and float64."""
+    from paper_2209_04579_b200 import tqp
+    rng = np.random.default_rng(21)
+    keys = np.sort(rng.integers(-10**6, 10**6, 1_000_003))
+    for probes in (np.sort(rng.integers(-2 * 10**6, 2 * 10**6, 3_000_001)),
+                   rng.integers(-2 * 10**6, 2 * 10**6, 700_001),
+                   np.repeat(keys[::997], 3)):
+        for side in ("left", "right"):
+            got = tqp.searchsorted(keys.reshape(-1, 1), probes.reshape(-1, 1), side).numpy().ravel()
+            np.testing.assert_array_equal(got, np.searchsorted(keys, probes, side=side), err_msg=side)
+    fk = np.sort(rng.normal(size=200_000).round(3))
+    fp = rng.normal(size=300_000).round(3)
+    for side in ("left", "right"):
+        got = tqp.searchsorted(fk.reshape(-1, 1), fp.reshape(-1, 1), side).numpy().ravel()
+        np.testing.assert_array_equal(got, np.searchsorted(fk, fp, side=side))
+
+
+def test_segment_starts_one_column(ctx):
+    """16-flags-per-store one-column segment starts (kernels.cu
+    k_segment_starts1): byte and int64 keys, lengths off the 16 multiple."""
+    from paper_2209_04579_b200 import tqp
+    rng = np.random.default_rng(22)
+    for n in (1, 15, 16, 17, 1_000_003):
+        k64 = np.sort(rng.integers(0, max(1, n // 7), n))
+        want = np.concatenate([[True], k64[1:] != k64[:-1]])
+        np.testing.assert_array_equal(tqp.segment_starts(k64.reshape(-1, 1)).numpy().ravel().astype(bool), want)
+        k8 = np.sort(rng.integers(0, 3, n)).astype(np.uint8) + ord("A")
+        chars = k8.reshape(-1, 1)
+        want8 = np.concatenate([[True], k8[1:] != k8[:-1]])
+        got8 = tqp.segment_starts(tqp.Tensor.from_numpy(chars, utf8=True)).numpy().ravel().astype(bool)
+        np.testing.assert_array_equal(got8, want8)
