@@ -85,6 +85,7 @@ typedef struct tqp_table tqp_table;
 typedef struct tqp_plan tqp_plan;
 typedef struct tqp_executor tqp_executor;
 typedef struct tqp_result tqp_result;
+typedef struct tqp_pending tqp_pending;
 
 /* ---- context (replaces KernelBackend/backend_by_name, backend.hpp:22-70) -- */
 int tqp_abi_version(void);
@@ -298,6 +299,21 @@ tqp_executor* tqp_executor_create(tqp_ctx* ctx, const tqp_plan* p, unsigned flag
  * (case-insensitive). Result stays on device until downloaded. */
 tqp_result* tqp_executor_execute(tqp_executor* ex, const char* const* names,
                                  tqp_table* const* tables, int ntables, tqp_status* st);
+/* Executor::execute without its final host synchronisation (an extension of
+ * executor.cpp:346: a serving loop submits the next query while this one
+ * runs). When the plan's last fused unit can defer its precondition check
+ * (only instruction-free steps follow it), returns with the work queued on
+ * the context stream; otherwise the run completes first. tqp_pending_wait
+ * finishes it: the unit's check word is read, a unit that met data outside
+ * its contract re-runs the plan on the checked path (the tables must stay
+ * alive until then), and the completed result is returned - the same
+ * result and errors as tqp_executor_execute. */
+tqp_pending* tqp_executor_execute_async(tqp_executor* ex, const char* const* names,
+                                        tqp_table* const* tables, int ntables, tqp_status* st);
+/* Completes and frees `p`; returns the result (or NULL, status set). */
+tqp_result* tqp_pending_wait(tqp_pending* p, tqp_status* st);
+/* Frees a pending execution without waiting for its result. */
+void tqp_pending_free(tqp_pending* p);
 /* Same run with a ProfileTrace (executor.hpp:12-38) rendered as Chrome
  * trace-event JSON into a malloc'd string the caller frees with tqp_free_str. */
 tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names,

@@ -31,6 +31,10 @@ struct tqp_result {
   Result r;
   std::vector<tqp_tensor*> handles;
 };
+struct tqp_pending {
+  tqp_executor* ex = nullptr;
+  AsyncResult a;
+};
 
 namespace {
 
@@ -140,6 +144,7 @@ void tqp_shutdown(tqp_ctx* ctx) {
   if (ctx->c.copy_stream) cudaStreamSynchronize(ctx->c.copy_stream);
   if (ctx->c.decode_stream) cudaStreamSynchronize(ctx->c.decode_stream);
   ctx->c.release_stages();
+  ctx->c.release_pinned();
   cudaFree(ctx->c.d_err);
   cudaFree(ctx->c.d_defer);
   cudaFreeHost(ctx->c.h_err);
@@ -537,6 +542,50 @@ static tqp_result* run_exec(tqp_executor* ex, const char* const* names, tqp_tabl
 tqp_result* tqp_executor_execute(tqp_executor* ex, const char* const* names, tqp_table* const* tables, int n,
                                  tqp_status* st) {
   return guard(st, [&] { return run_exec(ex, names, tables, n, nullptr); });
+}
+
+tqp_pending* tqp_executor_execute_async(tqp_executor* ex, const char* const* names, tqp_table* const* tables, int n,
+                                        tqp_status* st) {
+  return guard(st, [&] {
+    if (!ex) throw Error(TQP_ERR_ARG, "null executor");
+    TableSet ts;
+    for (int i = 0; i < n; ++i) ts.push_back({names[i], &tables[i]->t});
+    wait_tables(ts);
+    auto* p = new tqp_pending;
+    p->ex = ex;
+    try {
+      p->a = ex->ex->execute_async(ts);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    return p;
+  });
+}
+
+tqp_result* tqp_pending_wait(tqp_pending* p, tqp_status* st) {
+  return guard(st, [&] {
+    if (!p) throw Error(TQP_ERR_ARG, "null pending execution");
+    std::unique_ptr<tqp_pending> own(p);
+    auto* r = new tqp_result;
+    try {
+      r->r = p->ex->ex->wait(p->a);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    for (auto& c : r->r.cols) r->handles.push_back(wrap(c.t));
+    return r;
+  });
+}
+
+void tqp_pending_free(tqp_pending* p) {
+  if (!p) return;
+  if (p->a.done) {
+    cudaEventSynchronize(p->a.done);  // the slot is written by the queued copy
+    cudaEventDestroy(p->a.done);
+  }
+  delete p;
 }
 
 tqp_result* tqp_executor_profile(tqp_executor* ex, const char* const* names, tqp_table* const* tables, int n,

@@ -363,12 +363,67 @@ void Executor::check_inputs(const TableSet& tables) const {
 }
 
 Result Executor::execute(const TableSet& tables, ProfileTrace* trace, bool allow_defer) {
+  UnitPending pend;
+  Result r = run_units(tables, trace, allow_defer, pend, true);
+  if (pend.active) {
+    // collect_outputs synchronised: the deferred word is on the host
+    long long herr[4];
+    std::memcpy(herr, ctx_.h_err + Ctx::kPinnedUnitErr, sizeof(herr));
+    if (herr[0] || herr[1]) return execute(tables, trace, false);  // the checked path decides (fallback / 8 slots)
+    const long long nrows = pend.nrows >= 0 ? pend.nrows : herr[2];
+    for (auto& col : r.cols)
+      if (std::find(pend.outs.begin(), pend.outs.end(), col.t.data()) != pend.outs.end()) col.t.rows = nrows;
+    check_result_rows(r);
+  }
+  return r;
+}
+
+AsyncResult Executor::execute_async(const TableSet& tables) {
+  AsyncResult a;
+  a.tables = tables;
+  a.slot = ctx_.pinned_slot();
+  a.pend.host = a.slot.get();
+  a.r = run_units(tables, nullptr, true, a.pend, false);
+  if (!a.pend.active) {  // nothing deferred: complete it now
+    ctx_.sync();
+    if (ctx_.time_kernels) collect_kernel_events();
+    check_result_rows(a.r);
+    a.complete = true;
+    return a;
+  }
+  TQP_CUDA(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+  TQP_CUDA(cudaEventRecord(a.done, ctx_.stream));
+  return a;
+}
+
+Result Executor::wait(AsyncResult& a) {
+  if (a.complete) return a.r;
+  TQP_CUDA(cudaEventSynchronize(a.done));
+  cudaEventDestroy(a.done);
+  a.done = nullptr;
+  if (ctx_.time_kernels) collect_kernel_events();
+  long long herr[4];
+  std::memcpy(herr, a.slot.get(), sizeof(herr));
+  a.complete = true;
+  if (herr[0] || herr[1]) {
+    a.r = execute(a.tables, nullptr, false);  // the checked path decides (fallback / 8 slots)
+    return a.r;
+  }
+  const long long nrows = a.pend.nrows >= 0 ? a.pend.nrows : herr[2];
+  for (auto& col : a.r.cols)
+    if (std::find(a.pend.outs.begin(), a.pend.outs.end(), col.t.data()) != a.pend.outs.end()) col.t.rows = nrows;
+  check_result_rows(a.r);
+  return a.r;
+}
+
+// the plan over `tables` up to its outputs; `pend` receives a deferred last
+// unit's check, `sync` false leaves the context stream running
+Result Executor::run_units(const TableSet& tables, ProfileTrace* trace, bool allow_defer, UnitPending& pend, bool sync) {
   HostProf hp("exec");
   check_inputs(tables);
   hp.mark("inputs");
   // the last fused unit defers its check when only instruction-free steps
   // follow it (its outputs are the result)
-  UnitPending pend;
   int defer_unit = -1;
   if (allow_defer && !trace && !units_.empty()) {
     const FusedUnit& last = units_.back();
@@ -420,28 +475,19 @@ Result Executor::execute(const TableSet& tables, ProfileTrace* trace, bool allow
     hp.mark("step");
     ++s;
   }
-  Result r = collect_outputs(slots, !pend.active);
+  Result r = collect_outputs(slots, !pend.active && sync, sync);
   hp.mark("collect");
-  if (pend.active) {
-    // collect_outputs synchronised: the deferred word is on the host
-    long long herr[4];
-    std::memcpy(herr, ctx_.h_err + Ctx::kPinnedUnitErr, sizeof(herr));
-    if (herr[0] || herr[1]) return execute(tables, trace, false);  // the checked path decides (fallback / 8 slots)
-    const long long nrows = pend.nrows >= 0 ? pend.nrows : herr[2];
-    for (auto& col : r.cols)
-      if (std::find(pend.outs.begin(), pend.outs.end(), col.t.data()) != pend.outs.end()) col.t.rows = nrows;
-    check_result_rows(r);
-  }
   return r;
 }
 
-Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows) {
+Result Executor::collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows, bool sync) {
   Result res;
   for (const auto& o : plan_.outputs) {
     if (!slots[o.slot]) exec_fail("internal: slot " + std::to_string(o.slot) + " read after release");
     res.cols.push_back({o.name, o.type, *slots[o.slot]});
   }
   if (check_rows) check_result_rows(res);
+  if (!sync) return res;
   ctx_.sync();
   if (ctx_.time_kernels) collect_kernel_events();
   return res;

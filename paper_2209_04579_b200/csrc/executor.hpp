@@ -166,6 +166,23 @@ struct UnitPending {
   long long nrows = -1;            // host-known row count, or -1: err[2]
   std::vector<const void*> outs;   // device buffers of the unit's outputs
   std::shared_ptr<DevBuf> err;     // the device word (kept until read)
+  long long* host = nullptr;       // pinned destination of the 4 words (null: Ctx::kPinnedUnitErr)
+};
+
+// An execution whose last fused unit's check is still on the device
+// (Executor::execute_async): the outputs are queued on the context stream,
+// the unit's error words travel to `host` (a pinned slot of the context) and
+// an event marks their arrival. wait() checks them and either finishes the
+// result (row count patched) or, when the unit met data outside its
+// contract, runs the plan again on the checked path over the same tables
+// (the caller keeps them alive until then).
+struct AsyncResult {
+  Result r;
+  UnitPending pend;
+  TableSet tables;
+  cudaEvent_t done = nullptr;
+  std::shared_ptr<long long> slot;  // pinned, 4 words
+  bool complete = false;            // r is final already (nothing deferred)
 };
 
 struct FusedUnit {
@@ -187,6 +204,11 @@ class Executor {
  public:
   Executor(Ctx& ctx, Plan plan, unsigned flags);
   Result execute(const TableSet& tables, ProfileTrace* trace = nullptr, bool allow_defer = true);
+  // execute() without the final synchronisation when the plan's last fused
+  // unit can defer its check (only instruction-free steps after it); else
+  // the completed result. wait() finishes it (see AsyncResult).
+  AsyncResult execute_async(const TableSet& tables);
+  Result wait(AsyncResult& a);
 
   // Sharded execution: every shard runs phase 1 over its
   // rows of the fact table; the concatenated partials of all shards (rank
@@ -243,7 +265,8 @@ class Executor {
                 int64_t run_start);
   void release_after(int s, std::vector<std::optional<Tensor>>& slots);
   void check_inputs(const TableSet& tables) const;
-  Result collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows = true);
+  Result collect_outputs(std::vector<std::optional<Tensor>>& slots, bool check_rows = true, bool sync = true);
+  Result run_units(const TableSet& tables, ProfileTrace* trace, bool allow_defer, UnitPending& pend, bool sync);
   Result gather_and_execute(const TableSet& tables, const ShardEnv& env);
 
   Ctx& ctx_;

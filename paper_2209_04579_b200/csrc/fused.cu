@@ -4045,7 +4045,8 @@ struct Runner {
     if (pend && !po) {
       // deferred: the word travels with the outputs and is checked at the
       // result's synchronisation; rows are patched there when device-side
-      TQP_CUDA(cudaMemcpyAsync(c.h_err + Ctx::kPinnedUnitErr, err, 32, cudaMemcpyDeviceToHost, c.stream));
+      TQP_CUDA(cudaMemcpyAsync(pend->host ? pend->host : c.h_err + Ctx::kPinnedUnitErr, err, 32, cudaMemcpyDeviceToHost,
+                               c.stream));
       pend->active = true;
       pend->nrows = nrows;
       pend->err = err_buf;

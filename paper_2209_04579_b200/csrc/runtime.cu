@@ -112,6 +112,29 @@ std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
   return b;
 }
 
+std::shared_ptr<long long> Ctx::pinned_slot() {
+  std::lock_guard<std::mutex> lk(small_mu);
+  if (pinned_free.empty()) {
+    long long* chunk = nullptr;
+    TQP_CUDA(cudaMallocHost(&chunk, 4096));
+    pinned_chunks.push_back(chunk);
+    for (int i = 0; i < 128; ++i) pinned_free.push_back(chunk + 4 * i);
+  }
+  long long* p = pinned_free.back();
+  pinned_free.pop_back();
+  p[0] = p[1] = p[2] = p[3] = 0;
+  return std::shared_ptr<long long>(p, [this](long long* q) {
+    std::lock_guard<std::mutex> lk2(small_mu);
+    pinned_free.push_back(q);
+  });
+}
+
+void Ctx::release_pinned() {
+  for (long long* ch : pinned_chunks) cudaFreeHost(ch);
+  pinned_chunks.clear();
+  pinned_free.clear();
+}
+
 void Ctx::release_stages() {
   for (auto& s : stages) {
     if (s.ptr) cudaFree(s.ptr);

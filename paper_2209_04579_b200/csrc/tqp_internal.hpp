@@ -182,6 +182,11 @@ struct Ctx {
   Stage stages[kStages];
   int stage_next = 0;
   void release_stages();
+  // 4-word pinned host slots for asynchronous executions' deferred checks
+  // (Executor::execute_async), carved from 4 KB pinned chunks
+  std::vector<long long*> pinned_free, pinned_chunks;
+  std::shared_ptr<long long> pinned_slot();
+  void release_pinned();
   // decodes of encoded uploads run here, so the context stream's queued
   // work (a query over the previous tables) does not hold them up; the
   // decoded tensor carries a ready event (DevBuf::ready)

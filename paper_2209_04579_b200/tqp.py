@@ -116,6 +116,9 @@ def _load() -> C.CDLL:
         "tqp_codec_encode": (I64_, [I, I64_, I64_, P, P, I64_, P, S]),
         "tqp_tensor_from_encoded": (P, [P, I, I64_, I64_, P, P, I64_, S]),
         "tqp_tensor_wait": (I, [P, S]),
+        "tqp_executor_execute_async": (P, [P, C.POINTER(C.c_char_p), C.POINTER(P), I, S]),
+        "tqp_pending_wait": (P, [P, S]),
+        "tqp_pending_free": (None, [P]),
         "tqp_tensor_from_host_utf8_i32": (P, [P, I64_, I64_, P, S]),
         "tqp_tensor_from_device": (P, [P, I, I64_, I64_, P, S]),
         "tqp_tensor_dtype": (I, [P]), "tqp_tensor_rows": (I64_, [P]), "tqp_tensor_cols": (I64_, [P]),
@@ -738,6 +741,30 @@ class Result:
         return [(n, t, self.column(i).numpy()) for i, (n, t) in enumerate(self.columns())]
 
 
+class Pending:
+    """A queued execution (Executor.execute_async)."""
+
+    def __init__(self, handle, ctx: Context, tables):
+        self.h = handle
+        self.ctx = ctx
+        self._tables = tables  # alive until the result is taken
+
+    def result(self) -> Result:
+        h, self.h = self.h, None
+        if not h:
+            raise RuntimeError("result already taken")
+        st = Status()
+        r = lib.tqp_pending_wait(h, C.byref(st))
+        self._tables = None
+        _check(st, bool(r))
+        return Result(r, self.ctx)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.tqp_pending_free(self.h)
+            self.h = None
+
+
 SHARD_REPLICATED, SHARD_COPARTITIONED, SHARD_ROWS = 0, 1, 2
 # layout of the generator's sharded TPC-H tables (tqp_gen_table shard/nshards):
 # lineitem and orders cut on order boundaries, part and customer by rows
@@ -849,6 +876,16 @@ class Executor:
         h = lib.tqp_executor_execute(self.h, cn, th, n, C.byref(st))
         _check(st, bool(h))
         return Result(h, self.ctx)
+
+    def execute_async(self, tables: Mapping[str, Table]) -> "Pending":
+        """execute() without the final synchronisation (tqp_executor_execute_async):
+        Pending.result() returns the same result and raises the same errors.
+        Keep `tables` alive until then."""
+        cn, th, n = self._args(tables)
+        st = Status()
+        h = lib.tqp_executor_execute_async(self.h, cn, th, n, C.byref(st))
+        _check(st, bool(h))
+        return Pending(h, self.ctx, tables)
 
     # ---- sharded execution (SURVEY.md §8(e)); see distributed.py ----
     def shardable(self) -> Tuple[bool, str]:

@@ -194,3 +194,35 @@ def test_typed_scalar_access_checks_dtype(ctx):
             tqp.last_or_zero(t)
     np.testing.assert_array_equal(tqp.last_or_zero(tqp.Tensor.from_numpy(np.array([[3], [9]], np.int64))).numpy(),
                                   [[9]])
+
+
+def test_execute_async_matches_execute(ctx):
+    """execute_async + result() (queries submitted back to back, results
+    taken afterwards) gives the golden results; a fused unit whose deferred
+    check flags its data (Q64.64 range, see the fixed-point guards test)
+    re-runs on the checked path inside result() and returns the exact
+    path's result."""
+    import json
+    from conftest import load_tpch_golden
+    from test_oracle import compare_tables
+    from paper_2209_04579_b200 import tqp
+    gold = load_tpch_golden()
+    tables = {n: tqp.Table.generate(n, gold["sf"], gold["seed"], ctx=ctx) for n in ("lineitem", "orders", "customer", "part")}
+    execs = {q: tqp.Executor(json.loads((ROOT / "paper_2209_04579_b200" / "plans" / f"{q}.opplan.json").read_text()), ctx=ctx)
+             for q in ("q1", "q6", "q14", "q3")}
+    for _ in range(3):
+        pend = {q: ex.execute_async(tables) for q, ex in execs.items()}
+        for q, p in pend.items():
+            compare_tables(p.result().to_numpy(), gold["results"][q])
+    p = execs["q6"].execute_async(tables)
+    del p  # freed without a result
+    ctx.sync()
+    plan = json.loads((PLANS / "q3.opplan.json").read_text())
+    base = {n: tqp.Table.generate(n, 0.005, 7) for n in ("lineitem", "orders", "customer")}
+    scaled = dict(base, lineitem=_with_column(tqp, base["lineitem"], "l_extendedprice", lambda a: a * 1e15))
+    fused = tqp.Executor(plan, fuse=True)
+    got = as_numpy(fused.execute_async(scaled).result())
+    assert fused.fallbacks == 1
+    want = as_numpy(tqp.Executor(plan, fuse=False).execute(scaled))
+    for (n, _, g), (_, _, w) in zip(got, want):
+        np.testing.assert_array_equal(g, w, err_msg=n)
