@@ -322,9 +322,11 @@ Tensor radix_sort_cols(Ctx& c, const Tensor& col, int64_t j, const Tensor* perm,
   const size_t hist_off = 64, ctr_off = hist_off + sizeof(unsigned long long) * 256 * kMaxPasses;
   const size_t desc_off = (ctr_off + sizeof(int) * kMaxPasses + 255) & ~size_t(255);
   const size_t desc_bytes = sizeof(unsigned long long) * 256 * static_cast<size_t>(tiles);
-  auto scratch = c.alloc_bytes(desc_off + desc_bytes * npass);
+  // one descriptor array, cleared before each pass (all passes' at once
+  // would be npass x 2 KB per 2048 keys: 4.8 GB for 600 M int64 keys)
+  auto scratch = c.alloc_bytes(desc_off + desc_bytes);
   unsigned char* sb = static_cast<unsigned char*>(scratch->ptr);
-  TQP_CUDA(cudaMemsetAsync(sb, 0, desc_off + desc_bytes * npass, c.stream));
+  TQP_CUDA(cudaMemsetAsync(sb, 0, desc_off, c.stream));
   TQP_CUDA(cudaMemcpyAsync(sb, shifts.data(), sizeof(int) * npass, cudaMemcpyHostToDevice, c.stream));
   auto* hist = reinterpret_cast<unsigned long long*>(sb + hist_off);
   k_os_hist<<<c.grid_for(n, kThreads, 4, 4), kThreads, 0, c.stream>>>(reinterpret_cast<uint64_t*>(keys.data()), n,
@@ -335,9 +337,10 @@ Tensor radix_sort_cols(Ctx& c, const Tensor& col, int64_t j, const Tensor* perm,
   Tensor kin = keys, pin = payload, kout = k2, pout = p2;
   for (int q = 0; q < npass; ++q) {
     const bool last = q + 1 == npass;
+    TQP_CUDA(cudaMemsetAsync(sb + desc_off, 0, desc_bytes, c.stream));
     k_onesweep<<<tiles, kThreads, 0, c.stream>>>(
         reinterpret_cast<uint64_t*>(kin.data()), pin.ptr<int64_t>(), reinterpret_cast<uint64_t*>(kout.data()),
-        pout.ptr<int64_t>(), n, shifts[q], hist + 256 * q, reinterpret_cast<unsigned long long*>(sb + desc_off + desc_bytes * q),
+        pout.ptr<int64_t>(), n, shifts[q], hist + 256 * q, reinterpret_cast<unsigned long long*>(sb + desc_off),
         reinterpret_cast<int*>(sb + ctr_off) + q, last ? 0 : 1);
     c.count_launch();
     if (q == 0) {
