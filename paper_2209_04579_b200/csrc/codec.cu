@@ -447,8 +447,15 @@ Tensor decode_column(Ctx& c, int dtype, int64_t rows, int64_t cols, const tqp_co
   struct StreamSwap {
     Ctx& c;
     cudaStream_t old;
-    StreamSwap(Ctx& c_, cudaStream_t s) : c(c_), old(c_.stream) { c.stream = s; }
-    ~StreamSwap() { c.stream = old; }
+    bool old_pool_only;
+    StreamSwap(Ctx& c_, cudaStream_t s) : c(c_), old(c_.stream), old_pool_only(c_.pool_only) {
+      c.stream = s;
+      c.pool_only = true;  // the small-block free list is ordered by the context stream only
+    }
+    ~StreamSwap() {
+      c.stream = old;
+      c.pool_only = old_pool_only;
+    }
   } swap(c, c.decodes());
   Tensor out = c.alloc(dtype, rows, cols);
   Ctx::Stage* slot = nullptr;

@@ -93,7 +93,7 @@ std::shared_ptr<DevBuf> Ctx::alloc_bytes(size_t bytes) {
   b->ctx = this;
   b->bytes = bytes;
   if (!bytes) return b;
-  if (bytes <= (size_t(256) << (kSmallBuckets - 1))) {
+  if (!pool_only && bytes <= (size_t(256) << (kSmallBuckets - 1))) {
     int i = 0;
     while ((size_t(256) << i) < bytes) ++i;
     b->bucket = i;

@@ -139,6 +139,9 @@ struct Ctx {
   // does (a block freed after its last enqueued use is only handed to work
   // enqueued later on the same stream).
   static constexpr int kSmallBuckets = 9;  // 256 B << i, up to 64 KB
+  // set while work is enqueued on another stream (codec.cu's decode stream):
+  // the free list is ordered by `stream` only, so allocations bypass it
+  bool pool_only = false;
   std::mutex small_mu;
   std::vector<void*> small_free[kSmallBuckets];
   void release_small();
