@@ -2378,6 +2378,16 @@ const void* tile_kernel(int mode, int nacc) {
   return nullptr;
 }
 
+const void* tile_kernel_lean(int nacc) {
+  switch (nacc) {
+    case 1: return reinterpret_cast<const void*>(&k_tile<MODE_HASH, 1, true>);
+    case 2: return reinterpret_cast<const void*>(&k_tile<MODE_HASH, 2, true>);
+    case 3: return reinterpret_cast<const void*>(&k_tile<MODE_HASH, 3, true>);
+    case 4: return reinterpret_cast<const void*>(&k_tile<MODE_HASH, 4, true>);
+    default: return tile_kernel(MODE_HASH, nacc);
+  }
+}
+
 // ---- run-time specialised pipeline kernels (jit.cu) ------------------------------
 // The generic k_tile reads its pipeline description from shared memory and
 // dispatches per term / factor at run time. For large scans the same pipeline
@@ -3859,7 +3869,18 @@ struct Runner {
       if (!col_index(ps.keys[i])) return nofuse(__LINE__);
     for (int i = 0; i < ps.nhkeys; ++i)  // int64 fact keys come from the staged tile
       if (!ps.hkeys[i].width && ps.hkeys[i].x.src < 0 && !col_index(ps.hkeys[i].x)) return nofuse(__LINE__);
-    ts.rows = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::ROWS : kTileRows;
+    // the common hash-group shape runs the lean instance (fused_kernels.cuh)
+    bool lean = P.mode == MODE_HASH && !ps.hpriv && !ps.htag && ps.hlimbs == 2 && ps.hflags < 0 && ps.nprobes == 0 &&
+                !ps.weighted && !std::getenv("TQP_HASH_NOLEAN");
+    for (int i = 0; lean && i < ps.nhkeys; ++i) {
+      const GKey& K = ps.hkeys[i];
+      lean = K.x.src < 0 && K.x.col >= 0 && !K.width && !K.dkeys;
+    }
+    for (int a = 0; lean && a < ps.nacc; ++a) {
+      lean = ps.acc[a].gate_probe < 0;
+      for (int i = 0; lean && i < kFixedFactors; ++i) lean = ps.acc[a].f[i].x.src < 0;
+    }
+    ts.rows = P.mode == MODE_SMALL ? TileShape<MODE_SMALL>::ROWS : lean ? TileShape<MODE_HASH, true>::ROWS : kTileRows;
     ts.aux_bytes = static_cast<int>(P.mode == MODE_SMALL    ? aux_bytes_for<MODE_SMALL>(ps.nacc)
                                     : P.mode == MODE_SCALAR ? aux_bytes_for<MODE_SCALAR>(ps.nacc)
                                                             : aux_bytes_for<MODE_BUILDGRP>(ps.nacc));
@@ -3887,7 +3908,7 @@ struct Runner {
     const int optin = c.smem_optin();
     cudaFuncAttributes fa{};
     const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
-    const void* kfn = tile_kernel(P.mode, ps.nacc);
+    const void* kfn = lean ? tile_kernel_lean(ps.nacc) : tile_kernel(P.mode, ps.nacc);
     if (!kfn) return nofuse(__LINE__);
     const bool jit = jit_wanted(ps.n) && P.mode != MODE_HASH && !generic_only && ps.nacc > 0;
     if (jit) {
@@ -3912,7 +3933,7 @@ struct Runner {
     const std::string tile_name = std::string(jit ? "q_tile<" : "k_tile<") +
                                   (P.mode == MODE_SCALAR  ? "scalar"
                                    : P.mode == MODE_SMALL ? "small"
-                                   : P.mode == MODE_HASH  ? (ps.hpriv ? "hash-priv" : ps.hdirect ? "hash-direct" : "hash")
+                                   : P.mode == MODE_HASH  ? (ps.hpriv ? "hash-priv" : lean ? "hash-lean" : ps.hdirect ? "hash-direct" : "hash")
                                                           : "buildgrp") + "," +
                                   std::to_string(ps.nacc) + ">";
     auto launch_tile = [&](const void* kernel, int threads, int grid_) -> void {
@@ -3968,7 +3989,7 @@ struct Runner {
       launch_tile(kfn, small_threads, grid);
       if (!po) nrows = final_small(c, reinterpret_cast<const SmallPart*>(ps.part), grid, fs, err, outs);
     } else if (P.mode == MODE_HASH) {
-      launch_tile(kfn, TileShape<MODE_HASH>::THREADS, grid);
+      launch_tile(kfn, lean ? TileShape<MODE_HASH, true>::THREADS : TileShape<MODE_HASH>::THREADS, grid);
       auto pres = c.alloc_bytes(sizeof(unsigned) * ((hcap + 31) / 32 + 1));
       keep.push_back(pres);
       keep.push_back(htag_buf);

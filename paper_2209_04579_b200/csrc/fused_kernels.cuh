@@ -314,9 +314,16 @@ __device__ void load_desc(const TileSpec& t, TileDesc& d) {
   for (int p = 0; p < s.nprobes; ++p) d.p_off[p] = static_cast<unsigned>(t.col_off[s.probes[p].key.col]);
 }
 
-template <int MODE, int NA_>
-__global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const TileSpec t) {
-  using S = TileShape<MODE>;
+// LEAN (MODE_HASH only): the common hash-group shape compiled without the
+// general features - fact-column int keys (no dictionary, no string bytes),
+// a direct table of 2-limb records, no probes, weights, gates or special-value
+// flags. Same operation order as the general instance (same bits); the
+// general kernel is ~14 k instructions and its hot loop missed the
+// instruction cache (ncu: 40 % of warp stalls were no_instructions).
+template <int MODE, int NA_, bool LEAN = false>
+__global__ void __launch_bounds__(TileShape<MODE, LEAN>::THREADS, 1) k_tile(const TileSpec t) {
+  using S = TileShape<MODE, LEAN>;
+  constexpr bool LN = LEAN && MODE == MODE_HASH;
   constexpr int CW = S::CW, CT = S::CT, R = S::R, SUB = S::SUB;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long s_wred[MODE == MODE_SMALL ? kGroups : 1][kMaxAcc + 1][CW];
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       RowCtx rc[R];
 #pragma unroll
       for (int p = 0; p < kMaxProbes; ++p) {
-        if (p < d.nprobes) {
+        if (!LN && p < d.nprobes) {
           const Probe& pr = s.probes[p];
           const unsigned long long* col = reinterpret_cast<const unsigned long long*>(stage + d.p_off[p]);
 #pragma unroll
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         wt[k] = 1u;
-        if (s.weighted && pass[k]) {
+        if (!LN && s.weighted && pass[k]) {
 #pragma unroll
           for (int p = 0; p < kMaxProbes; ++p) {
             if (p < d.nprobes) {
@@ -507,12 +514,18 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 long long rid = rc[k].rid[0];  // static select keeps rc in registers
 #pragma unroll
                 for (int p = 1; p < kMaxProbes; ++p) rid = K.x.src == p ? rc[k].rid[p] : rid;
-                const long long krow = K.x.src < 0 ? row : rid;
+                const long long krow = (LN || K.x.src < 0) ? row : rid;
                 unsigned long long raw = 0;
-                if (!K.width)
-                  raw = K.x.src < 0 ? reinterpret_cast<const unsigned long long*>(stage + t.col_off[K.x.col])[k * CT + ct]
-                                    : ld_row(K.x, rid);
-                const unsigned long long dg = gkey_digit(K, raw, krow);
+                if (LN || !K.width)
+                  raw = (LN || K.x.src < 0) ? reinterpret_cast<const unsigned long long*>(stage + t.col_off[K.x.col])[k * CT + ct]
+                                            : ld_row(K.x, rid);
+                unsigned long long dg;
+                if constexpr (LN) {
+                  dg = raw - static_cast<unsigned long long>(K.kmin);
+                  if (K.step != 1) dg /= static_cast<unsigned long long>(K.step);
+                } else {
+                  dg = gkey_digit(K, raw, krow);
+                }
                 bad = bad || dg >= K.range;
                 code += dg * K.stride;
               }
@@ -520,12 +533,12 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             long long slot = -1;
             if (bad) {
               set_fallback(s.err, FR_KEY_RANGE);
-            } else if (s.hpriv) {
+            } else if (!LN && s.hpriv) {
               slot = static_cast<long long>(code);
               atomicAdd(s_stage_val + slot * (1 + kLimbWords * NA_), static_cast<unsigned long long>(wt[k]));
             } else {
               // direct tables are zeroed up front (no tag, no claim)
-              slot = s.htag ? hash_claim(s, code) : static_cast<long long>(code);
+              slot = (!LN && s.htag) ? hash_claim(s, code) : static_cast<long long>(code);
               if (slot < 0) set_fallback(s.err, FR_HASH_FULL);
               else red_add_hint(s.gcnt + slot * s.gstride, static_cast<unsigned long long>(wt[k]) + kCntAdd, l2_policy_evict_last());
             }
@@ -561,7 +574,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
             const int isrc = MODE == MODE_HASH ? d.a_src[a][0] : -1;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-              if (MODE == MODE_HASH && isrc >= 0) {  // a probe's root column at the matched row
+              if (MODE == MODE_HASH && !LN && isrc >= 0) {  // a probe's root column at the matched row
                 long long rid = rc[k].rid[0];
 #pragma unroll
                 for (int p = 1; p < kMaxProbes; ++p) rid = isrc == p ? rc[k].rid[p] : rid;
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
               } else {
                 v[k] = pass[k] ? col[k * CT + ct] : 0ULL;
               }
-              if (s.weighted && wt[k] != 1u) {  // v * weight, exactly or the exact path
+              if (!LN && s.weighted && wt[k] != 1u) {  // v * weight, exactly or the exact path
                 const __int128 pw = static_cast<__int128>(static_cast<long long>(v[k])) * wt[k];
                 if (pw != static_cast<__int128>(static_cast<long long>(pw))) set_fallback(s.err, FR_INT_RANGE);
                 v[k] = static_cast<unsigned long long>(static_cast<long long>(pw));
@@ -598,7 +611,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
 #pragma unroll
               for (int k = 0; k < R; ++k) {
                 double x = has ? __longlong_as_double(static_cast<long long>(col[k * CT + ct])) : 0.0;
-                if (MODE == MODE_HASH && fsrc >= 0) {  // a probe's root column at the matched row
+                if (MODE == MODE_HASH && !LN && fsrc >= 0) {  // a probe's root column at the matched row
                   long long rid = rc[k].rid[0];
 #pragma unroll
                   for (int p = 1; p < kMaxProbes; ++p) rid = fsrc == p ? rc[k].rid[p] : rid;
@@ -610,7 +623,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
 #pragma unroll
             for (int k = 0; k < R; ++k) dvals[a][k] = dv[k];
             const int gp = d.a_gate_probe[a];
-            if (gp >= 0) {
+            if (!LN && gp >= 0) {
               const int gb = d.a_gate_bit[a];
               const double ge = d.a_gate_else[a];
 #pragma unroll
@@ -654,7 +667,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 const double dv = __longlong_as_double(static_cast<long long>(v[k]));
                 if (!f64_to_qf(dv, MODE == MODE_HASH ? s.qfrac : 64, qv)) {
                   qv = 0;
-                  if (MODE == MODE_HASH && s.hflags >= 0 && (isnan(dv) || isinf(dv))) {
+                  if (MODE == MODE_HASH && !LN && s.hflags >= 0 && (isnan(dv) || isinf(dv))) {
                     const unsigned long long bit = isnan(dv) ? 1ULL : dv > 0 ? 2ULL : 4ULL;
                     atomicOr(s.gcnt + static_cast<long long>(g[k]) * s.gstride + s.hflags, bit << (3 * a));
                   } else {
@@ -665,14 +678,14 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
                 } else {
                   fabsmax = fmax(fabsmax, fabs(dv));
                 }
-                if (wt[k] != 1u) {  // exact: the weight multiplies the fixed-point value
+                if (!LN && wt[k] != 1u) {  // exact: the weight multiplies the fixed-point value
                   qv *= static_cast<__int128>(wt[k]);
                   fabsmax = fmax(fabsmax, fabs(dv) * static_cast<double>(wt[k]));
                 }
               }
-              if (MODE == MODE_HASH && s.hpriv) {
+              if (MODE == MODE_HASH && !LN && s.hpriv) {
                 atomic_add_limbs(s_stage_val + static_cast<long long>(g[k]) * (1 + kLimbWords * NA_) + 1 + a * kLimbWords, qv);
-              } else if (MODE == MODE_HASH && s.hlimbs == 2) {
+              } else if (MODE == MODE_HASH && (LN || s.hlimbs == 2)) {
                 if (!atomic_add_limbs2(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * 2, qv, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
               } else {
                 atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
@@ -739,7 +752,7 @@ __global__ void __launch_bounds__(TileShape<MODE>::THREADS, 1) k_tile(const Tile
       out[kMaxAcc] = c;
     }
   } else if constexpr (MODE == MODE_HASH) {
-    if (s.hpriv) {
+    if (!LN && s.hpriv) {
       // flush the CTA's records into the (direct) global table: one add per
       // word per CTA, limbs re-split so every added limb is < 2^42; the
       // packed count carries the adds for the reader's limb bound

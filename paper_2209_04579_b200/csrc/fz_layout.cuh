@@ -663,16 +663,19 @@ constexpr int kMaxCols = 10;
 
 // consumer warps per mode (+1 producer warp): small-group keeps 48 register
 // accumulators per thread, so it runs fewer, wider threads
-template <int MODE>
+template <int MODE, bool LEAN = false>
 struct TileShape {
   // small-group keeps per-thread shared-memory accumulators (groups x
-  // accumulators x threads), so its tiles are half as tall
+  // accumulators x threads), so its tiles are half as tall. The lean
+  // hash-group instance (LEAN) has the same shape: 24 or 28 consumer warps
+  // (2 rows per thread) ran its scan 3-7 % slower than 16 (qg at SF10)
   static constexpr int ROWS = MODE == MODE_SMALL ? 1024 : kTileRows;  // MODE_HASH: as SCALAR
   static constexpr int CW = MODE == MODE_SMALL ? 8 : 16;
   static constexpr int CT = CW * 32;
   static constexpr int THREADS = CT + 32;
   static constexpr int R = ROWS / CT;  // rows per consumer thread
   static constexpr int SUB = R;
+  static_assert(ROWS % CT == 0, "a tile is a whole number of rows per consumer thread");
 };
 
 struct TileSpec {

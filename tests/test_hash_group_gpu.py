@@ -62,3 +62,24 @@ def test_qg_sf10_fused_equals_per_instruction(ctx):
     c = fused.execute(li).to_numpy()
     for (na, _, xa), (_, _, xc) in zip(a, c):
         assert np.array_equal(xa.view(np.uint8), xc.view(np.uint8)), na
+
+
+def test_qg_lean_kernel_equals_general(ctx, monkeypatch):
+    """The lean hash-group instance (fact int keys, direct 2-limb table) and
+    the general k_tile<MODE_HASH> produce the same bits (TQP_HASH_NOLEAN
+    forces the general one)."""
+    from paper_2209_04579_b200 import tqp
+    li = {"lineitem": tqp.Table.generate("lineitem", 1.0, 7)}
+    ex = tqp.Executor(PLAN)
+    ex.set_timing(True)
+    a = ex.execute(li).to_numpy()
+    assert any("hash-lean" in k for k in ex.timings()), ex.timings()
+    monkeypatch.setenv("TQP_HASH_NOLEAN", "1")
+    ex2 = tqp.Executor(PLAN)
+    ex2.set_timing(True)
+    b = ex2.execute(li).to_numpy()
+    assert not any("hash-lean" in k for k in ex2.timings()), ex2.timings()
+    assert ex.fallbacks == 0 and ex2.fallbacks == 0
+    for (na, ta, xa), (nb, tb, xb) in zip(a, b):
+        assert (na, ta) == (nb, tb)
+        assert np.array_equal(xa.view(np.uint8), xb.view(np.uint8)), na
