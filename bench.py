@@ -546,7 +546,9 @@ def run_hash_group(args, tqp, torch, ctx, stream, tables, L):
     ctx.sync()
     units = ex.timings()
     ex.set_timing(False)
-    groups = ex.execute(li).to_numpy()[0][2].shape[0]
+    res = ex.execute(li).to_numpy()
+    groups = res[0][2].shape[0]
+    passing = int(res[-1][2].sum())  # COUNT(*) per group
     nf = tqp.Executor(plan, fuse=False, ctx=ctx)
     nf.execute(li)
     ms_nf = timed_queries(torch, stream, lambda q: nf.execute(li), ["qg"], 3)["qg"]
@@ -559,7 +561,18 @@ def run_hash_group(args, tqp, torch, ctx, stream, tables, L):
             "hbm_frac": b / (ms / 1e3) / 1e9 / peak, "scan_kernel_ms": scan_ms,
             "scan_kernel_hbm_frac": (b / (scan_ms / 1e3) / 1e9 / peak) if scan_ms else None,
             "units": units, "explain": ex.explain(), "cold_ms": cold, "fallbacks": ex.fallbacks,
-            "per_instruction_ms": ms_nf, "speedup_vs_per_instruction": ms_nf / ms}
+            "per_instruction_ms": ms_nf, "speedup_vs_per_instruction": ms_nf / ms,
+            # the scan's real bound: one RED for the group's count and two
+            # (2-limb exact sums) per accumulator for every passing row, against
+            # the measured ceiling of random 64-bit REDs (profiles/r2_red_probe.txt)
+            "atomic_roofline": ({"bound": "l2_atomics", "reds_per_launch": passing * (1 + 2 * 2),
+                                 "achieved": passing * 5 / (scan_ms / 1e3) / 1e9, "peak": RED_PEAK_GOPS,
+                                 "unit": "G RED/s", "frac": passing * 5 / (scan_ms / 1e3) / 1e9 / RED_PEAK_GOPS,
+                                 "peak_source": "tools/red_probe.cu on a B200 (profiles/r2_red_probe.txt)"}
+                                if scan_ms else None)}
+
+
+RED_PEAK_GOPS = 188.0  # random 64-bit REDs per second, measured (profiles/r2_red_probe.txt)
 
 
 def run_dropin_leg(sf: float = 1.0):

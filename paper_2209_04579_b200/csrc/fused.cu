@@ -1353,6 +1353,8 @@ struct GroupSpec {
   int flag_word = -1;                 // MODE_HASH special run: record word of the NaN/Inf bits
   int qfrac = 64;                     // fixed-point fraction bits of the sums
   int limb2 = 0;                      // MODE_HASH 2-limb sums (checked per group against fmax)
+  int acc_off[kMaxAcc] = {};           // limb2: word of accumulator a (ProbeSpec::hoff)
+  unsigned acc_int1 = 0;              // limb2: accumulator a is one int64 word (bit a)
   const long long* fmax = nullptr;    // max |fp64 value| (bits) of the scan
   int direct_codes = 0;               // MODE_HASH direct table: the group's code is its slot
   int row_in_cnt = 0;                 // BUILDGRP row_rec build: count word = (row + 1) << 32 | rows
@@ -1388,7 +1390,11 @@ __device__ __forceinline__ bool group_limbs_ok(const GroupSpec& s, unsigned g) {
 
 // accumulator a of group g as int128
 __device__ __forceinline__ __int128 group_acc(const GroupSpec& s, unsigned g, int a) {
-  if (s.limb2) return limbs2_to_i128(s.gacc + static_cast<long long>(g) * s.acc_stride + a * 2);
+  if (s.limb2) {
+    const unsigned long long* w = s.gacc + static_cast<long long>(g) * s.acc_stride + s.acc_off[a];
+    if ((s.acc_int1 >> a) & 1u) return static_cast<__int128>(static_cast<long long>(w[0]));
+    return limbs2_to_i128(w);
+  }
   const unsigned long long* w = s.gacc + static_cast<long long>(g) * s.acc_stride + a * s.acc_words;
   if (s.acc_words == kLimbWords) return limbs_to_i128(w);
   return static_cast<__int128>((static_cast<unsigned __int128>(w[1]) << 64) | w[0]);
@@ -2528,6 +2534,20 @@ std::string gen_pipeline(const TileSpec& ts, int mode, int cw, const std::vector
     if (s.group_probe < 0 || s.group_probe >= s.nprobes) throw Error(TQP_ERR_EXEC, "internal: build-group pipeline without a group probe");
     o << "  gid = gid" << s.group_probe << ";\n";
   }
+  if (mode == MODE_HASH) {
+    // lean hash-group shape only (fact int keys, direct table): the group's
+    // slot is its code, the mixed-radix number of the key digits
+    o << "  { unsigned long long c = 0ULL;\n";
+    for (int q = 0; q < s.nhkeys; ++q) {
+      const GKey& K = s.hkeys[q];
+      o << "    { unsigned long long d = q_u64(stage, " << off(K.x.col) << ", ri) - " << hex64(static_cast<unsigned long long>(K.kmin))
+        << ";\n";
+      if (K.step != 1) o << "      d /= " << hex64(static_cast<unsigned long long>(K.step)) << ";\n";
+      o << "      if (pass && d >= " << hex64(K.range) << ") { set_fallback(t.p.err, FR_KEY_RANGE); pass = false; }\n"
+        << "      c += d * " << hex64(K.stride) << "; }\n";
+    }
+    o << "    gid = pass ? static_cast<unsigned>(c) : 0u; }\n";
+  }
   if (mode == MODE_SMALL) {
     o << "  code = 0u;\n";
     for (int q = 0; q < s.nkeys; ++q)
@@ -3064,6 +3084,10 @@ GroupSpec hash_group_spec(const ProbeSpec& ps, const FinalSpec& fs, const unsign
   gs.flag_word = ps.hflags;
   gs.qfrac = ps.qfrac;
   gs.limb2 = ps.hlimbs == 2 ? 1 : 0;
+  for (int a = 0; a < ps.nacc && a < kMaxAcc; ++a) {
+    gs.acc_off[a] = ps.hoff[a];
+    if (gs.limb2 && ps.acc[a].is_int) gs.acc_int1 |= 1u << a;
+  }
   gs.fmax = ps.fmax_out;
   for (int i = 0; i < ps.nhkeys; ++i) {
     gs.key_cols[i] = nullptr;
@@ -3765,9 +3789,15 @@ struct Runner {
       // 3-limb records are padded to whole 32-byte sectors, 2-limb ones are
       // kept dense (an L2-resident table is worth more than aligned records)
       const int L = (hlimbs == 2 && !po) ? 2 : kLimbWords;  // sharded partials: 3 limbs (no per-group fmax check)
-      hrec_words = 1 + L * std::max(1, nacc_all) + (special ? 1 : 0);
+      int W = 0;  // accumulator words per record (ProbeSpec::hoff)
+      for (int a = 0; a < ps.nacc; ++a) {
+        ps.hoff[a] = W;
+        W += (L == 2 && ps.acc[a].is_int) ? 1 : L;
+      }
+      W = std::max(W, L * std::max(0, 1 - ps.nacc));  // no accumulator: one (unused) slot
+      hrec_words = 1 + W + (special ? 1 : 0);
       if (L == kLimbWords) hrec_words = (hrec_words + 3) & ~3;
-      ps.hflags = special ? 1 + L * std::max(1, nacc_all) : -1;
+      ps.hflags = special ? 1 + W : -1;
       ps.hlimbs = L;
       const size_t priv_bytes = static_cast<size_t>(R) * (1 + kLimbWords * nacc_all) * sizeof(unsigned long long);
       ps.hpriv = priv_bytes <= kHashPrivBytes && !std::getenv("TQP_HASH_NOPRIV");
@@ -3910,7 +3940,7 @@ struct Runner {
     const size_t fixed = 256 + static_cast<size_t>(ts.aux_bytes);
     const void* kfn = lean ? tile_kernel_lean(ps.nacc) : tile_kernel(P.mode, ps.nacc);
     if (!kfn) return nofuse(__LINE__);
-    const bool jit = jit_wanted(ps.n) && P.mode != MODE_HASH && !generic_only && ps.nacc > 0;
+    const bool jit = jit_wanted(ps.n) && (P.mode != MODE_HASH || lean) && !generic_only && ps.nacc > 0;
     if (jit) {
       std::vector<int> bm;
       for (const auto& pd : P.probes) bm.push_back(probe_mode_of(P.builds[pd.build]));

@@ -686,7 +686,9 @@ __global__ void __launch_bounds__(TileShape<MODE, LEAN>::THREADS, 1) k_tile(cons
               if (MODE == MODE_HASH && !LN && s.hpriv) {
                 atomic_add_limbs(s_stage_val + static_cast<long long>(g[k]) * (1 + kLimbWords * NA_) + 1 + a * kLimbWords, qv);
               } else if (MODE == MODE_HASH && (LN || s.hlimbs == 2)) {
-                if (!atomic_add_limbs2(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * 2, qv, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
+                unsigned long long* w = s.gacc + static_cast<long long>(g[k]) * s.gstride + s.hoff[a];
+                if (is_int) red_add_hint(w, static_cast<unsigned long long>(static_cast<long long>(qv)), l2_policy_evict_last());
+                else if (!atomic_add_limbs2(w, qv, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
               } else {
                 atomic_add_limbs(s.gacc + static_cast<long long>(g[k]) * s.gstride + a * kLimbWords, qv);
               }
@@ -768,7 +770,9 @@ __global__ void __launch_bounds__(TileShape<MODE, LEAN>::THREADS, 1) k_tile(cons
         for (int a = 0; a < NA_; ++a) {
           const __int128 v = limbs_to_i128(r + 1 + a * kLimbWords);
           if (s.hlimbs == 2) {
-            if (!atomic_add_limbs2(s.gacc + code * s.gstride + a * 2, v, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
+            unsigned long long* w = s.gacc + code * s.gstride + s.hoff[a];
+            if (s.acc[a].is_int) red_add_hint(w, static_cast<unsigned long long>(static_cast<long long>(v)), l2_policy_evict_last());
+            else if (!atomic_add_limbs2(w, v, l2_policy_evict_last())) set_fallback(s.err, FR_LIMB2);
           } else {
             atomic_add_limbs(s.gacc + code * s.gstride + a * kLimbWords, v);
           }

@@ -224,6 +224,11 @@ struct ProbeSpec {
   // while every value fits 105 bits; the reader checks per group that
   // adds < 2^22 and fmax x rows < 2^41 (else the unit re-runs with 3 limbs)
   int hlimbs;
+  // word of accumulator a in a record (after the count word): 2-limb records
+  // keep an int64 sum in ONE word (exact: the reader checks the scan's max
+  // |value| x rows < 2^63 per group, so the wrapping add never wraps), an
+  // fp64 sum in two limbs; 3-limb records: a * 3
+  int hoff[kMaxAcc];
   long long* fmax_out;  // max |fp64 value| (bit pattern, atomicMax) over the scan
 };
 

@@ -60,7 +60,8 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int st = static_cast<int>(it % nst);
         if (it >= nst) mbar_wait(&empty[st], static_cast<unsigned>(((it / nst) - 1) & 1));
-        issue_tile(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
+        if (Q_MODE == MODE_HASH && t.evict_first) issue_tile<true>(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
+        else issue_tile(t, stages + static_cast<size_t>(st) * t.stage_bytes, &full[st], tile);
       }
     }
   } else {
@@ -168,6 +169,34 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
           cell[Q_NA * Q_CT] += pass[k] ? 1u : 0u;
         }
 #endif
+      } else if constexpr (Q_MODE == MODE_HASH) {
+        // k_tile<MODE_HASH, NA, LEAN>'s row update: packed count, then the
+        // exact 2-limb sums (Q(128-F).F fixed point, F = s.qfrac)
+        const unsigned long long pol = l2_policy_evict_last();
+#pragma unroll
+        for (int k = 0; k < Q_R; ++k) {
+          if (!pass[k]) continue;
+          unsigned long long* rec = s.gcnt + static_cast<long long>(gid[k]) * s.gstride;
+          red_add_hint(rec, 1ULL + kCntAdd, pol);
+#pragma unroll
+          for (int a = 0; a < Q_NA; ++a) {
+            __int128 qv;
+            if (q_is_int(a)) {
+              qv = static_cast<__int128>(static_cast<long long>(v[k][a]));
+            } else {
+              const double dv = __longlong_as_double(static_cast<long long>(v[k][a]));
+              if (!f64_to_qf(dv, s.qfrac, qv)) {
+                qv = 0;
+                set_fallback(s.err, FR_Q64_CONVERT);
+                if (s.qstats && !isnan(dv) && !isinf(dv)) atomicMax(s.qstats, static_cast<long long>(-lowbit_exp(dv)));
+              } else {
+                fabsmax = fmax(fabsmax, fabs(dv));
+              }
+            }
+            if (q_is_int(a)) red_add_hint(rec + 1 + s.hoff[a], static_cast<unsigned long long>(static_cast<long long>(qv)), pol);
+            else if (!atomic_add_limbs2(rec + 1 + s.hoff[a], qv, pol)) set_fallback(s.err, FR_LIMB2);
+          }
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < Q_R; ++k) {
@@ -194,8 +223,16 @@ extern "C" __global__ void __launch_bounds__(Q_CT + 32, 1) q_tile(const TileSpec
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    // int64 sums are exact only while |v| * rows < 2^63: otherwise the exact path
-    if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) set_fallback(s.err, FR_INT_RANGE);
+    // int64 sums are exact only while |v| * rows < 2^63: otherwise the exact
+    // path (hash groups: checked per group against the scan's max at output)
+    if constexpr (Q_MODE == MODE_HASH) {
+      if (s.absmax_out && absmax) atomicMax(s.absmax_out, absmax);
+      else if (!s.absmax_out && static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) set_fallback(s.err, FR_INT_RANGE);
+      q64_range_check(fabsmax, s.n, s.err, s.qfrac);
+      if (s.fmax_out && fabsmax > 0.0) atomicMax(s.fmax_out, __double_as_longlong(fabsmax));
+    } else if (static_cast<double>(absmax) * static_cast<double>(s.n) >= 9.0e18) {
+      set_fallback(s.err, FR_INT_RANGE);
+    }
     if constexpr (Q_MODE == MODE_BUILDGRP) q64_range_check(fabsmax, s.n, s.err);
     if constexpr (Q_MODE == MODE_SMALL) {
 #pragma unroll

@@ -64,22 +64,26 @@ def test_qg_sf10_fused_equals_per_instruction(ctx):
         assert np.array_equal(xa.view(np.uint8), xc.view(np.uint8)), na
 
 
-def test_qg_lean_kernel_equals_general(ctx, monkeypatch):
-    """The lean hash-group instance (fact int keys, direct 2-limb table) and
-    the general k_tile<MODE_HASH> produce the same bits (TQP_HASH_NOLEAN
-    forces the general one)."""
+def test_qg_hash_instances_agree(ctx, monkeypatch):
+    """The three kernels a lean hash-group unit can run - the NVRTC pipeline
+    (q_tile<hash-lean>), the lean template instance (TQP_JIT=0) and the
+    general k_tile<MODE_HASH> (TQP_HASH_NOLEAN) - produce the same bits."""
     from paper_2209_04579_b200 import tqp
     li = {"lineitem": tqp.Table.generate("lineitem", 1.0, 7)}
-    ex = tqp.Executor(PLAN)
-    ex.set_timing(True)
-    a = ex.execute(li).to_numpy()
-    assert any("hash-lean" in k for k in ex.timings()), ex.timings()
-    monkeypatch.setenv("TQP_HASH_NOLEAN", "1")
-    ex2 = tqp.Executor(PLAN)
-    ex2.set_timing(True)
-    b = ex2.execute(li).to_numpy()
-    assert not any("hash-lean" in k for k in ex2.timings()), ex2.timings()
-    assert ex.fallbacks == 0 and ex2.fallbacks == 0
-    for (na, ta, xa), (nb, tb, xb) in zip(a, b):
-        assert (na, ta) == (nb, tb)
-        assert np.array_equal(xa.view(np.uint8), xb.view(np.uint8)), na
+    runs = {}
+    for name, env in (("jit", {}), ("lean", {"TQP_JIT": "0"}), ("general", {"TQP_JIT": "0", "TQP_HASH_NOLEAN": "1"})):
+        for k in ("TQP_JIT", "TQP_HASH_NOLEAN"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ex = tqp.Executor(PLAN)
+        ex.set_timing(True)
+        runs[name] = ex.execute(li).to_numpy()
+        kernels = [k for k in ex.timings() if k.startswith("kernel:")]
+        want = {"jit": "q_tile<hash-lean", "lean": "k_tile<hash-lean", "general": "k_tile<hash-direct"}[name]
+        assert any(want in k for k in kernels), (name, kernels)
+        assert ex.fallbacks == 0
+    for name in ("lean", "general"):
+        for (na, ta, xa), (nb, tb, xb) in zip(runs["jit"], runs[name]):
+            assert (na, ta) == (nb, tb)
+            assert np.array_equal(xa.view(np.uint8), xb.view(np.uint8)), (name, na)
