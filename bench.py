@@ -562,12 +562,13 @@ def run_hash_group(args, tqp, torch, ctx, stream, tables, L):
             "scan_kernel_hbm_frac": (b / (scan_ms / 1e3) / 1e9 / peak) if scan_ms else None,
             "units": units, "explain": ex.explain(), "cold_ms": cold, "fallbacks": ex.fallbacks,
             "per_instruction_ms": ms_nf, "speedup_vs_per_instruction": ms_nf / ms,
-            # the scan's real bound: one RED for the group's count and two
-            # (2-limb exact sums) per accumulator for every passing row, against
-            # the measured ceiling of random 64-bit REDs (profiles/r2_red_probe.txt)
-            "atomic_roofline": ({"bound": "l2_atomics", "reds_per_launch": passing * (1 + 2 * 2),
-                                 "achieved": passing * 5 / (scan_ms / 1e3) / 1e9, "peak": RED_PEAK_GOPS,
-                                 "unit": "G RED/s", "frac": passing * 5 / (scan_ms / 1e3) / 1e9 / RED_PEAK_GOPS,
+            # the scan's real bound: per passing row one RED for the group's
+            # count, two for revenue (fp64: 2-limb exact sum) and one for
+            # sum_qty (int64: one word), against the measured ceiling of
+            # random 64-bit REDs (profiles/r2_red_probe.txt)
+            "atomic_roofline": ({"bound": "l2_atomics", "reds_per_launch": passing * 4,
+                                 "achieved": passing * 4 / (scan_ms / 1e3) / 1e9, "peak": RED_PEAK_GOPS,
+                                 "unit": "G RED/s", "frac": passing * 4 / (scan_ms / 1e3) / 1e9 / RED_PEAK_GOPS,
                                  "peak_source": "tools/red_probe.cu on a B200 (profiles/r2_red_probe.txt)"}
                                 if scan_ms else None)}
 
