@@ -9,8 +9,12 @@
 namespace tqp {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kItems = 8;  // rows per thread (warp-striped): 2048-row tiles
+#ifndef TQP_SCAN_THREADS
+#define TQP_SCAN_THREADS 256
+#define TQP_SCAN_ITEMS 8
+#endif
+constexpr int kThreads = TQP_SCAN_THREADS;
+constexpr int kItems = TQP_SCAN_ITEMS;  // rows per thread (warp-striped): 2048-row tiles
 constexpr int kTile = kThreads * kItems;
 
 struct ScanScratch {
