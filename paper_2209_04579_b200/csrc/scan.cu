@@ -76,7 +76,14 @@ __device__ __forceinline__ void tile_offsets(unsigned long long wtotal, unsigned
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restrict__ x, int64_t* __restrict__ out,
+// Occupancy sets this kernel's speed: a tile's loads are its only memory
+// parallelism, so the warp scans are done twice (totals before the lookback,
+// the exclusive prefixes after it) instead of keeping kItems prefixes in
+// registers across it: 64 -> 32 registers (a few words spilled to L1), 4 -> 8 resident tiles per SM.
+#ifndef TQP_SCAN_MINB
+#define TQP_SCAN_MINB 8
+#endif
+__global__ void __launch_bounds__(kThreads, TQP_SCAN_MINB) k_prefix_sum(const int64_t* __restrict__ x, int64_t* __restrict__ out,
                                                          int64_t n, longlong2* desc, int* counter, long long* err) {
   __shared__ int s_tile;
   __shared__ unsigned long long s_warp[kThreads / 32 + 1];
@@ -87,23 +94,22 @@ __global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restri
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wbase = static_cast<int64_t>(tile) * kTile + static_cast<int64_t>(warp) * 32 * kItems + lane;
   int64_t v[kItems];
-  unsigned long long ex[kItems];  // exclusive prefix within the warp
 #pragma unroll
   for (int j = 0; j < kItems; ++j) v[j] = wbase + j * 32 < n ? x[wbase + j * 32] : 0;
-  unsigned long long carry = 0;
+  unsigned long long lsum = 0;
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) lsum += static_cast<unsigned long long>(v[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  tile_offsets(lsum, s_warp, &s_prefix, desc, tile);
+  unsigned long long carry = static_cast<unsigned long long>(s_prefix) + s_warp[warp];
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const unsigned long long is = warp_incl_scan(static_cast<unsigned long long>(v[j]));
-    ex[j] = carry + is - static_cast<unsigned long long>(v[j]);
+    const unsigned long long acc = carry + is - static_cast<unsigned long long>(v[j]);
     carry += __shfl_sync(0xffffffffu, is, 31);
-  }
-  tile_offsets(carry, s_warp, &s_prefix, desc, tile);
-  const unsigned long long off = static_cast<unsigned long long>(s_prefix) + s_warp[warp];
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
     const int64_t i = wbase + j * 32;
     if (i < n) {
-      const unsigned long long acc = off + ex[j];
       out[i] = static_cast<int64_t>(acc);
       int64_t r;
       if (add_ovf(static_cast<int64_t>(acc), v[j], &r)) note_bad(err, i);
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_prefix_sum(const int64_t* __restri
 // output rows (coalesced, warp-striped as the prefix sum). Rows of several
 // columns (m > 1) are copied column by column per selected row.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_compact_onepass(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(kThreads, 8) k_compact_onepass(const T* __restrict__ vals, const uint8_t* __restrict__ mask,
                                                               int64_t n, int64_t m, T* __restrict__ out, longlong2* desc,
                                                               int* counter) {
   __shared__ int s_tile;

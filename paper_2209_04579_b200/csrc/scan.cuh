@@ -4,6 +4,10 @@
 
 #include "device.cuh"
 
+#ifndef TQP_LOOKBACK_SLEEP
+#define TQP_LOOKBACK_SLEEP 0
+#endif
+
 namespace tqp {
 
 // 16-byte tile descriptor {status, value}; published and read as one 128-bit
@@ -39,9 +43,15 @@ __device__ __forceinline__ long long tile_lookback(longlong2* desc, int tile, lo
     int idx = base - lane;
     longlong2 d = make_longlong2(TILE_INCLUSIVE, 0);
     if (idx >= 0) {
-      do {
+      d = tile_read(desc + idx);
+#if TQP_LOOKBACK_SLEEP
+      for (unsigned ns = TQP_LOOKBACK_SLEEP; d.x == TILE_INVALID; ns = ns < 1024 ? 2 * ns : ns) {
+        __nanosleep(ns);
         d = tile_read(desc + idx);
-      } while (d.x == TILE_INVALID);
+      }
+#else
+      while (d.x == TILE_INVALID) d = tile_read(desc + idx);
+#endif
     }
     unsigned incl = __ballot_sync(0xffffffffu, d.x == TILE_INCLUSIVE);
     int stop = incl ? __ffs(incl) - 1 : 31;
