@@ -37,6 +37,7 @@ struct SumF {
 struct SumI {
   __int128 s = 0, mn = 0, mx = 0;
   bool empty = true;
+  bool bounded = false;  // mn / mx are bounds of the prefixes, not their values (exact s)
 };
 template <typename T>
 struct MinMax {
@@ -52,6 +53,7 @@ __device__ __forceinline__ SumI combine(const SumI& a, const SumI& b) {
   SumI r;
   r.empty = false;
   r.s = a.s + b.s;
+  r.bounded = a.bounded || b.bounded;
   __int128 bmn = a.s + b.mn, bmx = a.s + b.mx;
   r.mn = a.mn < bmn ? a.mn : bmn;
   r.mx = a.mx > bmx ? a.mx : bmx;
@@ -92,6 +94,7 @@ __device__ __forceinline__ SumI shfl(const SumI& p, int src) {
   r.mn = shfl128(p.mn, src);
   r.mx = shfl128(p.mx, src);
   r.empty = __shfl_sync(0xffffffffu, static_cast<int>(p.empty), src);
+  r.bounded = __shfl_sync(0xffffffffu, static_cast<int>(p.bounded), src);
   return r;
 }
 template <typename T>
@@ -344,6 +347,61 @@ __global__ void k_long_chunks(const T* __restrict__ v, const int64_t* __restrict
     }
     return;
   }
+  if constexpr (std::is_same_v<T, int64_t> && OP == TQP_SUM) {
+    // int64 sums: while max|v| x rows < 2^62 no prefix of the chunk can leave
+    // int64, so a wrapping sum in any order is the exact chunk sum and
+    // +-max|v| x rows bound every prefix (the partial is marked bounded:
+    // k_long_finish decides overflow from the bounds or recomputes the
+    // segment exactly). Coalesced two-row loads; else the ordered monoid.
+    __shared__ unsigned long long s_sum[32], s_amax[32];
+    unsigned long long sum = 0, amax = 0;
+    const int64_t a2 = (a + 1) & ~int64_t(1);
+    auto take = [&](int64_t x) {
+      sum += static_cast<unsigned long long>(x);
+      const unsigned long long ax = x < 0 ? 0ULL - static_cast<unsigned long long>(x) : static_cast<unsigned long long>(x);
+      amax = ax > amax ? ax : amax;
+    };
+    if (threadIdx.x == 0 && a2 > a && a < b) take(v[a]);
+    const longlong2* v2 = reinterpret_cast<const longlong2*>(v + a2);
+    const int64_t np = b > a2 ? (b - a2) / 2 : 0;
+    for (int64_t i = threadIdx.x; i < np; i += blockDim.x) {
+      const longlong2 x = __ldg(v2 + i);
+      take(x.x);
+      take(x.y);
+    }
+    if (threadIdx.x == 0 && a2 + 2 * np < b && b - 1 >= a2) take(v[b - 1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, amax, o);
+      amax = y > amax ? y : amax;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_sum[warp] = sum;
+      s_amax[warp] = amax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nwarps; ++w) {
+        sum += s_sum[w];
+        amax = s_amax[w] > amax ? s_amax[w] : amax;
+      }
+      s_sum[0] = static_cast<double>(amax) * static_cast<double>(b - a) < 4.0e18 ? 1ULL : 0ULL;  // < 2^62
+      if (s_sum[0]) {
+        P r;
+        if (b > a) {
+          r.empty = false;
+          r.bounded = true;
+          r.s = static_cast<__int128>(static_cast<long long>(sum));
+          r.mx = static_cast<__int128>(amax) * static_cast<__int128>(b - a);
+          r.mn = -r.mx;
+        }
+        parts[blockIdx.x] = r;
+      }
+    }
+    __syncthreads();
+    if (s_sum[0]) return;
+  }
   int64_t len = b - a, per = (len + nwarps - 1) / nwarps;
   int64_t wa = a + warp * per, wb = wa + per < b ? wa + per : b;
   if (wa > wb) wa = wb;
@@ -363,7 +421,8 @@ __global__ void k_long_chunks(const T* __restrict__ v, const int64_t* __restrict
 template <typename T, int OP>
 __global__ void k_long_finish(const typename Acc<T, OP>::P* __restrict__ parts, const int64_t* __restrict__ seg,
                               const int64_t* __restrict__ first_item, const int64_t* __restrict__ nitems, int64_t nlong,
-                              T* __restrict__ out, long long* err) {
+                              T* __restrict__ out, long long* err, const T* __restrict__ v = nullptr,
+                              const int64_t* __restrict__ seg_lo = nullptr, const int64_t* __restrict__ seg_hi = nullptr) {
   using A = Acc<T, OP>;
   using P = typename A::P;
   const int lane = threadIdx.x & 31;
@@ -385,6 +444,14 @@ __global__ void k_long_finish(const typename Acc<T, OP>::P* __restrict__ parts, 
     for (int o = 1; o < 32; o <<= 1) {
       P other = shfl(acc, (lane + o) & 31);
       if ((lane & (2 * o - 1)) == 0 && lane + o < used) acc = A::comb(acc, other);
+    }
+    if constexpr (std::is_same_v<T, int64_t> && OP == TQP_SUM) {
+      // bounded chunk partials whose bounds leave int64: whether a prefix
+      // really overflows (and where) needs the ordered monoid over the rows
+      const SumI a0 = shfl(acc, 0);
+      const __int128 lo64 = static_cast<__int128>(std::numeric_limits<int64_t>::min());
+      const __int128 hi64 = static_cast<__int128>(std::numeric_limits<int64_t>::max());
+      if (a0.bounded && (a0.mn < lo64 || a0.mx > hi64)) acc = warp_reduce_range<T, OP>(v, seg_lo[seg[q]], seg_hi[seg[q]]);
     }
     if (lane == 0) {
       if constexpr (OP == TQP_SUM) {
@@ -495,7 +562,7 @@ void run_reduce(Ctx& c, const Tensor& values, const SegPlan& pl, Tensor& out) {
                                                        static_cast<P*>(parts->ptr));
   k_long_finish<T, OP><<<c.grid_for(pl.nlong * 32, 128), 128, 0, c.stream>>>(
       static_cast<P*>(parts->ptr), pl.d_seg.ptr<int64_t>(), pl.d_first.ptr<int64_t>(), pl.d_cnt.ptr<int64_t>(), pl.nlong,
-      out.ptr<T>(), c.d_err);
+      out.ptr<T>(), c.d_err, values.ptr<T>(), pl.lo.ptr<int64_t>(), pl.hi.ptr<int64_t>());
   c.count_launch(2);
 }
 

@@ -127,6 +127,32 @@ def test_segmented_reduce_long_segments(ctx):
     assert a.tobytes() == b.tobytes()
 
 
+def test_segmented_reduce_long_int64_bounds(ctx):
+    """Long int64 segments take bounded chunk sums (wrapping sum, +-max|v| x
+    rows prefix bounds); where the bounds leave int64 the segment is redone
+    in the ordered monoid: no false overflow, and a real one is still the
+    reference's error (kernels.cpp segmented_reduce)."""
+    from paper_2209_04579_b200 import tqp
+    n = 2_000_000
+    big = (1 << 46) - 1  # chunks stay bounded (x 64 K rows < 2^62), segments do not
+    ids = np.zeros(n, dtype=np.int64)
+    ids[n // 2:] = 1
+    alt = np.where(np.arange(n) % 2 == 0, big, -big).astype(np.int64)
+    alt[7] = 5
+    got = tqp.segmented_reduce(alt.reshape(-1, 1), ids.reshape(-1, 1), 2, "sum").numpy().ravel()
+    want = [int(alt[: n // 2].astype(object).sum()), int(alt[n // 2:].astype(object).sum())]
+    np.testing.assert_array_equal(got, want)
+    # chunks past the bound (values near 2^61): the ordered path per chunk
+    huge = np.where(np.arange(n) % 2 == 0, 1 << 61, -(1 << 61)).astype(np.int64)
+    got = tqp.segmented_reduce(huge.reshape(-1, 1), ids.reshape(-1, 1), 2, "sum").numpy().ravel()
+    np.testing.assert_array_equal(got, [0, 0])
+    # a real overflow in segment 1 only
+    up = np.full(n, big, dtype=np.int64)
+    up[: n // 2] = 1
+    with pytest.raises(tqp.KernelError, match="overflow in segment 1"):
+        tqp.segmented_reduce(up.reshape(-1, 1), ids.reshape(-1, 1), 2, "sum")
+
+
 def test_string_compare_and_plumbing(ctx):
     from paper_2209_04579_b200 import tqp
     strs = ["BUILDING", "AUTOMOBILE", "", "BUILD", "BUILDINGS"]
