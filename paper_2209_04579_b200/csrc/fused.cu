@@ -2074,7 +2074,7 @@ TopkKernel topk_kernel(int nk) {
 __global__ void k_group_rows(const __grid_constant__ GroupSpec s, const long long* __restrict__ gids, const long long* __restrict__ order,
                              long long n, long long* err) {
   for (long long r = gtid(); r < n; r += gstride()) {
-    unsigned g = static_cast<unsigned>(gids[order[r]]);
+    unsigned g = static_cast<unsigned>(gids[order ? order[r] : r]);
     for (int j = 0; j < s.f.nouts; ++j) {
       unsigned long long bits;
       bool f;
@@ -2084,6 +2084,56 @@ __global__ void k_group_rows(const __grid_constant__ GroupSpec s, const long lon
       }
       store_group_out(s, j, r, bits);
     }
+  }
+}
+
+// ascending slots i < n with cnt[i * stride] != 0: one pass, a tile of
+// kSlotTile slots per CTA (dynamic tile ids), ballot + popcount per warp item,
+// the output offset from the decoupled lookback (scan.cuh)
+constexpr int kSlotThreads = 256, kSlotItems = 8, kSlotTile = kSlotThreads * kSlotItems;
+__global__ void __launch_bounds__(kSlotThreads) k_nonzero_slots(const unsigned long long* __restrict__ cnt, long long stride,
+                                                                long long n, long long* __restrict__ out, longlong2* desc,
+                                                                int* counter) {
+  __shared__ int s_tile;
+  __shared__ unsigned long long s_warp[kSlotThreads / 32 + 1];
+  __shared__ long long s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1);
+  __syncthreads();
+  const int tile = s_tile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long wbase = static_cast<long long>(tile) * kSlotTile + static_cast<long long>(warp) * 32 * kSlotItems + lane;
+  unsigned ball[kSlotItems];
+  unsigned mine = 0;
+#pragma unroll
+  for (int j = 0; j < kSlotItems; ++j) {
+    const long long i = wbase + j * 32;
+    ball[j] = __ballot_sync(0xffffffffu, i < n && __ldg(cnt + i * stride) != 0ULL);
+    mine += __popc(ball[j]);
+  }
+  if (lane == 0) s_warp[warp] = mine;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int kW = kSlotThreads / 32;
+    const unsigned long long w = lane < kW ? s_warp[lane] : 0ULL;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    __syncwarp();
+    if (lane < kW) s_warp[lane] = wi - w;
+    const unsigned long long total = __shfl_sync(0xffffffffu, wi, kW - 1);
+    const long long pfx = tile_lookback(desc, tile, static_cast<long long>(total));
+    if (lane == 0) s_prefix = pfx;
+  }
+  __syncthreads();
+  unsigned long long pos = static_cast<unsigned long long>(s_prefix) + s_warp[warp];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kSlotItems; ++j) {
+    if ((ball[j] >> lane) & 1u) out[pos + __popc(ball[j] & lt)] = wbase + j * 32;
+    pos += __popc(ball[j]);
   }
 }
 
@@ -4024,14 +4074,17 @@ struct Runner {
       keep.push_back(pres);
       keep.push_back(htag_buf);
       keep.push_back(hrec_buf);
+      // a direct table's presence bits say no more than its count words:
+      // only the top-k walk reads them
+      const bool want_present = ps.htag || (P.topk && !fullsort);
       if (ps.htag)
         k_hash_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
             ps.htag, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
-      else
+      else if (want_present)
         k_count_present<<<c.grid_for(static_cast<long long>(hcap), 256), 256, 0, c.stream>>>(
             ps.gcnt, ps.gstride, static_cast<long long>(hcap), static_cast<unsigned*>(pres->ptr));
-      c.count_launch();
-      GroupSpec gs = hash_group_spec(ps, fs, static_cast<const unsigned*>(pres->ptr), hdict_vals);
+      if (want_present) c.count_launch();
+      GroupSpec gs = hash_group_spec(ps, fs, want_present ? static_cast<const unsigned*>(pres->ptr) : nullptr, hdict_vals);
       if (po) {
         Tensor gids = touched_groups(c, ps.gcnt, ps.gstride, static_cast<long long>(hcap), gs.present);
         const long long n = gids.rows;
@@ -4220,8 +4273,33 @@ struct Runner {
   }
 
   // cmask: the count bits of a count word (row_in_cnt: the low 32)
+  // ascending slots whose count word is nonzero, in one pass (k_nonzero_slots)
+  static Tensor nonzero_slots(Ctx& c, const unsigned long long* gcnt, long long cnt_stride, long long ngroups) {
+    if (!ngroups) return c.alloc(TQP_I64, 0, 1);
+    const long long tiles = (ngroups + kSlotTile - 1) / kSlotTile;
+    auto scratch = c.alloc_bytes(sizeof(longlong2) * (tiles + 1) + 16);
+    TQP_CUDA(cudaMemsetAsync(scratch->ptr, 0, scratch->bytes, c.stream));
+    auto* desc = static_cast<longlong2*>(scratch->ptr);
+    Tensor o = c.alloc(TQP_I64, ngroups, 1);
+    k_nonzero_slots<<<static_cast<unsigned>(tiles), kSlotThreads, 0, c.stream>>>(
+        gcnt, cnt_stride, ngroups, o.ptr<long long>(), desc, reinterpret_cast<int*>(desc + tiles + 1));
+    c.count_launch();
+    long long* h = c.h_err + Ctx::kPinnedRead;
+    TQP_CUDA(cudaMemcpyAsync(h, desc + tiles - 1, sizeof(longlong2), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const long long total = h[1];
+    if (total * 2 < ngroups) {
+      Tensor t = c.alloc(TQP_I64, total, 1);
+      if (total) TQP_CUDA(cudaMemcpyAsync(t.data(), o.data(), t.bytes(), cudaMemcpyDeviceToDevice, c.stream));
+      return t;
+    }
+    o.rows = total;
+    return o;
+  }
+
   static Tensor touched_groups(Ctx& c, const unsigned long long* gcnt, long long cnt_stride, long long ngroups,
                                const unsigned* present, unsigned long long cmask = ~0ULL) {
+    if (!present && cmask == ~0ULL) return nonzero_slots(c, gcnt, cnt_stride, ngroups);
     Tensor mask = c.alloc(TQP_BOOL, ngroups, 1);
     if (ngroups) {
       k_nonzero_groups<<<c.grid_for(ngroups, 256), 256, 0, c.stream>>>(gcnt, cnt_stride, ngroups, present, cmask,
@@ -4313,9 +4391,7 @@ struct Runner {
                                  gs.row_in_cnt ? 0xffffffffULL : ~0ULL);
     const long long n = gids.rows;
     Tensor order;
-    if (gids_sorted) {
-      order = k::iota(c, n);
-    } else {
+    if (!gids_sorted) {
       Tensor keys = c.alloc(TQP_I64, n, 1);
       if (n) {
         k_group_keys<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs.group_table, gs.row_in_cnt ? gs.gcnt : nullptr,
@@ -4331,7 +4407,8 @@ struct Runner {
       gs.f.out_ptr[j] = outs[j].data();
     }
     if (n) {
-      k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(), order.ptr<long long>(), n, err);
+      k_group_rows<<<c.grid_for(n, 256), 256, 0, c.stream>>>(gs, gids.ptr<long long>(),
+                                                              gids_sorted ? nullptr : order.ptr<long long>(), n, err);
       c.count_launch();
     }
     nrows = n;
