@@ -1366,7 +1366,8 @@ __device__ __forceinline__ long long group_src_row(const GroupSpec& s, unsigned 
 __device__ __forceinline__ long long group_key_value(const GroupSpec& s, int i, unsigned g) {
   if (s.codes || s.direct_codes) {
     const unsigned long long code = s.direct_codes ? static_cast<unsigned long long>(g) : s.codes[g] - 1ULL;
-    const unsigned long long dg = (code / s.kstride[i]) % s.krange[i];
+    // one key (stride 1, code < range): the digit is the code, no 64-bit divide
+    const unsigned long long dg = (s.kstride[i] == 1 && code < s.krange[i]) ? code : (code / s.kstride[i]) % s.krange[i];
     if (s.dvals[i]) return s.dvals[i][dg];
     return s.key_w[i] ? static_cast<long long>(dg) : s.kmin[i] + static_cast<long long>(dg * static_cast<unsigned long long>(s.kstep[i]));
   }
@@ -1442,7 +1443,7 @@ __device__ __noinline__ bool group_out_value(const GroupSpec& s, int j, unsigned
     return fits && limbs_ok;
   }
   double sum = s.qfrac == 64 ? q64_to_f64(lo, hi)
-                             : ldexp(static_cast<double>(static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo)), -s.qfrac);
+                             : ldexp(i128_to_f64_rn(static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo)), -s.qfrac);
   if (s.flag_word >= 0) {  // NaN / +Inf / -Inf among the group's values (IEEE sum)
     const unsigned f = static_cast<unsigned>(s.gcnt[g * s.cnt_stride + s.flag_word] >> (3 * o.acc)) & 7u;
     if ((f & 1u) || (f & 6u) == 6u) sum = __longlong_as_double(0x7ff8000000000000LL);

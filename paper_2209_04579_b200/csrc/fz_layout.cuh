@@ -541,9 +541,35 @@ __device__ __forceinline__ void q64_range_check(double fabsmax, long long rows, 
 
 // Q64.64 -> fp64, correctly rounded (one rounding of the exact value: the
 // int128 conversion rounds to nearest even, the 2^-64 scale is exact)
+// int128 -> fp64 rounded to nearest even: the top 64 significant bits with
+// every lower bit folded into their last (sticky) bit round exactly like
+// the whole value (11 spare bits below the double's 53), one 64-bit convert
+__device__ __forceinline__ double i128_to_f64_rn(__int128 v) {
+  const long long lo64 = static_cast<long long>(v);
+  if (static_cast<__int128>(lo64) == v) return static_cast<double>(lo64);
+  const bool neg = v < 0;
+  const unsigned __int128 u = neg ? static_cast<unsigned __int128>(0) - static_cast<unsigned __int128>(v)
+                                  : static_cast<unsigned __int128>(v);
+  const unsigned long long uh = static_cast<unsigned long long>(u >> 64), ul = static_cast<unsigned long long>(u);
+  unsigned long long top;
+  int e;  // u = top * 2^e (+ sticky bits)
+  if (uh == 0) {
+    top = ul;
+    e = 0;
+  } else {
+    const int lz = __clzll(static_cast<long long>(uh));
+    top = lz ? (uh << lz) | (ul >> (64 - lz)) : uh;
+    const unsigned long long rest = lz ? (ul << lz) : ul;
+    top |= rest != 0 ? 1ULL : 0ULL;
+    e = 64 - lz;
+  }
+  const double d = ldexp(__ull2double_rn(top), e);
+  return neg ? -d : d;
+}
+
 __device__ __forceinline__ double q64_to_f64(unsigned long long lo, unsigned long long hi) {
   const __int128 v = static_cast<__int128>((static_cast<unsigned __int128>(hi) << 64) | lo);
-  return static_cast<double>(v) * 5.421010862427522e-20;  // 2^-64
+  return i128_to_f64_rn(v) * 5.421010862427522e-20;  // 2^-64
 }
 
 __device__ __forceinline__ void atomic_add_q64(unsigned long long* p, __int128 v) {
