@@ -17,6 +17,6 @@ for sf in [float(x) for x in sys.argv[1:]]:
     tm = ex.timings()
     k = {n: round(v["total_ms"] / v["calls"], 4) for n, v in tm.items()}
     rows = 6e6 * sf
-    kt = [v for n, v in k.items() if n.startswith("kernel:k_tile")]
+    kt = [v for n, v in k.items() if n.startswith("kernel:") and "_tile<" in n]
     print(f"sf {sf}: {k}  ns/row {kt[0] * 1e6 / rows:.3f}" if kt else k, flush=True)
     del t, ex
